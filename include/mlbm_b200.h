@@ -1,0 +1,287 @@
+/*
+ * mlbm_b200.h — C ABI of the B200-native hot path of arXiv 2603.14982's
+ * adaptive multi-level HOME-LBM <-> MPM coupled solver.
+ *
+ * Every entry point is extern "C", takes device pointers + sizes + a CUDA
+ * stream (as void*), never allocates persistently (scratch comes from a
+ * caller-provided workspace), is asynchronous on the given stream and returns
+ * an int status (0 = launched, <0 = bad argument / launch failure).  Numerical
+ * failures (divergence, topology violations) are written to a device-side
+ * mlbm_error_t record that the host reads after the step.
+ *
+ * Each entry names the reference Python seam it replaces
+ * (paths relative to the reference package root pkg/src/mlbm/).
+ *
+ * Data layout:
+ *   - tiles of 4^dim cells; within-tile cell index lx + 4 ly + 16 lz
+ *   - per level, tiles stored in sorted (x, y, z) slot order; cell = slot*4^dim + local
+ *   - fields: structure of arrays, field k at base + k*stride (elements);
+ *     order drho, u[dim], S[dim(dim+1)/2] (xx,xy,(xz),yy,(yz),(zz)), eps, f[dim], phi
+ *     (drho = rho - 1 is the stored density: the shifted form keeps fp32 exact enough)
+ *   - dtype 0 = float32, 1 = float64
+ */
+#ifndef MLBM_B200_H
+#define MLBM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MLBM_MAX_LEVELS 6
+#define MLBM_MAX_BOXES 16
+
+/* face order x_min, x_max, y_min, y_max, z_min, z_max */
+enum { MLBM_FACE_PERIODIC = 0, MLBM_FACE_WALL = 1, MLBM_FACE_OUTLET = 2,
+       MLBM_FACE_LOG_INLET = 3 };
+
+/* cell flag bits */
+enum { MLBM_CF_ACTIVE = 1, MLBM_CF_SOLID = 2, MLBM_CF_GHOST_D = 4,
+       MLBM_CF_GHOST_U = 8, MLBM_CF_BC = 16, MLBM_CF_SPECIAL = 32,
+       MLBM_CF_LEAF = 64 };
+
+/* tile flag bits */
+enum { MLBM_TF_PLAIN = 1,      /* every cell active and non-special */
+       MLBM_TF_BC = 2,         /* holds an outlet / inlet layer cell */
+       MLBM_TF_LEAF = 4 };
+
+/* error codes in mlbm_error_t.code (first error wins) */
+enum { MLBM_OK = 0, MLBM_ERR_DENSITY = 1, MLBM_ERR_VELOCITY = 2,
+       MLBM_ERR_TOPOLOGY = 3, MLBM_ERR_STENCIL = 4, MLBM_ERR_DOMAIN = 5 };
+
+typedef struct {
+    int32_t code;
+    int32_t level;
+    int32_t count;
+    int32_t cells[5][3];
+    int32_t detail;
+} mlbm_error_t;
+
+/* One level of the sparse tile hierarchy (device pointers). */
+typedef struct {
+    int32_t dim;
+    int32_t level;
+    int32_t cells[3];           /* cells per axis at this level (1 for unused z) */
+    int32_t tiles[3];           /* tiles per axis */
+    int32_t periodic[3];
+    int32_t n_tiles;
+    const int32_t* tile_map;    /* dense tile grid -> slot or -1, index (x*ty + y)*tz + z */
+    const int32_t* tile_xyz;    /* [n_tiles][3] */
+    const int32_t* nbr;         /* [n_tiles][3^dim], offset index ox + 3 oy + 9 oz, o = d+1 */
+    const uint8_t* cell_flags;  /* [n_tiles * 4^dim] MLBM_CF_* */
+    const uint64_t* dir_masks;  /* [n_tiles * 4^dim] bit i: bounce-back dir i; bit 32+i: self source */
+    const uint8_t* tile_flags;  /* [n_tiles] MLBM_TF_* */
+} mlbm_level_t;
+
+typedef struct {
+    void* ptr;                  /* field 0 */
+    int64_t stride;             /* elements between consecutive fields */
+} mlbm_fields_t;
+
+typedef struct {
+    int32_t face[6];
+    double inlet_u0, inlet_beta, inlet_y0;
+    double rho0;
+} mlbm_bc_t;
+
+typedef struct {
+    int32_t n_boxes;
+    double boxes[MLBM_MAX_BOXES][6];   /* lo[3], hi[3] in finest units (2D: lo x,y,_ hi x,y,_) */
+    const float* heightmap;            /* finest (x[, z]) heights or NULL */
+    int32_t hm_dims[2];
+} mlbm_solid_t;
+
+typedef struct {
+    double tau;                 /* level relaxation time */
+    double gravity[3];          /* lattice gravity (force = rho g 2^level) */
+    double h3_xyz;              /* 3D Hermite coefficient of Gamma_xyz */
+    int32_t force_mode;         /* 0: gravity; 1: per-cell f fields of dst */
+    int32_t tau_mode;           /* 0: scalar tau; 1: tau0 * eps field of dst; 2: tau_ptr[cell] */
+    double tau0;
+    const void* tau_ptr;        /* per-cell relaxation times (tau_mode 2), run dtype */
+} mlbm_collide_t;
+
+/* ---- LBM level kernels ------------------------------------------------- */
+
+/* mode: 0 fused stream+collide+boundary (solver.py:483-488),
+ *       1 stream only   (solver.py:336-381 stream_kernel),
+ *       2 collide+boundary (solver.py:394-453 collide_kernel +
+ *         solver.py:460-481 boundary_kernel), 3 collide only, 4 boundary only. */
+int mlbm_level_step(const mlbm_level_t* lv, mlbm_fields_t src, mlbm_fields_t dst,
+                    int32_t dtype, int32_t mode, const mlbm_collide_t* cp,
+                    const mlbm_bc_t* bc, mlbm_error_t* err, void* stream);
+
+/* I^d fill (solver.py:501-526 downward_kernel): targets [n], src [n][2^dim]
+ * coarse cell indices (-1 where the weight is zero).  step 1 or 2. */
+int mlbm_downward(int32_t dim, int32_t n, const int32_t* targets, const int32_t* src,
+                  const int32_t* fine_tile_xyz,
+                  mlbm_fields_t olda, mlbm_fields_t newa, mlbm_fields_t dst,
+                  int32_t dtype, int32_t step, double kappa, void* stream);
+
+/* I^u fill (solver.py:536-560 upward_kernel): src [n][2^dim], column 0 is the
+ * coincident child; average != 0 uses the 2^dim mean. */
+int mlbm_upward(int32_t dim, int32_t n, const int32_t* targets, const int32_t* src,
+                mlbm_fields_t fine, mlbm_fields_t dst, int32_t dtype,
+                int32_t average, double kappa, void* stream);
+
+/* ---- tile hierarchy ------------------------------------------------------ */
+
+/* Whole-hierarchy view passed to the topology / adapt / migration kernels.
+ * kind[l]: dense tile grid of level l (index (x*ty + y)*tz + z): 0 absent,
+ * 1 leaf, 2 border.  tile_map[l]: dense grid -> slot or -1.  fields[t][l]:
+ * field base of tree t at level l (only used by migration). */
+typedef struct {
+    int32_t dim, levels;
+    int32_t finest[3];          /* finest cells per axis (unused axes = 4) */
+    int32_t periodic[3];
+    const uint8_t* kind[MLBM_MAX_LEVELS];
+    const int32_t* tile_map[MLBM_MAX_LEVELS];
+    void* fields[2][MLBM_MAX_LEVELS];
+    int64_t stride[MLBM_MAX_LEVELS];
+    int32_t n_tiles[MLBM_MAX_LEVELS];
+} mlbm_hier_t;
+
+/* bytes of scratch for the scans / selections over n items */
+int64_t mlbm_ws_bytes(int64_t n);
+
+/* ---- topology (sparse_grid.py:183-200 rebuild_level, 210-282 rasters) ---- */
+
+/* Compacts a level's kind grid into sorted slots (x, y, z lexicographic =
+ * reference sorted(coords) order).  Writes tile_map, tile_xyz[n][3],
+ * tile_kind[n], old_slot[n] (slot of the same tile in old_map or -1) and
+ * counts[0] = n tiles, counts[1] = fresh tiles. */
+int mlbm_compact_tiles(int32_t dim, const int32_t tiles[3], const uint8_t* kind,
+                       const int32_t* old_map, int32_t* tile_map, int32_t* tile_xyz,
+                       uint8_t* tile_kind, int32_t* old_slot, int32_t* counts,
+                       void* ws, int64_t ws_bytes, void* stream);
+
+/* 3^dim neighbour slots per tile with periodic wrap (-1 absent / outside). */
+int mlbm_build_neighbors(const mlbm_level_t* lv, int32_t* nbr, void* stream);
+
+/* Per-cell classification of one level (sparse_grid.py:468-544
+ * classify_interfaces, solver.py:177-273 _LevelTables): I^d / I^u ghosts,
+ * BC layer, solid, active, per-direction bounce-back / self-source masks,
+ * tile flags.  counts[0] += |I^d|, counts[1] += |I^u|; violations -> err. */
+int mlbm_classify_level(const mlbm_level_t* lv, const mlbm_hier_t* h,
+                        const mlbm_bc_t* bc, const mlbm_solid_t* solid,
+                        uint8_t* cell_flags, uint64_t* dir_masks, uint8_t* tile_flags,
+                        int32_t* counts, mlbm_error_t* err, void* stream);
+
+/* Compacts the I^d (which = 0) / I^u (which = 1) cells of `lv` in cell order
+ * and builds their 2^dim stencils into the coarser / finer level `other`
+ * (sparse_grid.py:439-465, 500-543).  counts[0] = n. */
+int mlbm_build_interface(const mlbm_level_t* lv, const mlbm_level_t* other, int32_t which,
+                         int32_t* targets, int32_t* src, int32_t* counts,
+                         mlbm_error_t* err, void* ws, int64_t ws_bytes, void* stream);
+
+/* ---- block maintenance (adapt.py) --------------------------------------- */
+
+/* seeds |= tile of floor(x) (adapt.py:54-65); x is [n][dim] SoA (x + a*xstride). */
+int mlbm_seed_tiles(int32_t dim, int32_t n, const void* x, int64_t xstride, int32_t dtype,
+                    const int32_t tiles0[3], uint8_t* seeds, mlbm_error_t* err, void* stream);
+
+/* out = op(in) over a level's tile grid (dims = child grid for group ops):
+ * op 0 align_up (adapt.py:77-81), 1 parents (adapt.py:84-87; out on the parent
+ * grid), 2 or-into (out |= in), 3 and-not (out &= ~in), 4 copy, 5 fill ones,
+ * 6 leaf-of-kind (out = kind == 1). */
+int mlbm_bitmap_op(int32_t op, int32_t dim, const int32_t dims[3], const uint8_t* in,
+                   uint8_t* out, void* stream);
+
+/* Chebyshev dilation by r tiles, separable, periodic per axis
+ * (sparse_grid.py:358-363); tmp has the grid's size. */
+int mlbm_dilate(int32_t dim, const int32_t dims[3], const int32_t periodic[3], int32_t r,
+                const uint8_t* in, uint8_t* out, uint8_t* tmp, void* stream);
+
+/* One level of adapt.py:152-182 (_effective_cumulative):
+ * cand = cur & ~des; streak = cand ? streak + 1 : 0;
+ * avail = streak >= 2 & cand & ~guard; act = avail on complete sibling groups;
+ * eff = des | (cur & ~act) | par_prev (par_prev may be NULL). */
+int mlbm_effective_level(int32_t dim, const int32_t dims[3], const uint8_t* des,
+                         const uint8_t* cur, const uint8_t* guard, const uint8_t* par_prev,
+                         int16_t* streak, uint8_t* eff, void* stream);
+
+/* adapt.py:184-194 + no-op test: own = eff & ~par_finer; storage = dilate(own, 2);
+ * new kind = own ? 1 : storage ? 2 : 0; changed[0] |= (new kind != old kind).
+ * `storage` is the already-dilated own bitmap. */
+int mlbm_plan_level(int32_t n, const uint8_t* own, const uint8_t* storage,
+                    const uint8_t* old_kind, uint8_t* new_kind, int32_t* changed,
+                    void* stream);
+
+/* Invariants (adapt.py:374-389): leaf coverage of every finest tile exactly
+ * once, two-tile rings, particles inside level-0 leaves -> viol[0..2]. */
+int mlbm_check_coverage(const mlbm_hier_t* h, int32_t* viol, void* stream);
+int mlbm_count_ring_violations(int64_t n, const uint8_t* dilated_leaf, const uint8_t* kind,
+                                int32_t* viol, void* stream);
+int mlbm_check_particles(int32_t dim, int32_t n, const void* x, int64_t xstride,
+                         int32_t dtype, const int32_t tiles0[3], const uint8_t* kind0,
+                         int32_t* viol, void* stream);
+
+/* Data migration after a rebuild (adapt.py:259-283): both trees, surviving
+ * tiles bitwise, fresh tiles get drho = 0, eps = 1, others 0. */
+int mlbm_migrate_level(int32_t dim, int32_t n_new_tiles, const int32_t* old_slot,
+                       mlbm_fields_t old0, mlbm_fields_t old1, mlbm_fields_t new0,
+                       mlbm_fields_t new1, int32_t dtype, void* stream);
+
+/* New-cell initialisation (adapt.py:301-372): for every cell of a fresh
+ * tile of level `level` (new topology `nh`), interpolate from the nearest old
+ * coarser level whose stencil is complete (S chain down), else copy the
+ * coincident old finer cell (S chain up).  taus[] per level, conv 0 derived /
+ * 1 paper_literal.  Unfilled cells counted into viol[0]. */
+int mlbm_init_new_cells(const mlbm_hier_t* old_h, const mlbm_hier_t* nh, int32_t level,
+                        const int32_t* tile_xyz, const int32_t* old_slot, int32_t n_tiles,
+                        mlbm_fields_t new0, mlbm_fields_t new1, const double* taus,
+                        int32_t conv, int32_t dtype, int32_t* viol, void* stream);
+
+/* ---- MPM + coupling (granular.py, coupling.py) -------------------------- */
+
+/* row counts of the level-0 raster and of the particle state */
+int mlbm_raster_rows(int32_t dim);
+int mlbm_particle_rows(int32_t dim);
+
+/* stencil + Kirchhoff stress + P2G scatter fused with rasterize_fractions
+ * (granular.py:137-178, 260-310; coupling.py:96-131).  x: float64 [dim][ps];
+ * p: run-dtype particle rows [rows][ps]; ras: zeroed accumulator rows. */
+int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, void* p, int64_t ps,
+             double lam, double mu, double alpha, void* ras, int64_t rs, int32_t dtype,
+             mlbm_error_t* err, void* stream);
+
+/* per level-0 cell: eps, Di Felice drag + limiter, grad eps, mixture force
+ * (written into both trees), MPM grid update with wall / sticky projection
+ * (coupling.py:134-197, 379-446; granular.py:313-341). */
+int mlbm_exchange(const mlbm_level_t* lv0, mlbm_fields_t w_tree, mlbm_fields_t r_tree,
+                  mlbm_fields_t tree0, mlbm_fields_t tree1, void* ras, int64_t rs,
+                  double eps_min, double nu, double d_p, double re_min, double dt,
+                  double rho0, const double* g_fluid, const double* g_sed,
+                  const int32_t* faces, double floor_friction, int32_t mode,
+                  int32_t dtype, void* stream);
+
+/* gather, advect (wrap / clamp to [2, dim-2]), F update, SVD + Drucker-Prager
+ * (granular.py:344-412). clamped += number of clamped coordinates. */
+int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, double* x, void* p, int64_t ps,
+             double lam, double mu, double alpha, const void* ras, int64_t rs, double dt,
+             int32_t plastic, int32_t dtype, int32_t* clamped, mlbm_error_t* err,
+             void* stream);
+
+/* entrainment stress raster (coupling.py:283-294) and powder transport
+ * (coupling.py:230-272, 275-322, 483-498). tmp: [n0] run-dtype scratch. */
+int mlbm_stress_raster(const mlbm_level_t* lv0, int32_t n, const double* x, const void* p,
+                       int64_t ps, double lam, double mu, double alpha, void* ras, int64_t rs,
+                       int32_t dtype, mlbm_error_t* err, void* stream);
+int mlbm_powder(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm_fields_t dst, void* ras,
+                int64_t rs, void* tmp, double diffusion, double sign, double dt,
+                double entrain, double eta_surface, int32_t with_source, int32_t dtype,
+                void* stream);
+
+/* diagnostics (coupling.py:500-531): out[0..dim-1] += vol sum rho u, out[dim] +=
+ * vol sum phi, out[dim+1] = min(out[dim+1], eps) over leaf cells;
+ * particles: out[0..dim-1] += sum m v, out[dim..2dim-1] += sum fs. */
+int mlbm_diag_level(const mlbm_level_t* lv, mlbm_fields_t f, double vol, int32_t dtype,
+                    double* out, void* stream);
+int mlbm_diag_particles(int32_t dim, int32_t n, const void* p, int64_t ps, const void* ras,
+                        int64_t rs, int64_t n0, int32_t dtype, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

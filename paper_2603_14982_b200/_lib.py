@@ -1,0 +1,203 @@
+"""Loader and ctypes bindings of the sm_100a C-ABI library (libmlbm_b200.so).
+
+The library is built in-tree by :func:`build` (nvcc, ``-gencode
+arch=compute_100a,code=sm_100a``) and loaded with ctypes; every product
+kernel goes through these bindings.  There is no CPU fallback: if the
+library is missing or no CUDA device is present, :func:`lib` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+LIBPATH = os.path.join(HERE, "libmlbm_b200.so")
+SOURCES = ["lbm.cu", "topology.cu", "mpm.cu"]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
+              "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
+              "-Xcompiler", "-Wno-deprecated-declarations",
+              "-diag-suppress", "1444"]
+
+MAX_LEVELS = 6
+
+
+def _nvcc():
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.isabs(cand) and os.path.exists(cand) or not os.path.isabs(cand)):
+            return cand
+    return "nvcc"
+
+
+def build(force=False, verbose=False):
+    """Compile every .cu into the in-tree shared library (objects cached)."""
+    objs = []
+    bdir = os.path.join(HERE, "build")
+    os.makedirs(bdir, exist_ok=True)
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    hdrs.append(os.path.join(INCLUDE, "mlbm_b200.h"))
+    hmt = max(os.path.getmtime(h) for h in hdrs)
+    for src in SOURCES:
+        sp = os.path.join(CSRC, src)
+        op = os.path.join(bdir, src.replace(".cu", ".o"))
+        objs.append(op)
+        if (not force and os.path.exists(op) and os.path.getmtime(op) >=
+                max(os.path.getmtime(sp), hmt)):
+            continue
+        cmd = [_nvcc()] + NVCC_FLAGS + ["-I", INCLUDE, "-c", sp, "-o", op]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+    if (force or not os.path.exists(LIBPATH) or
+            os.path.getmtime(LIBPATH) < max(os.path.getmtime(o) for o in objs)):
+        cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
+               "-o", LIBPATH] + objs + ["-lcudart"]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+    return LIBPATH
+
+
+# -- C structs (mirror include/mlbm_b200.h) ------------------------------------
+
+class Level(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("level", C.c_int32),
+                ("cells", C.c_int32 * 3), ("tiles", C.c_int32 * 3),
+                ("periodic", C.c_int32 * 3), ("n_tiles", C.c_int32),
+                ("tile_map", C.c_void_p), ("tile_xyz", C.c_void_p),
+                ("nbr", C.c_void_p), ("cell_flags", C.c_void_p),
+                ("dir_masks", C.c_void_p), ("tile_flags", C.c_void_p)]
+
+
+class Fields(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("stride", C.c_int64)]
+
+
+class BC(C.Structure):
+    _fields_ = [("face", C.c_int32 * 6), ("inlet_u0", C.c_double),
+                ("inlet_beta", C.c_double), ("inlet_y0", C.c_double),
+                ("rho0", C.c_double)]
+
+
+class Solid(C.Structure):
+    _fields_ = [("n_boxes", C.c_int32), ("boxes", (C.c_double * 6) * 16),
+                ("heightmap", C.c_void_p), ("hm_dims", C.c_int32 * 2)]
+
+
+class Collide(C.Structure):
+    _fields_ = [("tau", C.c_double), ("gravity", C.c_double * 3),
+                ("h3_xyz", C.c_double), ("force_mode", C.c_int32),
+                ("tau_mode", C.c_int32), ("tau0", C.c_double),
+                ("tau_ptr", C.c_void_p)]
+
+
+class Hier(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("levels", C.c_int32),
+                ("finest", C.c_int32 * 3), ("periodic", C.c_int32 * 3),
+                ("kind", C.c_void_p * MAX_LEVELS),
+                ("tile_map", C.c_void_p * MAX_LEVELS),
+                ("fields", (C.c_void_p * MAX_LEVELS) * 2),
+                ("stride", C.c_int64 * MAX_LEVELS),
+                ("n_tiles", C.c_int32 * MAX_LEVELS)]
+
+
+ERR_INTS = 19   # mlbm_error_t as int32 words
+
+P = C.c_void_p
+I32 = C.c_int32
+I64 = C.c_int64
+D = C.c_double
+_SIGS = {
+    "mlbm_level_step": [C.POINTER(Level), Fields, Fields, I32, I32,
+                        C.POINTER(Collide), C.POINTER(BC), P, P],
+    "mlbm_downward": [I32, I32, P, P, P, Fields, Fields, Fields, I32, I32, D, P],
+    "mlbm_upward": [I32, I32, P, P, Fields, Fields, I32, I32, D, P],
+    "mlbm_ws_bytes": [I64],
+    "mlbm_compact_tiles": [I32, P, P, P, P, P, P, P, P, P, I64, P],
+    "mlbm_build_neighbors": [C.POINTER(Level), P, P],
+    "mlbm_classify_level": [C.POINTER(Level), C.POINTER(Hier), C.POINTER(BC),
+                            C.POINTER(Solid), P, P, P, P, P, P],
+    "mlbm_build_interface": [C.POINTER(Level), C.POINTER(Level), I32, P, P, P, P,
+                             P, I64, P],
+    "mlbm_seed_tiles": [I32, I32, P, I64, I32, P, P, P, P],
+    "mlbm_bitmap_op": [I32, I32, P, P, P, P],
+    "mlbm_dilate": [I32, P, P, I32, P, P, P, P],
+    "mlbm_effective_level": [I32, P, P, P, P, P, P, P, P],
+    "mlbm_plan_level": [I32, P, P, P, P, P, P],
+    "mlbm_check_coverage": [C.POINTER(Hier), P, P],
+    "mlbm_count_ring_violations": [I64, P, P, P, P],
+    "mlbm_check_particles": [I32, I32, P, I64, I32, P, P, P, P],
+    "mlbm_migrate_level": [I32, I32, P, Fields, Fields, Fields, Fields, I32, P],
+    "mlbm_init_new_cells": [C.POINTER(Hier), C.POINTER(Hier), I32, P, P, I32,
+                            Fields, Fields, P, I32, I32, P, P],
+    "mlbm_raster_rows": [I32],
+    "mlbm_particle_rows": [I32],
+    "mlbm_p2g": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64, I32, P, P],
+    "mlbm_exchange": [C.POINTER(Level), Fields, Fields, Fields, Fields, P, I64,
+                      D, D, D, D, D, D, P, P, P, D, I32, I32, P],
+    "mlbm_g2p": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64, D, I32, I32,
+                 P, P, P],
+    "mlbm_stress_raster": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64,
+                           I32, P, P],
+    "mlbm_powder": [C.POINTER(Level), Fields, Fields, P, I64, P, D, D, D, D, D,
+                    I32, I32, P],
+    "mlbm_diag_level": [C.POINTER(Level), Fields, D, I32, P, P],
+    "mlbm_diag_particles": [I32, I32, P, I64, P, I64, I64, I32, P, P],
+}
+_RET64 = {"mlbm_ws_bytes"}
+
+_LIB = None
+
+
+class KernelError(RuntimeError):
+    pass
+
+
+def load(path=LIBPATH):
+    """Load the shared library and bind every exported symbol."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise KernelError(
+            f"CUDA library {path} is missing: run __graft_entry__.build() "
+            "(no CPU fallback exists)")
+    lib = C.CDLL(path)
+    for name, args in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_int64 if name in _RET64 else C.c_int
+    _LIB = lib
+    return lib
+
+
+def lib():
+    """The bound library; raises if it cannot run kernels here."""
+    import torch
+    if not torch.cuda.is_available():
+        raise KernelError("no CUDA device: the B200 path has no CPU fallback")
+    return load()
+
+
+def check(status, what):
+    if status != 0:
+        raise KernelError(f"{what} failed with status {status}")
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def stream_handle():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def fields(t):
+    """Fields struct of a [nf, n] tensor (row stride)."""
+    if t is None:
+        return Fields(0, 0)
+    return Fields(t.data_ptr(), t.stride(0))

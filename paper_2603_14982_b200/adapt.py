@@ -1,0 +1,308 @@
+"""GPU block maintenance (drop-in for ``pkg/src/mlbm/adapt.py``).
+
+``GridAdaptor.update(driver, pair)`` runs the reference's bitmap algorithm
+(adapt.py:54-230) as dense uint8 tile-grid kernels on the device:
+
+  seeds (particle tiles + static mask)          mlbm_seed_tiles       adapt.py:54-65
+  desired cumulative coverage                   mlbm_bitmap_op/dilate adapt.py:77-105
+  current cumulative coverage                   mlbm_bitmap_op        adapt.py:108-121
+  hysteresis (int16 streaks, sibling groups,
+    2-ring guard)                               mlbm_effective_level  adapt.py:152-182
+  leaf/border plan + no-op test                 mlbm_plan_level       adapt.py:184-225
+  rebuild (sorted slots) + bitwise migration    mlbm_compact_tiles,
+                                                mlbm_migrate_level    adapt.py:232-286
+  new-cell initialisation + S rescale chain     mlbm_init_new_cells   adapt.py:288-372
+  invariants                                    mlbm_check_*          adapt.py:374-389
+
+One small device->host copy per update returns the changed flags and
+violation counts; a topology change adds the two copies of the rebuild.
+The tile sets, streaks and surviving-tile bits are identical to the
+reference's by construction (integer work only).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .sparse_grid import (DEV_BORDER, DEV_LEAF, TILE, LevelFields, PingPongPair, Topology,
+                          dtype_code, fresh_block)
+from .solver import LevelParams
+
+PAD_TILES = 2
+
+
+@dataclass
+class RefineDriver:
+    """Inputs of the level-selection function (adapt.py:42-65).
+
+    ``positions``: (n, d) array / tensor in finest units, or a float64
+    device tensor laid out [d, n] (``positions_soa``) as the particle state
+    keeps it.
+    """
+    positions: object = None
+    static_tiles: np.ndarray | None = None
+    levels: int = 1
+    positions_soa: object = None
+
+    def device_positions(self, d, device):
+        if self.positions_soa is not None:
+            return self.positions_soa
+        if self.positions is None:
+            return None
+        x = torch.as_tensor(self.positions, dtype=torch.float64, device=device)
+        if x.numel() == 0:
+            return None
+        return x.reshape(-1, d).t().contiguous()
+
+    def seed_tiles(self, tiles_dims):
+        """Host reference of the seeds (test helper, adapt.py:54-65)."""
+        seeds = np.zeros(tiles_dims, dtype=bool)
+        if self.positions is not None and len(self.positions):
+            pos = np.asarray(self.positions.cpu() if torch.is_tensor(self.positions)
+                             else self.positions)
+            t = np.floor(pos).astype(np.int64) // TILE
+            if (t < 0).any() or any((t[:, a] >= tiles_dims[a]).any()
+                                    for a in range(len(tiles_dims))):
+                raise ValueError("particle outside the domain bounding box")
+            seeds[tuple(t.T)] = True
+        if self.static_tiles is not None:
+            seeds |= self.static_tiles
+        return seeds
+
+
+@dataclass
+class AdaptReport:
+    created: list = field(default_factory=list)
+    deleted: list = field(default_factory=list)
+    noop: bool = True
+    violations: list = field(default_factory=list)
+
+    def total_created(self):
+        return int(sum(self.created)) if self.created else 0
+
+    def total_deleted(self):
+        return int(sum(self.deleted)) if self.deleted else 0
+
+
+def _i3(v):
+    return (L.C.c_int32 * 3)(*v)
+
+
+class GridAdaptor:
+    """Incremental topology maintenance with coarsening hysteresis."""
+
+    def __init__(self, topology: Topology, level_params: LevelParams,
+                 rescale_convention: str = "derived"):
+        self.topology = topology
+        self.level_params = level_params
+        self.rescale_convention = rescale_convention
+        dev = topology.device
+        self._grids = [topology.tile_grid(l) for l in range(topology.levels)]
+        n = [int(np.prod(g)) for g in self._grids]
+        z = lambda k: torch.zeros(k, dtype=torch.uint8, device=dev)   # noqa: E731
+        self._streak = [torch.zeros(k, dtype=torch.int16, device=dev) for k in n]
+        self._des = [z(k) for k in n]
+        self._cur = [z(k) for k in n]
+        self._eff = [z(k) for k in n]
+        self._par = [z(k) for k in n]
+        self._guard = [z(k) for k in n]
+        self._own = [z(k) for k in n]
+        self._stor = [z(k) for k in n]
+        self._tmp = [z(k) for k in n]
+        self._new = [z(k) for k in n]
+        self._status = torch.zeros(topology.levels + 4, dtype=torch.int32, device=dev)
+        self._err = torch.zeros(L.ERR_INTS, dtype=torch.int32, device=dev)
+        self._taus = torch.tensor(level_params.taus, dtype=torch.float64, device=dev)
+        self._static_key = None
+        self._static_dev = None
+        self.launches = 0
+
+    @property
+    def streak(self):
+        """Host copy of the int16 streak bitmaps (adapt.py:147-148)."""
+        d = self.topology.d
+        out = []
+        for l, g in enumerate(self._grids):
+            a = self._streak[l].cpu().numpy().reshape(g)
+            out.append(a if d == 3 else a[..., 0])
+        return out
+
+    # -- bitmap helpers ------------------------------------------------------------
+    def _op(self, op, level, src, dst):
+        L.check(L.lib().mlbm_bitmap_op(op, self.topology.d, _i3(self._grids[level]),
+                                       L.ptr(src), L.ptr(dst), L.stream_handle()), "bitmap_op")
+        self.launches += 1
+
+    def _parents_into(self, level_child, src, dst):
+        self._op(1, level_child, src, dst)
+
+    def _dilate(self, level, src, dst):
+        topo = self.topology
+        L.check(L.lib().mlbm_dilate(topo.d, _i3(self._grids[level]), _i3(topo.periodic3()),
+                                    PAD_TILES, L.ptr(src), L.ptr(dst), L.ptr(self._tmp[level]),
+                                    L.stream_handle()), "dilate")
+        self.launches += 1
+
+    def _static(self, static):
+        if static is None:
+            return None
+        key = (id(static), static.shape)
+        if self._static_key != key:
+            a = np.asarray(static, dtype=np.uint8)
+            if a.ndim == 2:
+                a = a[..., None]
+            self._static_dev = torch.as_tensor(a.reshape(-1), device=self.topology.device)
+            self._static_key = key
+        return self._static_dev
+
+    # -- update ----------------------------------------------------------------------
+    def update(self, driver: RefineDriver, pair: PingPongPair) -> AdaptReport:
+        topo = self.topology
+        lib = L.lib()
+        s = L.stream_handle()
+        Lv = topo.levels
+        rep = AdaptReport(created=[0] * Lv, deleted=[0] * Lv)
+        self._status.zero_()
+        # seeds -> des[0]
+        seeds = self._tmp[0]
+        seeds.zero_()
+        x = driver.device_positions(topo.d, topo.device)
+        if x is not None and x.shape[1]:
+            L.check(lib.mlbm_seed_tiles(topo.d, x.shape[1], L.ptr(x), x.stride(0), 1,
+                                        _i3(self._grids[0]), L.ptr(seeds), L.ptr(self._err), s),
+                    "seed_tiles")
+        st = self._static(driver.static_tiles)
+        if st is not None:
+            self._op(2, 0, st, seeds)
+        des, cur, eff = self._des, self._cur, self._eff
+        if Lv == 1:
+            des[0].fill_(1)
+        else:
+            seeds_c = seeds.clone()
+            self._op(0, 0, seeds_c, des[0])
+            for l in range(1, Lv):
+                self._parents_into(l - 1, des[l - 1], self._par[l])
+                if l == Lv - 1:
+                    des[l].fill_(1)
+                else:
+                    self._dilate(l, self._par[l], self._guard[l])
+                    self._op(0, l, self._guard[l], des[l])
+        # current cumulative
+        for l in range(Lv):
+            self._op(6, l, topo.lv[l].kind, cur[l])
+            if l > 0:
+                self._parents_into(l - 1, cur[l - 1], self._par[l])
+                self._op(2, l, self._par[l], cur[l])
+        # effective (hysteresis)
+        for l in range(Lv):
+            guard = par = None
+            if l > 0:
+                self._parents_into(l - 1, eff[l - 1], self._par[l])
+                self._dilate(l, self._par[l], self._guard[l])
+                guard, par = self._guard[l], self._par[l]
+            L.check(lib.mlbm_effective_level(topo.d, _i3(self._grids[l]), L.ptr(des[l]),
+                                             L.ptr(cur[l]), L.ptr(guard), L.ptr(par),
+                                             L.ptr(self._streak[l]), L.ptr(eff[l]), s),
+                    "effective_level")
+            self.launches += 1
+        if Lv > 1:
+            eff[Lv - 1].fill_(1)
+        # storage plan + no-op test
+        for l in range(Lv):
+            self._op(4, l, eff[l], self._own[l])
+            if l > 0:
+                self._parents_into(l - 1, eff[l - 1], self._par[l])
+                self._op(3, l, self._par[l], self._own[l])
+            self._dilate(l, self._own[l], self._stor[l])
+            L.check(lib.mlbm_plan_level(self._own[l].numel(), L.ptr(self._own[l]),
+                                        L.ptr(self._stor[l]), L.ptr(topo.lv[l].kind),
+                                        L.ptr(self._new[l]), L.ptr(self._status[l:l + 1]), s),
+                    "plan_level")
+            self.launches += 1
+        status = self._status.cpu().numpy()
+        err = self._err.cpu().numpy()
+        if err[0]:
+            self._err.zero_()
+            raise ValueError("particle outside the domain bounding box")
+        changed = [l for l in range(Lv) if status[l]]
+        if changed:
+            rep.noop = False
+            self._apply(changed, pair, rep)
+        self._check_invariants(driver, rep)
+        return rep
+
+    def _apply(self, changed, pair, rep):
+        topo = self.topology
+        lib = L.lib()
+        s = L.stream_handle()
+        d = topo.d
+        T = TILE ** d
+        # snapshot of the old hierarchy (tile maps, kinds, fields)
+        old_h = topo.hier_struct(pair)
+        keep = [(topo.lv[l].tile_map, topo.lv[l].kind) for l in range(topo.levels)]
+        old_blocks = [[pair.trees[t].levels[l].data for l in range(topo.levels)] for t in range(2)]
+        old_counts = [topo.n_tiles(l) for l in range(topo.levels)]
+        topo.rebuild({l: self._new[l].clone() for l in changed})
+        dcode = dtype_code(pair.dtype)
+        viol = torch.zeros(1, dtype=torch.int32, device=topo.device)
+        new_h = topo.hier_struct()
+        conv = 0 if self.rescale_convention == "derived" else 1
+        for l in changed:
+            lt = topo.lv[l]
+            n_new = lt.n_tiles
+            rep.created[l] = lt.created
+            rep.deleted[l] = old_counts[l] - (n_new - lt.created)
+            nb = [fresh_block(d, n_new * T, pair.dtype, topo.device) for _ in range(2)]
+            if n_new:
+                L.check(lib.mlbm_migrate_level(d, n_new, L.ptr(lt.old_slot),
+                                               L.fields(old_blocks[0][l]), L.fields(old_blocks[1][l]),
+                                               L.fields(nb[0]), L.fields(nb[1]), dcode, s),
+                        "migrate_level")
+                if lt.created:
+                    L.check(lib.mlbm_init_new_cells(L.C.byref(old_h), L.C.byref(new_h), l,
+                                                    L.ptr(lt.tile_xyz), L.ptr(lt.old_slot), n_new,
+                                                    L.fields(nb[0]), L.fields(nb[1]),
+                                                    L.ptr(self._taus), conv, dcode, L.ptr(viol), s),
+                            "init_new_cells")
+            for t in range(2):
+                pair.trees[t].levels[l] = LevelFields(d, nb[t])
+        nv = int(viol.item())
+        if nv:
+            rep.violations.append(("uninitialized cell", nv))
+        del keep
+
+    def _check_invariants(self, driver, rep):
+        """Coverage, two-tile rings, particles in level-0 leaves
+        (adapt.py:374-389); reported, not raised."""
+        topo = self.topology
+        lib = L.lib()
+        s = L.stream_handle()
+        v = self._status[topo.levels:topo.levels + 3]
+        v.zero_()
+        h = topo.hier_struct()
+        L.check(lib.mlbm_check_coverage(L.C.byref(h), L.ptr(v), s), "check_coverage")
+        for l in range(topo.levels):
+            self._op(6, l, topo.lv[l].kind, self._own[l])
+            self._dilate(l, self._own[l], self._stor[l])
+            L.check(lib.mlbm_count_ring_violations(self._stor[l].numel(), L.ptr(self._stor[l]),
+                                                   L.ptr(topo.lv[l].kind), L.ptr(v), s),
+                    "ring_violations")
+        x = driver.device_positions(topo.d, topo.device)
+        if x is not None and x.shape[1]:
+            L.check(lib.mlbm_check_particles(topo.d, x.shape[1], L.ptr(x), x.stride(0), 1,
+                                             _i3(self._grids[0]), L.ptr(topo.lv[0].kind),
+                                             L.ptr(v), s), "check_particles")
+        cnt = v.cpu().numpy()
+        if cnt[0]:
+            rep.violations.append(("invariant", f"leaf coverage violated at {cnt[0]} tiles"))
+        if cnt[1]:
+            rep.violations.append(("invariant", f"{cnt[1]} ring tiles missing"))
+        if cnt[2]:
+            rep.violations.append(("particle not in level-0 leaf", int(cnt[2])))
+
+
+def update_grid(adaptor: GridAdaptor, driver: RefineDriver, pair) -> AdaptReport:
+    return adaptor.update(driver, pair)

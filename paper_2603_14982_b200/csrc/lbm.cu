@@ -1,0 +1,552 @@
+// HOME-LBM level kernels for sm_100a.
+//
+//   mlbm_level_step  — fused pull-stream + moment BGK collide + boundaries
+//                      (reference solver.py:336-481, one call per level step)
+//   mlbm_downward    — I^d fill from the coarser level (solver.py:501-526)
+//   mlbm_upward      — I^u fill from the finer level   (solver.py:536-560)
+//
+// Level step design: one 4^D tile per thread group, one thread
+// per cell.  Each cell turns its own moments into Hermite coefficients and
+// reconstructs its Q populations in opposite pairs (shared even/odd parts),
+// pushing the ones that stay inside the tile into a shared-memory buffer
+// fbuf[dir][cell].  Populations entering the tile from its 3^D-1 neighbour
+// tiles are reconstructed by a static halo work list (sorted by direction so
+// warps stay convergent).  After one barrier each cell pulls its Q incoming
+// populations, accumulates the bare moments in the shifted form
+// (g = f - w, drho = rho - 1), collides, and the BC tiles apply the
+// outlet/inlet passes in reference face order through shared memory.
+#include "common.cuh"
+
+namespace mlbm {
+
+// ---------------------------------------------------------------------------
+// compile-time halo work lists
+template <int D> struct HaloTable {
+    static constexpr int N = D == 2 ? 44 : 728;
+    uint32_t item[N];   // nbi | srcl << 5 | dir << 11 | dstl << 16
+};
+
+template <int D> constexpr HaloTable<D> make_halo_table() {
+    HaloTable<D> h{};
+    int n = 0;
+    constexpr int T = Geo<D>::T;
+    for (int i = 1; i < Geo<D>::Q; ++i) {
+        for (int x = 0; x < T; ++x) {
+            int l[3] = {x & 3, (x >> 2) & 3, D == 3 ? (x >> 4) & 3 : 0};
+            int s[3] = {0, 0, 0}, o[3] = {0, 0, 0};
+            bool outside = false;
+            for (int a = 0; a < 3; ++a) {
+                s[a] = l[a] - cvec<D>(i, a);
+                o[a] = s[a] < 0 ? -1 : (s[a] > 3 ? 1 : 0);
+                if (o[a] != 0) outside = true;
+                s[a] -= 4 * o[a];
+            }
+            if (!outside) continue;
+            int nbi = nb_index<D>(o[0], o[1], o[2]);
+            int srcl = s[0] + 4 * s[1] + (D == 3 ? 16 * s[2] : 0);
+            h.item[n++] = (uint32_t)nbi | ((uint32_t)srcl << 5) | ((uint32_t)i << 11) |
+                          ((uint32_t)x << 16);
+        }
+    }
+    return h;
+}
+
+constexpr HaloTable<2> k_halo2 = make_halo_table<2>();
+constexpr HaloTable<3> k_halo3 = make_halo_table<3>();
+__constant__ HaloTable<2> c_halo2 = k_halo2;
+__constant__ HaloTable<3> c_halo3 = k_halo3;
+
+template <int D> __device__ __forceinline__ uint32_t halo_item(int k) {
+    if constexpr (D == 2) return c_halo2.item[k]; else return c_halo3.item[k];
+}
+
+// ---------------------------------------------------------------------------
+// Hermite coefficients of one cell (shifted form):
+//   g_i = f_i - w_i = w_i [ dr + sum H2_ab(c_i) B_ab + sum c_a A_a + sum H3_t(c_i) G_t ]
+template <int D, typename R> struct Coef {
+    R dr;
+    R A[D];
+    R B[Geo<D>::NS];
+    R G[Geo<D>::N3];
+};
+
+template <int D, typename R>
+__device__ __forceinline__ void make_coef(const R (&m)[Geo<D>::NM], R h3xyz, Coef<D, R>& c) {
+    constexpr int NS = Geo<D>::NS;
+    const R rho = R(1) + m[0];
+    c.dr = m[0];
+    R u[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) { u[a] = m[1 + a]; c.A[a] = R(3) * rho * u[a]; }
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+        c.B[k] = (s_a<D>(k) == s_b<D>(k) ? R(4.5) : R(9)) * rho * m[1 + D + k];
+#pragma unroll
+    for (int t = 0; t < Geo<D>::N3; ++t) {
+        const int a = h3t<D>(t, 0), b = h3t<D>(t, 1), g = h3t<D>(t, 2);
+        const R Sab = m[1 + D + sidx<D>(a, b)], Sag = m[1 + D + sidx<D>(a, g)],
+                Sbg = m[1 + D + sidx<D>(b, g)];
+        const R gam = Sab * u[g] + Sag * u[b] + Sbg * u[a] - R(2) * u[a] * u[b] * u[g];
+        const R coef = (D == 3 && t == 6) ? h3xyz : R(13.5);
+        c.G[t] = coef * rho * gam;
+    }
+}
+
+template <int D, int I, typename R>
+__device__ __forceinline__ R even_part(const Coef<D, R>& c) {
+    R e = c.dr;
+#pragma unroll
+    for (int k = 0; k < Geo<D>::NS; ++k) e += R(h2v<D>(I, s_a<D>(k), s_b<D>(k))) * c.B[k];
+    return e;
+}
+template <int D, int I, typename R>
+__device__ __forceinline__ R odd_part(const Coef<D, R>& c) {
+    R o = R(0);
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+        if (cvec<D>(I, a) != 0) o += R(cvec<D>(I, a)) * c.A[a];
+#pragma unroll
+    for (int t = 0; t < Geo<D>::N3; ++t)
+        if (h3v<D>(I, t) != 0.0) o += R(h3v<D>(I, t)) * c.G[t];
+    return o;
+}
+template <int D, int I, typename R>
+__device__ __forceinline__ R g_dir(const Coef<D, R>& c) {
+    return R(wdir<D>(I)) * (even_part<D, I>(c) + odd_part<D, I>(c));
+}
+
+// runtime-direction reconstruct (halo items, special cells): switch over I
+template <int D, typename R, int I = 0>
+__device__ __forceinline__ R g_dir_rt(int i, const Coef<D, R>& c) {
+    if constexpr (I + 1 >= Geo<D>::Q) {
+        return g_dir<D, I>(c);
+    } else {
+        if (i == I) return g_dir<D, I>(c);
+        return g_dir_rt<D, R, I + 1>(i, c);
+    }
+}
+
+template <int D, typename R>
+__device__ __forceinline__ void load_moments(const FieldsT<R>& f, int64_t cell,
+                                             R (&m)[Geo<D>::NM]) {
+#pragma unroll
+    for (int k = 0; k < Geo<D>::NM; ++k) m[k] = __ldg(&f.at(k, cell));
+}
+
+// ---------------------------------------------------------------------------
+struct StepArgs {
+    mlbm_level_t lv;
+    mlbm_fields_t src, dst;
+    mlbm_collide_t cp;
+    mlbm_bc_t bc;
+    mlbm_error_t* err;
+};
+
+template <int D, int I, typename R>
+__device__ __forceinline__ void accumulate(R g, R& dr, R (&mm)[D], R (&pi)[Geo<D>::NS]) {
+    dr += g;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+        if (cvec<D>(I, a) != 0) mm[a] += R(cvec<D>(I, a)) * g;
+#pragma unroll
+    for (int k = 0; k < Geo<D>::NS; ++k) {
+        const double h = h2v<D>(I, s_a<D>(k), s_b<D>(k));
+        if (h != 0.0) pi[k] += R(h) * g;
+    }
+}
+
+template <int D, typename R, int P = 0>
+__device__ __forceinline__ void push_pairs(const Coef<D, R>& c, R* fb, int lc, const int (&l)[3]) {
+    if constexpr (P < Geo<D>::NP) {
+        constexpr int I = 2 * P + 1, J = 2 * P + 2;
+        constexpr int T = Geo<D>::T;
+        const R e = even_part<D, I>(c), o = odd_part<D, I>(c);
+        const R w = R(wdir<D>(I));
+        const R gp = w * (e + o), gm = w * (e - o);
+        constexpr int c0 = cvec<D>(I, 0), c1 = cvec<D>(I, 1), c2 = cvec<D>(I, 2);
+        // +c lands at l + c, -c at l - c
+        const bool inp = (unsigned)(l[0] + c0) < 4u && (unsigned)(l[1] + c1) < 4u &&
+                         (D == 2 || (unsigned)(l[2] + c2) < 4u);
+        const bool inm = (unsigned)(l[0] - c0) < 4u && (unsigned)(l[1] - c1) < 4u &&
+                         (D == 2 || (unsigned)(l[2] - c2) < 4u);
+        constexpr int doff = c0 + 4 * c1 + (D == 3 ? 16 * c2 : 0);
+        if (inp) fb[I * T + lc + doff] = gp;
+        if (inm) fb[J * T + lc - doff] = gm;
+        push_pairs<D, R, P + 1>(c, fb, lc, l);
+    }
+}
+
+template <int D, typename R, int I = 0>
+__device__ __forceinline__ void pull_all(const R* fb, int lc, bool special, uint64_t mask,
+                                         const Coef<D, R>& own, R& dr, R (&mm)[D],
+                                         R (&pi)[Geo<D>::NS]) {
+    if constexpr (I < Geo<D>::Q) {
+        constexpr int T = Geo<D>::T;
+        R g = fb[I * T + lc];
+        if (special) {
+            if ((mask >> I) & 1ull) g = g_dir<D, opp<D>(I)>(own);
+            else if ((mask >> (32 + I)) & 1ull) g = g_dir<D, I>(own);
+        }
+        accumulate<D, I>(g, dr, mm, pi);
+        pull_all<D, R, I + 1>(fb, lc, special, mask, own, dr, mm, pi);
+    }
+}
+
+template <int D, typename R>
+__device__ __forceinline__ void halo_work(const StepArgs& A, const FieldsT<R>& src, R* fb,
+                                          const int* snb, int lc, R h3xyz) {
+    constexpr int T = Geo<D>::T;
+    constexpr int NH = HaloTable<D>::N;
+    for (int k = lc; k < NH; k += T) {
+        const uint32_t it = halo_item<D>(k);
+        const int nbi = it & 31, srcl = (it >> 5) & 63, dir = (it >> 11) & 31,
+                  dstl = (it >> 16) & 63;
+        const int ns = snb[nbi];
+        if (ns < 0) continue;
+        R m[Geo<D>::NM];
+        load_moments<D, R>(src, (int64_t)ns * T + srcl, m);
+        Coef<D, R> c;
+        make_coef<D, R>(m, h3xyz, c);
+        fb[dir * T + dstl] = g_dir_rt<D, R>(dir, c);
+    }
+}
+
+// mode 0 fused, 1 stream only, 2 collide+bc only
+template <int D, typename R, int MODE>
+__global__ void __launch_bounds__(128) level_kernel(const StepArgs A) {
+    constexpr int T = Geo<D>::T, Q = Geo<D>::Q, NS = Geo<D>::NS, NM = Geo<D>::NM;
+    constexpr int TPC = 128 / T;
+    __shared__ R fbuf_all[TPC][Q * T];
+    __shared__ int snb_all[TPC][Geo<D>::NB];
+
+    const int grp = threadIdx.x / T, lc = threadIdx.x % T;
+    const int tile = blockIdx.x * TPC + grp;
+    const bool valid = tile < A.lv.n_tiles;
+    R* fb = fbuf_all[grp];
+    int* snb = snb_all[grp];
+    const FieldsT<R> src = fields_of<R>(A.src), dst = fields_of<R>(A.dst);
+    const R h3xyz = R(A.cp.h3_xyz);
+
+    if (MODE != 2 && valid && lc < Geo<D>::NB) snb[lc] = A.lv.nbr[(int64_t)tile * Geo<D>::NB + lc];
+
+    const int64_t cell = (int64_t)tile * T + lc;
+    int l[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
+    uint8_t cf = MLBM_CF_ACTIVE, tf = MLBM_TF_PLAIN;
+    int gx[3] = {0, 0, 0};
+    if (valid) {
+        tf = A.lv.tile_flags[tile];
+        cf = (tf & MLBM_TF_PLAIN) ? (uint8_t)MLBM_CF_ACTIVE : A.lv.cell_flags[cell];
+#pragma unroll
+        for (int a = 0; a < D; ++a) gx[a] = A.lv.tile_xyz[tile * 3 + a] * 4 + l[a];
+    }
+    const int any_bc = __syncthreads_or(valid && (tf & MLBM_TF_BC));
+    const bool active = cf & MLBM_CF_ACTIVE;
+
+    R dr, mm[D], pi[NS];
+    if constexpr (MODE != 2) {
+        Coef<D, R> own;
+        if (valid) {
+            R m[NM];
+            load_moments<D, R>(src, cell, m);
+            make_coef<D, R>(m, h3xyz, own);
+            push_pairs<D, R>(own, fb, lc, l);
+            fb[lc] = R(wdir<D>(0)) * even_part<D, 0>(own);
+            halo_work<D, R>(A, src, fb, snb, lc, h3xyz);
+        }
+        __syncthreads();
+        dr = R(0);
+#pragma unroll
+        for (int a = 0; a < D; ++a) mm[a] = R(0);
+#pragma unroll
+        for (int k = 0; k < NS; ++k) pi[k] = R(0);
+        if (valid) {
+            const bool special = cf & MLBM_CF_SPECIAL;
+            const uint64_t mask = special ? A.lv.dir_masks[cell] : 0ull;
+            pull_all<D, R>(fb, lc, special, mask, own, dr, mm, pi);
+        }
+        if constexpr (MODE == 1) {
+            if (valid) {
+                dst.at(0, cell) = dr;
+#pragma unroll
+                for (int a = 0; a < D; ++a) dst.at(1 + a, cell) = mm[a];
+#pragma unroll
+                for (int k = 0; k < NS; ++k) dst.at(1 + D + k, cell) = pi[k];
+                dst.at(fi_eps<D>(), cell) = src.at(fi_eps<D>(), cell);
+                dst.at(fi_phi<D>(), cell) = src.at(fi_phi<D>(), cell);
+            }
+            return;
+        }
+    } else {   // MODE 2, 3, 4 read the bare (2, 3) or collided (4) moments of dst
+        if (valid) {
+            dr = dst.at(0, cell);
+#pragma unroll
+            for (int a = 0; a < D; ++a) mm[a] = dst.at(1 + a, cell);
+#pragma unroll
+            for (int k = 0; k < NS; ++k) pi[k] = dst.at(1 + D + k, cell);
+        }
+    }
+
+    // ---- collide (solver.py:394-453) -------------------------------------
+    R out[NM];
+    if (MODE == 4 && valid) {
+        out[0] = dr;
+#pragma unroll
+        for (int a = 0; a < D; ++a) out[1 + a] = mm[a];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) out[1 + D + k] = pi[k];
+    }
+    if (MODE != 4 && valid) {
+        const R rho = R(1) + dr;
+        if (active && !(rho > R(0) && isfinite((double)rho)))
+            report_error(A.err, MLBM_ERR_DENSITY, A.lv.level, gx[0], gx[1], gx[2]);
+        R F[D];
+        if (A.cp.force_mode == 0) {
+            const R sc = R(1 << A.lv.level);
+#pragma unroll
+            for (int a = 0; a < D; ++a) F[a] = rho * (R(A.cp.gravity[a]) * sc);
+        } else {
+#pragma unroll
+            for (int a = 0; a < D; ++a) F[a] = dst.at(fi_f<D>(a), cell);
+        }
+        const R tau = A.cp.tau_mode == 0 ? R(A.cp.tau)
+                    : A.cp.tau_mode == 1 ? dst.at(fi_eps<D>(), cell) * R(A.cp.tau0)
+                                         : ((const R*)A.cp.tau_ptr)[cell];
+        const R inv_rho = R(1) / rho;
+        R us[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) us[a] = (mm[a] + R(0.5) * F[a]) * inv_rho;
+        const R inv_tau = R(1) / tau;
+        const R fcoef = (R(2) * tau - R(1)) / (R(2) * tau) * inv_rho;
+        out[0] = dr;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            const int a = s_a<D>(k), b = s_b<D>(k);
+            out[1 + D + k] = (R(1) - inv_tau) * (pi[k] * inv_rho) + inv_tau * us[a] * us[b] +
+                             fcoef * (F[a] * us[b] + F[b] * us[a]);
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a) out[1 + a] = us[a] + R(0.5) * F[a] * inv_rho;
+        if (!active) {
+#pragma unroll
+            for (int k = 0; k < NM; ++k) out[k] = src.at(k, cell);
+        } else {
+            bool bad = false;
+#pragma unroll
+            for (int a = 0; a < D; ++a) bad |= !isfinite((double)out[1 + a]);
+            if (bad) report_error(A.err, MLBM_ERR_VELOCITY, A.lv.level, gx[0], gx[1], gx[2]);
+        }
+    }
+
+    // ---- boundaries (solver.py:460-481), face order x-,x+,y-,y+,z-,z+ ------
+    if (MODE != 3 && any_bc) {   // block-uniform
+        __syncthreads();
+        R* mb = fb;   // reuse: [NM][T]
+        if (valid) {
+#pragma unroll
+            for (int k = 0; k < NM; ++k) mb[k * T + lc] = out[k];
+        }
+        __syncthreads();
+        const bool bct = valid && (tf & MLBM_TF_BC);
+        for (int face = 0; face < 2 * D; ++face) {
+            const int kind = A.bc.face[face];
+            if (kind != MLBM_FACE_OUTLET) continue;   // uniform
+            const int axis = face >> 1, side = face & 1;
+            const int edge = side == 0 ? 0 : A.lv.cells[axis] - 1;
+            R nv[NM];
+            bool on = bct && gx[axis] == edge;
+            if (on) {
+                const int inner = lc + (side == 0 ? 1 : -1) * (axis == 0 ? 1 : axis == 1 ? 4 : 16);
+                const R sgn = side == 0 ? R(-1) : R(1);
+                R un = sgn * mb[(1 + axis) * T + inner];
+                un = un > R(0) ? un : R(0);
+                un = un < R(1) ? un : R(1);
+#pragma unroll
+                for (int k = 0; k < NM; ++k) {
+                    const R v = mb[k * T + lc];
+                    nv[k] = v - un * (v - mb[k * T + inner]);
+                }
+            }
+            __syncthreads();
+            if (on) {
+#pragma unroll
+                for (int k = 0; k < NM; ++k) mb[k * T + lc] = nv[k];
+            }
+            __syncthreads();
+        }
+        if (A.bc.face[0] == MLBM_FACE_LOG_INLET && bct && gx[0] == 0) {
+            const double ypos = (double)gx[1] * (double)(1 << A.lv.level);
+            const double arg = 1.0 + A.bc.inlet_beta * (ypos - A.bc.inlet_y0);
+            const double uxv = ypos >= A.bc.inlet_y0 ? A.bc.inlet_u0 * log(arg > 1.0 ? arg : 1.0) : 0.0;
+            mb[lc] = R(A.bc.rho0 - 1.0);
+#pragma unroll
+            for (int a = 0; a < D; ++a) mb[(1 + a) * T + lc] = a == 0 ? R(uxv) : R(0);
+#pragma unroll
+            for (int k = 0; k < NS; ++k) mb[(1 + D + k) * T + lc] = k == 0 ? R(uxv * uxv) : R(0);
+        }
+        __syncthreads();
+        if (valid) {
+#pragma unroll
+            for (int k = 0; k < NM; ++k) out[k] = mb[k * T + lc];
+        }
+    }
+
+    if (valid) {
+#pragma unroll
+        for (int k = 0; k < NM; ++k) dst.at(k, cell) = out[k];
+        if ((MODE == 0 || !active) && MODE != 4) {
+            dst.at(fi_eps<D>(), cell) = src.at(fi_eps<D>(), cell);
+            dst.at(fi_phi<D>(), cell) = src.at(fi_phi<D>(), cell);
+        }
+    }
+}
+
+template <int D, typename R>
+int launch_level(const StepArgs& a, int mode, cudaStream_t s) {
+    constexpr int TPC = 128 / Geo<D>::T;
+    const int blocks = (a.lv.n_tiles + TPC - 1) / TPC;
+    if (blocks == 0) return 0;
+    switch (mode) {
+    case 0: level_kernel<D, R, 0><<<blocks, 128, 0, s>>>(a); break;
+    case 1: level_kernel<D, R, 1><<<blocks, 128, 0, s>>>(a); break;
+    case 2: level_kernel<D, R, 2><<<blocks, 128, 0, s>>>(a); break;
+    case 3: level_kernel<D, R, 3><<<blocks, 128, 0, s>>>(a); break;
+    default: level_kernel<D, R, 4><<<blocks, 128, 0, s>>>(a); break;
+    }
+    return launch_status();
+}
+
+// ---------------------------------------------------------------------------
+template <int D, typename R>
+__global__ void downward_kernel(int n, const int32_t* __restrict__ targets,
+                                const int32_t* __restrict__ srcs,
+                                const int32_t* __restrict__ tile_xyz,
+                                FieldsT<R> olda, FieldsT<R> newa, FieldsT<R> dst,
+                                int step, R kappa) {
+    constexpr int NC = Geo<D>::NC, NS = Geo<D>::NS, T = Geo<D>::T;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int tgt = targets[j];
+    const int slot = tgt / T, lc = tgt % T;
+    int par[3] = {lc & 1, (lc >> 2) & 1, (lc >> 4) & 1};
+    // fine coords parity == local parity (tile origin is a multiple of 4)
+    (void)tile_xyz; (void)slot;
+    R w[NC];
+    int s[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        R wk = R(1);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const int o = (k >> a) & 1;
+            const R fr = par[a] ? R(0.5) : R(0);
+            wk *= o ? fr : R(1) - fr;
+        }
+        w[k] = wk;
+        s[k] = srcs[(int64_t)j * NC + k];
+    }
+    constexpr int NV = Geo<D>::NM + 2;   // moments + eps + phi
+    R v[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        const int fk = q < Geo<D>::NM ? q : (q == Geo<D>::NM ? fi_eps<D>() : fi_phi<D>());
+        R acc = R(0);
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+            if (s[k] < 0) continue;
+            R x = olda.at(fk, s[k]);
+            if (step == 2) x = R(0.5) * (x + newa.at(fk, s[k]));
+            acc += x * w[k];
+        }
+        v[q] = acc;
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        const R eq = v[1 + s_a<D>(k)] * v[1 + s_b<D>(k)];
+        v[1 + D + k] = kappa * (v[1 + D + k] - eq) + eq;
+    }
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        const int fk = q < Geo<D>::NM ? q : (q == Geo<D>::NM ? fi_eps<D>() : fi_phi<D>());
+        dst.at(fk, tgt) = v[q];
+    }
+}
+
+template <int D, typename R>
+__global__ void upward_kernel(int n, const int32_t* __restrict__ targets,
+                              const int32_t* __restrict__ srcs, FieldsT<R> fine,
+                              FieldsT<R> dst, int average, R kappa) {
+    constexpr int NC = Geo<D>::NC, NS = Geo<D>::NS;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int tgt = targets[j];
+    constexpr int NV = Geo<D>::NM + 2;
+    R v[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        const int fk = q < Geo<D>::NM ? q : (q == Geo<D>::NM ? fi_eps<D>() : fi_phi<D>());
+        if (average) {
+            R acc = R(0);
+#pragma unroll
+            for (int k = 0; k < NC; ++k) acc += fine.at(fk, srcs[(int64_t)j * NC + k]);
+            v[q] = acc / R(NC);
+        } else {
+            v[q] = fine.at(fk, srcs[(int64_t)j * NC]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        const R eq = v[1 + s_a<D>(k)] * v[1 + s_b<D>(k)];
+        v[1 + D + k] = kappa * (v[1 + D + k] - eq) + eq;
+    }
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        const int fk = q < Geo<D>::NM ? q : (q == Geo<D>::NM ? fi_eps<D>() : fi_phi<D>());
+        dst.at(fk, tgt) = v[q];
+    }
+}
+
+}  // namespace mlbm
+
+using namespace mlbm;
+
+extern "C" int mlbm_level_step(const mlbm_level_t* lv, mlbm_fields_t src, mlbm_fields_t dst,
+                               int32_t dtype, int32_t mode, const mlbm_collide_t* cp,
+                               const mlbm_bc_t* bc, mlbm_error_t* err, void* stream) {
+    if (!lv || !cp || !bc || mode < 0 || mode > 4) return -1;
+    StepArgs a{*lv, src, dst, *cp, *bc, err};
+    cudaStream_t s = as_stream(stream);
+    if (lv->dim == 2) return dtype ? launch_level<2, double>(a, mode, s) : launch_level<2, float>(a, mode, s);
+    if (lv->dim == 3) return dtype ? launch_level<3, double>(a, mode, s) : launch_level<3, float>(a, mode, s);
+    return -1;
+}
+
+extern "C" int mlbm_downward(int32_t dim, int32_t n, const int32_t* targets, const int32_t* src,
+                             const int32_t* tile_xyz, mlbm_fields_t olda, mlbm_fields_t newa,
+                             mlbm_fields_t dst, int32_t dtype, int32_t step, double kappa,
+                             void* stream) {
+    if (n <= 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    const int B = 128, G = (n + B - 1) / B;
+#define DOWN(D, R) downward_kernel<D, R><<<G, B, 0, s>>>(n, targets, src, tile_xyz, \
+        fields_of<R>(olda), fields_of<R>(newa), fields_of<R>(dst), step, R(kappa))
+    if (dim == 2) { if (dtype) DOWN(2, double); else DOWN(2, float); }
+    else if (dim == 3) { if (dtype) DOWN(3, double); else DOWN(3, float); }
+    else return -1;
+#undef DOWN
+    return launch_status();
+}
+
+extern "C" int mlbm_upward(int32_t dim, int32_t n, const int32_t* targets, const int32_t* src,
+                           mlbm_fields_t fine, mlbm_fields_t dst, int32_t dtype,
+                           int32_t average, double kappa, void* stream) {
+    if (n <= 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    const int B = 128, G = (n + B - 1) / B;
+#define UP(D, R) upward_kernel<D, R><<<G, B, 0, s>>>(n, targets, src, fields_of<R>(fine), \
+        fields_of<R>(dst), average, R(kappa))
+    if (dim == 2) { if (dtype) UP(2, double); else UP(2, float); }
+    else if (dim == 3) { if (dtype) UP(3, double); else UP(3, float); }
+    else return -1;
+#undef UP
+    return launch_status();
+}

@@ -1,0 +1,875 @@
+// MPM sand + fluid-sediment exchange kernels (sm_100a).
+//
+//   mlbm_p2g        — stencil + Kirchhoff stress + P2G scatter fused with the
+//                     fraction rasterisation (granular.py:137-178, 260-310;
+//                     coupling.py:96-131)
+//   mlbm_exchange   — per level-0 cell: eps, cell velocity, Di Felice drag +
+//                     limiter, grad eps, mixture force (written into both
+//                     trees), MPM grid update with wall / sticky projection
+//                     (coupling.py:134-197, 379-446; granular.py:313-341)
+//   mlbm_g2p        — gather, advect, deformation update, SVD, Drucker-Prager
+//                     return map (granular.py:344-412)
+//   mlbm_stress_raster / mlbm_powder — entrainment source and powder
+//                     transport (coupling.py:200-322, 483-498)
+//   mlbm_diag_level / mlbm_diag_particles — diagnostics (coupling.py:500-531)
+//
+// Particle positions are always float64 (sub-cell offsets at x ~ 1e3 need
+// ~1e-8 absolute resolution); everything else follows the run dtype.
+#include "common.cuh"
+
+namespace mlbm {
+
+// raster row layout over level-0 cells
+template <int D> struct Rows {
+    static constexpr int MASS = 0, MOM = 1, FINT = 1 + D, ETA = 1 + 2 * D, AREA = 2 + 2 * D,
+                         VMOM = 3 + 2 * D, VEL = 3 + 3 * D, FS = 3 + 4 * D, EPS = 3 + 5 * D,
+                         GRAD = 4 + 5 * D, REL = 4 + 6 * D, SIG = 4 + 7 * D,
+                         N = 4 + 7 * D + Geo<D>::NS, NACC = 3 + 3 * D;
+};
+// particle row layout (after the float64 positions): v[D] C[D*D] F[D*D] m V0 vc
+template <int D> struct PRows {
+    static constexpr int V = 0, C = D, F = D + D * D, M = D + 2 * D * D, V0 = M + 1, VC = M + 2,
+                         N = M + 3;
+};
+
+struct TopoL0 {
+    int32_t cells[3], tiles[3], periodic[3];
+    const int32_t* tile_map;
+};
+
+MLBM_HD int64_t g3(const int* d, int x, int y, int z) { return ((int64_t)x * d[1] + y) * d[2] + z; }
+
+template <int D>
+__device__ __forceinline__ int64_t node_index(const TopoL0& t, int (&c)[3], bool& bad) {
+    for (int a = 0; a < D; ++a) {
+        if (t.periodic[a]) c[a] = ((c[a] % t.cells[a]) + t.cells[a]) % t.cells[a];
+        else if (c[a] < 0 || c[a] >= t.cells[a]) { bad = true; return -1; }
+    }
+    const int s = t.tile_map[g3(t.tiles, c[0] >> 2, c[1] >> 2, D == 3 ? c[2] >> 2 : 0)];
+    if (s < 0) { bad = true; return -1; }
+    return (int64_t)s * Geo<D>::T + local_of<D>(c[0] & 3, c[1] & 3, c[2] & 3);
+}
+
+// -- small dense linear algebra --------------------------------------------
+template <typename R> __device__ __forceinline__ R rsqrt_(R x) { return R(1) / sqrt(x); }
+
+// 2x2 closed form (granular.py:181-213)
+template <typename R>
+__device__ void svd2(const R (&F)[4], R (&U)[4], R (&s)[2], R (&V)[4]) {
+    const R a = F[0], b = F[1], c = F[2], d = F[3];
+    const R e = R(0.5) * (a + d), f = R(0.5) * (a - d), g = R(0.5) * (c + b), h = R(0.5) * (c - b);
+    const R q = hypot(e, h), r = hypot(f, g);
+    const R a1 = atan2(g, f), a2 = atan2(h, e);
+    const R tu = R(0.5) * (a1 + a2), tv = R(0.5) * (a1 - a2);
+    const R cu = cos(tu), su = sin(tu), cv = cos(tv), sv = sin(tv);
+    U[0] = cu; U[1] = -su; U[2] = su; U[3] = cu;
+    V[0] = cv; V[1] = -sv; V[2] = sv; V[3] = cv;
+    s[0] = q + r;
+    s[1] = q - r;
+}
+
+// 3x3 rotation-variant SVD: Jacobi on F^T F, Gram-Schmidt for U,
+// det U = det V = +1, sign on the smallest singular value.
+template <typename R>
+__device__ void svd3(const R (&F)[9], R (&U)[9], R (&s)[3], R (&V)[9]) {
+    R A[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            R acc = R(0);
+            for (int k = 0; k < 3; ++k) acc += F[k * 3 + i] * F[k * 3 + j];
+            A[i * 3 + j] = acc;
+        }
+    for (int i = 0; i < 9; ++i) V[i] = (i % 4 == 0) ? R(1) : R(0);
+    for (int sweep = 0; sweep < 10; ++sweep) {
+        const R off = A[1] * A[1] + A[2] * A[2] + A[5] * A[5];
+        const R dia = A[0] * A[0] + A[4] * A[4] + A[8] * A[8];
+        if (!(off > dia * R(sizeof(R) == 8 ? 1e-34 : 1e-16))) break;
+        for (int pq = 0; pq < 3; ++pq) {
+            const int p = pq == 2 ? 1 : 0, q = pq == 0 ? 1 : 2;
+            const R apq = A[p * 3 + q];
+            if (apq == R(0)) continue;
+            const R theta = (A[q * 3 + q] - A[p * 3 + p]) / (R(2) * apq);
+            const R t = (theta >= R(0) ? R(1) : R(-1)) / (fabs(theta) + sqrt(theta * theta + R(1)));
+            const R c = rsqrt_(t * t + R(1)), sn = t * c;
+            // A <- J^T A J
+            for (int k = 0; k < 3; ++k) {
+                const R akp = A[k * 3 + p], akq = A[k * 3 + q];
+                A[k * 3 + p] = c * akp - sn * akq;
+                A[k * 3 + q] = sn * akp + c * akq;
+            }
+            for (int k = 0; k < 3; ++k) {
+                const R apk = A[p * 3 + k], aqk = A[q * 3 + k];
+                A[p * 3 + k] = c * apk - sn * aqk;
+                A[q * 3 + k] = sn * apk + c * aqk;
+            }
+            for (int k = 0; k < 3; ++k) {
+                const R vkp = V[k * 3 + p], vkq = V[k * 3 + q];
+                V[k * 3 + p] = c * vkp - sn * vkq;
+                V[k * 3 + q] = sn * vkp + c * vkq;
+            }
+        }
+    }
+    // sort eigenvalues descending (columns of V)
+    R lam[3] = {A[0], A[4], A[8]};
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2 - i; ++j)
+            if (lam[j] < lam[j + 1]) {
+                const R tl = lam[j]; lam[j] = lam[j + 1]; lam[j + 1] = tl;
+                for (int k = 0; k < 3; ++k) {
+                    const R tv = V[k * 3 + j]; V[k * 3 + j] = V[k * 3 + j + 1]; V[k * 3 + j + 1] = tv;
+                }
+            }
+    // det V = +1
+    const R detV = V[0] * (V[4] * V[8] - V[5] * V[7]) - V[1] * (V[3] * V[8] - V[5] * V[6]) +
+                   V[2] * (V[3] * V[7] - V[4] * V[6]);
+    if (detV < R(0)) for (int k = 0; k < 3; ++k) V[k * 3 + 2] = -V[k * 3 + 2];
+    // B = F V
+    R B[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            R acc = R(0);
+            for (int k = 0; k < 3; ++k) acc += F[i * 3 + k] * V[k * 3 + j];
+            B[i * 3 + j] = acc;
+        }
+    // u0
+    R n0 = sqrt(B[0] * B[0] + B[3] * B[3] + B[6] * B[6]);
+    R u0[3];
+    if (n0 > R(0)) { u0[0] = B[0] / n0; u0[1] = B[3] / n0; u0[2] = B[6] / n0; }
+    else { u0[0] = R(1); u0[1] = R(0); u0[2] = R(0); }
+    R b1[3] = {B[1], B[4], B[7]};
+    R d01 = u0[0] * b1[0] + u0[1] * b1[1] + u0[2] * b1[2];
+    for (int k = 0; k < 3; ++k) b1[k] -= d01 * u0[k];
+    R n1 = sqrt(b1[0] * b1[0] + b1[1] * b1[1] + b1[2] * b1[2]);
+    R u1[3];
+    if (n1 > R(0) && n1 > n0 * R(sizeof(R) == 8 ? 1e-14 : 1e-6)) {
+        for (int k = 0; k < 3; ++k) u1[k] = b1[k] / n1;
+    } else {
+        // any unit vector orthogonal to u0
+        R e[3] = {R(0), R(0), R(0)};
+        int m = fabs(u0[0]) < fabs(u0[1]) ? (fabs(u0[0]) < fabs(u0[2]) ? 0 : 2) : (fabs(u0[1]) < fabs(u0[2]) ? 1 : 2);
+        e[m] = R(1);
+        R dd = u0[0] * e[0] + u0[1] * e[1] + u0[2] * e[2];
+        for (int k = 0; k < 3; ++k) e[k] -= dd * u0[k];
+        R ne = sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+        for (int k = 0; k < 3; ++k) u1[k] = e[k] / ne;
+    }
+    R u2[3] = {u0[1] * u1[2] - u0[2] * u1[1], u0[2] * u1[0] - u0[0] * u1[2], u0[0] * u1[1] - u0[1] * u1[0]};
+    for (int k = 0; k < 3; ++k) { U[k * 3 + 0] = u0[k]; U[k * 3 + 1] = u1[k]; U[k * 3 + 2] = u2[k]; }
+    s[0] = u0[0] * B[0] + u0[1] * B[3] + u0[2] * B[6];
+    s[1] = u1[0] * B[1] + u1[1] * B[4] + u1[2] * B[7];
+    s[2] = u2[0] * B[2] + u2[1] * B[5] + u2[2] * B[8];
+}
+
+template <int D, typename R>
+__device__ __forceinline__ void svd(const R (&F)[D * D], R (&U)[D * D], R (&s)[D], R (&V)[D * D]) {
+    if constexpr (D == 2) svd2<R>(F, U, s, V); else svd3<R>(F, U, s, V);
+}
+
+struct MatParams {
+    double lam, mu, alpha, floor_friction;
+};
+
+// tau = U diag(2 mu eps + lam tr) U^T  (granular.py:260-279)
+template <int D, typename R>
+__device__ void kirchhoff(const R (&F)[D * D], const MatParams& mp, R (&tau)[D * D]) {
+    R U[D * D], s[D], V[D * D];
+    svd<D, R>(F, U, s, V);
+    R e[D], tr = R(0);
+#pragma unroll
+    for (int a = 0; a < D; ++a) { e[a] = log(s[a] > R(1e-12) ? s[a] : R(1e-12)); tr += e[a]; }
+    R tp[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) tp[a] = R(2.0 * mp.mu) * e[a] + R(mp.lam) * tr;
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            R acc = R(0);
+#pragma unroll
+            for (int k = 0; k < D; ++k) acc += U[i * D + k] * tp[k] * U[j * D + k];
+            tau[i * D + j] = acc;
+        }
+}
+
+// B-spline stencil of one particle (granular.py:137-178)
+template <int D, typename R> struct Stencil {
+    int base[3];
+    R w[D][3], dw[D][3];
+    R frac[D];
+};
+template <int D, typename R>
+__device__ __forceinline__ void make_stencil(const double (&x)[D], Stencil<D, R>& st) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const double b = floor(x[a] - 0.5);
+        st.base[a] = (int)b;
+        const R f = R(x[a] - b);
+        st.frac[a] = f;
+        st.w[a][0] = R(0.5) * (R(1.5) - f) * (R(1.5) - f);
+        st.w[a][1] = R(0.75) - (f - R(1)) * (f - R(1));
+        st.w[a][2] = R(0.5) * (f - R(0.5)) * (f - R(0.5));
+        st.dw[a][0] = f - R(1.5);
+        st.dw[a][1] = R(-2) * (f - R(1));
+        st.dw[a][2] = f - R(0.5);
+    }
+    if (D == 2) st.base[2] = 0;
+}
+
+struct PartArgs {
+    int32_t dim, n;
+    const double* x;     // [D][n]
+    double* xw;          // writable positions (g2p)
+    void* p;             // [PRows::N][n] of R
+    int64_t ps;          // stride of p and x
+};
+
+template <typename R> __device__ __forceinline__ void aadd(R* a, R v) { atomicAdd(a, v); }
+
+// ---------------------------------------------------------------------------
+template <int D, typename R>
+__global__ void __launch_bounds__(128) k_p2g(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int64_t rs,
+                                             mlbm_error_t* err) {
+    constexpr int K = Geo<D>::K;
+    using RW = Rows<D>;
+    using PR = PRows<D>;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P.n) return;
+    const R* pp = (const R*)P.p;
+    double x[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) x[a] = P.x[a * P.ps + p];
+    Stencil<D, R> st;
+    make_stencil<D, R>(x, st);
+    R v[D], C[D * D], F[D * D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) v[a] = pp[(PR::V + a) * P.ps + p];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) { C[k] = pp[(PR::C + k) * P.ps + p]; F[k] = pp[(PR::F + k) * P.ps + p]; }
+    const R m = pp[PR::M * P.ps + p], V0 = pp[PR::V0 * P.ps + p];
+    R tau[D * D];
+    kirchhoff<D, R>(F, mp, tau);
+    const R ap = D == 2 ? R(2) * sqrt(V0 / R(3.14159265358979323846))
+                        : R(3.14159265358979323846) * pow(R(3) * V0 / (R(4) * R(3.14159265358979323846)), R(2.0 / 3.0));
+    bool bad = false;
+#pragma unroll 1
+    for (int k = 0; k < K; ++k) {
+        const int o[3] = {k % 3, (k / 3) % 3, k / 9};
+        int c[3] = {st.base[0] + o[0], st.base[1] + o[1], D == 3 ? st.base[2] + o[2] : 0};
+        const int64_t ni = node_index<D>(t0, c, bad);
+        if (ni < 0) continue;
+        R w = R(1), gr[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) { w *= st.w[a][o[a]]; gr[a] = R(1); }
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = 0; b < D; ++b) gr[b] *= (a == b) ? st.dw[a][o[a]] : st.w[a][o[a]];
+        R dpos[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) dpos[a] = R((double)(st.base[a] + o[a]) - x[a]);
+        const R wm = w * m;
+        aadd(&ras[RW::MASS * rs + ni], wm);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            R aff = v[a];
+#pragma unroll
+            for (int b = 0; b < D; ++b) aff += C[a * D + b] * dpos[b];
+            aadd(&ras[(RW::MOM + a) * rs + ni], wm * aff);
+            R fa = R(0);
+#pragma unroll
+            for (int b = 0; b < D; ++b) fa += V0 * tau[a * D + b] * gr[b];
+            aadd(&ras[(RW::FINT + a) * rs + ni], -fa);
+            aadd(&ras[(RW::VMOM + a) * rs + ni], wm * v[a]);
+        }
+        aadd(&ras[RW::ETA * rs + ni], w * V0);
+        aadd(&ras[RW::AREA * rs + ni], w * ap);
+    }
+    if (bad) report_error(err, MLBM_ERR_STENCIL, 0, st.base[0], st.base[1], st.base[2]);
+}
+
+// ---------------------------------------------------------------------------
+struct ExchArgs {
+    mlbm_level_t lv;          // level 0
+    mlbm_fields_t w_tree, r_tree;   // level-0 write (post-stream) / read trees
+    mlbm_fields_t tree0, tree1;     // both trees (eps / force written into both)
+    void* ras;
+    int64_t rs;
+    double eps_min, nu, d_p, re_min, dt, rho0;
+    double g_fluid[3], g_sed[3];
+    int32_t face[6];
+    double floor_friction;
+    int32_t mode;             // 1 exchange (drag + force + grid update), 0 grid update only
+};
+
+template <int D, typename R>
+__device__ __forceinline__ R eps_of(const R* ras, int64_t rs, const FieldsT<R>& rt, int64_t c, R eps_min) {
+    const R phi = rt.at(fi_phi<D>(), c);
+    R eta = ras[Rows<D>::ETA * rs + c] - phi;
+    eta = eta > R(0) ? eta : R(0);
+    R e = R(1) - eta - phi;
+    e = e < eps_min ? eps_min : (e > R(1) ? R(1) : e);
+    return e;
+}
+
+template <int D, typename R>
+__global__ void k_exchange(ExchArgs A) {
+    constexpr int T = Geo<D>::T;
+    using RW = Rows<D>;
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= (int64_t)A.lv.n_tiles * T) return;
+    R* ras = (R*)A.ras;
+    const int64_t rs = A.rs;
+    const FieldsT<R> wt = fields_of<R>(A.w_tree), rt = fields_of<R>(A.r_tree);
+    const int slot = (int)(c / T), lc = (int)(c % T);
+    const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
+    int g[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) g[a] = A.lv.tile_xyz[slot * 3 + a] * 4 + l3[a];
+    const R mass = ras[RW::MASS * rs + c];
+    R fs[D];
+    for (int a = 0; a < D; ++a) fs[a] = R(0);
+    const R eps_min = R(A.eps_min);
+    if (A.mode == 1) {
+        const R eps = eps_of<D, R>(ras, rs, rt, c, eps_min);
+        R eta = ras[RW::ETA * rs + c] - rt.at(fi_phi<D>(), c);
+        eta = eta > R(0) ? eta : R(0);
+        R vcell[D];
+        for (int a = 0; a < D; ++a) vcell[a] = mass > R(0) ? ras[(RW::VMOM + a) * rs + c] / mass : R(0);
+        const R rho = R(1) + wt.at(0, c);
+        R u[D], rel[D], sp2 = R(0);
+        for (int a = 0; a < D; ++a) {
+            u[a] = wt.at(1 + a, c) / rho;
+            rel[a] = u[a] - vcell[a];
+            sp2 += rel[a] * rel[a];
+        }
+        const R speed = sqrt(sp2);
+        const R area = ras[RW::AREA * rs + c];
+        if (area > R(0) && speed > R(0)) {
+            R re = eps * speed * R(A.d_p) / R(A.nu);
+            re = re > R(A.re_min) ? re : R(A.re_min);
+            const R cd = (R(0.63) + R(4.8) / sqrt(re)) * (R(0.63) + R(4.8) / sqrt(re));
+            const R lg = R(1.5) - log10(re);
+            const R chi = R(3.7) - R(0.65) * exp(R(-0.5) * lg * lg);
+            const R coef = R(0.5) * cd * pow(eps, -chi) * rho * area * speed;
+            for (int a = 0; a < D; ++a) fs[a] = coef * rel[a];
+            // limiter (coupling.py:379-401)
+            R mag2 = R(0);
+            for (int a = 0; a < D; ++a) mag2 += fs[a] * fs[a];
+            const R mag = sqrt(mag2);
+            if (mag > R(0)) {
+                const R inv_m = R(1) / rho + R(1) / (mass > R(1e-12) ? mass : R(1e-12));
+                const R beta = mag * R(A.dt) * inv_m / (speed > R(1e-14) ? speed : R(1e-14));
+                R over = beta - R(0.5);
+                over = over > R(0) ? over : R(0);
+                const R real = (beta < R(0.5) ? beta : R(0.5)) + over / (R(1) + over);
+                const R scale = real / (beta > R(1e-14) ? beta : R(1e-14));
+                for (int a = 0; a < D; ++a) fs[a] *= scale;
+            }
+        }
+        // grad eps (coupling.py:159-182): neighbours clip / wrap, missing -> own
+        R grad[D];
+        for (int a = 0; a < D; ++a) {
+            R pm[2];
+            for (int sgn = 0; sgn < 2; ++sgn) {
+                int nb[3] = {g[0], g[1], g[2]};
+                nb[a] += sgn == 0 ? 1 : -1;
+                if (A.lv.periodic[a]) nb[a] = (nb[a] + A.lv.cells[a]) % A.lv.cells[a];
+                else nb[a] = nb[a] < 0 ? 0 : (nb[a] >= A.lv.cells[a] ? A.lv.cells[a] - 1 : nb[a]);
+                const int s = A.lv.tile_map[g3(A.lv.tiles, nb[0] >> 2, nb[1] >> 2, D == 3 ? nb[2] >> 2 : 0)];
+                const int64_t ni = s >= 0 ? (int64_t)s * T + local_of<D>(nb[0] & 3, nb[1] & 3, nb[2] & 3) : c;
+                pm[sgn] = eps_of<D, R>(ras, rs, rt, ni, eps_min);
+            }
+            grad[a] = R(0.5) * (pm[0] - pm[1]);
+        }
+        const R coefg = (rho - R(A.rho0)) / eps;
+        const FieldsT<R> t0 = fields_of<R>(A.tree0), t1 = fields_of<R>(A.tree1);
+        for (int a = 0; a < D; ++a) {
+            const R gt = coefg * grad[a];
+            const R force = gt + rho * R(A.g_fluid[a]) - fs[a];
+            t0.at(fi_f<D>(a), c) = force;
+            t1.at(fi_f<D>(a), c) = force;
+            ras[(RW::GRAD + a) * rs + c] = gt;
+            ras[(RW::REL + a) * rs + c] = rel[a];
+            ras[(RW::FS + a) * rs + c] = fs[a];
+            ras[(RW::VMOM + a) * rs + c] = vcell[a];   // becomes the cell velocity
+        }
+        t0.at(fi_eps<D>(), c) = eps;
+        t1.at(fi_eps<D>(), c) = eps;
+        ras[RW::EPS * rs + c] = eps;
+        ras[RW::ETA * rs + c] = eta;                   // becomes eta_eff
+    }
+    // MPM grid update (granular.py:313-341)
+    R vel[D];
+    if (mass > R(0)) {
+        const R inv_m = R(1) / mass;
+        for (int a = 0; a < D; ++a)
+            vel[a] = (ras[(RW::MOM + a) * rs + c] + R(A.dt) * (ras[(RW::FINT + a) * rs + c] + fs[a])) * inv_m
+                     + R(A.dt) * R(A.g_sed[a]);
+    } else {
+        for (int a = 0; a < D; ++a) vel[a] = R(0);
+    }
+    for (int f = 0; f < 2 * D; ++f) {
+        if (A.face[f] != MLBM_FACE_WALL) continue;
+        const int axis = f >> 1;
+        const bool lo = (f & 1) == 0;
+        const bool in_band = lo ? g[axis] <= 1 : g[axis] >= A.lv.cells[axis] - 2;
+        if (!in_band) continue;
+        const R sgn = lo ? R(1) : R(-1);
+        const R vn = sgn * vel[axis];
+        if (!(vn < R(0))) continue;
+        R vt2 = R(0);
+        for (int b = 0; b < D; ++b) if (b != axis) vt2 += vel[b] * vel[b];
+        const R vtn = sqrt(vt2);
+        R scale = R(1) - R(A.floor_friction) * (-vn) / (vtn > R(1e-14) ? vtn : R(1e-14));
+        scale = scale > R(0) ? scale : R(0);
+        vel[axis] = R(0);
+        for (int b = 0; b < D; ++b) if (b != axis) vel[b] *= scale;
+    }
+    if (A.lv.cell_flags[c] & MLBM_CF_SOLID)
+        for (int a = 0; a < D; ++a) vel[a] = R(0);
+    for (int a = 0; a < D; ++a) ras[(RW::VEL + a) * rs + c] = vel[a];
+}
+
+// ---------------------------------------------------------------------------
+template <int D, typename R>
+__global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp, const R* ras, int64_t rs,
+                                             double dt, int plastic, int32_t* clamped, mlbm_error_t* err) {
+    constexpr int K = Geo<D>::K;
+    using RW = Rows<D>;
+    using PR = PRows<D>;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P.n) return;
+    R* pp = (R*)P.p;
+    double x[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) x[a] = P.x[a * P.ps + p];
+    Stencil<D, R> st;
+    make_stencil<D, R>(x, st);
+    R v[D], B[D * D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) v[a] = R(0);
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) B[k] = R(0);
+    bool bad = false;
+#pragma unroll 1
+    for (int k = 0; k < K; ++k) {
+        const int o[3] = {k % 3, (k / 3) % 3, k / 9};
+        int c[3] = {st.base[0] + o[0], st.base[1] + o[1], D == 3 ? st.base[2] + o[2] : 0};
+        const int64_t ni = node_index<D>(t0, c, bad);
+        if (ni < 0) continue;
+        R w = R(1);
+#pragma unroll
+        for (int a = 0; a < D; ++a) w *= st.w[a][o[a]];
+        R dpos[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) dpos[a] = R((double)(st.base[a] + o[a]) - x[a]);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const R wg = w * ras[(RW::VEL + a) * rs + ni];
+            v[a] += wg;
+#pragma unroll
+            for (int b = 0; b < D; ++b) B[a * D + b] += wg * dpos[b];
+        }
+    }
+    if (bad) report_error(err, MLBM_ERR_STENCIL, 0, st.base[0], st.base[1], st.base[2]);
+    R C[D * D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) C[k] = R(4) * B[k];
+    int ncl = 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        double xn = x[a] + dt * (double)v[a];
+        const double dim = (double)t0.cells[a];
+        if (t0.periodic[a]) {
+            xn = fmod(xn, dim);
+            if (xn < 0) xn += dim;
+            if (xn >= dim) xn -= dim;
+        } else {
+            if (xn < 2.0 || xn > dim - 2.0) ++ncl;
+            xn = xn < 2.0 ? 2.0 : (xn > dim - 2.0 ? dim - 2.0 : xn);
+        }
+        P.xw[a * P.ps + p] = xn;
+        pp[(PR::V + a) * P.ps + p] = v[a];
+    }
+    if (ncl) atomicAdd(clamped, ncl);
+    R F[D * D], Fn[D * D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) { F[k] = pp[(PR::F + k) * P.ps + p]; pp[(PR::C + k) * P.ps + p] = C[k]; }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            R acc = R(0);
+#pragma unroll
+            for (int k = 0; k < D; ++k) acc += ((i == k ? R(1) : R(0)) + R(dt) * C[i * D + k]) * F[k * D + j];
+            Fn[i * D + j] = acc;
+        }
+    if (plastic) {
+        R U[D * D], s[D], V[D * D];
+        svd<D, R>(Fn, U, s, V);
+        R e[D], tr = R(0);
+        const R vc = pp[PR::VC * P.ps + p];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            R sa = s[a] < R(0.05) ? R(0.05) : (s[a] > R(4) ? R(4) : s[a]);
+            e[a] = log(sa) + vc / R(D);
+            tr += e[a];
+        }
+        R eh[D], nrm2 = R(0);
+#pragma unroll
+        for (int a = 0; a < D; ++a) { eh[a] = e[a] - tr / R(D); nrm2 += eh[a] * eh[a]; }
+        const R nrm = sqrt(nrm2);
+        const R dg = nrm + R((D * mp.lam + 2.0 * mp.mu) / (2.0 * mp.mu)) * tr * R(mp.alpha);
+        R en[D];
+        if (tr > R(0)) {
+#pragma unroll
+            for (int a = 0; a < D; ++a) en[a] = R(0);
+        } else if (nrm > R(0) && dg > R(0)) {
+            const R sc = dg / nrm;
+#pragma unroll
+            for (int a = 0; a < D; ++a) en[a] = e[a] - sc * eh[a];
+        } else {
+#pragma unroll
+            for (int a = 0; a < D; ++a) en[a] = e[a];
+        }
+        R sum = R(0), se[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) { sum += en[a]; se[a] = exp(en[a]); }
+        pp[PR::VC * P.ps + p] = tr - sum;
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                R acc = R(0);
+#pragma unroll
+                for (int k = 0; k < D; ++k) acc += U[i * D + k] * se[k] * V[j * D + k];
+                Fn[i * D + j] = acc;
+            }
+    }
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) pp[(PR::F + k) * P.ps + p] = Fn[k];
+}
+
+// ---------------------------------------------------------------------------
+// entrainment stress raster (coupling.py:283-294) with post-G2P positions
+template <int D, typename R>
+__global__ void k_stress_raster(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int64_t rs, mlbm_error_t* err) {
+    constexpr int K = Geo<D>::K, NS = Geo<D>::NS;
+    using RW = Rows<D>;
+    using PR = PRows<D>;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P.n) return;
+    const R* pp = (const R*)P.p;
+    double x[D];
+    for (int a = 0; a < D; ++a) x[a] = P.x[a * P.ps + p];
+    Stencil<D, R> st;
+    make_stencil<D, R>(x, st);
+    R F[D * D];
+    for (int k = 0; k < D * D; ++k) F[k] = pp[(PR::F + k) * P.ps + p];
+    R tau[D * D];
+    kirchhoff<D, R>(F, mp, tau);
+    const R V0 = pp[PR::V0 * P.ps + p];
+    bool bad = false;
+    for (int k = 0; k < K; ++k) {
+        const int o[3] = {k % 3, (k / 3) % 3, k / 9};
+        int c[3] = {st.base[0] + o[0], st.base[1] + o[1], D == 3 ? st.base[2] + o[2] : 0};
+        const int64_t ni = node_index<D>(t0, c, bad);
+        if (ni < 0) continue;
+        R w = V0;
+        for (int a = 0; a < D; ++a) w *= st.w[a][o[a]];
+        for (int q = 0; q < NS; ++q) aadd(&ras[(RW::SIG + q) * rs + ni], w * tau[s_a<D>(q) * D + s_b<D>(q)]);
+    }
+    if (bad) report_error(err, MLBM_ERR_STENCIL, 0, st.base[0], st.base[1], st.base[2]);
+}
+
+// renormalised multilinear sample of a level-0 field (coupling.py:200-227)
+template <int D, typename R>
+__device__ R sample_lin(const R* f, const double (&pos)[D], const mlbm_level_t& lv) {
+    constexpr int T = Geo<D>::T;
+    int b[D];
+    double fr[D];
+    for (int a = 0; a < D; ++a) { const double fl = floor(pos[a]); b[a] = (int)fl; fr[a] = pos[a] - fl; }
+    double acc = 0.0, ws = 0.0;
+    for (int k = 0; k < (1 << D); ++k) {
+        int c[3] = {0, 0, 0};
+        double w = 1.0;
+        for (int a = 0; a < D; ++a) {
+            const int o = (k >> a) & 1;
+            int v = b[a] + o;
+            if (lv.periodic[a]) v = ((v % lv.cells[a]) + lv.cells[a]) % lv.cells[a];
+            else v = v < 0 ? 0 : (v >= lv.cells[a] ? lv.cells[a] - 1 : v);
+            c[a] = v;
+            w *= o ? fr[a] : 1.0 - fr[a];
+        }
+        const int s = lv.tile_map[g3(lv.tiles, c[0] >> 2, c[1] >> 2, D == 3 ? c[2] >> 2 : 0)];
+        if (s < 0) continue;
+        const int64_t ni = (int64_t)s * T + local_of<D>(c[0] & 3, c[1] & 3, c[2] & 3);
+        acc += w * (double)f[ni];
+        ws += w;
+    }
+    return ws > 0.0 ? R(acc / ws) : R(acc);
+}
+
+struct PowderArgs {
+    mlbm_level_t lv;
+    mlbm_fields_t src, dst;   // last read / write trees of level 0
+    void* ras;
+    int64_t rs;
+    void* tmp;                // [n0] scratch (advected phi)
+    double diffusion, sign, dt, entrain, eta_surface;
+    int32_t with_source;
+};
+
+template <int D, typename R>
+__global__ void k_powder_advect(PowderArgs A) {
+    constexpr int T = Geo<D>::T;
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= (int64_t)A.lv.n_tiles * T) return;
+    const FieldsT<R> src = fields_of<R>(A.src), dst = fields_of<R>(A.dst);
+    const int slot = (int)(c / T), lc = (int)(c % T);
+    const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
+    double pos[D];
+    for (int a = 0; a < D; ++a) pos[a] = (double)(A.lv.tile_xyz[slot * 3 + a] * 4 + l3[a]);
+    const R* u[D];
+    for (int a = 0; a < D; ++a) u[a] = &dst.at(1 + a, 0);
+    double k1[D], k2[D], k3[D], q[D];
+    for (int a = 0; a < D; ++a) k1[a] = (double)sample_lin<D, R>(u[a], pos, A.lv);
+    for (int a = 0; a < D; ++a) q[a] = pos[a] - 0.5 * A.dt * k1[a];
+    for (int a = 0; a < D; ++a) k2[a] = (double)sample_lin<D, R>(u[a], q, A.lv);
+    for (int a = 0; a < D; ++a) q[a] = pos[a] - 0.75 * A.dt * k2[a];
+    for (int a = 0; a < D; ++a) k3[a] = (double)sample_lin<D, R>(u[a], q, A.lv);
+    for (int a = 0; a < D; ++a) q[a] = pos[a] - A.dt * (2.0 * k1[a] + 3.0 * k2[a] + 4.0 * k3[a]) / 9.0;
+    ((R*)A.tmp)[c] = sample_lin<D, R>(&src.at(fi_phi<D>(), 0), q, A.lv);
+}
+
+template <int D, typename R>
+__global__ void k_powder_diffuse(PowderArgs A) {
+    constexpr int T = Geo<D>::T, NS = Geo<D>::NS;
+    using RW = Rows<D>;
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= (int64_t)A.lv.n_tiles * T) return;
+    const FieldsT<R> dst = fields_of<R>(A.dst);
+    const R* adv = (const R*)A.tmp;
+    const R* ras = (const R*)A.ras;
+    const int64_t rs = A.rs;
+    const int slot = (int)(c / T), lc = (int)(c % T);
+    const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
+    int g[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) g[a] = A.lv.tile_xyz[slot * 3 + a] * 4 + l3[a];
+    R lap = R(-2 * D) * adv[c];
+    bool has_empty = false;
+    const R eta_c = A.with_source ? ras[RW::ETA * rs + c] : R(0);
+    for (int a = 0; a < D; ++a)
+        for (int sgn = 0; sgn < 2; ++sgn) {
+            int nb[3] = {g[0], g[1], g[2]};
+            nb[a] += sgn == 0 ? 1 : -1;
+            if (A.lv.periodic[a]) nb[a] = (nb[a] + A.lv.cells[a]) % A.lv.cells[a];
+            else nb[a] = nb[a] < 0 ? 0 : (nb[a] >= A.lv.cells[a] ? A.lv.cells[a] - 1 : nb[a]);
+            const int s = A.lv.tile_map[g3(A.lv.tiles, nb[0] >> 2, nb[1] >> 2, D == 3 ? nb[2] >> 2 : 0)];
+            const int64_t ni = s >= 0 ? (int64_t)s * T + local_of<D>(nb[0] & 3, nb[1] & 3, nb[2] & 3) : c;
+            lap += adv[ni];
+            if (A.with_source) {
+                if (s < 0) has_empty = true;
+                else if (ras[RW::ETA * rs + ni] < R(1e-3)) has_empty = true;
+            }
+        }
+    R out = adv[c] + R(A.sign * A.diffusion * A.dt) * lap;
+    if (A.with_source) {
+        R sp2 = R(0), v[D];
+        for (int a = 0; a < D; ++a) { v[a] = ras[(RW::VMOM + a) * rs + c]; sp2 += v[a] * v[a]; }
+        const R speed = sqrt(sp2);
+        R q = R(0);
+        if (eta_c > R(0) && eta_c < R(A.eta_surface) && has_empty && speed > R(0)) {
+            R vsv = R(0);
+            for (int k = 0; k < NS; ++k) {
+                const int a = s_a<D>(k), b = s_b<D>(k);
+                vsv += (a == b ? R(1) : R(2)) * v[a] * v[b] * ras[(RW::SIG + k) * rs + c];
+            }
+            q = R(A.entrain) * fabs(vsv) / speed;
+        }
+        out += R(A.dt) * q;
+    }
+    dst.at(fi_phi<D>(), c) = out;
+}
+
+// ---------------------------------------------------------------------------
+// diagnostics: out[0..D-1] += vol * sum rho u (leaf), out[D] += vol * sum phi,
+// out[D+1] = min eps (leaf), via double atomics
+template <int D, typename R>
+__global__ void k_diag_level(mlbm_level_t lv, mlbm_fields_t f, double vol, double* out) {
+    constexpr int T = Geo<D>::T;
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double acc[D + 1];
+    for (int k = 0; k <= D; ++k) acc[k] = 0.0;
+    double emin = 1e300;
+    if (c < (int64_t)lv.n_tiles * T && (lv.cell_flags[c] & MLBM_CF_LEAF)) {
+        const FieldsT<R> a = fields_of<R>(f);
+        const double rho = 1.0 + (double)a.at(0, c);
+        for (int k = 0; k < D; ++k) acc[k] = vol * rho * (double)a.at(1 + k, c);
+        acc[D] = vol * (double)a.at(fi_phi<D>(), c);
+        emin = (double)a.at(fi_eps<D>(), c);
+    }
+    for (int k = 0; k <= D; ++k)
+        for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_down_sync(0xffffffffu, acc[k], off);
+    for (int off = 16; off > 0; off >>= 1) emin = fmin(emin, __shfl_down_sync(0xffffffffu, emin, off));
+    if ((threadIdx.x & 31) == 0) {
+        for (int k = 0; k <= D; ++k) if (acc[k] != 0.0) atomicAdd(&out[k], acc[k]);
+        if (emin < 1e300) {
+            unsigned long long* addr = (unsigned long long*)&out[D + 1];
+            unsigned long long old = *addr, assumed;
+            do {
+                assumed = old;
+                if (__longlong_as_double(assumed) <= emin) break;
+                old = atomicCAS(addr, assumed, __double_as_longlong(emin));
+            } while (assumed != old);
+        }
+    }
+}
+
+// out[0..D-1] += sum m v ; out[D..2D-1] += sum fs (level-0 cells)
+template <int D, typename R>
+__global__ void k_diag_particles(PartArgs P, const R* ras, int64_t rs, int64_t n0, double* out) {
+    using PR = PRows<D>;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double acc[2 * D];
+    for (int k = 0; k < 2 * D; ++k) acc[k] = 0.0;
+    if (i < P.n) {
+        const R* pp = (const R*)P.p;
+        const double m = (double)pp[PR::M * P.ps + i];
+        for (int a = 0; a < D; ++a) acc[a] = m * (double)pp[(PR::V + a) * P.ps + i];
+    }
+    if (ras && i < n0)
+        for (int a = 0; a < D; ++a) acc[D + a] = (double)ras[(Rows<D>::FS + a) * rs + i];
+    for (int k = 0; k < 2 * D; ++k) {
+        for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_down_sync(0xffffffffu, acc[k], off);
+        if ((threadIdx.x & 31) == 0 && acc[k] != 0.0) atomicAdd(&out[k], acc[k]);
+    }
+}
+
+}  // namespace mlbm
+
+using namespace mlbm;
+
+static inline int nblk(int64_t n, int b) { return (int)((n + b - 1) / b); }
+static TopoL0 topo0(const mlbm_level_t* lv) {
+    TopoL0 t;
+    for (int a = 0; a < 3; ++a) { t.cells[a] = lv->cells[a]; t.tiles[a] = lv->tiles[a]; t.periodic[a] = lv->periodic[a]; }
+    t.tile_map = lv->tile_map;
+    return t;
+}
+
+extern "C" int mlbm_raster_rows(int32_t dim) { return dim == 2 ? Rows<2>::N : Rows<3>::N; }
+extern "C" int mlbm_particle_rows(int32_t dim) { return dim == 2 ? PRows<2>::N : PRows<3>::N; }
+
+extern "C" int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, void* p, int64_t ps,
+                        double lam, double mu, double alpha, void* ras, int64_t rs, int32_t dtype,
+                        mlbm_error_t* err, void* stream) {
+    if (n <= 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    PartArgs P{lv0->dim, n, x, nullptr, p, ps};
+    MatParams mp{lam, mu, alpha, 0.0};
+    const TopoL0 t = topo0(lv0);
+#define P2G(D, R) k_p2g<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err)
+    if (lv0->dim == 2) { if (dtype) P2G(2, double); else P2G(2, float); }
+    else { if (dtype) P2G(3, double); else P2G(3, float); }
+#undef P2G
+    return launch_status();
+}
+
+extern "C" int mlbm_exchange(const mlbm_level_t* lv0, mlbm_fields_t w_tree, mlbm_fields_t r_tree,
+                             mlbm_fields_t tree0, mlbm_fields_t tree1, void* ras, int64_t rs,
+                             double eps_min, double nu, double d_p, double re_min, double dt,
+                             double rho0, const double* g_fluid, const double* g_sed,
+                             const int32_t* faces, double floor_friction, int32_t mode,
+                             int32_t dtype, void* stream) {
+    const int T = lv0->dim == 2 ? 16 : 64;
+    const int64_t n = (int64_t)lv0->n_tiles * T;
+    if (n == 0) return 0;
+    ExchArgs A;
+    A.lv = *lv0; A.w_tree = w_tree; A.r_tree = r_tree; A.tree0 = tree0; A.tree1 = tree1;
+    A.ras = ras; A.rs = rs; A.eps_min = eps_min; A.nu = nu; A.d_p = d_p; A.re_min = re_min;
+    A.dt = dt; A.rho0 = rho0;
+    for (int a = 0; a < 3; ++a) { A.g_fluid[a] = g_fluid[a]; A.g_sed[a] = g_sed[a]; }
+    for (int f = 0; f < 6; ++f) A.face[f] = faces[f];
+    A.floor_friction = floor_friction;
+    A.mode = mode;
+    cudaStream_t s = as_stream(stream);
+#define EX(D, R) k_exchange<D, R><<<nblk(n, 128), 128, 0, s>>>(A)
+    if (lv0->dim == 2) { if (dtype) EX(2, double); else EX(2, float); }
+    else { if (dtype) EX(3, double); else EX(3, float); }
+#undef EX
+    return launch_status();
+}
+
+extern "C" int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, double* x, void* p, int64_t ps,
+                        double lam, double mu, double alpha, const void* ras, int64_t rs, double dt,
+                        int32_t plastic, int32_t dtype, int32_t* clamped, mlbm_error_t* err,
+                        void* stream) {
+    if (n <= 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    PartArgs P{lv0->dim, n, x, x, p, ps};
+    MatParams mp{lam, mu, alpha, 0.0};
+    const TopoL0 t = topo0(lv0);
+#define G2P(D, R) k_g2p<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (const R*)ras, rs, dt, plastic, clamped, err)
+    if (lv0->dim == 2) { if (dtype) G2P(2, double); else G2P(2, float); }
+    else { if (dtype) G2P(3, double); else G2P(3, float); }
+#undef G2P
+    return launch_status();
+}
+
+extern "C" int mlbm_stress_raster(const mlbm_level_t* lv0, int32_t n, const double* x, const void* p,
+                                  int64_t ps, double lam, double mu, double alpha, void* ras, int64_t rs,
+                                  int32_t dtype, mlbm_error_t* err, void* stream) {
+    if (n <= 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    PartArgs P{lv0->dim, n, x, nullptr, (void*)p, ps};
+    MatParams mp{lam, mu, alpha, 0.0};
+    const TopoL0 t = topo0(lv0);
+#define SR(D, R) k_stress_raster<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err)
+    if (lv0->dim == 2) { if (dtype) SR(2, double); else SR(2, float); }
+    else { if (dtype) SR(3, double); else SR(3, float); }
+#undef SR
+    return launch_status();
+}
+
+extern "C" int mlbm_powder(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm_fields_t dst, void* ras,
+                           int64_t rs, void* tmp, double diffusion, double sign, double dt,
+                           double entrain, double eta_surface, int32_t with_source, int32_t dtype,
+                           void* stream) {
+    const int T = lv0->dim == 2 ? 16 : 64;
+    const int64_t n = (int64_t)lv0->n_tiles * T;
+    if (n == 0) return 0;
+    PowderArgs A{*lv0, src, dst, ras, rs, tmp, diffusion, sign, dt, entrain, eta_surface, with_source};
+    cudaStream_t s = as_stream(stream);
+#define PW(D, R) do { k_powder_advect<D, R><<<nblk(n, 128), 128, 0, s>>>(A); \
+                      k_powder_diffuse<D, R><<<nblk(n, 128), 128, 0, s>>>(A); } while (0)
+    if (lv0->dim == 2) { if (dtype) PW(2, double); else PW(2, float); }
+    else { if (dtype) PW(3, double); else PW(3, float); }
+#undef PW
+    return launch_status();
+}
+
+extern "C" int mlbm_diag_level(const mlbm_level_t* lv, mlbm_fields_t f, double vol, int32_t dtype,
+                               double* out, void* stream) {
+    const int T = lv->dim == 2 ? 16 : 64;
+    const int64_t n = (int64_t)lv->n_tiles * T;
+    if (n == 0) return 0;
+    cudaStream_t s = as_stream(stream);
+#define DG(D, R) k_diag_level<D, R><<<nblk(n, 256), 256, 0, s>>>(*lv, f, vol, out)
+    if (lv->dim == 2) { if (dtype) DG(2, double); else DG(2, float); }
+    else { if (dtype) DG(3, double); else DG(3, float); }
+#undef DG
+    return launch_status();
+}
+
+extern "C" int mlbm_diag_particles(int32_t dim, int32_t n, const void* p, int64_t ps, const void* ras,
+                                   int64_t rs, int64_t n0, int32_t dtype, double* out, void* stream) {
+    const int64_t m = n > n0 ? n : n0;
+    if (m == 0) return 0;
+    PartArgs P{dim, n, nullptr, nullptr, (void*)p, ps};
+    cudaStream_t s = as_stream(stream);
+#define DP(D, R) k_diag_particles<D, R><<<nblk(m, 256), 256, 0, s>>>(P, (const R*)ras, rs, n0, out)
+    if (dim == 2) { if (dtype) DP(2, double); else DP(2, float); }
+    else { if (dtype) DP(3, double); else DP(3, float); }
+#undef DP
+    return launch_status();
+}

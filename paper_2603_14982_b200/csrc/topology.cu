@@ -1,0 +1,766 @@
+// Sparse tile hierarchy on the GPU: compaction into sorted slots, neighbour
+// tables, per-cell classification (interfaces / BC / solid / bounce-back
+// masks), interface stencils, the bitmap passes of block maintenance, data
+// migration and new-cell initialisation.
+//
+// Reference seams: sparse_grid.py:183-200 (rebuild_level), 210-282 (rasters),
+// 304-363 (validation, dilation), 439-544 (interfaces); solver.py:159-273
+// (solid raster, _LevelTables); adapt.py:54-389 (GridAdaptor).
+//
+// Integer work only (except migration / init): every pass is a coalesced
+// sweep over a dense uint8 tile grid or over the stored cells, bit-exact with
+// the reference by construction (no floating point decides topology).
+#include <cub/cub.cuh>
+#include "common.cuh"
+
+namespace mlbm {
+
+MLBM_HD int64_t gidx3(const int* d, int x, int y, int z) {
+    return ((int64_t)x * d[1] + y) * d[2] + z;
+}
+MLBM_HD void gdec3(const int* d, int64_t g, int& x, int& y, int& z) {
+    z = (int)(g % d[2]);
+    g /= d[2];
+    y = (int)(g % d[1]);
+    x = (int)(g / d[1]);
+}
+struct I3 { int v[3]; };
+MLBM_HD I3 tdims_of(const mlbm_hier_t& h, int l) {
+    I3 r;
+    for (int a = 0; a < 3; ++a) r.v[a] = a < h.dim ? (h.finest[a] >> l) / 4 : 1;
+    return r;
+}
+MLBM_HD I3 cdims_of(const mlbm_hier_t& h, int l) {
+    I3 r;
+    for (int a = 0; a < 3; ++a) r.v[a] = a < h.dim ? (h.finest[a] >> l) : 1;
+    return r;
+}
+
+__device__ bool solid_at(const mlbm_solid_t& s, int dim, const int (&g)[3]) {
+    for (int b = 0; b < s.n_boxes; ++b) {
+        bool in = true;
+        for (int a = 0; a < dim; ++a)
+            in &= (double)g[a] >= s.boxes[b][a] && (double)g[a] < s.boxes[b][3 + a];
+        if (in) return true;
+    }
+    if (s.heightmap) {
+        int hx = g[0] < 0 ? 0 : (g[0] >= s.hm_dims[0] ? s.hm_dims[0] - 1 : g[0]);
+        float h;
+        if (dim == 2) h = s.heightmap[hx];
+        else {
+            int hz = g[2] < 0 ? 0 : (g[2] >= s.hm_dims[1] ? s.hm_dims[1] - 1 : g[2]);
+            h = s.heightmap[(int64_t)hx * s.hm_dims[1] + hz];
+        }
+        if (h > 0.f && (float)g[1] < h) return true;
+    }
+    return false;
+}
+
+// ---------------------------------------------------------------------------
+// compaction
+__global__ void k_kind_flags(int64_t n, const uint8_t* kind, int32_t* flags, int32_t* counts) {
+    int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g == 0) counts[1] = 0;
+    if (g < n) flags[g] = kind[g] != 0;
+}
+
+__global__ void k_scatter_tiles(int64_t n, I3 td, const uint8_t* kind, const int32_t* pos,
+                                const int32_t* old_map, int32_t* tile_map, int32_t* tile_xyz,
+                                uint8_t* tile_kind, int32_t* old_slot, int32_t* counts) {
+    int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const uint8_t k = kind[g];
+    if (k) {
+        const int slot = pos[g];
+        tile_map[g] = slot;
+        int x, y, z;
+        gdec3(td.v, g, x, y, z);
+        tile_xyz[slot * 3 + 0] = x;
+        tile_xyz[slot * 3 + 1] = y;
+        tile_xyz[slot * 3 + 2] = z;
+        tile_kind[slot] = k;
+        const int os = old_map ? old_map[g] : -1;
+        old_slot[slot] = os;
+        if (os < 0) atomicAdd(&counts[1], 1);
+    } else {
+        tile_map[g] = -1;
+    }
+    if (g == n - 1) counts[0] = pos[g] + (k != 0);
+}
+
+static int64_t align256(int64_t v) { return (v + 255) & ~(int64_t)255; }
+
+static int64_t cub_temp_bytes(int64_t n) {
+    size_t a = 0, b = 0;
+    int32_t* p = nullptr;
+    cub::DeviceScan::ExclusiveSum(nullptr, a, p, p, (int)n);
+    cub::CountingInputIterator<int32_t> it(0);
+    cub::DeviceSelect::Flagged(nullptr, b, it, (const int8_t*)nullptr, p, p, (int)n);
+    return align256((int64_t)(a > b ? a : b));
+}
+
+// ---------------------------------------------------------------------------
+// neighbours
+template <int D>
+__global__ void k_neighbors(mlbm_level_t lv, int32_t* nbr) {
+    constexpr int NB = Geo<D>::NB;
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= (int64_t)lv.n_tiles * NB) return;
+    const int t = (int)(j / NB), k = (int)(j % NB);
+    const int o[3] = {k % 3 - 1, (k / 3) % 3 - 1, D == 3 ? k / 9 - 1 : 0};
+    int c[3];
+    for (int a = 0; a < 3; ++a) {
+        c[a] = lv.tile_xyz[t * 3 + a] + o[a];
+        if (a >= D) continue;
+        if (lv.periodic[a]) c[a] = (c[a] + lv.tiles[a]) % lv.tiles[a];
+        else if (c[a] < 0 || c[a] >= lv.tiles[a]) { nbr[j] = -1; return; }
+    }
+    nbr[j] = lv.tile_map[gidx3(lv.tiles, c[0], c[1], c[2])];
+}
+
+// ---------------------------------------------------------------------------
+// owner level of a level-l cell position (finest leaf wins, corner sample)
+__device__ int owner_of(const mlbm_hier_t& h, int l, const int (&c)[3]) {
+    for (int lp = 0; lp < h.levels; ++lp) {
+        const I3 td = tdims_of(h, lp);
+        int p[3];
+        for (int a = 0; a < 3; ++a) {
+            if (a >= h.dim) { p[a] = 0; continue; }
+            const int s = lp >= l ? (c[a] >> (lp - l)) : (c[a] << (l - lp));
+            p[a] = s >> 2;
+        }
+        if (h.kind[lp][gidx3(td.v, p[0], p[1], p[2])] == 1) return lp;
+    }
+    return -1;
+}
+
+template <int D>
+__global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hier_t h, mlbm_bc_t bc,
+                                                     mlbm_solid_t solid, uint8_t* cell_flags,
+                                                     uint64_t* dir_masks, uint8_t* tile_flags,
+                                                     int32_t* counts, mlbm_error_t* err) {
+    constexpr int T = Geo<D>::T, NB = Geo<D>::NB, Q = Geo<D>::Q;
+    const int tile = blockIdx.x, lc = threadIdx.x;
+    const int level = lv.level;
+    __shared__ int snb[NB];
+    if (lc < NB) snb[lc] = lv.nbr[(int64_t)tile * NB + lc];
+    const int tx[3] = {lv.tile_xyz[tile * 3], lv.tile_xyz[tile * 3 + 1], lv.tile_xyz[tile * 3 + 2]};
+    const uint8_t tkind = h.kind[level][gidx3(lv.tiles, tx[0], tx[1], tx[2])];
+    const int l[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
+    int g[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) g[a] = tx[a] * 4 + l[a];
+    // rim: some in-domain neighbour tile is absent
+    bool gapnb = false;
+    if (lc < NB) {
+        const int o[3] = {lc % 3 - 1, (lc / 3) % 3 - 1, D == 3 ? lc / 9 - 1 : 0};
+        bool indom = true;
+        for (int a = 0; a < D; ++a) {
+            const int c = tx[a] + o[a];
+            if (!lv.periodic[a] && (c < 0 || c >= lv.tiles[a])) indom = false;
+        }
+        gapnb = indom && lv.nbr[(int64_t)tile * NB + lc] < 0;
+    }
+    const int rim = __syncthreads_or(gapnb);
+
+    int gf[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) gf[a] = g[a] << level;
+    const bool solid_c = solid_at(solid, D, gf);
+    bool bcl = false;
+    for (int f = 0; f < 2 * D; ++f) {
+        const int k = bc.face[f];
+        if (k != MLBM_FACE_OUTLET && k != MLBM_FACE_LOG_INLET) continue;
+        const int axis = f >> 1;
+        if (g[axis] == ((f & 1) ? lv.cells[axis] - 1 : 0)) bcl = true;
+    }
+    bool id = false, iu = false;
+    if (rim) {
+        for (int k = 0; k < NB; ++k) {
+            const int o[3] = {k % 3 - 1, (k / 3) % 3 - 1, D == 3 ? k / 9 - 1 : 0};
+            if (snb[k] >= 0) continue;
+            bool indom = true;
+            int nt[3];
+            for (int a = 0; a < 3; ++a) {
+                nt[a] = tx[a] + o[a];
+                if (a >= D) continue;
+                if (lv.periodic[a]) nt[a] = (nt[a] + lv.tiles[a]) % lv.tiles[a];
+                else if (nt[a] < 0 || nt[a] >= lv.tiles[a]) indom = false;
+            }
+            if (!indom) continue;
+            // cells of that tile within Chebyshev 2 of g (unwrapped displacement)
+            int lo[3], hi[3];
+            for (int a = 0; a < 3; ++a) {
+                if (a >= D) { lo[a] = hi[a] = 0; continue; }
+                const int base = (tx[a] + o[a]) * 4;     // unwrapped origin
+                lo[a] = max(0, g[a] - 2 - base);
+                hi[a] = min(3, g[a] + 2 - base);
+            }
+            for (int mz = lo[2]; mz <= hi[2]; ++mz)
+                for (int my = lo[1]; my <= hi[1]; ++my)
+                    for (int mx = lo[0]; mx <= hi[0]; ++mx) {
+                        const int m[3] = {mx, my, mz};
+                        int cc[3] = {0, 0, 0};
+                        int dist = 0;
+                        for (int a = 0; a < D; ++a) {
+                            const int uc = (tx[a] + o[a]) * 4 + m[a];
+                            dist = max(dist, abs(uc - g[a]));
+                            cc[a] = nt[a] * 4 + m[a];
+                        }
+                        const int own = owner_of(h, level, cc);
+                        if (own > level && dist <= 2) id = true;
+                        if (own >= 0 && own < level && dist <= 1) iu = true;
+                    }
+        }
+        if (id && iu) report_error(err, MLBM_ERR_TOPOLOGY, level, g[0], g[1], g[2], 1);
+        if (id && level == h.levels - 1) report_error(err, MLBM_ERR_TOPOLOGY, level, g[0], g[1], g[2], 2);
+        if (iu && level == 0) report_error(err, MLBM_ERR_TOPOLOGY, level, g[0], g[1], g[2], 3);
+    }
+    const bool active = !(id || iu || bcl || solid_c);
+    uint64_t mask = 0;
+    for (int i = 1; i < Q; ++i) {
+        int s[3];
+        bool oob = false, bb = false;
+        for (int a = 0; a < 3; ++a) {
+            const int ci = cvec<D>(i, a);
+            s[a] = g[a] - ci;
+            if (a >= D) continue;
+            if (lv.periodic[a]) s[a] = (s[a] + lv.cells[a]) % lv.cells[a];
+            else if (s[a] < 0) { oob = true; if (bc.face[2 * a] == MLBM_FACE_WALL) bb = true; }
+            else if (s[a] >= lv.cells[a]) { oob = true; if (bc.face[2 * a + 1] == MLBM_FACE_WALL) bb = true; }
+        }
+        bool stored = false;
+        if (!oob) {
+            int sf[3] = {0, 0, 0};
+            for (int a = 0; a < D; ++a) sf[a] = s[a] << level;
+            if (solid_at(solid, D, sf)) bb = true;
+            stored = lv.tile_map[gidx3(lv.tiles, s[0] >> 2, s[1] >> 2, D == 3 ? s[2] >> 2 : 0)] >= 0;
+        }
+        if (bb) mask |= 1ull << i;
+        else if (oob || !stored) {
+            mask |= 1ull << (32 + i);
+            if (active) report_error(err, MLBM_ERR_TOPOLOGY, level, g[0], g[1], g[2], 4);
+        }
+    }
+    uint8_t f = 0;
+    if (active) f |= MLBM_CF_ACTIVE;
+    if (solid_c) f |= MLBM_CF_SOLID;
+    if (id) f |= MLBM_CF_GHOST_D;
+    if (iu) f |= MLBM_CF_GHOST_U;
+    if (bcl) f |= MLBM_CF_BC;
+    if (mask) f |= MLBM_CF_SPECIAL;
+    if (tkind == 1) f |= MLBM_CF_LEAF;
+    const int64_t cell = (int64_t)tile * T + lc;
+    cell_flags[cell] = f;
+    dir_masks[cell] = mask;
+    if (id) atomicAdd(&counts[0], 1);
+    if (iu) atomicAdd(&counts[1], 1);
+    const int plain = __syncthreads_and(active && mask == 0);
+    const int anybc = __syncthreads_or(bcl);
+    if (lc == 0)
+        tile_flags[tile] = (plain ? MLBM_TF_PLAIN : 0) | (anybc ? MLBM_TF_BC : 0) |
+                           (tkind == 1 ? MLBM_TF_LEAF : 0);
+}
+
+// ---------------------------------------------------------------------------
+// interfaces
+__global__ void k_iface_flags(int64_t n, const uint8_t* cf, uint8_t bit, int8_t* out) {
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c < n) out[c] = (cf[c] & bit) ? 1 : 0;
+}
+
+template <int D>
+__global__ void k_iface_stencil(mlbm_level_t lv, mlbm_level_t other, int which, const int32_t* counts,
+                                const int32_t* targets, int32_t* src, mlbm_error_t* err) {
+    constexpr int T = Geo<D>::T, NC = Geo<D>::NC;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= counts[0]) return;
+    const int c = targets[j];
+    const int slot = c / T, lc = c % T;
+    const int l[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
+    int g[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) g[a] = lv.tile_xyz[slot * 3 + a] * 4 + l[a];
+    for (int k = 0; k < NC; ++k) {
+        int cc[3] = {0, 0, 0};
+        bool wpos = true;
+        for (int a = 0; a < D; ++a) {
+            const int o = (k >> a) & 1;
+            int v;
+            if (which == 0) {
+                v = (g[a] >> 1) + o;
+                if (o == 1 && !(g[a] & 1)) wpos = false;
+            } else {
+                v = g[a] * 2 + o;
+            }
+            const int dimc = other.cells[a];
+            if (other.periodic[a]) v = (v % dimc + dimc) % dimc;
+            else v = v < 0 ? 0 : (v >= dimc ? dimc - 1 : v);
+            cc[a] = v;
+        }
+        const int s = other.tile_map[gidx3(other.tiles, cc[0] >> 2, cc[1] >> 2, D == 3 ? cc[2] >> 2 : 0)];
+        int idx = -1;
+        if (s >= 0) idx = s * T + local_of<D>(cc[0] & 3, cc[1] & 3, cc[2] & 3);
+        else if ((which == 0 && wpos) || which == 1)
+            report_error(err, MLBM_ERR_TOPOLOGY, lv.level, g[0], g[1], g[2], which == 0 ? 5 : 6);
+        src[(int64_t)j * NC + k] = idx;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// block maintenance bitmaps
+template <typename R>
+__global__ void k_seed(int dim, int n, const R* x, int64_t xs, I3 t0, uint8_t* seeds, mlbm_error_t* err) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int t[3] = {0, 0, 0};
+    bool bad = false;
+    for (int a = 0; a < dim; ++a) {
+        const double v = (double)x[a * xs + p];
+        const int64_t c = (int64_t)floor(v);
+        const int64_t tt = c >= 0 ? c / 4 : -((-c + 3) / 4);
+        if (tt < 0 || tt >= t0.v[a] || !(v == v)) bad = true;
+        t[a] = (int)tt;
+    }
+    if (bad) { report_error(err, MLBM_ERR_DOMAIN, 0, t[0], t[1], t[2]); return; }
+    seeds[gidx3(t0.v, t[0], t[1], t[2])] = 1;
+}
+
+__global__ void k_bitmap_op(int op, int dim, I3 d, const uint8_t* in, uint8_t* out) {
+    // grid over the output (parents: parent grid; else same grid)
+    I3 od = d;
+    if (op == 1) for (int a = 0; a < dim; ++a) od.v[a] = d.v[a] / 2;
+    const int64_t n = (int64_t)od.v[0] * od.v[1] * od.v[2];
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    int x[3];
+    gdec3(od.v, g, x[0], x[1], x[2]);
+    switch (op) {
+    case 0:
+    case 1: {
+        int b[3];
+        for (int a = 0; a < 3; ++a) b[a] = a < dim ? (op == 0 ? (x[a] & ~1) : 2 * x[a]) : x[a];
+        uint8_t any = 0;
+        for (int k = 0; k < (1 << dim); ++k) {
+            int c[3] = {b[0] + (k & 1), b[1] + ((k >> 1) & 1), dim == 3 ? b[2] + ((k >> 2) & 1) : b[2]};
+            any |= in[gidx3(d.v, c[0], c[1], c[2])] ? 1 : 0;
+        }
+        out[g] = any;
+        break;
+    }
+    case 2: out[g] = (out[g] | (in[g] ? 1 : 0)); break;
+    case 3: out[g] = (out[g] && !in[g]) ? 1 : 0; break;
+    case 4: out[g] = in[g] ? 1 : 0; break;
+    case 5: out[g] = 1; break;
+    case 6: out[g] = in[g] == 1 ? 1 : 0; break;
+    case 7: out[g] = in[g] != 0 ? 1 : 0; break;
+    }
+}
+
+__global__ void k_dilate_axis(I3 d, int axis, int periodic, int r, const uint8_t* in, uint8_t* out) {
+    const int64_t n = (int64_t)d.v[0] * d.v[1] * d.v[2];
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    int x[3];
+    gdec3(d.v, g, x[0], x[1], x[2]);
+    const int N = d.v[axis];
+    uint8_t any = 0;
+    for (int k = -r; k <= r && !any; ++k) {
+        int c = x[axis] + k;
+        if (periodic) c = ((c % N) + N) % N;
+        else if (c < 0 || c >= N) continue;
+        int y[3] = {x[0], x[1], x[2]};
+        y[axis] = c;
+        any = in[gidx3(d.v, y[0], y[1], y[2])] ? 1 : 0;
+    }
+    out[g] = any;
+}
+
+// one thread per sibling group (grouped) or per tile (top level)
+__global__ void k_effective(int dim, I3 d, int grouped, const uint8_t* des, const uint8_t* cur,
+                            const uint8_t* guard, const uint8_t* par_prev, int16_t* streak,
+                            uint8_t* eff) {
+    I3 gd = d;
+    if (grouped) for (int a = 0; a < dim; ++a) gd.v[a] = d.v[a] / 2;
+    const int64_t n = (int64_t)gd.v[0] * gd.v[1] * gd.v[2];
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int x[3];
+    gdec3(gd.v, j, x[0], x[1], x[2]);
+    const int K = grouped ? (1 << dim) : 1;
+    int64_t gi[8];
+    bool cand[8], avail[8];
+    bool all = true;
+    for (int k = 0; k < K; ++k) {
+        int c[3];
+        for (int a = 0; a < 3; ++a) c[a] = (grouped && a < dim) ? 2 * x[a] + ((k >> a) & 1) : x[a];
+        const int64_t g = gidx3(d.v, c[0], c[1], c[2]);
+        gi[k] = g;
+        cand[k] = cur[g] && !des[g];
+        const int16_t s = cand[k] ? (int16_t)(streak[g] + 1) : (int16_t)0;
+        streak[g] = s;
+        avail[k] = cand[k] && s >= 2 && !(guard && guard[g]);
+        all &= avail[k];
+    }
+    for (int k = 0; k < K; ++k) {
+        const int64_t g = gi[k];
+        const bool act = grouped ? (avail[k] && all) : false;
+        eff[g] = (des[g] || (cur[g] && !act) || (par_prev && par_prev[g])) ? 1 : 0;
+    }
+}
+
+__global__ void k_plan(int64_t n, const uint8_t* own, const uint8_t* storage, const uint8_t* old_kind,
+                       uint8_t* new_kind, int32_t* changed) {
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const uint8_t k = own[g] ? 1 : (storage[g] ? 2 : 0);
+    new_kind[g] = k;
+    if (k != old_kind[g]) atomicOr(changed, 1);
+}
+
+__global__ void k_coverage(mlbm_hier_t h, int32_t* viol) {
+    const I3 t0 = tdims_of(h, 0);
+    const int64_t n = (int64_t)t0.v[0] * t0.v[1] * t0.v[2];
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    int x[3];
+    gdec3(t0.v, g, x[0], x[1], x[2]);
+    int cnt = 0;
+    for (int l = 0; l < h.levels; ++l) {
+        const I3 td = tdims_of(h, l);
+        int c[3];
+        for (int a = 0; a < 3; ++a) c[a] = a < h.dim ? x[a] >> l : 0;
+        cnt += h.kind[l][gidx3(td.v, c[0], c[1], c[2])] == 1;
+    }
+    if (cnt != 1) atomicAdd(&viol[0], 1);
+}
+
+__global__ void k_ring_viol(int64_t n, const uint8_t* dil, const uint8_t* kind, int32_t* viol) {
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g < n && dil[g] && kind[g] == 0) atomicAdd(&viol[1], 1);
+}
+
+template <typename R>
+__global__ void k_particle_leaf(int dim, int n, const R* x, int64_t xs, I3 t0, const uint8_t* kind0,
+                                int32_t* viol) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int t[3] = {0, 0, 0};
+    for (int a = 0; a < dim; ++a) {
+        const int64_t c = (int64_t)floor((double)x[a * xs + p]);
+        t[a] = (int)(c >= 0 ? c / 4 : -((-c + 3) / 4));
+        if (t[a] < 0 || t[a] >= t0.v[a]) { atomicAdd(&viol[2], 1); return; }
+    }
+    if (kind0[gidx3(t0.v, t[0], t[1], t[2])] != 1) atomicAdd(&viol[2], 1);
+}
+
+// ---------------------------------------------------------------------------
+// migration + new-cell init (adapt.py:259-372)
+template <int D, typename R>
+__global__ void k_migrate(int64_t ncells, const int32_t* old_slot, FieldsT<R> o0, FieldsT<R> o1,
+                          FieldsT<R> n0, FieldsT<R> n1) {
+    constexpr int T = Geo<D>::T, NF = Geo<D>::NF;
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= ncells) return;
+    const int os = old_slot[c / T];
+    const int64_t oc = (int64_t)os * T + c % T;
+#pragma unroll
+    for (int k = 0; k < NF; ++k) {
+        const R def = k == fi_eps<D>() ? R(1) : R(0);
+        n0.at(k, c) = os >= 0 ? o0.at(k, oc) : def;
+        n1.at(k, c) = os >= 0 ? o1.at(k, oc) : def;
+    }
+}
+
+MLBM_HD double kap_down(double tf, double tc, int conv) { return conv == 0 ? tf / (2.0 * tc) : 2.0 * tc / tf; }
+MLBM_HD double kap_up(double tf, double tc, int conv) { return conv == 0 ? 2.0 * tc / tf : tc / (2.0 * tf); }
+
+template <int D, typename R>
+__global__ void k_init_new(mlbm_hier_t oh, mlbm_hier_t nh, int level, const int32_t* tile_xyz,
+                           const int32_t* old_slot, int n_tiles, FieldsT<R> n0, FieldsT<R> n1,
+                           const double* taus, int conv, int32_t* viol) {
+    constexpr int T = Geo<D>::T, NC = Geo<D>::NC, NS = Geo<D>::NS, NM = Geo<D>::NM;
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= (int64_t)n_tiles * T) return;
+    const int slot = (int)(c / T), lc = (int)(c % T);
+    if (old_slot[slot] >= 0) return;
+    const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
+    int g[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) g[a] = tile_xyz[slot * 3 + a] * 4 + l3[a];
+    const FieldsT<R> dstt[2] = {n0, n1};
+    // coarser: nearest level with a complete stencil
+    for (int sl = level + 1; sl < oh.levels; ++sl) {
+        if (oh.n_tiles[sl] == 0) continue;
+        const int r = sl - level;
+        const I3 cd = cdims_of(oh, sl), td = tdims_of(oh, sl);
+        int idx[NC];
+        R w[NC];
+        bool ok = true;
+        for (int k = 0; k < NC; ++k) {
+            int cc[3] = {0, 0, 0};
+            double wk = 1.0;
+            for (int a = 0; a < D; ++a) {
+                const int o = (k >> a) & 1;
+                const double fr = (double)(g[a] & ((1 << r) - 1)) / (double)(1 << r);
+                int v = (g[a] >> r) + o;
+                if (oh.periodic[a]) v = ((v % cd.v[a]) + cd.v[a]) % cd.v[a];
+                else v = v < 0 ? 0 : (v >= cd.v[a] ? cd.v[a] - 1 : v);
+                cc[a] = v;
+                wk *= o ? fr : 1.0 - fr;
+            }
+            const int s = oh.tile_map[sl][gidx3(td.v, cc[0] >> 2, cc[1] >> 2, D == 3 ? cc[2] >> 2 : 0)];
+            idx[k] = s >= 0 ? s * T + local_of<D>(cc[0] & 3, cc[1] & 3, cc[2] & 3) : 0;
+            w[k] = R(wk);
+            if (wk > 0.0 && s < 0) ok = false;
+        }
+        if (!ok) continue;
+        for (int t = 0; t < 2; ++t) {
+            const FieldsT<R> src{(R*)oh.fields[t][sl], oh.stride[sl]};
+            R v[NM + 2];
+            for (int q = 0; q < NM + 2; ++q) {
+                const int fk = q < NM ? q : (q == NM ? fi_eps<D>() : fi_phi<D>());
+                R acc = R(0);
+                for (int k = 0; k < NC; ++k) acc += src.at(fk, idx[k]) * w[k];
+                v[q] = acc;
+            }
+            for (int lvl = sl; lvl > level; --lvl) {
+                const R kap = R(kap_down(taus[lvl - 1], taus[lvl], conv));
+                for (int k = 0; k < NS; ++k) {
+                    const R eq = v[1 + s_a<D>(k)] * v[1 + s_b<D>(k)];
+                    v[1 + D + k] = kap * (v[1 + D + k] - eq) + eq;
+                }
+            }
+            for (int q = 0; q < NM + 2; ++q) {
+                const int fk = q < NM ? q : (q == NM ? fi_eps<D>() : fi_phi<D>());
+                dstt[t].at(fk, c) = v[q];
+            }
+        }
+        return;
+    }
+    // finer: coincident cell of the nearest old finer level
+    for (int sl = level - 1; sl >= 0; --sl) {
+        if (oh.n_tiles[sl] == 0) continue;
+        const int sh = level - sl;
+        const I3 td = tdims_of(oh, sl);
+        int cc[3] = {0, 0, 0};
+        for (int a = 0; a < D; ++a) cc[a] = g[a] << sh;
+        const int s = oh.tile_map[sl][gidx3(td.v, cc[0] >> 2, cc[1] >> 2, D == 3 ? cc[2] >> 2 : 0)];
+        if (s < 0) continue;
+        const int64_t si = (int64_t)s * T + local_of<D>(cc[0] & 3, cc[1] & 3, cc[2] & 3);
+        for (int t = 0; t < 2; ++t) {
+            const FieldsT<R> src{(R*)oh.fields[t][sl], oh.stride[sl]};
+            R v[NM + 2];
+            for (int q = 0; q < NM + 2; ++q) {
+                const int fk = q < NM ? q : (q == NM ? fi_eps<D>() : fi_phi<D>());
+                v[q] = src.at(fk, si);
+            }
+            for (int lvl = sl; lvl < level; ++lvl) {
+                const R kap = R(kap_up(taus[lvl], taus[lvl + 1], conv));
+                for (int k = 0; k < NS; ++k) {
+                    const R eq = v[1 + s_a<D>(k)] * v[1 + s_b<D>(k)];
+                    v[1 + D + k] = kap * (v[1 + D + k] - eq) + eq;
+                }
+            }
+            for (int q = 0; q < NM + 2; ++q) {
+                const int fk = q < NM ? q : (q == NM ? fi_eps<D>() : fi_phi<D>());
+                dstt[t].at(fk, c) = v[q];
+            }
+        }
+        return;
+    }
+    atomicAdd(viol, 1);
+}
+
+}  // namespace mlbm
+
+using namespace mlbm;
+
+static inline int blocks_for(int64_t n, int b) { return (int)((n + b - 1) / b); }
+
+extern "C" int64_t mlbm_ws_bytes(int64_t n) {
+    if (n < 1) n = 1;
+    return align256(4 * n) * 2 + cub_temp_bytes(n) + 256;
+}
+
+extern "C" int mlbm_compact_tiles(int32_t dim, const int32_t tiles[3], const uint8_t* kind,
+                                  const int32_t* old_map, int32_t* tile_map, int32_t* tile_xyz,
+                                  uint8_t* tile_kind, int32_t* old_slot, int32_t* counts,
+                                  void* ws, int64_t ws_bytes, void* stream) {
+    (void)dim;
+    const int64_t n = (int64_t)tiles[0] * tiles[1] * tiles[2];
+    if (n <= 0 || ws_bytes < mlbm_ws_bytes(n)) return -1;
+    cudaStream_t s = as_stream(stream);
+    char* w = (char*)ws;
+    int32_t* flags = (int32_t*)w;
+    int32_t* pos = (int32_t*)(w + align256(4 * n));
+    void* tmp = w + 2 * align256(4 * n);
+    size_t tmpb = (size_t)cub_temp_bytes(n);
+    k_kind_flags<<<blocks_for(n, 256), 256, 0, s>>>(n, kind, flags, counts);
+    cub::DeviceScan::ExclusiveSum(tmp, tmpb, flags, pos, (int)n, s);
+    I3 td{{tiles[0], tiles[1], tiles[2]}};
+    k_scatter_tiles<<<blocks_for(n, 256), 256, 0, s>>>(n, td, kind, pos, old_map, tile_map, tile_xyz,
+                                                       tile_kind, old_slot, counts);
+    return launch_status();
+}
+
+extern "C" int mlbm_build_neighbors(const mlbm_level_t* lv, int32_t* nbr, void* stream) {
+    const int NB = lv->dim == 2 ? 9 : 27;
+    const int64_t n = (int64_t)lv->n_tiles * NB;
+    if (n == 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    if (lv->dim == 2) k_neighbors<2><<<blocks_for(n, 256), 256, 0, s>>>(*lv, nbr);
+    else k_neighbors<3><<<blocks_for(n, 256), 256, 0, s>>>(*lv, nbr);
+    return launch_status();
+}
+
+extern "C" int mlbm_classify_level(const mlbm_level_t* lv, const mlbm_hier_t* h, const mlbm_bc_t* bc,
+                                   const mlbm_solid_t* solid, uint8_t* cell_flags, uint64_t* dir_masks,
+                                   uint8_t* tile_flags, int32_t* counts, mlbm_error_t* err,
+                                   void* stream) {
+    if (lv->n_tiles == 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    if (lv->dim == 2)
+        k_classify<2><<<lv->n_tiles, 16, 0, s>>>(*lv, *h, *bc, *solid, cell_flags, dir_masks,
+                                                 tile_flags, counts, err);
+    else
+        k_classify<3><<<lv->n_tiles, 64, 0, s>>>(*lv, *h, *bc, *solid, cell_flags, dir_masks,
+                                                 tile_flags, counts, err);
+    return launch_status();
+}
+
+extern "C" int mlbm_build_interface(const mlbm_level_t* lv, const mlbm_level_t* other, int32_t which,
+                                    int32_t* targets, int32_t* src, int32_t* counts,
+                                    mlbm_error_t* err, void* ws, int64_t ws_bytes, void* stream) {
+    const int T = lv->dim == 2 ? 16 : 64;
+    const int64_t n = (int64_t)lv->n_tiles * T;
+    if (n == 0) return 0;
+    if (ws_bytes < mlbm_ws_bytes(n)) return -1;
+    cudaStream_t s = as_stream(stream);
+    char* w = (char*)ws;
+    int8_t* fl = (int8_t*)w;
+    void* tmp = w + 2 * align256(4 * n);
+    size_t tmpb = (size_t)cub_temp_bytes(n);
+    k_iface_flags<<<blocks_for(n, 256), 256, 0, s>>>(n, lv->cell_flags,
+                                                     which == 0 ? MLBM_CF_GHOST_D : MLBM_CF_GHOST_U, fl);
+    cub::CountingInputIterator<int32_t> it(0);
+    cub::DeviceSelect::Flagged(tmp, tmpb, it, fl, targets, counts, (int)n, s);
+    if (lv->dim == 2)
+        k_iface_stencil<2><<<blocks_for(n, 128), 128, 0, s>>>(*lv, *other, which, counts, targets, src, err);
+    else
+        k_iface_stencil<3><<<blocks_for(n, 128), 128, 0, s>>>(*lv, *other, which, counts, targets, src, err);
+    return launch_status();
+}
+
+extern "C" int mlbm_seed_tiles(int32_t dim, int32_t n, const void* x, int64_t xstride, int32_t dtype,
+                               const int32_t tiles0[3], uint8_t* seeds, mlbm_error_t* err,
+                               void* stream) {
+    if (n <= 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    I3 t0{{tiles0[0], tiles0[1], tiles0[2]}};
+    if (dtype) k_seed<double><<<blocks_for(n, 256), 256, 0, s>>>(dim, n, (const double*)x, xstride, t0, seeds, err);
+    else k_seed<float><<<blocks_for(n, 256), 256, 0, s>>>(dim, n, (const float*)x, xstride, t0, seeds, err);
+    return launch_status();
+}
+
+extern "C" int mlbm_bitmap_op(int32_t op, int32_t dim, const int32_t dims[3], const uint8_t* in,
+                              uint8_t* out, void* stream) {
+    I3 d{{dims[0], dims[1], dims[2]}};
+    int64_t n = (int64_t)dims[0] * dims[1] * dims[2];
+    if (op == 1) { n = 1; for (int a = 0; a < 3; ++a) n *= a < dim ? dims[a] / 2 : dims[a]; }
+    if (n <= 0) return 0;
+    k_bitmap_op<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(op, dim, d, in, out);
+    return launch_status();
+}
+
+extern "C" int mlbm_dilate(int32_t dim, const int32_t dims[3], const int32_t periodic[3], int32_t r,
+                           const uint8_t* in, uint8_t* out, uint8_t* tmp, void* stream) {
+    I3 d{{dims[0], dims[1], dims[2]}};
+    const int64_t n = (int64_t)dims[0] * dims[1] * dims[2];
+    if (n <= 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    const int B = blocks_for(n, 256);
+    if (dim == 2) {
+        k_dilate_axis<<<B, 256, 0, s>>>(d, 0, periodic[0], r, in, tmp);
+        k_dilate_axis<<<B, 256, 0, s>>>(d, 1, periodic[1], r, tmp, out);
+    } else {
+        k_dilate_axis<<<B, 256, 0, s>>>(d, 0, periodic[0], r, in, out);
+        k_dilate_axis<<<B, 256, 0, s>>>(d, 1, periodic[1], r, out, tmp);
+        k_dilate_axis<<<B, 256, 0, s>>>(d, 2, periodic[2], r, tmp, out);
+    }
+    return launch_status();
+}
+
+extern "C" int mlbm_effective_level(int32_t dim, const int32_t dims[3], const uint8_t* des,
+                                    const uint8_t* cur, const uint8_t* guard, const uint8_t* par_prev,
+                                    int16_t* streak, uint8_t* eff, void* stream) {
+    I3 d{{dims[0], dims[1], dims[2]}};
+    bool grouped = true;
+    for (int a = 0; a < dim; ++a) grouped &= (dims[a] % 2) == 0;
+    int64_t n = 1;
+    for (int a = 0; a < 3; ++a) n *= (grouped && a < dim) ? dims[a] / 2 : dims[a];
+    if (n <= 0) return 0;
+    k_effective<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(dim, d, grouped ? 1 : 0, des, cur, guard,
+                                                                  par_prev, streak, eff);
+    return launch_status();
+}
+
+extern "C" int mlbm_plan_level(int32_t n, const uint8_t* own, const uint8_t* storage,
+                               const uint8_t* old_kind, uint8_t* new_kind, int32_t* changed,
+                               void* stream) {
+    if (n <= 0) return 0;
+    k_plan<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(n, own, storage, old_kind, new_kind, changed);
+    return launch_status();
+}
+
+extern "C" int mlbm_check_coverage(const mlbm_hier_t* h, int32_t* viol, void* stream) {
+    const I3 t0 = tdims_of(*h, 0);
+    const int64_t n = (int64_t)t0.v[0] * t0.v[1] * t0.v[2];
+    k_coverage<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(*h, viol);
+    return launch_status();
+}
+
+extern "C" int mlbm_count_ring_violations(int64_t n, const uint8_t* dil, const uint8_t* kind,
+                                          int32_t* viol, void* stream) {
+    if (n <= 0) return 0;
+    k_ring_viol<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(n, dil, kind, viol);
+    return launch_status();
+}
+
+extern "C" int mlbm_check_particles(int32_t dim, int32_t n, const void* x, int64_t xstride, int32_t dtype,
+                                    const int32_t tiles0[3], const uint8_t* kind0, int32_t* viol,
+                                    void* stream) {
+    if (n <= 0) return 0;
+    I3 t0{{tiles0[0], tiles0[1], tiles0[2]}};
+    cudaStream_t s = as_stream(stream);
+    if (dtype) k_particle_leaf<double><<<blocks_for(n, 256), 256, 0, s>>>(dim, n, (const double*)x, xstride, t0, kind0, viol);
+    else k_particle_leaf<float><<<blocks_for(n, 256), 256, 0, s>>>(dim, n, (const float*)x, xstride, t0, kind0, viol);
+    return launch_status();
+}
+
+extern "C" int mlbm_migrate_level(int32_t dim, int32_t n_new_tiles, const int32_t* old_slot,
+                                  mlbm_fields_t old0, mlbm_fields_t old1, mlbm_fields_t new0,
+                                  mlbm_fields_t new1, int32_t dtype, void* stream) {
+    const int T = dim == 2 ? 16 : 64;
+    const int64_t n = (int64_t)n_new_tiles * T;
+    if (n == 0) return 0;
+    cudaStream_t s = as_stream(stream);
+#define MIG(D, R) k_migrate<D, R><<<blocks_for(n, 256), 256, 0, s>>>(n, old_slot, fields_of<R>(old0), \
+        fields_of<R>(old1), fields_of<R>(new0), fields_of<R>(new1))
+    if (dim == 2) { if (dtype) MIG(2, double); else MIG(2, float); }
+    else { if (dtype) MIG(3, double); else MIG(3, float); }
+#undef MIG
+    return launch_status();
+}
+
+extern "C" int mlbm_init_new_cells(const mlbm_hier_t* old_h, const mlbm_hier_t* nh, int32_t level,
+                                   const int32_t* tile_xyz, const int32_t* old_slot, int32_t n_tiles,
+                                   mlbm_fields_t new0, mlbm_fields_t new1, const double* taus,
+                                   int32_t conv, int32_t dtype, int32_t* viol, void* stream) {
+    const int T = old_h->dim == 2 ? 16 : 64;
+    const int64_t n = (int64_t)n_tiles * T;
+    if (n == 0) return 0;
+    cudaStream_t s = as_stream(stream);
+#define INI(D, R) k_init_new<D, R><<<blocks_for(n, 128), 128, 0, s>>>(*old_h, *nh, level, tile_xyz, old_slot, \
+        n_tiles, fields_of<R>(new0), fields_of<R>(new1), taus, conv, viol)
+    if (old_h->dim == 2) { if (dtype) INI(2, double); else INI(2, float); }
+    else { if (dtype) INI(3, double); else INI(3, float); }
+#undef INI
+    return launch_status();
+}
