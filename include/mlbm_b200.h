@@ -248,7 +248,8 @@ int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, void* p, int64
 
 /* per level-0 cell: eps, Di Felice drag + limiter, grad eps, mixture force
  * (written into both trees), MPM grid update with wall / sticky projection
- * (coupling.py:134-197, 379-446; granular.py:313-341). */
+ * (coupling.py:134-197, 379-446; granular.py:313-341).  mode 1: full exchange;
+ * mode 0: grid update only, with the drag already in the FS rows. */
 int mlbm_exchange(const mlbm_level_t* lv0, mlbm_fields_t w_tree, mlbm_fields_t r_tree,
                   mlbm_fields_t tree0, mlbm_fields_t tree1, void* ras, int64_t rs,
                   double eps_min, double nu, double d_p, double re_min, double dt,
@@ -257,7 +258,8 @@ int mlbm_exchange(const mlbm_level_t* lv0, mlbm_fields_t w_tree, mlbm_fields_t r
                   int32_t dtype, void* stream);
 
 /* gather, advect (wrap / clamp to [2, dim-2]), F update, SVD + Drucker-Prager
- * (granular.py:344-412). clamped += number of clamped coordinates. */
+ * (granular.py:344-412). clamped[0] += clamped coordinates; clamped[1] |= CFL
+ * violation (max |v| dt >= 0.5, granular.py:428-432). */
 int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, double* x, void* p, int64_t ps,
              double lam, double mu, double alpha, const void* ras, int64_t rs, double dt,
              int32_t plastic, int32_t dtype, int32_t* clamped, mlbm_error_t* err,

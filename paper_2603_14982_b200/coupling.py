@@ -1,0 +1,313 @@
+"""Two-way fluid-sediment coupling and the coupled step on the B200
+(drop-in for ``pkg/src/mlbm/coupling.py``).
+
+One finest cycle (CoupledSim.step, coupling.py:448-481) issues:
+
+  coarser levels (Alg. 1 prelude)          mlbm_downward / mlbm_level_step / mlbm_upward
+  level-0 stream (bare moments)            mlbm_level_step(mode=1)
+  exchange: P2G + fractions               mlbm_p2g            coupling.py:96-131, granular.py:282-310
+            eps, drag, limiter, grad eps,
+            mixture force -> both trees,
+            MPM grid update               mlbm_exchange       coupling.py:134-197, 379-446
+            G2P + plasticity              mlbm_g2p            granular.py:344-412
+  level-0 collide + boundaries             mlbm_level_step(mode=2, force/tau from fields)
+  powder transport (+ entrainment)         mlbm_stress_raster, mlbm_powder
+  block maintenance                        GridAdaptor.update (adapt.py)
+  diagnostics                              mlbm_diag_level / mlbm_diag_particles
+
+Diagnostics rows accumulate on the device and are materialised lazily.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .adapt import GridAdaptor, RefineDriver
+from .granular import MpmGrid, Particles, SandMaterial, _d3, _faces
+from .solver import FIELD_FORCE, FIELD_TAU, MultiLevelSolver
+from .sparse_grid import dtype_code
+
+
+@dataclass
+class UnitScale:
+    """coupling.py:26-56."""
+    dx: float = 1.0
+    dt: float = 1.0
+    rho: float = 1.0
+
+    def __post_init__(self):
+        if self.dx <= 0 or self.dt <= 0 or self.rho <= 0:
+            raise ValueError("unit scales must be positive")
+
+    @property
+    def C(self) -> float:
+        return self.rho * self.dx / self.dt ** 2
+
+    def velocity_to_lattice(self, v):
+        return v * self.dt / self.dx
+
+    def accel_to_lattice(self, a):
+        return a * self.dt ** 2 / self.dx
+
+    def force_density_to_lattice(self, f):
+        return f / self.C
+
+    def stress_to_lattice(self, s):
+        return s / (self.rho * (self.dx / self.dt) ** 2)
+
+    def time_to_lattice(self, t):
+        return t / self.dt
+
+
+@dataclass
+class DragParams:
+    d_p: float | None = None
+    re_min: float = 0.01
+
+
+@dataclass
+class PowderParams:
+    entrain: float = 0.0
+    diffusion: float = 0.05
+    sign: float = 1.0
+    eta_surface: float = 0.6
+
+    def check_stability(self, dt: float = 1.0):
+        if self.sign > 0 and self.diffusion * dt > 0.25:
+            raise ValueError(f"diffusion number D*dt={self.diffusion * dt} exceeds 0.25")
+
+
+@dataclass
+class DiagRow:
+    step: int
+    t_phys: float
+    fluid_mom: tuple
+    sediment_mom: tuple
+    drag_impulse: tuple
+    sum_phi: float
+    tiles: tuple
+    eps_min: float
+
+
+def particle_diameter(V0, d):
+    if d == 2:
+        return 2.0 * np.sqrt(V0 / np.pi)
+    return 2.0 * (3.0 * V0 / (4.0 * np.pi)) ** (1.0 / 3.0)
+
+
+class CouplingFields:
+    """Device views of the last exchange (coupling.py:80-93)."""
+
+    def __init__(self, grid: MpmGrid, tree_level0):
+        d = grid.d
+        self.d = d
+        r = grid.ras
+        R = grid.R
+        self.eps = r[R["eps"]]
+        self.eta = r[R["eta"]]
+        self.v = r[R["vmom"]:R["vmom"] + d].t()
+        self.area = r[R["area"]]
+        self.mass = r[R["mass"]]
+        self.fs = r[R["fs"]:R["fs"] + d].t()
+        self.grad_term = r[R["grad"]:R["grad"] + d].t()
+        self.rel = r[R["rel"]:R["rel"] + d].t()
+        base = tree_level0.index["f" + "x"]
+        self.force = tree_level0.data[base:base + d].t()
+
+
+class CoupledSim:
+    """Owns the solver, the granular phase and the exchange (coupling.py:337-538)."""
+
+    def __init__(self, solver: MultiLevelSolver, particles: Particles | None,
+                 material: SandMaterial | None = None, sediment_gravity=None,
+                 drag: DragParams | None = None, powder: PowderParams | None = None,
+                 adaptor: GridAdaptor | None = None, static_tiles=None,
+                 unit_scale: UnitScale | None = None):
+        self.solver = solver
+        self.topology = solver.topology
+        self.d = self.topology.d
+        self.pair = solver.pair
+        self.dtype = solver.dtype
+        self.particles = particles if particles is not None else \
+            Particles(0, self.d, self.dtype, self.topology.device)
+        self.material = material or SandMaterial()
+        self.drag_params = drag or DragParams()
+        self.powder = powder
+        self.adaptor = adaptor
+        self.static_tiles = static_tiles
+        self.unit_scale = unit_scale or UnitScale()
+        g = sediment_gravity if sediment_gravity is not None else solver.params.gravity
+        self.sediment_gravity = np.asarray(g, dtype=float)
+        self.grid = MpmGrid(self.topology, solver.boundaries, self.dtype,
+                            tables=lambda: solver.tables(0))
+        self.cadence = solver.params.mpm_cadence
+        self.step_count = 0
+        self.threads = 1
+        self.clamped_particles = 0
+        self.last_fields = None
+        self._diag = []            # device rows, materialised lazily
+        self._diag_rows = []
+        self._counters = torch.zeros(2, dtype=torch.int32, device=self.topology.device)
+        self._tmp = None
+        self.last_report = None
+        if self.drag_params.d_p is None and len(self.particles):
+            self.drag_params.d_p = float(particle_diameter(float(self.particles.V0.double().mean()),
+                                                           self.d))
+        if self.powder is not None:
+            self.powder.check_stability(1.0)
+
+    @property
+    def coupling_active(self) -> bool:
+        return len(self.particles) > 0
+
+    @property
+    def cfl_flags(self):
+        return int(self._cfl)
+
+    # -- exchange ------------------------------------------------------------------
+    def _exchange(self, solver):
+        r, w = solver.roles(0)
+        grid = self.grid
+        grid.sync_topology()
+        p = self.particles
+        lib = L.lib()
+        s = L.stream_handle()
+        dcode = dtype_code(self.dtype)
+        mat = self.material
+        lv0 = grid.level0()
+        grid.clear()
+        L.check(lib.mlbm_p2g(L.C.byref(lv0), len(p), L.ptr(p.xd), L.ptr(p.pd), p.pd.stride(0),
+                             mat.lam, mat.mu, mat.alpha, L.ptr(grid.ras), grid.ras.stride(0),
+                             dcode, L.ptr(grid._err), s), "p2g")
+        sp = solver.params
+        L.check(lib.mlbm_exchange(L.C.byref(lv0), L.fields(solver.arrays(w, 0).data),
+                                  L.fields(solver.arrays(r, 0).data),
+                                  L.fields(self.pair.trees[0].levels[0].data),
+                                  L.fields(self.pair.trees[1].levels[0].data),
+                                  L.ptr(grid.ras), grid.ras.stride(0), float(sp.eps_min),
+                                  float(solver.level_params.nu(0)),
+                                  float(self.drag_params.d_p or 1.0), float(self.drag_params.re_min),
+                                  float(self.cadence), float(sp.rho0), _d3(sp.gravity, self.d),
+                                  _d3(self.sediment_gravity, self.d), _faces(solver.boundaries),
+                                  float(mat.floor_friction), 1, dcode, s), "exchange")
+        L.check(lib.mlbm_g2p(L.C.byref(lv0), len(p), L.ptr(p.xd), L.ptr(p.pd), p.pd.stride(0),
+                             mat.lam, mat.mu, mat.alpha, L.ptr(grid.ras), grid.ras.stride(0),
+                             float(self.cadence), 1, dcode, L.ptr(self._counters), L.ptr(grid._err),
+                             s), "g2p")
+        solver.launches += 3
+        self.last_fields = CouplingFields(grid, self.pair.trees[0].levels[0])
+        return FIELD_FORCE, FIELD_TAU
+
+    @staticmethod
+    def _held(solver):
+        return FIELD_FORCE, FIELD_TAU
+
+    def step(self):
+        """One finest cycle of the coupled pipeline (coupling.py:448-481)."""
+        solver = self.solver
+        schedule = solver._schedule
+        cycle = schedule[solver.k[0] % len(schedule)]
+        is_mpm = self.coupling_active and (self.step_count % self.cadence == 0)
+        if is_mpm:
+            solver.run_cycle(cycle, hook=self._exchange)
+        elif self.coupling_active:
+            solver.run_cycle(cycle, hook=self._held)
+        else:
+            solver.run_cycle(cycle)
+        if self.coupling_active and is_mpm:
+            self.grid.raise_pending()
+        if self.powder is not None:
+            self._powder_cycle(is_mpm)
+        if self.adaptor is not None and self.coupling_active and \
+                self.step_count % self.cadence == 0:
+            driver = RefineDriver(positions_soa=self.particles.xd,
+                                  static_tiles=self.static_tiles, levels=self.topology.levels)
+            self.last_report = self.adaptor.update(driver, self.pair)
+            self.grid.sync_topology()
+        self.step_count += 1
+        self._record_diagnostics()
+
+    def _powder_cycle(self, is_mpm):
+        solver = self.solver
+        r, w = solver.last_roles(0)
+        grid = self.grid
+        lib = L.lib()
+        s = L.stream_handle()
+        dcode = dtype_code(self.dtype)
+        n0 = self.topology.cell_count(0)
+        if self._tmp is None or self._tmp.numel() != n0:
+            self._tmp = torch.empty(n0, dtype=self.dtype, device=self.topology.device)
+        src = is_mpm and self.last_fields is not None and self.powder.entrain > 0.0 \
+            and len(self.particles) > 0
+        if src:
+            R = grid.R
+            grid.ras[R["sig"]:R["n"]].zero_()
+            p = self.particles
+            lv0 = grid.level0()
+            L.check(lib.mlbm_stress_raster(L.C.byref(lv0), len(p), L.ptr(p.xd), L.ptr(p.pd),
+                                           p.pd.stride(0), self.material.lam, self.material.mu,
+                                           self.material.alpha, L.ptr(grid.ras),
+                                           grid.ras.stride(0), dcode, L.ptr(grid._err), s),
+                    "stress_raster")
+        lv0 = solver._structs[0]
+        pw = self.powder
+        L.check(lib.mlbm_powder(L.C.byref(lv0), L.fields(solver.arrays(r, 0).data),
+                                L.fields(solver.arrays(w, 0).data), L.ptr(grid.ras),
+                                grid.ras.stride(0), L.ptr(self._tmp), float(pw.diffusion),
+                                float(pw.sign), 1.0, float(pw.entrain), float(pw.eta_surface),
+                                1 if src else 0, dcode, s), "powder")
+
+    # -- diagnostics -------------------------------------------------------------------
+    def _record_diagnostics(self):
+        solver = self.solver
+        d = self.d
+        lib = L.lib()
+        s = L.stream_handle()
+        dcode = dtype_code(self.dtype)
+        out = torch.zeros(2 * d + 4, dtype=torch.float64, device=self.topology.device)
+        out[d + 1] = 1.0
+        for l in range(self.topology.levels):
+            if not self.topology.n_tiles(l):
+                continue
+            lw = solver.last_roles(l)[1] if solver.k[l] else 0
+            a = solver.arrays(lw, l)
+            L.check(lib.mlbm_diag_level(L.C.byref(solver._structs[l]), L.fields(a.data),
+                                        float((1 << d) ** l), dcode, L.ptr(out[:d + 2]), s),
+                    "diag_level")
+        p = self.particles
+        g = self.grid
+        n0 = self.topology.cell_count(0) if self.last_fields is not None else 0
+        L.check(lib.mlbm_diag_particles(d, len(p), L.ptr(p.pd), p.pd.stride(0), L.ptr(g.ras),
+                                        g.ras.stride(0), n0, dcode, L.ptr(out[d + 2:]), s),
+                "diag_particles")
+        self._diag.append((self.step_count, tuple(self.topology.n_tiles(l)
+                                                  for l in range(self.topology.levels)), out))
+
+    @property
+    def diagnostics(self):
+        d = self.d
+        while self._diag:
+            step, tiles, out = self._diag.pop(0)
+            o = out.cpu().numpy()
+            self._diag_rows.append(DiagRow(
+                step=step, t_phys=step * self.unit_scale.dt,
+                fluid_mom=tuple(float(v) for v in o[:d]),
+                sediment_mom=tuple(float(v) for v in o[d + 2:2 * d + 2]),
+                drag_impulse=tuple(float(-v) for v in o[2 * d + 2:3 * d + 2])
+                if len(o) >= 3 * d + 2 else (0.0,) * d,
+                sum_phi=float(o[d]), tiles=tiles, eps_min=float(o[d + 1])))
+        return self._diag_rows
+
+    def fluid_momentum(self):
+        rows = self.diagnostics
+        if not rows:
+            self._record_diagnostics()
+            return np.array(self.diagnostics.pop().fluid_mom)
+        return np.array(rows[-1].fluid_mom)
+
+    @property
+    def _cfl(self):
+        return int(self._counters[1].item())

@@ -326,7 +326,7 @@ __global__ void k_exchange(ExchArgs A) {
     for (int a = 0; a < D; ++a) g[a] = A.lv.tile_xyz[slot * 3 + a] * 4 + l3[a];
     const R mass = ras[RW::MASS * rs + c];
     R fs[D];
-    for (int a = 0; a < D; ++a) fs[a] = R(0);
+    for (int a = 0; a < D; ++a) fs[a] = A.mode == 1 ? R(0) : ras[(RW::FS + a) * rs + c];
     const R eps_min = R(A.eps_min);
     if (A.mode == 1) {
         const R eps = eps_of<D, R>(ras, rs, rt, c, eps_min);
@@ -491,6 +491,12 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
         pp[(PR::V + a) * P.ps + p] = v[a];
     }
     if (ncl) atomicAdd(clamped, ncl);
+    {
+        R vmax = R(0);
+#pragma unroll
+        for (int a = 0; a < D; ++a) vmax = fabs(v[a]) > vmax ? fabs(v[a]) : vmax;
+        if (!((double)vmax * dt < 0.5)) atomicOr(clamped + 1, 1);   // cfl_check (granular.py:428-432)
+    }
     R F[D * D], Fn[D * D];
 #pragma unroll
     for (int k = 0; k < D * D; ++k) { F[k] = pp[(PR::F + k) * P.ps + p]; pp[(PR::C + k) * P.ps + p] = C[k]; }

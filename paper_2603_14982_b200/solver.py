@@ -223,6 +223,58 @@ class _LevelTables:
         return (self.cell_flags & 1).bool()
 
 
+def build_tables(topo: Topology, bc, solid, err):
+    """Classify every level (flags, bounce-back masks, interface stencils) on
+    the device (solver.py:177-274 + sparse_grid.py:468-544).  Raises
+    TopologyError on violations."""
+    lib = L.lib()
+    s = L.stream_handle()
+    T = TILE ** topo.d
+    err.zero_()
+    counts = torch.zeros((topo.levels, 2), dtype=torch.int32, device=topo.device)
+    hier = topo.hier_struct()
+    tables = {}
+    for l in range(topo.levels):
+        n = topo.n_tiles(l)
+        if not n:
+            continue
+        t = _LevelTables(n * T, n, topo.device)
+        lvs = topo.level_struct(l)
+        L.check(lib.mlbm_classify_level(L.C.byref(lvs), L.C.byref(hier), L.C.byref(bc),
+                                        L.C.byref(solid), L.ptr(t.cell_flags),
+                                        L.ptr(t.dir_masks), L.ptr(t.tile_flags),
+                                        L.ptr(counts[l]), L.ptr(err), s), "classify_level")
+        tables[l] = t
+    cnt = counts.cpu().numpy()
+    NC = 1 << topo.d
+    for l, t in tables.items():
+        for which, nsel, other in ((0, int(cnt[l, 0]), l + 1), (1, int(cnt[l, 1]), l - 1)):
+            if nsel == 0:
+                continue
+            if other < 0 or other >= topo.levels or other not in tables:
+                raise TopologyError(f"level {l}: interface without a "
+                                    f"{'coarser' if which == 0 else 'finer'} level")
+            tg = torch.empty(nsel, dtype=torch.int32, device=topo.device)
+            src = torch.empty((nsel, NC), dtype=torch.int32, device=topo.device)
+            c1 = torch.zeros(1, dtype=torch.int32, device=topo.device)
+            ws = topo.workspace(topo.cell_count(l))
+            lv_a = topo.level_struct(l, t)
+            lv_b = topo.level_struct(other, tables[other])
+            L.check(lib.mlbm_build_interface(L.C.byref(lv_a), L.C.byref(lv_b), which,
+                                             L.ptr(tg), L.ptr(src), L.ptr(c1), L.ptr(err),
+                                             L.ptr(ws), ws.numel(), s), "build_interface")
+            if which == 0:
+                t.down = (tg, src, nsel)
+            else:
+                t.up = (tg, src, nsel)
+    e = err.cpu().numpy()
+    if e[0]:
+        err.zero_()
+        raise TopologyError(f"topology violation code {e[0]} detail {e[18]} at level "
+                            f"{e[1]} cell {tuple(e[3:3 + topo.d])}")
+    return tables
+
+
 class MultiLevelSolver:
     """Owns the kernels and the recursion schedule (solver.py:277-612)."""
 
@@ -257,56 +309,9 @@ class MultiLevelSolver:
         topo = self.topology
         if self._tables_version == topo.version:
             return
-        lib = L.lib()
-        s = L.stream_handle()
-        T = TILE ** self.d
-        self._err.zero_()
-        counts = torch.zeros((topo.levels, 2), dtype=torch.int32, device=topo.device)
-        hier = topo.hier_struct()
-        tables = {}
-        for l in range(topo.levels):
-            n = topo.n_tiles(l)
-            if not n:
-                continue
-            t = _LevelTables(n * T, n, topo.device)
-            lvs = topo.level_struct(l)
-            L.check(lib.mlbm_classify_level(L.C.byref(lvs), L.C.byref(hier), L.C.byref(self._bc),
-                                            L.C.byref(self._solid), L.ptr(t.cell_flags),
-                                            L.ptr(t.dir_masks), L.ptr(t.tile_flags),
-                                            L.ptr(counts[l]), L.ptr(self._err), s),
-                    "classify_level")
-            tables[l] = t
-        cnt = counts.cpu().numpy()
-        NC = 1 << self.d
-        for l, t in tables.items():
-            for which, nsel, other in ((0, int(cnt[l, 0]), l + 1), (1, int(cnt[l, 1]), l - 1)):
-                if nsel == 0 or other < 0 or other >= topo.levels or other not in tables:
-                    if nsel:
-                        self._raise_topology(f"level {l}: interface without a "
-                                             f"{'coarser' if which == 0 else 'finer'} level")
-                    continue
-                tg = torch.empty(nsel, dtype=torch.int32, device=topo.device)
-                src = torch.empty((nsel, NC), dtype=torch.int32, device=topo.device)
-                c1 = torch.zeros(1, dtype=torch.int32, device=topo.device)
-                ws = topo.workspace(topo.cell_count(l))
-                lv_a = topo.level_struct(l, t)
-                lv_b = topo.level_struct(other, tables[other])
-                L.check(lib.mlbm_build_interface(L.C.byref(lv_a), L.C.byref(lv_b), which,
-                                                 L.ptr(tg), L.ptr(src), L.ptr(c1),
-                                                 L.ptr(self._err), L.ptr(ws), ws.numel(), s),
-                        "build_interface")
-                if which == 0:
-                    t.down = (tg, src, nsel)
-                else:
-                    t.up = (tg, src, nsel)
-        self._tables = tables
+        self._tables = build_tables(topo, self._bc, self._solid, self._err)
         self._tables_version = topo.version
-        self._structs = {l: topo.level_struct(l, t) for l, t in tables.items()}
-        err = self._err.cpu().numpy()
-        if err[0]:
-            self._err.zero_()
-            self._raise_topology(f"topology violation code {err[0]} detail {err[18]} at level "
-                                 f"{err[1]} cell {tuple(err[3:6])}")
+        self._structs = {l: topo.level_struct(l, t) for l, t in self._tables.items()}
 
     def _raise_topology(self, msg):
         raise TopologyError(msg)

@@ -179,4 +179,3 @@ def test_fp32_shifted_rel_l2(d):
     for nm in names:
         r = rel_l2(otopo, lambda l: last(osv, l), dsv.topology, lambda l: last(dsv, l), [nm])
         assert r <= 1e-5, (nm, r)
-EOF
