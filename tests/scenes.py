@@ -1,0 +1,100 @@
+"""Scene dicts used by the parity tests and the bench.
+
+2D scenes restate the reference's shipped scenes (pkg/scenes/*.toml) and the
+2D analogs of BASELINE.json configs; 3D scenes are the
+configs at test / bench sizes."""
+import copy
+
+TAYLOR_GREEN_2D = {"domain": {"cells": [64, 64], "levels": 1},
+                   "fluid": {"tau0": 0.8, "init": "taylor_green", "init_u0": 0.05}}
+
+SAND_COLLAPSE_2D = {
+    "domain": {"cells": [192, 64], "levels": 1},
+    "fluid": {"tau0": 1.8, "gravity": [0.0, -1e-3]},
+    "boundaries": {"x_min": "wall", "x_max": "wall", "y_min": "wall", "y_max": "wall"},
+    "materials": {"density_ratio": 2.0, "E": 0.08, "nu": 0.3, "friction_angle_deg": 30.0,
+                  "floor_friction": 0.5},
+    "particles": {"blocks": [[84.0, 2.0, 108.0, 44.0]], "per_cell": 10},
+    "runtime": {"seed": 11}}
+
+DUNE_2D = {
+    "domain": {"cells": [256, 128], "levels": 3},
+    "fluid": {"tau0": 1.8, "eps_min": 0.5, "gravity": [0.0, 0.0]},
+    "boundaries": {"x_min": {"kind": "log_inlet", "u0": 0.04, "beta": 0.35, "y0": 6.0},
+                   "x_max": "outlet", "y_min": "wall", "y_max": "outlet"},
+    "materials": {"density_ratio": 40.0, "E": 0.08, "nu": 0.3, "friction_angle_deg": 30.0,
+                  "floor_friction": 0.5},
+    "particles": {"blocks": [[64.0, 2.5, 140.0, 10.0]], "per_cell": 4},
+    "runtime": {"seed": 42, "mpm_cadence": 1}}
+
+POWDER_BOX_2D = {
+    "domain": {"cells": [64, 64], "levels": 1},
+    "fluid": {"tau0": 1.8, "eps_min": 0.5, "gravity": [0.0, -5e-5]},
+    "boundaries": {"x_min": "periodic", "x_max": "periodic", "y_min": "wall", "y_max": "wall"},
+    "materials": {"density_ratio": 20.0, "E": 0.08},
+    "particles": {"blocks": [[24.0, 6.0, 40.0, 22.0]], "per_cell": 4},
+    "powder": {"enabled": True, "entrain": 0.02, "diffusion": 0.05},
+    "runtime": {"seed": 3}}
+
+# dispersed cloud forcing per-step block churn (config 5, 2D analog)
+CLOUD_2D = {
+    "domain": {"cells": [128, 128], "levels": 3},
+    "fluid": {"tau0": 1.8, "eps_min": 0.5},
+    "materials": {"density_ratio": 10.0, "E": 0.08},
+    "particles": {"blocks": [[40.0, 40.0, 56.0, 56.0], [80.0, 70.0, 92.0, 86.0]], "per_cell": 1},
+    "runtime": {"seed": 9}}
+
+# ---- 3D -------------------------------------------------------------------------
+COLUMN_3D_SMALL = {     # config 2 at test size
+    "domain": {"cells": [32, 32, 32], "levels": 2},
+    "fluid": {"tau0": 1.8, "eps_min": 0.5, "gravity": [0.0, -1e-4, 0.0]},
+    "boundaries": {"x_min": "wall", "x_max": "wall", "y_min": "wall", "y_max": "wall",
+                   "z_min": "wall", "z_max": "wall"},
+    "materials": {"density_ratio": 40.0, "E": 0.08},
+    "particles": {"blocks": [[12.0, 2.0, 12.0, 20.0, 18.0, 20.0]], "per_cell": 2},
+    "runtime": {"seed": 5}}
+
+DUNE_3D_SMALL = {       # config 3 at test size
+    "domain": {"cells": [64, 32, 16], "levels": 2},
+    "fluid": {"tau0": 1.8, "eps_min": 0.5},
+    "boundaries": {"x_min": {"kind": "log_inlet", "u0": 0.04, "beta": 0.35, "y0": 6.0},
+                   "x_max": "outlet", "y_min": "wall", "y_max": "outlet",
+                   "z_min": "periodic", "z_max": "periodic"},
+    "materials": {"density_ratio": 40.0, "E": 0.08},
+    "particles": {"blocks": [[16.0, 2.0, 0.0, 36.0, 8.0, 16.0]], "per_cell": 2},
+    "runtime": {"seed": 42}}
+
+POWDER_3D_SMALL = {     # config 4 ingredients at test size (powder on, solids)
+    "domain": {"cells": [32, 32, 16], "levels": 1},
+    "fluid": {"tau0": 1.8, "eps_min": 0.5, "gravity": [0.0, -5e-5, 0.0]},
+    "boundaries": {"y_min": "wall", "y_max": "outlet",
+                   "solid_boxes": [[0.0, 0.0, 0.0, 8.0, 3.0, 16.0]]},
+    "materials": {"density_ratio": 20.0, "E": 0.08},
+    "particles": {"blocks": [[12.0, 6.0, 4.0, 20.0, 14.0, 12.0]], "per_cell": 2},
+    "powder": {"enabled": True, "entrain": 0.02, "diffusion": 0.05},
+    "runtime": {"seed": 3}}
+
+# BASELINE.json configs[1]: two-level 128^3-effective column collapse in air,
+# 262,144 particles
+COLUMN_3D_C2 = {
+    "domain": {"cells": [128, 128, 128], "levels": 2},
+    "fluid": {"tau0": 1.8, "eps_min": 0.5, "gravity": [0.0, -1e-4, 0.0]},
+    "boundaries": {"x_min": "wall", "x_max": "wall", "y_min": "wall", "y_max": "wall",
+                   "z_min": "wall", "z_max": "wall"},
+    "materials": {"density_ratio": 40.0, "E": 0.08, "nu": 0.3, "friction_angle_deg": 30.0,
+                  "floor_friction": 0.5},
+    "particles": {"blocks": [[48.0, 4.0, 48.0, 80.0, 68.0, 80.0]], "per_cell": 4},
+    "runtime": {"seed": 5, "dtype": "f32"}}
+
+# configs[0]: single-level 64^3 periodic Taylor-Green
+TAYLOR_GREEN_3D_C1 = {"domain": {"cells": [64, 64, 64], "levels": 1},
+                      "fluid": {"tau0": 0.8, "init": "taylor_green", "init_u0": 0.05},
+                      "runtime": {"dtype": "f32"}}
+
+
+def scene(d, **over):
+    s = copy.deepcopy(d)
+    for k, v in over.items():
+        tbl, key = k.split("__")
+        s.setdefault(tbl, {})[key] = v
+    return s

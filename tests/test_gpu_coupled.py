@@ -1,0 +1,151 @@
+"""GPU parity of the full coupled step (LBM levels + exchange + MPM + powder +
+block maintenance) against the oracle, 2D and 3D, fp64.
+
+Gate A: integer topology bit-exact after every step
+(tile sets and streaks), fields / particles within 1e-9 absolute (the
+only difference is fp64 atomic summation order in P2G).
+"""
+import numpy as np
+import pytest
+import torch
+
+import scenes as S
+from oracle import scene as OS
+
+pytestmark = pytest.mark.gpu
+
+B = pytest.importorskip("paper_2603_14982_b200")
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def build_both(scene_dict):
+    from paper_2603_14982_b200.harness import build_scene, validate_scene
+    cfg = validate_scene(scene_dict)
+    dsim = build_scene(cfg)
+    osim = OS.build_scene(cfg.raw, heightmap=cfg.heightmap())
+    return osim, dsim
+
+
+def field_diff(osim, dsim):
+    worst = 0.0
+    d = dsim.d
+    names = B.field_names(d)
+    for l in range(dsim.topology.levels):
+        ot, dt = osim.topo, dsim.topology
+        if not dt.n_tiles(l):
+            continue
+        ow = osim.solver.last_roles(l)[1] if osim.solver.k[l] else 0
+        dw = dsim.solver.last_roles(l)[1] if dsim.solver.k[l] else 0
+        assert ow == dw
+        oa = osim.solver.arrays(ow, l)
+        da = dsim.solver.arrays(dw, l)
+        dmap = {tuple(c): i for i, c in enumerate(dt.cell_coords(l))}
+        perm = np.array([dmap[tuple(c)] for c in ot.cell_coords(l)])
+        for nm in names:
+            worst = max(worst, float(np.abs(da[nm].cpu().numpy()[perm] - oa[nm]).max()))
+    return worst
+
+
+def particle_diff(osim, dsim):
+    if not len(osim.p):
+        return 0.0
+    dx = np.abs(dsim.particles.x.cpu().numpy() - osim.p.x).max()
+    dv = np.abs(dsim.particles.v.cpu().numpy() - osim.p.v).max()
+    dF = np.abs(dsim.particles.F.cpu().numpy() - osim.p.F).max()
+    return float(max(dx, dv, dF))
+
+
+def run_and_compare(scene_dict, steps, tol=1e-9, check_streaks=True):
+    _need_gpu()
+    osim, dsim = build_both(scene_dict)
+    assert dsim.topology.tile_set() == osim.topo.tile_set()
+    for s in range(steps):
+        osim.step()
+        dsim.step()
+        assert dsim.topology.tile_set() == osim.topo.tile_set(), f"tile sets differ at step {s}"
+        if check_streaks and osim.adaptor is not None:
+            for l, (a, b) in enumerate(zip(dsim.adaptor.streak, osim.adaptor.streak)):
+                assert np.array_equal(a, b), f"streaks differ at step {s} level {l}"
+    fd = field_diff(osim, dsim)
+    pd = particle_diff(osim, dsim)
+    assert fd <= tol, f"fields differ by {fd}"
+    assert pd <= tol, f"particles differ by {pd}"
+    od = osim.diagnostics[-1]
+    dd = dsim.diagnostics[-1]
+    assert np.allclose(dd.fluid_mom, od["fluid_mom"], rtol=1e-9, atol=1e-12)
+    assert np.allclose(dd.sediment_mom, od["sediment_mom"], rtol=1e-9, atol=1e-12)
+    assert dd.tiles == od["tiles"]
+    assert abs(dd.sum_phi - od["sum_phi"]) <= 1e-9 * max(1.0, abs(od["sum_phi"]))
+    assert abs(dd.eps_min - od["eps_min"]) <= 1e-12
+    return osim, dsim
+
+
+def test_taylor_green_scene_2d():
+    run_and_compare(S.TAYLOR_GREEN_2D, 10)
+
+
+def test_sand_collapse_2d():
+    run_and_compare(S.SAND_COLLAPSE_2D, 15)
+
+
+def test_powder_box_2d():
+    run_and_compare(S.POWDER_BOX_2D, 15)
+
+
+def test_dune_2d_three_levels():
+    run_and_compare(S.DUNE_2D, 12)
+
+
+def test_cloud_2d_block_churn():
+    sc = S.scene(S.CLOUD_2D)
+    osim, dsim = build_both(sc)
+    rng = np.random.default_rng(4)
+    n = len(osim.p)
+    v = rng.normal(0, 0.08, (n, 2)).clip(-0.45, 0.45)
+    osim.p.v[:] = v
+    dsim.particles.v = v
+    changes = 0
+    for s in range(25):
+        osim.step()
+        dsim.step()
+        assert dsim.topology.tile_set() == osim.topo.tile_set(), f"step {s}"
+        for a, b in zip(dsim.adaptor.streak, osim.adaptor.streak):
+            assert np.array_equal(a, b)
+        if not osim.last_report.noop:
+            changes += 1
+    assert changes > 0
+    assert field_diff(osim, dsim) <= 1e-9
+    assert particle_diff(osim, dsim) <= 1e-9
+
+
+def test_column_3d_two_levels():
+    run_and_compare(S.COLUMN_3D_SMALL, 8)
+
+
+def test_dune_3d_inlet_outlet():
+    run_and_compare(S.DUNE_3D_SMALL, 6)
+
+
+def test_powder_3d_solids():
+    run_and_compare(S.POWDER_3D_SMALL, 6)
+
+
+def test_fp32_column_3d_short():
+    """Gate B on the coupled path: fp32 device vs fp64 oracle after 20 steps."""
+    _need_gpu()
+    sc = S.scene(S.COLUMN_3D_SMALL, runtime__dtype="f32")
+    osim, dsim = build_both(sc)
+    for _ in range(20):
+        osim.step()
+        dsim.step()
+    assert dsim.topology.tile_set() == osim.topo.tile_set()
+    x = dsim.particles.x.cpu().numpy()
+    v = dsim.particles.v.double().cpu().numpy()
+    rx = np.linalg.norm(x - osim.p.x) / np.linalg.norm(osim.p.x)
+    rv = np.linalg.norm(v - osim.p.v) / max(np.linalg.norm(osim.p.v), 1e-30)
+    assert rx <= 1e-5, rx
+    assert rv <= 1e-4, rv
