@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Benchmark of the coupled adaptive HOME-LBM <-> MPM step on B200.
+
+Workload (BASELINE.json configs[1]): two-level
+128^3-effective granular column collapse in air, 262,144 MPM sand particles,
+walls on all faces, two-way coupling, block maintenance every step, fp32
+device state (shifted density).  One bench "step" = one finest coupled
+cycle ``CoupledSim.step()`` (coupling.py:448-481): coarser-level prelude,
+level-0 stream, exchange + MPM, level-0 collide, adapt, diagnostics.
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the CPU oracle
+port of the same path instead (the reference is pure NumPy and 2D-only, see
+DESIGN.md §1).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = ("effective MLUPS and MPM particles/s per coupled step at 1/2/4/8 B200; "
+          "HBM GB/s vs peak")
+UNIT = "effective MLUPS"
+REF_TIMED_STEPS_CAP = 5
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--scene", default="c2", choices=["c2", "c1"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def scene_dict(name):
+    import scenes as S
+    return S.COLUMN_3D_C2 if name == "c2" else S.TAYLOR_GREEN_3D_C1
+
+
+def workload_name(name):
+    return ("C2: two-level 128^3-effective 3D granular column collapse in air, 262,144 "
+            "MPM sand particles, two-way coupled, adapt every step" if name == "c2" else
+            "C1: single-level 64^3 periodic Taylor-Green (D3Q27)")
+
+
+# -- clocks -------------------------------------------------------------------------
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 6 and p[0].isdigit():
+                    rows.append(p)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
+        sm = [int(r[0]) for r in rows]
+        return {"sm_mhz": int(statistics.median(sm)), "sm_max_mhz": int(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+# -- algorithmic bytes per kernel class ---------------------------------
+def kernel_class(rec, d, s):
+    name, _, _, _ = rec[:4]
+    args = rec[4]
+    NM = 1 + d + d * (d + 1) // 2
+    T = 4 ** d
+    if name == "mlbm_level_step":
+        lv, mode = args[0]._obj, int(args[4])
+        cells = lv.n_tiles * T
+        if mode in (0, 1):
+            return f"level_step[{'fused' if mode == 0 else 'stream'}]", cells * 2 * NM * s, cells
+        return "level_step[collide+bc]", cells * (2 * NM + d + 1) * s, cells
+    if name == "mlbm_p2g":
+        n = int(args[1])
+        return "p2g", n * (8 * d + (2 * d + 2 * d * d + 2) * s), n
+    if name == "mlbm_g2p":
+        n = int(args[1])
+        return "g2p", n * (16 * d + (d * d + 1) * s + (d + 2 * d * d + 1) * s), n
+    if name == "mlbm_exchange":
+        cells = args[0]._obj.n_tiles * T
+        return "exchange", cells * (17 + 25) * s, cells
+    if name in ("mlbm_downward", "mlbm_upward"):
+        n = int(args[1])
+        nc = 1 << d
+        return "transfer", n * (nc * (NM + 2) * (2 if name == "mlbm_downward" else 1)
+                                + (NM + 2)) * s, n
+    if name.startswith("mlbm_diag"):
+        return "diagnostics", 0, 0
+    return "adapt/topology", 0, 0
+
+
+def run_mine(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2603_14982_b200 import _lib as L
+    from paper_2603_14982_b200.harness import build_scene, validate_scene
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = validate_scene(scene_dict(args.scene))
+    sim = build_scene(cfg)
+    d = cfg.dim
+    eff_cells = int(np.prod(cfg.cells))
+    n_part = len(sim.particles)
+    s = 4 if cfg.dtype == torch.float32 else 8
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        sim.step()
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    # ---- timed region: device time per step (CUDA events), L2 flushed between steps
+    clocks = Clocks(local_rank)
+    launches0 = L.TRACE.launches
+    L.TRACE.start()
+    L.TRACE.records_args = True
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        sim.step()
+        e1.record()
+        ev.append((e0, e1))
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    recs = L.TRACE.stop()
+    launches = L.TRACE.launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_ms = sum(step_ms)
+    t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    ms_per_step = t_ms / args.steps
+    value = world * eff_cells * args.steps / (t_ms * 1e-3) / 1e6
+    pps = world * n_part * args.steps / (t_ms * 1e-3)
+
+    # ---- per-kernel classes inside the timed region
+    classes = {}
+    for r in recs:
+        name, e0, e1, _ = r[:4]
+        cls, nbytes, units = kernel_class(r, d, s)
+        c = classes.setdefault(cls, {"ms": 0.0, "launches": 0, "bytes": 0.0})
+        c["ms"] += e0.elapsed_time(e1)
+        c["launches"] += 1
+        c["bytes"] += nbytes
+    peak, peak_kind = measured_peak()
+    total_k = sum(c["ms"] for c in classes.values())
+    for c in classes.values():
+        c["share_of_step"] = c["ms"] / t_ms if t_ms else 0.0
+        c["achieved_gbs"] = c["bytes"] / (c["ms"] * 1e-3) / 1e9 if c["ms"] and c["bytes"] else None
+    dom = max((k for k in classes if classes[k]["bytes"]), key=lambda k: classes[k]["ms"])
+
+    def roof(k):
+        c = classes[k]
+        ach = c["achieved_gbs"]
+        return {"kernel": k, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(ach / peak, 4), "peak_source": peak_kind,
+                "bytes_per_launch": c["bytes"] / c["launches"],
+                "avg_launch_us": 1e3 * c["ms"] / c["launches"], "traffic": None}
+
+    lbm_keys = [k for k in classes if k.startswith("level_step")]
+    lbm_bytes = sum(classes[k]["bytes"] for k in lbm_keys)
+    lbm_ms = sum(classes[k]["ms"] for k in lbm_keys)
+
+    # ---- e2e through the public API with host-owned particle state
+    e2e = None
+    if not args.no_e2e:
+        p = sim.particles
+        hx = torch.empty_like(p.xd, device="cpu").pin_memory()
+        hp = torch.empty_like(p.pd, device="cpu").pin_memory()
+        hx.copy_(p.xd)
+        hp.copy_(p.pd)
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        diag_bytes = 0
+        for _ in range(args.steps):
+            p.xd.copy_(hx, non_blocking=True)
+            p.pd.copy_(hp, non_blocking=True)
+            sim.step()
+            hx.copy_(p.xd, non_blocking=True)
+            hp.copy_(p.pd, non_blocking=True)
+            row = sim.diagnostics[-1]        # D2H of the step's diagnostics row
+            diag_bytes = 8 * (3 * d + 2)
+        e1.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te = float(te.item())
+        nb = p.xd.numel() * 8 + p.pd.numel() * p.pd.element_size()
+        e2e = {"value": round(world * eff_cells * args.steps / (te * 1e-3) / 1e6, 3), "unit": UNIT,
+               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb + diag_bytes,
+               "particles_per_s": round(world * n_part * args.steps / (te * 1e-3), 1),
+               "ms_per_step": te / args.steps,
+               "path": "CoupledSim.step() with particle state uploaded from / read back to "
+                       "pinned host memory every step + diagnostics row D2H"}
+        del row
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.scene)
+
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if s == 4 else "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args.scene),
+                   "effective_cells": eff_cells, "particles": n_part,
+                   "levels": cfg.levels, "lattice": "D3Q27" if d == 3 else "D2Q9",
+                   "stored_tiles": [sim.topology.n_tiles(l) for l in range(cfg.levels)],
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "flushed (256 MB write) between timed steps, outside the events"},
+        "particles_per_s": round(pps, 1),
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": roof(dom),
+        "roofline_lbm": {"kernel": "level_step (all modes)", "bound": "hbm",
+                         "achieved": round(lbm_bytes / (lbm_ms * 1e-3) / 1e9, 1) if lbm_ms else None,
+                         "peak": peak, "unit": "GB/s",
+                         "frac": round(lbm_bytes / (lbm_ms * 1e-3) / 1e9 / peak, 4) if lbm_ms else None,
+                         "share_of_step": round(lbm_ms / t_ms, 4)},
+        "kernels": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv)
+                        for kk, vv in v.items()} for k, v in sorted(classes.items())},
+        "kernel_time_share": round(total_k / t_ms, 4),
+        "cpu_baseline": cpu,
+        "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def oracle_sample(scene):
+    """Bounded CPU sample of the same workload: the fp64 NumPy oracle port."""
+    from oracle import scene as OS
+    from paper_2603_14982_b200.harness.config import validate_scene
+    cfg = validate_scene(scene_dict(scene))
+    return cfg, OS.build_scene(cfg.raw, heightmap=cfg.heightmap())
+
+
+def cpu_baseline(scene):
+    import numpy as np
+    cfg, sim = oracle_sample(scene)
+    t0 = time.perf_counter()
+    sim.step()
+    dt = time.perf_counter() - t0
+    eff = int(np.prod(cfg.cells))
+    return {"value": round(eff / dt / 1e6, 4), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"1 coupled step of the full {scene.upper()} scene in the fp64 NumPy oracle "
+                      f"port (oracle/, single thread) after scene build: {dt:.2f} s",
+            "particles_per_s": round(len(sim.p) / dt, 1)}
+
+
+def run_reference(args, rank):
+    """--impl reference: the CPU implementation of the path (oracle port; the
+    reference itself is 2D-only NumPy and cannot run this 3D config)."""
+    import numpy as np
+    if rank != 0:
+        return
+    cfg, sim = oracle_sample(args.scene)
+    eff = int(np.prod(cfg.cells))
+    for _ in range(min(args.warmup, 1)):
+        sim.step()
+    k = min(args.steps, REF_TIMED_STEPS_CAP)
+    t0 = time.perf_counter()
+    for _ in range(k):
+        sim.step()
+    dt = time.perf_counter() - t0
+    value = eff * k / dt / 1e6
+    sample = (f"{k} coupled steps (of {args.steps} requested, capped to bound CPU time) of the "
+              f"full {args.scene.upper()} scene in the fp64 NumPy oracle port, 1 thread")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": k, "warmup": min(args.warmup, 1),
+        "ms_per_step": round(1e3 * dt / k, 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args.scene), "effective_cells": eff,
+                   "particles": len(sim.p)},
+        "particles_per_s": round(len(sim.p) * k / dt, 1),
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_mine(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -5,7 +5,8 @@
  * Every entry point is extern "C", takes device pointers + sizes + a CUDA
  * stream (as void*), never allocates persistently (scratch comes from a
  * caller-provided workspace), is asynchronous on the given stream and returns
- * an int status (0 = launched, <0 = bad argument / launch failure).  Numerical
+ * an int status (>= 0: number of kernels launched, < 0: bad argument / launch
+ * failure, -cudaError).  Numerical
  * failures (divergence, topology violations) are written to a device-side
  * mlbm_error_t record that the host reads after the step.
  *

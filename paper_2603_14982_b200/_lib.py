@@ -40,6 +40,7 @@ def build(force=False, verbose=False):
     hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     hdrs.append(os.path.join(INCLUDE, "mlbm_b200.h"))
     hmt = max(os.path.getmtime(h) for h in hdrs)
+    procs = []
     for src in SOURCES:
         sp = os.path.join(CSRC, src)
         op = os.path.join(bdir, src.replace(".cu", ".o"))
@@ -50,7 +51,10 @@ def build(force=False, verbose=False):
         cmd = [_nvcc()] + NVCC_FLAGS + ["-I", INCLUDE, "-c", sp, "-o", op]
         if verbose:
             print(" ".join(cmd))
-        subprocess.run(cmd, check=True)
+        procs.append((cmd, subprocess.Popen(cmd)))
+    for cmd, p in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, cmd)
     if (force or not os.path.exists(LIBPATH) or
             os.path.getmtime(LIBPATH) < max(os.path.getmtime(o) for o in objs)):
         cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
@@ -174,16 +178,71 @@ def load(path=LIBPATH):
     return lib
 
 
+class _Tracer:
+    """Counts kernel launches of the library and, when enabled, brackets each
+    C-ABI call with CUDA events on the current stream (bench.py uses it to
+    time kernels inside the timed region)."""
+
+    def __init__(self):
+        self.launches = 0
+        self.enabled = False
+        self.records = []
+
+    def start(self):
+        self.enabled = True
+        self.records = []
+
+    def stop(self):
+        self.enabled = False
+        return self.records
+
+
+TRACE = _Tracer()
+
+
+class _TracedLib:
+    def __init__(self, lib):
+        self._lib = lib
+        self._cache = {}
+
+    def __getattr__(self, name):
+        fn = getattr(self._lib, name)
+        if not name.startswith("mlbm_") or name in _RET64 or name.endswith("_rows"):
+            return fn
+
+        def call(*args):
+            if TRACE.enabled:
+                import torch
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                r = fn(*args)
+                e1.record()
+                TRACE.records.append((name, e0, e1, r, args))
+            else:
+                r = fn(*args)
+            if r > 0:
+                TRACE.launches += r
+            return r
+        return call
+
+
+_TRACED = None
+
+
 def lib():
     """The bound library; raises if it cannot run kernels here."""
+    global _TRACED
     import torch
     if not torch.cuda.is_available():
         raise KernelError("no CUDA device: the B200 path has no CPU fallback")
-    return load()
+    if _TRACED is None:
+        _TRACED = _TracedLib(load())
+    return _TRACED
 
 
 def check(status, what):
-    if status != 0:
+    if status < 0:
         raise KernelError(f"{what} failed with status {status}")
 
 

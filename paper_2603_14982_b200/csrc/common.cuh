@@ -118,9 +118,10 @@ __device__ __forceinline__ void report_error(mlbm_error_t* err, int code, int le
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-inline int launch_status() {
+// returns the number of kernels launched (>= 0) or -cudaError
+inline int launch_status(int launched = 1) {
     cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? 0 : -(int)e;
+    return e == cudaSuccess ? launched : -(int)e;
 }
 
 }  // namespace mlbm

@@ -412,7 +412,7 @@ int launch_level(const StepArgs& a, int mode, cudaStream_t s) {
     case 3: level_kernel<D, R, 3><<<blocks, 128, 0, s>>>(a); break;
     default: level_kernel<D, R, 4><<<blocks, 128, 0, s>>>(a); break;
     }
-    return launch_status();
+    return launch_status(1);
 }
 
 // ---------------------------------------------------------------------------
@@ -533,7 +533,7 @@ extern "C" int mlbm_downward(int32_t dim, int32_t n, const int32_t* targets, con
     else if (dim == 3) { if (dtype) DOWN(3, double); else DOWN(3, float); }
     else return -1;
 #undef DOWN
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_upward(int32_t dim, int32_t n, const int32_t* targets, const int32_t* src,
@@ -548,5 +548,5 @@ extern "C" int mlbm_upward(int32_t dim, int32_t n, const int32_t* targets, const
     else if (dim == 3) { if (dtype) UP(3, double); else UP(3, float); }
     else return -1;
 #undef UP
-    return launch_status();
+    return launch_status(1);
 }

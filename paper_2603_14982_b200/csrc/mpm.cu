@@ -778,7 +778,7 @@ extern "C" int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, voi
     if (lv0->dim == 2) { if (dtype) P2G(2, double); else P2G(2, float); }
     else { if (dtype) P2G(3, double); else P2G(3, float); }
 #undef P2G
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_exchange(const mlbm_level_t* lv0, mlbm_fields_t w_tree, mlbm_fields_t r_tree,
@@ -803,7 +803,7 @@ extern "C" int mlbm_exchange(const mlbm_level_t* lv0, mlbm_fields_t w_tree, mlbm
     if (lv0->dim == 2) { if (dtype) EX(2, double); else EX(2, float); }
     else { if (dtype) EX(3, double); else EX(3, float); }
 #undef EX
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, double* x, void* p, int64_t ps,
@@ -819,7 +819,7 @@ extern "C" int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, double* x, void* p, 
     if (lv0->dim == 2) { if (dtype) G2P(2, double); else G2P(2, float); }
     else { if (dtype) G2P(3, double); else G2P(3, float); }
 #undef G2P
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_stress_raster(const mlbm_level_t* lv0, int32_t n, const double* x, const void* p,
@@ -834,7 +834,7 @@ extern "C" int mlbm_stress_raster(const mlbm_level_t* lv0, int32_t n, const doub
     if (lv0->dim == 2) { if (dtype) SR(2, double); else SR(2, float); }
     else { if (dtype) SR(3, double); else SR(3, float); }
 #undef SR
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_powder(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm_fields_t dst, void* ras,
@@ -851,7 +851,7 @@ extern "C" int mlbm_powder(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm_fiel
     if (lv0->dim == 2) { if (dtype) PW(2, double); else PW(2, float); }
     else { if (dtype) PW(3, double); else PW(3, float); }
 #undef PW
-    return launch_status();
+    return launch_status(2);
 }
 
 extern "C" int mlbm_diag_level(const mlbm_level_t* lv, mlbm_fields_t f, double vol, int32_t dtype,
@@ -864,7 +864,7 @@ extern "C" int mlbm_diag_level(const mlbm_level_t* lv, mlbm_fields_t f, double v
     if (lv->dim == 2) { if (dtype) DG(2, double); else DG(2, float); }
     else { if (dtype) DG(3, double); else DG(3, float); }
 #undef DG
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_diag_particles(int32_t dim, int32_t n, const void* p, int64_t ps, const void* ras,
@@ -877,5 +877,5 @@ extern "C" int mlbm_diag_particles(int32_t dim, int32_t n, const void* p, int64_
     if (dim == 2) { if (dtype) DP(2, double); else DP(2, float); }
     else { if (dtype) DP(3, double); else DP(3, float); }
 #undef DP
-    return launch_status();
+    return launch_status(1);
 }

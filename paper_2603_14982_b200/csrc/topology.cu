@@ -597,7 +597,7 @@ extern "C" int mlbm_compact_tiles(int32_t dim, const int32_t tiles[3], const uin
     I3 td{{tiles[0], tiles[1], tiles[2]}};
     k_scatter_tiles<<<blocks_for(n, 256), 256, 0, s>>>(n, td, kind, pos, old_map, tile_map, tile_xyz,
                                                        tile_kind, old_slot, counts);
-    return launch_status();
+    return launch_status(4);
 }
 
 extern "C" int mlbm_build_neighbors(const mlbm_level_t* lv, int32_t* nbr, void* stream) {
@@ -607,7 +607,7 @@ extern "C" int mlbm_build_neighbors(const mlbm_level_t* lv, int32_t* nbr, void* 
     cudaStream_t s = as_stream(stream);
     if (lv->dim == 2) k_neighbors<2><<<blocks_for(n, 256), 256, 0, s>>>(*lv, nbr);
     else k_neighbors<3><<<blocks_for(n, 256), 256, 0, s>>>(*lv, nbr);
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_classify_level(const mlbm_level_t* lv, const mlbm_hier_t* h, const mlbm_bc_t* bc,
@@ -622,7 +622,7 @@ extern "C" int mlbm_classify_level(const mlbm_level_t* lv, const mlbm_hier_t* h,
     else
         k_classify<3><<<lv->n_tiles, 64, 0, s>>>(*lv, *h, *bc, *solid, cell_flags, dir_masks,
                                                  tile_flags, counts, err);
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_build_interface(const mlbm_level_t* lv, const mlbm_level_t* other, int32_t which,
@@ -645,7 +645,7 @@ extern "C" int mlbm_build_interface(const mlbm_level_t* lv, const mlbm_level_t* 
         k_iface_stencil<2><<<blocks_for(n, 128), 128, 0, s>>>(*lv, *other, which, counts, targets, src, err);
     else
         k_iface_stencil<3><<<blocks_for(n, 128), 128, 0, s>>>(*lv, *other, which, counts, targets, src, err);
-    return launch_status();
+    return launch_status(4);
 }
 
 extern "C" int mlbm_seed_tiles(int32_t dim, int32_t n, const void* x, int64_t xstride, int32_t dtype,
@@ -656,7 +656,7 @@ extern "C" int mlbm_seed_tiles(int32_t dim, int32_t n, const void* x, int64_t xs
     I3 t0{{tiles0[0], tiles0[1], tiles0[2]}};
     if (dtype) k_seed<double><<<blocks_for(n, 256), 256, 0, s>>>(dim, n, (const double*)x, xstride, t0, seeds, err);
     else k_seed<float><<<blocks_for(n, 256), 256, 0, s>>>(dim, n, (const float*)x, xstride, t0, seeds, err);
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_bitmap_op(int32_t op, int32_t dim, const int32_t dims[3], const uint8_t* in,
@@ -666,7 +666,7 @@ extern "C" int mlbm_bitmap_op(int32_t op, int32_t dim, const int32_t dims[3], co
     if (op == 1) { n = 1; for (int a = 0; a < 3; ++a) n *= a < dim ? dims[a] / 2 : dims[a]; }
     if (n <= 0) return 0;
     k_bitmap_op<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(op, dim, d, in, out);
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_dilate(int32_t dim, const int32_t dims[3], const int32_t periodic[3], int32_t r,
@@ -684,7 +684,7 @@ extern "C" int mlbm_dilate(int32_t dim, const int32_t dims[3], const int32_t per
         k_dilate_axis<<<B, 256, 0, s>>>(d, 1, periodic[1], r, out, tmp);
         k_dilate_axis<<<B, 256, 0, s>>>(d, 2, periodic[2], r, tmp, out);
     }
-    return launch_status();
+    return launch_status(dim);
 }
 
 extern "C" int mlbm_effective_level(int32_t dim, const int32_t dims[3], const uint8_t* des,
@@ -698,7 +698,7 @@ extern "C" int mlbm_effective_level(int32_t dim, const int32_t dims[3], const ui
     if (n <= 0) return 0;
     k_effective<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(dim, d, grouped ? 1 : 0, des, cur, guard,
                                                                   par_prev, streak, eff);
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_plan_level(int32_t n, const uint8_t* own, const uint8_t* storage,
@@ -706,21 +706,21 @@ extern "C" int mlbm_plan_level(int32_t n, const uint8_t* own, const uint8_t* sto
                                void* stream) {
     if (n <= 0) return 0;
     k_plan<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(n, own, storage, old_kind, new_kind, changed);
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_check_coverage(const mlbm_hier_t* h, int32_t* viol, void* stream) {
     const I3 t0 = tdims_of(*h, 0);
     const int64_t n = (int64_t)t0.v[0] * t0.v[1] * t0.v[2];
     k_coverage<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(*h, viol);
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_count_ring_violations(int64_t n, const uint8_t* dil, const uint8_t* kind,
                                           int32_t* viol, void* stream) {
     if (n <= 0) return 0;
     k_ring_viol<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(n, dil, kind, viol);
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_check_particles(int32_t dim, int32_t n, const void* x, int64_t xstride, int32_t dtype,
@@ -731,7 +731,7 @@ extern "C" int mlbm_check_particles(int32_t dim, int32_t n, const void* x, int64
     cudaStream_t s = as_stream(stream);
     if (dtype) k_particle_leaf<double><<<blocks_for(n, 256), 256, 0, s>>>(dim, n, (const double*)x, xstride, t0, kind0, viol);
     else k_particle_leaf<float><<<blocks_for(n, 256), 256, 0, s>>>(dim, n, (const float*)x, xstride, t0, kind0, viol);
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_migrate_level(int32_t dim, int32_t n_new_tiles, const int32_t* old_slot,
@@ -746,7 +746,7 @@ extern "C" int mlbm_migrate_level(int32_t dim, int32_t n_new_tiles, const int32_
     if (dim == 2) { if (dtype) MIG(2, double); else MIG(2, float); }
     else { if (dtype) MIG(3, double); else MIG(3, float); }
 #undef MIG
-    return launch_status();
+    return launch_status(1);
 }
 
 extern "C" int mlbm_init_new_cells(const mlbm_hier_t* old_h, const mlbm_hier_t* nh, int32_t level,
@@ -762,5 +762,5 @@ extern "C" int mlbm_init_new_cells(const mlbm_hier_t* old_h, const mlbm_hier_t* 
     if (old_h->dim == 2) { if (dtype) INI(2, double); else INI(2, float); }
     else { if (dtype) INI(3, double); else INI(3, float); }
 #undef INI
-    return launch_status();
+    return launch_status(1);
 }
