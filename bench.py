@@ -166,8 +166,7 @@ def run_mine(args, rank, world, local_rank):
     # ---- timed region: device time per step (CUDA events), L2 flushed between steps
     clocks = Clocks(local_rank)
     launches0 = L.TRACE.launches
-    L.TRACE.start()
-    L.TRACE.records_args = True
+    caps0, chg0 = sim.graph_captures, sim.topology_changes
     barrier()
     torch.cuda.synchronize()
     clocks.start()
@@ -183,8 +182,9 @@ def run_mine(args, rank, world, local_rank):
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    recs = L.TRACE.stop()
     launches = L.TRACE.launches - launches0
+    graph_info = {"graph_replays_per_step": 1, "graph_captures": sim.graph_captures - caps0,
+                  "topology_changes": sim.topology_changes - chg0}
     step_ms = [a.elapsed_time(b) for a, b in ev]
     t_ms = sum(step_ms)
     t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
@@ -195,7 +195,22 @@ def run_mine(args, rank, world, local_rank):
     value = world * eff_cells * args.steps / (t_ms * 1e-3) / 1e6
     pps = world * n_part * args.steps / (t_ms * 1e-3)
 
-    # ---- per-kernel classes inside the timed region
+    # ---- per-kernel device times: an eager pass of the same steps with every
+    #      C-ABI call bracketed by CUDA events on the launching stream
+    sim.use_graphs = False
+    kp = min(args.steps, 10)
+    L.TRACE.start()
+    ek0 = torch.cuda.Event(enable_timing=True)
+    ek1 = torch.cuda.Event(enable_timing=True)
+    ek0.record()
+    for _ in range(kp):
+        flush.zero_()
+        sim.step()
+    ek1.record()
+    torch.cuda.synchronize()
+    recs = L.TRACE.stop()
+    t_eager_ms = ek0.elapsed_time(ek1)
+    sim.use_graphs = True
     classes = {}
     for r in recs:
         name, e0, e1, _ = r[:4]
@@ -207,7 +222,8 @@ def run_mine(args, rank, world, local_rank):
     peak, peak_kind = measured_peak()
     total_k = sum(c["ms"] for c in classes.values())
     for c in classes.values():
-        c["share_of_step"] = c["ms"] / t_ms if t_ms else 0.0
+        c["ms_per_step"] = c["ms"] / kp
+        c["share_of_graph_step"] = c["ms_per_step"] / ms_per_step if ms_per_step else 0.0
         c["achieved_gbs"] = c["bytes"] / (c["ms"] * 1e-3) / 1e9 if c["ms"] and c["bytes"] else None
     dom = max((k for k in classes if classes[k]["bytes"]), key=lambda k: classes[k]["ms"])
 
@@ -283,10 +299,14 @@ def run_mine(args, rank, world, local_rank):
                          "achieved": round(lbm_bytes / (lbm_ms * 1e-3) / 1e9, 1) if lbm_ms else None,
                          "peak": peak, "unit": "GB/s",
                          "frac": round(lbm_bytes / (lbm_ms * 1e-3) / 1e9 / peak, 4) if lbm_ms else None,
-                         "share_of_step": round(lbm_ms / t_ms, 4)},
+                         "share_of_graph_step": round(lbm_ms / kp / ms_per_step, 4)},
         "kernels": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv)
                         for kk, vv in v.items()} for k, v in sorted(classes.items())},
-        "kernel_time_share": round(total_k / t_ms, 4),
+        "kernel_profile": {"steps": kp, "mode": "eager pass after the timed region, each C-ABI "
+                                                 "call bracketed by CUDA events",
+                           "kernel_ms_per_step": round(total_k / kp, 4),
+                           "eager_ms_per_step": round(t_eager_ms / kp, 4)},
+        "graph": graph_info,
         "cpu_baseline": cpu,
         "clocks": clk,
     }

@@ -113,6 +113,7 @@ class GridAdaptor:
         self._stor = [z(k) for k in n]
         self._tmp = [z(k) for k in n]
         self._new = [z(k) for k in n]
+        self._seeds = z(n[0])
         self._status = torch.zeros(topology.levels + 4, dtype=torch.int32, device=dev)
         self._err = torch.zeros(L.ERR_INTS, dtype=torch.int32, device=dev)
         self._taus = torch.tensor(level_params.taus, dtype=torch.float64, device=dev)
@@ -160,14 +161,27 @@ class GridAdaptor:
 
     # -- update ----------------------------------------------------------------------
     def update(self, driver: RefineDriver, pair: PingPongPair) -> AdaptReport:
+        """One adaptation pass (adapt.py:198-230)."""
+        self.plan_device(driver)
+        status = self._status.cpu().numpy()
+        err = self._err.cpu().numpy()
+        return self.finish(driver, pair, status, err)
+
+    def status_tensors(self):
+        """Device tensors whose host copies ``finish`` consumes."""
+        return self._status, self._err
+
+    def plan_device(self, driver: RefineDriver):
+        """Every kernel of the pass that does not depend on its outcome: seeds,
+        desired / current / effective coverage, plan and no-op flags
+        (status[0:L]) and the invariants of the current topology
+        (status[L:L+3]).  No host synchronisation (CUDA-graph capturable)."""
         topo = self.topology
         lib = L.lib()
         s = L.stream_handle()
         Lv = topo.levels
-        rep = AdaptReport(created=[0] * Lv, deleted=[0] * Lv)
         self._status.zero_()
-        # seeds -> des[0]
-        seeds = self._tmp[0]
+        seeds = self._seeds
         seeds.zero_()
         x = driver.device_positions(topo.d, topo.device)
         if x is not None and x.shape[1]:
@@ -181,8 +195,7 @@ class GridAdaptor:
         if Lv == 1:
             des[0].fill_(1)
         else:
-            seeds_c = seeds.clone()
-            self._op(0, 0, seeds_c, des[0])
+            self._op(0, 0, seeds, des[0])
             for l in range(1, Lv):
                 self._parents_into(l - 1, des[l - 1], self._par[l])
                 if l == Lv - 1:
@@ -190,13 +203,11 @@ class GridAdaptor:
                 else:
                     self._dilate(l, self._par[l], self._guard[l])
                     self._op(0, l, self._guard[l], des[l])
-        # current cumulative
         for l in range(Lv):
             self._op(6, l, topo.lv[l].kind, cur[l])
             if l > 0:
                 self._parents_into(l - 1, cur[l - 1], self._par[l])
                 self._op(2, l, self._par[l], cur[l])
-        # effective (hysteresis)
         for l in range(Lv):
             guard = par = None
             if l > 0:
@@ -210,7 +221,6 @@ class GridAdaptor:
             self.launches += 1
         if Lv > 1:
             eff[Lv - 1].fill_(1)
-        # storage plan + no-op test
         for l in range(Lv):
             self._op(4, l, eff[l], self._own[l])
             if l > 0:
@@ -222,16 +232,25 @@ class GridAdaptor:
                                         L.ptr(self._new[l]), L.ptr(self._status[l:l + 1]), s),
                     "plan_level")
             self.launches += 1
-        status = self._status.cpu().numpy()
-        err = self._err.cpu().numpy()
+        self._invariants_device(driver)
+
+    def finish(self, driver, pair, status, err) -> AdaptReport:
+        """Host half: raise on seed errors, rebuild + migrate if a level
+        changed (then re-check the invariants), build the report."""
+        topo = self.topology
+        Lv = topo.levels
+        rep = AdaptReport(created=[0] * Lv, deleted=[0] * Lv)
         if err[0]:
             self._err.zero_()
             raise ValueError("particle outside the domain bounding box")
         changed = [l for l in range(Lv) if status[l]]
+        viol = status[Lv:Lv + 3]
         if changed:
             rep.noop = False
             self._apply(changed, pair, rep)
-        self._check_invariants(driver, rep)
+            self._invariants_device(driver)
+            viol = self._status[Lv:Lv + 3].cpu().numpy()
+        self._report_invariants(viol, rep)
         return rep
 
     def _apply(self, changed, pair, rep):
@@ -274,9 +293,9 @@ class GridAdaptor:
             rep.violations.append(("uninitialized cell", nv))
         del keep
 
-    def _check_invariants(self, driver, rep):
+    def _invariants_device(self, driver):
         """Coverage, two-tile rings, particles in level-0 leaves
-        (adapt.py:374-389); reported, not raised."""
+        (adapt.py:374-389) -> status[L:L+3]; reported, not raised."""
         topo = self.topology
         lib = L.lib()
         s = L.stream_handle()
@@ -295,7 +314,9 @@ class GridAdaptor:
             L.check(lib.mlbm_check_particles(topo.d, x.shape[1], L.ptr(x), x.stride(0), 1,
                                              _i3(self._grids[0]), L.ptr(topo.lv[0].kind),
                                              L.ptr(v), s), "check_particles")
-        cnt = v.cpu().numpy()
+
+    @staticmethod
+    def _report_invariants(cnt, rep):
         if cnt[0]:
             rep.violations.append(("invariant", f"leaf coverage violated at {cnt[0]} tiles"))
         if cnt[1]:

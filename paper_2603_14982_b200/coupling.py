@@ -15,7 +15,10 @@ One finest cycle (CoupledSim.step, coupling.py:448-481) issues:
   block maintenance                        GridAdaptor.update (adapt.py)
   diagnostics                              mlbm_diag_level / mlbm_diag_particles
 
-Diagnostics rows accumulate on the device and are materialised lazily.
+By default the whole step is replayed as a CUDA graph (one per cycle /
+buffer-parity key, recaptured after each topology change) followed by ONE
+device->host copy of the error records, adapt flags and diagnostics row; the
+host only runs the rebuild when a level's tile set changed.
 """
 from __future__ import annotations
 
@@ -148,11 +151,21 @@ class CoupledSim:
         self.threads = 1
         self.clamped_particles = 0
         self.last_fields = None
-        self._diag = []            # device rows, materialised lazily
         self._diag_rows = []
         self._counters = torch.zeros(2, dtype=torch.int32, device=self.topology.device)
         self._tmp = None
         self.last_report = None
+        self._diag_buf = torch.zeros(2 * self.d + 4, dtype=torch.float64,
+                                     device=self.topology.device)
+        # CUDA-graph step: one graph per (cycle, buffer parities,
+        # exchange kind), recaptured after every topology change
+        self.use_graphs = True
+        self._graphs = {}
+        self._graph_ver = None
+        self._pool = None
+        self.graph_replays = 0
+        self.graph_captures = 0
+        self.topology_changes = 0
         if self.drag_params.d_p is None and len(self.particles):
             self.drag_params.d_p = float(particle_diameter(float(self.particles.V0.double().mean()),
                                                            self.d))
@@ -209,8 +222,20 @@ class CoupledSim:
         """One finest cycle of the coupled pipeline (coupling.py:448-481)."""
         solver = self.solver
         schedule = solver._schedule
-        cycle = schedule[solver.k[0] % len(schedule)]
+        ci = solver.k[0] % len(schedule)
         is_mpm = self.coupling_active and (self.step_count % self.cadence == 0)
+        adapt_now = self.adaptor is not None and self.coupling_active and \
+            self.step_count % self.cadence == 0
+        if self.use_graphs and torch.cuda.is_available():
+            self._step_graph(ci, is_mpm, adapt_now)
+        else:
+            self._step_eager(ci, is_mpm, adapt_now)
+        self.step_count += 1
+
+    # -- eager path (host checks after every phase) --------------------------------
+    def _step_eager(self, ci, is_mpm, adapt_now):
+        solver = self.solver
+        cycle = solver._schedule[ci]
         if is_mpm:
             solver.run_cycle(cycle, hook=self._exchange)
         elif self.coupling_active:
@@ -221,14 +246,136 @@ class CoupledSim:
             self.grid.raise_pending()
         if self.powder is not None:
             self._powder_cycle(is_mpm)
-        if self.adaptor is not None and self.coupling_active and \
-                self.step_count % self.cadence == 0:
-            driver = RefineDriver(positions_soa=self.particles.xd,
-                                  static_tiles=self.static_tiles, levels=self.topology.levels)
+        if adapt_now:
+            driver = self._driver()
             self.last_report = self.adaptor.update(driver, self.pair)
+            if not self.last_report.noop:
+                self.topology_changes += 1
             self.grid.sync_topology()
-        self.step_count += 1
         self._record_diagnostics()
+        self._push_diag_row(self._diag_buf.cpu().numpy())
+
+    def _driver(self):
+        return RefineDriver(positions_soa=self.particles.xd, static_tiles=self.static_tiles,
+                            levels=self.topology.levels)
+
+    # -- graph path: all kernels of the step replayed as one CUDA graph, one
+    #    device->host status copy, host work only when the topology changes --
+    def _device_step(self, ci, is_mpm, adapt_now):
+        solver = self.solver
+        cycle = solver._schedule[ci]
+        check = solver.check_errors
+        solver.check_errors = False
+        try:
+            if is_mpm:
+                solver.run_cycle(cycle, hook=self._exchange)
+            elif self.coupling_active:
+                solver.run_cycle(cycle, hook=self._held)
+            else:
+                solver.run_cycle(cycle)
+        finally:
+            solver.check_errors = check
+        if self.powder is not None:
+            self._powder_cycle(is_mpm)
+        if adapt_now:
+            self.adaptor.plan_device(self._driver())
+        self._record_diagnostics()
+        parts = self._status_sources(adapt_now)
+        off = 0
+        for t in parts:
+            n = t.numel()
+            self._host_status[off:off + n].copy_(t.to(torch.float64) if t.dtype != torch.float64
+                                                 else t, non_blocking=True)
+            off += n
+
+    def _status_sources(self, adapt_now):
+        parts = [self.solver._err, self.grid._err, self._diag_buf, self._counters]
+        if adapt_now:
+            st, er = self.adaptor.status_tensors()
+            parts += [st, er]
+        return parts
+
+    def _ensure_host_status(self, adapt_now):
+        n = sum(t.numel() for t in self._status_sources(adapt_now))
+        if getattr(self, "_host_status", None) is None or self._host_status.numel() < n:
+            self._host_status = torch.zeros(n, dtype=torch.float64).pin_memory()
+
+    def _step_graph(self, ci, is_mpm, adapt_now):
+        solver = self.solver
+        topo = self.topology
+        if self._graph_ver != topo.version:
+            self._graphs.clear()
+            self._graph_ver = topo.version
+        # refresh host-side tables / rasters before capture (may sync)
+        solver._refresh_tables()
+        self.grid.sync_topology()
+        self.grid.level0()
+        self._ensure_host_status(adapt_now)
+        key = (ci, tuple(k & 1 for k in solver.k), is_mpm, adapt_now,
+               self.powder is not None and is_mpm and self.last_fields is not None)
+        entry = self._graphs.get(key)
+        if entry is None:
+            if self._pool is None:
+                self._pool = torch.cuda.graph_pool_handle()
+            k0, b0 = list(solver.k), self.pair.bounce
+            g = torch.cuda.CUDAGraph()
+            torch.cuda.synchronize()
+            n0 = L.TRACE.launches
+            tracing = L.TRACE.enabled
+            L.TRACE.enabled = False
+            try:
+                with torch.cuda.graph(g, pool=self._pool):
+                    self._device_step(ci, is_mpm, adapt_now)
+            finally:
+                L.TRACE.enabled = tracing
+            nk = L.TRACE.launches - n0
+            L.TRACE.launches = n0          # captured, not executed
+            dk = [a - b for a, b in zip(solver.k, k0)]
+            db = self.pair.bounce - b0
+            solver.k[:] = k0
+            self.pair.bounce = b0
+            entry = (g, dk, db, self.last_fields, nk)
+            self._graphs[key] = entry
+            self.graph_captures += 1
+        g, dk, db, lf, nk = entry
+        g.replay()
+        L.TRACE.launches += nk
+        self.graph_replays += 1
+        for l, v in enumerate(dk):
+            solver.k[l] += v
+        self.pair.bounce += db
+        if is_mpm:
+            self.last_fields = lf
+        torch.cuda.current_stream().synchronize()
+        self._finish_graph_step(adapt_now)
+
+    def _finish_graph_step(self, adapt_now):
+        h = self._host_status.numpy()
+        ne = L.ERR_INTS
+        serr, gerr = h[:ne].astype(np.int64), h[ne:2 * ne].astype(np.int64)
+        off = 2 * ne
+        nd = self._diag_buf.numel()
+        diag = h[off:off + nd].copy()
+        off += nd + self._counters.numel()
+        if serr[0]:
+            self.solver._err.copy_(torch.as_tensor(serr, dtype=torch.int32))
+            self.solver.raise_pending()
+        if gerr[0]:
+            self.grid._err.copy_(torch.as_tensor(gerr, dtype=torch.int32))
+            self.grid.raise_pending()
+        if adapt_now:
+            st, er = self.adaptor.status_tensors()
+            status = h[off:off + st.numel()].astype(np.int64)
+            off += st.numel()
+            err = h[off:off + er.numel()].astype(np.int64)
+            self.last_report = self.adaptor.finish(self._driver(), self.pair, status, err)
+            if not self.last_report.noop:
+                self.topology_changes += 1
+                self.grid.sync_topology()
+                self.solver._refresh_tables()
+                self._record_diagnostics()
+                diag = self._diag_buf.cpu().numpy()
+        self._push_diag_row(diag)
 
     def _powder_cycle(self, is_mpm):
         solver = self.solver
@@ -262,12 +409,14 @@ class CoupledSim:
 
     # -- diagnostics -------------------------------------------------------------------
     def _record_diagnostics(self):
+        """Device reductions of coupling.py:500-531 into a persistent buffer."""
         solver = self.solver
         d = self.d
         lib = L.lib()
         s = L.stream_handle()
         dcode = dtype_code(self.dtype)
-        out = torch.zeros(2 * d + 4, dtype=torch.float64, device=self.topology.device)
+        out = self._diag_buf
+        out.zero_()
         out[d + 1] = 1.0
         for l in range(self.topology.levels):
             if not self.topology.n_tiles(l):
@@ -283,29 +432,29 @@ class CoupledSim:
         L.check(lib.mlbm_diag_particles(d, len(p), L.ptr(p.pd), p.pd.stride(0), L.ptr(g.ras),
                                         g.ras.stride(0), n0, dcode, L.ptr(out[d + 2:]), s),
                 "diag_particles")
-        self._diag.append((self.step_count, tuple(self.topology.n_tiles(l)
-                                                  for l in range(self.topology.levels)), out))
+
+    def _push_diag_row(self, o):
+        d = self.d
+        step = self.step_count + 1
+        self._diag_rows.append(DiagRow(
+            step=step, t_phys=step * self.unit_scale.dt,
+            fluid_mom=tuple(float(v) for v in o[:d]),
+            sediment_mom=tuple(float(v) for v in o[d + 2:2 * d + 2]),
+            drag_impulse=tuple(float(-v) for v in o[2 * d + 2:3 * d + 2]),
+            sum_phi=float(o[d]),
+            tiles=tuple(self.topology.n_tiles(l) for l in range(self.topology.levels)),
+            eps_min=float(o[d + 1])))
 
     @property
     def diagnostics(self):
-        d = self.d
-        while self._diag:
-            step, tiles, out = self._diag.pop(0)
-            o = out.cpu().numpy()
-            self._diag_rows.append(DiagRow(
-                step=step, t_phys=step * self.unit_scale.dt,
-                fluid_mom=tuple(float(v) for v in o[:d]),
-                sediment_mom=tuple(float(v) for v in o[d + 2:2 * d + 2]),
-                drag_impulse=tuple(float(-v) for v in o[2 * d + 2:3 * d + 2])
-                if len(o) >= 3 * d + 2 else (0.0,) * d,
-                sum_phi=float(o[d]), tiles=tiles, eps_min=float(o[d + 1])))
         return self._diag_rows
 
     def fluid_momentum(self):
         rows = self.diagnostics
         if not rows:
             self._record_diagnostics()
-            return np.array(self.diagnostics.pop().fluid_mom)
+            o = self._diag_buf.cpu().numpy()
+            return np.array(o[:self.d])
         return np.array(rows[-1].fluid_mom)
 
     @property
