@@ -245,7 +245,18 @@ int mlbm_particle_rows(int32_t dim);
  * p: run-dtype particle rows [rows][ps]; ras: zeroed accumulator rows. */
 int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, void* p, int64_t ps,
              double lam, double mu, double alpha, void* ras, int64_t rs, int32_t dtype,
-             mlbm_error_t* err, void* stream);
+             int32_t smem, mlbm_error_t* err, void* stream);
+
+/* MPM particle sort (no reference counterpart — ordering only, SURVEY.md
+ * §2.3 K7): radix-sort by (level-0 tile slot, cell) of the stencil base cell
+ * and gather every particle row (positions, state rows, ids) into the _out
+ * buffers.  smem != 0 in mlbm_p2g then accumulates per block in shared
+ * memory over the block's bounding box. */
+int64_t mlbm_sort_ws_bytes(int64_t n);
+int mlbm_particle_sort(const mlbm_level_t* lv0, int32_t n, const double* x, const void* p,
+                       const int32_t* pid, int64_t ps, double* x_out, void* p_out,
+                       int32_t* pid_out, int32_t dtype, void* ws, int64_t ws_bytes,
+                       void* stream);
 
 /* per level-0 cell: eps, Di Felice drag + limiter, grad eps, mixture force
  * (written into both trees), MPM grid update with wall / sticky projection
@@ -259,11 +270,13 @@ int mlbm_exchange(const mlbm_level_t* lv0, mlbm_fields_t w_tree, mlbm_fields_t r
                   int32_t dtype, void* stream);
 
 /* gather, advect (wrap / clamp to [2, dim-2]), F update, SVD + Drucker-Prager
- * (granular.py:344-412). clamped[0] += clamped coordinates; clamped[1] |= CFL
+ * (granular.py:344-412), reading the (sorted) _in rows and writing the _out rows
+ * (in place when they alias). clamped[0] += clamped coordinates; clamped[1] |= CFL
  * violation (max |v| dt >= 0.5, granular.py:428-432). */
-int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, double* x, void* p, int64_t ps,
-             double lam, double mu, double alpha, const void* ras, int64_t rs, double dt,
-             int32_t plastic, int32_t dtype, int32_t* clamped, mlbm_error_t* err,
+int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, const double* x_in, double* x_out,
+             const void* p_in, void* p_out, const int32_t* pid_in, int32_t* pid_out,
+             int64_t ps, double lam, double mu, double alpha, const void* ras, int64_t rs,
+             double dt, int32_t plastic, int32_t dtype, int32_t* clamped, mlbm_error_t* err,
              void* stream);
 
 /* entrainment stress raster (coupling.py:283-294) and powder transport

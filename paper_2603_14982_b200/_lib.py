@@ -139,11 +139,13 @@ _SIGS = {
                             Fields, Fields, P, I32, I32, P, P],
     "mlbm_raster_rows": [I32],
     "mlbm_particle_rows": [I32],
-    "mlbm_p2g": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64, I32, P, P],
+    "mlbm_p2g": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64, I32, I32, P, P],
+    "mlbm_sort_ws_bytes": [I64],
+    "mlbm_particle_sort": [C.POINTER(Level), I32, P, P, P, I64, P, P, P, I32, P, I64, P],
     "mlbm_exchange": [C.POINTER(Level), Fields, Fields, Fields, Fields, P, I64,
                       D, D, D, D, D, D, P, P, P, D, I32, I32, P],
-    "mlbm_g2p": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64, D, I32, I32,
-                 P, P, P],
+    "mlbm_g2p": [C.POINTER(Level), I32, P, P, P, P, P, P, I64, D, D, D, P, I64, D, I32,
+                 I32, P, P, P],
     "mlbm_stress_raster": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64,
                            I32, P, P],
     "mlbm_powder": [C.POINTER(Level), Fields, Fields, P, I64, P, D, D, D, D, D,
@@ -151,7 +153,7 @@ _SIGS = {
     "mlbm_diag_level": [C.POINTER(Level), Fields, D, I32, P, P],
     "mlbm_diag_particles": [I32, I32, P, I64, P, I64, I64, I32, P, P],
 }
-_RET64 = {"mlbm_ws_bytes"}
+_RET64 = {"mlbm_ws_bytes", "mlbm_sort_ws_bytes"}
 
 _LIB = None
 

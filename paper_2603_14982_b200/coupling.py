@@ -160,6 +160,7 @@ class CoupledSim:
         # CUDA-graph step: one graph per (cycle, buffer parities,
         # exchange kind), recaptured after every topology change
         self.use_graphs = True
+        self.sort_particles = True
         self._graphs = {}
         self._graph_ver = None
         self._pool = None
@@ -192,9 +193,20 @@ class CoupledSim:
         mat = self.material
         lv0 = grid.level0()
         grid.clear()
-        L.check(lib.mlbm_p2g(L.C.byref(lv0), len(p), L.ptr(p.xd), L.ptr(p.pd), p.pd.stride(0),
+        n = len(p)
+        ps = p.pd.stride(0)
+        if self.sort_particles and n:
+            xa, pa, ida, ws = p.scratch()
+            L.check(lib.mlbm_particle_sort(L.C.byref(lv0), n, L.ptr(p.xd), L.ptr(p.pd),
+                                           L.ptr(p.pid), ps, L.ptr(xa), L.ptr(pa), L.ptr(ida),
+                                           dcode, L.ptr(ws), ws.numel(), s), "particle_sort")
+            src_x, src_p, src_id, smem = xa, pa, ida, 1
+            p.permuted = True
+        else:
+            src_x, src_p, src_id, smem = p.xd, p.pd, None, 0
+        L.check(lib.mlbm_p2g(L.C.byref(lv0), n, L.ptr(src_x), L.ptr(src_p), ps,
                              mat.lam, mat.mu, mat.alpha, L.ptr(grid.ras), grid.ras.stride(0),
-                             dcode, L.ptr(grid._err), s), "p2g")
+                             dcode, smem, L.ptr(grid._err), s), "p2g")
         sp = solver.params
         L.check(lib.mlbm_exchange(L.C.byref(lv0), L.fields(solver.arrays(w, 0).data),
                                   L.fields(solver.arrays(r, 0).data),
@@ -206,10 +218,11 @@ class CoupledSim:
                                   float(self.cadence), float(sp.rho0), _d3(sp.gravity, self.d),
                                   _d3(self.sediment_gravity, self.d), _faces(solver.boundaries),
                                   float(mat.floor_friction), 1, dcode, s), "exchange")
-        L.check(lib.mlbm_g2p(L.C.byref(lv0), len(p), L.ptr(p.xd), L.ptr(p.pd), p.pd.stride(0),
-                             mat.lam, mat.mu, mat.alpha, L.ptr(grid.ras), grid.ras.stride(0),
-                             float(self.cadence), 1, dcode, L.ptr(self._counters), L.ptr(grid._err),
-                             s), "g2p")
+        L.check(lib.mlbm_g2p(L.C.byref(lv0), n, L.ptr(src_x), L.ptr(p.xd), L.ptr(src_p),
+                             L.ptr(p.pd), L.ptr(src_id), L.ptr(p.pid) if src_id is not None else
+                             L.ptr(None), ps, mat.lam, mat.mu, mat.alpha, L.ptr(grid.ras),
+                             grid.ras.stride(0), float(self.cadence), 1, dcode,
+                             L.ptr(self._counters), L.ptr(grid._err), s), "g2p")
         solver.launches += 3
         self.last_fields = CouplingFields(grid, self.pair.trees[0].levels[0])
         return FIELD_FORCE, FIELD_TAU
@@ -417,7 +430,7 @@ class CoupledSim:
         dcode = dtype_code(self.dtype)
         out = self._diag_buf
         out.zero_()
-        out[d + 1] = 1.0
+        out[d + 1:d + 2].fill_(1.0)
         for l in range(self.topology.levels):
             if not self.topology.n_tiles(l):
                 continue

@@ -15,6 +15,7 @@
 //
 // Particle positions are always float64 (sub-cell offsets at x ~ 1e3 need
 // ~1e-8 absolute resolution); everything else follows the run dtype.
+#include <cub/cub.cuh>
 #include "common.cuh"
 
 namespace mlbm {
@@ -221,6 +222,9 @@ struct PartArgs {
     double* xw;          // writable positions (g2p)
     void* p;             // [PRows::N][n] of R
     int64_t ps;          // stride of p and x
+    void* pw;            // g2p output rows (may alias p)
+    const int32_t* pid;  // g2p: particle ids in / out (may be null)
+    int32_t* pidw;
 };
 
 template <typename R> __device__ __forceinline__ void aadd(R* a, R v) { atomicAdd(a, v); }
@@ -438,7 +442,8 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
     using PR = PRows<D>;
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= P.n) return;
-    R* pp = (R*)P.p;
+    const R* pp = (const R*)P.p;
+    R* pw = (R*)P.pw;
     double x[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) x[a] = P.x[a * P.ps + p];
@@ -488,7 +493,7 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
             xn = xn < 2.0 ? 2.0 : (xn > dim - 2.0 ? dim - 2.0 : xn);
         }
         P.xw[a * P.ps + p] = xn;
-        pp[(PR::V + a) * P.ps + p] = v[a];
+        pw[(PR::V + a) * P.ps + p] = v[a];
     }
     if (ncl) atomicAdd(clamped, ncl);
     {
@@ -499,7 +504,7 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
     }
     R F[D * D], Fn[D * D];
 #pragma unroll
-    for (int k = 0; k < D * D; ++k) { F[k] = pp[(PR::F + k) * P.ps + p]; pp[(PR::C + k) * P.ps + p] = C[k]; }
+    for (int k = 0; k < D * D; ++k) { F[k] = pp[(PR::F + k) * P.ps + p]; pw[(PR::C + k) * P.ps + p] = C[k]; }
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
@@ -540,7 +545,7 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
         R sum = R(0), se[D];
 #pragma unroll
         for (int a = 0; a < D; ++a) { sum += en[a]; se[a] = exp(en[a]); }
-        pp[PR::VC * P.ps + p] = tr - sum;
+        pw[PR::VC * P.ps + p] = tr - sum;
 #pragma unroll
         for (int i = 0; i < D; ++i)
 #pragma unroll
@@ -552,7 +557,13 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
             }
     }
 #pragma unroll
-    for (int k = 0; k < D * D; ++k) pp[(PR::F + k) * P.ps + p] = Fn[k];
+    for (int k = 0; k < D * D; ++k) pw[(PR::F + k) * P.ps + p] = Fn[k];
+    if (pw != pp) {
+        if (!plastic) pw[PR::VC * P.ps + p] = pp[PR::VC * P.ps + p];
+        pw[PR::M * P.ps + p] = pp[PR::M * P.ps + p];
+        pw[PR::V0 * P.ps + p] = pp[PR::V0 * P.ps + p];
+    }
+    if (P.pidw) P.pidw[p] = P.pid[p];
 }
 
 // ---------------------------------------------------------------------------
@@ -751,6 +762,160 @@ __global__ void k_diag_particles(PartArgs P, const R* ras, int64_t rs, int64_t n
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// particle sort by (level-0 tile slot, cell) of the stencil base cell
+template <int D>
+__global__ void k_sort_keys(int n, const double* x, int64_t ps, TopoL0 t0, uint32_t* keys, int32_t* vals) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int c[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) {
+        int b = (int)floor(x[a * ps + p] - 0.5);
+        if (t0.periodic[a]) b = ((b % t0.cells[a]) + t0.cells[a]) % t0.cells[a];
+        else b = b < 0 ? 0 : (b >= t0.cells[a] ? t0.cells[a] - 1 : b);
+        c[a] = b;
+    }
+    const int s = t0.tile_map[g3(t0.tiles, c[0] >> 2, c[1] >> 2, D == 3 ? c[2] >> 2 : 0)];
+    keys[p] = s < 0 ? 0xffffffffu : (uint32_t)s * Geo<D>::T + local_of<D>(c[0] & 3, c[1] & 3, c[2] & 3);
+    vals[p] = p;
+}
+
+template <typename R>
+__global__ void k_gather_particles(int n, int nrows, const int32_t* perm, const double* x, int dim,
+                                   const R* pdat, const int32_t* pid, int64_t ps, double* xo, R* po,
+                                   int32_t* pido) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int j = perm[i];
+    for (int a = 0; a < dim; ++a) xo[a * ps + i] = x[a * ps + j];
+    for (int r = 0; r < nrows; ++r) po[r * ps + i] = pdat[r * ps + j];
+    pido[i] = pid[j];
+}
+
+// P2G with per-block shared-memory accumulation over the bounding box of
+// the block's (sorted) particles; blocks whose box does not fit fall back to
+// global atomics.  Same arithmetic per contribution as k_p2g.
+template <int D, typename R> struct P2GSmem {
+    static constexpr int NV = 3 + 3 * D;                        // mass, mom, fint, eta, area, vmom
+    static constexpr int MAXN = sizeof(R) == 4 ? 512 : 256;
+};
+
+template <int D, typename R>
+__global__ void __launch_bounds__(256) k_p2g_smem(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int64_t rs,
+                                                  mlbm_error_t* err) {
+    constexpr int K = Geo<D>::K;
+    constexpr int NV = P2GSmem<D, R>::NV, MAXN = P2GSmem<D, R>::MAXN;
+    using RW = Rows<D>;
+    using PR = PRows<D>;
+    __shared__ R acc[NV * MAXN];
+    __shared__ int s_lo[3], s_hi[3];
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = p < P.n;
+    const R* pp = (const R*)P.p;
+    double x[D];
+    Stencil<D, R> st;
+    if (valid) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) x[a] = P.x[a * P.ps + p];
+        make_stencil<D, R>(x, st);
+    }
+    if (threadIdx.x < 3) { s_lo[threadIdx.x] = 0x7fffffff; s_hi[threadIdx.x] = -0x7fffffff; }
+    __syncthreads();
+    if (valid) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) { atomicMin(&s_lo[a], st.base[a]); atomicMax(&s_hi[a], st.base[a] + 2); }
+    }
+    __syncthreads();
+    int ext[3] = {1, 1, 1}, lo[3] = {0, 0, 0};
+    int nbox = 1;
+#pragma unroll
+    for (int a = 0; a < D; ++a) { lo[a] = s_lo[a]; ext[a] = s_hi[a] - s_lo[a] + 1; nbox *= ext[a]; }
+    const bool use_smem = nbox <= MAXN && nbox > 0;
+    if (use_smem) {
+        for (int i = threadIdx.x; i < NV * nbox; i += blockDim.x) acc[(i / nbox) * MAXN + i % nbox] = R(0);
+    }
+    __syncthreads();
+    if (valid) {
+        R v[D], C[D * D], F[D * D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) v[a] = pp[(PR::V + a) * P.ps + p];
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) { C[k] = pp[(PR::C + k) * P.ps + p]; F[k] = pp[(PR::F + k) * P.ps + p]; }
+        const R m = pp[PR::M * P.ps + p], V0 = pp[PR::V0 * P.ps + p];
+        R tau[D * D];
+        kirchhoff<D, R>(F, mp, tau);
+        const R ap = D == 2 ? R(2) * sqrt(V0 / R(3.14159265358979323846))
+                            : R(3.14159265358979323846) * pow(R(3) * V0 / (R(4) * R(3.14159265358979323846)), R(2.0 / 3.0));
+        bool bad = false;
+#pragma unroll 1
+        for (int k = 0; k < K; ++k) {
+            const int o[3] = {k % 3, (k / 3) % 3, k / 9};
+            R w = R(1), gr[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) { w *= st.w[a][o[a]]; gr[a] = R(1); }
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int b = 0; b < D; ++b) gr[b] *= (a == b) ? st.dw[a][o[a]] : st.w[a][o[a]];
+            R dpos[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) dpos[a] = R((double)(st.base[a] + o[a]) - x[a]);
+            const R wm = w * m;
+            R val[NV];
+            val[0] = wm;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                R aff = v[a];
+#pragma unroll
+                for (int b = 0; b < D; ++b) aff += C[a * D + b] * dpos[b];
+                val[1 + a] = wm * aff;
+                R fa = R(0);
+#pragma unroll
+                for (int b = 0; b < D; ++b) fa += V0 * tau[a * D + b] * gr[b];
+                val[1 + D + a] = -fa;
+                val[3 + 2 * D + a] = wm * v[a];
+            }
+            val[1 + 2 * D] = w * V0;
+            val[2 + 2 * D] = w * ap;
+            if (use_smem) {
+                int li = 0;
+#pragma unroll
+                for (int a = D - 1; a >= 0; --a) li = li * ext[a] + (st.base[a] + o[a] - lo[a]);
+#pragma unroll
+                for (int q = 0; q < NV; ++q) atomicAdd(&acc[q * MAXN + li], val[q]);
+            } else {
+                int c[3] = {st.base[0] + o[0], st.base[1] + o[1], D == 3 ? st.base[2] + o[2] : 0};
+                const int64_t ni = node_index<D>(t0, c, bad);
+                if (ni < 0) continue;
+                // row order of the raster: mass, mom, fint, eta, area, vmom
+#pragma unroll
+                for (int q = 0; q < NV; ++q) aadd(&ras[q * rs + ni], val[q]);
+            }
+        }
+        if (bad) report_error(err, MLBM_ERR_STENCIL, 0, st.base[0], st.base[1], st.base[2]);
+    }
+    if (!use_smem) return;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nbox; i += blockDim.x) {
+        if (acc[i] == R(0) && acc[(2 * D + 2) * MAXN + i] == R(0)) {
+            // no mass and no area landed here: every row is zero
+            continue;
+        }
+        int c[3] = {0, 0, 0};
+        int r = i;
+#pragma unroll
+        for (int a = 0; a < D; ++a) { c[a] = lo[a] + r % ext[a]; r /= ext[a]; }
+        bool bad = false;
+        const int64_t ni = node_index<D>(t0, c, bad);
+        if (ni < 0) { report_error(err, MLBM_ERR_STENCIL, 0, c[0], c[1], c[2]); continue; }
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const R vq = acc[q * MAXN + i];
+            if (vq != R(0)) aadd(&ras[q * rs + ni], vq);
+        }
+    }
+}
 }  // namespace mlbm
 
 using namespace mlbm;
@@ -768,17 +933,55 @@ extern "C" int mlbm_particle_rows(int32_t dim) { return dim == 2 ? PRows<2>::N :
 
 extern "C" int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, void* p, int64_t ps,
                         double lam, double mu, double alpha, void* ras, int64_t rs, int32_t dtype,
-                        mlbm_error_t* err, void* stream) {
+                        int32_t smem, mlbm_error_t* err, void* stream) {
     if (n <= 0) return 0;
     cudaStream_t s = as_stream(stream);
-    PartArgs P{lv0->dim, n, x, nullptr, p, ps};
+    PartArgs P{lv0->dim, n, x, nullptr, p, ps, nullptr, nullptr, nullptr};
     MatParams mp{lam, mu, alpha, 0.0};
     const TopoL0 t = topo0(lv0);
-#define P2G(D, R) k_p2g<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err)
+#define P2G(D, R) do { if (smem) k_p2g_smem<D, R><<<nblk(n, 256), 256, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
+                       else k_p2g<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err); } while (0)
     if (lv0->dim == 2) { if (dtype) P2G(2, double); else P2G(2, float); }
     else { if (dtype) P2G(3, double); else P2G(3, float); }
 #undef P2G
     return launch_status(1);
+}
+
+extern "C" int64_t mlbm_sort_ws_bytes(int64_t n) {
+    if (n < 1) n = 1;
+    size_t b = 0;
+    uint32_t* k = nullptr;
+    int32_t* v = nullptr;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, k, k, v, v, (int)n);
+    auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
+    return 4 * al(4 * n) + al((int64_t)b);
+}
+
+extern "C" int mlbm_particle_sort(const mlbm_level_t* lv0, int32_t n, const double* x, const void* p,
+                                  const int32_t* pid, int64_t ps, double* x_out, void* p_out,
+                                  int32_t* pid_out, int32_t dtype, void* ws, int64_t ws_bytes,
+                                  void* stream) {
+    if (n <= 0) return 0;
+    if (ws_bytes < mlbm_sort_ws_bytes(n)) return -1;
+    auto al = [](int64_t v) { return (v + 255) & ~(int64_t)255; };
+    char* w = (char*)ws;
+    uint32_t* k0 = (uint32_t*)w;
+    uint32_t* k1 = (uint32_t*)(w + al(4 * (int64_t)n));
+    int32_t* v0 = (int32_t*)(w + 2 * al(4 * (int64_t)n));
+    int32_t* v1 = (int32_t*)(w + 3 * al(4 * (int64_t)n));
+    void* tmp = w + 4 * al(4 * (int64_t)n);
+    size_t tb = (size_t)(ws_bytes - 4 * al(4 * (int64_t)n));
+    cudaStream_t s = as_stream(stream);
+    const TopoL0 t = topo0(lv0);
+    int bits = 1;
+    while (bits < 32 && ((int64_t)1 << bits) <= (int64_t)lv0->n_tiles * (lv0->dim == 2 ? 16 : 64)) ++bits;
+    if (lv0->dim == 2) k_sort_keys<2><<<nblk(n, 256), 256, 0, s>>>(n, x, ps, t, k0, v0);
+    else k_sort_keys<3><<<nblk(n, 256), 256, 0, s>>>(n, x, ps, t, k0, v0);
+    cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, v1, n, 0, bits < 32 ? bits + 1 : 32, s);
+    const int rows = lv0->dim == 2 ? PRows<2>::N : PRows<3>::N;
+    if (dtype) k_gather_particles<double><<<nblk(n, 256), 256, 0, s>>>(n, rows, v1, x, lv0->dim, (const double*)p, pid, ps, x_out, (double*)p_out, pid_out);
+    else k_gather_particles<float><<<nblk(n, 256), 256, 0, s>>>(n, rows, v1, x, lv0->dim, (const float*)p, pid, ps, x_out, (float*)p_out, pid_out);
+    return launch_status(5);
 }
 
 extern "C" int mlbm_exchange(const mlbm_level_t* lv0, mlbm_fields_t w_tree, mlbm_fields_t r_tree,
@@ -806,13 +1009,14 @@ extern "C" int mlbm_exchange(const mlbm_level_t* lv0, mlbm_fields_t w_tree, mlbm
     return launch_status(1);
 }
 
-extern "C" int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, double* x, void* p, int64_t ps,
-                        double lam, double mu, double alpha, const void* ras, int64_t rs, double dt,
-                        int32_t plastic, int32_t dtype, int32_t* clamped, mlbm_error_t* err,
-                        void* stream) {
+extern "C" int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, const double* x_in, double* x_out,
+                        const void* p_in, void* p_out, const int32_t* pid_in, int32_t* pid_out,
+                        int64_t ps, double lam, double mu, double alpha, const void* ras, int64_t rs,
+                        double dt, int32_t plastic, int32_t dtype, int32_t* clamped,
+                        mlbm_error_t* err, void* stream) {
     if (n <= 0) return 0;
     cudaStream_t s = as_stream(stream);
-    PartArgs P{lv0->dim, n, x, x, p, ps};
+    PartArgs P{lv0->dim, n, x_in, x_out, (void*)p_in, ps, p_out, pid_in, pid_in ? pid_out : nullptr};
     MatParams mp{lam, mu, alpha, 0.0};
     const TopoL0 t = topo0(lv0);
 #define G2P(D, R) k_g2p<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (const R*)ras, rs, dt, plastic, clamped, err)
@@ -827,7 +1031,7 @@ extern "C" int mlbm_stress_raster(const mlbm_level_t* lv0, int32_t n, const doub
                                   int32_t dtype, mlbm_error_t* err, void* stream) {
     if (n <= 0) return 0;
     cudaStream_t s = as_stream(stream);
-    PartArgs P{lv0->dim, n, x, nullptr, (void*)p, ps};
+    PartArgs P{lv0->dim, n, x, nullptr, (void*)p, ps, nullptr, nullptr, nullptr};
     MatParams mp{lam, mu, alpha, 0.0};
     const TopoL0 t = topo0(lv0);
 #define SR(D, R) k_stress_raster<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err)
@@ -871,7 +1075,7 @@ extern "C" int mlbm_diag_particles(int32_t dim, int32_t n, const void* p, int64_
                                    int64_t rs, int64_t n0, int32_t dtype, double* out, void* stream) {
     const int64_t m = n > n0 ? n : n0;
     if (m == 0) return 0;
-    PartArgs P{dim, n, nullptr, nullptr, (void*)p, ps};
+    PartArgs P{dim, n, nullptr, nullptr, (void*)p, ps, nullptr, nullptr, nullptr};
     cudaStream_t s = as_stream(stream);
 #define DP(D, R) k_diag_particles<D, R><<<nblk(m, 256), 256, 0, s>>>(P, (const R*)ras, rs, n0, out)
     if (dim == 2) { if (dtype) DP(2, double); else DP(2, float); }

@@ -60,6 +60,35 @@ class Particles:
             self.pd[self.R["F"] + a * d + a] = 1.0
         self.pd[self.R["m"]] = 1.0
         self.pd[self.R["V0"]] = 1.0
+        # storage order may be permuted by the per-step sort (coupling); pid
+        # maps storage index -> original (reference) particle index
+        self.pid = torch.arange(n, dtype=torch.int32, device=self.device)
+        self.permuted = False
+        self._scratch = None
+
+    def scratch(self):
+        """Sort targets + radix-sort workspace (allocated once)."""
+        if self._scratch is None:
+            n = len(self)
+            ws = torch.empty(int(L.lib().mlbm_sort_ws_bytes(max(n, 1))), dtype=torch.uint8,
+                             device=self.device)
+            self._scratch = (torch.empty_like(self.xd), torch.empty_like(self.pd),
+                             torch.empty_like(self.pid), ws)
+        return self._scratch
+
+    def _orig(self, t):
+        """Rows [k, n] in storage order -> rows in original particle order."""
+        if not self.permuted:
+            return t
+        out = torch.empty_like(t)
+        out[:, self.pid.long()] = t
+        return out
+
+    def _store(self, rows, val):
+        """Write rows given in original particle order into storage order."""
+        if self.permuted:
+            val = val[:, self.pid.long()]
+        rows.copy_(val)
 
     def __len__(self):
         return self.xd.shape[1]
@@ -70,60 +99,67 @@ class Particles:
     # reference-style (n, ...) views / setters -----------------------------------
     @property
     def x(self):
-        return self.xd.t()
+        return self._orig(self.xd).t()
 
     @x.setter
     def x(self, v):
-        self.xd.copy_(torch.as_tensor(np.asarray(v) if not torch.is_tensor(v) else v,
-                                      dtype=torch.float64, device=self.device).reshape(-1, self.d).t())
+        self._store(self.xd, torch.as_tensor(np.asarray(v) if not torch.is_tensor(v) else v,
+                                             dtype=torch.float64,
+                                             device=self.device).reshape(-1, self.d).t())
 
     @property
     def v(self):
-        return self._rows("v", self.d).t()
+        return self._orig(self._rows("v", self.d)).t()
 
     @v.setter
     def v(self, val):
-        self._rows("v", self.d).copy_(self._as(val).reshape(-1, self.d).t())
+        self._store(self._rows("v", self.d), self._as(val).reshape(-1, self.d).t())
 
     @property
     def C(self):
-        return self._rows("C", self.d * self.d).t().reshape(-1, self.d, self.d)
+        return self._orig(self._rows("C", self.d * self.d)).t().reshape(-1, self.d, self.d)
 
     @C.setter
     def C(self, val):
-        self._rows("C", self.d * self.d).copy_(self._as(val).reshape(-1, self.d * self.d).t())
+        self._store(self._rows("C", self.d * self.d), self._as(val).reshape(-1, self.d * self.d).t())
 
     @property
     def F(self):
-        return self._rows("F", self.d * self.d).t().reshape(-1, self.d, self.d)
+        return self._orig(self._rows("F", self.d * self.d)).t().reshape(-1, self.d, self.d)
 
     @F.setter
     def F(self, val):
-        self._rows("F", self.d * self.d).copy_(self._as(val).reshape(-1, self.d * self.d).t())
+        self._store(self._rows("F", self.d * self.d), self._as(val).reshape(-1, self.d * self.d).t())
+
+    def _row(self, name):
+        return self._orig(self.pd[self.R[name]:self.R[name] + 1])[0]
+
+    def _set_row(self, name, val):
+        self._store(self.pd[self.R[name]:self.R[name] + 1], self._as(val).reshape(1, -1))
 
     @property
     def m(self):
-        return self.pd[self.R["m"]]
+        return self._row("m")
 
     @m.setter
     def m(self, val):
-        self.pd[self.R["m"]].copy_(self._as(val))
+        self._set_row("m", val)
 
     @property
     def V0(self):
-        return self.pd[self.R["V0"]]
+        return self._row("V0")
 
     @V0.setter
     def V0(self, val):
-        self.pd[self.R["V0"]].copy_(self._as(val))
+        self._set_row("V0", val)
 
     @property
     def vol_corr(self):
-        return self.pd[self.R["vc"]]
+        return self._row("vc")
 
     @vol_corr.setter
     def vol_corr(self, val):
-        self.pd[self.R["vc"]].copy_(self._as(val))
+        self._set_row("vc", val)
 
     def _as(self, v):
         return torch.as_tensor(v if torch.is_tensor(v) else np.asarray(v), dtype=self.dtype,
@@ -281,7 +317,7 @@ def p2g(particles: Particles, grid: MpmGrid, mat: SandMaterial, st=None):
     L.check(L.lib().mlbm_p2g(L.C.byref(lv0), len(particles), L.ptr(particles.xd),
                              L.ptr(particles.pd), particles.pd.stride(0), mat.lam, mat.mu,
                              mat.alpha, L.ptr(grid.ras), grid.ras.stride(0),
-                             dtype_code(grid.dtype), L.ptr(grid._err), L.stream_handle()), "p2g")
+                             dtype_code(grid.dtype), 0, L.ptr(grid._err), L.stream_handle()), "p2g")
 
 
 def grid_update(grid: MpmGrid, dt: float, gravity, drag=None, floor_friction: float = 0.5):
@@ -309,7 +345,8 @@ def g2p(particles: Particles, grid: MpmGrid, dt: float, mat: SandMaterial,
     lv0 = grid.level0()
     grid.counters.zero_()
     L.check(L.lib().mlbm_g2p(L.C.byref(lv0), len(particles), L.ptr(particles.xd),
-                             L.ptr(particles.pd), particles.pd.stride(0), mat.lam, mat.mu,
+                             L.ptr(particles.xd), L.ptr(particles.pd), L.ptr(particles.pd),
+                             L.ptr(None), L.ptr(None), particles.pd.stride(0), mat.lam, mat.mu,
                              mat.alpha, L.ptr(grid.ras), grid.ras.stride(0), float(dt),
                              1 if plastic else 0, dtype_code(grid.dtype), L.ptr(grid.counters),
                              L.ptr(grid._err), L.stream_handle()), "g2p")
