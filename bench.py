@@ -135,6 +135,9 @@ def kernel_class(rec, d, s):
                                 + (NM + 2)) * s, n
     if name.startswith("mlbm_diag"):
         return "diagnostics", 0, 0
+    if name == "mlbm_particle_sort":
+        n = int(args[1])
+        return "particle_sort", n * 2 * (8 * d + (d + 2 * d * d + 3) * s + 4), n
     return "adapt/topology", 0, 0
 
 

@@ -318,7 +318,13 @@ class CoupledSim:
         topo = self.topology
         if self._graph_ver != topo.version:
             self._graphs.clear()
+            self._pool = None          # graphs of the old topology freed with their pool
             self._graph_ver = topo.version
+        # persistent buffers are allocated outside any capture
+        if self.sort_particles and len(self.particles):
+            self.particles.scratch()
+        if self.powder is not None:
+            self._powder_tmp()
         # refresh host-side tables / rasters before capture (may sync)
         solver._refresh_tables()
         self.grid.sync_topology()
@@ -390,6 +396,12 @@ class CoupledSim:
                 diag = self._diag_buf.cpu().numpy()
         self._push_diag_row(diag)
 
+    def _powder_tmp(self):
+        n0 = self.topology.cell_count(0)
+        if self._tmp is None or self._tmp.numel() != n0:
+            self._tmp = torch.empty(n0, dtype=self.dtype, device=self.topology.device)
+        return self._tmp
+
     def _powder_cycle(self, is_mpm):
         solver = self.solver
         r, w = solver.last_roles(0)
@@ -397,9 +409,7 @@ class CoupledSim:
         lib = L.lib()
         s = L.stream_handle()
         dcode = dtype_code(self.dtype)
-        n0 = self.topology.cell_count(0)
-        if self._tmp is None or self._tmp.numel() != n0:
-            self._tmp = torch.empty(n0, dtype=self.dtype, device=self.topology.device)
+        self._powder_tmp()
         src = is_mpm and self.last_fields is not None and self.powder.entrain > 0.0 \
             and len(self.particles) > 0
         if src:

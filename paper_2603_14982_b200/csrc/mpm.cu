@@ -848,8 +848,12 @@ __global__ void __launch_bounds__(256) k_p2g_smem(PartArgs P, TopoL0 t0, MatPara
         const R ap = D == 2 ? R(2) * sqrt(V0 / R(3.14159265358979323846))
                             : R(3.14159265358979323846) * pow(R(3) * V0 / (R(4) * R(3.14159265358979323846)), R(2.0 / 3.0));
         bool bad = false;
+        // sorted neighbours share their stencil: stagger the node order per
+        // lane so that lanes of one cell hit different shared-memory words
+        const int k0 = (threadIdx.x & 31) % K;
 #pragma unroll 1
-        for (int k = 0; k < K; ++k) {
+        for (int kk = 0; kk < K; ++kk) {
+            const int k = (kk + k0) % K;
             const int o[3] = {k % 3, (k / 3) % 3, k / 9};
             R w = R(1), gr[D];
 #pragma unroll
