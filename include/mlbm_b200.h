@@ -250,8 +250,9 @@ int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, void* p, int64
 /* MPM particle sort (no reference counterpart — ordering only, SURVEY.md
  * §2.3 K7): radix-sort by (level-0 tile slot, cell) of the stencil base cell
  * and gather every particle row (positions, state rows, ids) into the _out
- * buffers.  smem != 0 in mlbm_p2g then accumulates per block in shared
- * memory over the block's bounding box. */
+ * buffers.  In mlbm_p2g, smem = 1 accumulates per block in shared memory over
+ * the block's bounding box; smem = 2 accumulates per warp in registers (nodes
+ * owned by lanes, particles broadcast by shuffles) — both need sorted input. */
 int64_t mlbm_sort_ws_bytes(int64_t n);
 int mlbm_particle_sort(const mlbm_level_t* lv0, int32_t n, const double* x, const void* p,
                        const int32_t* pid, int64_t ps, double* x_out, void* p_out,

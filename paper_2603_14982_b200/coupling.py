@@ -161,6 +161,7 @@ class CoupledSim:
         # exchange kind), recaptured after every topology change
         self.use_graphs = True
         self.sort_particles = True
+        self.p2g_mode = 2          # 1: block smem, 2: warp registers (sorted input)
         self._graphs = {}
         self._graph_ver = None
         self._pool = None
@@ -200,7 +201,7 @@ class CoupledSim:
             L.check(lib.mlbm_particle_sort(L.C.byref(lv0), n, L.ptr(p.xd), L.ptr(p.pd),
                                            L.ptr(p.pid), ps, L.ptr(xa), L.ptr(pa), L.ptr(ida),
                                            dcode, L.ptr(ws), ws.numel(), s), "particle_sort")
-            src_x, src_p, src_id, smem = xa, pa, ida, 1
+            src_x, src_p, src_id, smem = xa, pa, ida, self.p2g_mode
             p.permuted = True
         else:
             src_x, src_p, src_id, smem = p.xd, p.pd, None, 0

@@ -15,6 +15,7 @@
 //
 // Particle positions are always float64 (sub-cell offsets at x ~ 1e3 need
 // ~1e-8 absolute resolution); everything else follows the run dtype.
+#include <algorithm>
 #include <cub/cub.cuh>
 #include "common.cuh"
 
@@ -166,6 +167,71 @@ __device__ __forceinline__ void svd(const R (&F)[D * D], R (&U)[D * D], R (&s)[D
     if constexpr (D == 2) svd2<R>(F, U, s, V); else svd3<R>(F, U, s, V);
 }
 
+// Cyclic Jacobi on a symmetric 3x3 (entries a00 a01 a02 a11 a12 a22), only the
+// touched entries updated.  Returns eigenvalues lam and eigenvectors as the
+// columns of Q (Q diag(lam) Q^T = a).
+template <typename R>
+__device__ __forceinline__ void sym_eig3(R a00, R a01, R a02, R a11, R a12, R a22, R (&lam)[3],
+                                         R (&Q)[9]) {
+    R A[3][3] = {{a00, a01, a02}, {a01, a11, a12}, {a02, a12, a22}};
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Q[i] = (i % 4 == 0) ? R(1) : R(0);
+    const R tol = R(sizeof(R) == 8 ? 1e-32 : 1e-15);
+#pragma unroll 1
+    for (int sweep = 0; sweep < 8; ++sweep) {
+        const R off = A[0][1] * A[0][1] + A[0][2] * A[0][2] + A[1][2] * A[1][2];
+        const R dia = A[0][0] * A[0][0] + A[1][1] * A[1][1] + A[2][2] * A[2][2];
+        if (!(off > dia * tol)) break;
+#pragma unroll
+        for (int pq = 0; pq < 3; ++pq) {
+            const int p = pq == 2 ? 1 : 0, q = pq == 0 ? 1 : 2, r = 3 - p - q;
+            const R apq = A[p][q];
+            if (apq == R(0)) continue;
+            const R theta = (A[q][q] - A[p][p]) / (R(2) * apq);
+            const R t = (theta >= R(0) ? R(1) : R(-1)) / (fabs(theta) + sqrt(theta * theta + R(1)));
+            const R c = R(1) / sqrt(t * t + R(1)), sn = t * c;
+            A[p][p] -= t * apq;
+            A[q][q] += t * apq;
+            A[p][q] = A[q][p] = R(0);
+            const R arp = A[r][p], arq = A[r][q];
+            A[r][p] = A[p][r] = c * arp - sn * arq;
+            A[r][q] = A[q][r] = sn * arp + c * arq;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const R vkp = Q[k * 3 + p], vkq = Q[k * 3 + q];
+                Q[k * 3 + p] = c * vkp - sn * vkq;
+                Q[k * 3 + q] = sn * vkp + c * vkq;
+            }
+        }
+    }
+    lam[0] = A[0][0];
+    lam[1] = A[1][1];
+    lam[2] = A[2][2];
+}
+
+// principal stretches of F from b = F F^T (left vectors U = Q); the sign of
+// det F goes on the smallest value (the rotation-variant SVD convention)
+template <typename R>
+__device__ __forceinline__ void left_stretch3(const R (&F)[9], R (&U)[9], R (&s)[3]) {
+    const R b00 = F[0] * F[0] + F[1] * F[1] + F[2] * F[2];
+    const R b01 = F[0] * F[3] + F[1] * F[4] + F[2] * F[5];
+    const R b02 = F[0] * F[6] + F[1] * F[7] + F[2] * F[8];
+    const R b11 = F[3] * F[3] + F[4] * F[4] + F[5] * F[5];
+    const R b12 = F[3] * F[6] + F[4] * F[7] + F[5] * F[8];
+    const R b22 = F[6] * F[6] + F[7] * F[7] + F[8] * F[8];
+    R lam[3];
+    sym_eig3<R>(b00, b01, b02, b11, b12, b22, lam, U);
+    int imin = 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        s[i] = sqrt(lam[i] > R(0) ? lam[i] : R(0));
+        if (lam[i] < lam[imin]) imin = i;
+    }
+    const R det = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
+                  F[2] * (F[3] * F[7] - F[4] * F[6]);
+    if (det < R(0)) s[imin] = -s[imin];
+}
+
 struct MatParams {
     double lam, mu, alpha, floor_friction;
 };
@@ -173,8 +239,13 @@ struct MatParams {
 // tau = U diag(2 mu eps + lam tr) U^T  (granular.py:260-279)
 template <int D, typename R>
 __device__ void kirchhoff(const R (&F)[D * D], const MatParams& mp, R (&tau)[D * D]) {
-    R U[D * D], s[D], V[D * D];
-    svd<D, R>(F, U, s, V);
+    R U[D * D], s[D];
+    if constexpr (D == 3) {
+        left_stretch3<R>(F, U, s);
+    } else {
+        R V[D * D];
+        svd<D, R>(F, U, s, V);
+    }
     R e[D], tr = R(0);
 #pragma unroll
     for (int a = 0; a < D; ++a) { e[a] = log(s[a] > R(1e-12) ? s[a] : R(1e-12)); tr += e[a]; }
@@ -214,6 +285,13 @@ __device__ __forceinline__ void make_stencil(const double (&x)[D], Stencil<D, R>
         st.dw[a][2] = f - R(0.5);
     }
     if (D == 2) st.base[2] = 0;
+}
+
+// register-resident pick of a per-axis stencil value (a dynamic index into
+// the w / dw arrays would force them into local memory)
+template <typename R>
+__device__ __forceinline__ R sel3(const R (&v)[3], int o) {
+    return o == 0 ? v[0] : (o == 1 ? v[1] : v[2]);
 }
 
 struct PartArgs {
@@ -263,11 +341,11 @@ __global__ void __launch_bounds__(128) k_p2g(PartArgs P, TopoL0 t0, MatParams mp
         if (ni < 0) continue;
         R w = R(1), gr[D];
 #pragma unroll
-        for (int a = 0; a < D; ++a) { w *= st.w[a][o[a]]; gr[a] = R(1); }
+        for (int a = 0; a < D; ++a) { w *= sel3<R>(st.w[a], o[a]); gr[a] = R(1); }
 #pragma unroll
         for (int a = 0; a < D; ++a)
 #pragma unroll
-            for (int b = 0; b < D; ++b) gr[b] *= (a == b) ? st.dw[a][o[a]] : st.w[a][o[a]];
+            for (int b = 0; b < D; ++b) gr[b] *= (a == b) ? sel3<R>(st.dw[a], o[a]) : sel3<R>(st.w[a], o[a]);
         R dpos[D];
 #pragma unroll
         for (int a = 0; a < D; ++a) dpos[a] = R((double)(st.base[a] + o[a]) - x[a]);
@@ -463,7 +541,7 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
         if (ni < 0) continue;
         R w = R(1);
 #pragma unroll
-        for (int a = 0; a < D; ++a) w *= st.w[a][o[a]];
+        for (int a = 0; a < D; ++a) w *= sel3<R>(st.w[a], o[a]);
         R dpos[D];
 #pragma unroll
         for (int a = 0; a < D; ++a) dpos[a] = R((double)(st.base[a] + o[a]) - x[a]);
@@ -516,7 +594,12 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
         }
     if (plastic) {
         R U[D * D], s[D], V[D * D];
-        svd<D, R>(Fn, U, s, V);
+        bool fast = false;
+        if constexpr (D == 3) {
+            left_stretch3<R>(Fn, U, s);
+            fast = fabs(s[0]) > R(1e-6) && fabs(s[1]) > R(1e-6) && fabs(s[2]) > R(1e-6);
+        }
+        if (!fast) svd<D, R>(Fn, U, s, V);
         R e[D], tr = R(0);
         const R vc = pp[PR::VC * P.ps + p];
 #pragma unroll
@@ -546,15 +629,40 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
 #pragma unroll
         for (int a = 0; a < D; ++a) { sum += en[a]; se[a] = exp(en[a]); }
         pw[PR::VC * P.ps + p] = tr - sum;
+        if (fast) {
+            // F_new = U diag(s_new / s) U^T F  ( = U diag(s_new) V^T )
+            R M[D * D], G[D * D];
 #pragma unroll
-        for (int i = 0; i < D; ++i)
+            for (int i = 0; i < D; ++i)
 #pragma unroll
-            for (int j = 0; j < D; ++j) {
-                R acc = R(0);
+                for (int j = 0; j < D; ++j) {
+                    R acc = R(0);
 #pragma unroll
-                for (int k = 0; k < D; ++k) acc += U[i * D + k] * se[k] * V[j * D + k];
-                Fn[i * D + j] = acc;
-            }
+                    for (int k = 0; k < D; ++k) acc += U[i * D + k] * (se[k] / s[k]) * U[j * D + k];
+                    M[i * D + j] = acc;
+                }
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    R acc = R(0);
+#pragma unroll
+                    for (int k = 0; k < D; ++k) acc += M[i * D + k] * Fn[k * D + j];
+                    G[i * D + j] = acc;
+                }
+#pragma unroll
+            for (int k = 0; k < D * D; ++k) Fn[k] = G[k];
+        } else {
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    R acc = R(0);
+#pragma unroll
+                    for (int k = 0; k < D; ++k) acc += U[i * D + k] * se[k] * V[j * D + k];
+                    Fn[i * D + j] = acc;
+                }
+        }
     }
 #pragma unroll
     for (int k = 0; k < D * D; ++k) pw[(PR::F + k) * P.ps + p] = Fn[k];
@@ -592,7 +700,7 @@ __global__ void k_stress_raster(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int
         const int64_t ni = node_index<D>(t0, c, bad);
         if (ni < 0) continue;
         R w = V0;
-        for (int a = 0; a < D; ++a) w *= st.w[a][o[a]];
+        for (int a = 0; a < D; ++a) w *= sel3<R>(st.w[a], o[a]);
         for (int q = 0; q < NS; ++q) aadd(&ras[(RW::SIG + q) * rs + ni], w * tau[s_a<D>(q) * D + s_b<D>(q)]);
     }
     if (bad) report_error(err, MLBM_ERR_STENCIL, 0, st.base[0], st.base[1], st.base[2]);
@@ -710,58 +818,79 @@ __global__ void k_powder_diffuse(PowderArgs A) {
 
 // ---------------------------------------------------------------------------
 // diagnostics: out[0..D-1] += vol * sum rho u (leaf), out[D] += vol * sum phi,
-// out[D+1] = min eps (leaf), via double atomics
+// out[D+1] = min eps (leaf); warp shuffles -> shared memory -> one double
+// atomic per block and value
+template <int NV>
+__device__ __forceinline__ void block_sum_atomic(double (&acc)[NV], double* out) {
+    __shared__ double red[NV][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        double v = acc[k];
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+        if (lane == 0) red[k][wid] = v;
+    }
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double v = lane < nw ? red[k][lane] : 0.0;
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+            if (lane == 0 && v != 0.0) atomicAdd(&out[k], v);
+        }
+    }
+}
+
+__device__ __forceinline__ void atomic_min_double(double* addr, double v) {
+    unsigned long long* a = (unsigned long long*)addr;
+    unsigned long long old = *a, assumed;
+    do {
+        assumed = old;
+        if (__longlong_as_double(assumed) <= v) break;
+        old = atomicCAS(a, assumed, __double_as_longlong(v));
+    } while (assumed != old);
+}
+
 template <int D, typename R>
 __global__ void k_diag_level(mlbm_level_t lv, mlbm_fields_t f, double vol, double* out) {
     constexpr int T = Geo<D>::T;
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     double acc[D + 1];
     for (int k = 0; k <= D; ++k) acc[k] = 0.0;
     double emin = 1e300;
-    if (c < (int64_t)lv.n_tiles * T && (lv.cell_flags[c] & MLBM_CF_LEAF)) {
-        const FieldsT<R> a = fields_of<R>(f);
+    const FieldsT<R> a = fields_of<R>(f);
+    const int64_t n = (int64_t)lv.n_tiles * T;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        if (!(lv.cell_flags[c] & MLBM_CF_LEAF)) continue;
         const double rho = 1.0 + (double)a.at(0, c);
-        for (int k = 0; k < D; ++k) acc[k] = vol * rho * (double)a.at(1 + k, c);
-        acc[D] = vol * (double)a.at(fi_phi<D>(), c);
-        emin = (double)a.at(fi_eps<D>(), c);
+        for (int k = 0; k < D; ++k) acc[k] += vol * rho * (double)a.at(1 + k, c);
+        acc[D] += vol * (double)a.at(fi_phi<D>(), c);
+        emin = fmin(emin, (double)a.at(fi_eps<D>(), c));
     }
-    for (int k = 0; k <= D; ++k)
-        for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_down_sync(0xffffffffu, acc[k], off);
     for (int off = 16; off > 0; off >>= 1) emin = fmin(emin, __shfl_down_sync(0xffffffffu, emin, off));
-    if ((threadIdx.x & 31) == 0) {
-        for (int k = 0; k <= D; ++k) if (acc[k] != 0.0) atomicAdd(&out[k], acc[k]);
-        if (emin < 1e300) {
-            unsigned long long* addr = (unsigned long long*)&out[D + 1];
-            unsigned long long old = *addr, assumed;
-            do {
-                assumed = old;
-                if (__longlong_as_double(assumed) <= emin) break;
-                old = atomicCAS(addr, assumed, __double_as_longlong(emin));
-            } while (assumed != old);
-        }
-    }
+    if ((threadIdx.x & 31) == 0 && emin < 1e300) atomic_min_double(&out[D + 1], emin);
+    block_sum_atomic<D + 1>(acc, out);
 }
 
 // out[0..D-1] += sum m v ; out[D..2D-1] += sum fs (level-0 cells)
 template <int D, typename R>
 __global__ void k_diag_particles(PartArgs P, const R* ras, int64_t rs, int64_t n0, double* out) {
     using PR = PRows<D>;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     double acc[2 * D];
     for (int k = 0; k < 2 * D; ++k) acc[k] = 0.0;
-    if (i < P.n) {
-        const R* pp = (const R*)P.p;
-        const double m = (double)pp[PR::M * P.ps + i];
-        for (int a = 0; a < D; ++a) acc[a] = m * (double)pp[(PR::V + a) * P.ps + i];
+    const R* pp = (const R*)P.p;
+    const int64_t m = P.n > n0 ? P.n : n0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < P.n) {
+            const double mass = (double)pp[PR::M * P.ps + i];
+            for (int a = 0; a < D; ++a) acc[a] += mass * (double)pp[(PR::V + a) * P.ps + i];
+        }
+        if (ras && i < n0)
+            for (int a = 0; a < D; ++a) acc[D + a] += (double)ras[(Rows<D>::FS + a) * rs + i];
     }
-    if (ras && i < n0)
-        for (int a = 0; a < D; ++a) acc[D + a] = (double)ras[(Rows<D>::FS + a) * rs + i];
-    for (int k = 0; k < 2 * D; ++k) {
-        for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_down_sync(0xffffffffu, acc[k], off);
-        if ((threadIdx.x & 31) == 0 && acc[k] != 0.0) atomicAdd(&out[k], acc[k]);
-    }
+    block_sum_atomic<2 * D>(acc, out);
 }
-
 
 // ---------------------------------------------------------------------------
 // particle sort by (level-0 tile slot, cell) of the stencil base cell
@@ -857,11 +986,11 @@ __global__ void __launch_bounds__(256) k_p2g_smem(PartArgs P, TopoL0 t0, MatPara
             const int o[3] = {k % 3, (k / 3) % 3, k / 9};
             R w = R(1), gr[D];
 #pragma unroll
-            for (int a = 0; a < D; ++a) { w *= st.w[a][o[a]]; gr[a] = R(1); }
+            for (int a = 0; a < D; ++a) { w *= sel3<R>(st.w[a], o[a]); gr[a] = R(1); }
 #pragma unroll
             for (int a = 0; a < D; ++a)
 #pragma unroll
-                for (int b = 0; b < D; ++b) gr[b] *= (a == b) ? st.dw[a][o[a]] : st.w[a][o[a]];
+                for (int b = 0; b < D; ++b) gr[b] *= (a == b) ? sel3<R>(st.dw[a], o[a]) : sel3<R>(st.w[a], o[a]);
             R dpos[D];
 #pragma unroll
             for (int a = 0; a < D; ++a) dpos[a] = R((double)(st.base[a] + o[a]) - x[a]);
@@ -920,6 +1049,229 @@ __global__ void __launch_bounds__(256) k_p2g_smem(PartArgs P, TopoL0 t0, MatPara
         }
     }
 }
+
+// ---------------------------------------------------------------------------
+// Warp-cooperative P2G for sorted particles.  Each lane owns up to NPL nodes of
+// the warp's node bounding box and accumulates all 3+3D rows for them in
+// registers while the warp's 32 particles are broadcast one by one (shuffles);
+// a warp whose box exceeds 32*NPL nodes scatters per particle instead.
+// Contribution algebra (granular.py:282-310) with dpos = o - f:
+//   mass  w m          mom_a  w (q_a + sum_b P_ab o_b),  q = m v - m C f,  P = m C
+//   fint_a -sum_b S_ab grad_b (S = V0 tau)   eta w V0   area w a_p   vmom_a w m v_a
+template <int D, typename R, int NPL>
+__global__ void __launch_bounds__(256) k_p2g_warp(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int64_t rs,
+                                                  mlbm_error_t* err) {
+    constexpr int NV = 3 + 3 * D;
+    using PR = PRows<D>;
+    const int lane = threadIdx.x & 31;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = p < P.n;
+    const R* pp = (const R*)P.p;
+    // ---- per-particle quantities
+    int base[3] = {0, 0, 0};
+    R f[D], m = R(0), V0 = R(0), ap = R(0), mv[D], q[D], PC[D * D], S[D * (D + 1) / 2];
+#pragma unroll
+    for (int a = 0; a < D; ++a) { f[a] = R(0); mv[a] = R(0); q[a] = R(0); }
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) PC[k] = R(0);
+#pragma unroll
+    for (int k = 0; k < D * (D + 1) / 2; ++k) S[k] = R(0);
+    if (valid) {
+        double x[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            x[a] = P.x[a * P.ps + p];
+            const double b = floor(x[a] - 0.5);
+            base[a] = (int)b;
+            f[a] = R(x[a] - b);
+        }
+        m = pp[PR::M * P.ps + p];
+        V0 = pp[PR::V0 * P.ps + p];
+        R v[D], C[D * D], F[D * D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) v[a] = pp[(PR::V + a) * P.ps + p];
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) { C[k] = pp[(PR::C + k) * P.ps + p]; F[k] = pp[(PR::F + k) * P.ps + p]; }
+        R tau[D * D];
+        kirchhoff<D, R>(F, mp, tau);
+        ap = D == 2 ? R(2) * sqrt(V0 / R(3.14159265358979323846))
+                    : R(3.14159265358979323846) * pow(R(3) * V0 / (R(4) * R(3.14159265358979323846)), R(2.0 / 3.0));
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            mv[a] = m * v[a];
+            R cf = R(0);
+#pragma unroll
+            for (int b = 0; b < D; ++b) { PC[a * D + b] = m * C[a * D + b]; cf += C[a * D + b] * f[b]; }
+            q[a] = m * (v[a] - cf);
+        }
+        int k = 0;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = a; b < D; ++b) S[k++] = V0 * tau[a * D + b];
+    }
+    // ---- warp node box
+    int lo[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
+    int nbox = 1;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        int mn = valid ? base[a] : 0x7fffffff, mx = valid ? base[a] : -0x7fffffff;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        }
+        lo[a] = mn;
+        ext[a] = mx + 2 - mn + 1;
+        nbox *= ext[a];
+    }
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    if (vmask == 0) return;
+    if (nbox <= 32 * NPL) {
+        R acc[NPL][NV];
+        int nc[NPL][3];
+#pragma unroll
+        for (int r = 0; r < NPL; ++r) {
+            int li = lane + 32 * r;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                if (a < D) { nc[r][a] = lo[a] + li % ext[a]; li /= ext[a]; } else nc[r][a] = 0;
+            }
+#pragma unroll
+            for (int qv = 0; qv < NV; ++qv) acc[r][qv] = R(0);
+        }
+        for (int j = 0; j < 32; ++j) {
+            if (!((vmask >> j) & 1u)) continue;
+            int bj[3];
+            R fj[D], mj, V0j, apj, mvj[D], qj[D], Pj[D * D], Sj[D * (D + 1) / 2];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                bj[a] = __shfl_sync(0xffffffffu, base[a], j);
+                fj[a] = __shfl_sync(0xffffffffu, f[a], j);
+                mvj[a] = __shfl_sync(0xffffffffu, mv[a], j);
+                qj[a] = __shfl_sync(0xffffffffu, q[a], j);
+            }
+#pragma unroll
+            for (int k = 0; k < D * D; ++k) Pj[k] = __shfl_sync(0xffffffffu, PC[k], j);
+#pragma unroll
+            for (int k = 0; k < D * (D + 1) / 2; ++k) Sj[k] = __shfl_sync(0xffffffffu, S[k], j);
+            mj = __shfl_sync(0xffffffffu, m, j);
+            V0j = __shfl_sync(0xffffffffu, V0, j);
+            apj = __shfl_sync(0xffffffffu, ap, j);
+            R W[D][3], DW[D][3];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const R fa = fj[a];
+                W[a][0] = R(0.5) * (R(1.5) - fa) * (R(1.5) - fa);
+                W[a][1] = R(0.75) - (fa - R(1)) * (fa - R(1));
+                W[a][2] = R(0.5) * (fa - R(0.5)) * (fa - R(0.5));
+                DW[a][0] = fa - R(1.5);
+                DW[a][1] = R(-2) * (fa - R(1));
+                DW[a][2] = fa - R(0.5);
+            }
+#pragma unroll
+            for (int r = 0; r < NPL; ++r) {
+                int o[3] = {0, 0, 0};
+                bool in = lane + 32 * r < nbox;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    o[a] = nc[r][a] - bj[a];
+                    in &= (unsigned)o[a] < 3u;
+                }
+                if (!in) continue;
+                R wa[D], dwa[D];
+#pragma unroll
+                for (int a = 0; a < D; ++a) { wa[a] = sel3<R>(W[a], o[a]); dwa[a] = sel3<R>(DW[a], o[a]); }
+                R w = R(1);
+#pragma unroll
+                for (int a = 0; a < D; ++a) w *= wa[a];
+                R gr[D];
+#pragma unroll
+                for (int b = 0; b < D; ++b) {
+                    R g = dwa[b];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) if (a != b) g *= wa[a];
+                    gr[b] = g;
+                }
+                acc[r][0] += w * mj;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    R mo = qj[a];
+#pragma unroll
+                    for (int b = 0; b < D; ++b) mo += Pj[a * D + b] * R(o[b]);
+                    acc[r][1 + a] += w * mo;
+                    R fa = R(0);
+#pragma unroll
+                    for (int b = 0; b < D; ++b) {
+                        const int sk = a <= b ? a * D - a * (a - 1) / 2 + (b - a) : b * D - b * (b - 1) / 2 + (a - b);
+                        fa += Sj[sk] * gr[b];
+                    }
+                    acc[r][1 + D + a] -= fa;
+                    acc[r][3 + 2 * D + a] += w * mvj[a];
+                }
+                acc[r][1 + 2 * D] += w * V0j;
+                acc[r][2 + 2 * D] += w * apj;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < NPL; ++r) {
+            if (lane + 32 * r >= nbox) continue;
+            if (acc[r][0] == R(0) && acc[r][2 + 2 * D] == R(0)) continue;
+            int c[3] = {nc[r][0], nc[r][1], nc[r][2]};
+            bool bad = false;
+            const int64_t ni = node_index<D>(t0, c, bad);
+            if (ni < 0) { report_error(err, MLBM_ERR_STENCIL, 0, nc[r][0], nc[r][1], nc[r][2]); continue; }
+#pragma unroll
+            for (int qv = 0; qv < NV; ++qv)
+                if (acc[r][qv] != R(0)) aadd(&ras[qv * rs + ni], acc[r][qv]);
+        }
+        return;
+    }
+    // ---- fallback: per-particle scatter
+    if (!valid) return;
+    bool bad = false;
+#pragma unroll 1
+    for (int k = 0; k < Geo<D>::K; ++k) {
+        const int o[3] = {k % 3, (k / 3) % 3, k / 9};
+        R wa[D], dwa[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const R fa = f[a];
+            const R W0 = R(0.5) * (R(1.5) - fa) * (R(1.5) - fa), W1 = R(0.75) - (fa - R(1)) * (fa - R(1)),
+                    W2 = R(0.5) * (fa - R(0.5)) * (fa - R(0.5));
+            wa[a] = o[a] == 0 ? W0 : (o[a] == 1 ? W1 : W2);
+            dwa[a] = o[a] == 0 ? fa - R(1.5) : (o[a] == 1 ? R(-2) * (fa - R(1)) : fa - R(0.5));
+        }
+        R w = R(1);
+#pragma unroll
+        for (int a = 0; a < D; ++a) w *= wa[a];
+        int c[3] = {base[0] + o[0], base[1] + o[1], D == 3 ? base[2] + o[2] : 0};
+        const int64_t ni = node_index<D>(t0, c, bad);
+        if (ni < 0) continue;
+        aadd(&ras[0 * rs + ni], w * m);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            R mo = q[a];
+#pragma unroll
+            for (int b = 0; b < D; ++b) mo += PC[a * D + b] * R(o[b]);
+            aadd(&ras[(1 + a) * rs + ni], w * mo);
+            R fa = R(0);
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+                R g = dwa[b];
+#pragma unroll
+                for (int e = 0; e < D; ++e) if (e != b) g *= wa[e];
+                const int sk = a <= b ? a * D - a * (a - 1) / 2 + (b - a) : b * D - b * (b - 1) / 2 + (a - b);
+                fa += S[sk] * g;
+            }
+            aadd(&ras[(1 + D + a) * rs + ni], -fa);
+            aadd(&ras[(3 + 2 * D + a) * rs + ni], w * mv[a]);
+        }
+        aadd(&ras[(1 + 2 * D) * rs + ni], w * V0);
+        aadd(&ras[(2 + 2 * D) * rs + ni], w * ap);
+    }
+    if (bad) report_error(err, MLBM_ERR_STENCIL, 0, base[0], base[1], base[2]);
+}
 }  // namespace mlbm
 
 using namespace mlbm;
@@ -943,7 +1295,8 @@ extern "C" int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, voi
     PartArgs P{lv0->dim, n, x, nullptr, p, ps, nullptr, nullptr, nullptr};
     MatParams mp{lam, mu, alpha, 0.0};
     const TopoL0 t = topo0(lv0);
-#define P2G(D, R) do { if (smem) k_p2g_smem<D, R><<<nblk(n, 256), 256, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
+#define P2G(D, R) do { if (smem == 2) k_p2g_warp<D, R, 3><<<nblk(n, 256), 256, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
+                       else if (smem) k_p2g_smem<D, R><<<nblk(n, 256), 256, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
                        else k_p2g<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err); } while (0)
     if (lv0->dim == 2) { if (dtype) P2G(2, double); else P2G(2, float); }
     else { if (dtype) P2G(3, double); else P2G(3, float); }
@@ -1068,7 +1421,8 @@ extern "C" int mlbm_diag_level(const mlbm_level_t* lv, mlbm_fields_t f, double v
     const int64_t n = (int64_t)lv->n_tiles * T;
     if (n == 0) return 0;
     cudaStream_t s = as_stream(stream);
-#define DG(D, R) k_diag_level<D, R><<<nblk(n, 256), 256, 0, s>>>(*lv, f, vol, out)
+    const int gb = (int)std::min<int64_t>(nblk(n, 256), 592);
+#define DG(D, R) k_diag_level<D, R><<<gb, 256, 0, s>>>(*lv, f, vol, out)
     if (lv->dim == 2) { if (dtype) DG(2, double); else DG(2, float); }
     else { if (dtype) DG(3, double); else DG(3, float); }
 #undef DG
@@ -1081,7 +1435,8 @@ extern "C" int mlbm_diag_particles(int32_t dim, int32_t n, const void* p, int64_
     if (m == 0) return 0;
     PartArgs P{dim, n, nullptr, nullptr, (void*)p, ps, nullptr, nullptr, nullptr};
     cudaStream_t s = as_stream(stream);
-#define DP(D, R) k_diag_particles<D, R><<<nblk(m, 256), 256, 0, s>>>(P, (const R*)ras, rs, n0, out)
+    const int gb = (int)std::min<int64_t>(nblk(m, 256), 592);
+#define DP(D, R) k_diag_particles<D, R><<<gb, 256, 0, s>>>(P, (const R*)ras, rs, n0, out)
     if (dim == 2) { if (dtype) DP(2, double); else DP(2, float); }
     else { if (dtype) DP(3, double); else DP(3, float); }
 #undef DP
