@@ -1059,7 +1059,7 @@ __global__ void __launch_bounds__(256) k_p2g_smem(PartArgs P, TopoL0 t0, MatPara
 //   mass  w m          mom_a  w (q_a + sum_b P_ab o_b),  q = m v - m C f,  P = m C
 //   fint_a -sum_b S_ab grad_b (S = V0 tau)   eta w V0   area w a_p   vmom_a w m v_a
 template <int D, typename R, int NPL>
-__global__ void __launch_bounds__(256) k_p2g_warp(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int64_t rs,
+__global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int64_t rs,
                                                   mlbm_error_t* err) {
     constexpr int NV = 3 + 3 * D;
     using PR = PRows<D>;
@@ -1110,29 +1110,43 @@ __global__ void __launch_bounds__(256) k_p2g_warp(PartArgs P, TopoL0 t0, MatPara
 #pragma unroll
             for (int b = a; b < D; ++b) S[k++] = V0 * tau[a * D + b];
     }
-    // ---- warp node box
-    int lo[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
-    int nbox = 1;
+    const unsigned vmask_all = __ballot_sync(0xffffffffu, valid);
+    if (vmask_all == 0) return;
+    bool done = false;
+    // pass 0: the whole warp; pass 1: each half of the warp separately
+#pragma unroll 1
+    for (int pass = 0; pass < 2 && !done; ++pass) {
+        const unsigned group = pass == 0 ? 0xffffffffu : (lane < 16 ? 0x0000ffffu : 0xffff0000u);
+        const bool mine = valid && ((group >> lane) & 1u);
+        int lo[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
+        int nbox = 1;
 #pragma unroll
-    for (int a = 0; a < D; ++a) {
-        int mn = valid ? base[a] : 0x7fffffff, mx = valid ? base[a] : -0x7fffffff;
+        for (int a = 0; a < D; ++a) {
+            int mn = mine ? base[a] : 0x7fffffff, mx = mine ? base[a] : -0x7fffffff;
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
-            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            for (int off = 16; off > 0; off >>= 1) {
+                if (pass == 1 && off == 16) continue;      // stay inside the half
+                mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+                mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            }
+            lo[a] = mn;
+            ext[a] = mx + 2 - mn + 1;
+            nbox *= ext[a];
         }
-        lo[a] = mn;
-        ext[a] = mx + 2 - mn + 1;
-        nbox *= ext[a];
-    }
-    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-    if (vmask == 0) return;
-    if (nbox <= 32 * NPL) {
+        const unsigned vmask = __ballot_sync(0xffffffffu, mine);
+        // per-group decision (both halves agree inside a half)
+        const bool fits = vmask == 0 || nbox <= (pass == 0 ? 32 : 16) * NPL;
+        const bool all_fit = __all_sync(0xffffffffu, fits);
+        if (pass == 0 && !all_fit) continue;
+        if (pass == 1 && !all_fit) break;
+        // node ownership: pass 0 -> lane owns lane + 32 r ; pass 1 -> (lane & 15) + 16 r
+        const int sub = pass == 0 ? 32 : 16;
+        const int ml = pass == 0 ? lane : (lane & 15);
         R acc[NPL][NV];
         int nc[NPL][3];
 #pragma unroll
         for (int r = 0; r < NPL; ++r) {
-            int li = lane + 32 * r;
+            int li = ml + sub * r;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 if (a < D) { nc[r][a] = lo[a] + li % ext[a]; li /= ext[a]; } else nc[r][a] = 0;
@@ -1140,8 +1154,12 @@ __global__ void __launch_bounds__(256) k_p2g_warp(PartArgs P, TopoL0 t0, MatPara
 #pragma unroll
             for (int qv = 0; qv < NV; ++qv) acc[r][qv] = R(0);
         }
-        for (int j = 0; j < 32; ++j) {
-            if (!((vmask >> j) & 1u)) continue;
+        const int jlo = pass == 0 ? 0 : 0, jn = pass == 0 ? 32 : 16;
+        const int jbase = pass == 0 ? 0 : (lane < 16 ? 0 : 16);
+        for (int jj = jlo; jj < jn; ++jj) {
+            // in pass 1 the two halves broadcast from their own half (jbase)
+            const int j = jbase + jj;
+            if (!__shfl_sync(0xffffffffu, (int)valid, j)) continue;
             int bj[3];
             R fj[D], mj, V0j, apj, mvj[D], qj[D], Pj[D * D], Sj[D * (D + 1) / 2];
 #pragma unroll
@@ -1172,7 +1190,7 @@ __global__ void __launch_bounds__(256) k_p2g_warp(PartArgs P, TopoL0 t0, MatPara
 #pragma unroll
             for (int r = 0; r < NPL; ++r) {
                 int o[3] = {0, 0, 0};
-                bool in = lane + 32 * r < nbox;
+                bool in = ml + sub * r < nbox;
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
                     o[a] = nc[r][a] - bj[a];
@@ -1215,7 +1233,7 @@ __global__ void __launch_bounds__(256) k_p2g_warp(PartArgs P, TopoL0 t0, MatPara
         }
 #pragma unroll
         for (int r = 0; r < NPL; ++r) {
-            if (lane + 32 * r >= nbox) continue;
+            if (ml + sub * r >= nbox || vmask == 0) continue;
             if (acc[r][0] == R(0) && acc[r][2 + 2 * D] == R(0)) continue;
             int c[3] = {nc[r][0], nc[r][1], nc[r][2]};
             bool bad = false;
@@ -1225,8 +1243,9 @@ __global__ void __launch_bounds__(256) k_p2g_warp(PartArgs P, TopoL0 t0, MatPara
             for (int qv = 0; qv < NV; ++qv)
                 if (acc[r][qv] != R(0)) aadd(&ras[qv * rs + ni], acc[r][qv]);
         }
-        return;
+        done = true;
     }
+    if (done) return;
     // ---- fallback: per-particle scatter
     if (!valid) return;
     bool bad = false;
@@ -1295,7 +1314,7 @@ extern "C" int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, voi
     PartArgs P{lv0->dim, n, x, nullptr, p, ps, nullptr, nullptr, nullptr};
     MatParams mp{lam, mu, alpha, 0.0};
     const TopoL0 t = topo0(lv0);
-#define P2G(D, R) do { if (smem == 2) k_p2g_warp<D, R, 3><<<nblk(n, 256), 256, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
+#define P2G(D, R) do { if (smem == 2) k_p2g_warp<D, R, 3><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
                        else if (smem) k_p2g_smem<D, R><<<nblk(n, 256), 256, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
                        else k_p2g<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err); } while (0)
     if (lv0->dim == 2) { if (dtype) P2G(2, double); else P2G(2, float); }

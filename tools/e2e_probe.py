@@ -11,6 +11,7 @@ torch.cuda.synchronize()
 p = sim.particles
 hx = torch.empty_like(p.xd, device="cpu").pin_memory()
 hp = torch.empty_like(p.pd, device="cpu").pin_memory()
+hx.copy_(p.xd); hp.copy_(p.pd); torch.cuda.synchronize()
 def timeit(fn, n=10):
     torch.cuda.synchronize(); t = time.perf_counter()
     for _ in range(n): fn()
@@ -23,3 +24,9 @@ def full():
     sim.step()
     hx.copy_(p.xd, non_blocking=True); hp.copy_(p.pd, non_blocking=True)
 print("full ms", timeit(full), "captures", sim.graph_captures, "changes", sim.topology_changes)
+import time as _t
+for i in range(5):
+    t0=_t.perf_counter(); p.xd.copy_(hx, non_blocking=True); p.pd.copy_(hp, non_blocking=True); torch.cuda.synchronize(); t1=_t.perf_counter()
+    sim.step(); torch.cuda.synchronize(); t2=_t.perf_counter()
+    hx.copy_(p.xd, non_blocking=True); hp.copy_(p.pd, non_blocking=True); torch.cuda.synchronize(); t3=_t.perf_counter()
+    print("phase ms h2d %.3f step %.3f d2h %.3f captures %d changes %d" % ((t1-t0)*1e3,(t2-t1)*1e3,(t3-t2)*1e3, sim.graph_captures, sim.topology_changes))
