@@ -198,6 +198,43 @@ def run_mine(args, rank, world, local_rank):
     value = world * eff_cells * args.steps / (t_ms * 1e-3) / 1e6
     pps = world * n_part * args.steps / (t_ms * 1e-3)
 
+    # ---- e2e through the public API with host-owned particle state
+    e2e = None
+    if not args.no_e2e:
+        p = sim.particles
+        hx = torch.empty_like(p.xd, device="cpu").pin_memory()
+        hp = torch.empty_like(p.pd, device="cpu").pin_memory()
+        hx.copy_(p.xd)
+        hp.copy_(p.pd)
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        diag_bytes = 0
+        for _ in range(args.steps):
+            p.xd.copy_(hx, non_blocking=True)
+            p.pd.copy_(hp, non_blocking=True)
+            sim.step()
+            hx.copy_(p.xd, non_blocking=True)
+            hp.copy_(p.pd, non_blocking=True)
+            row = sim.diagnostics[-1]        # D2H of the step's diagnostics row
+            diag_bytes = 8 * (3 * d + 2)
+        e1.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te = float(te.item())
+        nb = p.xd.numel() * 8 + p.pd.numel() * p.pd.element_size()
+        e2e = {"value": round(world * eff_cells * args.steps / (te * 1e-3) / 1e6, 3), "unit": UNIT,
+               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb + diag_bytes,
+               "particles_per_s": round(world * n_part * args.steps / (te * 1e-3), 1),
+               "ms_per_step": te / args.steps,
+               "path": "CoupledSim.step() with particle state uploaded from / read back to "
+                       "pinned host memory every step + diagnostics row D2H"}
+        del row
+
     # ---- per-kernel device times: an eager pass of the same steps with every
     #      C-ABI call bracketed by CUDA events on the launching stream
     sim.use_graphs = False
@@ -241,43 +278,6 @@ def run_mine(args, rank, world, local_rank):
     lbm_keys = [k for k in classes if k.startswith("level_step")]
     lbm_bytes = sum(classes[k]["bytes"] for k in lbm_keys)
     lbm_ms = sum(classes[k]["ms"] for k in lbm_keys)
-
-    # ---- e2e through the public API with host-owned particle state
-    e2e = None
-    if not args.no_e2e:
-        p = sim.particles
-        hx = torch.empty_like(p.xd, device="cpu").pin_memory()
-        hp = torch.empty_like(p.pd, device="cpu").pin_memory()
-        hx.copy_(p.xd)
-        hp.copy_(p.pd)
-        torch.cuda.synchronize()
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        diag_bytes = 0
-        for _ in range(args.steps):
-            p.xd.copy_(hx, non_blocking=True)
-            p.pd.copy_(hp, non_blocking=True)
-            sim.step()
-            hx.copy_(p.xd, non_blocking=True)
-            hp.copy_(p.pd, non_blocking=True)
-            row = sim.diagnostics[-1]        # D2H of the step's diagnostics row
-            diag_bytes = 8 * (3 * d + 2)
-        e1.record()
-        torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        te = float(te.item())
-        nb = p.xd.numel() * 8 + p.pd.numel() * p.pd.element_size()
-        e2e = {"value": round(world * eff_cells * args.steps / (te * 1e-3) / 1e6, 3), "unit": UNIT,
-               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb + diag_bytes,
-               "particles_per_s": round(world * n_part * args.steps / (te * 1e-3), 1),
-               "ms_per_step": te / args.steps,
-               "path": "CoupledSim.step() with particle state uploaded from / read back to "
-                       "pinned host memory every step + diagnostics row D2H"}
-        del row
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -1110,43 +1110,43 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
 #pragma unroll
             for (int b = a; b < D; ++b) S[k++] = V0 * tau[a * D + b];
     }
-    const unsigned vmask_all = __ballot_sync(0xffffffffu, valid);
-    if (vmask_all == 0) return;
-    bool done = false;
-    // pass 0: the whole warp; pass 1: each half of the warp separately
-#pragma unroll 1
-    for (int pass = 0; pass < 2 && !done; ++pass) {
-        const unsigned group = pass == 0 ? 0xffffffffu : (lane < 16 ? 0x0000ffffu : 0xffff0000u);
-        const bool mine = valid && ((group >> lane) & 1u);
-        int lo[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
-        int nbox = 1;
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    if (vmask == 0) return;
+    // Warp-uniform segmentation of the sorted particles: a segment grows
+    // while the bounding box of its stencils stays within 32*NPL nodes.
+    int j0 = 0;
+    while (j0 < 32) {
+        if (!((vmask >> j0) & 1u)) { ++j0; continue; }
+        int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
 #pragma unroll
         for (int a = 0; a < D; ++a) {
-            int mn = mine ? base[a] : 0x7fffffff, mx = mine ? base[a] : -0x7fffffff;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                if (pass == 1 && off == 16) continue;      // stay inside the half
-                mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
-                mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-            }
-            lo[a] = mn;
-            ext[a] = mx + 2 - mn + 1;
-            nbox *= ext[a];
+            lo[a] = __shfl_sync(0xffffffffu, base[a], j0);
+            hi[a] = lo[a] + 2;
         }
-        const unsigned vmask = __ballot_sync(0xffffffffu, mine);
-        // per-group decision (both halves agree inside a half)
-        const bool fits = vmask == 0 || nbox <= (pass == 0 ? 32 : 16) * NPL;
-        const bool all_fit = __all_sync(0xffffffffu, fits);
-        if (pass == 0 && !all_fit) continue;
-        if (pass == 1 && !all_fit) break;
-        // node ownership: pass 0 -> lane owns lane + 32 r ; pass 1 -> (lane & 15) + 16 r
-        const int sub = pass == 0 ? 32 : 16;
-        const int ml = pass == 0 ? lane : (lane & 15);
+        int j1 = j0 + 1;
+        while (j1 < 32) {
+            if (!((vmask >> j1) & 1u)) { ++j1; continue; }
+            int nl[3], nh[3], nb = 1;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const int b = __shfl_sync(0xffffffffu, base[a], j1);
+                nl[a] = min(lo[a], b);
+                nh[a] = max(hi[a], b + 2);
+                nb *= nh[a] - nl[a] + 1;
+            }
+            if (nb > 32 * NPL) break;
+#pragma unroll
+            for (int a = 0; a < D; ++a) { lo[a] = nl[a]; hi[a] = nh[a]; }
+            ++j1;
+        }
+        int ext[3] = {1, 1, 1}, nbox = 1;
+#pragma unroll
+        for (int a = 0; a < D; ++a) { ext[a] = hi[a] - lo[a] + 1; nbox *= ext[a]; }
         R acc[NPL][NV];
         int nc[NPL][3];
 #pragma unroll
         for (int r = 0; r < NPL; ++r) {
-            int li = ml + sub * r;
+            int li = lane + 32 * r;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 if (a < D) { nc[r][a] = lo[a] + li % ext[a]; li /= ext[a]; } else nc[r][a] = 0;
@@ -1154,12 +1154,8 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
 #pragma unroll
             for (int qv = 0; qv < NV; ++qv) acc[r][qv] = R(0);
         }
-        const int jlo = pass == 0 ? 0 : 0, jn = pass == 0 ? 32 : 16;
-        const int jbase = pass == 0 ? 0 : (lane < 16 ? 0 : 16);
-        for (int jj = jlo; jj < jn; ++jj) {
-            // in pass 1 the two halves broadcast from their own half (jbase)
-            const int j = jbase + jj;
-            if (!__shfl_sync(0xffffffffu, (int)valid, j)) continue;
+        for (int j = j0; j < j1; ++j) {
+            if (!((vmask >> j) & 1u)) continue;
             int bj[3];
             R fj[D], mj, V0j, apj, mvj[D], qj[D], Pj[D * D], Sj[D * (D + 1) / 2];
 #pragma unroll
@@ -1190,7 +1186,7 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
 #pragma unroll
             for (int r = 0; r < NPL; ++r) {
                 int o[3] = {0, 0, 0};
-                bool in = ml + sub * r < nbox;
+                bool in = lane + 32 * r < nbox;
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
                     o[a] = nc[r][a] - bj[a];
@@ -1233,7 +1229,7 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
         }
 #pragma unroll
         for (int r = 0; r < NPL; ++r) {
-            if (ml + sub * r >= nbox || vmask == 0) continue;
+            if (lane + 32 * r >= nbox) continue;
             if (acc[r][0] == R(0) && acc[r][2 + 2 * D] == R(0)) continue;
             int c[3] = {nc[r][0], nc[r][1], nc[r][2]};
             bool bad = false;
@@ -1243,53 +1239,8 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
             for (int qv = 0; qv < NV; ++qv)
                 if (acc[r][qv] != R(0)) aadd(&ras[qv * rs + ni], acc[r][qv]);
         }
-        done = true;
+        j0 = j1;
     }
-    if (done) return;
-    // ---- fallback: per-particle scatter
-    if (!valid) return;
-    bool bad = false;
-#pragma unroll 1
-    for (int k = 0; k < Geo<D>::K; ++k) {
-        const int o[3] = {k % 3, (k / 3) % 3, k / 9};
-        R wa[D], dwa[D];
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-            const R fa = f[a];
-            const R W0 = R(0.5) * (R(1.5) - fa) * (R(1.5) - fa), W1 = R(0.75) - (fa - R(1)) * (fa - R(1)),
-                    W2 = R(0.5) * (fa - R(0.5)) * (fa - R(0.5));
-            wa[a] = o[a] == 0 ? W0 : (o[a] == 1 ? W1 : W2);
-            dwa[a] = o[a] == 0 ? fa - R(1.5) : (o[a] == 1 ? R(-2) * (fa - R(1)) : fa - R(0.5));
-        }
-        R w = R(1);
-#pragma unroll
-        for (int a = 0; a < D; ++a) w *= wa[a];
-        int c[3] = {base[0] + o[0], base[1] + o[1], D == 3 ? base[2] + o[2] : 0};
-        const int64_t ni = node_index<D>(t0, c, bad);
-        if (ni < 0) continue;
-        aadd(&ras[0 * rs + ni], w * m);
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-            R mo = q[a];
-#pragma unroll
-            for (int b = 0; b < D; ++b) mo += PC[a * D + b] * R(o[b]);
-            aadd(&ras[(1 + a) * rs + ni], w * mo);
-            R fa = R(0);
-#pragma unroll
-            for (int b = 0; b < D; ++b) {
-                R g = dwa[b];
-#pragma unroll
-                for (int e = 0; e < D; ++e) if (e != b) g *= wa[e];
-                const int sk = a <= b ? a * D - a * (a - 1) / 2 + (b - a) : b * D - b * (b - 1) / 2 + (a - b);
-                fa += S[sk] * g;
-            }
-            aadd(&ras[(1 + D + a) * rs + ni], -fa);
-            aadd(&ras[(3 + 2 * D + a) * rs + ni], w * mv[a]);
-        }
-        aadd(&ras[(1 + 2 * D) * rs + ni], w * V0);
-        aadd(&ras[(2 + 2 * D) * rs + ni], w * ap);
-    }
-    if (bad) report_error(err, MLBM_ERR_STENCIL, 0, base[0], base[1], base[2]);
 }
 }  // namespace mlbm
 
