@@ -161,7 +161,7 @@ class CoupledSim:
         # exchange kind), recaptured after every topology change
         self.use_graphs = True
         self.sort_particles = True
-        self.p2g_mode = 2          # 1: block smem, 2: warp registers (sorted input)
+        self.p2g_mode = 3          # sorted input: 1 block smem, 2 warp registers, 3 cell lanes
         self._graphs = {}
         self._graph_ver = None
         self._pool = None

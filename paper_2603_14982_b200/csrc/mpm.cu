@@ -1242,6 +1242,190 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
         j0 = j1;
     }
 }
+
+// ---------------------------------------------------------------------------
+// Cell-cooperative P2G for sorted particles (smem mode 3).  Within a warp, the
+// particles of one cell share their 3^D stencil nodes: lane k < 3^D owns node
+// k of the current cell and accumulates all 3+3D rows in registers while the
+// cell's particles are broadcast; at each cell change the lanes flush into a
+// block-wide shared-memory box (one conflict-free RED per lane and row), and
+// the block box is flushed to HBM once.  No coverage tests, no idle-node work.
+template <int D, typename R>
+__global__ void __launch_bounds__(256) k_p2g_cell(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int64_t rs,
+                                                  mlbm_error_t* err) {
+    constexpr int K = Geo<D>::K, NV = 3 + 3 * D, NS = D * (D + 1) / 2;
+    constexpr int MAXN = sizeof(R) == 4 ? 512 : 256;
+    using PR = PRows<D>;
+    __shared__ R sacc[NV * MAXN];
+    __shared__ int s_lo[3], s_hi[3];
+    const int lane = threadIdx.x & 31;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = p < P.n;
+    const R* pp = (const R*)P.p;
+    int base[3] = {0, 0, 0};
+    R f[D], m = R(0), V0 = R(0), ap = R(0), mv[D], q[D], PC[D * D], S[NS];
+#pragma unroll
+    for (int a = 0; a < D; ++a) { f[a] = R(0); mv[a] = R(0); q[a] = R(0); }
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) PC[k] = R(0);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) S[k] = R(0);
+    if (valid) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const double x = P.x[a * P.ps + p];
+            const double b = floor(x - 0.5);
+            base[a] = (int)b;
+            f[a] = R(x - b);
+        }
+        m = pp[PR::M * P.ps + p];
+        V0 = pp[PR::V0 * P.ps + p];
+        R v[D], C[D * D], F[D * D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) v[a] = pp[(PR::V + a) * P.ps + p];
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) { C[k] = pp[(PR::C + k) * P.ps + p]; F[k] = pp[(PR::F + k) * P.ps + p]; }
+        R tau[D * D];
+        kirchhoff<D, R>(F, mp, tau);
+        ap = D == 2 ? R(2) * sqrt(V0 / R(3.14159265358979323846))
+                    : R(3.14159265358979323846) * pow(R(3) * V0 / (R(4) * R(3.14159265358979323846)), R(2.0 / 3.0));
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            mv[a] = m * v[a];
+            R cf = R(0);
+#pragma unroll
+            for (int b = 0; b < D; ++b) { PC[a * D + b] = m * C[a * D + b]; cf += C[a * D + b] * f[b]; }
+            q[a] = m * (v[a] - cf);
+        }
+        int k = 0;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = a; b < D; ++b) S[k++] = V0 * tau[a * D + b];
+    }
+    // block node box (shared-memory accumulation when it fits)
+    if (threadIdx.x < 3) { s_lo[threadIdx.x] = 0x7fffffff; s_hi[threadIdx.x] = -0x7fffffff; }
+    __syncthreads();
+    if (valid) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) { atomicMin(&s_lo[a], base[a]); atomicMax(&s_hi[a], base[a] + 2); }
+    }
+    __syncthreads();
+    int lo[3] = {0, 0, 0}, ext[3] = {1, 1, 1}, nbox = 1;
+#pragma unroll
+    for (int a = 0; a < D; ++a) { lo[a] = s_lo[a]; ext[a] = s_hi[a] - s_lo[a] + 1; nbox *= ext[a]; }
+    const bool use_smem = nbox > 0 && nbox <= MAXN;
+    if (use_smem)
+        for (int i = threadIdx.x; i < NV * nbox; i += blockDim.x) sacc[(i / nbox) * MAXN + i % nbox] = R(0);
+    __syncthreads();
+
+    const int o[3] = {lane % 3, (lane / 3) % 3, D == 3 ? (lane / 9) % 3 : 0};
+    const bool node_lane = lane < K;
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    R acc[NV];
+#pragma unroll
+    for (int qv = 0; qv < NV; ++qv) acc[qv] = R(0);
+    int cur[3] = {0, 0, 0};
+    bool have = false;
+    bool bad = false;
+    auto flush = [&]() {
+        if (!have || !node_lane) return;
+        if (acc[0] == R(0) && acc[2 + 2 * D] == R(0)) return;
+        int c[3] = {cur[0] + o[0], cur[1] + o[1], D == 3 ? cur[2] + o[2] : 0};
+        if (use_smem) {
+            int li = 0;
+#pragma unroll
+            for (int a = D - 1; a >= 0; --a) li = li * ext[a] + (c[a] - lo[a]);
+#pragma unroll
+            for (int qv = 0; qv < NV; ++qv) atomicAdd(&sacc[qv * MAXN + li], acc[qv]);
+        } else {
+            const int64_t ni = node_index<D>(t0, c, bad);
+            if (ni >= 0) {
+#pragma unroll
+                for (int qv = 0; qv < NV; ++qv) aadd(&ras[qv * rs + ni], acc[qv]);
+            }
+        }
+    };
+    for (int j = 0; j < 32; ++j) {
+        if (!((vmask >> j) & 1u)) continue;
+        int bj[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) bj[a] = a < D ? __shfl_sync(0xffffffffu, base[a], j) : 0;
+        if (!have || bj[0] != cur[0] || bj[1] != cur[1] || (D == 3 && bj[2] != cur[2])) {
+            flush();
+#pragma unroll
+            for (int qv = 0; qv < NV; ++qv) acc[qv] = R(0);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) cur[a] = bj[a];
+            have = true;
+        }
+        R fj[D], mvj[D], qj[D], Pj[D * D], Sj[NS];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            fj[a] = __shfl_sync(0xffffffffu, f[a], j);
+            mvj[a] = __shfl_sync(0xffffffffu, mv[a], j);
+            qj[a] = __shfl_sync(0xffffffffu, q[a], j);
+        }
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) Pj[k] = __shfl_sync(0xffffffffu, PC[k], j);
+#pragma unroll
+        for (int k = 0; k < NS; ++k) Sj[k] = __shfl_sync(0xffffffffu, S[k], j);
+        const R mj = __shfl_sync(0xffffffffu, m, j);
+        const R V0j = __shfl_sync(0xffffffffu, V0, j);
+        const R apj = __shfl_sync(0xffffffffu, ap, j);
+        R wa[D], dwa[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const R fa = fj[a];
+            wa[a] = o[a] == 0 ? R(0.5) * (R(1.5) - fa) * (R(1.5) - fa)
+                  : (o[a] == 1 ? R(0.75) - (fa - R(1)) * (fa - R(1)) : R(0.5) * (fa - R(0.5)) * (fa - R(0.5)));
+            dwa[a] = o[a] == 0 ? fa - R(1.5) : (o[a] == 1 ? R(-2) * (fa - R(1)) : fa - R(0.5));
+        }
+        R w = R(1);
+#pragma unroll
+        for (int a = 0; a < D; ++a) w *= wa[a];
+        acc[0] += w * mj;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            R mo = qj[a];
+#pragma unroll
+            for (int b = 0; b < D; ++b) mo += Pj[a * D + b] * R(o[b]);
+            acc[1 + a] += w * mo;
+            R fa = R(0);
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+                R g = dwa[b];
+#pragma unroll
+                for (int e = 0; e < D; ++e) if (e != b) g *= wa[e];
+                const int sk = a <= b ? a * D - a * (a - 1) / 2 + (b - a) : b * D - b * (b - 1) / 2 + (a - b);
+                fa += Sj[sk] * g;
+            }
+            acc[1 + D + a] -= fa;
+            acc[3 + 2 * D + a] += w * mvj[a];
+        }
+        acc[1 + 2 * D] += w * V0j;
+        acc[2 + 2 * D] += w * apj;
+    }
+    flush();
+    if (bad) report_error(err, MLBM_ERR_STENCIL, 0, cur[0], cur[1], cur[2]);
+    if (!use_smem) return;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nbox; i += blockDim.x) {
+        if (sacc[i] == R(0) && sacc[(2 + 2 * D) * MAXN + i] == R(0)) continue;
+        int c[3] = {0, 0, 0};
+        int r = i;
+#pragma unroll
+        for (int a = 0; a < D; ++a) { c[a] = lo[a] + r % ext[a]; r /= ext[a]; }
+        bool b2 = false;
+        const int64_t ni = node_index<D>(t0, c, b2);
+        if (ni < 0) { report_error(err, MLBM_ERR_STENCIL, 0, c[0], c[1], c[2]); continue; }
+#pragma unroll
+        for (int qv = 0; qv < NV; ++qv) {
+            const R vq = sacc[qv * MAXN + i];
+            if (vq != R(0)) aadd(&ras[qv * rs + ni], vq);
+        }
+    }
+}
 }  // namespace mlbm
 
 using namespace mlbm;
@@ -1265,7 +1449,8 @@ extern "C" int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, voi
     PartArgs P{lv0->dim, n, x, nullptr, p, ps, nullptr, nullptr, nullptr};
     MatParams mp{lam, mu, alpha, 0.0};
     const TopoL0 t = topo0(lv0);
-#define P2G(D, R) do { if (smem == 2) k_p2g_warp<D, R, 3><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
+#define P2G(D, R) do { if (smem == 3) k_p2g_cell<D, R><<<nblk(n, 256), 256, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
+                       else if (smem == 2) k_p2g_warp<D, R, 3><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
                        else if (smem) k_p2g_smem<D, R><<<nblk(n, 256), 256, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
                        else k_p2g<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err); } while (0)
     if (lv0->dim == 2) { if (dtype) P2G(2, double); else P2G(2, float); }
