@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIBPATH = os.path.join(HERE, "libmlbm_b200.so")
-SOURCES = ["lbm.cu", "topology.cu", "mpm.cu"]
+SOURCES = ["lbm.cu", "topology.cu", "mpm.cu", "adapt.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
               "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-Wno-deprecated-declarations",
@@ -137,6 +137,7 @@ _SIGS = {
     "mlbm_migrate_level": [I32, I32, P, Fields, Fields, Fields, Fields, I32, P],
     "mlbm_init_new_cells": [C.POINTER(Hier), C.POINTER(Hier), I32, P, P, I32,
                             Fields, Fields, P, I32, I32, P, P],
+    "mlbm_adapt_pass": [C.POINTER(Hier), P, P, P, P, P, P, P, P, P, P, I64, I32, P, P, P, P],
     "mlbm_raster_rows": [I32],
     "mlbm_particle_rows": [I32],
     "mlbm_p2g": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64, I32, I32, P, P],

@@ -119,6 +119,8 @@ class GridAdaptor:
         self._taus = torch.tensor(level_params.taus, dtype=torch.float64, device=dev)
         self._static_key = None
         self._static_dev = None
+        self._bar = torch.zeros(2, dtype=torch.int32, device=dev)
+        self.fused = True          # one cooperative launch per pass (csrc/adapt.cu)
         self.launches = 0
 
     @property
@@ -176,6 +178,8 @@ class GridAdaptor:
         desired / current / effective coverage, plan and no-op flags
         (status[0:L]) and the invariants of the current topology
         (status[L:L+3]).  No host synchronisation (CUDA-graph capturable)."""
+        if self.fused:
+            return self._plan_fused(driver)
         topo = self.topology
         lib = L.lib()
         s = L.stream_handle()
@@ -233,6 +237,23 @@ class GridAdaptor:
                     "plan_level")
             self.launches += 1
         self._invariants_device(driver)
+
+    def _plan_fused(self, driver):
+        topo = self.topology
+        Lv = topo.levels
+        arr = lambda ts: (L.C.c_void_p * Lv)(*[t.data_ptr() for t in ts])   # noqa: E731
+        x = driver.device_positions(topo.d, topo.device)
+        st = self._static(driver.static_tiles)
+        h = topo.hier_struct()
+        self._status.zero_()
+        L.check(L.lib().mlbm_adapt_pass(L.C.byref(h), arr(self._des), arr(self._cur),
+                                        arr(self._eff), arr(self._par), arr(self._own),
+                                        arr(self._new), arr(self._streak), L.ptr(self._seeds),
+                                        L.ptr(st), L.ptr(x), x.stride(0) if x is not None else 0,
+                                        x.shape[1] if x is not None else 0, L.ptr(self._status),
+                                        L.ptr(self._err), L.ptr(self._bar), L.stream_handle()),
+                "adapt_pass")
+        self.launches += 1
 
     def finish(self, driver, pair, status, err) -> AdaptReport:
         """Host half: raise on seed errors, rebuild + migrate if a level

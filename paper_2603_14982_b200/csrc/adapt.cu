@@ -1,0 +1,407 @@
+// One-launch block-maintenance pass (reference adapt.py:54-230, 374-389).
+//
+// All bitmap passes of GridAdaptor.update that do not depend on the rebuild
+// run in ONE cooperative kernel separated by grid barriers:
+//
+//   A  seeds <- static mask; invariants of the current topology (coverage,
+//      two-tile rings); cur[0] = leaf(kind[0])
+//   B  seeds |= particle tiles (domain check); particles in level-0 leaves
+//   C  des[0] = align_up(seeds); cur[1] = leaf(kind[1]) | parents(cur[0])
+//   D/E per level l >= 1: par = parents(des[l-1]); des[l] = align_up(dilate2(par))
+//      (top level: all ones); cur[l+1]
+//   F  eff[0] = hysteresis(des[0], cur[0])          (int16 streaks)
+//   G/H per level l >= 1: par = parents(eff[l-1]);
+//      eff[l] = hysteresis(des[l], cur[l], guard = dilate2(par), par)
+//   I  own[l] = eff[l] & ~parents(eff[l-1])
+//   J  storage = dilate2(own); new kind = own ? leaf : storage ? border : 0;
+//      changed[l] |= new kind != kind
+//
+// Integer-only, bit-exact with the reference bitmap algorithm.  The grid
+// barrier needs co-resident blocks: the kernel is launched cooperatively
+// with at most the occupancy-limited number of blocks.
+#include <algorithm>
+#include "common.cuh"
+
+namespace mlbm {
+
+struct AdaptArgs {
+    int32_t dim, levels;
+    int32_t tdims[MLBM_MAX_LEVELS][3];
+    int32_t periodic[3];
+    const uint8_t* kind[MLBM_MAX_LEVELS];
+    uint8_t* des[MLBM_MAX_LEVELS];
+    uint8_t* cur[MLBM_MAX_LEVELS];
+    uint8_t* eff[MLBM_MAX_LEVELS];
+    uint8_t* par[MLBM_MAX_LEVELS];
+    uint8_t* own[MLBM_MAX_LEVELS];
+    uint8_t* nkind[MLBM_MAX_LEVELS];
+    int16_t* streak[MLBM_MAX_LEVELS];
+    uint8_t* seeds;
+    const uint8_t* static_tiles;
+    const double* x;
+    int64_t xs;
+    int32_t n;
+    int32_t* status;        // [levels] changed, [levels..+2] violations
+    mlbm_error_t* err;
+    unsigned int* bar;      // 2 words, zero-initialised once
+};
+
+__device__ __forceinline__ int64_t gi3(const int* d, int x, int y, int z) {
+    return ((int64_t)x * d[1] + y) * d[2] + z;
+}
+__device__ __forceinline__ void dec3(const int* d, int64_t g, int& x, int& y, int& z) {
+    z = (int)(g % d[2]);
+    g /= d[2];
+    y = (int)(g % d[1]);
+    x = (int)(g / d[1]);
+}
+
+__device__ void grid_barrier(unsigned int* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned int* vgen = bar + 1;
+        const unsigned int g = *vgen;
+        __threadfence();
+        if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(&bar[1], 1u);
+        } else {
+            while (*vgen == g) { __nanosleep(32); }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// any of src over the Chebyshev window [c - r, c + r] (wrap / clip per axis)
+__device__ bool window_any(const uint8_t* src, const int* d, int dim, const int* per, const int (&c)[3],
+                           int r) {
+    const int rz = dim == 3 ? r : 0;
+    for (int dz = -rz; dz <= rz; ++dz) {
+        int z = c[2] + dz;
+        if (dim == 3) {
+            if (per[2]) z = (z % d[2] + d[2]) % d[2];
+            else if (z < 0 || z >= d[2]) continue;
+        }
+        for (int dy = -r; dy <= r; ++dy) {
+            int y = c[1] + dy;
+            if (per[1]) y = (y % d[1] + d[1]) % d[1];
+            else if (y < 0 || y >= d[1]) continue;
+            for (int dx = -r; dx <= r; ++dx) {
+                int x = c[0] + dx;
+                if (per[0]) x = (x % d[0] + d[0]) % d[0];
+                else if (x < 0 || x >= d[0]) continue;
+                if (src[gi3(d, x, y, z)]) return true;
+            }
+        }
+    }
+    return false;
+}
+
+// align_up(dilate_r(src)) at tile c: any over the parent-group window
+__device__ bool group_window_any(const uint8_t* src, const int* d, int dim, const int* per,
+                                 const int (&c)[3], int r) {
+    int g0[3] = {c[0] & ~1, c[1] & ~1, dim == 3 ? (c[2] & ~1) : c[2]};
+    const int lz = dim == 3 ? -r : 0, hz = dim == 3 ? r + 1 : 0;
+    for (int dz = lz; dz <= hz; ++dz) {
+        int z = g0[2] + dz;
+        if (dim == 3) {
+            if (per[2]) z = (z % d[2] + d[2]) % d[2];
+            else if (z < 0 || z >= d[2]) continue;
+        }
+        for (int dy = -r; dy <= r + 1; ++dy) {
+            int y = g0[1] + dy;
+            if (per[1]) y = (y % d[1] + d[1]) % d[1];
+            else if (y < 0 || y >= d[1]) continue;
+            for (int dx = -r; dx <= r + 1; ++dx) {
+                int x = g0[0] + dx;
+                if (per[0]) x = (x % d[0] + d[0]) % d[0];
+                else if (x < 0 || x >= d[0]) continue;
+                if (src[gi3(d, x, y, z)]) return true;
+            }
+        }
+    }
+    return false;
+}
+
+// any over the 2^dim children of parent tile c (child grid dims dc)
+__device__ bool children_any(const uint8_t* src, const int* dc, int dim, const int (&c)[3]) {
+    for (int k = 0; k < (1 << dim); ++k) {
+        const int x = 2 * c[0] + (k & 1), y = 2 * c[1] + ((k >> 1) & 1),
+                  z = dim == 3 ? 2 * c[2] + ((k >> 2) & 1) : c[2];
+        if (src[gi3(dc, x, y, z)]) return true;
+    }
+    return false;
+}
+
+__device__ void effective_stage(const AdaptArgs& A, int l, bool with_guard, int64_t tid, int64_t nth) {
+    const int* d = A.tdims[l];
+    const int dim = A.dim;
+    bool grouped = true;
+    for (int a = 0; a < dim; ++a) grouped &= (d[a] % 2) == 0;
+    int gd[3] = {d[0], d[1], d[2]};
+    if (grouped) for (int a = 0; a < dim; ++a) gd[a] = d[a] / 2;
+    const int64_t ng = (int64_t)gd[0] * gd[1] * gd[2];
+    const int K = grouped ? (1 << dim) : 1;
+    const uint8_t* par = A.par[l];
+    for (int64_t j = tid; j < ng; j += nth) {
+        int x[3];
+        dec3(gd, j, x[0], x[1], x[2]);
+        int64_t gix[8];
+        bool avail[8];
+        bool all = true;
+        for (int k = 0; k < K; ++k) {
+            int c[3];
+            for (int a = 0; a < 3; ++a) c[a] = (grouped && a < dim) ? 2 * x[a] + ((k >> a) & 1) : x[a];
+            const int64_t g = gi3(d, c[0], c[1], c[2]);
+            gix[k] = g;
+            const bool cand = A.cur[l][g] && !A.des[l][g];
+            const int16_t s = cand ? (int16_t)(A.streak[l][g] + 1) : (int16_t)0;
+            A.streak[l][g] = s;
+            bool guard = false;
+            if (with_guard && cand && s >= 2) guard = window_any(par, d, dim, A.periodic, c, 2);
+            avail[k] = cand && s >= 2 && !guard;
+            all &= avail[k];
+        }
+        for (int k = 0; k < K; ++k) {
+            const int64_t g = gix[k];
+            const bool act = grouped ? (avail[k] && all) : false;
+            const bool pp = with_guard ? par[g] != 0 : false;
+            A.eff[l][g] = (A.des[l][g] || (A.cur[l][g] && !act) || pp) ? 1 : 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_adapt_pass(AdaptArgs A) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int dim = A.dim, L = A.levels;
+    const int* d0 = A.tdims[0];
+    const int64_t n0 = (int64_t)d0[0] * d0[1] * d0[2];
+
+    // ---- A: seeds <- static, invariants of the current topology, cur[0]
+    for (int64_t g = tid; g < n0; g += nth) {
+        A.seeds[g] = A.static_tiles ? (A.static_tiles[g] ? 1 : 0) : 0;
+        A.cur[0][g] = A.kind[0][g] == 1;
+        int x[3];
+        dec3(d0, g, x[0], x[1], x[2]);
+        int cnt = 0;
+        for (int l = 0; l < L; ++l) {
+            int c[3];
+            for (int a = 0; a < 3; ++a) c[a] = a < dim ? x[a] >> l : 0;
+            cnt += A.kind[l][gi3(A.tdims[l], c[0], c[1], c[2])] == 1;
+        }
+        if (cnt != 1) atomicAdd(&A.status[L], 1);
+    }
+    for (int l = 0; l < L; ++l) {
+        const int* d = A.tdims[l];
+        const int64_t n = (int64_t)d[0] * d[1] * d[2];
+        for (int64_t g = tid; g < n; g += nth) {
+            if (A.kind[l][g] != 0) continue;
+            int c[3];
+            dec3(d, g, c[0], c[1], c[2]);
+            // a leaf within Chebyshev 2 of an absent tile = missing ring tile
+            bool leaf_near = false;
+            const int rz = dim == 3 ? 2 : 0;
+            for (int dz = -rz; dz <= rz && !leaf_near; ++dz) {
+                int z = c[2] + dz;
+                if (dim == 3) {
+                    if (A.periodic[2]) z = (z % d[2] + d[2]) % d[2];
+                    else if (z < 0 || z >= d[2]) continue;
+                }
+                for (int dy = -2; dy <= 2 && !leaf_near; ++dy) {
+                    int y = c[1] + dy;
+                    if (A.periodic[1]) y = (y % d[1] + d[1]) % d[1];
+                    else if (y < 0 || y >= d[1]) continue;
+                    for (int dx = -2; dx <= 2; ++dx) {
+                        int xx = c[0] + dx;
+                        if (A.periodic[0]) xx = (xx % d[0] + d[0]) % d[0];
+                        else if (xx < 0 || xx >= d[0]) continue;
+                        if (A.kind[l][gi3(d, xx, y, z)] == 1) { leaf_near = true; break; }
+                    }
+                }
+            }
+            if (leaf_near) atomicAdd(&A.status[L + 1], 1);
+        }
+    }
+    grid_barrier(A.bar);
+
+    // ---- B: particle seeds + particles in level-0 leaves
+    for (int64_t p = tid; p < A.n; p += nth) {
+        int t[3] = {0, 0, 0};
+        bool bad = false;
+        for (int a = 0; a < dim; ++a) {
+            const double v = A.x[a * A.xs + p];
+            const int64_t c = (int64_t)floor(v);
+            const int64_t tt = c >= 0 ? c / 4 : -((-c + 3) / 4);
+            if (tt < 0 || tt >= d0[a] || !(v == v)) bad = true;
+            t[a] = (int)tt;
+        }
+        if (bad) { report_error(A.err, MLBM_ERR_DOMAIN, 0, t[0], t[1], t[2]); atomicAdd(&A.status[L + 2], 1); continue; }
+        const int64_t g = gi3(d0, t[0], t[1], t[2]);
+        A.seeds[g] = 1;
+        if (A.kind[0][g] != 1) atomicAdd(&A.status[L + 2], 1);
+    }
+    grid_barrier(A.bar);
+
+    // ---- C: des[0], cur[1]
+    if (L == 1) {
+        for (int64_t g = tid; g < n0; g += nth) A.des[0][g] = 1;
+    } else {
+        for (int64_t g = tid; g < n0; g += nth) {
+            int c[3];
+            dec3(d0, g, c[0], c[1], c[2]);
+            int g0[3] = {c[0] & ~1, c[1] & ~1, dim == 3 ? (c[2] & ~1) : c[2]};
+            bool any = false;
+            for (int k = 0; k < (1 << dim) && !any; ++k) {
+                const int x = g0[0] + (k & 1), y = g0[1] + ((k >> 1) & 1),
+                          z = dim == 3 ? g0[2] + ((k >> 2) & 1) : g0[2];
+                any = A.seeds[gi3(d0, x, y, z)] != 0;
+            }
+            A.des[0][g] = any;
+        }
+        const int* d1 = A.tdims[1];
+        const int64_t n1 = (int64_t)d1[0] * d1[1] * d1[2];
+        for (int64_t g = tid; g < n1; g += nth) {
+            int c[3];
+            dec3(d1, g, c[0], c[1], c[2]);
+            A.cur[1][g] = (A.kind[1][g] == 1) || children_any(A.cur[0], d0, dim, c);
+        }
+    }
+    grid_barrier(A.bar);
+
+    // ---- D/E: desired coverage of coarser levels
+    for (int l = 1; l < L; ++l) {
+        const int* d = A.tdims[l];
+        const int64_t n = (int64_t)d[0] * d[1] * d[2];
+        for (int64_t g = tid; g < n; g += nth) {
+            int c[3];
+            dec3(d, g, c[0], c[1], c[2]);
+            A.par[l][g] = children_any(A.des[l - 1], A.tdims[l - 1], dim, c);
+        }
+        if (l + 1 < L) {
+            const int* dn = A.tdims[l + 1];
+            const int64_t nn = (int64_t)dn[0] * dn[1] * dn[2];
+            for (int64_t g = tid; g < nn; g += nth) {
+                int c[3];
+                dec3(dn, g, c[0], c[1], c[2]);
+                A.cur[l + 1][g] = (A.kind[l + 1][g] == 1) || children_any(A.cur[l], d, dim, c);
+            }
+        }
+        grid_barrier(A.bar);
+        for (int64_t g = tid; g < n; g += nth) {
+            if (l == L - 1) { A.des[l][g] = 1; continue; }
+            int c[3];
+            dec3(d, g, c[0], c[1], c[2]);
+            A.des[l][g] = group_window_any(A.par[l], d, dim, A.periodic, c, 2);
+        }
+        grid_barrier(A.bar);
+    }
+
+    // ---- F/G/H: hysteresis per level
+    effective_stage(A, 0, false, tid, nth);
+    grid_barrier(A.bar);
+    for (int l = 1; l < L; ++l) {
+        const int* d = A.tdims[l];
+        const int64_t n = (int64_t)d[0] * d[1] * d[2];
+        for (int64_t g = tid; g < n; g += nth) {
+            int c[3];
+            dec3(d, g, c[0], c[1], c[2]);
+            A.par[l][g] = children_any(A.eff[l - 1], A.tdims[l - 1], dim, c);
+        }
+        grid_barrier(A.bar);
+        effective_stage(A, l, true, tid, nth);
+        grid_barrier(A.bar);
+        if (l == L - 1) {
+            for (int64_t g = tid; g < n; g += nth) A.eff[l][g] = 1;
+            grid_barrier(A.bar);
+        }
+    }
+    // par[l] now holds parents(eff[l-1]) for every l >= 1 (eff[L-1] = 1 set
+    // after its own parents were taken, as in adapt.py:180-181)
+
+    // ---- I: own
+    for (int l = 0; l < L; ++l) {
+        const int* d = A.tdims[l];
+        const int64_t n = (int64_t)d[0] * d[1] * d[2];
+        for (int64_t g = tid; g < n; g += nth)
+            A.own[l][g] = A.eff[l][g] && !(l > 0 && A.par[l][g]);
+    }
+    grid_barrier(A.bar);
+
+    // ---- J: storage plan + no-op flags
+    for (int l = 0; l < L; ++l) {
+        const int* d = A.tdims[l];
+        const int64_t n = (int64_t)d[0] * d[1] * d[2];
+        bool changed = false;
+        for (int64_t g = tid; g < n; g += nth) {
+            uint8_t k;
+            if (A.own[l][g]) k = 1;
+            else {
+                int c[3];
+                dec3(d, g, c[0], c[1], c[2]);
+                k = window_any(A.own[l], d, dim, A.periodic, c, 2) ? 2 : 0;
+            }
+            A.nkind[l][g] = k;
+            changed |= k != A.kind[l][g];
+        }
+        if (__syncthreads_or(changed) && threadIdx.x == 0) atomicOr(&A.status[l], 1);
+    }
+}
+
+}  // namespace mlbm
+
+using namespace mlbm;
+
+extern "C" int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_t* const* cur,
+                               uint8_t* const* eff, uint8_t* const* par, uint8_t* const* own,
+                               uint8_t* const* nkind, int16_t* const* streak, uint8_t* seeds,
+                               const uint8_t* static_tiles, const double* x, int64_t xs, int32_t n,
+                               int32_t* status, mlbm_error_t* err, unsigned int* bar, void* stream) {
+    AdaptArgs A;
+    A.dim = h->dim;
+    A.levels = h->levels;
+    for (int l = 0; l < h->levels; ++l) {
+        for (int a = 0; a < 3; ++a) A.tdims[l][a] = a < h->dim ? (h->finest[a] >> l) / 4 : 1;
+        A.kind[l] = h->kind[l];
+        A.des[l] = des[l];
+        A.cur[l] = cur[l];
+        A.eff[l] = eff[l];
+        A.par[l] = par[l];
+        A.own[l] = own[l];
+        A.nkind[l] = nkind[l];
+        A.streak[l] = streak[l];
+    }
+    for (int a = 0; a < 3; ++a) A.periodic[a] = h->periodic[a];
+    A.seeds = seeds;
+    A.static_tiles = static_tiles;
+    A.x = x;
+    A.xs = xs;
+    A.n = n;
+    A.status = status;
+    A.err = err;
+    A.bar = bar;
+    static int grid = 0;
+    if (grid == 0) {
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adapt_pass, 256, 0);
+        grid = sms * std::min(per, 2);
+        if (grid < 1) grid = 1;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_adapt_pass, A);
+    if (e != cudaSuccess) return -(int)e;
+    return launch_status(1);
+}

@@ -1,0 +1,97 @@
+"""Device block maintenance vs the reference (golden adapt walk) and the
+oracle (3D random walks): tile sets, int16 streaks, created / deleted
+counts bit-exact after every update; surviving tiles keep their cells
+bitwise (test_adapt.py:118-147)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import adapt as OA
+from oracle import grid as OG
+from oracle import lbm as OL
+
+pytestmark = pytest.mark.gpu
+B = pytest.importorskip("paper_2603_14982_b200")
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def tiles_of(topo):
+    return np.array(sorted(topo.tile_set()), dtype=np.int64).reshape(-1, 2 + topo.d)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_adapt_walk_matches_reference_golden(fused):
+    _need_gpu()
+    g = np.load(os.path.join(GOLD, "adapt_walk.npz"))
+    topo = B.Topology.uniform((64, 64), 3)
+    pair = B.PingPongPair(topo)
+    ad = B.GridAdaptor(topo, B.LevelParams(3, 0.8))
+    ad.fused = fused
+    for step in range(60):
+        rep = ad.update(B.RefineDriver(positions=g[f"pos{step}"], levels=3), pair)
+        assert np.array_equal(tiles_of(topo), g[f"tiles{step}"]), step
+        for l, st in enumerate(ad.streak):
+            assert np.array_equal(st, g[f"streak{step}_{l}"]), (step, l)
+        assert list(rep.created) == list(g[f"created{step}"])
+        assert list(rep.deleted) == list(g[f"deleted{step}"])
+        assert rep.violations == []
+
+
+def test_adapt_3d_random_walk_vs_oracle():
+    _need_gpu()
+    rng = np.random.default_rng(11)
+    cells, levels = (64, 32, 32), 3
+    otopo = OG.Topology.uniform(cells, levels)
+    opair = OG.PingPongPair(otopo)
+    oad = OA.GridAdaptor(otopo, OL.LevelParams(levels, 0.8))
+    dtopo = B.Topology.uniform(cells, levels)
+    dpair = B.PingPongPair(dtopo)
+    dad = B.GridAdaptor(dtopo, B.LevelParams(levels, 0.8))
+    pos = rng.random((4, 3)) * np.array(cells) * 0.8 + 2
+    for step in range(40):
+        pos = np.clip(pos + rng.normal(0, 2.0, pos.shape), 0.5, np.array(cells) - 0.5)
+        orep = oad.update(OA.RefineDriver(pos, None, levels), opair)
+        drep = dad.update(B.RefineDriver(positions=pos, levels=levels), dpair)
+        assert dtopo.tile_set() == otopo.tile_set(), step
+        for a, b in zip(dad.streak, oad.streak):
+            assert np.array_equal(a, b), step
+        assert list(drep.created) == list(orep.created)
+        assert list(drep.deleted) == list(orep.deleted)
+        assert drep.noop == orep.noop
+
+
+def test_surviving_cells_keep_values_bitwise():
+    _need_gpu()
+    topo = B.Topology.uniform((64, 64), 3)
+    pair = B.PingPongPair(topo)
+    ad = B.GridAdaptor(topo, B.LevelParams(3, 0.8))
+    ad.update(B.RefineDriver(positions=np.array([[10.5, 13.2]]), levels=3), pair)
+    rng = np.random.default_rng(1)
+    lv = pair.trees[0].levels[1]
+    lv["sxy"] = rng.random(lv.data.shape[1])
+    snap = {tuple(c): lv["sxy"][i * 16:(i + 1) * 16].cpu().numpy().copy()
+            for i, c in enumerate(topo.tile_coords(1))}
+    ad.update(B.RefineDriver(positions=np.array([[10.5, 13.2], [51.0, 49.0]]), levels=3), pair)
+    lv2 = pair.trees[0].levels[1]
+    hit = 0
+    for i, c in enumerate(topo.tile_coords(1)):
+        if tuple(c) in snap:
+            assert np.array_equal(lv2["sxy"][i * 16:(i + 1) * 16].cpu().numpy(), snap[tuple(c)])
+            hit += 1
+    assert hit > 0
+
+
+def test_particle_outside_domain_raises():
+    _need_gpu()
+    topo = B.Topology.uniform((64, 64), 3)
+    pair = B.PingPongPair(topo)
+    ad = B.GridAdaptor(topo, B.LevelParams(3, 0.8))
+    with pytest.raises(ValueError):
+        ad.update(B.RefineDriver(positions=np.array([[70.0, 3.0]]), levels=3), pair)
