@@ -152,15 +152,29 @@ class CoupledSim:
         self.clamped_particles = 0
         self.last_fields = None
         self._diag_rows = []
-        self._counters = torch.zeros(2, dtype=torch.int32, device=self.topology.device)
         self._tmp = None
         self.last_report = None
         self._diag_buf = torch.zeros(2 * self.d + 4, dtype=torch.float64,
                                      device=self.topology.device)
         # CUDA-graph step: one graph per (cycle, buffer parities,
         # exchange kind), recaptured after every topology change
+        # one int32 block holding every device status word of the step (error
+        # records, counters, adapt flags) -> a single D2H copy per step
+        ne = L.ERR_INTS
+        nst = self.topology.levels + 4 if adaptor is not None else 0
+        self._sblock = torch.zeros(2 * ne + 2 + nst + (ne if adaptor is not None else 0),
+                                   dtype=torch.int32, device=self.topology.device)
+        self._sblock[:ne].copy_(solver._err)
+        solver._err = self._sblock[:ne]
+        self.grid._err = self._sblock[ne:2 * ne]
+        self._counters = self._sblock[2 * ne:2 * ne + 2]
+        if adaptor is not None:
+            adaptor._status = self._sblock[2 * ne + 2:2 * ne + 2 + nst]
+            adaptor._err = self._sblock[2 * ne + 2 + nst:]
         self.use_graphs = True
         self.sort_particles = True
+        self.sort_every = 4        # particles move < 1 cell/step: re-sort every few steps
+        self._sort_now = True
         self.p2g_mode = 3          # sorted input: 1 block smem, 2 warp registers, 3 cell lanes
         self._graphs = {}
         self._graph_ver = None
@@ -196,7 +210,7 @@ class CoupledSim:
         grid.clear()
         n = len(p)
         ps = p.pd.stride(0)
-        if self.sort_particles and n:
+        if self.sort_particles and n and self._sort_now:
             xa, pa, ida, ws = p.scratch()
             L.check(lib.mlbm_particle_sort(L.C.byref(lv0), n, L.ptr(p.xd), L.ptr(p.pd),
                                            L.ptr(p.pid), ps, L.ptr(xa), L.ptr(pa), L.ptr(ida),
@@ -204,7 +218,8 @@ class CoupledSim:
             src_x, src_p, src_id, smem = xa, pa, ida, self.p2g_mode
             p.permuted = True
         else:
-            src_x, src_p, src_id, smem = p.xd, p.pd, None, 0
+            src_x, src_p, src_id = p.xd, p.pd, None
+            smem = self.p2g_mode if (self.sort_particles and p.permuted) else 0
         L.check(lib.mlbm_p2g(L.C.byref(lv0), n, L.ptr(src_x), L.ptr(src_p), ps,
                              mat.lam, mat.mu, mat.alpha, L.ptr(grid.ras), grid.ras.stride(0),
                              dcode, smem, L.ptr(grid._err), s), "p2g")
@@ -249,6 +264,7 @@ class CoupledSim:
     # -- eager path (host checks after every phase) --------------------------------
     def _step_eager(self, ci, is_mpm, adapt_now):
         solver = self.solver
+        self._sort_now = (self.step_count % self.sort_every) == 0
         cycle = solver._schedule[ci]
         if is_mpm:
             solver.run_cycle(cycle, hook=self._exchange)
@@ -294,25 +310,13 @@ class CoupledSim:
         if adapt_now:
             self.adaptor.plan_device(self._driver())
         self._record_diagnostics()
-        parts = self._status_sources(adapt_now)
-        off = 0
-        for t in parts:
-            n = t.numel()
-            self._host_status[off:off + n].copy_(t.to(torch.float64) if t.dtype != torch.float64
-                                                 else t, non_blocking=True)
-            off += n
+        self._host_i32.copy_(self._sblock, non_blocking=True)
+        self._host_f64.copy_(self._diag_buf, non_blocking=True)
 
-    def _status_sources(self, adapt_now):
-        parts = [self.solver._err, self.grid._err, self._diag_buf, self._counters]
-        if adapt_now:
-            st, er = self.adaptor.status_tensors()
-            parts += [st, er]
-        return parts
-
-    def _ensure_host_status(self, adapt_now):
-        n = sum(t.numel() for t in self._status_sources(adapt_now))
-        if getattr(self, "_host_status", None) is None or self._host_status.numel() < n:
-            self._host_status = torch.zeros(n, dtype=torch.float64).pin_memory()
+    def _ensure_host_status(self, adapt_now=None):
+        if getattr(self, "_host_i32", None) is None:
+            self._host_i32 = torch.zeros(self._sblock.numel(), dtype=torch.int32).pin_memory()
+            self._host_f64 = torch.zeros(self._diag_buf.numel(), dtype=torch.float64).pin_memory()
 
     def _step_graph(self, ci, is_mpm, adapt_now):
         solver = self.solver
@@ -331,7 +335,8 @@ class CoupledSim:
         self.grid.sync_topology()
         self.grid.level0()
         self._ensure_host_status(adapt_now)
-        key = (ci, tuple(k & 1 for k in solver.k), is_mpm, adapt_now,
+        self._sort_now = (self.step_count % self.sort_every) == 0
+        key = (ci, tuple(k & 1 for k in solver.k), is_mpm, adapt_now, self._sort_now,
                self.powder is not None and is_mpm and self.last_fields is not None)
         entry = self._graphs.get(key)
         if entry is None:
@@ -370,13 +375,10 @@ class CoupledSim:
         self._finish_graph_step(adapt_now)
 
     def _finish_graph_step(self, adapt_now):
-        h = self._host_status.numpy()
+        h = self._host_i32.numpy().astype(np.int64)
         ne = L.ERR_INTS
-        serr, gerr = h[:ne].astype(np.int64), h[ne:2 * ne].astype(np.int64)
-        off = 2 * ne
-        nd = self._diag_buf.numel()
-        diag = h[off:off + nd].copy()
-        off += nd + self._counters.numel()
+        serr, gerr = h[:ne], h[ne:2 * ne]
+        diag = self._host_f64.numpy().copy()
         if serr[0]:
             self.solver._err.copy_(torch.as_tensor(serr, dtype=torch.int32))
             self.solver.raise_pending()
@@ -384,10 +386,9 @@ class CoupledSim:
             self.grid._err.copy_(torch.as_tensor(gerr, dtype=torch.int32))
             self.grid.raise_pending()
         if adapt_now:
-            st, er = self.adaptor.status_tensors()
-            status = h[off:off + st.numel()].astype(np.int64)
-            off += st.numel()
-            err = h[off:off + er.numel()].astype(np.int64)
+            nst = self.topology.levels + 4
+            status = h[2 * ne + 2:2 * ne + 2 + nst]
+            err = h[2 * ne + 2 + nst:]
             self.last_report = self.adaptor.finish(self._driver(), self.pair, status, err)
             if not self.last_report.noop:
                 self.topology_changes += 1

@@ -67,7 +67,7 @@ __device__ void grid_barrier(unsigned int* bar) {
             __threadfence();
             atomicAdd(&bar[1], 1u);
         } else {
-            while (*vgen == g) { __nanosleep(32); }
+            while (*vgen == g) { }
         }
         __threadfence();
     }
@@ -173,7 +173,7 @@ __device__ void effective_stage(const AdaptArgs& A, int l, bool with_guard, int6
     }
 }
 
-__global__ void __launch_bounds__(256) k_adapt_pass(AdaptArgs A) {
+__global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int dim = A.dim, L = A.levels;
@@ -387,13 +387,13 @@ extern "C" int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_
         int dev = 0, sms = 0, per = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adapt_pass, 256, 0);
-        grid = sms * std::min(per, 2);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adapt_pass, 512, 0);
+        grid = sms * std::min(per, 1);
         if (grid < 1) grid = 1;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(512);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = as_stream(stream);
     cudaLaunchAttribute attr[1];
