@@ -212,13 +212,15 @@ int mlbm_plan_level(int32_t n, const uint8_t* own, const uint8_t* storage,
 /* The whole per-update bitmap pass in ONE cooperative launch (grid barriers
  * between the stages of adapt.py:54-194 + 374-389): seeds, desired / current
  * cumulative coverage, int16 hysteresis, plan, no-op flags status[0..L-1],
- * invariant counts status[L..L+2] of the current topology.  Per-level buffer
+ * invariant counts status[L..L+2] of the current topology (ring violations
+ * are counted as (leaf, absent neighbour) pairs).  Per-level buffer
  * arrays have h->levels entries; bar: 2 zero-initialised words. */
 int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_t* const* cur,
                     uint8_t* const* eff, uint8_t* const* par, uint8_t* const* own,
-                    uint8_t* const* nkind, int16_t* const* streak, uint8_t* seeds,
-                    const uint8_t* static_tiles, const double* x, int64_t xs, int32_t n,
-                    int32_t* status, mlbm_error_t* err, unsigned int* bar, void* stream);
+                    uint8_t* const* nkind, uint8_t* const* stor, int16_t* const* streak,
+                    uint8_t* seeds, const uint8_t* static_tiles, const double* x, int64_t xs,
+                    int32_t n, int32_t* status, mlbm_error_t* err, unsigned int* bar,
+                    void* stream);
 
 /* Invariants (adapt.py:374-389): leaf coverage of every finest tile exactly
  * once, two-tile rings, particles inside level-0 leaves -> viol[0..2]. */

@@ -137,7 +137,7 @@ _SIGS = {
     "mlbm_migrate_level": [I32, I32, P, Fields, Fields, Fields, Fields, I32, P],
     "mlbm_init_new_cells": [C.POINTER(Hier), C.POINTER(Hier), I32, P, P, I32,
                             Fields, Fields, P, I32, I32, P, P],
-    "mlbm_adapt_pass": [C.POINTER(Hier), P, P, P, P, P, P, P, P, P, P, I64, I32, P, P, P, P],
+    "mlbm_adapt_pass": [C.POINTER(Hier), P, P, P, P, P, P, P, P, P, P, P, I64, I32, P, P, P, P],
     "mlbm_raster_rows": [I32],
     "mlbm_particle_rows": [I32],
     "mlbm_p2g": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64, I32, I32, P, P],

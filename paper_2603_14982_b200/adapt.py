@@ -248,7 +248,8 @@ class GridAdaptor:
         self._status.zero_()
         L.check(L.lib().mlbm_adapt_pass(L.C.byref(h), arr(self._des), arr(self._cur),
                                         arr(self._eff), arr(self._par), arr(self._own),
-                                        arr(self._new), arr(self._streak), L.ptr(self._seeds),
+                                        arr(self._new), arr(self._stor), arr(self._streak),
+                                        L.ptr(self._seeds),
                                         L.ptr(st), L.ptr(x), x.stride(0) if x is not None else 0,
                                         x.shape[1] if x is not None else 0, L.ptr(self._status),
                                         L.ptr(self._err), L.ptr(self._bar), L.stream_handle()),

@@ -35,6 +35,7 @@ struct AdaptArgs {
     uint8_t* par[MLBM_MAX_LEVELS];
     uint8_t* own[MLBM_MAX_LEVELS];
     uint8_t* nkind[MLBM_MAX_LEVELS];
+    uint8_t* stor[MLBM_MAX_LEVELS];
     int16_t* streak[MLBM_MAX_LEVELS];
     uint8_t* seeds;
     const uint8_t* static_tiles;
@@ -74,26 +75,30 @@ __device__ void grid_barrier(unsigned int* bar) {
     __syncthreads();
 }
 
+// wrapped / clipped coordinates of the window c-r..c+r along one axis (-1 = outside)
+__device__ __forceinline__ void axis_window(int c, int r, int n, int per, int (&o)[5]) {
+    for (int k = 0; k < 2 * r + 1; ++k) {
+        int v = c - r + k;
+        if (per) { v = v < 0 ? v + n : (v >= n ? v - n : v); }
+        else if (v < 0 || v >= n) v = -1;
+        o[k] = v;
+    }
+}
+
 // any of src over the Chebyshev window [c - r, c + r] (wrap / clip per axis)
 __device__ bool window_any(const uint8_t* src, const int* d, int dim, const int* per, const int (&c)[3],
                            int r) {
-    const int rz = dim == 3 ? r : 0;
-    for (int dz = -rz; dz <= rz; ++dz) {
-        int z = c[2] + dz;
-        if (dim == 3) {
-            if (per[2]) z = (z % d[2] + d[2]) % d[2];
-            else if (z < 0 || z >= d[2]) continue;
-        }
-        for (int dy = -r; dy <= r; ++dy) {
-            int y = c[1] + dy;
-            if (per[1]) y = (y % d[1] + d[1]) % d[1];
-            else if (y < 0 || y >= d[1]) continue;
-            for (int dx = -r; dx <= r; ++dx) {
-                int x = c[0] + dx;
-                if (per[0]) x = (x % d[0] + d[0]) % d[0];
-                else if (x < 0 || x >= d[0]) continue;
-                if (src[gi3(d, x, y, z)]) return true;
-            }
+    int wx[5], wy[5], wz[5] = {c[2], -1, -1, -1, -1};
+    axis_window(c[0], r, d[0], per[0], wx);
+    axis_window(c[1], r, d[1], per[1], wy);
+    const int nz = dim == 3 ? 2 * r + 1 : 1;
+    if (dim == 3) axis_window(c[2], r, d[2], per[2], wz);
+    for (int iz = 0; iz < nz; ++iz) {
+        if (wz[iz] < 0) continue;
+        for (int iy = 0; iy < 2 * r + 1; ++iy) {
+            if (wy[iy] < 0) continue;
+            for (int ix = 0; ix < 2 * r + 1; ++ix)
+                if (wx[ix] >= 0 && src[gi3(d, wx[ix], wy[iy], wz[iz])]) return true;
         }
     }
     return false;
@@ -198,31 +203,26 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
         const int* d = A.tdims[l];
         const int64_t n = (int64_t)d[0] * d[1] * d[2];
         for (int64_t g = tid; g < n; g += nth) {
-            if (A.kind[l][g] != 0) continue;
+            A.stor[l][g] = 0;
+            if (A.kind[l][g] != 1) continue;
+            // two-tile ring of a leaf: count absent tiles (sparse_grid.py:320-337)
             int c[3];
             dec3(d, g, c[0], c[1], c[2]);
-            // a leaf within Chebyshev 2 of an absent tile = missing ring tile
-            bool leaf_near = false;
-            const int rz = dim == 3 ? 2 : 0;
-            for (int dz = -rz; dz <= rz && !leaf_near; ++dz) {
-                int z = c[2] + dz;
-                if (dim == 3) {
-                    if (A.periodic[2]) z = (z % d[2] + d[2]) % d[2];
-                    else if (z < 0 || z >= d[2]) continue;
-                }
-                for (int dy = -2; dy <= 2 && !leaf_near; ++dy) {
-                    int y = c[1] + dy;
-                    if (A.periodic[1]) y = (y % d[1] + d[1]) % d[1];
-                    else if (y < 0 || y >= d[1]) continue;
-                    for (int dx = -2; dx <= 2; ++dx) {
-                        int xx = c[0] + dx;
-                        if (A.periodic[0]) xx = (xx % d[0] + d[0]) % d[0];
-                        else if (xx < 0 || xx >= d[0]) continue;
-                        if (A.kind[l][gi3(d, xx, y, z)] == 1) { leaf_near = true; break; }
-                    }
+            int wx[5], wy[5], wz[5] = {c[2], -1, -1, -1, -1};
+            axis_window(c[0], 2, d[0], A.periodic[0], wx);
+            axis_window(c[1], 2, d[1], A.periodic[1], wy);
+            const int nz = dim == 3 ? 5 : 1;
+            if (dim == 3) axis_window(c[2], 2, d[2], A.periodic[2], wz);
+            int miss = 0;
+            for (int iz = 0; iz < nz; ++iz) {
+                if (wz[iz] < 0) continue;
+                for (int iy = 0; iy < 5; ++iy) {
+                    if (wy[iy] < 0) continue;
+                    for (int ix = 0; ix < 5; ++ix)
+                        if (wx[ix] >= 0 && A.kind[l][gi3(d, wx[ix], wy[iy], wz[iz])] == 0) ++miss;
                 }
             }
-            if (leaf_near) atomicAdd(&A.status[L + 1], 1);
+            if (miss) atomicAdd(&A.status[L + 1], miss);
         }
     }
     grid_barrier(A.bar);
@@ -330,19 +330,37 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
     }
     grid_barrier(A.bar);
 
-    // ---- J: storage plan + no-op flags
+    // ---- J: storage = dilate2(own) by scattering from own tiles, then the
+    //      new kinds and the no-op flags (adapt.py:184-225)
+    for (int l = 0; l < L; ++l) {
+        const int* d = A.tdims[l];
+        const int64_t n = (int64_t)d[0] * d[1] * d[2];
+        for (int64_t g = tid; g < n; g += nth) {
+            if (!A.own[l][g]) continue;
+            int c[3];
+            dec3(d, g, c[0], c[1], c[2]);
+            int wx[5], wy[5], wz[5] = {c[2], -1, -1, -1, -1};
+            axis_window(c[0], 2, d[0], A.periodic[0], wx);
+            axis_window(c[1], 2, d[1], A.periodic[1], wy);
+            const int nz = dim == 3 ? 5 : 1;
+            if (dim == 3) axis_window(c[2], 2, d[2], A.periodic[2], wz);
+            for (int iz = 0; iz < nz; ++iz) {
+                if (wz[iz] < 0) continue;
+                for (int iy = 0; iy < 5; ++iy) {
+                    if (wy[iy] < 0) continue;
+                    for (int ix = 0; ix < 5; ++ix)
+                        if (wx[ix] >= 0) A.stor[l][gi3(d, wx[ix], wy[iy], wz[iz])] = 1;
+                }
+            }
+        }
+    }
+    grid_barrier(A.bar);
     for (int l = 0; l < L; ++l) {
         const int* d = A.tdims[l];
         const int64_t n = (int64_t)d[0] * d[1] * d[2];
         bool changed = false;
         for (int64_t g = tid; g < n; g += nth) {
-            uint8_t k;
-            if (A.own[l][g]) k = 1;
-            else {
-                int c[3];
-                dec3(d, g, c[0], c[1], c[2]);
-                k = window_any(A.own[l], d, dim, A.periodic, c, 2) ? 2 : 0;
-            }
+            const uint8_t k = A.own[l][g] ? 1 : (A.stor[l][g] ? 2 : 0);
             A.nkind[l][g] = k;
             changed |= k != A.kind[l][g];
         }
@@ -356,7 +374,8 @@ using namespace mlbm;
 
 extern "C" int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_t* const* cur,
                                uint8_t* const* eff, uint8_t* const* par, uint8_t* const* own,
-                               uint8_t* const* nkind, int16_t* const* streak, uint8_t* seeds,
+                               uint8_t* const* nkind, uint8_t* const* stor, int16_t* const* streak,
+                               uint8_t* seeds,
                                const uint8_t* static_tiles, const double* x, int64_t xs, int32_t n,
                                int32_t* status, mlbm_error_t* err, unsigned int* bar, void* stream) {
     AdaptArgs A;
@@ -371,6 +390,7 @@ extern "C" int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_
         A.par[l] = par[l];
         A.own[l] = own[l];
         A.nkind[l] = nkind[l];
+        A.stor[l] = stor[l];
         A.streak[l] = streak[l];
     }
     for (int a = 0; a < 3; ++a) A.periodic[a] = h->periodic[a];

@@ -1251,13 +1251,18 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
 // block-wide shared-memory box (one conflict-free RED per lane and row), and
 // the block box is flushed to HBM once.  No coverage tests, no idle-node work.
 template <int D, typename R>
-__global__ void __launch_bounds__(256) k_p2g_cell(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int64_t rs,
+__global__ void __launch_bounds__(128) k_p2g_cell(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int64_t rs,
                                                   mlbm_error_t* err) {
     constexpr int K = Geo<D>::K, NV = 3 + 3 * D, NS = D * (D + 1) / 2;
     constexpr int MAXN = sizeof(R) == 4 ? 512 : 256;
     using PR = PRows<D>;
     __shared__ R sacc[NV * MAXN];
     __shared__ int s_lo[3], s_hi[3];
+    // per-warp particle slabs: one 32-float record per particle, broadcast to
+    // the node lanes with uniform-address vector loads (fp32 only)
+    constexpr bool SLAB = sizeof(R) == 4;
+    constexpr int REC = 32;
+    __shared__ __align__(16) float slab[SLAB ? 4 : 1][SLAB ? 32 * REC : 1];
     const int lane = threadIdx.x & 31;
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = p < P.n;
@@ -1302,6 +1307,26 @@ __global__ void __launch_bounds__(256) k_p2g_cell(PartArgs P, TopoL0 t0, MatPara
         for (int a = 0; a < D; ++a)
 #pragma unroll
             for (int b = a; b < D; ++b) S[k++] = V0 * tau[a * D + b];
+    }
+    if constexpr (SLAB) {
+        float* rec = &slab[threadIdx.x >> 5][lane * REC];
+        int o2 = 0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) rec[o2++] = __int_as_float(a < D ? base[a] : 0);
+#pragma unroll
+        for (int a = 0; a < D; ++a) rec[o2++] = (float)f[a];
+#pragma unroll
+        for (int a = 0; a < D; ++a) rec[o2++] = (float)mv[a];
+#pragma unroll
+        for (int a = 0; a < D; ++a) rec[o2++] = (float)q[a];
+#pragma unroll
+        for (int kk = 0; kk < D * D; ++kk) rec[o2++] = (float)PC[kk];
+#pragma unroll
+        for (int kk = 0; kk < NS; ++kk) rec[o2++] = (float)S[kk];
+        rec[o2++] = (float)m;
+        rec[o2++] = (float)V0;
+        rec[o2++] = (float)ap;
+        __syncwarp();
     }
     // block node box (shared-memory accumulation when it fits)
     if (threadIdx.x < 3) { s_lo[threadIdx.x] = 0x7fffffff; s_hi[threadIdx.x] = -0x7fffffff; }
@@ -1349,8 +1374,48 @@ __global__ void __launch_bounds__(256) k_p2g_cell(PartArgs P, TopoL0 t0, MatPara
     for (int j = 0; j < 32; ++j) {
         if (!((vmask >> j) & 1u)) continue;
         int bj[3];
+        R fj[D], mvj[D], qj[D], Pj[D * D], Sj[NS], mj, V0j, apj;
+        if constexpr (SLAB) {
+            float r[REC];
+            const float4* rp = reinterpret_cast<const float4*>(&slab[threadIdx.x >> 5][j * REC]);
 #pragma unroll
-        for (int a = 0; a < 3; ++a) bj[a] = a < D ? __shfl_sync(0xffffffffu, base[a], j) : 0;
+            for (int v4 = 0; v4 < REC / 4; ++v4) {
+                const float4 t = rp[v4];
+                r[4 * v4] = t.x; r[4 * v4 + 1] = t.y; r[4 * v4 + 2] = t.z; r[4 * v4 + 3] = t.w;
+            }
+            int o2 = 0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) bj[a] = __float_as_int(r[o2++]);
+#pragma unroll
+            for (int a = 0; a < D; ++a) fj[a] = r[o2++];
+#pragma unroll
+            for (int a = 0; a < D; ++a) mvj[a] = r[o2++];
+#pragma unroll
+            for (int a = 0; a < D; ++a) qj[a] = r[o2++];
+#pragma unroll
+            for (int kk = 0; kk < D * D; ++kk) Pj[kk] = r[o2++];
+#pragma unroll
+            for (int kk = 0; kk < NS; ++kk) Sj[kk] = r[o2++];
+            mj = r[o2++];
+            V0j = r[o2++];
+            apj = r[o2++];
+        } else {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) bj[a] = a < D ? __shfl_sync(0xffffffffu, base[a], j) : 0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                fj[a] = __shfl_sync(0xffffffffu, f[a], j);
+                mvj[a] = __shfl_sync(0xffffffffu, mv[a], j);
+                qj[a] = __shfl_sync(0xffffffffu, q[a], j);
+            }
+#pragma unroll
+            for (int kk = 0; kk < D * D; ++kk) Pj[kk] = __shfl_sync(0xffffffffu, PC[kk], j);
+#pragma unroll
+            for (int kk = 0; kk < NS; ++kk) Sj[kk] = __shfl_sync(0xffffffffu, S[kk], j);
+            mj = __shfl_sync(0xffffffffu, m, j);
+            V0j = __shfl_sync(0xffffffffu, V0, j);
+            apj = __shfl_sync(0xffffffffu, ap, j);
+        }
         if (!have || bj[0] != cur[0] || bj[1] != cur[1] || (D == 3 && bj[2] != cur[2])) {
             flush();
 #pragma unroll
@@ -1359,20 +1424,6 @@ __global__ void __launch_bounds__(256) k_p2g_cell(PartArgs P, TopoL0 t0, MatPara
             for (int a = 0; a < 3; ++a) cur[a] = bj[a];
             have = true;
         }
-        R fj[D], mvj[D], qj[D], Pj[D * D], Sj[NS];
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-            fj[a] = __shfl_sync(0xffffffffu, f[a], j);
-            mvj[a] = __shfl_sync(0xffffffffu, mv[a], j);
-            qj[a] = __shfl_sync(0xffffffffu, q[a], j);
-        }
-#pragma unroll
-        for (int k = 0; k < D * D; ++k) Pj[k] = __shfl_sync(0xffffffffu, PC[k], j);
-#pragma unroll
-        for (int k = 0; k < NS; ++k) Sj[k] = __shfl_sync(0xffffffffu, S[k], j);
-        const R mj = __shfl_sync(0xffffffffu, m, j);
-        const R V0j = __shfl_sync(0xffffffffu, V0, j);
-        const R apj = __shfl_sync(0xffffffffu, ap, j);
         R wa[D], dwa[D];
 #pragma unroll
         for (int a = 0; a < D; ++a) {
@@ -1449,7 +1500,7 @@ extern "C" int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, voi
     PartArgs P{lv0->dim, n, x, nullptr, p, ps, nullptr, nullptr, nullptr};
     MatParams mp{lam, mu, alpha, 0.0};
     const TopoL0 t = topo0(lv0);
-#define P2G(D, R) do { if (smem == 3) k_p2g_cell<D, R><<<nblk(n, 256), 256, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
+#define P2G(D, R) do { if (smem == 3) k_p2g_cell<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
                        else if (smem == 2) k_p2g_warp<D, R, 3><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
                        else if (smem) k_p2g_smem<D, R><<<nblk(n, 256), 256, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
                        else k_p2g<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err); } while (0)
