@@ -20,7 +20,13 @@
 // barrier needs co-resident blocks: the kernel is launched cooperatively
 // with at most the occupancy-limited number of blocks.
 #include <algorithm>
+#include <cstdlib>
+#include <cooperative_groups.h>
 #include "common.cuh"
+
+#ifndef MLBM_NO_CG_GRID_SYNC
+#define MLBM_CG_GRID_SYNC 1
+#endif
 
 namespace mlbm {
 
@@ -45,6 +51,7 @@ struct AdaptArgs {
     int32_t* status;        // [levels] changed, [levels..+2] violations
     mlbm_error_t* err;
     unsigned int* bar;      // 2 words, zero-initialised once
+    unsigned long long* ts; // optional stage timestamps (block 0), may be null
 };
 
 __device__ __forceinline__ int64_t gi3(const int* d, int x, int y, int z) {
@@ -58,6 +65,11 @@ __device__ __forceinline__ void dec3(const int* d, int64_t g, int& x, int& y, in
 }
 
 __device__ void grid_barrier(unsigned int* bar) {
+#ifdef MLBM_CG_GRID_SYNC
+    (void)bar;
+    cooperative_groups::this_grid().sync();
+    return;
+#endif
     __syncthreads();
     if (threadIdx.x == 0) {
         volatile unsigned int* vgen = bar + 1;
@@ -156,17 +168,30 @@ __device__ void effective_stage(const AdaptArgs& A, int l, bool with_guard, int6
         int64_t gix[8];
         bool avail[8];
         bool all = true;
-        for (int k = 0; k < K; ++k) {
+        bool cand[8];
+        int16_t st[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (k >= K) break;
             int c[3];
             for (int a = 0; a < 3; ++a) c[a] = (grouped && a < dim) ? 2 * x[a] + ((k >> a) & 1) : x[a];
             const int64_t g = gi3(d, c[0], c[1], c[2]);
             gix[k] = g;
-            const bool cand = A.cur[l][g] && !A.des[l][g];
-            const int16_t s = cand ? (int16_t)(A.streak[l][g] + 1) : (int16_t)0;
-            A.streak[l][g] = s;
+            cand[k] = A.cur[l][g] && !A.des[l][g];
+            st[k] = A.streak[l][g];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (k >= K) break;
+            const int16_t s = cand[k] ? (int16_t)(st[k] + 1) : (int16_t)0;
+            A.streak[l][gix[k]] = s;
             bool guard = false;
-            if (with_guard && cand && s >= 2) guard = window_any(par, d, dim, A.periodic, c, 2);
-            avail[k] = cand && s >= 2 && !guard;
+            if (with_guard && cand[k] && s >= 2) {
+                int c[3];
+                for (int a = 0; a < 3; ++a) c[a] = (grouped && a < dim) ? 2 * x[a] + ((k >> a) & 1) : x[a];
+                guard = window_any(par, d, dim, A.periodic, c, 2);
+            }
+            avail[k] = cand[k] && s >= 2 && !guard;
             all &= avail[k];
         }
         for (int k = 0; k < K; ++k) {
@@ -178,16 +203,141 @@ __device__ void effective_stage(const AdaptArgs& A, int l, bool with_guard, int6
     }
 }
 
+// Branchless, fully unrolled radius-2 windows: out-of-domain taps are
+// redirected to the centre tile and masked, so all 25 / 125 accesses issue
+// back to back (memory-level parallelism instead of a serial loop).
+__device__ __forceinline__ void window_axes(const int* d, const int* per, const int (&c)[3], int dim,
+                                            int (&w)[3][5], unsigned (&ok)[3]) {
+    for (int a = 0; a < 3; ++a) {
+        ok[a] = 0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            int v = c[a] + k - 2;
+            bool in = true;
+            if (a < dim) {
+                if (per[a]) v = v < 0 ? v + d[a] : (v >= d[a] ? v - d[a] : v);
+                else if (v < 0 || v >= d[a]) { in = false; v = c[a]; }
+            } else {
+                v = c[a];
+                in = k == 2;
+            }
+            w[a][k] = v;
+            if (in) ok[a] |= 1u << k;
+        }
+    }
+}
+
+// number of absent (kind == 0) tiles in the radius-2 window
+template <bool UNUSED>
+__device__ __forceinline__ int window_count(const uint8_t* kind, const int* d, int dim, const int* per,
+                                            const int (&c)[3]) {
+    int w[3][5];
+    unsigned ok[3];
+    window_axes(d, per, c, dim, w, ok);
+    int miss = 0;
+#pragma unroll
+    for (int iz = 0; iz < 5; ++iz)
+#pragma unroll
+        for (int iy = 0; iy < 5; ++iy)
+#pragma unroll
+            for (int ix = 0; ix < 5; ++ix) {
+                const bool in = ((ok[2] >> iz) & (ok[1] >> iy) & (ok[0] >> ix)) & 1u;
+                const uint8_t k = kind[gi3(d, w[0][ix], w[1][iy], w[2][iz])];
+                miss += (in && k == 0) ? 1 : 0;
+            }
+    return miss;
+}
+
+__device__ __forceinline__ bool window_any2(const uint8_t* src, const int* d, int dim, const int* per,
+                                            const int (&c)[3]) {
+    int w[3][5];
+    unsigned ok[3];
+    window_axes(d, per, c, dim, w, ok);
+    int any = 0;
+#pragma unroll
+    for (int iz = 0; iz < 5; ++iz)
+#pragma unroll
+        for (int iy = 0; iy < 5; ++iy)
+#pragma unroll
+            for (int ix = 0; ix < 5; ++ix) {
+                const bool in = ((ok[2] >> iz) & (ok[1] >> iy) & (ok[0] >> ix)) & 1u;
+                any |= (in && src[gi3(d, w[0][ix], w[1][iy], w[2][iz])]) ? 1 : 0;
+            }
+    return any != 0;
+}
+
+__device__ __forceinline__ void window_mark(uint8_t* dst, const int* d, int dim, const int* per,
+                                            const int (&c)[3]) {
+    int w[3][5];
+    unsigned ok[3];
+    window_axes(d, per, c, dim, w, ok);
+#pragma unroll
+    for (int iz = 0; iz < 5; ++iz)
+#pragma unroll
+        for (int iy = 0; iy < 5; ++iy)
+#pragma unroll
+            for (int ix = 0; ix < 5; ++ix) {
+                const bool in = ((ok[2] >> iz) & (ok[1] >> iy) & (ok[0] >> ix)) & 1u;
+                if (in) dst[gi3(d, w[0][ix], w[1][iy], w[2][iz])] = 1;
+            }
+}
+
+// Warp-cooperative window pass: the warp scans 32 tiles per iteration, and
+// for every selected tile (ballot) its (2r+1)^dim window is split over the
+// lanes.  op(l, window_tile_index) is called once per in-domain window tile.
+template <typename Sel, typename Op>
+__device__ __forceinline__ void warp_window_pass(const int* d, int dim, const int* per, int64_t n, int r,
+                                                 Sel sel, Op op) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int w = 2 * r + 1, nwin = dim == 3 ? w * w * w : w * w;
+    for (int64_t base = wid * 32; base < n; base += nw * 32) {
+        const int64_t g = base + lane;
+        unsigned m = __ballot_sync(0xffffffffu, g < n && sel(g));
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const int64_t t = base + src;
+            int c[3];
+            dec3(d, t, c[0], c[1], c[2]);
+            for (int k = lane; k < nwin; k += 32) {
+                int o[3] = {k % w - r, (k / w) % w - r, dim == 3 ? k / (w * w) - r : 0};
+                int q[3];
+                bool in = true;
+                for (int a = 0; a < 3; ++a) {
+                    int v = c[a] + o[a];
+                    if (a < dim) {
+                        if (per[a]) v = v < 0 ? v + d[a] : (v >= d[a] ? v - d[a] : v);
+                        else if (v < 0 || v >= d[a]) in = false;
+                    }
+                    q[a] = v;
+                }
+                if (in) op(gi3(d, q[0], q[1], q[2]));
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void stamp(const AdaptArgs& A, int k) {
+    if (A.ts && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        A.ts[k] = t;
+    }
+}
+#define STAMP_BARRIER(k) do { grid_barrier(A.bar); stamp(A, k); } while (0)
+
 __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int dim = A.dim, L = A.levels;
     const int* d0 = A.tdims[0];
     const int64_t n0 = (int64_t)d0[0] * d0[1] * d0[2];
+    stamp(A, 0);
 
     // ---- A: seeds <- static, invariants of the current topology, cur[0]
     for (int64_t g = tid; g < n0; g += nth) {
-        A.seeds[g] = A.static_tiles ? (A.static_tiles[g] ? 1 : 0) : 0;
         A.cur[0][g] = A.kind[0][g] == 1;
         int x[3];
         dec3(d0, g, x[0], x[1], x[2]);
@@ -202,32 +352,18 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
     for (int l = 0; l < L; ++l) {
         const int* d = A.tdims[l];
         const int64_t n = (int64_t)d[0] * d[1] * d[2];
+        // two-tile ring of every leaf: count absent tiles (sparse_grid.py:320-337)
+        const uint8_t* kind = A.kind[l];
         for (int64_t g = tid; g < n; g += nth) {
-            A.stor[l][g] = 0;
-            if (A.kind[l][g] != 1) continue;
-            // two-tile ring of a leaf: count absent tiles (sparse_grid.py:320-337)
+            if (kind[g] != 1) continue;
             int c[3];
             dec3(d, g, c[0], c[1], c[2]);
-            int wx[5], wy[5], wz[5] = {c[2], -1, -1, -1, -1};
-            axis_window(c[0], 2, d[0], A.periodic[0], wx);
-            axis_window(c[1], 2, d[1], A.periodic[1], wy);
-            const int nz = dim == 3 ? 5 : 1;
-            if (dim == 3) axis_window(c[2], 2, d[2], A.periodic[2], wz);
-            int miss = 0;
-            for (int iz = 0; iz < nz; ++iz) {
-                if (wz[iz] < 0) continue;
-                for (int iy = 0; iy < 5; ++iy) {
-                    if (wy[iy] < 0) continue;
-                    for (int ix = 0; ix < 5; ++ix)
-                        if (wx[ix] >= 0 && A.kind[l][gi3(d, wx[ix], wy[iy], wz[iz])] == 0) ++miss;
-                }
-            }
+            const int miss = window_count<false>(kind, d, dim, A.periodic, c);
             if (miss) atomicAdd(&A.status[L + 1], miss);
         }
     }
-    grid_barrier(A.bar);
-
-    // ---- B: particle seeds + particles in level-0 leaves
+    // ---- B (same stage): particle seeds (seeds are all-zero on entry, they are
+    //      cleared at the end of every pass) + particles in level-0 leaves
     for (int64_t p = tid; p < A.n; p += nth) {
         int t[3] = {0, 0, 0};
         bool bad = false;
@@ -243,7 +379,7 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
         A.seeds[g] = 1;
         if (A.kind[0][g] != 1) atomicAdd(&A.status[L + 2], 1);
     }
-    grid_barrier(A.bar);
+    STAMP_BARRIER(2);
 
     // ---- C: des[0], cur[1]
     if (L == 1) {
@@ -257,7 +393,8 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
             for (int k = 0; k < (1 << dim) && !any; ++k) {
                 const int x = g0[0] + (k & 1), y = g0[1] + ((k >> 1) & 1),
                           z = dim == 3 ? g0[2] + ((k >> 2) & 1) : g0[2];
-                any = A.seeds[gi3(d0, x, y, z)] != 0;
+                const int64_t gg = gi3(d0, x, y, z);
+                any = A.seeds[gg] != 0 || (A.static_tiles && A.static_tiles[gg]);
             }
             A.des[0][g] = any;
         }
@@ -269,7 +406,7 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
             A.cur[1][g] = (A.kind[1][g] == 1) || children_any(A.cur[0], d0, dim, c);
         }
     }
-    grid_barrier(A.bar);
+    STAMP_BARRIER(3);
 
     // ---- D/E: desired coverage of coarser levels
     for (int l = 1; l < L; ++l) {
@@ -289,19 +426,19 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
                 A.cur[l + 1][g] = (A.kind[l + 1][g] == 1) || children_any(A.cur[l], d, dim, c);
             }
         }
-        grid_barrier(A.bar);
+        STAMP_BARRIER(4);
         for (int64_t g = tid; g < n; g += nth) {
             if (l == L - 1) { A.des[l][g] = 1; continue; }
             int c[3];
             dec3(d, g, c[0], c[1], c[2]);
             A.des[l][g] = group_window_any(A.par[l], d, dim, A.periodic, c, 2);
         }
-        grid_barrier(A.bar);
+        STAMP_BARRIER(5);
     }
 
     // ---- F/G/H: hysteresis per level
     effective_stage(A, 0, false, tid, nth);
-    grid_barrier(A.bar);
+    STAMP_BARRIER(6);
     for (int l = 1; l < L; ++l) {
         const int* d = A.tdims[l];
         const int64_t n = (int64_t)d[0] * d[1] * d[2];
@@ -310,12 +447,12 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
             dec3(d, g, c[0], c[1], c[2]);
             A.par[l][g] = children_any(A.eff[l - 1], A.tdims[l - 1], dim, c);
         }
-        grid_barrier(A.bar);
+        STAMP_BARRIER(7);
         effective_stage(A, l, true, tid, nth);
-        grid_barrier(A.bar);
+        STAMP_BARRIER(8);
         if (l == L - 1) {
             for (int64_t g = tid; g < n; g += nth) A.eff[l][g] = 1;
-            grid_barrier(A.bar);
+            STAMP_BARRIER(9);
         }
     }
     // par[l] now holds parents(eff[l-1]) for every l >= 1 (eff[L-1] = 1 set
@@ -328,39 +465,23 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
         for (int64_t g = tid; g < n; g += nth)
             A.own[l][g] = A.eff[l][g] && !(l > 0 && A.par[l][g]);
     }
-    grid_barrier(A.bar);
+    STAMP_BARRIER(10);
 
-    // ---- J: storage = dilate2(own) by scattering from own tiles, then the
-    //      new kinds and the no-op flags (adapt.py:184-225)
-    for (int l = 0; l < L; ++l) {
-        const int* d = A.tdims[l];
-        const int64_t n = (int64_t)d[0] * d[1] * d[2];
-        for (int64_t g = tid; g < n; g += nth) {
-            if (!A.own[l][g]) continue;
-            int c[3];
-            dec3(d, g, c[0], c[1], c[2]);
-            int wx[5], wy[5], wz[5] = {c[2], -1, -1, -1, -1};
-            axis_window(c[0], 2, d[0], A.periodic[0], wx);
-            axis_window(c[1], 2, d[1], A.periodic[1], wy);
-            const int nz = dim == 3 ? 5 : 1;
-            if (dim == 3) axis_window(c[2], 2, d[2], A.periodic[2], wz);
-            for (int iz = 0; iz < nz; ++iz) {
-                if (wz[iz] < 0) continue;
-                for (int iy = 0; iy < 5; ++iy) {
-                    if (wy[iy] < 0) continue;
-                    for (int ix = 0; ix < 5; ++ix)
-                        if (wx[ix] >= 0) A.stor[l][gi3(d, wx[ix], wy[iy], wz[iz])] = 1;
-                }
-            }
-        }
-    }
-    grid_barrier(A.bar);
+    // ---- J: storage = dilate2(own) (unrolled gather), new kinds, no-op flags
+    //      (adapt.py:184-225); seeds cleared for the next pass
+    for (int64_t g = tid; g < n0; g += nth) A.seeds[g] = 0;
     for (int l = 0; l < L; ++l) {
         const int* d = A.tdims[l];
         const int64_t n = (int64_t)d[0] * d[1] * d[2];
         bool changed = false;
         for (int64_t g = tid; g < n; g += nth) {
-            const uint8_t k = A.own[l][g] ? 1 : (A.stor[l][g] ? 2 : 0);
+            uint8_t k;
+            if (A.own[l][g]) k = 1;
+            else {
+                int c[3];
+                dec3(d, g, c[0], c[1], c[2]);
+                k = window_any2(A.own[l], d, dim, A.periodic, c) ? 2 : 0;
+            }
             A.nkind[l][g] = k;
             changed |= k != A.kind[l][g];
         }
@@ -372,12 +493,18 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
 
 using namespace mlbm;
 
+extern "C" unsigned long long* mlbm_adapt_timestamps_ptr();
+
+static unsigned long long* g_ts_last = nullptr;
+extern "C" unsigned long long* mlbm_adapt_timestamps_ptr() { return g_ts_last; }
+
 extern "C" int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_t* const* cur,
                                uint8_t* const* eff, uint8_t* const* par, uint8_t* const* own,
                                uint8_t* const* nkind, uint8_t* const* stor, int16_t* const* streak,
                                uint8_t* seeds,
                                const uint8_t* static_tiles, const double* x, int64_t xs, int32_t n,
                                int32_t* status, mlbm_error_t* err, unsigned int* bar, void* stream) {
+    static unsigned long long* ts_env = nullptr;
     AdaptArgs A;
     A.dim = h->dim;
     A.levels = h->levels;
@@ -402,6 +529,12 @@ extern "C" int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_
     A.status = status;
     A.err = err;
     A.bar = bar;
+    A.ts = nullptr;
+    if (getenv("MLBM_ADAPT_TIMESTAMPS")) {
+        if (!ts_env) cudaMalloc(&ts_env, 64 * sizeof(unsigned long long));
+        A.ts = ts_env;
+        g_ts_last = ts_env;
+    }
     static int grid = 0;
     if (grid == 0) {
         int dev = 0, sms = 0, per = 0;

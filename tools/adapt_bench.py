@@ -1,0 +1,36 @@
+"""Time GridAdaptor.plan_device (fused cooperative pass) on the C2 scene."""
+import sys
+sys.path.insert(0, "."); sys.path.insert(0, "tests")
+import torch
+import scenes as S
+from paper_2603_14982_b200.harness import build_scene, validate_scene
+sim = build_scene(validate_scene(S.COLUMN_3D_C2))
+for _ in range(3):
+    sim.step()
+ad = sim.adaptor
+drv = sim._driver()
+torch.cuda.synchronize()
+for fused in (True, False):
+    ad.fused = fused
+    for _ in range(3):
+        ad.plan_device(drv)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        ad.plan_device(drv)
+    e1.record(); torch.cuda.synchronize()
+    print("fused" if fused else "separate", "plan_device us", 1e3 * e0.elapsed_time(e1) / 20)
+import os, ctypes
+from paper_2603_14982_b200 import _lib as L
+if os.environ.get("MLBM_ADAPT_TIMESTAMPS"):
+    ad.fused = True
+    ad.plan_device(drv); torch.cuda.synchronize()
+    lib = L.load()
+    lib.mlbm_adapt_timestamps_ptr.restype = ctypes.c_void_p
+    ptr = lib.mlbm_adapt_timestamps_ptr()
+    buf = (ctypes.c_uint64 * 64)()
+    import ctypes.util
+    cudart = ctypes.CDLL("libcudart.so")
+    cudart.cudaMemcpy(buf, ctypes.c_void_p(ptr), ctypes.c_size_t(64 * 8), 2)
+    ts = list(buf)[:16]
+    print("stage deltas us:", [round((ts[i] - ts[i - 1]) / 1e3, 2) for i in range(1, 16) if ts[i]])
