@@ -180,6 +180,7 @@ class GridAdaptor:
         (status[L:L+3]).  No host synchronisation (CUDA-graph capturable)."""
         if self.fused:
             return self._plan_fused(driver)
+        self._seeds_dirty = True
         topo = self.topology
         lib = L.lib()
         s = L.stream_handle()
@@ -240,6 +241,9 @@ class GridAdaptor:
 
     def _plan_fused(self, driver):
         topo = self.topology
+        if getattr(self, "_seeds_dirty", False):     # left set by the unfused path
+            self._seeds.zero_()
+            self._seeds_dirty = False
         Lv = topo.levels
         arr = lambda ts: (L.C.c_void_p * Lv)(*[t.data_ptr() for t in ts])   # noqa: E731
         x = driver.device_positions(topo.d, topo.device)

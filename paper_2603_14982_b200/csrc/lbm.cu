@@ -20,32 +20,63 @@
 namespace mlbm {
 
 // ---------------------------------------------------------------------------
-// compile-time halo work lists
+// compile-time halo tables.  The (4+2)^D box around a tile minus the tile is
+// the halo: HB cells, each staged once (its Hermite coefficients) in shared
+// memory.  Items are the (halo cell, direction, destination) pulls that enter
+// the tile, sorted by direction so warps stay convergent.
 template <int D> struct HaloTable {
-    static constexpr int N = D == 2 ? 44 : 728;
-    uint32_t item[N];   // nbi | srcl << 5 | dir << 11 | dstl << 16
+    static constexpr int HB = D == 2 ? 20 : 152;     // halo cells
+    static constexpr int N = D == 2 ? 44 : 728;      // halo items
+    uint32_t cell[HB];                               // nbi | srcl << 5
+    uint32_t item[N];                                // h | dir << 8 | dstl << 13
 };
+
+template <int D> constexpr int box_halo_index(int bx, int by, int bz) {
+    // halo cells enumerated in box order (bx fastest), skipping the tile
+    int h = 0;
+    for (int z = (D == 3 ? -1 : 0); z <= (D == 3 ? 4 : 0); ++z)
+        for (int y = -1; y <= 4; ++y)
+            for (int x = -1; x <= 4; ++x) {
+                const bool inside = x >= 0 && x < 4 && y >= 0 && y < 4 && (D == 2 || (z >= 0 && z < 4));
+                if (inside) continue;
+                if (x == bx && y == by && z == bz) return h;
+                ++h;
+            }
+    return -1;
+}
 
 template <int D> constexpr HaloTable<D> make_halo_table() {
     HaloTable<D> h{};
+    int nh = 0;
+    for (int z = (D == 3 ? -1 : 0); z <= (D == 3 ? 4 : 0); ++z)
+        for (int y = -1; y <= 4; ++y)
+            for (int x = -1; x <= 4; ++x) {
+                const bool inside = x >= 0 && x < 4 && y >= 0 && y < 4 && (D == 2 || (z >= 0 && z < 4));
+                if (inside) continue;
+                const int b[3] = {x, y, z};
+                int o[3] = {0, 0, 0}, s[3] = {0, 0, 0};
+                for (int a = 0; a < 3; ++a) {
+                    o[a] = b[a] < 0 ? -1 : (b[a] > 3 ? 1 : 0);
+                    s[a] = b[a] - 4 * o[a];
+                }
+                const int nbi = nb_index<D>(o[0], o[1], o[2]);
+                const int srcl = s[0] + 4 * s[1] + (D == 3 ? 16 * s[2] : 0);
+                h.cell[nh++] = (uint32_t)nbi | ((uint32_t)srcl << 5);
+            }
     int n = 0;
     constexpr int T = Geo<D>::T;
     for (int i = 1; i < Geo<D>::Q; ++i) {
         for (int x = 0; x < T; ++x) {
             int l[3] = {x & 3, (x >> 2) & 3, D == 3 ? (x >> 4) & 3 : 0};
-            int s[3] = {0, 0, 0}, o[3] = {0, 0, 0};
+            int s[3] = {0, 0, 0};
             bool outside = false;
             for (int a = 0; a < 3; ++a) {
                 s[a] = l[a] - cvec<D>(i, a);
-                o[a] = s[a] < 0 ? -1 : (s[a] > 3 ? 1 : 0);
-                if (o[a] != 0) outside = true;
-                s[a] -= 4 * o[a];
+                if (s[a] < 0 || s[a] > 3) outside = true;
             }
             if (!outside) continue;
-            int nbi = nb_index<D>(o[0], o[1], o[2]);
-            int srcl = s[0] + 4 * s[1] + (D == 3 ? 16 * s[2] : 0);
-            h.item[n++] = (uint32_t)nbi | ((uint32_t)srcl << 5) | ((uint32_t)i << 11) |
-                          ((uint32_t)x << 16);
+            const int hidx = box_halo_index<D>(s[0], s[1], s[2]);
+            h.item[n++] = (uint32_t)hidx | ((uint32_t)i << 8) | ((uint32_t)x << 13);
         }
     }
     return h;
@@ -58,6 +89,9 @@ __constant__ HaloTable<3> c_halo3 = k_halo3;
 
 template <int D> __device__ __forceinline__ uint32_t halo_item(int k) {
     if constexpr (D == 2) return c_halo2.item[k]; else return c_halo3.item[k];
+}
+template <int D> __device__ __forceinline__ uint32_t halo_cell(int k) {
+    if constexpr (D == 2) return c_halo2.cell[k]; else return c_halo3.cell[k];
 }
 
 // ---------------------------------------------------------------------------
@@ -123,6 +157,54 @@ __device__ __forceinline__ R g_dir_rt(int i, const Coef<D, R>& c) {
     } else {
         if (i == I) return g_dir<D, I>(c);
         return g_dir_rt<D, R, I + 1>(i, c);
+    }
+}
+
+// coefficient slot layout: dr | A[D] | B[NS] | G[N3]
+template <int D> struct CoefSlots {
+    static constexpr int DR = 0, A = 1, B = 1 + D, G = 1 + D + Geo<D>::NS, N = 1 + D + Geo<D>::NS + Geo<D>::N3;
+};
+
+template <int D, typename R>
+__device__ __forceinline__ void store_coef(const Coef<D, R>& c, R* hc, int h, int HB) {
+    using CS = CoefSlots<D>;
+    hc[CS::DR * HB + h] = c.dr;
+#pragma unroll
+    for (int a = 0; a < D; ++a) hc[(CS::A + a) * HB + h] = c.A[a];
+#pragma unroll
+    for (int k = 0; k < Geo<D>::NS; ++k) hc[(CS::B + k) * HB + h] = c.B[k];
+#pragma unroll
+    for (int t = 0; t < Geo<D>::N3; ++t) hc[(CS::G + t) * HB + h] = c.G[t];
+}
+
+// g_I of a staged halo cell, reading only the coefficients direction I needs
+template <int D, int I, typename R>
+__device__ __forceinline__ R g_dir_staged(const R* hc, int h, int HB) {
+    using CS = CoefSlots<D>;
+    R e = hc[CS::DR * HB + h];
+#pragma unroll
+    for (int k = 0; k < Geo<D>::NS; ++k) {
+        constexpr int dummy = 0; (void)dummy;
+        const double hv = h2v<D>(I, s_a<D>(k), s_b<D>(k));
+        if (hv != 0.0) e += R(hv) * hc[(CS::B + k) * HB + h];
+    }
+    R o = R(0);
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+        if (cvec<D>(I, a) != 0) o += R(cvec<D>(I, a)) * hc[(CS::A + a) * HB + h];
+#pragma unroll
+    for (int t = 0; t < Geo<D>::N3; ++t)
+        if (h3v<D>(I, t) != 0.0) o += R(h3v<D>(I, t)) * hc[(CS::G + t) * HB + h];
+    return R(wdir<D>(I)) * (e + o);
+}
+
+template <int D, typename R, int I = 1>
+__device__ __forceinline__ R g_dir_staged_rt(int i, const R* hc, int h, int HB) {
+    if constexpr (I + 1 >= Geo<D>::Q) {
+        return g_dir_staged<D, I>(hc, h, HB);
+    } else {
+        if (i == I) return g_dir_staged<D, I>(hc, h, HB);
+        return g_dir_staged_rt<D, R, I + 1>(i, hc, h, HB);
     }
 }
 
@@ -193,33 +275,48 @@ __device__ __forceinline__ void pull_all(const R* fb, int lc, bool special, uint
 }
 
 template <int D, typename R>
-__device__ __forceinline__ void halo_work(const StepArgs& A, const FieldsT<R>& src, R* fb,
-                                          const int* snb, int lc, R h3xyz) {
-    constexpr int T = Geo<D>::T;
-    constexpr int NH = HaloTable<D>::N;
-    for (int k = lc; k < NH; k += T) {
-        const uint32_t it = halo_item<D>(k);
-        const int nbi = it & 31, srcl = (it >> 5) & 63, dir = (it >> 11) & 31,
-                  dstl = (it >> 16) & 63;
-        const int ns = snb[nbi];
-        if (ns < 0) continue;
+__device__ __forceinline__ void halo_stage(const FieldsT<R>& src, R* hc, const int* snb, int lc, R h3xyz) {
+    constexpr int T = Geo<D>::T, HB = HaloTable<D>::HB;
+    for (int h = lc; h < HB; h += T) {
+        const uint32_t hcell = halo_cell<D>(h);
+        const int ns = snb[hcell & 31];
+        if (ns < 0) continue;        // absent neighbour: its pulls are special-cased
         R m[Geo<D>::NM];
-        load_moments<D, R>(src, (int64_t)ns * T + srcl, m);
+        load_moments<D, R>(src, (int64_t)ns * T + (int)(hcell >> 5), m);
         Coef<D, R> c;
         make_coef<D, R>(m, h3xyz, c);
-        fb[dir * T + dstl] = g_dir_rt<D, R>(dir, c);
+        store_coef<D, R>(c, hc, h, HB);
+    }
+}
+
+template <int D, typename R>
+__device__ __forceinline__ void halo_items(R* fb, const R* hc, const int* snb, int lc) {
+    constexpr int T = Geo<D>::T, HB = HaloTable<D>::HB, NH = HaloTable<D>::N;
+    for (int k = lc; k < NH; k += T) {
+        const uint32_t it = halo_item<D>(k);
+        const int h = it & 255, dir = (it >> 8) & 31, dstl = (it >> 13) & 63;
+        if (snb[halo_cell<D>(h) & 31] < 0) continue;
+        fb[dir * T + dstl] = g_dir_staged_rt<D, R>(dir, hc, h, HB);
     }
 }
 
 // mode 0 fused, 1 stream only, 2 collide+bc only
+template <int D, typename R> struct LevelCfg {
+    static constexpr int TPC = D == 2 ? 8 : (sizeof(R) == 4 ? 2 : 1);   // tiles per CTA
+    static constexpr int THREADS = TPC * Geo<D>::T;
+};
+
 template <int D, typename R, int MODE>
-__global__ void __launch_bounds__(128) level_kernel(const StepArgs A) {
+__global__ void __launch_bounds__(LevelCfg<D, R>::THREADS) level_kernel(const StepArgs A) {
     constexpr int T = Geo<D>::T, Q = Geo<D>::Q, NS = Geo<D>::NS, NM = Geo<D>::NM;
-    constexpr int TPC = 128 / T;
+    constexpr int TPC = LevelCfg<D, R>::TPC;
+    constexpr int HB = HaloTable<D>::HB, NCO = CoefSlots<D>::N;
     __shared__ R fbuf_all[TPC][Q * T];
+    __shared__ R hcoef_all[MODE == 2 || MODE == 3 || MODE == 4 ? 1 : TPC][MODE == 2 || MODE == 3 || MODE == 4 ? 1 : NCO * HB];
     __shared__ int snb_all[TPC][Geo<D>::NB];
 
     const int grp = threadIdx.x / T, lc = threadIdx.x % T;
+    (void)hcoef_all;
     const int tile = blockIdx.x * TPC + grp;
     const bool valid = tile < A.lv.n_tiles;
     R* fb = fbuf_all[grp];
@@ -251,8 +348,10 @@ __global__ void __launch_bounds__(128) level_kernel(const StepArgs A) {
             make_coef<D, R>(m, h3xyz, own);
             push_pairs<D, R>(own, fb, lc, l);
             fb[lc] = R(wdir<D>(0)) * even_part<D, 0>(own);
-            halo_work<D, R>(A, src, fb, snb, lc, h3xyz);
+            halo_stage<D, R>(src, hcoef_all[grp], snb, lc, h3xyz);
         }
+        __syncthreads();
+        if (valid) halo_items<D, R>(fb, hcoef_all[grp], snb, lc);
         __syncthreads();
         dr = R(0);
 #pragma unroll
@@ -402,15 +501,15 @@ __global__ void __launch_bounds__(128) level_kernel(const StepArgs A) {
 
 template <int D, typename R>
 int launch_level(const StepArgs& a, int mode, cudaStream_t s) {
-    constexpr int TPC = 128 / Geo<D>::T;
+    constexpr int TPC = LevelCfg<D, R>::TPC, NT = LevelCfg<D, R>::THREADS;
     const int blocks = (a.lv.n_tiles + TPC - 1) / TPC;
     if (blocks == 0) return 0;
     switch (mode) {
-    case 0: level_kernel<D, R, 0><<<blocks, 128, 0, s>>>(a); break;
-    case 1: level_kernel<D, R, 1><<<blocks, 128, 0, s>>>(a); break;
-    case 2: level_kernel<D, R, 2><<<blocks, 128, 0, s>>>(a); break;
-    case 3: level_kernel<D, R, 3><<<blocks, 128, 0, s>>>(a); break;
-    default: level_kernel<D, R, 4><<<blocks, 128, 0, s>>>(a); break;
+    case 0: level_kernel<D, R, 0><<<blocks, NT, 0, s>>>(a); break;
+    case 1: level_kernel<D, R, 1><<<blocks, NT, 0, s>>>(a); break;
+    case 2: level_kernel<D, R, 2><<<blocks, NT, 0, s>>>(a); break;
+    case 3: level_kernel<D, R, 3><<<blocks, NT, 0, s>>>(a); break;
+    default: level_kernel<D, R, 4><<<blocks, NT, 0, s>>>(a); break;
     }
     return launch_status(1);
 }
