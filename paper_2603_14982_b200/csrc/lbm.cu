@@ -84,14 +84,17 @@ template <int D> constexpr HaloTable<D> make_halo_table() {
 
 constexpr HaloTable<2> k_halo2 = make_halo_table<2>();
 constexpr HaloTable<3> k_halo3 = make_halo_table<3>();
-__constant__ HaloTable<2> c_halo2 = k_halo2;
-__constant__ HaloTable<3> c_halo3 = k_halo3;
+// in global memory, read through L1 with __ldg: lanes index consecutive
+// entries (coalesced); a __constant__ table would serialise the divergent
+// per-lane indices in the constant cache
+__device__ const HaloTable<2> g_halo2 = k_halo2;
+__device__ const HaloTable<3> g_halo3 = k_halo3;
 
 template <int D> __device__ __forceinline__ uint32_t halo_item(int k) {
-    if constexpr (D == 2) return c_halo2.item[k]; else return c_halo3.item[k];
+    if constexpr (D == 2) return __ldg(&g_halo2.item[k]); else return __ldg(&g_halo3.item[k]);
 }
 template <int D> __device__ __forceinline__ uint32_t halo_cell(int k) {
-    if constexpr (D == 2) return c_halo2.cell[k]; else return c_halo3.cell[k];
+    if constexpr (D == 2) return __ldg(&g_halo2.cell[k]); else return __ldg(&g_halo3.cell[k]);
 }
 
 // ---------------------------------------------------------------------------
