@@ -28,7 +28,7 @@ template <int D> struct HaloTable {
     static constexpr int HB = D == 2 ? 20 : 152;     // halo cells
     static constexpr int N = D == 2 ? 44 : 728;      // halo items
     uint32_t cell[HB];                               // nbi | srcl << 5
-    uint32_t item[N];                                // h | dir << 8 | dstl << 13
+    uint32_t item[N];                                // h | dir << 8 | dstl << 13 | nbi << 19
 };
 
 template <int D> constexpr int box_halo_index(int bx, int by, int bz) {
@@ -76,10 +76,25 @@ template <int D> constexpr HaloTable<D> make_halo_table() {
             }
             if (!outside) continue;
             const int hidx = box_halo_index<D>(s[0], s[1], s[2]);
-            h.item[n++] = (uint32_t)hidx | ((uint32_t)i << 8) | ((uint32_t)x << 13);
+            int o[3] = {0, 0, 0};
+            for (int a = 0; a < 3; ++a) o[a] = s[a] < 0 ? -1 : (s[a] > 3 ? 1 : 0);
+            const int nbi = nb_index<D>(o[0], o[1], o[2]);
+            h.item[n++] = (uint32_t)hidx | ((uint32_t)i << 8) | ((uint32_t)x << 13) | ((uint32_t)nbi << 19);
         }
     }
     return h;
+}
+
+// items of direction i: tile cells whose pull source lies outside the tile
+template <int D> constexpr int halo_count(int i) {
+    int inside = 1;
+    for (int a = 0; a < D; ++a) inside *= 4 - (cvec<D>(i, a) != 0 ? 1 : 0);
+    return Geo<D>::T - inside;
+}
+template <int D> constexpr int halo_offset(int i) {
+    int o = 0;
+    for (int j = 1; j < i; ++j) o += halo_count<D>(j);
+    return o;
 }
 
 constexpr HaloTable<2> k_halo2 = make_halo_table<2>();
@@ -292,8 +307,32 @@ __device__ __forceinline__ void halo_stage(const FieldsT<R>& src, R* hc, const i
     }
 }
 
+// 3D: warp PAR of the tile handles direction 2p+1+PAR of every pair p, one
+// compile-time-specialised direction at a time (no divergence, only the
+// coefficients that direction needs are read)
+template <int D, typename R, int PAR, int P = 0>
+__device__ __forceinline__ void halo_items_dir(R* fb, const R* hc, const int* snb, int lane) {
+    if constexpr (P < Geo<D>::NP) {
+        constexpr int I = 2 * P + 1 + PAR;
+        constexpr int T = Geo<D>::T, HB = HaloTable<D>::HB;
+        constexpr int OFF = halo_offset<D>(I), CNT = halo_count<D>(I);
+#pragma unroll
+        for (int j = lane; j < CNT; j += 32) {
+            const uint32_t it = halo_item<D>(OFF + j);
+            const int h = it & 255, dstl = (it >> 13) & 63, nbi = (it >> 19) & 31;
+            if (snb[nbi] >= 0) fb[I * T + dstl] = g_dir_staged<D, I>(hc, h, HB);
+        }
+        halo_items_dir<D, R, PAR, P + 1>(fb, hc, snb, lane);
+    }
+}
+
 template <int D, typename R>
 __device__ __forceinline__ void halo_items(R* fb, const R* hc, const int* snb, int lc) {
+    if constexpr (D == 3) {
+        if (lc < 32) halo_items_dir<D, R, 0>(fb, hc, snb, lc);
+        else halo_items_dir<D, R, 1>(fb, hc, snb, lc - 32);
+        return;
+    }
     constexpr int T = Geo<D>::T, HB = HaloTable<D>::HB, NH = HaloTable<D>::N;
     for (int k = lc; k < NH; k += T) {
         const uint32_t it = halo_item<D>(k);
