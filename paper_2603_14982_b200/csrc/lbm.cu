@@ -276,19 +276,19 @@ __device__ __forceinline__ void push_pairs(const Coef<D, R>& c, R* fb, int lc, c
     }
 }
 
-template <int D, typename R, int I = 0>
-__device__ __forceinline__ void pull_all(const R* fb, int lc, bool special, uint64_t mask,
+template <int D, typename R, bool SPECIAL, int I = 0>
+__device__ __forceinline__ void pull_all(const R* fb, int lc, uint64_t mask,
                                          const Coef<D, R>& own, R& dr, R (&mm)[D],
                                          R (&pi)[Geo<D>::NS]) {
     if constexpr (I < Geo<D>::Q) {
         constexpr int T = Geo<D>::T;
         R g = fb[I * T + lc];
-        if (special) {
+        if constexpr (SPECIAL) {
             if ((mask >> I) & 1ull) g = g_dir<D, opp<D>(I)>(own);
             else if ((mask >> (32 + I)) & 1ull) g = g_dir<D, I>(own);
         }
         accumulate<D, I>(g, dr, mm, pi);
-        pull_all<D, R, I + 1>(fb, lc, special, mask, own, dr, mm, pi);
+        pull_all<D, R, SPECIAL, I + 1>(fb, lc, mask, own, dr, mm, pi);
     }
 }
 
@@ -402,8 +402,8 @@ __global__ void __launch_bounds__(LevelCfg<D, R>::THREADS) level_kernel(const St
         for (int k = 0; k < NS; ++k) pi[k] = R(0);
         if (valid) {
             const bool special = cf & MLBM_CF_SPECIAL;
-            const uint64_t mask = special ? A.lv.dir_masks[cell] : 0ull;
-            pull_all<D, R>(fb, lc, special, mask, own, dr, mm, pi);
+            if (special) pull_all<D, R, true>(fb, lc, A.lv.dir_masks[cell], own, dr, mm, pi);
+            else pull_all<D, R, false>(fb, lc, 0ull, own, dr, mm, pi);
         }
         if constexpr (MODE == 1) {
             if (valid) {
