@@ -10,6 +10,9 @@ hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
 h = rows[hi]
 data = [r for r in rows[hi + 1:] if len(r) == len(h)]
 ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+mi = h.index("Metric Name") if "Metric Name" in h else None
+if mi is not None:
+    data = [r for r in data if r[mi] == "gpu__time_duration.sum"]
 scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
 agg = collections.defaultdict(lambda: [0, 0.0])
 for r in data[skip:]:
