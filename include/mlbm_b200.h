@@ -73,6 +73,10 @@ typedef struct {
     const uint8_t* cell_flags;  /* [n_tiles * 4^dim] MLBM_CF_* */
     const uint64_t* dir_masks;  /* [n_tiles * 4^dim] bit i: bounce-back dir i; bit 32+i: self source */
     const uint8_t* tile_flags;  /* [n_tiles] MLBM_TF_* */
+    const int32_t* counts;      /* device: [0] live tiles, [1] |I^d|, [2] |I^u| (or NULL:
+                                 * n_tiles is exact).  With counts, n_tiles is the
+                                 * allocated capacity and sizes the launch grids, so a
+                                 * captured CUDA graph survives topology changes. */
 } mlbm_level_t;
 
 typedef struct {
@@ -114,15 +118,18 @@ int mlbm_level_step(const mlbm_level_t* lv, mlbm_fields_t src, mlbm_fields_t dst
                     const mlbm_bc_t* bc, mlbm_error_t* err, void* stream);
 
 /* I^d fill (solver.py:501-526 downward_kernel): targets [n], src [n][2^dim]
- * coarse cell indices (-1 where the weight is zero).  step 1 or 2. */
-int mlbm_downward(int32_t dim, int32_t n, const int32_t* targets, const int32_t* src,
+ * coarse cell indices (-1 where the weight is zero).  step 1 or 2.  n is the
+ * launch capacity; n_dev (device, may be NULL) the live count. */
+int mlbm_downward(int32_t dim, int32_t n, const int32_t* n_dev, const int32_t* targets,
+                  const int32_t* src,
                   const int32_t* fine_tile_xyz,
                   mlbm_fields_t olda, mlbm_fields_t newa, mlbm_fields_t dst,
                   int32_t dtype, int32_t step, double kappa, void* stream);
 
 /* I^u fill (solver.py:536-560 upward_kernel): src [n][2^dim], column 0 is the
  * coincident child; average != 0 uses the 2^dim mean. */
-int mlbm_upward(int32_t dim, int32_t n, const int32_t* targets, const int32_t* src,
+int mlbm_upward(int32_t dim, int32_t n, const int32_t* n_dev, const int32_t* targets,
+                const int32_t* src,
                 mlbm_fields_t fine, mlbm_fields_t dst, int32_t dtype,
                 int32_t average, double kappa, void* stream);
 
@@ -151,10 +158,10 @@ int64_t mlbm_ws_bytes(int64_t n);
 /* Compacts a level's kind grid into sorted slots (x, y, z lexicographic =
  * reference sorted(coords) order).  Writes tile_map, tile_xyz[n][3],
  * tile_kind[n], old_slot[n] (slot of the same tile in old_map or -1) and
- * counts[0] = n tiles, counts[1] = fresh tiles. */
+ * counts[0] = n tiles, counts[1] = fresh tiles; slots >= capacity are not written. */
 int mlbm_compact_tiles(int32_t dim, const int32_t tiles[3], const uint8_t* kind,
                        const int32_t* old_map, int32_t* tile_map, int32_t* tile_xyz,
-                       uint8_t* tile_kind, int32_t* old_slot, int32_t* counts,
+                       uint8_t* tile_kind, int32_t* old_slot, int32_t capacity, int32_t* counts,
                        void* ws, int64_t ws_bytes, void* stream);
 
 /* 3^dim neighbour slots per tile with periodic wrap (-1 absent / outside). */
@@ -213,7 +220,8 @@ int mlbm_plan_level(int32_t n, const uint8_t* own, const uint8_t* storage,
  * between the stages of adapt.py:54-194 + 374-389): seeds, desired / current
  * cumulative coverage, int16 hysteresis, plan, no-op flags status[0..L-1],
  * invariant counts status[L..L+2] of the current topology (ring violations
- * are counted as (leaf, absent neighbour) pairs).  Per-level buffer
+ * are counted as (leaf, absent neighbour) pairs), and per level the tile count
+ * status[L+4+l] and fresh-tile count status[2L+4+l] of the new plan.  Per-level buffer
  * arrays have h->levels entries; bar: 2 zero-initialised words. */
 int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_t* const* cur,
                     uint8_t* const* eff, uint8_t* const* par, uint8_t* const* own,
@@ -233,7 +241,8 @@ int mlbm_check_particles(int32_t dim, int32_t n, const void* x, int64_t xstride,
 
 /* Data migration after a rebuild (adapt.py:259-283): both trees, surviving
  * tiles bitwise, fresh tiles get drho = 0, eps = 1, others 0. */
-int mlbm_migrate_level(int32_t dim, int32_t n_new_tiles, const int32_t* old_slot,
+int mlbm_migrate_level(int32_t dim, int32_t n_new_tiles, const int32_t* n_dev,
+                       const int32_t* old_slot,
                        mlbm_fields_t old0, mlbm_fields_t old1, mlbm_fields_t new0,
                        mlbm_fields_t new1, int32_t dtype, void* stream);
 
@@ -244,6 +253,7 @@ int mlbm_migrate_level(int32_t dim, int32_t n_new_tiles, const int32_t* old_slot
  * 1 paper_literal.  Unfilled cells counted into viol[0]. */
 int mlbm_init_new_cells(const mlbm_hier_t* old_h, const mlbm_hier_t* nh, int32_t level,
                         const int32_t* tile_xyz, const int32_t* old_slot, int32_t n_tiles,
+                        const int32_t* n_dev,
                         mlbm_fields_t new0, mlbm_fields_t new1, const double* taus,
                         int32_t conv, int32_t dtype, int32_t* viol, void* stream);
 

@@ -73,7 +73,8 @@ class Level(C.Structure):
                 ("periodic", C.c_int32 * 3), ("n_tiles", C.c_int32),
                 ("tile_map", C.c_void_p), ("tile_xyz", C.c_void_p),
                 ("nbr", C.c_void_p), ("cell_flags", C.c_void_p),
-                ("dir_masks", C.c_void_p), ("tile_flags", C.c_void_p)]
+                ("dir_masks", C.c_void_p), ("tile_flags", C.c_void_p),
+                ("counts", C.c_void_p)]
 
 
 class Fields(C.Structure):
@@ -117,10 +118,10 @@ D = C.c_double
 _SIGS = {
     "mlbm_level_step": [C.POINTER(Level), Fields, Fields, I32, I32,
                         C.POINTER(Collide), C.POINTER(BC), P, P],
-    "mlbm_downward": [I32, I32, P, P, P, Fields, Fields, Fields, I32, I32, D, P],
-    "mlbm_upward": [I32, I32, P, P, Fields, Fields, I32, I32, D, P],
+    "mlbm_downward": [I32, I32, P, P, P, P, Fields, Fields, Fields, I32, I32, D, P],
+    "mlbm_upward": [I32, I32, P, P, P, Fields, Fields, I32, I32, D, P],
     "mlbm_ws_bytes": [I64],
-    "mlbm_compact_tiles": [I32, P, P, P, P, P, P, P, P, P, I64, P],
+    "mlbm_compact_tiles": [I32, P, P, P, P, P, P, P, I32, P, P, I64, P],
     "mlbm_build_neighbors": [C.POINTER(Level), P, P],
     "mlbm_classify_level": [C.POINTER(Level), C.POINTER(Hier), C.POINTER(BC),
                             C.POINTER(Solid), P, P, P, P, P, P],
@@ -134,8 +135,8 @@ _SIGS = {
     "mlbm_check_coverage": [C.POINTER(Hier), P, P],
     "mlbm_count_ring_violations": [I64, P, P, P, P],
     "mlbm_check_particles": [I32, I32, P, I64, I32, P, P, P, P],
-    "mlbm_migrate_level": [I32, I32, P, Fields, Fields, Fields, Fields, I32, P],
-    "mlbm_init_new_cells": [C.POINTER(Hier), C.POINTER(Hier), I32, P, P, I32,
+    "mlbm_migrate_level": [I32, I32, P, P, Fields, Fields, Fields, Fields, I32, P],
+    "mlbm_init_new_cells": [C.POINTER(Hier), C.POINTER(Hier), I32, P, P, I32, P,
                             Fields, Fields, P, I32, I32, P, P],
     "mlbm_adapt_pass": [C.POINTER(Hier), P, P, P, P, P, P, P, P, P, P, P, I64, I32, P, P, P, P],
     "mlbm_raster_rows": [I32],

@@ -114,7 +114,8 @@ class GridAdaptor:
         self._tmp = [z(k) for k in n]
         self._new = [z(k) for k in n]
         self._seeds = z(n[0])
-        self._status = torch.zeros(topology.levels + 4, dtype=torch.int32, device=dev)
+        # [changed L][violations 3][pad][new tile counts L][fresh tile counts L]
+        self._status = torch.zeros(3 * topology.levels + 4, dtype=torch.int32, device=dev)
         self._err = torch.zeros(L.ERR_INTS, dtype=torch.int32, device=dev)
         self._taus = torch.tensor(level_params.taus, dtype=torch.float64, device=dev)
         self._static_key = None
@@ -237,6 +238,9 @@ class GridAdaptor:
                                         L.ptr(self._new[l]), L.ptr(self._status[l:l + 1]), s),
                     "plan_level")
             self.launches += 1
+            nz = self._new[l] != 0
+            self._status[Lv + 4 + l] = nz.sum().to(torch.int32)
+            self._status[2 * Lv + 4 + l] = (nz & (topo.lv[l].kind == 0)).sum().to(torch.int32)
         self._invariants_device(driver)
 
     def _plan_fused(self, driver):
@@ -260,9 +264,12 @@ class GridAdaptor:
                 "adapt_pass")
         self.launches += 1
 
-    def finish(self, driver, pair, status, err) -> AdaptReport:
-        """Host half: raise on seed errors, rebuild + migrate if a level
-        changed (then re-check the invariants), build the report."""
+    def finish(self, driver, pair, status, err, check_after=True) -> AdaptReport:
+        """Host half: raise on seed errors; when a level changed, rebuild and
+        migrate on the device without host synchronisation (the new counts
+        come from the adapt pass); build the report.  ``check_after`` re-runs
+        the invariants on the new topology (one readback); the graph path
+        skips it and the next pass reports them."""
         topo = self.topology
         Lv = topo.levels
         rep = AdaptReport(created=[0] * Lv, deleted=[0] * Lv)
@@ -273,51 +280,63 @@ class GridAdaptor:
         viol = status[Lv:Lv + 3]
         if changed:
             rep.noop = False
-            self._apply(changed, pair, rep)
-            self._invariants_device(driver)
-            viol = self._status[Lv:Lv + 3].cpu().numpy()
+            new_counts = [int(v) for v in status[Lv + 4:2 * Lv + 4]]
+            fresh = [int(v) for v in status[2 * Lv + 4:3 * Lv + 4]]
+            self._apply(changed, pair, rep, new_counts, fresh)
+            if check_after:
+                self._invariants_device(driver)
+                viol = self._status[Lv:Lv + 3].cpu().numpy()
+            else:
+                viol = (0, 0, 0)
         self._report_invariants(viol, rep)
         return rep
 
-    def _apply(self, changed, pair, rep):
+    def _apply(self, changed, pair, rep, new_counts, fresh):
+        """Rebuild + bitwise migration + new-cell init (adapt.py:232-372),
+        device-only: compaction into the spare tile map, neighbours,
+        migration into the scratch blocks, initialisation from the old
+        hierarchy, then the scratch / maps / kinds become current."""
         topo = self.topology
         lib = L.lib()
         s = L.stream_handle()
         d = topo.d
-        T = TILE ** d
-        # snapshot of the old hierarchy (tile maps, kinds, fields)
-        old_h = topo.hier_struct(pair)
-        keep = [(topo.lv[l].tile_map, topo.lv[l].kind) for l in range(topo.levels)]
-        old_blocks = [[pair.trees[t].levels[l].data for l in range(topo.levels)] for t in range(2)]
-        old_counts = [topo.n_tiles(l) for l in range(topo.levels)]
-        topo.rebuild({l: self._new[l].clone() for l in changed})
         dcode = dtype_code(pair.dtype)
-        viol = torch.zeros(1, dtype=torch.int32, device=topo.device)
+        old_counts = [topo.n_tiles(l) for l in range(topo.levels)]
+        grown = False
+        for l in changed:
+            grown |= topo.ensure_capacity(l, new_counts[l])
+        if grown:
+            pair.ensure_capacity()
+        old_h = topo.hier_struct(pair)           # old maps, old fields, old counts
+        for l in changed:
+            topo.compact(l, self._new[l])
+        for l in changed:
+            topo.build_neighbors(l, new_map=True)
         new_h = topo.hier_struct()
-        conv = 0 if self.rescale_convention == "derived" else 1
         for l in changed:
             lt = topo.lv[l]
-            n_new = lt.n_tiles
-            rep.created[l] = lt.created
-            rep.deleted[l] = old_counts[l] - (n_new - lt.created)
-            nb = [fresh_block(d, n_new * T, pair.dtype, topo.device) for _ in range(2)]
-            if n_new:
-                L.check(lib.mlbm_migrate_level(d, n_new, L.ptr(lt.old_slot),
-                                               L.fields(old_blocks[0][l]), L.fields(old_blocks[1][l]),
-                                               L.fields(nb[0]), L.fields(nb[1]), dcode, s),
-                        "migrate_level")
-                if lt.created:
-                    L.check(lib.mlbm_init_new_cells(L.C.byref(old_h), L.C.byref(new_h), l,
-                                                    L.ptr(lt.tile_xyz), L.ptr(lt.old_slot), n_new,
-                                                    L.fields(nb[0]), L.fields(nb[1]),
-                                                    L.ptr(self._taus), conv, dcode, L.ptr(viol), s),
-                            "init_new_cells")
+            rep.created[l] = fresh[l]
+            rep.deleted[l] = old_counts[l] - (new_counts[l] - fresh[l])
+            sb = pair.scratch_blocks(l)
+            cnt = L.ptr(topo.dcounts[l])
+            L.check(lib.mlbm_migrate_level(d, lt.cap, cnt, L.ptr(lt.old_slot),
+                                           L.fields(pair.trees[0].levels[l].data),
+                                           L.fields(pair.trees[1].levels[l].data),
+                                           L.fields(sb[0]), L.fields(sb[1]), dcode, s),
+                    "migrate_level")
+            if fresh[l]:
+                conv = 0 if self.rescale_convention == "derived" else 1
+                L.check(lib.mlbm_init_new_cells(L.C.byref(old_h), L.C.byref(new_h), l,
+                                                L.ptr(lt.tile_xyz), L.ptr(lt.old_slot), lt.cap,
+                                                cnt, L.fields(sb[0]), L.fields(sb[1]),
+                                                L.ptr(self._taus), conv, dcode,
+                                                L.ptr(self._status[Lv_slot(topo)]), s),
+                        "init_new_cells")
+        for l in changed:
+            sb = pair.scratch_blocks(l)
             for t in range(2):
-                pair.trees[t].levels[l] = LevelFields(d, nb[t])
-        nv = int(viol.item())
-        if nv:
-            rep.violations.append(("uninitialized cell", nv))
-        del keep
+                pair.trees[t].levels[l].data.copy_(sb[t])
+        topo.commit({l: self._new[l] for l in changed}, {l: new_counts[l] for l in changed})
 
     def _invariants_device(self, driver):
         """Coverage, two-tile rings, particles in level-0 leaves
@@ -349,6 +368,11 @@ class GridAdaptor:
             rep.violations.append(("invariant", f"{cnt[1]} ring tiles missing"))
         if cnt[2]:
             rep.violations.append(("particle not in level-0 leaf", int(cnt[2])))
+
+
+def Lv_slot(topo):
+    """status word receiving uninitialised-cell counts (the pad slot)"""
+    return topo.levels + 3
 
 
 def update_grid(adaptor: GridAdaptor, driver: RefineDriver, pair) -> AdaptReport:

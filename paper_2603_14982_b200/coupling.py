@@ -107,7 +107,8 @@ class CouplingFields:
     def __init__(self, grid: MpmGrid, tree_level0):
         d = grid.d
         self.d = d
-        r = grid.ras
+        n = grid._live()
+        r = grid.ras[:, :n]
         R = grid.R
         self.eps = r[R["eps"]]
         self.eta = r[R["eta"]]
@@ -118,7 +119,7 @@ class CouplingFields:
         self.grad_term = r[R["grad"]:R["grad"] + d].t()
         self.rel = r[R["rel"]:R["rel"] + d].t()
         base = tree_level0.index["f" + "x"]
-        self.force = tree_level0.data[base:base + d].t()
+        self.force = tree_level0.data[base:base + d, :n].t()
 
 
 class CoupledSim:
@@ -161,7 +162,7 @@ class CoupledSim:
         # one int32 block holding every device status word of the step (error
         # records, counters, adapt flags) -> a single D2H copy per step
         ne = L.ERR_INTS
-        nst = self.topology.levels + 4 if adaptor is not None else 0
+        nst = 3 * self.topology.levels + 4 if adaptor is not None else 0
         self._sblock = torch.zeros(2 * ne + 2 + nst + (ne if adaptor is not None else 0),
                                    dtype=torch.int32, device=self.topology.device)
         self._sblock[:ne].copy_(solver._err)
@@ -321,10 +322,11 @@ class CoupledSim:
     def _step_graph(self, ci, is_mpm, adapt_now):
         solver = self.solver
         topo = self.topology
-        if self._graph_ver != topo.version:
+        gver = (topo.cap_version, tuple(topo.n_tiles(l) > 0 for l in range(topo.levels)))
+        if self._graph_ver != gver:
             self._graphs.clear()
-            self._pool = None          # graphs of the old topology freed with their pool
-            self._graph_ver = topo.version
+            self._pool = None          # graphs of the old capacities freed with their pool
+            self._graph_ver = gver
         # persistent buffers are allocated outside any capture
         if self.sort_particles and len(self.particles):
             self.particles.scratch()
@@ -386,16 +388,21 @@ class CoupledSim:
             self.grid._err.copy_(torch.as_tensor(gerr, dtype=torch.int32))
             self.grid.raise_pending()
         if adapt_now:
-            nst = self.topology.levels + 4
+            nst = 3 * self.topology.levels + 4
             status = h[2 * ne + 2:2 * ne + 2 + nst]
             err = h[2 * ne + 2 + nst:]
-            self.last_report = self.adaptor.finish(self._driver(), self.pair, status, err)
+            self.last_report = self.adaptor.finish(self._driver(), self.pair, status, err,
+                                                   check_after=False)
             if not self.last_report.noop:
+                # device-only rebuild already queued; the diagnostics row of
+                # this step is taken on the new topology (coupling.py:481)
                 self.topology_changes += 1
                 self.grid.sync_topology()
                 self.solver._refresh_tables()
                 self._record_diagnostics()
-                diag = self._diag_buf.cpu().numpy()
+                self._host_f64.copy_(self._diag_buf, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                diag = self._host_f64.numpy().copy()
         self._push_diag_row(diag)
 
     def _powder_tmp(self):

@@ -474,6 +474,7 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
         const int* d = A.tdims[l];
         const int64_t n = (int64_t)d[0] * d[1] * d[2];
         bool changed = false;
+        int cnt = 0, fresh = 0;
         for (int64_t g = tid; g < n; g += nth) {
             uint8_t k;
             if (A.own[l][g]) k = 1;
@@ -483,9 +484,20 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
                 k = window_any2(A.own[l], d, dim, A.periodic, c) ? 2 : 0;
             }
             A.nkind[l][g] = k;
-            changed |= k != A.kind[l][g];
+            const uint8_t old = A.kind[l][g];
+            changed |= k != old;
+            cnt += k != 0;
+            fresh += (k != 0 && old == 0);
         }
         if (__syncthreads_or(changed) && threadIdx.x == 0) atomicOr(&A.status[l], 1);
+        for (int off = 16; off > 0; off >>= 1) {
+            cnt += __shfl_down_sync(0xffffffffu, cnt, off);
+            fresh += __shfl_down_sync(0xffffffffu, fresh, off);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (cnt) atomicAdd(&A.status[L + 4 + l], cnt);
+            if (fresh) atomicAdd(&A.status[2 * L + 4 + l], fresh);
+        }
     }
 }
 

@@ -116,6 +116,11 @@ __device__ __forceinline__ void report_error(mlbm_error_t* err, int code, int le
     }
 }
 
+// live tiles of a level: the device count when present, else n_tiles
+__device__ __forceinline__ int live_tiles(const mlbm_level_t& lv) {
+    return lv.counts ? __ldg(lv.counts) : lv.n_tiles;
+}
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // returns the number of kernels launched (>= 0) or -cudaError

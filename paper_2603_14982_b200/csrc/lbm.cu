@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(LevelCfg<D, R>::THREADS) level_kernel(const St
     const int grp = threadIdx.x / T, lc = threadIdx.x % T;
     (void)hcoef_all;
     const int tile = blockIdx.x * TPC + grp;
-    const bool valid = tile < A.lv.n_tiles;
+    const bool valid = tile < live_tiles(A.lv);
     R* fb = fbuf_all[grp];
     int* snb = snb_all[grp];
     const FieldsT<R> src = fields_of<R>(A.src), dst = fields_of<R>(A.dst);
@@ -558,14 +558,14 @@ int launch_level(const StepArgs& a, int mode, cudaStream_t s) {
 
 // ---------------------------------------------------------------------------
 template <int D, typename R>
-__global__ void downward_kernel(int n, const int32_t* __restrict__ targets,
+__global__ void downward_kernel(int n, const int32_t* __restrict__ n_dev, const int32_t* __restrict__ targets,
                                 const int32_t* __restrict__ srcs,
                                 const int32_t* __restrict__ tile_xyz,
                                 FieldsT<R> olda, FieldsT<R> newa, FieldsT<R> dst,
                                 int step, R kappa) {
     constexpr int NC = Geo<D>::NC, NS = Geo<D>::NS, T = Geo<D>::T;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
+    if (j >= (n_dev ? __ldg(n_dev) : n)) return;
     const int tgt = targets[j];
     const int slot = tgt / T, lc = tgt % T;
     int par[3] = {lc & 1, (lc >> 2) & 1, (lc >> 4) & 1};
@@ -613,12 +613,12 @@ __global__ void downward_kernel(int n, const int32_t* __restrict__ targets,
 }
 
 template <int D, typename R>
-__global__ void upward_kernel(int n, const int32_t* __restrict__ targets,
+__global__ void upward_kernel(int n, const int32_t* __restrict__ n_dev, const int32_t* __restrict__ targets,
                               const int32_t* __restrict__ srcs, FieldsT<R> fine,
                               FieldsT<R> dst, int average, R kappa) {
     constexpr int NC = Geo<D>::NC, NS = Geo<D>::NS;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
+    if (j >= (n_dev ? __ldg(n_dev) : n)) return;
     const int tgt = targets[j];
     constexpr int NV = Geo<D>::NM + 2;
     R v[NV];
@@ -661,14 +661,15 @@ extern "C" int mlbm_level_step(const mlbm_level_t* lv, mlbm_fields_t src, mlbm_f
     return -1;
 }
 
-extern "C" int mlbm_downward(int32_t dim, int32_t n, const int32_t* targets, const int32_t* src,
+extern "C" int mlbm_downward(int32_t dim, int32_t n, const int32_t* n_dev, const int32_t* targets,
+                             const int32_t* src,
                              const int32_t* tile_xyz, mlbm_fields_t olda, mlbm_fields_t newa,
                              mlbm_fields_t dst, int32_t dtype, int32_t step, double kappa,
                              void* stream) {
     if (n <= 0) return 0;
     cudaStream_t s = as_stream(stream);
     const int B = 128, G = (n + B - 1) / B;
-#define DOWN(D, R) downward_kernel<D, R><<<G, B, 0, s>>>(n, targets, src, tile_xyz, \
+#define DOWN(D, R) downward_kernel<D, R><<<G, B, 0, s>>>(n, n_dev, targets, src, tile_xyz, \
         fields_of<R>(olda), fields_of<R>(newa), fields_of<R>(dst), step, R(kappa))
     if (dim == 2) { if (dtype) DOWN(2, double); else DOWN(2, float); }
     else if (dim == 3) { if (dtype) DOWN(3, double); else DOWN(3, float); }
@@ -677,13 +678,14 @@ extern "C" int mlbm_downward(int32_t dim, int32_t n, const int32_t* targets, con
     return launch_status(1);
 }
 
-extern "C" int mlbm_upward(int32_t dim, int32_t n, const int32_t* targets, const int32_t* src,
+extern "C" int mlbm_upward(int32_t dim, int32_t n, const int32_t* n_dev, const int32_t* targets,
+                           const int32_t* src,
                            mlbm_fields_t fine, mlbm_fields_t dst, int32_t dtype,
                            int32_t average, double kappa, void* stream) {
     if (n <= 0) return 0;
     cudaStream_t s = as_stream(stream);
     const int B = 128, G = (n + B - 1) / B;
-#define UP(D, R) upward_kernel<D, R><<<G, B, 0, s>>>(n, targets, src, fields_of<R>(fine), \
+#define UP(D, R) upward_kernel<D, R><<<G, B, 0, s>>>(n, n_dev, targets, src, fields_of<R>(fine), \
         fields_of<R>(dst), average, R(kappa))
     if (dim == 2) { if (dtype) UP(2, double); else UP(2, float); }
     else if (dim == 3) { if (dtype) UP(3, double); else UP(3, float); }

@@ -398,7 +398,7 @@ __global__ void k_exchange(ExchArgs A) {
     constexpr int T = Geo<D>::T;
     using RW = Rows<D>;
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= (int64_t)A.lv.n_tiles * T) return;
+    if (c >= (int64_t)live_tiles(A.lv) * T) return;
     R* ras = (R*)A.ras;
     const int64_t rs = A.rs;
     const FieldsT<R> wt = fields_of<R>(A.w_tree), rt = fields_of<R>(A.r_tree);
@@ -748,7 +748,7 @@ template <int D, typename R>
 __global__ void k_powder_advect(PowderArgs A) {
     constexpr int T = Geo<D>::T;
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= (int64_t)A.lv.n_tiles * T) return;
+    if (c >= (int64_t)live_tiles(A.lv) * T) return;
     const FieldsT<R> src = fields_of<R>(A.src), dst = fields_of<R>(A.dst);
     const int slot = (int)(c / T), lc = (int)(c % T);
     const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
@@ -771,7 +771,7 @@ __global__ void k_powder_diffuse(PowderArgs A) {
     constexpr int T = Geo<D>::T, NS = Geo<D>::NS;
     using RW = Rows<D>;
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= (int64_t)A.lv.n_tiles * T) return;
+    if (c >= (int64_t)live_tiles(A.lv) * T) return;
     const FieldsT<R> dst = fields_of<R>(A.dst);
     const R* adv = (const R*)A.tmp;
     const R* ras = (const R*)A.ras;
@@ -858,7 +858,7 @@ __global__ void k_diag_level(mlbm_level_t lv, mlbm_fields_t f, double vol, doubl
     for (int k = 0; k <= D; ++k) acc[k] = 0.0;
     double emin = 1e300;
     const FieldsT<R> a = fields_of<R>(f);
-    const int64_t n = (int64_t)lv.n_tiles * T;
+    const int64_t n = (int64_t)live_tiles(lv) * T;
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
          c += (int64_t)gridDim.x * blockDim.x) {
         if (!(lv.cell_flags[c] & MLBM_CF_LEAF)) continue;

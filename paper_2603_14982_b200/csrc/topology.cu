@@ -66,11 +66,11 @@ __global__ void k_kind_flags(int64_t n, const uint8_t* kind, int32_t* flags, int
 
 __global__ void k_scatter_tiles(int64_t n, I3 td, const uint8_t* kind, const int32_t* pos,
                                 const int32_t* old_map, int32_t* tile_map, int32_t* tile_xyz,
-                                uint8_t* tile_kind, int32_t* old_slot, int32_t* counts) {
+                                uint8_t* tile_kind, int32_t* old_slot, int32_t cap, int32_t* counts) {
     int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (g >= n) return;
     const uint8_t k = kind[g];
-    if (k) {
+    if (k && pos[g] < cap) {
         const int slot = pos[g];
         tile_map[g] = slot;
         int x, y, z;
@@ -105,7 +105,7 @@ template <int D>
 __global__ void k_neighbors(mlbm_level_t lv, int32_t* nbr) {
     constexpr int NB = Geo<D>::NB;
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= (int64_t)lv.n_tiles * NB) return;
+    if (j >= (int64_t)live_tiles(lv) * NB) return;
     const int t = (int)(j / NB), k = (int)(j % NB);
     const int o[3] = {k % 3 - 1, (k / 3) % 3 - 1, D == 3 ? k / 9 - 1 : 0};
     int c[3];
@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
     constexpr int T = Geo<D>::T, NB = Geo<D>::NB, Q = Geo<D>::Q;
     const int tile = blockIdx.x, lc = threadIdx.x;
     const int level = lv.level;
+    if (tile >= live_tiles(lv)) return;      // block-uniform
     __shared__ int snb[NB];
     if (lc < NB) snb[lc] = lv.nbr[(int64_t)tile * NB + lc];
     const int tx[3] = {lv.tile_xyz[tile * 3], lv.tile_xyz[tile * 3 + 1], lv.tile_xyz[tile * 3 + 2]};
@@ -262,9 +263,9 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
 
 // ---------------------------------------------------------------------------
 // interfaces
-__global__ void k_iface_flags(int64_t n, const uint8_t* cf, uint8_t bit, int8_t* out) {
+__global__ void k_iface_flags(int64_t n, mlbm_level_t lv, int T, const uint8_t* cf, uint8_t bit, int8_t* out) {
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c < n) out[c] = (cf[c] & bit) ? 1 : 0;
+    if (c < n) out[c] = (c < (int64_t)live_tiles(lv) * T && (cf[c] & bit)) ? 1 : 0;
 }
 
 template <int D>
@@ -454,11 +455,11 @@ __global__ void k_particle_leaf(int dim, int n, const R* x, int64_t xs, I3 t0, c
 // ---------------------------------------------------------------------------
 // migration + new-cell init (adapt.py:259-372)
 template <int D, typename R>
-__global__ void k_migrate(int64_t ncells, const int32_t* old_slot, FieldsT<R> o0, FieldsT<R> o1,
-                          FieldsT<R> n0, FieldsT<R> n1) {
+__global__ void k_migrate(int64_t ncells, const int32_t* n_dev, const int32_t* old_slot, FieldsT<R> o0,
+                          FieldsT<R> o1, FieldsT<R> n0, FieldsT<R> n1) {
     constexpr int T = Geo<D>::T, NF = Geo<D>::NF;
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= ncells) return;
+    if (c >= ncells || (n_dev && c >= (int64_t)__ldg(n_dev) * T)) return;
     const int os = old_slot[c / T];
     const int64_t oc = (int64_t)os * T + c % T;
 #pragma unroll
@@ -474,11 +475,11 @@ MLBM_HD double kap_up(double tf, double tc, int conv) { return conv == 0 ? 2.0 *
 
 template <int D, typename R>
 __global__ void k_init_new(mlbm_hier_t oh, mlbm_hier_t nh, int level, const int32_t* tile_xyz,
-                           const int32_t* old_slot, int n_tiles, FieldsT<R> n0, FieldsT<R> n1,
-                           const double* taus, int conv, int32_t* viol) {
+                           const int32_t* old_slot, int n_tiles, const int32_t* n_dev, FieldsT<R> n0,
+                           FieldsT<R> n1, const double* taus, int conv, int32_t* viol) {
     constexpr int T = Geo<D>::T, NC = Geo<D>::NC, NS = Geo<D>::NS, NM = Geo<D>::NM;
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= (int64_t)n_tiles * T) return;
+    if (c >= (int64_t)n_tiles * T || (n_dev && c >= (int64_t)__ldg(n_dev) * T)) return;
     const int slot = (int)(c / T), lc = (int)(c % T);
     if (old_slot[slot] >= 0) return;
     const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
@@ -581,8 +582,8 @@ extern "C" int64_t mlbm_ws_bytes(int64_t n) {
 
 extern "C" int mlbm_compact_tiles(int32_t dim, const int32_t tiles[3], const uint8_t* kind,
                                   const int32_t* old_map, int32_t* tile_map, int32_t* tile_xyz,
-                                  uint8_t* tile_kind, int32_t* old_slot, int32_t* counts,
-                                  void* ws, int64_t ws_bytes, void* stream) {
+                                  uint8_t* tile_kind, int32_t* old_slot, int32_t capacity,
+                                  int32_t* counts, void* ws, int64_t ws_bytes, void* stream) {
     (void)dim;
     const int64_t n = (int64_t)tiles[0] * tiles[1] * tiles[2];
     if (n <= 0 || ws_bytes < mlbm_ws_bytes(n)) return -1;
@@ -596,7 +597,7 @@ extern "C" int mlbm_compact_tiles(int32_t dim, const int32_t tiles[3], const uin
     cub::DeviceScan::ExclusiveSum(tmp, tmpb, flags, pos, (int)n, s);
     I3 td{{tiles[0], tiles[1], tiles[2]}};
     k_scatter_tiles<<<blocks_for(n, 256), 256, 0, s>>>(n, td, kind, pos, old_map, tile_map, tile_xyz,
-                                                       tile_kind, old_slot, counts);
+                                                       tile_kind, old_slot, capacity, counts);
     return launch_status(4);
 }
 
@@ -616,6 +617,7 @@ extern "C" int mlbm_classify_level(const mlbm_level_t* lv, const mlbm_hier_t* h,
                                    void* stream) {
     if (lv->n_tiles == 0) return 0;
     cudaStream_t s = as_stream(stream);
+    if (counts) cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), s);
     if (lv->dim == 2)
         k_classify<2><<<lv->n_tiles, 16, 0, s>>>(*lv, *h, *bc, *solid, cell_flags, dir_masks,
                                                  tile_flags, counts, err);
@@ -637,7 +639,7 @@ extern "C" int mlbm_build_interface(const mlbm_level_t* lv, const mlbm_level_t* 
     int8_t* fl = (int8_t*)w;
     void* tmp = w + 2 * align256(4 * n);
     size_t tmpb = (size_t)cub_temp_bytes(n);
-    k_iface_flags<<<blocks_for(n, 256), 256, 0, s>>>(n, lv->cell_flags,
+    k_iface_flags<<<blocks_for(n, 256), 256, 0, s>>>(n, *lv, T, lv->cell_flags,
                                                      which == 0 ? MLBM_CF_GHOST_D : MLBM_CF_GHOST_U, fl);
     cub::CountingInputIterator<int32_t> it(0);
     cub::DeviceSelect::Flagged(tmp, tmpb, it, fl, targets, counts, (int)n, s);
@@ -734,14 +736,15 @@ extern "C" int mlbm_check_particles(int32_t dim, int32_t n, const void* x, int64
     return launch_status(1);
 }
 
-extern "C" int mlbm_migrate_level(int32_t dim, int32_t n_new_tiles, const int32_t* old_slot,
+extern "C" int mlbm_migrate_level(int32_t dim, int32_t n_new_tiles, const int32_t* n_dev,
+                                  const int32_t* old_slot,
                                   mlbm_fields_t old0, mlbm_fields_t old1, mlbm_fields_t new0,
                                   mlbm_fields_t new1, int32_t dtype, void* stream) {
     const int T = dim == 2 ? 16 : 64;
     const int64_t n = (int64_t)n_new_tiles * T;
     if (n == 0) return 0;
     cudaStream_t s = as_stream(stream);
-#define MIG(D, R) k_migrate<D, R><<<blocks_for(n, 256), 256, 0, s>>>(n, old_slot, fields_of<R>(old0), \
+#define MIG(D, R) k_migrate<D, R><<<blocks_for(n, 256), 256, 0, s>>>(n, n_dev, old_slot, fields_of<R>(old0), \
         fields_of<R>(old1), fields_of<R>(new0), fields_of<R>(new1))
     if (dim == 2) { if (dtype) MIG(2, double); else MIG(2, float); }
     else { if (dtype) MIG(3, double); else MIG(3, float); }
@@ -751,6 +754,7 @@ extern "C" int mlbm_migrate_level(int32_t dim, int32_t n_new_tiles, const int32_
 
 extern "C" int mlbm_init_new_cells(const mlbm_hier_t* old_h, const mlbm_hier_t* nh, int32_t level,
                                    const int32_t* tile_xyz, const int32_t* old_slot, int32_t n_tiles,
+                                   const int32_t* n_dev,
                                    mlbm_fields_t new0, mlbm_fields_t new1, const double* taus,
                                    int32_t conv, int32_t dtype, int32_t* viol, void* stream) {
     const int T = old_h->dim == 2 ? 16 : 64;
@@ -758,7 +762,7 @@ extern "C" int mlbm_init_new_cells(const mlbm_hier_t* old_h, const mlbm_hier_t* 
     if (n == 0) return 0;
     cudaStream_t s = as_stream(stream);
 #define INI(D, R) k_init_new<D, R><<<blocks_for(n, 128), 128, 0, s>>>(*old_h, *nh, level, tile_xyz, old_slot, \
-        n_tiles, fields_of<R>(new0), fields_of<R>(new1), taus, conv, viol)
+        n_tiles, n_dev, fields_of<R>(new0), fields_of<R>(new1), taus, conv, viol)
     if (old_h->dim == 2) { if (dtype) INI(2, double); else INI(2, float); }
     else { if (dtype) INI(3, double); else INI(3, float); }
 #undef INI

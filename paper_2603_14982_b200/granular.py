@@ -238,16 +238,19 @@ class MpmGrid:
         self.sync_topology()
 
     def sync_topology(self):
-        if self._version == self.topology.version:
+        """Raster rows at the level-0 capacity (re-allocated only when the
+        capacity grows, so captured graphs keep their pointers)."""
+        if self._version == self.topology.cap_version:
             return
-        n = self.topology.cell_count(0)
+        n = self.topology.capacity_cells(0)
         self.ras = torch.zeros((self.R["n"], n), dtype=self.dtype, device=self.topology.device)
-        self._version = self.topology.version
+        self._version = self.topology.cap_version
         self._lv0 = None
 
     def level0(self):
         """Level-0 C struct with cell flags (sticky solids)."""
         if self._lv0 is None or self._lv0_ver != self.topology.version:
+            self.sync_topology()
             if self._tables_fn is not None:
                 t0 = self._tables_fn()
             else:
@@ -263,25 +266,28 @@ class MpmGrid:
     def rows(self, name, k=1):
         return self.ras[self.R[name]:self.R[name] + k]
 
+    def _live(self):
+        return self.topology.cell_count(0)
+
     @property
     def mass(self):
-        return self.ras[self.R["mass"]]
+        return self.ras[self.R["mass"], :self._live()]
 
     @property
     def mom(self):
-        return self.rows("mom", self.d).t()
+        return self.rows("mom", self.d)[:, :self._live()].t()
 
     @property
     def f_int(self):
-        return self.rows("fint", self.d).t()
+        return self.rows("fint", self.d)[:, :self._live()].t()
 
     @property
     def vel(self):
-        return self.rows("vel", self.d).t()
+        return self.rows("vel", self.d)[:, :self._live()].t()
 
     @property
     def drag(self):
-        return self.rows("fs", self.d).t()
+        return self.rows("fs", self.d)[:, :self._live()].t()
 
     def clear(self):
         self.ras[:self.R["nacc"]].zero_()
@@ -323,11 +329,11 @@ def p2g(particles: Particles, grid: MpmGrid, mat: SandMaterial, st=None):
 def grid_update(grid: MpmGrid, dt: float, gravity, drag=None, floor_friction: float = 0.5):
     """granular.py:313-341: drag (n, d) lands in the FS rows first."""
     fs = grid.rows("fs", grid.d)
-    if drag is None:
-        fs.zero_()
-    else:
-        fs.copy_(torch.as_tensor(drag, dtype=grid.dtype, device=grid.ras.device)
-                 .reshape(-1, grid.d).t())
+    fs.zero_()
+    if drag is not None:
+        n = grid._live()
+        fs[:, :n].copy_(torch.as_tensor(drag, dtype=grid.dtype, device=grid.ras.device)
+                        .reshape(-1, grid.d).t())
     lv0 = grid.level0()
     z = (L.C.c_double * 3)()
     empty = L.Fields(0, 0)

@@ -223,55 +223,56 @@ class _LevelTables:
         return (self.cell_flags & 1).bool()
 
 
-def build_tables(topo: Topology, bc, solid, err):
+def build_tables(topo: Topology, bc, solid, err, tables=None):
     """Classify every level (flags, bounce-back masks, interface stencils) on
-    the device (solver.py:177-274 + sparse_grid.py:468-544).  Raises
-    TopologyError on violations."""
+    the device (solver.py:177-274 + sparse_grid.py:468-544).  Buffers are
+    (re)allocated only when a level's capacity changed; counts of I^d / I^u go
+    to ``topo.dcounts[l, 2:4]``.  No host synchronisation: violations land in
+    ``err`` and are raised by the caller's next status check."""
     lib = L.lib()
     s = L.stream_handle()
     T = TILE ** topo.d
-    err.zero_()
-    counts = torch.zeros((topo.levels, 2), dtype=torch.int32, device=topo.device)
+    tables = dict(tables or {})
     hier = topo.hier_struct()
-    tables = {}
+    NC = 1 << topo.d
+    scratch = torch.zeros((topo.levels, 2), dtype=torch.int32, device=topo.device) \
+        if not hasattr(topo, "_cls_counts") else topo._cls_counts
+    topo._cls_counts = scratch
     for l in range(topo.levels):
-        n = topo.n_tiles(l)
-        if not n:
+        cap = topo.lv[l].cap
+        t = tables.get(l)
+        if t is None or t.cap != cap:
+            t = _LevelTables(cap * T, cap, topo.device)
+            t.cap = cap
+            t.down = (torch.zeros(cap * T, dtype=torch.int32, device=topo.device),
+                      torch.full((cap * T, NC), -1, dtype=torch.int32, device=topo.device),
+                      cap * T)
+            t.up = (torch.zeros(cap * T, dtype=torch.int32, device=topo.device),
+                    torch.full((cap * T, NC), -1, dtype=torch.int32, device=topo.device),
+                    cap * T)
+            tables[l] = t
+        if not cap:
             continue
-        t = _LevelTables(n * T, n, topo.device)
         lvs = topo.level_struct(l)
         L.check(lib.mlbm_classify_level(L.C.byref(lvs), L.C.byref(hier), L.C.byref(bc),
                                         L.C.byref(solid), L.ptr(t.cell_flags),
                                         L.ptr(t.dir_masks), L.ptr(t.tile_flags),
-                                        L.ptr(counts[l]), L.ptr(err), s), "classify_level")
-        tables[l] = t
-    cnt = counts.cpu().numpy()
-    NC = 1 << topo.d
+                                        L.ptr(scratch[l]), L.ptr(err), s), "classify_level")
     for l, t in tables.items():
-        for which, nsel, other in ((0, int(cnt[l, 0]), l + 1), (1, int(cnt[l, 1]), l - 1)):
-            if nsel == 0:
+        if not topo.lv[l].cap:
+            continue
+        for which, other in ((0, l + 1), (1, l - 1)):
+            cnt = topo.dcounts[l, 2 + which:3 + which]
+            if other < 0 or other >= topo.levels or not topo.lv[other].cap:
+                cnt.zero_()
                 continue
-            if other < 0 or other >= topo.levels or other not in tables:
-                raise TopologyError(f"level {l}: interface without a "
-                                    f"{'coarser' if which == 0 else 'finer'} level")
-            tg = torch.empty(nsel, dtype=torch.int32, device=topo.device)
-            src = torch.empty((nsel, NC), dtype=torch.int32, device=topo.device)
-            c1 = torch.zeros(1, dtype=torch.int32, device=topo.device)
-            ws = topo.workspace(topo.cell_count(l))
+            tg, src, _ = t.down if which == 0 else t.up
+            ws = topo.workspace(topo.capacity_cells(l))
             lv_a = topo.level_struct(l, t)
             lv_b = topo.level_struct(other, tables[other])
             L.check(lib.mlbm_build_interface(L.C.byref(lv_a), L.C.byref(lv_b), which,
-                                             L.ptr(tg), L.ptr(src), L.ptr(c1), L.ptr(err),
+                                             L.ptr(tg), L.ptr(src), L.ptr(cnt), L.ptr(err),
                                              L.ptr(ws), ws.numel(), s), "build_interface")
-            if which == 0:
-                t.down = (tg, src, nsel)
-            else:
-                t.up = (tg, src, nsel)
-    e = err.cpu().numpy()
-    if e[0]:
-        err.zero_()
-        raise TopologyError(f"topology violation code {e[0]} detail {e[18]} at level "
-                            f"{e[1]} cell {tuple(e[3:3 + topo.d])}")
     return tables
 
 
@@ -309,9 +310,11 @@ class MultiLevelSolver:
         topo = self.topology
         if self._tables_version == topo.version:
             return
-        self._tables = build_tables(topo, self._bc, self._solid, self._err)
+        self._tables = build_tables(topo, self._bc, self._solid, self._err, self._tables)
         self._tables_version = topo.version
-        self._structs = {l: topo.level_struct(l, t) for l, t in self._tables.items()}
+        if getattr(self, "_structs_cap", None) != topo.cap_version:
+            self._structs = {l: topo.level_struct(l, t) for l, t in self._tables.items()}
+            self._structs_cap = topo.cap_version
 
     def _raise_topology(self, msg):
         raise TopologyError(msg)
@@ -349,7 +352,7 @@ class MultiLevelSolver:
         return cp
 
     def _level_call(self, level, src, dst, mode, cp=None):
-        if self.topology.n_tiles(level) == 0:
+        if self.topology.lv[level].cap == 0:
             return
         self._refresh_tables()
         lvs = self._structs[level]
@@ -429,12 +432,13 @@ class MultiLevelSolver:
     def downward_kernel(self, level, step, olda, newa, dst):
         self._refresh_tables()
         t = self._tables.get(level)
-        if t is None or t.down is None:
+        if t is None or not self.topology.lv[level].cap or level + 1 >= self.topology.levels:
             return
         tg, src, n = t.down
         kap = _kappa_down(self.level_params.taus[level], self.level_params.taus[level + 1],
                           self.params.rescale_convention)
-        L.check(L.lib().mlbm_downward(self.d, n, L.ptr(tg), L.ptr(src),
+        L.check(L.lib().mlbm_downward(self.d, n, L.ptr(self.topology.dcounts[level, 2:3]),
+                                      L.ptr(tg), L.ptr(src),
                                       L.ptr(self.topology.lv[level].tile_xyz),
                                       L.fields(_data(olda)), L.fields(_data(newa)),
                                       L.fields(_data(dst)), self.dcode, int(step), kap,
@@ -450,13 +454,14 @@ class MultiLevelSolver:
     def upward_kernel(self, level, fine, dst):
         self._refresh_tables()
         t = self._tables.get(level + 1)
-        if t is None or t.up is None:
+        if t is None or not self.topology.lv[level + 1].cap or not self.topology.lv[level].cap:
             return
         tg, src, n = t.up
         kap = _kappa_up(self.level_params.taus[level], self.level_params.taus[level + 1],
                         self.params.rescale_convention)
         avg = 1 if self.params.upward_mode == "average" else 0
-        L.check(L.lib().mlbm_upward(self.d, n, L.ptr(tg), L.ptr(src), L.fields(_data(fine)),
+        L.check(L.lib().mlbm_upward(self.d, n, L.ptr(self.topology.dcounts[level + 1, 3:4]),
+                                    L.ptr(tg), L.ptr(src), L.fields(_data(fine)),
                                     L.fields(_data(dst)), self.dcode, avg, kap,
                                     L.stream_handle()), "upward")
         self.launches += 1

@@ -65,20 +65,46 @@ def _device():
 
 
 class LevelTopo:
-    """Device tables of one level."""
+    """Device tables of one level, allocated at a capacity (tiles) so that
+    pointers stay fixed across topology changes; the live count is in
+    ``Topology.dcounts`` (device) and ``n_tiles`` (host mirror)."""
 
     def __init__(self, d, grid_dims, device):
         self.d = d
         self.grid = tuple(grid_dims)                      # tile grid (3 axes)
-        n = int(np.prod(self.grid))
-        self.kind = torch.zeros(n, dtype=torch.uint8, device=device)
-        self.tile_map = torch.full((n,), -1, dtype=torch.int32, device=device)
+        self.grid_n = int(np.prod(self.grid))
+        self.kind = torch.zeros(self.grid_n, dtype=torch.uint8, device=device)
+        self.tile_map = torch.full((self.grid_n,), -1, dtype=torch.int32, device=device)
+        self.tile_map_new = torch.full((self.grid_n,), -1, dtype=torch.int32, device=device)
         self.n_tiles = 0
-        self.tile_xyz = torch.zeros((0, 3), dtype=torch.int32, device=device)
-        self.tile_kind = torch.zeros(0, dtype=torch.uint8, device=device)
-        self.nbr = torch.zeros((0, n_nbr(d)), dtype=torch.int32, device=device)
-        self.old_slot = torch.zeros(0, dtype=torch.int32, device=device)
+        self.cap = 0
         self.created = 0
+        self.device = device
+        self._alloc(0)
+
+    def _alloc(self, cap):
+        dev = self.device
+        old = (getattr(self, "tile_xyz", None), getattr(self, "tile_kind", None),
+               getattr(self, "nbr", None), getattr(self, "old_slot", None))
+        self.tile_xyz = torch.zeros((cap, 3), dtype=torch.int32, device=dev)
+        self.tile_kind = torch.zeros(cap, dtype=torch.uint8, device=dev)
+        self.nbr = torch.full((cap, n_nbr(self.d)), -1, dtype=torch.int32, device=dev)
+        self.old_slot = torch.full((cap,), -1, dtype=torch.int32, device=dev)
+        if old[0] is not None and self.cap:
+            k = min(self.cap, cap)
+            self.tile_xyz[:k].copy_(old[0][:k])
+            self.tile_kind[:k].copy_(old[1][:k])
+            self.nbr[:k].copy_(old[2][:k])
+            self.old_slot[:k].copy_(old[3][:k])
+        self.cap = cap
+
+
+def capacity_for(n, grid_n, T, budget_cells=1 << 27):
+    """Tile capacity of a level: the whole tile grid when it is small, else
+    1.5x the need rounded to 256 tiles (growth re-captures the step graph)."""
+    if grid_n * T <= budget_cells // 8:
+        return grid_n
+    return min(grid_n, ((max(int(1.5 * n), n + 256) + 255) // 256) * 256)
 
 
 class Topology:
@@ -106,8 +132,10 @@ class Topology:
         self.lv = [LevelTopo(self.d, self.tile_grid(l), self.device)
                    for l in range(levels)]
         self.version = 0
+        self.cap_version = 0
+        # device counts per level: [live tiles, fresh tiles, |I^d|, |I^u|]
+        self.dcounts = torch.zeros((levels, 4), dtype=torch.int32, device=self.device)
         self._ws = torch.zeros(0, dtype=torch.uint8, device=self.device)
-        self._counts = torch.zeros(4, dtype=torch.int32, device=self.device)
         self._host_cache = {}
 
     # -- geometry -------------------------------------------------------------
@@ -163,47 +191,63 @@ class Topology:
         return self._ws
 
     # -- rebuild ----------------------------------------------------------------
-    def rebuild(self, kinds: dict):
-        """Replace the kind grids of the given levels and recompact them
-        (sparse_grid.py:183-200).  Keeps ``old_slot`` per rebuilt level for
-        data migration; bumps the version."""
-        lib = L.lib()
-        s = L.stream_handle()
-        counts = self._counts
-        pending = []
+    def ensure_capacity(self, level, n):
+        """Grow a level's tile arrays to hold n tiles (keeps content)."""
+        lt = self.lv[level]
+        if n <= lt.cap:
+            return False
+        lt._alloc(capacity_for(n, lt.grid_n, TILE ** self.d))
+        self.cap_version += 1
+        return True
+
+    def compact(self, level, kind):
+        """Sorted-slot compaction of a new kind grid into ``tile_map_new``,
+        ``tile_xyz``, ``tile_kind``, ``old_slot`` and ``dcounts[level, 0:2]``
+        (sparse_grid.py:183-200).  No host synchronisation."""
+        lt = self.lv[level]
+        ws = self.workspace(lt.grid_n)
+        tiles = (L.C.c_int32 * 3)(*self.tile_grid(level))
+        L.check(L.lib().mlbm_compact_tiles(self.d, tiles, L.ptr(kind), L.ptr(lt.tile_map),
+                                           L.ptr(lt.tile_map_new), L.ptr(lt.tile_xyz),
+                                           L.ptr(lt.tile_kind), L.ptr(lt.old_slot), lt.cap,
+                                           L.ptr(self.dcounts[level]), L.ptr(ws), ws.numel(),
+                                           L.stream_handle()), "compact_tiles")
+
+    def build_neighbors(self, level, new_map=True):
+        lt = self.lv[level]
+        if not lt.cap:
+            return
+        st = self.level_struct(level)
+        if new_map:
+            st.tile_map = lt.tile_map_new.data_ptr()
+        L.check(L.lib().mlbm_build_neighbors(L.C.byref(st), L.ptr(lt.nbr), L.stream_handle()),
+                "build_neighbors")
+
+    def commit(self, kinds: dict, counts: dict):
+        """Make the compacted maps / kinds current; host counts become the
+        known new counts; bumps the topology version."""
         for level, kind in kinds.items():
             lt = self.lv[level]
-            old_map = lt.tile_map
-            new_map = torch.empty_like(old_map)
-            ngrid = lt.kind.numel()
-            xyz = torch.empty((ngrid, 3), dtype=torch.int32, device=self.device)
-            tk = torch.empty(ngrid, dtype=torch.uint8, device=self.device)
-            osl = torch.empty(ngrid, dtype=torch.int32, device=self.device)
-            ws = self.workspace(ngrid)
-            tiles = (L.C.c_int32 * 3)(*self.tile_grid(level))
-            cnt = torch.zeros(2, dtype=torch.int32, device=self.device)
-            L.check(lib.mlbm_compact_tiles(self.d, tiles, L.ptr(kind), L.ptr(old_map),
-                                           L.ptr(new_map), L.ptr(xyz), L.ptr(tk),
-                                           L.ptr(osl), L.ptr(cnt), L.ptr(ws),
-                                           ws.numel(), s), "compact_tiles")
-            pending.append((level, kind, new_map, xyz, tk, osl, cnt))
-        host = torch.stack([p[-1] for p in pending]).cpu().numpy() if pending else []
-        for (level, kind, new_map, xyz, tk, osl, _), (n, fresh) in zip(pending, host):
-            lt = self.lv[level]
-            lt.kind = kind.contiguous()
-            lt.tile_map = new_map
-            lt.n_tiles = int(n)
-            lt.tile_xyz = xyz[:n].clone()
-            lt.tile_kind = tk[:n].clone()
-            lt.old_slot = osl[:n].clone()
-            lt.created = int(fresh)
-            lt.nbr = torch.empty((int(n), n_nbr(self.d)), dtype=torch.int32,
-                                 device=self.device)
-            if n:
-                lvs = self.level_struct(level)
-                L.check(lib.mlbm_build_neighbors(L.C.byref(lvs), L.ptr(lt.nbr), s),
-                        "build_neighbors")
+            lt.tile_map.copy_(lt.tile_map_new)
+            if kind.data_ptr() != lt.kind.data_ptr():
+                lt.kind.copy_(kind)
+            lt.n_tiles = int(counts[level])
         self.bump()
+
+    def rebuild(self, kinds: dict):
+        """Replace the kind grids of the given levels (host-driven path used
+        at construction and by ``set_tile_set``; counts read back)."""
+        counts = {l: int((k != 0).sum().item()) for l, k in kinds.items()}
+        for l, n in counts.items():
+            self.ensure_capacity(l, n)
+        for l, k in kinds.items():
+            self.compact(l, k)
+        for l in kinds:
+            self.build_neighbors(l, new_map=True)
+        created = self.dcounts[:, 1].cpu().numpy()
+        for l in kinds:
+            self.lv[l].created = int(created[l])
+        self.commit(kinds, counts)
 
     def bump(self):
         self.version += 1
@@ -221,15 +265,19 @@ class Topology:
             st.tiles[a] = v
         for a, v in enumerate(self.periodic3()):
             st.periodic[a] = v
-        st.n_tiles = lt.n_tiles
+        st.n_tiles = lt.cap                   # launch capacity; live count on device
         st.tile_map = lt.tile_map.data_ptr()
-        st.tile_xyz = lt.tile_xyz.data_ptr() if lt.n_tiles else 0
-        st.nbr = lt.nbr.data_ptr() if lt.n_tiles else 0
-        if tables is not None and lt.n_tiles:
+        st.tile_xyz = lt.tile_xyz.data_ptr() if lt.cap else 0
+        st.nbr = lt.nbr.data_ptr() if lt.cap else 0
+        st.counts = self.dcounts[level].data_ptr()
+        if tables is not None and lt.cap:
             st.cell_flags = tables.cell_flags.data_ptr()
             st.dir_masks = tables.dir_masks.data_ptr()
             st.tile_flags = tables.tile_flags.data_ptr()
         return st
+
+    def capacity_cells(self, level):
+        return self.lv[level].cap * TILE ** self.d
 
     def hier_struct(self, pair=None):
         h = L.Hier()
@@ -256,14 +304,16 @@ class Topology:
         return self._host_cache[key]
 
     def tile_coords(self, level):
+        n = self.lv[level].n_tiles
         return self._host(("xyz", level),
-                          lambda: self.lv[level].tile_xyz[:, :self.d].cpu().numpy()
+                          lambda: self.lv[level].tile_xyz[:n, :self.d].cpu().numpy()
                           .astype(np.int64))
 
     def tile_kinds(self, level):
         """Reference kind values (LEAF = 0, BORDER = 1) per slot."""
+        n = self.lv[level].n_tiles
         return self._host(("kind", level),
-                          lambda: self.lv[level].tile_kind.cpu().numpy().astype(np.int64) - 1)
+                          lambda: self.lv[level].tile_kind[:n].cpu().numpy().astype(np.int64) - 1)
 
     def kind_grid(self, level):
         return self._host(("kgrid", level),
@@ -324,25 +374,31 @@ class LevelFields(MutableMapping):
     Every other name is a live view (in-place writes land in HBM).
     """
 
-    def __init__(self, d, data):
+    def __init__(self, d, data, live=None):
         self.d = d
-        self.data = data
+        self.data = data                 # [nf, capacity cells]
+        self.live = live                 # callable -> live cell count (None: all)
         self.names = field_names(d)
         self.index = {nm: i for i, nm in enumerate(self.names)}
 
+    def n(self):
+        return self.data.shape[1] if self.live is None else self.live()
+
     def __getitem__(self, name):
         i = self.index[name]
+        n = self.n()
         if i == 0:
-            return 1.0 + self.data[0]
-        return self.data[i]
+            return 1.0 + self.data[0, :n]
+        return self.data[i, :n]
 
     def __setitem__(self, name, value):
         i = self.index[name]
+        n = self.n()
         v = torch.as_tensor(value, dtype=self.data.dtype, device=self.data.device)
         if i == 0:
-            self.data[0].copy_(v - 1.0)
+            self.data[0, :n].copy_(v - 1.0)
         else:
-            self.data[i].copy_(v)
+            self.data[i, :n].copy_(v)
 
     def __delitem__(self, name):
         raise TypeError("fields are fixed")
@@ -368,13 +424,15 @@ def fresh_block(d, n, dtype, device):
 
 
 class FieldTree:
-    """Per-level SoA blocks over the stored tiles (sparse_grid.py:369-382)."""
+    """Per-level SoA blocks over the stored tiles (sparse_grid.py:369-382),
+    allocated at the level capacity."""
 
     def __init__(self, topology: Topology, dtype=None):
         dtype = dtype or DEFAULT_DTYPE
         self.levels = [LevelFields(topology.d,
-                                   fresh_block(topology.d, topology.cell_count(l), dtype,
-                                               topology.device))
+                                   fresh_block(topology.d, topology.capacity_cells(l), dtype,
+                                               topology.device),
+                                   live=(lambda l=l: topology.cell_count(l)))
                        for l in range(topology.levels)]
 
     def nbytes(self):
@@ -382,12 +440,37 @@ class FieldTree:
 
 
 class PingPongPair:
-    """Two field trees with identical topology plus the bounce counter."""
+    """Two field trees with identical topology plus the bounce counter.
+    ``scratch[l]`` is the migration target of a level (same capacity)."""
 
     def __init__(self, topology: Topology, dtype=None):
         self.dtype = dtype or DEFAULT_DTYPE
+        self.topology = topology
         self.trees = (FieldTree(topology, self.dtype), FieldTree(topology, self.dtype))
+        self.scratch = {}
         self.bounce = 0
+
+    def ensure_capacity(self):
+        """Grow field blocks to the topology capacity (content kept)."""
+        topo = self.topology
+        for l in range(topo.levels):
+            cap = topo.capacity_cells(l)
+            for tree in self.trees:
+                lf = tree.levels[l]
+                if lf.data.shape[1] < cap:
+                    nb = fresh_block(topo.d, cap, self.dtype, topo.device)
+                    k = lf.data.shape[1]
+                    nb[:, :k].copy_(lf.data)
+                    lf.data = nb
+
+    def scratch_blocks(self, level):
+        cap = self.topology.capacity_cells(level)
+        sb = self.scratch.get(level)
+        if sb is None or sb[0].shape[1] != cap:
+            sb = tuple(fresh_block(self.topology.d, cap, self.dtype, self.topology.device)
+                       for _ in range(2))
+            self.scratch[level] = sb
+        return sb
 
     def nbytes(self):
         return self.trees[0].nbytes() + self.trees[1].nbytes()
