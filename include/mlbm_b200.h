@@ -317,11 +317,13 @@ int mlbm_powder(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm_fields_t dst, v
 
 /* diagnostics (coupling.py:500-531): out[0..dim-1] += vol sum rho u, out[dim] +=
  * vol sum phi, out[dim+1] = min(out[dim+1], eps) over leaf cells;
- * particles: out[0..dim-1] += sum m v, out[dim..2dim-1] += sum fs. */
+ * particles: out[0..dim-1] += sum m v, out[dim..2dim-1] += sum fs over the first
+ * min(n0, live[0] * tile cells) raster cells (live may be NULL: n0 cells). */
 int mlbm_diag_level(const mlbm_level_t* lv, mlbm_fields_t f, double vol, int32_t dtype,
                     double* out, void* stream);
 int mlbm_diag_particles(int32_t dim, int32_t n, const void* p, int64_t ps, const void* ras,
-                        int64_t rs, int64_t n0, int32_t dtype, double* out, void* stream);
+                        int64_t rs, int64_t n0, const int32_t* live, int32_t dtype,
+                        double* out, void* stream);
 
 #ifdef __cplusplus
 }

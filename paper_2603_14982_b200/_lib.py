@@ -153,7 +153,7 @@ _SIGS = {
     "mlbm_powder": [C.POINTER(Level), Fields, Fields, P, I64, P, D, D, D, D, D,
                     I32, I32, P],
     "mlbm_diag_level": [C.POINTER(Level), Fields, D, I32, P, P],
-    "mlbm_diag_particles": [I32, I32, P, I64, P, I64, I64, I32, P, P],
+    "mlbm_diag_particles": [I32, I32, P, I64, P, I64, I64, P, I32, P, P],
 }
 _RET64 = {"mlbm_ws_bytes", "mlbm_sort_ws_bytes"}
 

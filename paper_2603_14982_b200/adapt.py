@@ -264,12 +264,14 @@ class GridAdaptor:
                 "adapt_pass")
         self.launches += 1
 
-    def finish(self, driver, pair, status, err, check_after=True) -> AdaptReport:
+    def finish(self, driver, pair, status, err, check_after=True, device_runner=None):
         """Host half: raise on seed errors; when a level changed, rebuild and
         migrate on the device without host synchronisation (the new counts
         come from the adapt pass); build the report.  ``check_after`` re-runs
         the invariants on the new topology (one readback); the graph path
-        skips it and the next pass reports them."""
+        skips it and the next pass reports them.  ``device_runner(fn, key)``
+        (graph path) runs the device half ``fn`` — eagerly or as a replay of a
+        graph cached under ``key`` — after the host bookkeeping is done."""
         topo = self.topology
         Lv = topo.levels
         rep = AdaptReport(created=[0] * Lv, deleted=[0] * Lv)
@@ -282,7 +284,14 @@ class GridAdaptor:
             rep.noop = False
             new_counts = [int(v) for v in status[Lv + 4:2 * Lv + 4]]
             fresh = [int(v) for v in status[2 * Lv + 4:3 * Lv + 4]]
-            self._apply(changed, pair, rep, new_counts, fresh)
+            for l in changed:
+                rep.created[l] = fresh[l]
+                rep.deleted[l] = topo.n_tiles(l) - (new_counts[l] - fresh[l])
+            dev = self._prepare(changed, pair, new_counts, fresh)
+            if device_runner is None:
+                dev()
+            else:
+                device_runner(dev, (tuple(changed), tuple(bool(fresh[l]) for l in changed)))
             if check_after:
                 self._invariants_device(driver)
                 viol = self._status[Lv:Lv + 3].cpu().numpy()
@@ -291,52 +300,58 @@ class GridAdaptor:
         self._report_invariants(viol, rep)
         return rep
 
-    def _apply(self, changed, pair, rep, new_counts, fresh):
-        """Rebuild + bitwise migration + new-cell init (adapt.py:232-372),
-        device-only: compaction into the spare tile map, neighbours,
+    def _prepare(self, changed, pair, new_counts, fresh):
+        """Rebuild + bitwise migration + new-cell init (adapt.py:232-372).
+        Host part here (capacity growth, host counts, version bump); returns
+        the device part — compaction into the spare tile map, neighbours,
         migration into the scratch blocks, initialisation from the old
-        hierarchy, then the scratch / maps / kinds become current."""
+        hierarchy, then scratch / maps / kinds become current — which launches
+        only kernels and device copies on fixed pointers (graph-capturable)."""
         topo = self.topology
-        lib = L.lib()
-        s = L.stream_handle()
-        d = topo.d
-        dcode = dtype_code(pair.dtype)
-        old_counts = [topo.n_tiles(l) for l in range(topo.levels)]
         grown = False
         for l in changed:
             grown |= topo.ensure_capacity(l, new_counts[l])
         if grown:
             pair.ensure_capacity()
+        for l in changed:
+            pair.scratch_blocks(l)
         old_h = topo.hier_struct(pair)           # old maps, old fields, old counts
-        for l in changed:
-            topo.compact(l, self._new[l])
-        for l in changed:
-            topo.build_neighbors(l, new_map=True)
+        topo.commit_host({l: new_counts[l] for l in changed})
         new_h = topo.hier_struct()
-        for l in changed:
-            lt = topo.lv[l]
-            rep.created[l] = fresh[l]
-            rep.deleted[l] = old_counts[l] - (new_counts[l] - fresh[l])
-            sb = pair.scratch_blocks(l)
-            cnt = L.ptr(topo.dcounts[l])
-            L.check(lib.mlbm_migrate_level(d, lt.cap, cnt, L.ptr(lt.old_slot),
-                                           L.fields(pair.trees[0].levels[l].data),
-                                           L.fields(pair.trees[1].levels[l].data),
-                                           L.fields(sb[0]), L.fields(sb[1]), dcode, s),
-                    "migrate_level")
-            if fresh[l]:
-                conv = 0 if self.rescale_convention == "derived" else 1
-                L.check(lib.mlbm_init_new_cells(L.C.byref(old_h), L.C.byref(new_h), l,
-                                                L.ptr(lt.tile_xyz), L.ptr(lt.old_slot), lt.cap,
-                                                cnt, L.fields(sb[0]), L.fields(sb[1]),
-                                                L.ptr(self._taus), conv, dcode,
-                                                L.ptr(self._status[Lv_slot(topo)]), s),
-                        "init_new_cells")
-        for l in changed:
-            sb = pair.scratch_blocks(l)
-            for t in range(2):
-                pair.trees[t].levels[l].data.copy_(sb[t])
-        topo.commit({l: self._new[l] for l in changed}, {l: new_counts[l] for l in changed})
+        d = topo.d
+        dcode = dtype_code(pair.dtype)
+        conv = 0 if self.rescale_convention == "derived" else 1
+        init = {l: bool(fresh[l]) for l in changed}
+
+        def device():
+            lib = L.lib()
+            s = L.stream_handle()
+            for l in changed:
+                topo.compact(l, self._new[l])
+            for l in changed:
+                topo.build_neighbors(l, new_map=True)
+            for l in changed:
+                lt = topo.lv[l]
+                sb = pair.scratch_blocks(l)
+                cnt = L.ptr(topo.dcounts[l])
+                L.check(lib.mlbm_migrate_level(d, lt.cap, cnt, L.ptr(lt.old_slot),
+                                               L.fields(pair.trees[0].levels[l].data),
+                                               L.fields(pair.trees[1].levels[l].data),
+                                               L.fields(sb[0]), L.fields(sb[1]), dcode, s),
+                        "migrate_level")
+                if init[l]:
+                    L.check(lib.mlbm_init_new_cells(L.C.byref(old_h), L.C.byref(new_h), l,
+                                                    L.ptr(lt.tile_xyz), L.ptr(lt.old_slot),
+                                                    lt.cap, cnt, L.fields(sb[0]),
+                                                    L.fields(sb[1]), L.ptr(self._taus), conv,
+                                                    dcode, L.ptr(self._status[Lv_slot(topo)]),
+                                                    s), "init_new_cells")
+            for l in changed:
+                sb = pair.scratch_blocks(l)
+                for t in range(2):
+                    pair.trees[t].levels[l].data.copy_(sb[t])
+            topo.commit_device({l: self._new[l] for l in changed})
+        return device
 
     def _invariants_device(self, driver):
         """Coverage, two-tile rings, particles in level-0 leaves

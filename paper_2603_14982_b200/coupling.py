@@ -183,6 +183,9 @@ class CoupledSim:
         self.graph_replays = 0
         self.graph_captures = 0
         self.topology_changes = 0
+        self.rebuild_eager = 0
+        self.rebuild_replays = 0
+        self._pending_row = None
         if self.drag_params.d_p is None and len(self.particles):
             self.drag_params.d_p = float(particle_diameter(float(self.particles.V0.double().mean()),
                                                            self.d))
@@ -377,6 +380,7 @@ class CoupledSim:
         self._finish_graph_step(adapt_now)
 
     def _finish_graph_step(self, adapt_now):
+        self._resolve_pending_diag()
         h = self._host_i32.numpy().astype(np.int64)
         ne = L.ERR_INTS
         serr, gerr = h[:ne], h[ne:2 * ne]
@@ -392,21 +396,76 @@ class CoupledSim:
             status = h[2 * ne + 2:2 * ne + 2 + nst]
             err = h[2 * ne + 2 + nst:]
             self.last_report = self.adaptor.finish(self._driver(), self.pair, status, err,
-                                                   check_after=False)
+                                                   check_after=False,
+                                                   device_runner=self._run_rebuild)
             if not self.last_report.noop:
-                # device-only rebuild already queued; the diagnostics row of
-                # this step is taken on the new topology (coupling.py:481)
+                # the rebuild graph re-takes this step's diagnostics on the new
+                # topology (coupling.py:481) into a second pinned buffer; the row
+                # is completed at the next synchronisation point
                 self.topology_changes += 1
-                self.grid.sync_topology()
-                self.solver._refresh_tables()
-                self._record_diagnostics()
-                self._host_f64.copy_(self._diag_buf, non_blocking=True)
-                torch.cuda.current_stream().synchronize()
-                diag = self._host_f64.numpy().copy()
+                self._push_diag_row(None)
+                return
         self._push_diag_row(diag)
 
+    def _run_rebuild(self, device_fn, key):
+        """Device half of a topology change + the table rebuild + the
+        diagnostics row, as one CUDA graph per (capacities, changed levels,
+        parities) — run eagerly the first time a key is seen (so every buffer
+        it needs is allocated outside capture), captured and replayed after."""
+        solver = self.solver
+        topo = self.topology
+        self.grid.sync_topology()
+        if getattr(self, "_host_rb", None) is None:
+            self._host_rb = torch.zeros(self._diag_buf.numel(), dtype=torch.float64).pin_memory()
+        full = (topo.cap_version, key, tuple(topo.n_tiles(l) > 0 for l in range(topo.levels)),
+                tuple(k & 1 for k in solver.k), self.last_fields is not None)
+        if getattr(self, "_rb_ver", None) != topo.cap_version:
+            self._rb_graphs, self._rb_seen, self._rb_ver = {}, set(), topo.cap_version
+
+        def body():
+            device_fn()
+            solver._refresh_tables()
+            self._record_diagnostics()
+            self._host_rb.copy_(self._diag_buf, non_blocking=True)
+
+        g = self._rb_graphs.get(full)
+        if g is None and full not in self._rb_seen:
+            self._rb_seen.add(full)
+            body()
+            self.rebuild_eager += 1
+            return
+        if g is None:
+            if self._pool is None:
+                self._pool = torch.cuda.graph_pool_handle()
+            g = torch.cuda.CUDAGraph()
+            n0 = L.TRACE.launches
+            tracing = L.TRACE.enabled
+            L.TRACE.enabled = False
+            try:
+                with torch.cuda.graph(g, pool=self._pool):
+                    body()
+            finally:
+                L.TRACE.enabled = tracing
+            g.nk = L.TRACE.launches - n0
+            L.TRACE.launches = n0
+            self._rb_graphs[full] = g
+            self.graph_captures += 1
+        g.replay()
+        L.TRACE.launches += g.nk
+        solver._tables_version = topo.version
+        self.rebuild_replays += 1
+
+    def _resolve_pending_diag(self):
+        """Complete a diagnostics row whose values a rebuild graph is still
+        copying (call after a stream synchronisation)."""
+        if self._pending_row is not None:
+            i = self._pending_row
+            self._pending_row = None
+            self._diag_rows[i] = self._make_diag_row(self._host_rb.numpy(),
+                                                     *self._diag_rows[i])
+
     def _powder_tmp(self):
-        n0 = self.topology.cell_count(0)
+        n0 = self.topology.capacity_cells(0)
         if self._tmp is None or self._tmp.numel() != n0:
             self._tmp = torch.empty(n0, dtype=self.dtype, device=self.topology.device)
         return self._tmp
@@ -460,25 +519,39 @@ class CoupledSim:
                     "diag_level")
         p = self.particles
         g = self.grid
-        n0 = self.topology.cell_count(0) if self.last_fields is not None else 0
+        n0 = self.topology.capacity_cells(0) if self.last_fields is not None else 0
         L.check(lib.mlbm_diag_particles(d, len(p), L.ptr(p.pd), p.pd.stride(0), L.ptr(g.ras),
-                                        g.ras.stride(0), n0, dcode, L.ptr(out[d + 2:]), s),
+                                        g.ras.stride(0), n0, L.ptr(self.topology.dcounts[0]),
+                                        dcode, L.ptr(out[d + 2:]), s),
                 "diag_particles")
 
-    def _push_diag_row(self, o):
+    def _make_diag_row(self, o, step, tiles):
         d = self.d
-        step = self.step_count + 1
-        self._diag_rows.append(DiagRow(
+        return DiagRow(
             step=step, t_phys=step * self.unit_scale.dt,
             fluid_mom=tuple(float(v) for v in o[:d]),
             sediment_mom=tuple(float(v) for v in o[d + 2:2 * d + 2]),
             drag_impulse=tuple(float(-v) for v in o[2 * d + 2:3 * d + 2]),
             sum_phi=float(o[d]),
-            tiles=tuple(self.topology.n_tiles(l) for l in range(self.topology.levels)),
-            eps_min=float(o[d + 1])))
+            tiles=tiles,
+            eps_min=float(o[d + 1]))
+
+    def _push_diag_row(self, o):
+        """Append this step's row; ``o is None``: values pending in the
+        rebuild buffer (completed by ``_resolve_pending_diag``)."""
+        step = self.step_count + 1
+        tiles = tuple(self.topology.n_tiles(l) for l in range(self.topology.levels))
+        if o is None:
+            self._pending_row = len(self._diag_rows)
+            self._diag_rows.append((step, tiles))
+        else:
+            self._diag_rows.append(self._make_diag_row(o, step, tiles))
 
     @property
     def diagnostics(self):
+        if self._pending_row is not None:
+            torch.cuda.current_stream().synchronize()
+            self._resolve_pending_diag()
         return self._diag_rows
 
     def fluid_momentum(self):

@@ -874,8 +874,10 @@ __global__ void k_diag_level(mlbm_level_t lv, mlbm_fields_t f, double vol, doubl
 
 // out[0..D-1] += sum m v ; out[D..2D-1] += sum fs (level-0 cells)
 template <int D, typename R>
-__global__ void k_diag_particles(PartArgs P, const R* ras, int64_t rs, int64_t n0, double* out) {
+__global__ void k_diag_particles(PartArgs P, const R* ras, int64_t rs, int64_t n0,
+                                 const int32_t* live, double* out) {
     using PR = PRows<D>;
+    if (live) n0 = min(n0, (int64_t)live[0] * Geo<D>::T);
     double acc[2 * D];
     for (int k = 0; k < 2 * D; ++k) acc[k] = 0.0;
     const R* pp = (const R*)P.p;
@@ -1636,13 +1638,14 @@ extern "C" int mlbm_diag_level(const mlbm_level_t* lv, mlbm_fields_t f, double v
 }
 
 extern "C" int mlbm_diag_particles(int32_t dim, int32_t n, const void* p, int64_t ps, const void* ras,
-                                   int64_t rs, int64_t n0, int32_t dtype, double* out, void* stream) {
+                                   int64_t rs, int64_t n0, const int32_t* live, int32_t dtype,
+                                   double* out, void* stream) {
     const int64_t m = n > n0 ? n : n0;
     if (m == 0) return 0;
     PartArgs P{dim, n, nullptr, nullptr, (void*)p, ps, nullptr, nullptr, nullptr};
     cudaStream_t s = as_stream(stream);
     const int gb = (int)std::min<int64_t>(nblk(m, 256), 592);
-#define DP(D, R) k_diag_particles<D, R><<<gb, 256, 0, s>>>(P, (const R*)ras, rs, n0, out)
+#define DP(D, R) k_diag_particles<D, R><<<gb, 256, 0, s>>>(P, (const R*)ras, rs, n0, live, out)
     if (dim == 2) { if (dtype) DP(2, double); else DP(2, float); }
     else { if (dtype) DP(3, double); else DP(3, float); }
 #undef DP

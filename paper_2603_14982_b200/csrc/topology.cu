@@ -174,43 +174,42 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
         if (g[axis] == ((f & 1) ? lv.cells[axis] - 1 : 0)) bcl = true;
     }
     bool id = false, iu = false;
-    if (rim) {
-        for (int k = 0; k < NB; ++k) {
-            const int o[3] = {k % 3 - 1, (k / 3) % 3 - 1, D == 3 ? k / 9 - 1 : 0};
-            if (snb[k] >= 0) continue;
+    // owner level of every cell within 2 of the tile (8^D box, smem), taken
+    // only in absent in-domain neighbour tiles (-1 elsewhere: no effect)
+    constexpr int W = D == 3 ? 512 : 64;
+    __shared__ int8_t sown[W];
+    if (rim) {                                   // block-uniform
+        for (int i = lc; i < W; i += T) {
+            const int m[3] = {i & 7, (i >> 3) & 7, D == 3 ? i >> 6 : 2};
+            int o[3] = {0, 0, 0}, cc[3] = {0, 0, 0};
             bool indom = true;
-            int nt[3];
-            for (int a = 0; a < 3; ++a) {
-                nt[a] = tx[a] + o[a];
-                if (a >= D) continue;
-                if (lv.periodic[a]) nt[a] = (nt[a] + lv.tiles[a]) % lv.tiles[a];
-                else if (nt[a] < 0 || nt[a] >= lv.tiles[a]) indom = false;
+            for (int a = 0; a < D; ++a) {
+                const int u = tx[a] * 4 + m[a] - 2;     // unwrapped cell
+                o[a] = (m[a] < 2) ? -1 : (m[a] >= 6 ? 1 : 0);
+                int c = u;
+                if (lv.periodic[a]) c = (c + lv.cells[a]) % lv.cells[a];
+                else if (c < 0 || c >= lv.cells[a]) indom = false;
+                cc[a] = c;
             }
-            if (!indom) continue;
-            // cells of that tile within Chebyshev 2 of g (unwrapped displacement)
-            int lo[3], hi[3];
-            for (int a = 0; a < 3; ++a) {
-                if (a >= D) { lo[a] = hi[a] = 0; continue; }
-                const int base = (tx[a] + o[a]) * 4;     // unwrapped origin
-                lo[a] = max(0, g[a] - 2 - base);
-                hi[a] = min(3, g[a] + 2 - base);
-            }
-            for (int mz = lo[2]; mz <= hi[2]; ++mz)
-                for (int my = lo[1]; my <= hi[1]; ++my)
-                    for (int mx = lo[0]; mx <= hi[0]; ++mx) {
-                        const int m[3] = {mx, my, mz};
-                        int cc[3] = {0, 0, 0};
-                        int dist = 0;
-                        for (int a = 0; a < D; ++a) {
-                            const int uc = (tx[a] + o[a]) * 4 + m[a];
-                            dist = max(dist, abs(uc - g[a]));
-                            cc[a] = nt[a] * 4 + m[a];
-                        }
-                        const int own = owner_of(h, level, cc);
-                        if (own > level && dist <= 2) id = true;
-                        if (own >= 0 && own < level && dist <= 1) iu = true;
-                    }
+            const int k = (o[0] + 1) + 3 * (o[1] + 1) + (D == 3 ? 9 * (o[2] + 1) : 0);
+            int8_t v = -1;
+            if (indom && snb[k] < 0) v = (int8_t)owner_of(h, level, cc);
+            sown[i] = v;
         }
+        __syncthreads();
+        const int b[3] = {l[0], l[1], D == 3 ? l[2] : 0};   // window origin = cell - 2 + 2
+#pragma unroll 1
+        for (int dz = (D == 3 ? 0 : 2); dz <= (D == 3 ? 4 : 2); ++dz)
+#pragma unroll
+            for (int dy = 0; dy <= 4; ++dy)
+#pragma unroll
+                for (int dx = 0; dx <= 4; ++dx) {
+                    const int idx = (b[0] + dx) + 8 * (b[1] + dy) + (D == 3 ? 64 * (b[2] + dz) : 0);
+                    const int own = sown[idx];
+                    const int dist = max(max(abs(dx - 2), abs(dy - 2)), abs(dz - 2));
+                    if (own > level) id = true;
+                    if (own >= 0 && own < level && dist <= 1) iu = true;
+                }
         if (id && iu) report_error(err, MLBM_ERR_TOPOLOGY, level, g[0], g[1], g[2], 1);
         if (id && level == h.levels - 1) report_error(err, MLBM_ERR_TOPOLOGY, level, g[0], g[1], g[2], 2);
         if (iu && level == 0) report_error(err, MLBM_ERR_TOPOLOGY, level, g[0], g[1], g[2], 3);
@@ -252,8 +251,9 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
     const int64_t cell = (int64_t)tile * T + lc;
     cell_flags[cell] = f;
     dir_masks[cell] = mask;
-    if (id) atomicAdd(&counts[0], 1);
-    if (iu) atomicAdd(&counts[1], 1);
+    const int nid = __syncthreads_count(id), niu = __syncthreads_count(iu);
+    if (lc == 0 && nid) atomicAdd(&counts[0], nid);
+    if (lc == 0 && niu) atomicAdd(&counts[1], niu);
     const int plain = __syncthreads_and(active && mask == 0);
     const int anybc = __syncthreads_or(bcl);
     if (lc == 0)

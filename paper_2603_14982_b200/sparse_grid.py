@@ -99,11 +99,11 @@ class LevelTopo:
         self.cap = cap
 
 
-def capacity_for(n, grid_n, T, budget_cells=1 << 27):
-    """Tile capacity of a level: the whole tile grid when it is small, else
-    1.5x the need rounded to 256 tiles (growth re-captures the step graph)."""
-    if grid_n * T <= budget_cells // 8:
-        return grid_n
+def capacity_for(n, grid_n, T):
+    """Tile capacity of a level: 1.5x the need (at least +256) rounded to 256
+    tiles, capped by the tile grid.  Kernels launch over the capacity and exit
+    past the live count, so headroom costs empty blocks; growth bumps
+    ``cap_version`` (the step graphs are re-captured)."""
     return min(grid_n, ((max(int(1.5 * n), n + 256) + 255) // 256) * 256)
 
 
@@ -223,16 +223,23 @@ class Topology:
         L.check(L.lib().mlbm_build_neighbors(L.C.byref(st), L.ptr(lt.nbr), L.stream_handle()),
                 "build_neighbors")
 
-    def commit(self, kinds: dict, counts: dict):
-        """Make the compacted maps / kinds current; host counts become the
-        known new counts; bumps the topology version."""
+    def commit_device(self, kinds: dict):
+        """Make the compacted maps / kinds current (device copies only)."""
         for level, kind in kinds.items():
             lt = self.lv[level]
             lt.tile_map.copy_(lt.tile_map_new)
             if kind.data_ptr() != lt.kind.data_ptr():
                 lt.kind.copy_(kind)
-            lt.n_tiles = int(counts[level])
+
+    def commit_host(self, counts: dict):
+        """Host mirrors take the known new counts; bumps the topology version."""
+        for level, n in counts.items():
+            self.lv[level].n_tiles = int(n)
         self.bump()
+
+    def commit(self, kinds: dict, counts: dict):
+        self.commit_device(kinds)
+        self.commit_host(counts)
 
     def rebuild(self, kinds: dict):
         """Replace the kind grids of the given levels (host-driven path used

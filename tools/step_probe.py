@@ -20,5 +20,5 @@ import numpy as np
 dts = np.array([r[1] for r in rows])
 ch = np.array([r[3] for r in rows]) > 0
 cp = np.array([r[2] for r in rows]) > 0
-print("mean %.3f ms, steps with change %d (mean %.3f ms), no-change no-capture mean %.3f ms" % (
+print("captures %d rebuild eager %d replays %d" % (sim.graph_captures, sim.rebuild_eager, sim.rebuild_replays)); print("mean %.3f ms, steps with change %d (mean %.3f ms), no-change no-capture mean %.3f ms" % (
     dts.mean(), ch.sum(), dts[ch].mean() if ch.any() else 0, dts[~ch & ~cp].mean()))
