@@ -276,8 +276,10 @@ int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, void* p, int64
  * buffers.  In mlbm_p2g, smem = 1 accumulates per block in shared memory over
  * the block's bounding box; smem = 2 accumulates per warp in registers (nodes
  * owned by lanes, particles broadcast by shuffles); smem = 3 lets lane k own
- * stencil node k of the current cell and flushes per cell into a block box
- * (the default) — all three need sorted input. */
+ * stencil node k of the current cell and flushes per cell into a block box;
+ * smem = 4 (fp32 only, the default for fp32 runs; fp64 falls back to 3) keeps
+ * one box copy per warp so the per-cell flushes need no shared-memory atomics
+ * — all four need sorted input. */
 int64_t mlbm_sort_ws_bytes(int64_t n);
 int mlbm_particle_sort(const mlbm_level_t* lv0, int32_t n, const double* x, const void* p,
                        const int32_t* pid, int64_t ps, double* x_out, void* p_out,

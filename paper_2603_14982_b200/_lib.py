@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-LIBPATH = os.path.join(HERE, "libmlbm_b200.so")
+LIBPATH = os.environ.get("MLBM_LIB") or os.path.join(HERE, "libmlbm_b200.so")
 SOURCES = ["lbm.cu", "topology.cu", "mpm.cu", "adapt.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
               "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
@@ -32,10 +32,12 @@ def _nvcc():
     return "nvcc"
 
 
-def build(force=False, verbose=False):
-    """Compile every .cu into the in-tree shared library (objects cached)."""
+def build(force=False, verbose=False, extra=(), out=None):
+    """Compile every .cu into the in-tree shared library (objects cached).
+    ``extra`` nvcc flags + ``out`` path build a tuning variant (tools/)."""
     objs = []
-    bdir = os.path.join(HERE, "build")
+    libpath = out or LIBPATH
+    bdir = os.path.join(os.path.dirname(out), "build") if out else os.path.join(HERE, "build")
     os.makedirs(bdir, exist_ok=True)
     hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     hdrs.append(os.path.join(INCLUDE, "mlbm_b200.h"))
@@ -48,21 +50,21 @@ def build(force=False, verbose=False):
         if (not force and os.path.exists(op) and os.path.getmtime(op) >=
                 max(os.path.getmtime(sp), hmt)):
             continue
-        cmd = [_nvcc()] + NVCC_FLAGS + ["-I", INCLUDE, "-c", sp, "-o", op]
+        cmd = [_nvcc()] + NVCC_FLAGS + list(extra) + ["-I", INCLUDE, "-c", sp, "-o", op]
         if verbose:
             print(" ".join(cmd))
         procs.append((cmd, subprocess.Popen(cmd)))
     for cmd, p in procs:
         if p.wait() != 0:
             raise subprocess.CalledProcessError(p.returncode, cmd)
-    if (force or not os.path.exists(LIBPATH) or
-            os.path.getmtime(LIBPATH) < max(os.path.getmtime(o) for o in objs)):
+    if (force or not os.path.exists(libpath) or
+            os.path.getmtime(libpath) < max(os.path.getmtime(o) for o in objs)):
         cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
-               "-o", LIBPATH] + objs + ["-lcudart"]
+               "-o", libpath] + objs + ["-lcudart"]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
-    return LIBPATH
+    return libpath
 
 
 # -- C structs (mirror include/mlbm_b200.h) ------------------------------------

@@ -176,7 +176,8 @@ class CoupledSim:
         self.sort_particles = True
         self.sort_every = 4        # particles move < 1 cell/step: re-sort every few steps
         self._sort_now = True
-        self.p2g_mode = 3          # sorted input: 1 block smem, 2 warp registers, 3 cell lanes
+        self.p2g_mode = 4          # sorted input: 1 block smem, 2 warp registers, 3 cell lanes,
+                                   # 4 cell lanes + per-warp box copies (fp32; fp64 runs mode 3)
         self._graphs = {}
         self._graph_ver = None
         self._pool = None

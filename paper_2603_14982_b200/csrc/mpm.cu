@@ -867,9 +867,16 @@ __global__ void k_diag_level(mlbm_level_t lv, mlbm_fields_t f, double vol, doubl
         acc[D] += vol * (double)a.at(fi_phi<D>(), c);
         emin = fmin(emin, (double)a.at(fi_eps<D>(), c));
     }
+    // block min, then one compare-and-swap per block (not per warp)
+    __shared__ double smin[32];
     for (int off = 16; off > 0; off >>= 1) emin = fmin(emin, __shfl_down_sync(0xffffffffu, emin, off));
-    if ((threadIdx.x & 31) == 0 && emin < 1e300) atomic_min_double(&out[D + 1], emin);
-    block_sum_atomic<D + 1>(acc, out);
+    if ((threadIdx.x & 31) == 0) smin[threadIdx.x >> 5] = emin;
+    block_sum_atomic<D + 1>(acc, out);          // contains __syncthreads
+    if (threadIdx.x == 0) {
+        double m = smin[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, smin[w]);
+        if (m < 1e300 && m < *(volatile double*)&out[D + 1]) atomic_min_double(&out[D + 1], m);
+    }
 }
 
 // out[0..D-1] += sum m v ; out[D..2D-1] += sum fs (level-0 cells)
@@ -1252,6 +1259,15 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
 // cell's particles are broadcast; at each cell change the lanes flush into a
 // block-wide shared-memory box (one conflict-free RED per lane and row), and
 // the block box is flushed to HBM once.  No coverage tests, no idle-node work.
+#ifndef P2G2_MAXN
+#define P2G2_MAXN 192
+#endif
+#ifndef P2G2_NW
+#define P2G2_NW 4
+#endif
+#ifndef P2G2_ROUNDS
+#define P2G2_ROUNDS 1
+#endif
 template <int D, typename R>
 __global__ void __launch_bounds__(128) k_p2g_cell(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int64_t rs,
                                                   mlbm_error_t* err) {
@@ -1479,6 +1495,273 @@ __global__ void __launch_bounds__(128) k_p2g_cell(PartArgs P, TopoL0 t0, MatPara
         }
     }
 }
+
+// ---------------------------------------------------------------------------
+// Cell-cooperative P2G, fp32, atomic-free in shared memory (smem mode 4).
+// Same decomposition as k_p2g_cell (lane k owns stencil node k of the current
+// cell; particles of a warp broadcast from a per-warp record slab), but
+//  * every warp owns a private copy of the block's node box, so the per-cell
+//    flushes are plain read-add-write (shared-memory fp32 atomics lower to a
+//    compare-and-swap loop on this architecture); the NW copies are summed
+//    once when the box is written to HBM;
+//  * the lane's B-spline weights are per-lane quadratics c0 + c1 f + c2 f^2
+//    (coefficients fixed by the lane's node offset), no selects per particle.
+// per-particle P2G record (fp32): base[3] f[D] m V0 ap q[D] mv[D] S[NS] PC[D*D]
+// (granular.py:282-310: APIC affine momentum, V0 * Kirchhoff stress, area)
+template <int D>
+__device__ __forceinline__ void p2g_record(const PartArgs& P, const MatParams& mp, int p, bool valid,
+                                           float* rec) {
+    constexpr int NS = D * (D + 1) / 2;
+    using PR = PRows<D>;
+    const float* pp = (const float*)P.p;
+    int base[3] = {0, 0, 0};
+        float f[D], m = 0.f, V0 = 0.f, ap = 0.f, mv[D], q[D], PC[D * D], S[NS];
+#pragma unroll
+        for (int a = 0; a < D; ++a) { f[a] = 0.f; mv[a] = 0.f; q[a] = 0.f; }
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) PC[k] = 0.f;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) S[k] = 0.f;
+        if (valid) {
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const double x = P.x[a * P.ps + p];
+                const double b = floor(x - 0.5);
+                base[a] = (int)b;
+                f[a] = (float)(x - b);
+            }
+            m = pp[PR::M * P.ps + p];
+            V0 = pp[PR::V0 * P.ps + p];
+            float v[D], C[D * D], F[D * D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) v[a] = pp[(PR::V + a) * P.ps + p];
+#pragma unroll
+            for (int k = 0; k < D * D; ++k) { C[k] = pp[(PR::C + k) * P.ps + p]; F[k] = pp[(PR::F + k) * P.ps + p]; }
+            float tau[D * D];
+            kirchhoff<D, float>(F, mp, tau);
+            ap = D == 2 ? 2.f * sqrtf(V0 / 3.14159265358979323846f)
+                        : 3.14159265358979323846f * powf(3.f * V0 / (4.f * 3.14159265358979323846f), 2.f / 3.f);
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                mv[a] = m * v[a];
+                float cf = 0.f;
+#pragma unroll
+                for (int b = 0; b < D; ++b) { PC[a * D + b] = m * C[a * D + b]; cf += C[a * D + b] * f[b]; }
+                q[a] = m * (v[a] - cf);
+            }
+            int k = 0;
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int b = a; b < D; ++b) S[k++] = V0 * tau[a * D + b];
+        }
+        // record: base[3] f[D] m V0 ap q[D] mv[D] S[NS] PC[D*D]
+        int o2 = 0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) rec[o2++] = __int_as_float(a < D ? base[a] : 0);
+#pragma unroll
+        for (int a = 0; a < D; ++a) rec[o2++] = f[a];
+        rec[o2++] = m;
+        rec[o2++] = V0;
+        rec[o2++] = ap;
+#pragma unroll
+        for (int a = 0; a < D; ++a) rec[o2++] = q[a];
+#pragma unroll
+        for (int a = 0; a < D; ++a) rec[o2++] = mv[a];
+#pragma unroll
+        for (int kk = 0; kk < NS; ++kk) rec[o2++] = S[kk];
+#pragma unroll
+        for (int kk = 0; kk < D * D; ++kk) rec[o2++] = PC[kk];
+    }
+
+template <int D, int NW, int ROUNDS>
+__global__ void __launch_bounds__(32 * NW) k_p2g_cell2(PartArgs P, TopoL0 t0, MatParams mp, float* ras,
+                                                       int64_t rs, mlbm_error_t* err) {
+    constexpr int K = Geo<D>::K, NV = 3 + 3 * D, NS = D * (D + 1) / 2;
+    constexpr int MAXN = P2G2_MAXN, REC = 32, BT = 32 * NW;
+    extern __shared__ __align__(16) float p2g_smem[];
+    float* sacc = p2g_smem;                                  // [NW][NV][MAXN]
+    float* slab = p2g_smem + NW * NV * MAXN;                 // [NW][32][REC]
+    __shared__ int s_lo[3], s_hi[3];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int p0 = blockIdx.x * (BT * ROUNDS);
+    // block node box over all rounds
+    if (threadIdx.x < 3) { s_lo[threadIdx.x] = 0x7fffffff; s_hi[threadIdx.x] = -0x7fffffff; }
+    __syncthreads();
+    {
+        int bl[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, bh[3] = {-0x7fffffff, -0x7fffffff, -0x7fffffff};
+#pragma unroll
+        for (int r = 0; r < ROUNDS; ++r) {
+            const int p = p0 + r * BT + threadIdx.x;
+            if (p < P.n) {
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    const int b = (int)floor(P.x[a * P.ps + p] - 0.5);
+                    bl[a] = min(bl[a], b);
+                    bh[a] = max(bh[a], b + 2);
+                }
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const int l2 = __reduce_min_sync(0xffffffffu, bl[a]);
+            const int h2 = __reduce_max_sync(0xffffffffu, bh[a]);
+            if (lane == 0 && l2 <= h2) { atomicMin(&s_lo[a], l2); atomicMax(&s_hi[a], h2); }
+        }
+    }
+    __syncthreads();
+    int lo[3] = {0, 0, 0}, ext[3] = {1, 1, 1}, nbox = 1;
+#pragma unroll
+    for (int a = 0; a < D; ++a) { lo[a] = s_lo[a]; ext[a] = s_hi[a] - s_lo[a] + 1; nbox *= ext[a]; }
+    const bool use_smem = nbox > 0 && nbox <= MAXN;
+    if (use_smem) {
+        const int n4 = (nbox + 3) >> 2;
+        float4* s4 = reinterpret_cast<float4*>(sacc);
+        for (int i = threadIdx.x; i < NW * NV * n4; i += BT) {
+            const int row = i / n4, c4 = i - row * n4;
+            s4[row * (MAXN / 4) + c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+    __syncthreads();
+
+    const int o[3] = {lane % 3, (lane / 3) % 3, D == 3 ? (lane / 9) % 3 : 0};
+    const bool node_lane = lane < K;
+    float c0[D], c1[D], c2[D], d0[D], d1[D], of[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const int oa = o[a];
+        c2[a] = oa == 1 ? -1.f : 0.5f;
+        c1[a] = oa == 0 ? -1.5f : (oa == 1 ? 2.f : -0.5f);
+        c0[a] = oa == 0 ? 1.125f : (oa == 1 ? -0.25f : 0.125f);
+        d1[a] = oa == 1 ? -2.f : 1.f;
+        d0[a] = oa == 0 ? -1.5f : (oa == 1 ? 2.f : -0.5f);
+        of[a] = (float)oa;
+    }
+    float* wacc = sacc + wid * NV * MAXN;
+    float* wslab = &slab[wid * 32 * REC];
+    float acc[NV];
+    int cur[3] = {0, 0, 0};
+    bool bad = false;
+    constexpr int OF = 3, OM = 3 + D, OQ = 6 + D, OMV = 6 + 2 * D, OS = 6 + 3 * D, OP = 6 + 3 * D + NS;
+    constexpr int NREC4 = (OP + D * D + 3) / 4;
+#pragma unroll 1
+    for (int rd = 0; rd < ROUNDS; ++rd) {
+        const int pw = p0 + rd * BT + wid * 32;           // first particle of this warp's chunk
+        const int nj = min(32, P.n - pw);
+        if (nj <= 0) break;                               // warp-uniform
+        const int p = pw + lane;
+        p2g_record<D>(P, mp, p, lane < nj, &wslab[lane * REC]);
+        __syncwarp();
+        // runs of equal stencil base (particles sorted by cell)
+        int base[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) base[a] = __float_as_int(wslab[lane * REC + a]);
+        bool start = lane < nj;
+        {
+            bool same = lane > 0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) same &= __shfl_up_sync(0xffffffffu, base[a], 1) == base[a];
+            start &= !same;
+        }
+        unsigned runs = __ballot_sync(0xffffffffu, start);
+        while (runs) {
+            const int j0 = __ffs(runs) - 1;
+            runs &= runs - 1;
+            const int j1 = runs ? __ffs(runs) - 1 : nj;
+    #pragma unroll
+            for (int a = 0; a < 3; ++a) cur[a] = __shfl_sync(0xffffffffu, a < D ? base[a] : 0, j0);
+    #pragma unroll
+            for (int qv = 0; qv < NV; ++qv) acc[qv] = 0.f;
+            for (int j = j0; j < j1; ++j) {
+                const float4* rp = reinterpret_cast<const float4*>(&wslab[j * REC]);
+                float r[4 * NREC4];
+    #pragma unroll
+                for (int v4 = 0; v4 < NREC4; ++v4) {
+                    const float4 t = rp[v4];
+                    r[4 * v4] = t.x; r[4 * v4 + 1] = t.y; r[4 * v4 + 2] = t.z; r[4 * v4 + 3] = t.w;
+                }
+                float wa[D], dwa[D];
+    #pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    const float fa = r[OF + a];
+                    wa[a] = fmaf(fmaf(c2[a], fa, c1[a]), fa, c0[a]);
+                    dwa[a] = fmaf(d1[a], fa, d0[a]);
+                }
+                float w = wa[0];
+    #pragma unroll
+                for (int a = 1; a < D; ++a) w *= wa[a];
+                float g[D];
+    #pragma unroll
+                for (int b = 0; b < D; ++b) {
+                    float gb = dwa[b];
+    #pragma unroll
+                    for (int e = 0; e < D; ++e) if (e != b) gb *= wa[e];
+                    g[b] = gb;
+                }
+                acc[0] = fmaf(w, r[OM], acc[0]);
+                acc[1 + 2 * D] = fmaf(w, r[OM + 1], acc[1 + 2 * D]);
+                acc[2 + 2 * D] = fmaf(w, r[OM + 2], acc[2 + 2 * D]);
+    #pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    float mo = r[OQ + a];
+    #pragma unroll
+                    for (int b = 0; b < D; ++b) mo = fmaf(r[OP + a * D + b], of[b], mo);
+                    acc[1 + a] = fmaf(w, mo, acc[1 + a]);
+                    float fa = acc[1 + D + a];
+    #pragma unroll
+                    for (int b = 0; b < D; ++b) {
+                        const int sk = a <= b ? a * D - a * (a - 1) / 2 + (b - a) : b * D - b * (b - 1) / 2 + (a - b);
+                        fa = fmaf(-r[OS + sk], g[b], fa);
+                    }
+                    acc[1 + D + a] = fa;
+                    acc[3 + 2 * D + a] = fmaf(w, r[OMV + a], acc[3 + 2 * D + a]);
+                }
+            }
+            if (node_lane && (acc[0] != 0.f || acc[2 + 2 * D] != 0.f)) {
+                int c[3] = {cur[0] + o[0], cur[1] + o[1], D == 3 ? cur[2] + o[2] : 0};
+                if (use_smem) {
+                    int li = 0;
+    #pragma unroll
+                    for (int a = D - 1; a >= 0; --a) li = li * ext[a] + (c[a] - lo[a]);
+    #pragma unroll
+                    for (int qv = 0; qv < NV; ++qv) wacc[qv * MAXN + li] += acc[qv];
+                } else {
+                    const int64_t ni = node_index<D>(t0, c, bad);
+                    if (ni >= 0) {
+    #pragma unroll
+                        for (int qv = 0; qv < NV; ++qv) atomicAdd(&ras[qv * rs + ni], acc[qv]);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        __syncwarp();                                     // slab reused next round
+    }
+    if (bad) report_error(err, MLBM_ERR_STENCIL, 0, cur[0], cur[1], cur[2]);
+    if (!use_smem) return;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nbox; i += blockDim.x) {
+        float tot[NV];
+#pragma unroll
+        for (int qv = 0; qv < NV; ++qv) {
+            float v = sacc[qv * MAXN + i];
+#pragma unroll
+            for (int w2 = 1; w2 < NW; ++w2) v += sacc[(w2 * NV + qv) * MAXN + i];
+            tot[qv] = v;
+        }
+        if (tot[0] == 0.f && tot[2 + 2 * D] == 0.f) continue;
+        int c[3] = {0, 0, 0};
+        int rr = i;
+#pragma unroll
+        for (int a = 0; a < D; ++a) { c[a] = lo[a] + rr % ext[a]; rr /= ext[a]; }
+        bool b2 = false;
+        const int64_t ni = node_index<D>(t0, c, b2);
+        if (ni < 0) { report_error(err, MLBM_ERR_STENCIL, 0, c[0], c[1], c[2]); continue; }
+#pragma unroll
+        for (int qv = 0; qv < NV; ++qv)
+            if (tot[qv] != 0.f) atomicAdd(&ras[qv * rs + ni], tot[qv]);
+    }
+}
 }  // namespace mlbm
 
 using namespace mlbm;
@@ -1502,6 +1785,21 @@ extern "C" int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, voi
     PartArgs P{lv0->dim, n, x, nullptr, p, ps, nullptr, nullptr, nullptr};
     MatParams mp{lam, mu, alpha, 0.0};
     const TopoL0 t = topo0(lv0);
+    if (smem == 4 && dtype == 0) {
+        constexpr int NW = P2G2_NW;
+        const int sh = (NW * (3 + 3 * 3) * P2G2_MAXN + NW * 32 * 32) * (int)sizeof(float);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_p2g_cell2<3, NW, P2G2_ROUNDS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
+            cudaFuncSetAttribute(k_p2g_cell2<2, NW, P2G2_ROUNDS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
+            attr = true;
+        }
+        constexpr int RD = P2G2_ROUNDS;
+        if (lv0->dim == 2) k_p2g_cell2<2, NW, RD><<<nblk(n, 32 * NW * RD), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
+        else k_p2g_cell2<3, NW, RD><<<nblk(n, 32 * NW * RD), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
+        return launch_status(1);
+    }
+    if (smem == 4) smem = 3;
 #define P2G(D, R) do { if (smem == 3) k_p2g_cell<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
                        else if (smem == 2) k_p2g_warp<D, R, 3><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
                        else if (smem) k_p2g_smem<D, R><<<nblk(n, 256), 256, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
@@ -1644,7 +1942,7 @@ extern "C" int mlbm_diag_particles(int32_t dim, int32_t n, const void* p, int64_
     if (m == 0) return 0;
     PartArgs P{dim, n, nullptr, nullptr, (void*)p, ps, nullptr, nullptr, nullptr};
     cudaStream_t s = as_stream(stream);
-    const int gb = (int)std::min<int64_t>(nblk(m, 256), 592);
+    const int gb = (int)std::min<int64_t>(nblk(m, 256), 296);
 #define DP(D, R) k_diag_particles<D, R><<<gb, 256, 0, s>>>(P, (const R*)ras, rs, n0, live, out)
     if (dim == 2) { if (dtype) DP(2, double); else DP(2, float); }
     else { if (dtype) DP(3, double); else DP(3, float); }

@@ -149,3 +149,38 @@ def test_fp32_column_3d_short():
     rv = np.linalg.norm(v - osim.p.v) / max(np.linalg.norm(osim.p.v), 1e-30)
     assert rx <= 1e-5, rx
     assert rv <= 1e-4, rv
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_p2g_modes_agree(dtype):
+    """Every P2G variant (atomic, block smem, warp registers, cell lanes,
+    per-warp box copies) rasterises the same sorted particle set: fp64
+    within summation-order noise, fp32 within 1e-5 of the row maximum."""
+    _need_gpu()
+    from paper_2603_14982_b200 import _lib as L
+    from paper_2603_14982_b200.harness import build_scene, validate_scene
+    sim = build_scene(validate_scene(S.scene(S.COLUMN_3D_SMALL, runtime__dtype=dtype)))
+    for _ in range(3):
+        sim.step()
+    lib, s = L.lib(), L.stream_handle()
+    p, grid, mat = sim.particles, sim.grid, sim.material
+    lv0 = grid.level0()
+    n, ps = len(p), p.pd.stride(0)
+    dcode = 1 if dtype == "f64" else 0
+    xa, pa, ida, ws = p.scratch()
+    L.check(lib.mlbm_particle_sort(L.C.byref(lv0), n, L.ptr(p.xd), L.ptr(p.pd), L.ptr(p.pid), ps,
+                                   L.ptr(xa), L.ptr(pa), L.ptr(ida), dcode, L.ptr(ws), ws.numel(),
+                                   s), "sort")
+    nacc = grid.R["nacc"]
+    out = []
+    for mode in range(5):
+        grid.clear()
+        L.check(lib.mlbm_p2g(L.C.byref(lv0), n, L.ptr(xa), L.ptr(pa), ps, mat.lam, mat.mu,
+                             mat.alpha, L.ptr(grid.ras), grid.ras.stride(0), dcode, mode,
+                             L.ptr(grid._err), s), "p2g")
+        out.append(grid.ras[:nacc, :grid._live()].double().clone())
+    grid.raise_pending()
+    scale = out[0].abs().amax(dim=1, keepdim=True).clamp_min(1e-300)
+    tol = 1e-12 if dtype == "f64" else 1e-5
+    for mode in range(1, 5):
+        assert ((out[mode] - out[0]).abs() / scale).max().item() <= tol, mode

@@ -1,0 +1,42 @@
+"""P2G / G2P kernel variants on the C2 particle state: time (CUDA events,
+L2 not flushed) and agreement of the rasters between modes."""
+import sys
+sys.path.insert(0, "."); sys.path.insert(0, "tests")
+import torch
+import scenes as S
+from paper_2603_14982_b200 import _lib as L
+from paper_2603_14982_b200.harness import build_scene, validate_scene
+sim = build_scene(validate_scene(S.COLUMN_3D_C2))
+for _ in range(12):
+    sim.step()
+torch.cuda.synchronize()
+lib = L.lib()
+s = L.stream_handle()
+p, grid, mat = sim.particles, sim.grid, sim.material
+lv0 = grid.level0()
+n = len(p)
+ps = p.pd.stride(0)
+xa, pa, ida, ws = p.scratch()
+L.check(lib.mlbm_particle_sort(L.C.byref(lv0), n, L.ptr(p.xd), L.ptr(p.pd), L.ptr(p.pid), ps,
+                               L.ptr(xa), L.ptr(pa), L.ptr(ida), 0, L.ptr(ws), ws.numel(), s), "sort")
+NACC = grid.R["nacc"]
+out = {}
+for mode in [int(m) for m in (sys.argv[1:] or ["3", "4"])]:
+    ts = []
+    for rep in range(30):
+        grid.clear()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        L.check(lib.mlbm_p2g(L.C.byref(lv0), n, L.ptr(xa), L.ptr(pa), ps, mat.lam, mat.mu, mat.alpha,
+                             L.ptr(grid.ras), grid.ras.stride(0), 0, mode, L.ptr(grid._err), s), "p2g")
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    out[mode] = grid.ras[:NACC].clone()
+    ts.sort()
+    print("p2g mode %d: median %.1f us  min %.1f us" % (mode, ts[len(ts) // 2], ts[0]))
+ref = out[min(out)]
+for m, r in out.items():
+    scale = ref.abs().amax(dim=1, keepdim=True).clamp_min(1e-30)
+    print("mode %d vs %d: max rel-to-row-max diff %.3e" % (m, min(out), ((r - ref).abs() / scale).max().item()))
+print("error record", grid._err.cpu().numpy()[:4])
