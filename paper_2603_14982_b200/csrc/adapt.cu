@@ -152,6 +152,9 @@ __device__ bool children_any(const uint8_t* src, const int* dc, int dim, const i
     return false;
 }
 
+// Hysteresis of one level (adapt.py:140-181): one thread per tile; the 2^dim
+// tiles of a sibling group sit in consecutive lanes, so "all siblings may
+// coarsen" is a 2^dim-lane AND over shuffles.
 __device__ void effective_stage(const AdaptArgs& A, int l, bool with_guard, int64_t tid, int64_t nth) {
     const int* d = A.tdims[l];
     const int dim = A.dim;
@@ -159,48 +162,55 @@ __device__ void effective_stage(const AdaptArgs& A, int l, bool with_guard, int6
     for (int a = 0; a < dim; ++a) grouped &= (d[a] % 2) == 0;
     int gd[3] = {d[0], d[1], d[2]};
     if (grouped) for (int a = 0; a < dim; ++a) gd[a] = d[a] / 2;
-    const int64_t ng = (int64_t)gd[0] * gd[1] * gd[2];
     const int K = grouped ? (1 << dim) : 1;
+    const int64_t total = (int64_t)gd[0] * gd[1] * gd[2] * K;
     const uint8_t* par = A.par[l];
-    for (int64_t j = tid; j < ng; j += nth) {
-        int x[3];
-        dec3(gd, j, x[0], x[1], x[2]);
-        int64_t gix[8];
-        bool avail[8];
-        bool all = true;
-        bool cand[8];
-        int16_t st[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (k >= K) break;
-            int c[3];
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = tid - lane; base < total; base += nth) {      // warp-uniform trip count
+        const int64_t t = base + lane;
+        const bool valid = t < total;
+        int64_t g = 0;
+        bool cand = false, avail = false;
+        int c[3] = {0, 0, 0};
+        if (valid) {
+            const int64_t j = t / K;
+            const int k = (int)(t - j * K);
+            int x[3];
+            dec3(gd, j, x[0], x[1], x[2]);
             for (int a = 0; a < 3; ++a) c[a] = (grouped && a < dim) ? 2 * x[a] + ((k >> a) & 1) : x[a];
-            const int64_t g = gi3(d, c[0], c[1], c[2]);
-            gix[k] = g;
-            cand[k] = A.cur[l][g] && !A.des[l][g];
-            st[k] = A.streak[l][g];
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (k >= K) break;
-            const int16_t s = cand[k] ? (int16_t)(st[k] + 1) : (int16_t)0;
-            A.streak[l][gix[k]] = s;
+            g = gi3(d, c[0], c[1], c[2]);
+            cand = A.cur[l][g] && !A.des[l][g];
+            const int16_t sv = cand ? (int16_t)(A.streak[l][g] + 1) : (int16_t)0;
+            A.streak[l][g] = sv;
             bool guard = false;
-            if (with_guard && cand[k] && s >= 2) {
-                int c[3];
-                for (int a = 0; a < 3; ++a) c[a] = (grouped && a < dim) ? 2 * x[a] + ((k >> a) & 1) : x[a];
-                guard = window_any(par, d, dim, A.periodic, c, 2);
-            }
-            avail[k] = cand[k] && s >= 2 && !guard;
-            all &= avail[k];
+            if (with_guard && cand && sv >= 2) guard = window_any(par, d, dim, A.periodic, c, 2);
+            avail = cand && sv >= 2 && !guard;
         }
-        for (int k = 0; k < K; ++k) {
-            const int64_t g = gix[k];
-            const bool act = grouped ? (avail[k] && all) : false;
+        bool all = avail;
+        for (int off = 1; off < K; off <<= 1) all &= __shfl_xor_sync(0xffffffffu, all, off) != 0;
+        if (valid) {
+            const bool act = grouped ? all : false;
             const bool pp = with_guard ? par[g] != 0 : false;
             A.eff[l][g] = (A.des[l][g] || (A.cur[l][g] && !act) || pp) ? 1 : 0;
         }
     }
+}
+
+// OR of src over the radius-2 window along one axis (wrap / clip)
+__device__ __forceinline__ bool axis_or2(const uint8_t* src, const int* d, const int* per, const int (&c)[3],
+                                         int axis) {
+    const int n = d[axis];
+    bool any = false;
+#pragma unroll
+    for (int k = -2; k <= 2; ++k) {
+        int v = c[axis] + k;
+        if (per[axis]) { v %= n; if (v < 0) v += n; }
+        else if (v < 0 || v >= n) continue;
+        int q[3] = {c[0], c[1], c[2]};
+        q[axis] = v;
+        any |= src[gi3(d, q[0], q[1], q[2])] != 0;
+    }
+    return any;
 }
 
 // Branchless, fully unrolled radius-2 windows: out-of-domain taps are
@@ -349,35 +359,63 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
         }
         if (cnt != 1) atomicAdd(&A.status[L], 1);
     }
+    // two-tile rings of the current leaves (sparse_grid.py:320-337): the
+    // absent tiles inside dilate2(leaf) are counted; the dilation is done as
+    // three separable radius-2 ORs spread over phases A (x -> stor), C
+    // (y -> nkind) and F (z + count), in buffers that are free until I/J
     for (int l = 0; l < L; ++l) {
         const int* d = A.tdims[l];
         const int64_t n = (int64_t)d[0] * d[1] * d[2];
-        // two-tile ring of every leaf: count absent tiles (sparse_grid.py:320-337)
         const uint8_t* kind = A.kind[l];
+        const int nx = d[0], per0 = A.periodic[0];
         for (int64_t g = tid; g < n; g += nth) {
-            if (kind[g] != 1) continue;
             int c[3];
             dec3(d, g, c[0], c[1], c[2]);
-            const int miss = window_count<false>(kind, d, dim, A.periodic, c);
-            if (miss) atomicAdd(&A.status[L + 1], miss);
+            bool any = false;
+#pragma unroll
+            for (int k = -2; k <= 2; ++k) {
+                int v = c[0] + k;
+                if (per0) { v %= nx; if (v < 0) v += nx; }
+                else if (v < 0 || v >= nx) continue;
+                any |= kind[gi3(d, v, c[1], c[2])] == 1;
+            }
+            A.stor[l][g] = any;
         }
     }
     // ---- B (same stage): particle seeds (seeds are all-zero on entry, they are
     //      cleared at the end of every pass) + particles in level-0 leaves
-    for (int64_t p = tid; p < A.n; p += nth) {
-        int t[3] = {0, 0, 0};
-        bool bad = false;
-        for (int a = 0; a < dim; ++a) {
-            const double v = A.x[a * A.xs + p];
-            const int64_t c = (int64_t)floor(v);
-            const int64_t tt = c >= 0 ? c / 4 : -((-c + 3) / 4);
-            if (tt < 0 || tt >= d0[a] || !(v == v)) bad = true;
-            t[a] = (int)tt;
+    constexpr int PU = 4;                       // particles per thread per trip (loads first)
+    for (int64_t p0 = tid; p0 < A.n; p0 += PU * nth) {
+        double v[PU][3];
+#pragma unroll
+        for (int u = 0; u < PU; ++u) {
+            const int64_t p = p0 + u * nth;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) v[u][a] = (p < A.n && a < dim) ? __ldg(&A.x[a * A.xs + p]) : 0.0;
         }
-        if (bad) { report_error(A.err, MLBM_ERR_DOMAIN, 0, t[0], t[1], t[2]); atomicAdd(&A.status[L + 2], 1); continue; }
-        const int64_t g = gi3(d0, t[0], t[1], t[2]);
-        A.seeds[g] = 1;
-        if (A.kind[0][g] != 1) atomicAdd(&A.status[L + 2], 1);
+#pragma unroll
+        for (int u = 0; u < PU; ++u) {
+            const int64_t p = p0 + u * nth;
+            if (p >= A.n) break;
+            int t[3] = {0, 0, 0};
+            bool bad = false;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                if (a >= dim) break;
+                const int64_t c = (int64_t)floor(v[u][a]);
+                const int64_t tt = c >= 0 ? c / 4 : -((-c + 3) / 4);
+                if (tt < 0 || tt >= d0[a] || !(v[u][a] == v[u][a])) bad = true;
+                t[a] = (int)tt;
+            }
+            if (bad) {
+                report_error(A.err, MLBM_ERR_DOMAIN, 0, t[0], t[1], t[2]);
+                atomicAdd(&A.status[L + 2], 1);
+                continue;
+            }
+            const int64_t g = gi3(d0, t[0], t[1], t[2]);
+            A.seeds[g] = 1;
+            if (A.kind[0][g] != 1) atomicAdd(&A.status[L + 2], 1);
+        }
     }
     STAMP_BARRIER(2);
 
@@ -405,6 +443,22 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
             dec3(d1, g, c[0], c[1], c[2]);
             A.cur[1][g] = (A.kind[1][g] == 1) || children_any(A.cur[0], d0, dim, c);
         }
+    }
+    {
+        int miss = 0;
+        for (int l = 0; l < L; ++l) {
+            const int* d = A.tdims[l];
+            const int64_t n = (int64_t)d[0] * d[1] * d[2];
+            for (int64_t g = tid; g < n; g += nth) {
+                int c[3];
+                dec3(d, g, c[0], c[1], c[2]);
+                const bool any = axis_or2(A.stor[l], d, A.periodic, c, 1);
+                if (dim == 3) A.nkind[l][g] = any;
+                else miss += any && A.kind[l][g] == 0;
+            }
+        }
+        for (int off = 16; off > 0; off >>= 1) miss += __shfl_down_sync(0xffffffffu, miss, off);
+        if ((threadIdx.x & 31) == 0 && miss) atomicAdd(&A.status[L + 1], miss);
     }
     STAMP_BARRIER(3);
 
@@ -436,7 +490,22 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
         STAMP_BARRIER(5);
     }
 
-    // ---- F/G/H: hysteresis per level
+    // ---- F/G/H: hysteresis per level (+ the z pass of the ring check)
+    if (dim == 3) {
+        int miss = 0;
+        for (int l = 0; l < L; ++l) {
+            const int* d = A.tdims[l];
+            const int64_t n = (int64_t)d[0] * d[1] * d[2];
+            for (int64_t g = tid; g < n; g += nth) {
+                if (A.kind[l][g] != 0) continue;
+                int c[3];
+                dec3(d, g, c[0], c[1], c[2]);
+                miss += axis_or2(A.nkind[l], d, A.periodic, c, 2);
+            }
+        }
+        for (int off = 16; off > 0; off >>= 1) miss += __shfl_down_sync(0xffffffffu, miss, off);
+        if ((threadIdx.x & 31) == 0 && miss) atomicAdd(&A.status[L + 1], miss);
+    }
     effective_stage(A, 0, false, tid, nth);
     STAMP_BARRIER(6);
     for (int l = 1; l < L; ++l) {
@@ -458,18 +527,43 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
     // par[l] now holds parents(eff[l-1]) for every l >= 1 (eff[L-1] = 1 set
     // after its own parents were taken, as in adapt.py:180-181)
 
-    // ---- I: own
+    // ---- I/J: own = eff & ~parents(eff[l-1]); storage = dilate2(own) as three
+    //      separable radius-2 ORs (x into stor, y into des, z on the fly);
+    //      new kinds, no-op flags (adapt.py:184-225); seeds cleared
     for (int l = 0; l < L; ++l) {
         const int* d = A.tdims[l];
         const int64_t n = (int64_t)d[0] * d[1] * d[2];
-        for (int64_t g = tid; g < n; g += nth)
+        const int per0 = A.periodic[0], nx = d[0];
+        for (int64_t g = tid; g < n; g += nth) {
+            int c[3];
+            dec3(d, g, c[0], c[1], c[2]);
             A.own[l][g] = A.eff[l][g] && !(l > 0 && A.par[l][g]);
+            bool any = false;
+#pragma unroll
+            for (int k = -2; k <= 2; ++k) {
+                int v = c[0] + k;
+                if (per0) { v %= nx; if (v < 0) v += nx; }
+                else if (v < 0 || v >= nx) continue;
+                const int64_t q = gi3(d, v, c[1], c[2]);
+                any |= A.eff[l][q] && !(l > 0 && A.par[l][q]);
+            }
+            A.stor[l][g] = any;
+        }
     }
-    STAMP_BARRIER(10);
-
-    // ---- J: storage = dilate2(own) (unrolled gather), new kinds, no-op flags
-    //      (adapt.py:184-225); seeds cleared for the next pass
     for (int64_t g = tid; g < n0; g += nth) A.seeds[g] = 0;
+    STAMP_BARRIER(10);
+    if (dim == 3) {
+        for (int l = 0; l < L; ++l) {
+            const int* d = A.tdims[l];
+            const int64_t n = (int64_t)d[0] * d[1] * d[2];
+            for (int64_t g = tid; g < n; g += nth) {
+                int c[3];
+                dec3(d, g, c[0], c[1], c[2]);
+                A.des[l][g] = axis_or2(A.stor[l], d, A.periodic, c, 1);
+            }
+        }
+        grid_barrier(A.bar);
+    }
     for (int l = 0; l < L; ++l) {
         const int* d = A.tdims[l];
         const int64_t n = (int64_t)d[0] * d[1] * d[2];
@@ -481,7 +575,9 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
             else {
                 int c[3];
                 dec3(d, g, c[0], c[1], c[2]);
-                k = window_any2(A.own[l], d, dim, A.periodic, c) ? 2 : 0;
+                const bool dil = dim == 3 ? axis_or2(A.des[l], d, A.periodic, c, 2)
+                                          : axis_or2(A.stor[l], d, A.periodic, c, 1);
+                k = dil ? 2 : 0;
             }
             A.nkind[l][g] = k;
             const uint8_t old = A.kind[l][g];
@@ -499,6 +595,7 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
             if (fresh) atomicAdd(&A.status[2 * L + 4 + l], fresh);
         }
     }
+    if (A.ts) STAMP_BARRIER(11);
 }
 
 }  // namespace mlbm

@@ -533,24 +533,44 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
 #pragma unroll
     for (int k = 0; k < D * D; ++k) B[k] = R(0);
     bool bad = false;
-#pragma unroll 1
+    // per-axis node coordinates of the 3^D stencil: tile coordinate (-1 when
+    // outside a non-periodic box) and in-tile offset; the 27 tile-map reads
+    // hit L1 (at most 2^D distinct tiles)
+    int tix[3][3], loc[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+            if (a >= D) { tix[a][o] = 0; loc[a][o] = 0; continue; }
+            int c = st.base[a] + o;
+            const int nc = t0.cells[a];
+            if (t0.periodic[a]) c = c < 0 ? c + nc : (c >= nc ? c - nc : c);
+            const bool in = c >= 0 && c < nc;
+            tix[a][o] = in ? c >> 2 : -1;
+            loc[a][o] = c & 3;
+        }
+    R dp[D][3];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int o = 0; o < 3; ++o) dp[a][o] = R(o) - st.frac[a];
+#pragma unroll
     for (int k = 0; k < K; ++k) {
-        const int o[3] = {k % 3, (k / 3) % 3, k / 9};
-        int c[3] = {st.base[0] + o[0], st.base[1] + o[1], D == 3 ? st.base[2] + o[2] : 0};
-        const int64_t ni = node_index<D>(t0, c, bad);
-        if (ni < 0) continue;
-        R w = R(1);
+        const int o[3] = {k % 3, (k / 3) % 3, D == 3 ? k / 9 : 0};
+        const int tx = tix[0][o[0]], ty = tix[1][o[1]], tz = tix[2][o[2]];
+        if ((tx | ty | tz) < 0) { bad = true; continue; }
+        const int sl = __ldg(&t0.tile_map[((int64_t)tx * t0.tiles[1] + ty) * t0.tiles[2] + tz]);
+        if (sl < 0) { bad = true; continue; }
+        const int64_t ni = (int64_t)sl * Geo<D>::T + local_of<D>(loc[0][o[0]], loc[1][o[1]], loc[2][o[2]]);
+        R w = st.w[0][o[0]];
 #pragma unroll
-        for (int a = 0; a < D; ++a) w *= sel3<R>(st.w[a], o[a]);
-        R dpos[D];
-#pragma unroll
-        for (int a = 0; a < D; ++a) dpos[a] = R((double)(st.base[a] + o[a]) - x[a]);
+        for (int a = 1; a < D; ++a) w *= st.w[a][o[a]];
 #pragma unroll
         for (int a = 0; a < D; ++a) {
             const R wg = w * ras[(RW::VEL + a) * rs + ni];
             v[a] += wg;
 #pragma unroll
-            for (int b = 0; b < D; ++b) B[a * D + b] += wg * dpos[b];
+            for (int b = 0; b < D; ++b) B[a * D + b] += wg * dp[b][o[b]];
         }
     }
     if (bad) report_error(err, MLBM_ERR_STENCIL, 0, st.base[0], st.base[1], st.base[2]);

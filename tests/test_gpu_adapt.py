@@ -95,3 +95,39 @@ def test_particle_outside_domain_raises():
     ad = B.GridAdaptor(topo, B.LevelParams(3, 0.8))
     with pytest.raises(ValueError):
         ad.update(B.RefineDriver(positions=np.array([[70.0, 3.0]]), levels=3), pair)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_invariant_violations_reported_fused_and_unfused(dim):
+    """A tile set with a leaf whose ring is incomplete and a finest tile
+    covered twice: the fused pass and the per-op pass report the same
+    coverage / ring / particle counts (adapt.py:374-389, reported not
+    raised), and a consistent tile set reports none."""
+    _need_gpu()
+    cells = (64, 64) if dim == 2 else (32, 32, 32)
+    topo = B.Topology.uniform(cells, 2)
+    pair = B.PingPongPair(topo)
+    ad = B.GridAdaptor(topo, B.LevelParams(2, 0.8))
+    ctr = np.array(cells, dtype=float) / 2 + 0.3
+    drv = B.RefineDriver(positions=ctr[None, :], levels=2)
+    for _ in range(3):
+        ad.update(drv, pair)
+    ok = topo.tile_set()
+    # drop one border tile next to a leaf at level 0 and add a stray leaf at level 0
+    lvl0 = sorted(t for t in ok if t[0] == 0)
+    border = [t for t in lvl0 if t[-1] == 1][0]
+    stray = (0,) + tuple(0 for _ in range(dim)) + (0,)
+    bad = (set(ok) - {border}) | {stray}
+    Lv = topo.levels
+    counts = {}
+    for fused in (True, False):
+        topo.set_tile_set(sorted(bad))
+        ad.fused = fused
+        ad.plan_device(drv)
+        counts[fused] = ad._status[Lv:Lv + 3].cpu().numpy().tolist()
+    assert counts[True] == counts[False], counts
+    assert counts[True][0] > 0 and counts[True][1] > 0, counts
+    topo.set_tile_set(sorted(ok))
+    ad.fused = True
+    ad.plan_device(drv)
+    assert ad._status[Lv:Lv + 3].cpu().numpy().tolist() == [0, 0, 0]

@@ -33,4 +33,11 @@ if os.environ.get("MLBM_ADAPT_TIMESTAMPS"):
     cudart = ctypes.CDLL("libcudart.so")
     cudart.cudaMemcpy(buf, ctypes.c_void_p(ptr), ctypes.c_size_t(64 * 8), 2)
     ts = list(buf)[:16]
-    print("stage deltas us:", [round((ts[i] - ts[i - 1]) / 1e3, 2) for i in range(1, 16) if ts[i]])
+    names = {0: "start", 2: "A+B seeds/invariants", 3: "C des0/cur1", 4: "D par/cur", 5: "E des[l]",
+             6: "F eff0", 7: "G par(eff)", 8: "H eff[l]", 9: "top eff", 10: "I own", 11: "J storage/kinds"}
+    prev = ts[0]
+    for i in range(2, 12):
+        if ts[i]:
+            print("  %-22s %6.2f us" % (names[i], (ts[i] - prev) / 1e3))
+            prev = ts[i]
+    print("  total                  %6.2f us" % ((prev - ts[0]) / 1e3))
