@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
-    ap.add_argument("--scene", default="c2", choices=["c2", "c1"])
+    ap.add_argument("--scene", default="c2", choices=["c2", "c3", "c1"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -47,13 +47,15 @@ def parse():
 
 def scene_dict(name):
     import scenes as S
-    return S.COLUMN_3D_C2 if name == "c2" else S.TAYLOR_GREEN_3D_C1
+    return {"c2": S.COLUMN_3D_C2, "c3": S.SANDSTORM_3D_C3, "c1": S.TAYLOR_GREEN_3D_C1}[name]
 
 
 def workload_name(name):
-    return ("C2: two-level 128^3-effective 3D granular column collapse in air, 262,144 "
-            "MPM sand particles, two-way coupled, adapt every step" if name == "c2" else
-            "C1: single-level 64^3 periodic Taylor-Green (D3Q27)")
+    return {"c2": "C2: two-level 128^3-effective 3D granular column collapse in air, 262,144 "
+                  "MPM sand particles, two-way coupled, adapt every step",
+            "c3": "C3: three-level 512x256x128-effective sand bed under log-law wind inflow, "
+                  "3,932,160 MPM sand particles, two-way coupled, adapt every step",
+            "c1": "C1: single-level 64^3 periodic Taylor-Green (D3Q27)"}[name]
 
 
 # -- clocks -------------------------------------------------------------------------
@@ -108,14 +110,17 @@ def measured_peak():
 
 
 # -- algorithmic bytes per kernel class ---------------------------------
-def kernel_class(rec, d, s):
+def kernel_class(rec, d, s, live):
+    """(class, algorithmic bytes, units) of one traced C-ABI call.  Kernels are
+    launched over tile capacities; ``live(lv_struct)`` / ``live(ptr)`` give the
+    live tile count of a level / the device count a pointer refers to."""
     name, _, _, _ = rec[:4]
     args = rec[4]
     NM = 1 + d + d * (d + 1) // 2
     T = 4 ** d
     if name == "mlbm_level_step":
         lv, mode = args[0]._obj, int(args[4])
-        cells = lv.n_tiles * T
+        cells = live(lv) * T
         if mode in (0, 1):
             return f"level_step[{'fused' if mode == 0 else 'stream'}]", cells * 2 * NM * s, cells
         return "level_step[collide+bc]", cells * (2 * NM + d + 1) * s, cells
@@ -126,10 +131,10 @@ def kernel_class(rec, d, s):
         n = int(args[1])
         return "g2p", n * (16 * d + (d * d + 1) * s + (d + 2 * d * d + 1) * s), n
     if name == "mlbm_exchange":
-        cells = args[0]._obj.n_tiles * T
+        cells = live(args[0]._obj) * T
         return "exchange", cells * (17 + 25) * s, cells
     if name in ("mlbm_downward", "mlbm_upward"):
-        n = int(args[1])
+        n = live(args[2])
         nc = 1 << d
         return "transfer", n * (nc * (NM + 2) * (2 if name == "mlbm_downward" else 1)
                                 + (NM + 2)) * s, n
@@ -252,9 +257,20 @@ def run_mine(args, rank, world, local_rank):
     t_eager_ms = ek0.elapsed_time(ek1)
     sim.use_graphs = True
     classes = {}
+    dc = sim.topology.dcounts.cpu().numpy()
+    base = sim.topology.dcounts.data_ptr()
+    by_ptr = {base + 4 * i: int(v) for i, v in enumerate(dc.reshape(-1))}
+
+    def live(x):
+        if isinstance(x, int):
+            return by_ptr.get(x, 0)
+        if hasattr(x, "value"):                     # ctypes c_void_p
+            return by_ptr.get(x.value or 0, 0)
+        return sim.topology.n_tiles(int(x.level))
+
     for r in recs:
         name, e0, e1, _ = r[:4]
-        cls, nbytes, units = kernel_class(r, d, s)
+        cls, nbytes, units = kernel_class(r, d, s, live)
         c = classes.setdefault(cls, {"ms": 0.0, "launches": 0, "bytes": 0.0})
         c["ms"] += e0.elapsed_time(e1)
         c["launches"] += 1

@@ -342,6 +342,425 @@ __device__ __forceinline__ void halo_items(R* fb, const R* hc, const int* snb, i
     }
 }
 
+// ===========================================================================
+// D3Q27 stream by sum factorisation.  D3Q27 is the tensor
+// product {-1,0,1}^3 and the reconstruction basis is separable:
+//   g(c) = w1(cx) w1(cy) w1(cz) sum_{n} a[nx][ny][nz] h_nx(cx) h_ny(cy) h_nz(cz)
+// with h0 = 1, h1 = c, h2 = c^2 - 1/3 and the 17 coefficients of make_coef
+// placed at their multi-indices (|n| <= 3).  All 27 populations of a cell cost
+// three 1D passes (~110 flops instead of 13 pairs x ~22); the bare moments of
+// the 27 pulled populations are the transposed passes (~66 adds).  Halo faces,
+// edges and corners are evaluated straight from the neighbour's moments in
+// registers: a face cell contracts its normal axis first and then does a 2D
+// pass over the 9 in-plane directions (no coefficient staging in shared memory).
+namespace tp {
+
+MLBM_HD constexpr double hp(int n, int c) { return n == 0 ? 1.0 : n == 1 ? (double)c : (double)(c * c) - CS2; }
+MLBM_HD constexpr double w1(int c) { return c == 0 ? 2.0 / 3.0 : 1.0 / 6.0; }
+MLBM_HD constexpr bool has3(int nx, int ny, int nz) { return nx + ny + nz <= 3; }
+MLBM_HD constexpr int dir3(int cx, int cy, int cz) {
+    int r = -1;
+    for (int i = 0; i < 27; ++i)
+        if (cvec<3>(i, 0) == cx && cvec<3>(i, 1) == cy && cvec<3>(i, 2) == cz) r = i;
+    return r;
+}
+// multiply by a compile-time Hermite value without rounding-neutral folds lost
+template <typename R> __device__ __forceinline__ R hmul(double h, R x) {
+    return h == 1.0 ? x : (h == -1.0 ? -x : R(h) * x);
+}
+// running sum whose "first" flag resolves at compile time after unrolling
+template <typename R> struct Acc {
+    R s;
+    bool z = true;
+    __device__ __forceinline__ void add(R t) { if (z) { s = t; z = false; } else s += t; }
+};
+
+template <typename R>
+__device__ __forceinline__ void tcoef(const Coef<3, R>& c, R (&a)[3][3][3]) {
+    a[0][0][0] = c.dr;
+    a[1][0][0] = c.A[0];
+    a[0][1][0] = c.A[1];
+    a[0][0][1] = c.A[2];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        int n[3] = {0, 0, 0};
+        ++n[s_a<3>(k)];
+        ++n[s_b<3>(k)];
+        a[n[0]][n[1]][n[2]] = c.B[k];
+    }
+#pragma unroll
+    for (int t = 0; t < 7; ++t) {
+        int n[3] = {0, 0, 0};
+        ++n[h3t<3>(t, 0)];
+        ++n[h3t<3>(t, 1)];
+        ++n[h3t<3>(t, 2)];
+        a[n[0]][n[1]][n[2]] = c.G[t];
+    }
+}
+
+template <typename R>
+__device__ __forceinline__ void load_tcoef(const FieldsT<R>& f, int64_t cell, R h3xyz, R (&a)[3][3][3]) {
+    R m[10];
+    load_moments<3, R>(f, cell, m);
+    Coef<3, R> c;
+    make_coef<3, R>(m, h3xyz, c);
+    tcoef<R>(c, a);
+}
+
+// all 27 populations g[cx+1][cy+1][cz+1]
+template <typename R>
+__device__ __forceinline__ void recon_all(const R (&a)[3][3][3], R (&g)[3][3][3]) {
+    Acc<R> P[3][3][3];   // [nx][ny][cz+1]
+#pragma unroll
+    for (int nx = 0; nx < 3; ++nx)
+#pragma unroll
+        for (int ny = 0; ny < 3; ++ny)
+#pragma unroll
+            for (int cz = -1; cz <= 1; ++cz)
+#pragma unroll
+                for (int nz = 0; nz < 3; ++nz) {
+                    if (!has3(nx, ny, nz) || hp(nz, cz) == 0.0) continue;
+                    P[nx][ny][cz + 1].add(hmul<R>(hp(nz, cz), a[nx][ny][nz]));
+                }
+    Acc<R> Q[3][3][3];   // [nx][cy+1][cz+1]
+#pragma unroll
+    for (int nx = 0; nx < 3; ++nx)
+#pragma unroll
+        for (int cy = -1; cy <= 1; ++cy)
+#pragma unroll
+            for (int cz = 0; cz < 3; ++cz)
+#pragma unroll
+                for (int ny = 0; ny < 3; ++ny) {
+                    if (P[nx][ny][cz].z || hp(ny, cy) == 0.0) continue;
+                    Q[nx][cy + 1][cz].add(hmul<R>(hp(ny, cy), P[nx][ny][cz].s));
+                }
+#pragma unroll
+    for (int cx = -1; cx <= 1; ++cx)
+#pragma unroll
+        for (int cy = 0; cy < 3; ++cy)
+#pragma unroll
+            for (int cz = 0; cz < 3; ++cz) {
+                Acc<R> s;
+#pragma unroll
+                for (int nx = 0; nx < 3; ++nx) {
+                    if (Q[nx][cy][cz].z || hp(nx, cx) == 0.0) continue;
+                    s.add(hmul<R>(hp(nx, cx), Q[nx][cy][cz].s));
+                }
+                g[cx + 1][cy][cz] = R(w1(cx) * w1(cy - 1) * w1(cz - 1)) * s.s;
+            }
+}
+
+// bare moments of 27 pulled populations: dr, m_a, Pi_ab = sum H2_ab g
+template <typename R>
+__device__ __forceinline__ void moments_of(const R (&g)[3][3][3], R& dr, R (&mm)[3], R (&pi)[6]) {
+    R X[3][3][3];        // [n][cy][cz] = sum_cx cx^n g
+#pragma unroll
+    for (int cy = 0; cy < 3; ++cy)
+#pragma unroll
+        for (int cz = 0; cz < 3; ++cz) {
+            const R s = g[2][cy][cz] + g[0][cy][cz];
+            X[0][cy][cz] = s + g[1][cy][cz];
+            X[1][cy][cz] = g[2][cy][cz] - g[0][cy][cz];
+            X[2][cy][cz] = s;
+        }
+    R Y[3][3][3];        // [nx][ny][cz], nx + ny <= 2
+#pragma unroll
+    for (int nx = 0; nx < 3; ++nx)
+#pragma unroll
+        for (int cz = 0; cz < 3; ++cz) {
+            const R s = X[nx][2][cz] + X[nx][0][cz];
+            Y[nx][0][cz] = s + X[nx][1][cz];
+            if (nx <= 1) Y[nx][1][cz] = X[nx][2][cz] - X[nx][0][cz];
+            if (nx == 0) Y[nx][2][cz] = s;
+        }
+    R M[3][3][3];        // [nx][ny][nz], |n| <= 2
+#pragma unroll
+    for (int nx = 0; nx < 3; ++nx)
+#pragma unroll
+        for (int ny = 0; ny < 3; ++ny) {
+            if (nx + ny > 2) continue;
+            const R s = Y[nx][ny][2] + Y[nx][ny][0];
+            M[nx][ny][0] = s + Y[nx][ny][1];
+            if (nx + ny <= 1) M[nx][ny][1] = Y[nx][ny][2] - Y[nx][ny][0];
+            if (nx + ny == 0) M[nx][ny][2] = s;
+        }
+    dr = M[0][0][0];
+    mm[0] = M[1][0][0];
+    mm[1] = M[0][1][0];
+    mm[2] = M[0][0][1];
+    const R third = dr * R(CS2);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        int n[3] = {0, 0, 0};
+        ++n[s_a<3>(k)];
+        ++n[s_b<3>(k)];
+        const R v = M[n[0]][n[1]][n[2]];
+        pi[k] = s_a<3>(k) == s_b<3>(k) ? v - third : v;
+    }
+}
+
+template <int A, int NA, int NU, int NV>
+MLBM_HD constexpr int pidx(int which) {   // multi-index of (nA along A, nU along U, nV along V)
+    constexpr int U = A == 0 ? 1 : 0, V = A == 2 ? 1 : 2;
+    return which == A ? NA : which == U ? NU : NV;
+}
+
+// face cell with normal axis A: 9 in-plane populations gf[cu+1][cv+1] for the
+// inward velocity cA = +-1 (runtime); U < V are the in-plane axes
+template <int A, typename R>
+__device__ __forceinline__ void face_eval(const R (&a)[3][3][3], R cA, R (&gf)[3][3]) {
+    constexpr int U = A == 0 ? 1 : 0, V = A == 2 ? 1 : 2;
+    Acc<R> b[3][3];      // [nu][nv]
+#pragma unroll
+    for (int nu = 0; nu < 3; ++nu)
+#pragma unroll
+        for (int nv = 0; nv < 3; ++nv)
+#pragma unroll
+            for (int na = 0; na < 3; ++na) {
+                int n[3];
+                n[A] = na; n[U] = nu; n[V] = nv;
+                if (!has3(n[0], n[1], n[2])) continue;
+                const R x = a[n[0]][n[1]][n[2]];
+                b[nu][nv].add(na == 0 ? x : (na == 1 ? cA * x : R(2.0 / 3.0) * x));
+            }
+    Acc<R> P[3][3];      // [nu][cv+1]
+#pragma unroll
+    for (int nu = 0; nu < 3; ++nu)
+#pragma unroll
+        for (int cv = -1; cv <= 1; ++cv)
+#pragma unroll
+            for (int nv = 0; nv < 3; ++nv) {
+                if (b[nu][nv].z || hp(nv, cv) == 0.0) continue;
+                P[nu][cv + 1].add(hmul<R>(hp(nv, cv), b[nu][nv].s));
+            }
+#pragma unroll
+    for (int cu = -1; cu <= 1; ++cu)
+#pragma unroll
+        for (int cv = 0; cv < 3; ++cv) {
+            Acc<R> s;
+#pragma unroll
+            for (int nu = 0; nu < 3; ++nu) {
+                if (P[nu][cv].z || hp(nu, cu) == 0.0) continue;
+                s.add(hmul<R>(hp(nu, cu), P[nu][cv].s));
+            }
+            gf[cu + 1][cv] = R(w1(1) * w1(cu) * w1(cv - 1)) * s.s;
+        }
+}
+
+// edge cell with free axis E: the 3 populations ge[cE+1] for inward velocities
+// cP, cQ = +-1 (runtime) on the two fixed axes P < Q
+template <int E, typename R>
+__device__ __forceinline__ void edge_eval(const R (&a)[3][3][3], R cP, R cQ, R (&ge)[3]) {
+    constexpr int P = E == 0 ? 1 : 0, Q = E == 2 ? 1 : 2;
+    const R hpq[3] = {R(1), cP, R(2.0 / 3.0)};
+    const R hqq[3] = {R(1), cQ, R(2.0 / 3.0)};
+    Acc<R> b[3];
+#pragma unroll
+    for (int ne = 0; ne < 3; ++ne)
+#pragma unroll
+        for (int np = 0; np < 3; ++np)
+#pragma unroll
+            for (int nq = 0; nq < 3; ++nq) {
+                int n[3];
+                n[E] = ne; n[P] = np; n[Q] = nq;
+                if (!has3(n[0], n[1], n[2])) continue;
+                R x = a[n[0]][n[1]][n[2]];
+                if (np) x *= hpq[np];
+                if (nq) x *= hqq[nq];
+                b[ne].add(x);
+            }
+#pragma unroll
+    for (int ce = -1; ce <= 1; ++ce) {
+        Acc<R> s;
+#pragma unroll
+        for (int ne = 0; ne < 3; ++ne) {
+            if (b[ne].z || hp(ne, ce) == 0.0) continue;
+            s.add(hmul<R>(hp(ne, ce), b[ne].s));
+        }
+        ge[ce + 1] = R(w1(1) * w1(1) * w1(ce)) * s.s;
+    }
+}
+
+template <typename R>
+__device__ __forceinline__ R corner_eval(const R (&a)[3][3][3], R cx, R cy, R cz) {
+    const R hx[3] = {R(1), cx, R(2.0 / 3.0)}, hy[3] = {R(1), cy, R(2.0 / 3.0)}, hz[3] = {R(1), cz, R(2.0 / 3.0)};
+    Acc<R> s;
+#pragma unroll
+    for (int nx = 0; nx < 3; ++nx)
+#pragma unroll
+        for (int ny = 0; ny < 3; ++ny)
+#pragma unroll
+            for (int nz = 0; nz < 3; ++nz) {
+                if (!has3(nx, ny, nz)) continue;
+                R x = a[nx][ny][nz];
+                if (nx) x *= hx[nx];
+                if (ny) x *= hy[ny];
+                if (nz) x *= hz[nz];
+                s.add(x);
+            }
+    return R(w1(1) * w1(1) * w1(1)) * s.s;
+}
+
+// direction index of a velocity with one runtime-signed component
+template <int A> MLBM_HD int dir_sel(bool neg, int cu, int cv) {
+    // component along A is -1 if neg else +1; cu, cv along the other two axes
+    constexpr int U = A == 0 ? 1 : 0, V = A == 2 ? 1 : 2;
+    int cp[3], cm[3];
+    cp[A] = 1; cm[A] = -1; cp[U] = cm[U] = cu; cp[V] = cm[V] = cv;
+    return neg ? dir3(cm[0], cm[1], cm[2]) : dir3(cp[0], cp[1], cp[2]);
+}
+
+// runtime-velocity direction index (unrolled compare over the 26 moving directions)
+MLBM_HD int dir_rt(int cx, int cy, int cz) {
+    int dir = 0;
+#pragma unroll
+    for (int i = 1; i < 27; ++i)
+        if (cvec<3>(i, 0) == cx && cvec<3>(i, 1) == cy && cvec<3>(i, 2) == cz) dir = i;
+    return dir;
+}
+
+template <int A, typename R>
+__device__ __forceinline__ void face_body(const FieldsT<R>& src, R* fb, const int* snb, int f, R h3xyz) {
+    constexpr int T = 64, U = A == 0 ? 1 : 0, V = A == 2 ? 1 : 2;
+    constexpr int SA = A == 0 ? 1 : A == 1 ? 4 : 16, SU = U == 0 ? 1 : 4, SV = V == 1 ? 4 : 16;
+    const int side = (f >> 4) & 1, u = f & 3, v = (f >> 2) & 3;
+    int o[3] = {0, 0, 0};
+    o[A] = side ? 1 : -1;
+    const int ns = snb[nb_index<3>(o[0], o[1], o[2])];
+    if (ns < 0) return;
+    const int srcl = (side ? 0 : 3) * SA + u * SU + v * SV;
+    R a[3][3][3];
+    load_tcoef<R>(src, (int64_t)ns * T + srcl, h3xyz, a);
+    R gf[3][3];
+    face_eval<A, R>(a, side ? R(-1) : R(1), gf);
+    const int base = (side ? 3 : 0) * SA;
+#pragma unroll
+    for (int cu = -1; cu <= 1; ++cu)
+#pragma unroll
+        for (int cv = -1; cv <= 1; ++cv) {
+            const int lu = u + cu, lv = v + cv;
+            if ((unsigned)lu > 3u || (unsigned)lv > 3u) continue;
+            fb[dir_sel<A>(side, cu, cv) * T + base + lu * SU + lv * SV] = gf[cu + 1][cv + 1];
+        }
+}
+
+template <int E, typename R>
+__device__ __forceinline__ void edge_body(const FieldsT<R>& src, R* fb, const int* snb, int e, R h3xyz) {
+    constexpr int T = 64, P = E == 0 ? 1 : 0, Q = E == 2 ? 1 : 2;
+    constexpr int SE = E == 0 ? 1 : E == 1 ? 4 : 16, SP = P == 0 ? 1 : 4, SQ = Q == 1 ? 4 : 16;
+    const int combo = (e >> 2) & 3, t = e & 3, sp = combo & 1, sq = combo >> 1;
+    int o[3];
+    o[E] = 0; o[P] = sp ? 1 : -1; o[Q] = sq ? 1 : -1;
+    const int ns = snb[nb_index<3>(o[0], o[1], o[2])];
+    if (ns < 0) return;
+    const int srcl = t * SE + (sp ? 0 : 3) * SP + (sq ? 0 : 3) * SQ;
+    R a[3][3][3];
+    load_tcoef<R>(src, (int64_t)ns * T + srcl, h3xyz, a);
+    const int cP = sp ? -1 : 1, cQ = sq ? -1 : 1;
+    R ge[3];
+    edge_eval<E, R>(a, R(cP), R(cQ), ge);
+    const int base = (sp ? 3 : 0) * SP + (sq ? 3 : 0) * SQ;
+#pragma unroll
+    for (int ce = -1; ce <= 1; ++ce) {
+        const int le = t + ce;
+        if ((unsigned)le > 3u) continue;
+        int c[3];
+        c[E] = ce; c[P] = cP; c[Q] = cQ;
+        fb[dir_rt(c[0], c[1], c[2]) * T + base + le * SE] = ge[ce + 1];
+    }
+}
+
+// own push + halo of one tile (all 64 threads of the tile group call it)
+template <typename R>
+__device__ __forceinline__ void stream_push(const FieldsT<R>& src, R* fb, const int* snb, int64_t cell,
+                                            int lc, bool valid, R h3xyz) {
+    constexpr int T = 64;
+    const int l[3] = {lc & 3, (lc >> 2) & 3, (lc >> 4) & 3};
+    if (valid) {
+        R a[3][3][3], g[3][3][3];
+        load_tcoef<R>(src, cell, h3xyz, a);
+        recon_all<R>(a, g);
+        bool okm[3], okp[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) { okm[q] = l[q] > 0; okp[q] = l[q] < 3; }
+#pragma unroll
+        for (int cx = -1; cx <= 1; ++cx)
+#pragma unroll
+            for (int cy = -1; cy <= 1; ++cy)
+#pragma unroll
+                for (int cz = -1; cz <= 1; ++cz) {
+                    const bool in = (cx < 0 ? okm[0] : cx > 0 ? okp[0] : true) &&
+                                    (cy < 0 ? okm[1] : cy > 0 ? okp[1] : true) &&
+                                    (cz < 0 ? okm[2] : cz > 0 ? okp[2] : true);
+                    if (in) fb[dir3(cx, cy, cz) * T + lc + cx + 4 * cy + 16 * cz] = g[cx + 1][cy + 1][cz + 1];
+                }
+        // ---- halo faces: 96 cells; warp-uniform normal axis per round
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int f = lc + 64 * r;
+            if (f >= 96) break;
+            const int A = f >> 5;
+            if (A == 0) face_body<0, R>(src, fb, snb, f, h3xyz);
+            else if (A == 1) face_body<1, R>(src, fb, snb, f, h3xyz);
+            else face_body<2, R>(src, fb, snb, f, h3xyz);
+        }
+        // ---- halo edges: 48 cells (free axis E, 4 sign combos, 4 positions)
+        if (lc < 48) {
+            const int E = lc >> 4;
+            if (E == 0) edge_body<0, R>(src, fb, snb, lc, h3xyz);
+            else if (E == 1) edge_body<1, R>(src, fb, snb, lc, h3xyz);
+            else edge_body<2, R>(src, fb, snb, lc, h3xyz);
+        } else if (lc < 56) {
+            // ---- halo corners: 8 cells, one population each
+            const int k = lc - 48, sx = k & 1, sy = (k >> 1) & 1, sz = k >> 2;
+            const int ns = snb[nb_index<3>(sx ? 1 : -1, sy ? 1 : -1, sz ? 1 : -1)];
+            if (ns >= 0) {
+                load_tcoef<R>(src, (int64_t)ns * T + (sx ? 0 : 3) + 4 * (sy ? 0 : 3) + 16 * (sz ? 0 : 3),
+                              h3xyz, a);
+                const int cx = sx ? -1 : 1, cy = sy ? -1 : 1, cz = sz ? -1 : 1;
+                const R gc = corner_eval<R>(a, R(cx), R(cy), R(cz));
+                const int dir = dir_rt(cx, cy, cz);
+                fb[dir * T + (sx ? 3 : 0) + 4 * (sy ? 3 : 0) + 16 * (sz ? 3 : 0)] = gc;
+            }
+        }
+    }
+}
+
+// pull the 27 incoming populations of a cell and form the bare moments;
+// special cells replace bounce-back / self-source directions by their own
+template <typename R>
+__device__ __forceinline__ void stream_pull(const FieldsT<R>& src, const R* fb, int64_t cell, int lc,
+                                            bool special, uint64_t mask, R h3xyz, R& dr, R (&mm)[3],
+                                            R (&pi)[6]) {
+    constexpr int T = 64;
+    R g[3][3][3];
+#pragma unroll
+    for (int cx = -1; cx <= 1; ++cx)
+#pragma unroll
+        for (int cy = -1; cy <= 1; ++cy)
+#pragma unroll
+            for (int cz = -1; cz <= 1; ++cz) g[cx + 1][cy + 1][cz + 1] = fb[dir3(cx, cy, cz) * T + lc];
+    if (special) {
+        R a[3][3][3], own[3][3][3];
+        load_tcoef<R>(src, cell, h3xyz, a);
+        recon_all<R>(a, own);
+#pragma unroll
+        for (int cx = -1; cx <= 1; ++cx)
+#pragma unroll
+            for (int cy = -1; cy <= 1; ++cy)
+#pragma unroll
+                for (int cz = -1; cz <= 1; ++cz) {
+                    constexpr int dummy = 0; (void)dummy;
+                    const int I = dir3(cx, cy, cz);
+                    if ((mask >> I) & 1ull) g[cx + 1][cy + 1][cz + 1] = own[1 - cx][1 - cy][1 - cz];
+                    else if ((mask >> (32 + I)) & 1ull) g[cx + 1][cy + 1][cz + 1] = own[cx + 1][cy + 1][cz + 1];
+                }
+    }
+    moments_of<R>(g, dr, mm, pi);
+}
+
+}  // namespace tp
+
 // mode 0 fused, 1 stream only, 2 collide+bc only
 template <int D, typename R> struct LevelCfg {
     static constexpr int TPC = D == 2 ? 8 : (sizeof(R) == 4 ? 2 : 1);   // tiles per CTA
@@ -354,7 +773,9 @@ __global__ void __launch_bounds__(LevelCfg<D, R>::THREADS) level_kernel(const St
     constexpr int TPC = LevelCfg<D, R>::TPC;
     constexpr int HB = HaloTable<D>::HB, NCO = CoefSlots<D>::N;
     __shared__ R fbuf_all[TPC][Q * T];
-    __shared__ R hcoef_all[MODE == 2 || MODE == 3 || MODE == 4 ? 1 : TPC][MODE == 2 || MODE == 3 || MODE == 4 ? 1 : NCO * HB];
+    // halo coefficient staging: 2D only (3D evaluates its halo in registers)
+    constexpr bool HC = !(MODE == 2 || MODE == 3 || MODE == 4) && D == 2;
+    __shared__ R hcoef_all[HC ? TPC : 1][HC ? NCO * HB : 1];
     __shared__ int snb_all[TPC][Geo<D>::NB];
 
     const int grp = threadIdx.x / T, lc = threadIdx.x % T;
@@ -382,7 +803,37 @@ __global__ void __launch_bounds__(LevelCfg<D, R>::THREADS) level_kernel(const St
     const bool active = cf & MLBM_CF_ACTIVE;
 
     R dr, mm[D], pi[NS];
-    if constexpr (MODE != 2) {
+    if constexpr (MODE != 2 && D == 3) {
+        tp::stream_push<R>(src, fb, snb, cell, lc, valid, h3xyz);
+        __syncthreads();
+        dr = R(0);
+#pragma unroll
+        for (int a = 0; a < D; ++a) mm[a] = R(0);
+#pragma unroll
+        for (int k = 0; k < NS; ++k) pi[k] = R(0);
+        if (valid) {
+            const bool special = cf & MLBM_CF_SPECIAL;
+            R mm3[3], pi6[6];
+            tp::stream_pull<R>(src, fb, cell, lc, special, special ? A.lv.dir_masks[cell] : 0ull, h3xyz,
+                               dr, mm3, pi6);
+#pragma unroll
+            for (int a = 0; a < D; ++a) mm[a] = mm3[a];
+#pragma unroll
+            for (int k = 0; k < NS; ++k) pi[k] = pi6[k];
+        }
+        if constexpr (MODE == 1) {
+            if (valid) {
+                dst.at(0, cell) = dr;
+#pragma unroll
+                for (int a = 0; a < D; ++a) dst.at(1 + a, cell) = mm[a];
+#pragma unroll
+                for (int k = 0; k < NS; ++k) dst.at(1 + D + k, cell) = pi[k];
+                dst.at(fi_eps<D>(), cell) = src.at(fi_eps<D>(), cell);
+                dst.at(fi_phi<D>(), cell) = src.at(fi_phi<D>(), cell);
+            }
+            return;
+        }
+    } else if constexpr (MODE != 2) {
         Coef<D, R> own;
         if (valid) {
             R m[NM];
