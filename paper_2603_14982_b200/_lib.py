@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIBPATH = os.environ.get("MLBM_LIB") or os.path.join(HERE, "libmlbm_b200.so")
-SOURCES = ["lbm.cu", "topology.cu", "mpm.cu", "adapt.cu"]
+SOURCES = ["lbm.cu", "topology.cu", "mpm.cu", "adapt.cu", "adapt_bits.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
               "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-Wno-deprecated-declarations",

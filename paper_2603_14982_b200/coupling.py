@@ -24,6 +24,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 import torch
 
@@ -176,6 +178,7 @@ class CoupledSim:
         self.sort_particles = True
         self.sort_every = 4        # particles move < 1 cell/step: re-sort every few steps
         self._sort_now = True
+        self.overlap_diag = os.environ.get("MLBM_OVERLAP_DIAG", "1") != "0"
         self.p2g_mode = 4          # sorted input: 1 block smem, 2 warp registers, 3 cell lanes,
                                    # 4 cell lanes + per-warp box copies (fp32; fp64 runs mode 3)
         self._graphs = {}
@@ -312,11 +315,32 @@ class CoupledSim:
             solver.check_errors = check
         if self.powder is not None:
             self._powder_cycle(is_mpm)
-        if adapt_now:
+        if adapt_now and self.overlap_diag:
+            # the diagnostics reductions read only fields and particles: they
+            # run on a side stream concurrently with the latency-bound adapt
+            # pass (both captured into the same graph, joined before the copy)
+            main = torch.cuda.current_stream()
+            side = self._side_stream()
+            fork = torch.cuda.Event()
+            fork.record(main)
+            side.wait_event(fork)
+            with torch.cuda.stream(side):
+                self._record_diagnostics()
             self.adaptor.plan_device(self._driver())
-        self._record_diagnostics()
+            join = torch.cuda.Event()
+            join.record(side)
+            main.wait_event(join)
+        else:
+            if adapt_now:
+                self.adaptor.plan_device(self._driver())
+            self._record_diagnostics()
         self._host_i32.copy_(self._sblock, non_blocking=True)
         self._host_f64.copy_(self._diag_buf, non_blocking=True)
+
+    def _side_stream(self):
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.topology.device)
+        return self._side
 
     def _ensure_host_status(self, adapt_now=None):
         if getattr(self, "_host_i32", None) is None:
@@ -331,7 +355,8 @@ class CoupledSim:
             self._graphs.clear()
             self._pool = None          # graphs of the old capacities freed with their pool
             self._graph_ver = gver
-        # persistent buffers are allocated outside any capture
+        # persistent buffers (and the side stream) are created outside any capture
+        self._side_stream()
         if self.sort_particles and len(self.particles):
             self.particles.scratch()
         if self.powder is not None:

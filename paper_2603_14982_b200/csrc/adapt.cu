@@ -603,6 +603,10 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
 using namespace mlbm;
 
 extern "C" unsigned long long* mlbm_adapt_timestamps_ptr();
+int mlbm_adapt_bits_launch(const mlbm_hier_t* h, uint8_t* const* nkind, int16_t* const* streak,
+                           uint8_t* seeds, const uint8_t* static_tiles, const double* x, int64_t xs,
+                           int32_t n, int32_t* status, mlbm_error_t* err, int64_t seeds_bytes,
+                           void* stream);
 
 static unsigned long long* g_ts_last = nullptr;
 extern "C" unsigned long long* mlbm_adapt_timestamps_ptr() { return g_ts_last; }
@@ -614,6 +618,18 @@ extern "C" int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_
                                const uint8_t* static_tiles, const double* x, int64_t xs, int32_t n,
                                int32_t* status, mlbm_error_t* err, unsigned int* bar, void* stream) {
     static unsigned long long* ts_env = nullptr;
+    // MLBM_ADAPT_PATH=bits selects the bit-packed single-CTA pass
+    // (adapt_bits.cu) when the hierarchy's bitmaps fit in shared memory.  It
+    // is bit-exact but slower on B200 (one SM against 148: 74 us vs 52 us on
+    // C2), so the cooperative byte pass is the default.
+    const char* path = getenv("MLBM_ADAPT_PATH");
+    if (path && path[0] == 'b') {
+        int64_t n0 = 1;
+        for (int a = 0; a < h->dim; ++a) n0 *= h->finest[a] / 4;
+        const int r = mlbm_adapt_bits_launch(h, nkind, streak, seeds, static_tiles, x, xs, n, status, err,
+                                             n0, stream);
+        if (r != 0) return r;
+    }
     AdaptArgs A;
     A.dim = h->dim;
     A.levels = h->levels;

@@ -804,6 +804,10 @@ __global__ void __launch_bounds__(LevelCfg<D, R>::THREADS) level_kernel(const St
 
     R dr, mm[D], pi[NS];
     if constexpr (MODE != 2 && D == 3) {
+        // eps / phi ride along to the write tree: fetch them now so the
+        // loads overlap the stream instead of stalling the epilogue
+        R eps_c = R(0), phi_c = R(0);
+        if (MODE == 1 && valid) { eps_c = src.at(fi_eps<D>(), cell); phi_c = src.at(fi_phi<D>(), cell); }
         tp::stream_push<R>(src, fb, snb, cell, lc, valid, h3xyz);
         __syncthreads();
         dr = R(0);
@@ -828,8 +832,8 @@ __global__ void __launch_bounds__(LevelCfg<D, R>::THREADS) level_kernel(const St
                 for (int a = 0; a < D; ++a) dst.at(1 + a, cell) = mm[a];
 #pragma unroll
                 for (int k = 0; k < NS; ++k) dst.at(1 + D + k, cell) = pi[k];
-                dst.at(fi_eps<D>(), cell) = src.at(fi_eps<D>(), cell);
-                dst.at(fi_phi<D>(), cell) = src.at(fi_phi<D>(), cell);
+                dst.at(fi_eps<D>(), cell) = eps_c;
+                dst.at(fi_phi<D>(), cell) = phi_c;
             }
             return;
         }

@@ -26,9 +26,12 @@ def tiles_of(topo):
     return np.array(sorted(topo.tile_set()), dtype=np.int64).reshape(-1, 2 + topo.d)
 
 
-@pytest.mark.parametrize("fused", [True, False])
-def test_adapt_walk_matches_reference_golden(fused):
+@pytest.mark.parametrize("fused,path", [(True, "bits"), (True, "coop"), (False, "ops")])
+def test_adapt_walk_matches_reference_golden(fused, path, monkeypatch):
+    """fused: the one-launch pass, byte cooperative grid (coop, default) or
+    bit-packed single CTA (bits, opt-in); unfused: one launch per bitmap op."""
     _need_gpu()
+    monkeypatch.setenv("MLBM_ADAPT_PATH", path)
     g = np.load(os.path.join(GOLD, "adapt_walk.npz"))
     topo = B.Topology.uniform((64, 64), 3)
     pair = B.PingPongPair(topo)
@@ -44,8 +47,10 @@ def test_adapt_walk_matches_reference_golden(fused):
         assert rep.violations == []
 
 
-def test_adapt_3d_random_walk_vs_oracle():
+@pytest.mark.parametrize("path", ["bits", "coop"])
+def test_adapt_3d_random_walk_vs_oracle(path, monkeypatch):
     _need_gpu()
+    monkeypatch.setenv("MLBM_ADAPT_PATH", path)
     rng = np.random.default_rng(11)
     cells, levels = (64, 32, 32), 3
     otopo = OG.Topology.uniform(cells, levels)
@@ -97,13 +102,15 @@ def test_particle_outside_domain_raises():
         ad.update(B.RefineDriver(positions=np.array([[70.0, 3.0]]), levels=3), pair)
 
 
+@pytest.mark.parametrize("path", ["bits", "coop"])
 @pytest.mark.parametrize("dim", [2, 3])
-def test_invariant_violations_reported_fused_and_unfused(dim):
+def test_invariant_violations_reported_fused_and_unfused(dim, path, monkeypatch):
     """A tile set with a leaf whose ring is incomplete and a finest tile
     covered twice: the fused pass and the per-op pass report the same
     coverage / ring / particle counts (adapt.py:374-389, reported not
     raised), and a consistent tile set reports none."""
     _need_gpu()
+    monkeypatch.setenv("MLBM_ADAPT_PATH", path)
     cells = (64, 64) if dim == 2 else (32, 32, 32)
     topo = B.Topology.uniform(cells, 2)
     pair = B.PingPongPair(topo)

@@ -41,3 +41,18 @@ if os.environ.get("MLBM_ADAPT_TIMESTAMPS"):
             print("  %-22s %6.2f us" % (names[i], (ts[i] - prev) / 1e3))
             prev = ts[i]
     print("  total                  %6.2f us" % ((prev - ts[0]) / 1e3))
+if os.environ.get("MLBM_ADAPT_TIMESTAMPS"):
+    lib.mlbm_adapt_bits_ts_ptr.restype = ctypes.c_void_p
+    ptr = lib.mlbm_adapt_bits_ts_ptr()
+    if ptr:
+        ad.plan_device(drv); torch.cuda.synchronize()
+        buf = (ctypes.c_uint64 * 64)()
+        cudart.cudaMemcpy(buf, ctypes.c_void_p(ptr), ctypes.c_size_t(64 * 8), 2)
+        ts = [v for v in list(buf)[:40]]
+        last = ts[0]
+        out = []
+        for k in range(1, 40):
+            if ts[k]:
+                out.append(round((ts[k] - last) / 1e3, 2))
+                last = ts[k]
+        print("bits phase deltas us:", out, "total", round((last - ts[0]) / 1e3, 2))
