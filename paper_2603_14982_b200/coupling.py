@@ -178,6 +178,7 @@ class CoupledSim:
         self.sort_particles = True
         self.sort_every = 4        # particles move < 1 cell/step: re-sort every few steps
         self._sort_now = True
+        self._use_sorted = self._sort_ahead = self._sorted_ahead = False
         self.overlap_diag = os.environ.get("MLBM_OVERLAP_DIAG", "1") != "0"
         self.p2g_mode = 4          # sorted input: 1 block smem, 2 warp registers, 3 cell lanes,
                                    # 4 cell lanes + per-warp box copies (fp32; fp64 runs mode 3)
@@ -218,11 +219,10 @@ class CoupledSim:
         grid.clear()
         n = len(p)
         ps = p.pd.stride(0)
-        if self.sort_particles and n and self._sort_now:
+        if self.sort_particles and n and (self._sort_now or self._use_sorted):
             xa, pa, ida, ws = p.scratch()
-            L.check(lib.mlbm_particle_sort(L.C.byref(lv0), n, L.ptr(p.xd), L.ptr(p.pd),
-                                           L.ptr(p.pid), ps, L.ptr(xa), L.ptr(pa), L.ptr(ida),
-                                           dcode, L.ptr(ws), ws.numel(), s), "particle_sort")
+            if not self._use_sorted:          # else sorted at the end of the last step
+                self._sort_into_scratch()
             src_x, src_p, src_id, smem = xa, pa, ida, self.p2g_mode
             p.permuted = True
         else:
@@ -251,6 +251,18 @@ class CoupledSim:
         self.last_fields = CouplingFields(grid, self.pair.trees[0].levels[0])
         return FIELD_FORCE, FIELD_TAU
 
+    def _sort_into_scratch(self):
+        """Radix sort of the particle rows by (level-0 tile slot, cell) into
+        the scratch buffers (no reference counterpart; ordering only)."""
+        p = self.particles
+        xa, pa, ida, ws = p.scratch()
+        lv0 = self.grid.level0()
+        L.check(L.lib().mlbm_particle_sort(L.C.byref(lv0), len(p), L.ptr(p.xd), L.ptr(p.pd),
+                                           L.ptr(p.pid), p.pd.stride(0), L.ptr(xa), L.ptr(pa),
+                                           L.ptr(ida), dtype_code(self.dtype), L.ptr(ws),
+                                           ws.numel(), L.stream_handle()), "particle_sort")
+        self.solver.launches += 1
+
     @staticmethod
     def _held(solver):
         return FIELD_FORCE, FIELD_TAU
@@ -273,6 +285,8 @@ class CoupledSim:
     def _step_eager(self, ci, is_mpm, adapt_now):
         solver = self.solver
         self._sort_now = (self.step_count % self.sort_every) == 0
+        self._use_sorted = False
+        self._sort_ahead = self._sorted_ahead = False
         cycle = solver._schedule[ci]
         if is_mpm:
             solver.run_cycle(cycle, hook=self._exchange)
@@ -326,6 +340,8 @@ class CoupledSim:
             side.wait_event(fork)
             with torch.cuda.stream(side):
                 self._record_diagnostics()
+                if self._sort_ahead:
+                    self._sort_into_scratch()
             self.adaptor.plan_device(self._driver())
             join = torch.cuda.Event()
             join.record(side)
@@ -366,8 +382,17 @@ class CoupledSim:
         self.grid.sync_topology()
         self.grid.level0()
         self._ensure_host_status(adapt_now)
-        self._sort_now = (self.step_count % self.sort_every) == 0
+        # particle sort: every sort_every steps; with the diagnostics overlap it
+        # runs at the end of the previous step beside the adapt pass (it only
+        # reads the particle rows the pass reads) and this step's P2G takes the
+        # sorted scratch as is
+        self._use_sorted = self._sorted_ahead
+        self._sort_now = (self.step_count % self.sort_every) == 0 and not self._use_sorted
+        self._sort_ahead = bool(self.overlap_diag and adapt_now and is_mpm and self.cadence == 1
+                                and self.sort_particles and len(self.particles)
+                                and (self.step_count + 1) % self.sort_every == 0)
         key = (ci, tuple(k & 1 for k in solver.k), is_mpm, adapt_now, self._sort_now,
+               self._use_sorted, self._sort_ahead,
                self.powder is not None and is_mpm and self.last_fields is not None)
         entry = self._graphs.get(key)
         if entry is None:
@@ -395,6 +420,7 @@ class CoupledSim:
             self.graph_captures += 1
         g, dk, db, lf, nk = entry
         g.replay()
+        self._sorted_ahead = self._sort_ahead
         L.TRACE.launches += nk
         self.graph_replays += 1
         for l, v in enumerate(dk):
