@@ -518,21 +518,85 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
     constexpr int K = Geo<D>::K;
     using RW = Rows<D>;
     using PR = PRows<D>;
+    constexpr int MAXB = sizeof(R) == 4 ? 512 : 256;
+    // grid velocities of the block's node box staged in shared memory (sorted
+    // particles: the 128 particles of a block span a few cells); absent nodes
+    // hold NaN so a particle touching one reports the stencil error
+    __shared__ R svel[D][MAXB];
+    __shared__ int s_lo[3], s_hi[3];
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= P.n) return;
+    const bool live = p < P.n;
     const R* pp = (const R*)P.p;
     R* pw = (R*)P.pw;
     double x[D];
 #pragma unroll
-    for (int a = 0; a < D; ++a) x[a] = P.x[a * P.ps + p];
+    for (int a = 0; a < D; ++a) x[a] = live ? P.x[a * P.ps + p] : 0.5 * t0.cells[a];
     Stencil<D, R> st;
     make_stencil<D, R>(x, st);
+    if (threadIdx.x < 3) { s_lo[threadIdx.x] = 0x7fffffff; s_hi[threadIdx.x] = -0x7fffffff; }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const int l2 = __reduce_min_sync(0xffffffffu, live ? st.base[a] : 0x7fffffff);
+        const int h2 = __reduce_max_sync(0xffffffffu, live ? st.base[a] + 2 : -0x7fffffff);
+        if ((threadIdx.x & 31) == 0 && l2 <= h2) { atomicMin(&s_lo[a], l2); atomicMax(&s_hi[a], h2); }
+    }
+    __syncthreads();
+    int blo[3] = {0, 0, 0}, bext[3] = {1, 1, 1}, nbox = 1;
+#pragma unroll
+    for (int a = 0; a < D; ++a) { blo[a] = s_lo[a]; bext[a] = s_hi[a] - s_lo[a] + 1; nbox *= bext[a]; }
+    const bool use_box = nbox > 0 && nbox <= MAXB;      // block-uniform
+    if (use_box) {
+        for (int i = threadIdx.x; i < nbox; i += blockDim.x) {
+            int c[3] = {0, 0, 0}, r = i;
+#pragma unroll
+            for (int a = 0; a < D; ++a) { c[a] = blo[a] + r % bext[a]; r /= bext[a]; }
+            bool nb = false;
+            const int64_t ni = node_index<D>(t0, c, nb);
+#pragma unroll
+            for (int a = 0; a < D; ++a) svel[a][i] = ni >= 0 ? ras[(RW::VEL + a) * rs + ni] : R(NAN);
+        }
+    }
+    __syncthreads();
+    if (!live) return;
     R v[D], B[D * D];
 #pragma unroll
     for (int a = 0; a < D; ++a) v[a] = R(0);
 #pragma unroll
     for (int k = 0; k < D * D; ++k) B[k] = R(0);
     bool bad = false;
+    if (use_box) {
+        R dp[D][3];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int o = 0; o < 3; ++o) dp[a][o] = R(o) - st.frac[a];
+        int pb = 0, oy[3] = {0, 0, 0}, oz[3] = {0, 0, 0};
+        {
+            int m = 1;
+#pragma unroll
+            for (int a = 0; a < D; ++a) { pb += (st.base[a] - blo[a]) * m; m *= bext[a]; }
+#pragma unroll
+            for (int o = 0; o < 3; ++o) { oy[o] = o * bext[0]; oz[o] = D == 3 ? o * bext[0] * bext[1] : 0; }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int o[3] = {k % 3, (k / 3) % 3, D == 3 ? k / 9 : 0};
+            const int bi = pb + o[0] + oy[o[1]] + oz[o[2]];
+            R w = st.w[0][o[0]];
+#pragma unroll
+            for (int a = 1; a < D; ++a) w *= st.w[a][o[a]];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const R wg = w * svel[a][bi];
+                v[a] += wg;
+#pragma unroll
+                for (int b = 0; b < D; ++b) B[a * D + b] += wg * dp[b][o[b]];
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a) bad |= isnan((double)v[a]);
+    } else {
     // per-axis node coordinates of the 3^D stencil: tile coordinate (-1 when
     // outside a non-periodic box) and in-tile offset; the 27 tile-map reads
     // hit L1 (at most 2^D distinct tiles)
@@ -572,6 +636,7 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
 #pragma unroll
             for (int b = 0; b < D; ++b) B[a * D + b] += wg * dp[b][o[b]];
         }
+    }
     }
     if (bad) report_error(err, MLBM_ERR_STENCIL, 0, st.base[0], st.base[1], st.base[2]);
     R C[D * D];

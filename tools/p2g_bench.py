@@ -40,3 +40,21 @@ for m, r in out.items():
     scale = ref.abs().amax(dim=1, keepdim=True).clamp_min(1e-30)
     print("mode %d vs %d: max rel-to-row-max diff %.3e" % (m, min(out), ((r - ref).abs() / scale).max().item()))
 print("error record", grid._err.cpu().numpy()[:4])
+
+# ---- G2P on the same sorted state (grid velocity rows from the last exchange)
+xo, po, ido = torch.empty_like(xa), torch.empty_like(pa), torch.empty_like(ida)
+cnt = torch.zeros(2, dtype=torch.int32, device="cuda")
+for plastic in (1, 0):
+    ts = []
+    for rep in range(30):
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        L.check(lib.mlbm_g2p(L.C.byref(lv0), n, L.ptr(xa), L.ptr(xo), L.ptr(pa), L.ptr(po), L.ptr(ida),
+                             L.ptr(ido), ps, mat.lam, mat.mu, mat.alpha, L.ptr(grid.ras),
+                             grid.ras.stride(0), float(sim.cadence), plastic, 0, L.ptr(cnt),
+                             L.ptr(grid._err), s), "g2p")
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    ts.sort()
+    print("g2p plastic=%d: median %.1f us" % (plastic, ts[len(ts) // 2]))
