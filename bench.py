@@ -333,6 +333,120 @@ def run_mine(args, rank, world, local_rank):
         print(json.dumps(out), flush=True)
 
 
+def run_slab(args, rank, world, local_rank):
+    """C1 (configs[0]) as a slab-decomposed single-level run: rank r owns a
+    64^3 slab of a (64 N) x 64 x 64 periodic Taylor-Green domain (weak
+    scaling); after every level step the owned edge tile columns go to the
+    neighbours' ghost columns by NCCL point-to-point (slab_lbm.py)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2603_14982_b200 import _lib as L
+    from paper_2603_14982_b200.harness.config import taylor_green_fn
+    from paper_2603_14982_b200.slab_lbm import SlabLBM
+    from paper_2603_14982_b200.solver import LevelParams
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    n = 64
+    cells = (n * world, n, n)
+    tau0 = 0.8
+    lp = LevelParams(1, tau0)
+    sim = SlabLBM(cells, rank, world, tau0, dtype=torch.float32,
+                  init=taylor_green_fn(0.05, n, lp.nu(0), lp.taus, 3), device=dev)
+    owned = sim.n_owned * 64
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        sim.step()
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    clocks = Clocks(local_rank)
+    launches0 = L.TRACE.launches
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev, kev = [], []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        w = sim.step_local()
+        e1.record()
+        sim.exchange(w)
+        e2.record()
+        ev.append((e0, e2))
+        kev.append((e0, e1))
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = L.TRACE.launches - launches0
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    k_ms = sum(a.elapsed_time(b) for a, b in kev)
+    t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    eff = world * n ** 3
+    value = eff * args.steps / (t_ms * 1e-3) / 1e6
+    # e2e: the moment state uploaded from pinned host memory and read back every step
+    trees = sim.pair.trees
+    host = [torch.empty_like(tr.levels[0].data, device="cpu").pin_memory() for tr in trees]
+    for h, tr in zip(host, trees):
+        h.copy_(tr.levels[0].data)
+    torch.cuda.synchronize()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    nb = 0
+    for _ in range(args.steps):
+        r, _w = sim.solver.roles(0)
+        trees[r].levels[0].data.copy_(host[r], non_blocking=True)
+        w = sim.step_local()
+        sim.exchange(w)
+        host[w].copy_(trees[w].levels[0].data, non_blocking=True)
+        nb = trees[w].levels[0].data.numel() * trees[w].levels[0].data.element_size()
+    e1.record()
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    te = float(te.item())
+    peak, peak_kind = measured_peak()
+    kbytes = owned * 2 * 10 * 4
+    ach = kbytes * args.steps / (k_ms * 1e-3) / 1e9
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.scene)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(t_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C1 slabs: single-level periodic Taylor-Green, D3Q27, a 64^3 "
+                                   "slab per GPU of a (64 N) x 64 x 64 domain, ghost tile columns "
+                                   "exchanged by NCCL P2P every step",
+                       "effective_cells": eff, "parallelism": f"slabs{world}",
+                       "l2": "flushed (256 MB write) between timed steps, outside the events"},
+            "e2e": {"value": round(eff * args.steps / (te * 1e-3) / 1e6, 3), "unit": UNIT,
+                    "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb,
+                    "path": "moment tree uploaded from / read back to pinned host memory every "
+                            "step around SlabLBM.step"},
+            "gpu_launches": launches,
+            "roofline": {"kernel": "level_kernel mode 0 (owned tiles)", "bound": "hbm",
+                         "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(ach / peak, 4), "peak_source": peak_kind,
+                         "bytes_per_launch": kbytes, "traffic": None,
+                         "avg_launch_us": round(1e3 * k_ms / args.steps, 2)},
+            "exchange_ms_per_step": round((t_ms - k_ms) / args.steps, 4),
+            "cpu_baseline": cpu, "clocks": clk}), flush=True)
+
+
 def oracle_sample(scene):
     """Bounded CPU sample of the same workload: the fp64 NumPy oracle port."""
     from oracle import scene as OS
@@ -400,7 +514,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_mine(args, rank, world, local_rank)
+        if args.scene == "c1":
+            run_slab(args, rank, world, local_rank)
+        else:
+            run_mine(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

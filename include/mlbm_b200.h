@@ -77,6 +77,9 @@ typedef struct {
                                  * n_tiles is exact).  With counts, n_tiles is the
                                  * allocated capacity and sizes the launch grids, so a
                                  * captured CUDA graph survives topology changes. */
+    int32_t first;              /* first slot the level step / diagnostics process
+                                 * (slots [first, live)); 0 except for slab ranks, whose
+                                 * x-sorted slots start with a ghost tile column */
 } mlbm_level_t;
 
 typedef struct {

@@ -76,7 +76,7 @@ class Level(C.Structure):
                 ("tile_map", C.c_void_p), ("tile_xyz", C.c_void_p),
                 ("nbr", C.c_void_p), ("cell_flags", C.c_void_p),
                 ("dir_masks", C.c_void_p), ("tile_flags", C.c_void_p),
-                ("counts", C.c_void_p)]
+                ("counts", C.c_void_p), ("first", C.c_int32)]
 
 
 class Fields(C.Structure):

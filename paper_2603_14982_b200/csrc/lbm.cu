@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(LevelCfg<D, R>::THREADS) level_kernel(const St
 
     const int grp = threadIdx.x / T, lc = threadIdx.x % T;
     (void)hcoef_all;
-    const int tile = blockIdx.x * TPC + grp;
+    const int tile = A.lv.first + blockIdx.x * TPC + grp;
     const bool valid = tile < live_tiles(A.lv);
     R* fb = fbuf_all[grp];
     int* snb = snb_all[grp];
@@ -999,7 +999,7 @@ __global__ void __launch_bounds__(LevelCfg<D, R>::THREADS) level_kernel(const St
 template <int D, typename R>
 int launch_level(const StepArgs& a, int mode, cudaStream_t s) {
     constexpr int TPC = LevelCfg<D, R>::TPC, NT = LevelCfg<D, R>::THREADS;
-    const int blocks = (a.lv.n_tiles + TPC - 1) / TPC;
+    const int blocks = (a.lv.n_tiles - a.lv.first + TPC - 1) / TPC;
     if (blocks == 0) return 0;
     switch (mode) {
     case 0: level_kernel<D, R, 0><<<blocks, NT, 0, s>>>(a); break;

@@ -944,7 +944,7 @@ __global__ void k_diag_level(mlbm_level_t lv, mlbm_fields_t f, double vol, doubl
     double emin = 1e300;
     const FieldsT<R> a = fields_of<R>(f);
     const int64_t n = (int64_t)live_tiles(lv) * T;
-    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
+    for (int64_t c = (int64_t)lv.first * T + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
          c += (int64_t)gridDim.x * blockDim.x) {
         if (!(lv.cell_flags[c] & MLBM_CF_LEAF)) continue;
         const double rho = 1.0 + (double)a.at(0, c);

@@ -58,24 +58,24 @@ def random_fields(d, shape, seed):
     return f
 
 
-def _worker(rank, port, case, q):
+def _worker(rank, port, case, q, world=WORLD):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         q.put((rank, case(rank)))
     finally:
         dist.destroy_process_group()
 
 
-def run_world(case):
+def run_world(case, world=WORLD):
     port = free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, port, case, q)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, case, q, world)) for r in range(world)]
     for p in procs:
         p.start()
-    out = dict(q.get(timeout=120) for _ in range(WORLD))
+    out = dict(q.get(timeout=120) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -151,6 +151,20 @@ def case_seeds(rank):
     return PS.allreduce_seeds(seeds).numpy()
 
 
+def case_slab_columns(rank):
+    """exchange_columns with 3 ranks, periodic: every rank's ghost columns
+    receive its neighbours' edge columns (the device path's exact calls)."""
+    from paper_2603_14982_b200.slab_lbm import exchange_columns
+    world = dist.get_world_size()
+    cols = torch.arange(4 * 6, dtype=torch.float64).reshape(4, 6) + 100 * rank
+    lo, hi = cols[:, :3], cols[:, 3:]
+    gl, gr = torch.zeros(4, 3, dtype=torch.float64), torch.zeros(4, 3, dtype=torch.float64)
+    send = [torch.empty(4, 3, dtype=torch.float64) for _ in range(2)]
+    recv = [torch.empty(4, 3, dtype=torch.float64) for _ in range(2)]
+    exchange_columns(lo, hi, gl, gr, (rank - 1) % world, (rank + 1) % world, send, recv)
+    return gl.numpy(), gr.numpy()
+
+
 # -- tests --------------------------------------------------------------------------
 
 def test_partition_arithmetic():
@@ -214,3 +228,14 @@ def test_seed_or_allreduce():
     want[10] = 1
     for r in range(WORLD):
         assert np.array_equal(out[r], want)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_column_exchange(world):
+    out = run_world(case_slab_columns, world)
+    for r in range(world):
+        gl, gr = out[r]
+        lft, rgt = (r - 1) % world, (r + 1) % world
+        base = np.arange(24, dtype=float).reshape(4, 6)
+        assert np.array_equal(gl, (base + 100 * lft)[:, 3:]), r      # left neighbour's high edge
+        assert np.array_equal(gr, (base + 100 * rgt)[:, :3]), r      # right neighbour's low edge
