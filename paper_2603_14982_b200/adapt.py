@@ -287,11 +287,16 @@ class GridAdaptor:
             for l in changed:
                 rep.created[l] = fresh[l]
                 rep.deleted[l] = topo.n_tiles(l) - (new_counts[l] - fresh[l])
-            dev = self._prepare(changed, pair, new_counts, fresh)
             if device_runner is None:
-                dev()
+                self._prepare(changed, pair, new_counts, fresh)()
             else:
-                device_runner(dev, (tuple(changed), tuple(bool(fresh[l]) for l in changed)))
+                # graph path: rebuild every non-empty level with the init kernel on,
+                # so the rebuild graph's key is only the level set (unchanged levels
+                # compact to the same map and migrate as an identity copy; init
+                # finds no fresh tile) and it is captured once, not per pattern
+                levels = [l for l in range(Lv) if new_counts[l] or topo.n_tiles(l)]
+                dev = self._prepare(levels, pair, new_counts, [1] * Lv)
+                device_runner(dev, tuple(levels))
             if check_after:
                 self._invariants_device(driver)
                 viol = self._status[Lv:Lv + 3].cpu().numpy()

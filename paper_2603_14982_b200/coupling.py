@@ -460,52 +460,52 @@ class CoupledSim:
         self._push_diag_row(diag)
 
     def _run_rebuild(self, device_fn, key):
-        """Device half of a topology change + the table rebuild + the
-        diagnostics row, as one CUDA graph per (capacities, changed levels,
-        parities) — run eagerly the first time a key is seen (so every buffer
-        it needs is allocated outside capture), captured and replayed after."""
+        """Device half of a topology change + the table rebuild as one CUDA
+        graph per (capacities, rebuilt levels) — run eagerly the first time a
+        key is seen (so every buffer it needs is allocated outside capture),
+        captured and replayed after; then the diagnostics row of the step on
+        the new topology (coupling.py:481) into a second pinned buffer."""
         solver = self.solver
         topo = self.topology
         self.grid.sync_topology()
         if getattr(self, "_host_rb", None) is None:
             self._host_rb = torch.zeros(self._diag_buf.numel(), dtype=torch.float64).pin_memory()
-        full = (topo.cap_version, key, tuple(topo.n_tiles(l) > 0 for l in range(topo.levels)),
-                tuple(k & 1 for k in solver.k), self.last_fields is not None)
+        full = (topo.cap_version, key, tuple(topo.n_tiles(l) > 0 for l in range(topo.levels)))
         if getattr(self, "_rb_ver", None) != topo.cap_version:
             self._rb_graphs, self._rb_seen, self._rb_ver = {}, set(), topo.cap_version
 
         def body():
             device_fn()
             solver._refresh_tables()
-            self._record_diagnostics()
-            self._host_rb.copy_(self._diag_buf, non_blocking=True)
 
         g = self._rb_graphs.get(full)
         if g is None and full not in self._rb_seen:
             self._rb_seen.add(full)
             body()
             self.rebuild_eager += 1
-            return
-        if g is None:
-            if self._pool is None:
-                self._pool = torch.cuda.graph_pool_handle()
-            g = torch.cuda.CUDAGraph()
-            n0 = L.TRACE.launches
-            tracing = L.TRACE.enabled
-            L.TRACE.enabled = False
-            try:
-                with torch.cuda.graph(g, pool=self._pool):
-                    body()
-            finally:
-                L.TRACE.enabled = tracing
-            g.nk = L.TRACE.launches - n0
-            L.TRACE.launches = n0
-            self._rb_graphs[full] = g
-            self.graph_captures += 1
-        g.replay()
-        L.TRACE.launches += g.nk
-        solver._tables_version = topo.version
-        self.rebuild_replays += 1
+        else:
+            if g is None:
+                if self._pool is None:
+                    self._pool = torch.cuda.graph_pool_handle()
+                g = torch.cuda.CUDAGraph()
+                n0 = L.TRACE.launches
+                tracing = L.TRACE.enabled
+                L.TRACE.enabled = False
+                try:
+                    with torch.cuda.graph(g, pool=self._pool):
+                        body()
+                finally:
+                    L.TRACE.enabled = tracing
+                g.nk = L.TRACE.launches - n0
+                L.TRACE.launches = n0
+                self._rb_graphs[full] = g
+                self.graph_captures += 1
+            g.replay()
+            L.TRACE.launches += g.nk
+            solver._tables_version = topo.version
+            self.rebuild_replays += 1
+        self._record_diagnostics()
+        self._host_rb.copy_(self._diag_buf, non_blocking=True)
 
     def _resolve_pending_diag(self):
         """Complete a diagnostics row whose values a rebuild graph is still

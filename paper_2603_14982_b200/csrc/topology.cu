@@ -216,6 +216,14 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
     }
     const bool active = !(id || iu || bcl || solid_c);
     uint64_t mask = 0;
+    // masks can only be non-zero next to an absent tile, the domain edge or a
+    // solid: plain interior tiles skip the 26-direction scan (block-uniform)
+    bool edge = false;
+    for (int a = 0; a < D; ++a)
+        edge |= !lv.periodic[a] && (tx[a] == 0 || tx[a] == lv.tiles[a] - 1);
+    const bool need = rim || edge || solid.n_boxes > 0 || solid.heightmap != nullptr;
+    if (need)
+#pragma unroll
     for (int i = 1; i < Q; ++i) {
         int s[3];
         bool oob = false, bb = false;
