@@ -15,6 +15,7 @@
 // populations, accumulates the bare moments in the shifted form
 // (g = f - w, drho = rho - 1), collides, and the BC tiles apply the
 // outlet/inlet passes in reference face order through shared memory.
+#include <algorithm>
 #include "common.cuh"
 
 namespace mlbm {
@@ -1012,58 +1013,75 @@ int launch_level(const StepArgs& a, int mode, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
+// One target per 16-lane group, lane q < n_m + 2 interpolates field q: the
+// 2^D gathers of all fields of a target are in flight at once (the per-target
+// loop of 12 x 8 dependent-address loads was latency-bound at ~12 % warps
+// active); the S rescale takes u from lanes 1..D of the group by shuffles.
 template <int D, typename R>
 __global__ void downward_kernel(int n, const int32_t* __restrict__ n_dev, const int32_t* __restrict__ targets,
                                 const int32_t* __restrict__ srcs,
                                 const int32_t* __restrict__ tile_xyz,
                                 FieldsT<R> olda, FieldsT<R> newa, FieldsT<R> dst,
                                 int step, R kappa) {
-    constexpr int NC = Geo<D>::NC, NS = Geo<D>::NS, T = Geo<D>::T;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= (n_dev ? __ldg(n_dev) : n)) return;
-    const int tgt = targets[j];
-    const int slot = tgt / T, lc = tgt % T;
-    int par[3] = {lc & 1, (lc >> 2) & 1, (lc >> 4) & 1};
-    // fine coords parity == local parity (tile origin is a multiple of 4)
-    (void)tile_xyz; (void)slot;
-    R w[NC];
-    int s[NC];
+    constexpr int NC = Geo<D>::NC, T = Geo<D>::T, NM = Geo<D>::NM;
+    constexpr int NV = NM + 2;   // moments + eps + phi
+    static_assert(NV <= 16, "one 16-lane group per target");
+    (void)tile_xyz;
+    const int q = threadIdx.x & 15;
+    const int live = n_dev ? __ldg(n_dev) : n;
+    const int groups = (gridDim.x * blockDim.x) >> 4;
+    const int base = threadIdx.x & ~15 & 31;
+    // grid-stride over the live targets (the launch is sized by the SM count,
+    // not by the interface capacity)
+    for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;; j += groups) {
+        if (__all_sync(0xffffffffu, j >= live)) break;      // warp-uniform exit
+        const bool on = j < live;
+        int tgt = 0;
+        R val = R(0);
+        if (on && q < NV) {
+            tgt = targets[j];
+            const int lc = tgt % T;
+            const int par[3] = {lc & 1, (lc >> 2) & 1, (lc >> 4) & 1};
+            const int fk = q < NM ? q : (q == NM ? fi_eps<D>() : fi_phi<D>());
+            int sk[NC];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) {
-        R wk = R(1);
+            for (int k = 0; k < NC; ++k) sk[k] = __ldg(&srcs[(int64_t)j * NC + k]);
+            R xs[NC];
 #pragma unroll
-        for (int a = 0; a < D; ++a) {
-            const int o = (k >> a) & 1;
-            const R fr = par[a] ? R(0.5) : R(0);
-            wk *= o ? fr : R(1) - fr;
+            for (int k = 0; k < NC; ++k) {
+                xs[k] = R(0);
+                if (sk[k] >= 0) {
+                    R x = olda.at(fk, sk[k]);
+                    if (step == 2) x = R(0.5) * (x + newa.at(fk, sk[k]));
+                    xs[k] = x;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+                if (sk[k] < 0) continue;
+                R wk = R(1);
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    const int o = (k >> a) & 1;
+                    const R fr = par[a] ? R(0.5) : R(0);
+                    wk *= o ? fr : R(1) - fr;
+                }
+                val += xs[k] * wk;
+            }
         }
-        w[k] = wk;
-        s[k] = srcs[(int64_t)j * NC + k];
-    }
-    constexpr int NV = Geo<D>::NM + 2;   // moments + eps + phi
-    R v[NV];
+        // S rescale: v_S = kappa (v_S - u_a u_b) + u_a u_b (lanes 1..D hold u)
+        R u[D];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) {
-        const int fk = q < Geo<D>::NM ? q : (q == Geo<D>::NM ? fi_eps<D>() : fi_phi<D>());
-        R acc = R(0);
-#pragma unroll
-        for (int k = 0; k < NC; ++k) {
-            if (s[k] < 0) continue;
-            R x = olda.at(fk, s[k]);
-            if (step == 2) x = R(0.5) * (x + newa.at(fk, s[k]));
-            acc += x * w[k];
+        for (int a = 0; a < D; ++a) u[a] = __shfl_sync(0xffffffffu, val, base + 1 + a);
+        if (on && q >= 1 + D && q < NM) {
+            const int k = q - 1 - D;
+            const R eq = u[s_a<D>(k)] * u[s_b<D>(k)];
+            val = kappa * (val - eq) + eq;
         }
-        v[q] = acc;
-    }
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-        const R eq = v[1 + s_a<D>(k)] * v[1 + s_b<D>(k)];
-        v[1 + D + k] = kappa * (v[1 + D + k] - eq) + eq;
-    }
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-        const int fk = q < Geo<D>::NM ? q : (q == Geo<D>::NM ? fi_eps<D>() : fi_phi<D>());
-        dst.at(fk, tgt) = v[q];
+        if (on && q < NV) {
+            const int fk = q < NM ? q : (q == NM ? fi_eps<D>() : fi_phi<D>());
+            dst.at(fk, tgt) = val;
+        }
     }
 }
 
@@ -1123,7 +1141,10 @@ extern "C" int mlbm_downward(int32_t dim, int32_t n, const int32_t* n_dev, const
                              void* stream) {
     if (n <= 0) return 0;
     cudaStream_t s = as_stream(stream);
-    const int B = 128, G = (n + B - 1) / B;
+    static int sms = 0;
+    if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
+    const int B = 256;
+    const int G = (int)std::min<int64_t>(((int64_t)n * 16 + B - 1) / B, (int64_t)sms * 8);
 #define DOWN(D, R) downward_kernel<D, R><<<G, B, 0, s>>>(n, n_dev, targets, src, tile_xyz, \
         fields_of<R>(olda), fields_of<R>(newa), fields_of<R>(dst), step, R(kappa))
     if (dim == 2) { if (dtype) DOWN(2, double); else DOWN(2, float); }
