@@ -101,6 +101,16 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def dram_traffic():
+    """Per-launch DRAM bytes of the top kernels from the committed ncu full-set
+    capture (profiles/r1_dram_traffic.json, tools/full_summary.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_dram_traffic.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -283,13 +293,22 @@ def run_mine(args, rank, world, local_rank):
         c["achieved_gbs"] = c["bytes"] / (c["ms"] * 1e-3) / 1e9 if c["ms"] and c["bytes"] else None
     dom = max((k for k in classes if classes[k]["bytes"]), key=lambda k: classes[k]["ms"])
 
+    traffic = dram_traffic()
+
     def roof(k):
         c = classes[k]
         ach = c["achieved_gbs"]
+        kern = {"p2g": "k_p2g_cell2", "g2p": "k_g2p", "exchange": "k_exchange",
+                "transfer": "downward_kernel"}.get(k, "level_kernel" if k.startswith("level") else k)
+        tr = traffic.get(kern)
         return {"kernel": k, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(ach / peak, 4), "peak_source": peak_kind,
                 "bytes_per_launch": c["bytes"] / c["launches"],
-                "avg_launch_us": 1e3 * c["ms"] / c["launches"], "traffic": None}
+                "avg_launch_us": 1e3 * c["ms"] / c["launches"],
+                "traffic": tr["bytes_per_launch"] if tr else None,
+                "traffic_source": ("profiles/r1_dram_traffic.json: dram__bytes_read.sum + "
+                                   "dram__bytes_write.sum per launch of " + kern + " from one "
+                                   "ncu --set full capture (C2)") if tr else None}
 
     lbm_keys = [k for k in classes if k.startswith("level_step")]
     lbm_bytes = sum(classes[k]["bytes"] for k in lbm_keys)

@@ -1,9 +1,20 @@
 #!/bin/bash
-# Bench line + ncu launch list + ncu --set full of the top kernels, for profiles/.
-python bench.py --steps 20 --warmup 3 > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
-echo "bench rc=$?"
-CMD="python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-e2e"
-$CMD > gpurun_out/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"level_kernel|k_p2g_cell|k_g2p|k_adapt_pass|k_exchange" -s 20 -c 8 -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1
-echo "profile rc=$?"
+# Round evidence for profiles/ (run under gpurun, 1 GPU): bench lines for C2
+# (default), C3 and C1, then — each only after its plain command exited 0 —
+# an ncu launch list of a short C2 bench and one ncu --set full capture of the
+# top kernels.
+mkdir -p gpurun_out
+python bench.py --steps 60 --warmup 20 > gpurun_out/ev_bench_c2.json 2> gpurun_out/ev_bench_c2.err; echo "bench c2 rc=$?"
+python bench.py --scene c3 --steps 30 --warmup 10 --no-cpu-baseline > gpurun_out/ev_bench_c3.json 2> gpurun_out/ev_bench_c3.err; echo "bench c3 rc=$?"
+python bench.py --scene c1 --steps 60 --warmup 10 > gpurun_out/ev_bench_c1.json 2> gpurun_out/ev_bench_c1.err; echo "bench c1 rc=$?"
+CMD="python bench.py --steps 8 --warmup 4 --no-cpu-baseline --no-e2e"
+$CMD > gpurun_out/ev_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file gpurun_out/ev_launches.csv $CMD > gpurun_out/ev_ncu_launches.log 2>&1
+echo "launch list rc=$?"
+CMD2="python tools/kernel_probe.py 2"
+SCENE=COLUMN_3D_C2 $CMD2 > gpurun_out/ev_plain2.log 2>&1 && \
+SCENE=COLUMN_3D_C2 ncu --set full --clock-control none --import-source on \
+    -k regex:"level_kernel|k_p2g_cell2|k_g2p|k_adapt_pass|k_exchange|downward_kernel" -c 12 \
+    -o gpurun_out/ev_full $CMD2 > gpurun_out/ev_ncu_full.log 2>&1
+echo "full set rc=$?"
