@@ -290,13 +290,11 @@ class GridAdaptor:
             if device_runner is None:
                 self._prepare(changed, pair, new_counts, fresh)()
             else:
-                # graph path: rebuild every non-empty level with the init kernel on,
-                # so the rebuild graph's key is only the level set (unchanged levels
-                # compact to the same map and migrate as an identity copy; init
-                # finds no fresh tile) and it is captured once, not per pattern
-                levels = [l for l in range(Lv) if new_counts[l] or topo.n_tiles(l)]
-                dev = self._prepare(levels, pair, new_counts, [1] * Lv)
-                device_runner(dev, tuple(levels))
+                # graph path: the init kernel always runs (it finds no fresh tile
+                # when there is none), so the rebuild graph's key is only the set
+                # of changed levels
+                dev = self._prepare(changed, pair, new_counts, [1] * Lv)
+                device_runner(dev, tuple(changed))
             if check_after:
                 self._invariants_device(driver)
                 viol = self._status[Lv:Lv + 3].cpu().numpy()

@@ -176,7 +176,9 @@ class CoupledSim:
             adaptor._err = self._sblock[2 * ne + 2 + nst:]
         self.use_graphs = True
         self.sort_particles = True
-        self.sort_every = 4        # particles move < 1 cell/step: re-sort every few steps
+        # particles move < 1 cell/step: re-sort every few steps (P2G / G2P only
+        # need same-cell particles to be mostly adjacent)
+        self.sort_every = int(os.environ.get("MLBM_SORT_EVERY", "16"))
         self._sort_now = True
         self._use_sorted = self._sort_ahead = self._sorted_ahead = False
         self.overlap_diag = os.environ.get("MLBM_OVERLAP_DIAG", "1") != "0"
@@ -474,9 +476,12 @@ class CoupledSim:
         if getattr(self, "_rb_ver", None) != topo.cap_version:
             self._rb_graphs, self._rb_seen, self._rb_ver = {}, set(), topo.cap_version
 
+        # tables of the changed levels and of their neighbours (interfaces)
+        affected = sorted({m for l in key for m in (l - 1, l, l + 1) if 0 <= m < topo.levels})
+
         def body():
             device_fn()
-            solver._refresh_tables()
+            solver._refresh_tables(only=affected)
 
         g = self._rb_graphs.get(full)
         if g is None and full not in self._rb_seen:

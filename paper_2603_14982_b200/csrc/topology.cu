@@ -222,30 +222,44 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
     for (int a = 0; a < D; ++a)
         edge |= !lv.periodic[a] && (tx[a] == 0 || tx[a] == lv.tiles[a] - 1);
     const bool need = rim || edge || solid.n_boxes > 0 || solid.heightmap != nullptr;
-    if (need)
+    if (need) {
+        // neighbour tile of the pull source from the smem neighbour slots (no
+        // tile-map reads); out-of-domain = neighbour tile outside a
+        // non-periodic axis
+        bool has_solids = solid.n_boxes > 0 || solid.heightmap != nullptr;
 #pragma unroll
-    for (int i = 1; i < Q; ++i) {
-        int s[3];
-        bool oob = false, bb = false;
-        for (int a = 0; a < 3; ++a) {
-            const int ci = cvec<D>(i, a);
-            s[a] = g[a] - ci;
-            if (a >= D) continue;
-            if (lv.periodic[a]) s[a] = (s[a] + lv.cells[a]) % lv.cells[a];
-            else if (s[a] < 0) { oob = true; if (bc.face[2 * a] == MLBM_FACE_WALL) bb = true; }
-            else if (s[a] >= lv.cells[a]) { oob = true; if (bc.face[2 * a + 1] == MLBM_FACE_WALL) bb = true; }
-        }
-        bool stored = false;
-        if (!oob) {
-            int sf[3] = {0, 0, 0};
-            for (int a = 0; a < D; ++a) sf[a] = s[a] << level;
-            if (solid_at(solid, D, sf)) bb = true;
-            stored = lv.tile_map[gidx3(lv.tiles, s[0] >> 2, s[1] >> 2, D == 3 ? s[2] >> 2 : 0)] >= 0;
-        }
-        if (bb) mask |= 1ull << i;
-        else if (oob || !stored) {
-            mask |= 1ull << (32 + i);
-            if (active) report_error(err, MLBM_ERR_TOPOLOGY, level, g[0], g[1], g[2], 4);
+        for (int i = 1; i < Q; ++i) {
+            int o[3] = {0, 0, 0};
+            bool oob = false, bb = false;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const int sa = l[a] - cvec<D>(i, a);
+                o[a] = sa < 0 ? -1 : (sa > 3 ? 1 : 0);
+                if (!lv.periodic[a] && o[a] != 0) {
+                    const int t = tx[a] + o[a];
+                    if (t < 0) { oob = true; if (bc.face[2 * a] == MLBM_FACE_WALL) bb = true; }
+                    else if (t >= lv.tiles[a]) { oob = true; if (bc.face[2 * a + 1] == MLBM_FACE_WALL) bb = true; }
+                }
+            }
+            bool stored = false;
+            if (!oob) {
+                stored = snb[nb_index<D>(o[0], o[1], o[2])] >= 0;
+                if (has_solids) {
+                    int sf[3] = {0, 0, 0};
+#pragma unroll
+                    for (int a = 0; a < D; ++a) {
+                        int sa = g[a] - cvec<D>(i, a);
+                        if (lv.periodic[a]) sa = (sa + lv.cells[a]) % lv.cells[a];
+                        sf[a] = sa << level;
+                    }
+                    if (solid_at(solid, D, sf)) bb = true;
+                }
+            }
+            if (bb) mask |= 1ull << i;
+            else if (oob || !stored) {
+                mask |= 1ull << (32 + i);
+                if (active) report_error(err, MLBM_ERR_TOPOLOGY, level, g[0], g[1], g[2], 4);
+            }
         }
     }
     uint8_t f = 0;

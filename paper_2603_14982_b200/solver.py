@@ -223,12 +223,14 @@ class _LevelTables:
         return (self.cell_flags & 1).bool()
 
 
-def build_tables(topo: Topology, bc, solid, err, tables=None):
+def build_tables(topo: Topology, bc, solid, err, tables=None, only=None):
     """Classify every level (flags, bounce-back masks, interface stencils) on
     the device (solver.py:177-274 + sparse_grid.py:468-544).  Buffers are
     (re)allocated only when a level's capacity changed; counts of I^d / I^u go
     to ``topo.dcounts[l, 2:4]``.  No host synchronisation: violations land in
-    ``err`` and are raised by the caller's next status check."""
+    ``err`` and are raised by the caller's next status check.  ``only``
+    restricts the classification and interface builds to a set of levels
+    (those whose own or adjacent kind grids changed); the others keep theirs."""
     lib = L.lib()
     s = L.stream_handle()
     T = TILE ** topo.d
@@ -251,7 +253,7 @@ def build_tables(topo: Topology, bc, solid, err, tables=None):
                     torch.full((cap * T, NC), -1, dtype=torch.int32, device=topo.device),
                     cap * T)
             tables[l] = t
-        if not cap:
+        if not cap or (only is not None and l not in only):
             continue
         lvs = topo.level_struct(l)
         L.check(lib.mlbm_classify_level(L.C.byref(lvs), L.C.byref(hier), L.C.byref(bc),
@@ -259,7 +261,7 @@ def build_tables(topo: Topology, bc, solid, err, tables=None):
                                         L.ptr(t.dir_masks), L.ptr(t.tile_flags),
                                         L.ptr(scratch[l]), L.ptr(err), s), "classify_level")
     for l, t in tables.items():
-        if not topo.lv[l].cap:
+        if not topo.lv[l].cap or (only is not None and l not in only):
             continue
         for which, other in ((0, l + 1), (1, l - 1)):
             cnt = topo.dcounts[l, 2 + which:3 + which]
@@ -306,11 +308,14 @@ class MultiLevelSolver:
         self._refresh_tables()
 
     # -- tables -----------------------------------------------------------------
-    def _refresh_tables(self):
+    def _refresh_tables(self, only=None):
         topo = self.topology
         if self._tables_version == topo.version:
             return
-        self._tables = build_tables(topo, self._bc, self._solid, self._err, self._tables)
+        if only is not None and (self._tables is None or
+                                 any(l not in self._tables for l in range(topo.levels))):
+            only = None
+        self._tables = build_tables(topo, self._bc, self._solid, self._err, self._tables, only)
         self._tables_version = topo.version
         if getattr(self, "_structs_cap", None) != topo.cap_version:
             self._structs = {l: topo.level_struct(l, t) for l, t in self._tables.items()}

@@ -4,7 +4,8 @@ sys.path.insert(0, "."); sys.path.insert(0, "tests")
 import torch
 import scenes as S
 from paper_2603_14982_b200.harness import build_scene, validate_scene
-sim = build_scene(validate_scene(S.COLUMN_3D_C2))
+import os
+sim = build_scene(validate_scene(getattr(S, os.environ.get("SCENE", "COLUMN_3D_C2"))))
 for _ in range(3):
     sim.step()
 ad = sim.adaptor

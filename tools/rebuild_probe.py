@@ -6,7 +6,8 @@ import torch
 import scenes as S
 from paper_2603_14982_b200 import _lib as L
 from paper_2603_14982_b200.harness import build_scene, validate_scene
-sim = build_scene(validate_scene(S.COLUMN_3D_C2))
+import os
+sim = build_scene(validate_scene(getattr(S, os.environ.get("SCENE", "COLUMN_3D_C2"))))
 for _ in range(30):
     sim.step()
 # force every later rebuild to run eagerly, traced
