@@ -944,13 +944,32 @@ __global__ void k_diag_level(mlbm_level_t lv, mlbm_fields_t f, double vol, doubl
     double emin = 1e300;
     const FieldsT<R> a = fields_of<R>(f);
     const int64_t n = (int64_t)live_tiles(lv) * T;
-    for (int64_t c = (int64_t)lv.first * T + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
-         c += (int64_t)gridDim.x * blockDim.x) {
-        if (!(lv.cell_flags[c] & MLBM_CF_LEAF)) continue;
-        const double rho = 1.0 + (double)a.at(0, c);
-        for (int k = 0; k < D; ++k) acc[k] += vol * rho * (double)a.at(1 + k, c);
-        acc[D] += vol * (double)a.at(fi_phi<D>(), c);
-        emin = fmin(emin, (double)a.at(fi_eps<D>(), c));
+    const int64_t st = (int64_t)gridDim.x * blockDim.x;
+    constexpr int U = 4;                 // 4 cells per trip: loads overlap
+    for (int64_t c0 = (int64_t)lv.first * T + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c0 < n;
+         c0 += U * st) {
+        bool lf[U];
+        R r0[U], uu[U][D], ph[U], ep[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t c = c0 + u * st;
+            lf[u] = c < n && (lv.cell_flags[c] & MLBM_CF_LEAF);
+            if (lf[u]) {
+                r0[u] = a.at(0, c);
+#pragma unroll
+                for (int k = 0; k < D; ++k) uu[u][k] = a.at(1 + k, c);
+                ph[u] = a.at(fi_phi<D>(), c);
+                ep[u] = a.at(fi_eps<D>(), c);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!lf[u]) continue;
+            const double rho = 1.0 + (double)r0[u];
+            for (int k = 0; k < D; ++k) acc[k] += vol * rho * (double)uu[u][k];
+            acc[D] += vol * (double)ph[u];
+            emin = fmin(emin, (double)ep[u]);
+        }
     }
     // block min, then one compare-and-swap per block (not per warp)
     __shared__ double smin[32];
@@ -974,14 +993,33 @@ __global__ void k_diag_particles(PartArgs P, const R* ras, int64_t rs, int64_t n
     for (int k = 0; k < 2 * D; ++k) acc[k] = 0.0;
     const R* pp = (const R*)P.p;
     const int64_t m = P.n > n0 ? P.n : n0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        if (i < P.n) {
-            const double mass = (double)pp[PR::M * P.ps + i];
-            for (int a = 0; a < D; ++a) acc[a] += mass * (double)pp[(PR::V + a) * P.ps + i];
+    const int64_t st = (int64_t)gridDim.x * blockDim.x;
+    constexpr int U = 4;                 // 4 elements per trip: loads overlap
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < m; i0 += U * st) {
+        R mv[U], vv[U][D], fv[U][D];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * st;
+            mv[u] = R(0);
+#pragma unroll
+            for (int a = 0; a < D; ++a) { vv[u][a] = R(0); fv[u][a] = R(0); }
+            if (i < P.n) {
+                mv[u] = pp[PR::M * P.ps + i];
+#pragma unroll
+                for (int a = 0; a < D; ++a) vv[u][a] = pp[(PR::V + a) * P.ps + i];
+            }
+            if (ras && i < n0) {
+#pragma unroll
+                for (int a = 0; a < D; ++a) fv[u][a] = ras[(Rows<D>::FS + a) * rs + i];
+            }
         }
-        if (ras && i < n0)
-            for (int a = 0; a < D; ++a) acc[D + a] += (double)ras[(Rows<D>::FS + a) * rs + i];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                acc[a] += (double)mv[u] * (double)vv[u][a];
+                acc[D + a] += (double)fv[u][a];
+            }
     }
     block_sum_atomic<2 * D>(acc, out);
 }
@@ -2012,7 +2050,9 @@ extern "C" int mlbm_diag_level(const mlbm_level_t* lv, mlbm_fields_t f, double v
     const int64_t n = (int64_t)lv->n_tiles * T;
     if (n == 0) return 0;
     cudaStream_t s = as_stream(stream);
-    const int gb = (int)std::min<int64_t>(nblk(n, 256), 592);
+    static int sms = 0;
+    if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
+    const int gb = (int)std::min<int64_t>(nblk(n, 256 * 4), (int64_t)sms * 4);
 #define DG(D, R) k_diag_level<D, R><<<gb, 256, 0, s>>>(*lv, f, vol, out)
     if (lv->dim == 2) { if (dtype) DG(2, double); else DG(2, float); }
     else { if (dtype) DG(3, double); else DG(3, float); }
@@ -2027,7 +2067,9 @@ extern "C" int mlbm_diag_particles(int32_t dim, int32_t n, const void* p, int64_
     if (m == 0) return 0;
     PartArgs P{dim, n, nullptr, nullptr, (void*)p, ps, nullptr, nullptr, nullptr};
     cudaStream_t s = as_stream(stream);
-    const int gb = (int)std::min<int64_t>(nblk(m, 256), 296);
+    static int sms = 0;
+    if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
+    const int gb = (int)std::min<int64_t>(nblk(m, 256 * 4), (int64_t)sms * 4);
 #define DP(D, R) k_diag_particles<D, R><<<gb, 256, 0, s>>>(P, (const R*)ras, rs, n0, live, out)
     if (dim == 2) { if (dtype) DP(2, double); else DP(2, float); }
     else { if (dtype) DP(3, double); else DP(3, float); }
