@@ -64,6 +64,17 @@ DUNE_3D_SMALL = {       # config 3 at test size
     "particles": {"blocks": [[16.0, 2.0, 0.0, 36.0, 8.0, 16.0]], "per_cell": 2},
     "runtime": {"seed": 42}}
 
+SANDSTORM_3D_SMALL = {  # config 3 (C3) at test size: three levels, inflow, z periodic
+    "domain": {"cells": [64, 32, 16], "levels": 3},
+    "fluid": {"tau0": 1.8, "eps_min": 0.5, "gravity": [0.0, -1e-4, 0.0]},
+    "boundaries": {"x_min": {"kind": "log_inlet", "u0": 0.05, "beta": 0.35, "y0": 6.0},
+                   "x_max": "outlet", "y_min": "wall", "y_max": "outlet",
+                   "z_min": "periodic", "z_max": "periodic"},
+    "materials": {"density_ratio": 40.0, "E": 0.08, "nu": 0.3, "friction_angle_deg": 30.0,
+                  "floor_friction": 0.5},
+    "particles": {"blocks": [[16.0, 2.0, 0.0, 44.0, 7.0, 16.0]], "per_cell": 2},
+    "runtime": {"seed": 9}}
+
 POWDER_3D_SMALL = {     # config 4 ingredients at test size (powder on, solids)
     "domain": {"cells": [32, 32, 16], "levels": 1},
     "fluid": {"tau0": 1.8, "eps_min": 0.5, "gravity": [0.0, -5e-5, 0.0]},

@@ -130,6 +130,28 @@ def test_dune_3d_inlet_outlet():
     run_and_compare(S.DUNE_3D_SMALL, 6)
 
 
+def test_sandstorm_3d_three_levels():
+    """C3 at test size: three levels, log inlet, outlets, z periodic, fp64."""
+    run_and_compare(S.SANDSTORM_3D_SMALL, 6)
+
+
+def test_fp32_sandstorm_3d_three_levels():
+    """Gate B on the three-level path: fp32 device vs fp64 oracle."""
+    _need_gpu()
+    sc = S.scene(S.SANDSTORM_3D_SMALL, runtime__dtype="f32")
+    osim, dsim = build_both(sc)
+    for _ in range(10):
+        osim.step()
+        dsim.step()
+        assert dsim.topology.tile_set() == osim.topo.tile_set()
+    x = dsim.particles.x.cpu().numpy()
+    v = dsim.particles.v.double().cpu().numpy()
+    rx = np.linalg.norm(x - osim.p.x) / np.linalg.norm(osim.p.x)
+    rv = np.linalg.norm(v - osim.p.v) / max(np.linalg.norm(osim.p.v), 1e-30)
+    assert rx <= 1e-5, rx
+    assert rv <= 1e-4, rv
+
+
 def test_powder_3d_solids():
     run_and_compare(S.POWDER_3D_SMALL, 6)
 
