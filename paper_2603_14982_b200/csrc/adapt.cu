@@ -462,10 +462,15 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
     }
     STAMP_BARRIER(3);
 
-    // ---- D/E: desired coverage of coarser levels
+    // ---- D/E: desired coverage of coarser levels (the top level is all ones
+    //      and needs neither its parents bitmap nor a barrier)
     for (int l = 1; l < L; ++l) {
         const int* d = A.tdims[l];
         const int64_t n = (int64_t)d[0] * d[1] * d[2];
+        if (l == L - 1) {
+            for (int64_t g = tid; g < n; g += nth) A.des[l][g] = 1;
+            break;
+        }
         for (int64_t g = tid; g < n; g += nth) {
             int c[3];
             dec3(d, g, c[0], c[1], c[2]);
@@ -482,7 +487,6 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
         }
         STAMP_BARRIER(4);
         for (int64_t g = tid; g < n; g += nth) {
-            if (l == L - 1) { A.des[l][g] = 1; continue; }
             int c[3];
             dec3(d, g, c[0], c[1], c[2]);
             A.des[l][g] = group_window_any(A.par[l], d, dim, A.periodic, c, 2);
@@ -517,15 +521,15 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
             A.par[l][g] = children_any(A.eff[l - 1], A.tdims[l - 1], dim, c);
         }
         STAMP_BARRIER(7);
-        effective_stage(A, l, true, tid, nth);
-        STAMP_BARRIER(8);
-        if (l == L - 1) {
-            for (int64_t g = tid; g < n; g += nth) A.eff[l][g] = 1;
-            STAMP_BARRIER(9);
+        // the top level's hysteresis is a no-op (des = 1: no candidate, its
+        // streaks stay 0) and its effective coverage is all ones
+        // (adapt.py:180-181): skipped, phase I reads eff[L-1] as 1
+        if (l < L - 1) {
+            effective_stage(A, l, true, tid, nth);
+            STAMP_BARRIER(8);
         }
     }
-    // par[l] now holds parents(eff[l-1]) for every l >= 1 (eff[L-1] = 1 set
-    // after its own parents were taken, as in adapt.py:180-181)
+    // par[l] now holds parents(eff[l-1]) for every l >= 1
 
     // ---- I/J: own = eff & ~parents(eff[l-1]); storage = dilate2(own) as three
     //      separable radius-2 ORs (x into stor, y into des, z on the fly);
@@ -537,7 +541,7 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
         for (int64_t g = tid; g < n; g += nth) {
             int c[3];
             dec3(d, g, c[0], c[1], c[2]);
-            A.own[l][g] = A.eff[l][g] && !(l > 0 && A.par[l][g]);
+            A.own[l][g] = (l == L - 1 || A.eff[l][g]) && !(l > 0 && A.par[l][g]);
             bool any = false;
 #pragma unroll
             for (int k = -2; k <= 2; ++k) {
@@ -545,7 +549,7 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
                 if (per0) { v %= nx; if (v < 0) v += nx; }
                 else if (v < 0 || v >= nx) continue;
                 const int64_t q = gi3(d, v, c[1], c[2]);
-                any |= A.eff[l][q] && !(l > 0 && A.par[l][q]);
+                any |= (l == L - 1 || A.eff[l][q]) && !(l > 0 && A.par[l][q]);
             }
             A.stor[l][g] = any;
         }
