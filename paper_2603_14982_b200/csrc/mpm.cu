@@ -559,6 +559,16 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
     }
     __syncthreads();
     if (!live) return;
+    // rows that only ride along (F, vc, m, V0, id): loaded now so their
+    // latency overlaps the gather instead of stalling the epilogue
+    R Fpre[D * D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) Fpre[k] = pp[(PR::F + k) * P.ps + p];
+    const R vc_pre = pp[PR::VC * P.ps + p];
+    const bool copy_rows = pw != pp;
+    const R m_pre = copy_rows ? pp[PR::M * P.ps + p] : R(0);
+    const R v0_pre = copy_rows ? pp[PR::V0 * P.ps + p] : R(0);
+    const int32_t id_pre = P.pidw ? P.pid[p] : 0;
     R v[D], B[D * D];
 #pragma unroll
     for (int a = 0; a < D; ++a) v[a] = R(0);
@@ -667,7 +677,7 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
     }
     R F[D * D], Fn[D * D];
 #pragma unroll
-    for (int k = 0; k < D * D; ++k) { F[k] = pp[(PR::F + k) * P.ps + p]; pw[(PR::C + k) * P.ps + p] = C[k]; }
+    for (int k = 0; k < D * D; ++k) { F[k] = Fpre[k]; pw[(PR::C + k) * P.ps + p] = C[k]; }
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
@@ -686,7 +696,7 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
         }
         if (!fast) svd<D, R>(Fn, U, s, V);
         R e[D], tr = R(0);
-        const R vc = pp[PR::VC * P.ps + p];
+        const R vc = vc_pre;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
             R sa = s[a] < R(0.05) ? R(0.05) : (s[a] > R(4) ? R(4) : s[a]);
@@ -751,12 +761,12 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
     }
 #pragma unroll
     for (int k = 0; k < D * D; ++k) pw[(PR::F + k) * P.ps + p] = Fn[k];
-    if (pw != pp) {
-        if (!plastic) pw[PR::VC * P.ps + p] = pp[PR::VC * P.ps + p];
-        pw[PR::M * P.ps + p] = pp[PR::M * P.ps + p];
-        pw[PR::V0 * P.ps + p] = pp[PR::V0 * P.ps + p];
+    if (copy_rows) {
+        if (!plastic) pw[PR::VC * P.ps + p] = vc_pre;
+        pw[PR::M * P.ps + p] = m_pre;
+        pw[PR::V0 * P.ps + p] = v0_pre;
     }
-    if (P.pidw) P.pidw[p] = P.pid[p];
+    if (P.pidw) P.pidw[p] = id_pre;
 }
 
 // ---------------------------------------------------------------------------
