@@ -185,3 +185,207 @@ def exchange_local(slabs, tree_idx):
             dst = slabs[sl.left].ghost_columns(tree_idx)[1]
             dst.copy_(lo_col)
     assert world == len(slabs)
+
+
+# ---------------------------------------------------------------------------------
+# Multi-level slabs (static hierarchy): SURVEY.md §8(e) collective (i) for every
+# level of the Alg. 1 recursion.
+
+class SlabMultiLevel:
+    """One rank's slab of a static multi-level LBM hierarchy.
+
+    The global tile set is cropped to the slab plus a ghost region one
+    coarsest tile wide on every side with a neighbour (2^(L-1-l) tile columns
+    at level l), shifted to a local box whose x faces are walls (ghost tiles
+    are never stepped).  Level steps run over the owned slot range of each
+    level; after every level step the owned edge columns of the level's write
+    tree are sent to the neighbours' ghost columns, so interface fills that
+    read coarse cells across the cut and the next pulls see the owners'
+    values.  Downward / upward transfers run on every target of the local box
+    (those in the ghost region recompute the owners' values from the same
+    inputs or are overwritten before use)."""
+
+    def __init__(self, global_cells, levels, global_tiles, rank, world, tau0,
+                 dtype=torch.float64, periodic=(True, True, True), init=None, device=None):
+        self.global_cells = tuple(int(v) for v in global_cells)
+        self.d = len(self.global_cells)
+        self.levels = levels
+        self.rank, self.world = rank, world
+        self.part = SlabPartition(self.global_cells, levels, world, periodic_x=bool(periodic[0]))
+        x0, x1 = self.part.slab(rank)
+        left, right = self.part.neighbors(rank)
+        self.left = left if world > 1 else None
+        self.right = right if world > 1 else None
+        cw = self.part.coarse_width                       # finest cells of one coarsest tile
+        self.gl = cw if self.left is not None else 0
+        self.gr = cw if self.right is not None else 0
+        self.x0 = x0 - self.gl
+        local = (x1 - x0 + self.gl + self.gr,) + self.global_cells[1:]
+        per_local = ((bool(periodic[0]) and world == 1),) + tuple(bool(p) for p in periodic[1:self.d])
+        self.topology = Topology(local, levels, periodic=per_local, device=device)
+        gx = self.global_cells[0]
+        tiles = set()
+        for e in global_tiles:
+            l, c = e[0], list(e[1:-1])
+            tw = TILE << l
+            for wrap in ((0, -gx, gx) if periodic[0] else (0,)):
+                lx = c[0] * tw + wrap - self.x0             # local finest x of the tile origin
+                if 0 <= lx < local[0]:
+                    tiles.add((l, lx // tw) + tuple(c[1:]) + (e[-1],))
+        self.topology.set_tile_set(sorted(tiles))
+        self.pair = PingPongPair(self.topology, dtype)
+        self.params = SolverParams(levels=levels, h3_xyz=H3_XYZ_HERMITE)
+        self.level_params = LevelParams(levels, tau0)
+        faces = {}
+        for a, ax in enumerate("xyz"[:self.d]):
+            kind = "periodic" if per_local[a] else "wall"
+            faces[ax + "_min"] = faces[ax + "_max"] = kind
+        self.solver = MultiLevelSolver(self.topology, self.pair, self.params, self.level_params,
+                                       BoundarySpec(faces=faces, dim=self.d))
+        self.solver.check_errors = False
+        # per level: owned slot range and the slot ranges of the edge / ghost columns
+        self.ranges = []
+        for l in range(levels):
+            xs = self.topology.tile_coords(l)[:, 0] if self.topology.n_tiles(l) else np.zeros(0, int)
+            wl = (self.gl // (TILE << l), self.gr // (TILE << l))
+            ncol = local[0] // (TILE << l)
+            cnt = lambda lo, hi: int(((xs >= lo) & (xs < hi)).sum())      # noqa: E731
+            a = cnt(0, wl[0])
+            b = a + cnt(wl[0], ncol - wl[1])
+            self.ranges.append({
+                "ghost_l": (0, a), "owned": (a, b), "ghost_r": (b, len(xs)),
+                "edge_l": (a, a + cnt(wl[0], 2 * wl[0])) if wl[0] else (a, a),
+                "edge_r": (b - cnt(ncol - 2 * wl[1], ncol - wl[1]), b) if wl[1] else (b, b)})
+        if init is not None:
+            self.set_fields(init)
+        self._lv = {}
+
+    def set_fields(self, fn):
+        for l in range(self.levels):
+            if not self.topology.n_tiles(l):
+                continue
+            pos = self.topology.cell_coords(l).astype(float) * float(1 << l)
+            pos[:, 0] = np.mod(pos[:, 0] + self.x0, self.global_cells[0])
+            vals = fn(pos, l)
+            for tree in self.pair.trees:
+                for nm, v in vals.items():
+                    tree.levels[l][nm] = v
+
+    def _owned_struct(self, level):
+        if level not in self._lv:
+            s = self.solver
+            s._refresh_tables()
+            lv = L.Level.from_buffer_copy(s._structs[level])
+            lv.counts = None
+            a, b = self.ranges[level]["owned"]
+            lv.first = a
+            lv.n_tiles = b
+            self._lv[level] = lv
+        return self._lv[level]
+
+    def step_level(self, level):
+        """Fused stream + collide of the owned tiles of one level; returns
+        the write tree index."""
+        s = self.solver
+        r, w = s.roles(level)
+        a, b = self.ranges[level]["owned"]
+        if b > a:
+            cp = s._collide_struct(level)
+            L.check(L.lib().mlbm_level_step(L.C.byref(self._owned_struct(level)),
+                                            L.fields(s.arrays(r, level).data),
+                                            L.fields(s.arrays(w, level).data), s.dcode, 0,
+                                            L.C.byref(cp), L.C.byref(s._bc), L.ptr(s._err),
+                                            L.stream_handle()), "level_step")
+        s.k[level] += 1
+        return w
+
+    def cells(self, level, rng):
+        T = TILE ** self.d
+        return rng[0] * T, rng[1] * T
+
+    def owned_cells(self, tree_idx, level, name):
+        a = self.pair.trees[tree_idx].levels[level]
+        lo, hi = self.cells(level, self.ranges[level]["owned"])
+        coords = self.topology.cell_coords(level)[lo:hi].copy()
+        coords[:, 0] = np.mod(coords[:, 0] + (self.x0 >> level), self.global_cells[0] >> level)
+        return coords, a[name].cpu().numpy()[lo:hi]
+
+
+def run_cycle_slabs(slabs, cycle, exchange):
+    """One finest cycle of the Alg. 1 schedule (solver.py:564-595) on slab
+    objects in lockstep; ``exchange(slabs, level, tree)`` after every level
+    step (device copies in one process, or P2P between processes)."""
+    s0 = slabs[0]
+    L_ = s0.levels
+    for kind, level, s in cycle["pre"]:
+        if kind == "down":
+            for sl in slabs:
+                sl.solver.downward_transfer(level, s)
+        elif kind == "sc":
+            w = None
+            for sl in slabs:
+                w = sl.step_level(level)
+            exchange(slabs, level, w)
+        elif kind == "up":
+            for sl in slabs:
+                sl.solver.upward_transfer(level)
+    if L_ > 1:
+        for sl in slabs:
+            sl.solver.downward_transfer(0, cycle["s0"])
+    w = None
+    for sl in slabs:
+        w = sl.step_level(0)
+    exchange(slabs, 0, w)
+    if L_ > 1 and cycle["s0"] == 2:
+        for sl in slabs:
+            sl.solver.upward_transfer(0)
+    if cycle["last"]:
+        for sl in slabs:
+            sl.pair.bounce += 1
+
+
+def exchange_levels_local(slabs, level, tree_idx):
+    """Single-process stand-in for the per-level P2P: owned edge columns of
+    ``level`` (write tree) -> the neighbours' ghost columns."""
+    nm = len(moment_names(slabs[0].d))
+    for sl in slabs:
+        a = sl.pair.trees[tree_idx].levels[level].data
+        for side, nb_idx in (("edge_r", sl.right), ("edge_l", sl.left)):
+            if nb_idx is None:
+                continue
+            nb = slabs[nb_idx]
+            g = "ghost_l" if side == "edge_r" else "ghost_r"
+            lo, hi = sl.cells(level, sl.ranges[level][side])
+            glo, ghi = nb.cells(level, nb.ranges[level][g])
+            assert hi - lo == ghi - glo, (level, side, hi - lo, ghi - glo)
+            nb.pair.trees[tree_idx].levels[level].data[:nm, glo:ghi].copy_(a[:nm, lo:hi])
+
+
+def exchange_levels_p2p(slabs, level, tree_idx):
+    """The per-level exchange between processes (one slab per rank): batch
+    P2P of the owned edge columns into the neighbours' ghost columns
+    (NCCL over NVLink for CUDA tensors)."""
+    (sl,) = slabs
+    if sl.world == 1:
+        return
+    nm = len(moment_names(sl.d))
+    a = sl.pair.trees[tree_idx].levels[level].data
+    r = sl.ranges[level]
+    lo_l, hi_l = sl.cells(level, r["edge_l"])
+    lo_r, hi_r = sl.cells(level, r["edge_r"])
+    glo_l, ghi_l = sl.cells(level, r["ghost_l"])
+    glo_r, ghi_r = sl.cells(level, r["ghost_r"])
+    edge_l = a[:nm, lo_l:hi_l]
+    edge_r = a[:nm, lo_r:hi_r]
+    ghost_l = a[:nm, glo_l:ghi_l] if sl.left is not None else None
+    ghost_r = a[:nm, glo_r:ghi_r] if sl.right is not None else None
+    key = (level, edge_l.shape[1], edge_r.shape[1],
+           0 if ghost_l is None else ghost_l.shape[1], 0 if ghost_r is None else ghost_r.shape[1])
+    bufs = getattr(sl, "_p2p_bufs", {})
+    if key not in bufs:
+        mk = lambda n: torch.empty((nm, n), dtype=a.dtype, device=a.device)     # noqa: E731
+        bufs[key] = ([mk(edge_l.shape[1]), mk(edge_r.shape[1])],
+                     [mk(key[3]), mk(key[4])])
+        sl._p2p_bufs = bufs
+    send, recv = bufs[key]
+    exchange_columns(edge_l, edge_r, ghost_l, ghost_r, sl.left, sl.right, send, recv)

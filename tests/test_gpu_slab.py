@@ -47,3 +47,47 @@ def test_slabs_equal_single_domain(d, cells, world, dtype):
             c2, got = sl.owned_cells(sl.solver.last_roles(0)[1], name)
             want = np.array([key[tuple(c)] for c in c2.tolist()])
             assert np.array_equal(got, want), (name, sl.rank)
+
+
+@pytest.mark.parametrize("d,cells,levels,world", [(3, (64, 16, 16), 2, 2), (3, (64, 32, 16), 3, 2),
+                                                  (2, (128, 64), 3, 3)])
+def test_multilevel_slabs_equal_single_domain(d, cells, levels, world):
+    """Static refined hierarchy whose fine region straddles the cuts: every
+    level's owned cells equal the single-domain run bit for bit (fp64)."""
+    _need_gpu()
+    from paper_2603_14982_b200.slab_lbm import (SlabMultiLevel, exchange_levels_local,
+                                                run_cycle_slabs)
+    from paper_2603_14982_b200.sparse_grid import moment_names
+    tau0 = 0.8
+    # global hierarchy: static refinement of a box across the middle of x
+    gt = B.Topology.uniform(cells, levels)
+    pair = B.PingPongPair(gt)
+    ad = B.GridAdaptor(gt, B.LevelParams(levels, tau0))
+    t0 = gt.tiles_dims(0)
+    mask = np.zeros(t0, dtype=bool)
+    mid = t0[0] // 2
+    sl = (slice(mid - 3, mid + 3), slice(t0[1] // 4, t0[1] // 2)) + ((slice(0, t0[2] // 2),) if d == 3 else ())
+    mask[sl] = True
+    for _ in range(3):
+        ad.update(B.RefineDriver(static_tiles=mask, levels=levels), pair)
+    tiles = gt.tile_set()
+    lp = B.LevelParams(levels, tau0)
+    from paper_2603_14982_b200.harness.config import taylor_green_fn
+    init = taylor_green_fn(0.04, cells[1], lp.nu(0), lp.taus, d)
+    whole = SlabMultiLevel(cells, levels, tiles, 0, 1, tau0, init=init)
+    slabs = [SlabMultiLevel(cells, levels, tiles, r, world, tau0, init=init) for r in range(world)]
+    noop = lambda s, l, t: None                                          # noqa: E731
+    sched = whole.solver._schedule
+    for i in range(2 * len(sched)):
+        run_cycle_slabs([whole], sched[i % len(sched)], noop)
+        run_cycle_slabs(slabs, sched[i % len(sched)], exchange_levels_local)
+    torch.cuda.synchronize()
+    for l in range(levels):
+        wi = whole.solver.last_roles(l)[1]
+        for name in moment_names(d):
+            coords, ref = whole.owned_cells(wi, l, name)
+            key = {tuple(c): v for c, v in zip(coords.tolist(), ref)}
+            for s in slabs:
+                c2, got = s.owned_cells(s.solver.last_roles(l)[1], l, name)
+                want = np.array([key[tuple(c)] for c in c2.tolist()])
+                assert np.array_equal(got, want), (l, name, s.rank, np.abs(got - want).max())
