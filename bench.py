@@ -36,8 +36,8 @@ REF_TIMED_STEPS_CAP = 5
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--scene", default="c2", choices=["c2", "c3", "c1"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -182,6 +182,9 @@ class CoupledSim:
         self._sort_now = True
         self._use_sorted = self._sort_ahead = self._sorted_ahead = False
         self.overlap_diag = os.environ.get("MLBM_OVERLAP_DIAG", "1") != "0"
+        # graphs of this many upcoming steps are captured whenever capacities
+        # change (first step included), so steady stepping only replays
+        self.precapture_steps = int(os.environ.get("MLBM_PRECAPTURE", "16")) or None
         self.p2g_mode = 4          # sorted input: 1 block smem, 2 warp registers, 3 cell lanes,
                                    # 4 cell lanes + per-warp box copies (fp32; fp64 runs mode 3)
         self._graphs = {}
@@ -365,11 +368,90 @@ class CoupledSim:
             self._host_i32 = torch.zeros(self._sblock.numel(), dtype=torch.int32).pin_memory()
             self._host_f64 = torch.zeros(self._diag_buf.numel(), dtype=torch.float64).pin_memory()
 
+    def _sort_flags(self, step, sorted_ahead, is_mpm, adapt_now):
+        """(use_sorted, sort_now, sort_ahead) of a step.  Particle sort: every
+        sort_every steps; with the diagnostics overlap it runs at the end of
+        the previous step beside the adapt pass (it only reads the particle
+        rows the pass reads) and this step's P2G takes the sorted scratch."""
+        use_sorted = sorted_ahead
+        sort_now = (step % self.sort_every) == 0 and not use_sorted
+        sort_ahead = bool(self.overlap_diag and adapt_now and is_mpm and self.cadence == 1
+                          and self.sort_particles and len(self.particles)
+                          and (step + 1) % self.sort_every == 0)
+        return use_sorted, sort_now, sort_ahead
+
+    def _step_kinds(self, step):
+        is_mpm = self.coupling_active and (step % self.cadence == 0)
+        adapt_now = self.adaptor is not None and self.coupling_active and step % self.cadence == 0
+        return is_mpm, adapt_now
+
+    def _capture(self, key, ci, is_mpm, adapt_now, k, bounce, flags):
+        """Capture the step graph of one key with the host state (level
+        counters, bounce, sort flags) that step will have; restores it."""
+        solver = self.solver
+        if self._pool is None:
+            self._pool = torch.cuda.graph_pool_handle()
+        saved = (list(solver.k), self.pair.bounce, self._use_sorted, self._sort_now,
+                 self._sort_ahead, self.last_fields)
+        solver.k[:] = k
+        self.pair.bounce = bounce
+        self._use_sorted, self._sort_now, self._sort_ahead = flags
+        g = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        n0 = L.TRACE.launches
+        tracing = L.TRACE.enabled
+        L.TRACE.enabled = False
+        try:
+            with torch.cuda.graph(g, pool=self._pool):
+                self._device_step(ci, is_mpm, adapt_now)
+        finally:
+            L.TRACE.enabled = tracing
+        nk = L.TRACE.launches - n0
+        L.TRACE.launches = n0          # captured, not executed
+        dk = [a - b for a, b in zip(solver.k, k)]
+        db = self.pair.bounce - bounce
+        entry = (g, dk, db, self.last_fields, nk)
+        (k0, self.pair.bounce, self._use_sorted, self._sort_now, self._sort_ahead,
+         self.last_fields) = saved
+        solver.k[:] = k0
+        self._graphs[key] = entry
+        self.graph_captures += 1
+        return entry
+
+    def _key(self, ci, k, is_mpm, adapt_now, flags, lf_set):
+        use_sorted, sort_now, sort_ahead = flags
+        return (ci, tuple(v & 1 for v in k), is_mpm, adapt_now, sort_now, use_sorted, sort_ahead,
+                self.powder is not None and is_mpm and lf_set)
+
+    def _precapture(self, n):
+        """Capture the graphs of the next ``n`` steps now (host state
+        predicted from each graph's level-counter increments), so steady
+        stepping replays only — re-run whenever capacities change."""
+        schedule = self.solver._schedule
+        k = list(self.solver.k)
+        b = self.pair.bounce
+        sa = self._sorted_ahead
+        lf = self.last_fields is not None
+        for j in range(n):
+            step = self.step_count + j
+            ci = k[0] % len(schedule)
+            is_mpm, adapt_now = self._step_kinds(step)
+            flags = self._sort_flags(step, sa, is_mpm, adapt_now)
+            key = self._key(ci, k, is_mpm, adapt_now, flags, lf)
+            entry = self._graphs.get(key)
+            if entry is None:
+                entry = self._capture(key, ci, is_mpm, adapt_now, k, b, flags)
+            k = [a + d for a, d in zip(k, entry[1])]
+            b += entry[2]
+            sa = flags[2]
+            lf = lf or is_mpm
+
     def _step_graph(self, ci, is_mpm, adapt_now):
         solver = self.solver
         topo = self.topology
         gver = (topo.cap_version, tuple(topo.n_tiles(l) > 0 for l in range(topo.levels)))
-        if self._graph_ver != gver:
+        fresh = self._graph_ver != gver
+        if fresh:
             self._graphs.clear()
             self._pool = None          # graphs of the old capacities freed with their pool
             self._graph_ver = gver
@@ -384,42 +466,15 @@ class CoupledSim:
         self.grid.sync_topology()
         self.grid.level0()
         self._ensure_host_status(adapt_now)
-        # particle sort: every sort_every steps; with the diagnostics overlap it
-        # runs at the end of the previous step beside the adapt pass (it only
-        # reads the particle rows the pass reads) and this step's P2G takes the
-        # sorted scratch as is
-        self._use_sorted = self._sorted_ahead
-        self._sort_now = (self.step_count % self.sort_every) == 0 and not self._use_sorted
-        self._sort_ahead = bool(self.overlap_diag and adapt_now and is_mpm and self.cadence == 1
-                                and self.sort_particles and len(self.particles)
-                                and (self.step_count + 1) % self.sort_every == 0)
-        key = (ci, tuple(k & 1 for k in solver.k), is_mpm, adapt_now, self._sort_now,
-               self._use_sorted, self._sort_ahead,
-               self.powder is not None and is_mpm and self.last_fields is not None)
+        if fresh and self.precapture_steps:
+            self._precapture(self.precapture_steps)
+        flags = self._sort_flags(self.step_count, self._sorted_ahead, is_mpm, adapt_now)
+        self._use_sorted, self._sort_now, self._sort_ahead = flags
+        key = self._key(ci, solver.k, is_mpm, adapt_now, flags, self.last_fields is not None)
         entry = self._graphs.get(key)
         if entry is None:
-            if self._pool is None:
-                self._pool = torch.cuda.graph_pool_handle()
-            k0, b0 = list(solver.k), self.pair.bounce
-            g = torch.cuda.CUDAGraph()
-            torch.cuda.synchronize()
-            n0 = L.TRACE.launches
-            tracing = L.TRACE.enabled
-            L.TRACE.enabled = False
-            try:
-                with torch.cuda.graph(g, pool=self._pool):
-                    self._device_step(ci, is_mpm, adapt_now)
-            finally:
-                L.TRACE.enabled = tracing
-            nk = L.TRACE.launches - n0
-            L.TRACE.launches = n0          # captured, not executed
-            dk = [a - b for a, b in zip(solver.k, k0)]
-            db = self.pair.bounce - b0
-            solver.k[:] = k0
-            self.pair.bounce = b0
-            entry = (g, dk, db, self.last_fields, nk)
-            self._graphs[key] = entry
-            self.graph_captures += 1
+            entry = self._capture(key, ci, is_mpm, adapt_now, list(solver.k), self.pair.bounce,
+                                  flags)
         g, dk, db, lf, nk = entry
         g.replay()
         self._sorted_ahead = self._sort_ahead
