@@ -1,0 +1,413 @@
+"""Slab decomposition of the coupled multi-level step over a static hierarchy
+(SURVEY.md §8(e) collectives (i), (ii), (iii), (v)).
+
+Each rank owns an x-slab (cut on the coarsest tile width) and keeps a local
+box = slab + one coarsest tile of ghost region per neighbour side
+(``slab_lbm.SlabMultiLevel``).  A local ``CoupledSim`` runs the reference's
+coupled cycle (coupling.py:448-481) with the same kernels, plus:
+
+  (i)   after every level-l stream / step / collide, the owned edge columns of
+        the level's write tree go to the neighbours' ghost columns;
+  (ii)  after P2G, the accumulator rows (mass, momentum, internal force, eta,
+        area, sum w m v) of the ghost region are added into the owners' edge
+        columns, and the completed edge rows are copied back into the ghost
+        region — so the exchange kernel (drag, grad eps, grid update) computes
+        the ghost cells near the cut exactly as their owner does, and G2P of
+        particles near the cut gathers correct grid velocities;
+  (iii) after the step, particles whose x left the slab move to the
+        neighbour (count, then payload);
+  (v)   the diagnostics row is reduced over ranks (sums; eps min).
+
+Block maintenance is not distributed (static hierarchy); the adapt pass
+would need the seed-bitmap OR (iv) and the global bitmaps on every rank.
+
+``ThreadExchanger`` runs the ranks as threads of one process on one GPU
+(tests); ``P2PExchanger`` is the torch.distributed (NCCL) version.
+"""
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+from .coupling import CoupledSim
+from .granular import Particles, _d3, _faces
+from .slab_lbm import SlabMultiLevel, exchange_columns
+from .solver import FIELD_FORCE, FIELD_TAU, MultiLevelSolver
+from .sparse_grid import TILE, dtype_code, moment_names
+
+
+class ThreadExchanger:
+    """Rank threads of one process: a shared mailbox and a barrier."""
+
+    def __init__(self, world):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.box = {}
+
+    def _post(self, rank, key, val):
+        self.box[(rank, key)] = val
+
+    def _sync(self):
+        torch.cuda.synchronize()
+        self.barrier.wait()
+
+    def columns(self, sl, edge_l, edge_r, ghost_l, ghost_r):
+        self._post(sl.rank, "cols", (edge_l.clone(), edge_r.clone()))
+        self._sync()
+        if ghost_l is not None:
+            ghost_l.copy_(self.box[(sl.left, "cols")][1])
+        if ghost_r is not None:
+            ghost_r.copy_(self.box[(sl.right, "cols")][0])
+        self._sync()
+
+    def ghost_reduce(self, sl, ghost_l, ghost_r, edge_l, edge_r):
+        self._post(sl.rank, "ghost", (None if ghost_l is None else ghost_l.clone(),
+                                       None if ghost_r is None else ghost_r.clone()))
+        self._sync()
+        if sl.left is not None:
+            edge_l.add_(self.box[(sl.left, "ghost")][1])
+        if sl.right is not None:
+            edge_r.add_(self.box[(sl.right, "ghost")][0])
+        self._sync()
+
+    def particles(self, sl, to_left, to_right):
+        self._post(sl.rank, "parts", (to_left, to_right))
+        self._sync()
+        got = []
+        if sl.left is not None:
+            got.append(self.box[(sl.left, "parts")][1])
+        if sl.right is not None and sl.right != sl.left:
+            got.append(self.box[(sl.right, "parts")][0])
+        elif sl.right is not None:
+            got.append(self.box[(sl.right, "parts")][0])
+        self._sync()
+        return got
+
+    def allreduce(self, sl, t, op):
+        self._post(sl.rank, "red", t.clone())
+        self._sync()
+        vals = [self.box[(r, "red")] for r in range(self.world)]
+        out = vals[0].clone()
+        for v in vals[1:]:
+            out = torch.minimum(out, v) if op == "min" else out + v
+        t.copy_(out)
+        self._sync()
+
+
+class P2PExchanger:
+    """torch.distributed point-to-point / all-reduce (NCCL between GPUs)."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def columns(self, sl, edge_l, edge_r, ghost_l, ghost_r):
+        key = ("c", edge_l.shape, edge_r.shape)
+        if key not in self._bufs:
+            self._bufs[key] = ([torch.empty_like(edge_l), torch.empty_like(edge_r)],
+                               [torch.empty_like(ghost_l) if ghost_l is not None else torch.empty_like(edge_l),
+                                torch.empty_like(ghost_r) if ghost_r is not None else torch.empty_like(edge_r)])
+        send, recv = self._bufs[key]
+        exchange_columns(edge_l, edge_r, ghost_l, ghost_r, sl.left, sl.right, send, recv)
+
+    def ghost_reduce(self, sl, ghost_l, ghost_r, edge_l, edge_r):
+        # send my ghost sums to their owners, receive theirs for my edges
+        recv_l = torch.empty_like(edge_l) if sl.left is not None else None
+        recv_r = torch.empty_like(edge_r) if sl.right is not None else None
+        ops = []
+        if sl.right is not None:
+            ops.append(dist.P2POp(dist.isend, ghost_r.contiguous(), sl.right))
+        if sl.left is not None:
+            ops.append(dist.P2POp(dist.isend, ghost_l.contiguous(), sl.left))
+        if sl.left is not None:
+            ops.append(dist.P2POp(dist.irecv, recv_l, sl.left))
+        if sl.right is not None:
+            ops.append(dist.P2POp(dist.irecv, recv_r, sl.right))
+        for q in dist.batch_isend_irecv(ops):
+            q.wait()
+        if recv_l is not None:
+            edge_l.add_(recv_l)
+        if recv_r is not None:
+            edge_r.add_(recv_r)
+
+    def particles(self, sl, to_left, to_right):
+        got = []
+        for send_to, payload, recv_from in ((sl.right, to_right, sl.left), (sl.left, to_left, sl.right)):
+            n_out = torch.tensor([payload.shape[1] if payload is not None else 0], dtype=torch.int64,
+                                 device=payload.device if payload is not None else "cuda")
+            n_in = torch.zeros_like(n_out)
+            ops = []
+            if send_to is not None:
+                ops.append(dist.P2POp(dist.isend, n_out, send_to))
+            if recv_from is not None:
+                ops.append(dist.P2POp(dist.irecv, n_in, recv_from))
+            for q in dist.batch_isend_irecv(ops):
+                q.wait()
+            rows = payload.shape[0]
+            buf = torch.empty((rows, int(n_in.item())), dtype=payload.dtype, device=payload.device)
+            ops = []
+            if send_to is not None and payload.shape[1]:
+                ops.append(dist.P2POp(dist.isend, payload.contiguous(), send_to))
+            if recv_from is not None and buf.shape[1]:
+                ops.append(dist.P2POp(dist.irecv, buf, recv_from))
+            if ops:
+                for q in dist.batch_isend_irecv(ops):
+                    q.wait()
+            got.append(buf)
+        return got
+
+    def allreduce(self, sl, t, op):
+        dist.all_reduce(t, op=dist.ReduceOp.MIN if op == "min" else dist.ReduceOp.SUM)
+
+
+class _SlabSolver(MultiLevelSolver):
+    """Level steps over the owned slot range; (i) after every write."""
+
+    slab = None
+
+    def _level_call(self, level, src, dst, mode, cp=None):
+        sl = self.slab
+        if self.topology.lv[level].cap == 0:
+            return
+        self._refresh_tables()
+        a, b = sl.ranges[level]["owned"]
+        if b > a:
+            cp = cp or self._collide_struct(level)
+            L.check(L.lib().mlbm_level_step(L.C.byref(sl._owned_struct(level)),
+                                            L.fields(dst_data(src)), L.fields(dst_data(dst)),
+                                            self.dcode, mode, L.C.byref(cp), L.C.byref(self._bc),
+                                            L.ptr(self._err), L.stream_handle()), "level_step")
+        self.launches += 1
+        sl.owner.exchange_level(level, dst)
+
+
+def dst_data(a):
+    return a.data if hasattr(a, "data") and not torch.is_tensor(a) else a
+
+
+class SlabCoupled(CoupledSim):
+    """One rank of the slab-decomposed coupled step (static hierarchy)."""
+
+    def __init__(self, ref: CoupledSim, rank: int, world: int, exchanger):
+        self.rank, self.world, self.xch = rank, world, exchanger
+        topo = ref.topology
+        d = topo.d
+        per = tuple(bool(p) for p in topo.periodic) + (True,) * (3 - d)
+        faces = dict(ref.solver.boundaries.faces)
+        self.sl = SlabMultiLevel(topo.finest_cells, topo.levels, topo.tile_set(), rank, world,
+                                 ref.solver.level_params.tau0, dtype=ref.dtype, periodic=per,
+                                 params=ref.solver.params, level_params=ref.solver.level_params,
+                                 faces=faces, solver_cls=_SlabSolver)
+        sl = self.sl
+        sl.owner = self
+        sl.solver.slab = sl
+        # fields of the reference state, by coordinates, into both local trees
+        for l in range(topo.levels):
+            if not sl.topology.n_tiles(l):
+                continue
+            gkey = {tuple(c): i for i, c in enumerate(topo.cell_coords(l).tolist())}
+            lc = sl.topology.cell_coords(l).copy()
+            lc[:, 0] = np.mod(lc[:, 0] + (sl.x0 >> l), topo.finest_cells[0] >> l)
+            idx = torch.as_tensor([gkey[tuple(c)] for c in lc.tolist()], device=topo.device)
+            nloc = sl.topology.cell_count(l)
+            for t in range(2):
+                sl.pair.trees[t].levels[l].data[:, :nloc].copy_(
+                    ref.pair.trees[t].levels[l].data[:, :topo.cell_count(l)][:, idx])
+        x0, x1 = sl.part.slab(rank)
+        self.x_lo, self.x_hi = x0, x1
+        p = ref.particles
+        gx = p.x.cpu().numpy()
+        own = (sl.part.owner(gx[:, 0]) == rank)
+        part = self._make_particles(ref, torch.as_tensor(np.nonzero(own)[0], device=topo.device))
+        super().__init__(sl.solver, part, ref.material, sediment_gravity=ref.sediment_gravity,
+                         drag=ref.drag_params, powder=None, adaptor=None,
+                         unit_scale=ref.unit_scale)
+        self.drag_params.d_p = ref.drag_params.d_p
+        self._global_active = len(ref.particles) > 0
+        self.use_graphs = False
+        self.sort_particles = False
+        self.step_count = ref.step_count
+        self.solver.k[:] = list(ref.solver.k)
+        self.pair.bounce = ref.pair.bounce
+
+    @property
+    def coupling_active(self) -> bool:
+        # every rank runs the hook when the global particle set is non-empty
+        # (the exchanges inside it pair up across ranks)
+        return getattr(self, "_global_active", len(self.particles) > 0)
+
+    # -- particles ----------------------------------------------------------------
+    def _make_particles(self, ref, idx):
+        p = ref.particles
+        n = int(idx.numel())
+        out = Particles(n, p.d, p.dtype, p.device)
+        gx = p._orig(p.xd)[:, idx]
+        gx[0] -= self.sl.x0
+        out.xd.copy_(gx)
+        out.pd.copy_(p._orig(p.pd)[:, idx])
+        out.pid.copy_(idx.to(torch.int32))
+        return out
+
+    def _local_x_range(self):
+        return self.x_lo - self.sl.x0, self.x_hi - self.sl.x0
+
+    # -- (i) per-level ghost columns ----------------------------------------------------
+    def exchange_level(self, level, dst):
+        sl = self.sl
+        if self.world == 1:
+            return
+        nm = len(moment_names(sl.d))
+        a = dst_data(dst)
+        r = sl.ranges[level]
+        lo_l, hi_l = sl.cells(level, r["edge_l"])
+        lo_r, hi_r = sl.cells(level, r["edge_r"])
+        glo_l, ghi_l = sl.cells(level, r["ghost_l"])
+        glo_r, ghi_r = sl.cells(level, r["ghost_r"])
+        self.xch.columns(sl, a[:nm, lo_l:hi_l], a[:nm, lo_r:hi_r],
+                         a[:nm, glo_l:ghi_l] if sl.left is not None else None,
+                         a[:nm, glo_r:ghi_r] if sl.right is not None else None)
+
+    # -- the coupling hook with (ii) ------------------------------------------------------
+    def _exchange(self, solver):
+        r, w = solver.roles(0)
+        grid = self.grid
+        grid.sync_topology()
+        p = self.particles
+        lib = L.lib()
+        s = L.stream_handle()
+        dcode = dtype_code(self.dtype)
+        mat = self.material
+        lv0 = grid.level0()
+        grid.clear()
+        n = len(p)
+        ps = p.pd.stride(0)
+        if n:
+            L.check(lib.mlbm_p2g(L.C.byref(lv0), n, L.ptr(p.xd), L.ptr(p.pd), ps, mat.lam, mat.mu,
+                                 mat.alpha, L.ptr(grid.ras), grid.ras.stride(0), dcode, 0,
+                                 L.ptr(grid._err), s), "p2g")
+        if self.world > 1:
+            sl = self.sl
+            nacc = grid.R["nacc"]
+            rr = sl.ranges[0]
+            lo_l, hi_l = sl.cells(0, rr["edge_l"])
+            lo_r, hi_r = sl.cells(0, rr["edge_r"])
+            glo_l, ghi_l = sl.cells(0, rr["ghost_l"])
+            glo_r, ghi_r = sl.cells(0, rr["ghost_r"])
+            ras = grid.ras
+            gl = ras[:nacc, glo_l:ghi_l] if sl.left is not None else None
+            gr = ras[:nacc, glo_r:ghi_r] if sl.right is not None else None
+            el, er = ras[:nacc, lo_l:hi_l], ras[:nacc, lo_r:hi_r]
+            self.xch.ghost_reduce(sl, gl, gr, el, er)            # (ii) sums to owners
+            self.xch.columns(sl, el, er, gl, gr)                 # completed rows back
+        sp = solver.params
+        L.check(lib.mlbm_exchange(L.C.byref(lv0), L.fields(solver.arrays(w, 0).data),
+                                  L.fields(solver.arrays(r, 0).data),
+                                  L.fields(self.pair.trees[0].levels[0].data),
+                                  L.fields(self.pair.trees[1].levels[0].data),
+                                  L.ptr(grid.ras), grid.ras.stride(0), float(sp.eps_min),
+                                  float(solver.level_params.nu(0)),
+                                  float(self.drag_params.d_p or 1.0), float(self.drag_params.re_min),
+                                  float(self.cadence), float(sp.rho0), _d3(sp.gravity, self.d),
+                                  _d3(self.sediment_gravity, self.d), _faces(solver.boundaries),
+                                  float(mat.floor_friction), 1, dcode, s), "exchange")
+        if n:
+            L.check(lib.mlbm_g2p(L.C.byref(lv0), n, L.ptr(p.xd), L.ptr(p.xd), L.ptr(p.pd),
+                                 L.ptr(p.pd), L.ptr(None), L.ptr(None), ps, mat.lam, mat.mu,
+                                 mat.alpha, L.ptr(grid.ras), grid.ras.stride(0),
+                                 float(self.cadence), 1, dcode, L.ptr(self._counters),
+                                 L.ptr(grid._err), s), "g2p")
+        from .coupling import CouplingFields
+        self.last_fields = CouplingFields(grid, self.pair.trees[0].levels[0])
+        return FIELD_FORCE, FIELD_TAU
+
+    # -- (iii) migration, (v) diagnostics ----------------------------------------------
+    def _migrate(self):
+        if self.world == 1:
+            return
+        p = self.particles
+        lo, hi = self._local_x_range()
+        x = p.xd[0]
+        gx = self.sl.global_cells[0]
+        go_l = x < lo
+        go_r = x >= hi
+        keep = ~(go_l | go_r)
+
+        def pack(mask):
+            if self.sl.left is None and mask is go_l or self.sl.right is None and mask is go_r:
+                mask = torch.zeros_like(mask)
+            xs = p.xd[:, mask].clone()
+            xs[0] += self.sl.x0                                    # global x
+            xs[0] = torch.remainder(xs[0], gx)
+            rows = torch.cat([xs, p.pd[:, mask].double(), p.pid[mask].double()[None]], 0)
+            return rows
+        got = self.xch.particles(self.sl, pack(go_l), pack(go_r))
+        parts = [torch.cat([p.xd[:, keep], p.pd[:, keep].double(), p.pid[keep].double()[None]], 0)]
+        for g in got:
+            g = g.clone()
+            g[0] = g[0] - self.sl.x0
+            # wrapped arrivals (periodic x): bring into the local box
+            g[0] = torch.where(g[0] < 0, g[0] + gx, g[0])
+            g[0] = torch.where(g[0] >= self.sl.topology.finest_cells[0], g[0] - gx, g[0])
+            parts.append(g)
+        allp = torch.cat(parts, 1)
+        d, R = p.d, p.pd.shape[0]
+        out = Particles(allp.shape[1], d, p.dtype, p.device)
+        out.xd.copy_(allp[:d])
+        out.pd.copy_(allp[d:d + R].to(p.dtype))
+        out.pid.copy_(allp[d + R].round().to(torch.int32))
+        self.particles = out
+
+    def _record_diagnostics(self):
+        solver = self.solver
+        d = self.d
+        sl = self.sl
+        lib = L.lib()
+        s = L.stream_handle()
+        dcode = dtype_code(self.dtype)
+        out = self._diag_buf
+        out.zero_()
+        out[d + 1:d + 2].fill_(1.0)
+        for l in range(self.topology.levels):
+            a, b = sl.ranges[l]["owned"]
+            if b <= a:
+                continue
+            lw = solver.last_roles(l)[1] if solver.k[l] else 0
+            arr = solver.arrays(lw, l)
+            st = L.Level.from_buffer_copy(solver._structs[l])
+            st.counts = None
+            st.first = a
+            st.n_tiles = b
+            L.check(lib.mlbm_diag_level(L.C.byref(st), L.fields(arr.data),
+                                        float((1 << d) ** l), dcode, L.ptr(out[:d + 2]), s),
+                    "diag_level")
+        p = self.particles
+        g = self.grid
+        a, b = sl.cells(0, sl.ranges[0]["owned"])
+        n0 = (b - a) if self.last_fields is not None else 0
+        ras = g.ras[:, a:]
+        L.check(lib.mlbm_diag_particles(d, len(p), L.ptr(p.pd), p.pd.stride(0), L.ptr(ras),
+                                        g.ras.stride(0), n0, L.ptr(None), dcode,
+                                        L.ptr(out[d + 2:]), s), "diag_particles")
+        if self.world > 1:
+            emin = out[d + 1:d + 2].clone()
+            out[d + 1] = 0.0
+            self.xch.allreduce(sl, out, "sum")
+            self.xch.allreduce(sl, emin, "min")
+            out[d + 1:d + 2].copy_(emin)
+
+    def step(self):
+        super().step()
+        self._migrate()
+
+    # -- gather for tests ---------------------------------------------------------------
+    def owned_particles(self):
+        """(pid, global x, v) of the owned particles."""
+        p = self.particles
+        x = p.xd.t().clone()
+        x[:, 0] += self.sl.x0
+        x[:, 0] = torch.remainder(x[:, 0], self.sl.global_cells[0])
+        v = p.pd[p.R["v"]:p.R["v"] + p.d].t()
+        return p.pid.cpu().numpy(), x.cpu().numpy(), v.double().cpu().numpy()

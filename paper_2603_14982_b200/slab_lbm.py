@@ -206,7 +206,8 @@ class SlabMultiLevel:
     inputs or are overwritten before use)."""
 
     def __init__(self, global_cells, levels, global_tiles, rank, world, tau0,
-                 dtype=torch.float64, periodic=(True, True, True), init=None, device=None):
+                 dtype=torch.float64, periodic=(True, True, True), init=None, device=None,
+                 params=None, level_params=None, faces=None, solver_cls=None):
         self.global_cells = tuple(int(v) for v in global_cells)
         self.d = len(self.global_cells)
         self.levels = levels
@@ -234,14 +235,25 @@ class SlabMultiLevel:
                     tiles.add((l, lx // tw) + tuple(c[1:]) + (e[-1],))
         self.topology.set_tile_set(sorted(tiles))
         self.pair = PingPongPair(self.topology, dtype)
-        self.params = SolverParams(levels=levels, h3_xyz=H3_XYZ_HERMITE)
-        self.level_params = LevelParams(levels, tau0)
-        faces = {}
+        self.params = params or SolverParams(levels=levels, h3_xyz=H3_XYZ_HERMITE)
+        self.level_params = level_params or LevelParams(levels, tau0)
+        lf = {}
         for a, ax in enumerate("xyz"[:self.d]):
             kind = "periodic" if per_local[a] else "wall"
-            faces[ax + "_min"] = faces[ax + "_max"] = kind
-        self.solver = MultiLevelSolver(self.topology, self.pair, self.params, self.level_params,
-                                       BoundarySpec(faces=faces, dim=self.d))
+            lf[ax + "_min"] = lf[ax + "_max"] = kind
+        if faces is not None:
+            # the scene's faces; x sides facing a neighbour rank become walls of
+            # the local box (their ghost cells are never stepped)
+            lf = dict(faces)
+            if world > 1:
+                if self.left is not None or lf.get("x_min") == "periodic":
+                    lf["x_min"] = "wall"
+                if self.right is not None or lf.get("x_max") == "periodic":
+                    lf["x_max"] = "wall"
+        self.faces = lf
+        cls = solver_cls or MultiLevelSolver
+        self.solver = cls(self.topology, self.pair, self.params, self.level_params,
+                          BoundarySpec(faces=lf, dim=self.d))
         self.solver.check_errors = False
         # per level: owned slot range and the slot ranges of the edge / ghost columns
         self.ranges = []

@@ -1,0 +1,87 @@
+"""Slab decomposition of the coupled multi-level step (static hierarchy) on
+one GPU: rank threads exchange ghost columns, P2G ghost sums, particles and
+the diagnostics row through a barrier mailbox (the same calls the NCCL path
+makes) and must reproduce the single-domain run: particles by id and owned
+fields within fp64 atomic-order noise, diagnostics row likewise."""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import scenes as S
+
+pytestmark = pytest.mark.gpu
+B = pytest.importorskip("paper_2603_14982_b200")
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _ref(scene):
+    from paper_2603_14982_b200.harness import build_scene, validate_scene
+    sim = build_scene(validate_scene(scene))
+    sim.adaptor = None          # static hierarchy (the one built around the particles)
+    sim.use_graphs = False
+    sim.sort_particles = False
+    return sim
+
+
+@pytest.mark.parametrize("scene,world,steps", [(S.COLUMN_3D_SMALL, 2, 6),
+                                               (S.SANDSTORM_3D_SMALL, 2, 6)])
+def test_coupled_slabs_equal_single_domain(scene, world, steps):
+    _need_gpu()
+    from paper_2603_14982_b200.slab_coupled import SlabCoupled, ThreadExchanger
+    ref = _ref(scene)
+    base = _ref(scene)                 # identical initial state for the slabs
+    xch = ThreadExchanger(world)
+    ranks = [SlabCoupled(base, r, world, xch) for r in range(world)]
+    errs = []
+
+    def run(sim):
+        try:
+            torch.cuda.set_device(0)
+            for _ in range(steps):
+                sim.step()
+        except BaseException as e:      # noqa: BLE001
+            errs.append(e)
+            xch.barrier.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in ranks]
+    for t in th:
+        t.start()
+    for _ in range(steps):
+        ref.step()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    torch.cuda.synchronize()
+    # particles by id
+    rx = ref.particles.x.cpu().numpy()
+    rv = ref.particles.v.cpu().numpy()
+    seen = 0
+    for r in ranks:
+        pid, x, v = r.owned_particles()
+        seen += len(pid)
+        assert np.abs(x - rx[pid]).max() <= 1e-10, r.rank
+        assert np.abs(v - rv[pid]).max() <= 1e-10, r.rank
+    assert seen == len(rx)
+    # owned level-0 moments
+    from paper_2603_14982_b200.sparse_grid import moment_names
+    wi = ref.solver.last_roles(0)[1]
+    ga = ref.solver.arrays(wi, 0)
+    gkey = {tuple(c): i for i, c in enumerate(ref.topology.cell_coords(0).tolist())}
+    for r in ranks:
+        for name in moment_names(ref.d):
+            c2, got = r.sl.owned_cells(r.solver.last_roles(0)[1], 0, name)
+            want = ga[name].cpu().numpy()[[gkey[tuple(c)] for c in c2.tolist()]]
+            assert np.abs(got - want).max() <= 1e-10, (name, r.rank)
+    # diagnostics row (reduced over ranks)
+    dr = ref.diagnostics[-1]
+    for r in ranks:
+        dd = r.diagnostics[-1]
+        assert np.allclose(dd.fluid_mom, dr.fluid_mom, rtol=1e-9, atol=1e-12)
+        assert np.allclose(dd.sediment_mom, dr.sediment_mom, rtol=1e-9, atol=1e-12)
+        assert abs(dd.eps_min - dr.eps_min) <= 1e-12
