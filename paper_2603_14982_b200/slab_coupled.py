@@ -33,11 +33,12 @@ import torch
 import torch.distributed as dist
 
 from . import _lib as L
+from .adapt import GridAdaptor, RefineDriver
 from .coupling import CoupledSim
 from .granular import Particles, _d3, _faces
 from .slab_lbm import SlabMultiLevel, exchange_columns
 from .solver import FIELD_FORCE, FIELD_TAU, MultiLevelSolver
-from .sparse_grid import TILE, dtype_code, moment_names
+from .sparse_grid import TILE, Topology, dtype_code, moment_names
 
 
 class ThreadExchanger:
@@ -93,7 +94,8 @@ class ThreadExchanger:
         vals = [self.box[(r, "red")] for r in range(self.world)]
         out = vals[0].clone()
         for v in vals[1:]:
-            out = torch.minimum(out, v) if op == "min" else out + v
+            out = (torch.minimum(out, v) if op == "min" else
+                   torch.maximum(out, v) if op == "max" else out + v)
         t.copy_(out)
         self._sync()
 
@@ -160,7 +162,8 @@ class P2PExchanger:
         return got
 
     def allreduce(self, sl, t, op):
-        dist.all_reduce(t, op=dist.ReduceOp.MIN if op == "min" else dist.ReduceOp.SUM)
+        dist.all_reduce(t, op={"min": dist.ReduceOp.MIN, "max": dist.ReduceOp.MAX}.get(
+            op, dist.ReduceOp.SUM))
 
 
 class _SlabSolver(MultiLevelSolver):
@@ -229,6 +232,21 @@ class SlabCoupled(CoupledSim):
         self._global_active = len(ref.particles) > 0
         self.use_graphs = False
         self.sort_particles = False
+        # (iv) block maintenance: every rank keeps the GLOBAL kind grids and
+        # adapt state and runs the pass redundantly on OR-reduced seeds; the
+        # new global kinds are cropped to the local box and the local
+        # topology is rebuilt / migrated with the same kernels
+        self.gad = None
+        if ref.adaptor is not None:
+            self.gtopo = Topology(topo.finest_cells, topo.levels, periodic=topo.periodic)
+            self.gtopo.set_tile_set(sorted(topo.tile_set()))
+            self.gad = GridAdaptor(self.gtopo, ref.solver.level_params,
+                                   ref.adaptor.rescale_convention)
+            for a, b in zip(self.gad._streak, ref.adaptor._streak):
+                a.copy_(b)
+            self.lad = GridAdaptor(sl.topology, ref.solver.level_params,
+                                   ref.adaptor.rescale_convention)
+            self.static_global = ref.static_tiles
         self.step_count = ref.step_count
         self.solver.k[:] = list(ref.solver.k)
         self.pair.bounce = ref.pair.bounce
@@ -398,9 +416,80 @@ class SlabCoupled(CoupledSim):
             self.xch.allreduce(sl, emin, "min")
             out[d + 1:d + 2].copy_(emin)
 
-    def step(self):
-        super().step()
+    def _step_eager(self, ci, is_mpm, adapt_now):
+        """coupling.py:448-481 on the slab: cycle (with (i)/(ii) inside),
+        migration (iii), global block maintenance (iv), reduced diagnostics (v)."""
+        solver = self.solver
+        cycle = solver._schedule[ci]
+        if is_mpm:
+            solver.run_cycle(cycle, hook=self._exchange)
+        elif self.coupling_active:
+            solver.run_cycle(cycle, hook=self._held)
+        else:
+            solver.run_cycle(cycle)
+        if self.coupling_active and is_mpm:
+            self.grid.raise_pending()
         self._migrate()
+        if self.gad is not None and self.coupling_active and self.step_count % self.cadence == 0:
+            self._adapt()
+        self._record_diagnostics()
+        self._push_diag_row(self._diag_buf.cpu().numpy())
+
+    # -- (iv) block maintenance -----------------------------------------------------
+    def _adapt(self):
+        gad, gtopo, sl = self.gad, self.gtopo, self.sl
+        lib = L.lib()
+        s = L.stream_handle()
+        d = self.d
+        p = self.particles
+        seeds = gad._seeds
+        seeds.zero_()
+        if len(p):
+            gx = p.xd.clone()
+            gx[0] = torch.remainder(gx[0] + sl.x0, sl.global_cells[0])
+            t0 = (L.C.c_int32 * 3)(*gtopo.tile_grid(0))
+            L.check(lib.mlbm_seed_tiles(d, len(p), L.ptr(gx), gx.stride(0), 1, t0,
+                                        L.ptr(seeds), L.ptr(gad._err), s), "seed_tiles")
+        if self.world > 1:
+            t = seeds.to(torch.int32)
+            self.xch.allreduce(sl, t, "max")
+            seeds.copy_(t.to(torch.uint8))
+        gad._seeds_dirty = False
+        # the fused pass with no particles: seeds are preset, cleared at its end
+        gad.plan_device(RefineDriver(static_tiles=self.static_global, levels=gtopo.levels))
+        status = gad._status.cpu().numpy()
+        Lv = gtopo.levels
+        changed = [l for l in range(Lv) if status[l]]
+        if not changed:
+            return
+        self.topology_changes += 1
+        # global kinds (no fields on the global topology)
+        gtopo.rebuild({l: gad._new[l].clone() for l in changed})
+        # crop to the local box (ghosts wrap periodically) and rebuild locally
+        lt = sl.topology
+        lchanged, counts, fresh = [], [0] * Lv, [0] * Lv
+        for l in range(Lv):
+            g = gtopo.tile_grid(l)
+            tw = TILE << l
+            cols = (torch.arange(lt.tile_grid(l)[0], device=lt.device) + sl.x0 // tw) % g[0]
+            new = gtopo.lv[l].kind.view(g)[cols].reshape(-1)
+            old = lt.lv[l].kind
+            self.lad._new[l].copy_(new)
+            if not torch.equal(new, old):
+                lchanged.append(l)
+            nz = new != 0
+            counts[l] = int(nz.sum().item())
+            fresh[l] = int((nz & (old == 0)).sum().item())
+        if lchanged:
+            self.lad._prepare(lchanged, self.pair, counts, [1] * Lv)()
+            self.solver._refresh_tables()
+            self.grid.sync_topology()
+            sl.compute_ranges()
+        # fresh ghost tiles hold locally initialised values: refresh both trees'
+        # ghost columns from the owners (every rank: the global change is common)
+        for l in range(Lv):
+            for t in range(2):
+                self.exchange_level(l, self.pair.trees[t].levels[l])
 
     # -- gather for tests ---------------------------------------------------------------
     def owned_particles(self):

@@ -255,9 +255,19 @@ class SlabMultiLevel:
         self.solver = cls(self.topology, self.pair, self.params, self.level_params,
                           BoundarySpec(faces=lf, dim=self.d))
         self.solver.check_errors = False
-        # per level: owned slot range and the slot ranges of the edge / ghost columns
+        self.local_cells = local
+        self.compute_ranges()
+        if init is not None:
+            self.set_fields(init)
+        self._lv = {}
+
+    def compute_ranges(self):
+        """Per level: owned slot range and the slot ranges of the edge / ghost
+        columns (slots are x-major, so each is contiguous); re-run after a
+        topology change."""
+        local = self.local_cells
         self.ranges = []
-        for l in range(levels):
+        for l in range(self.levels):
             xs = self.topology.tile_coords(l)[:, 0] if self.topology.n_tiles(l) else np.zeros(0, int)
             wl = (self.gl // (TILE << l), self.gr // (TILE << l))
             ncol = local[0] // (TILE << l)
@@ -268,8 +278,6 @@ class SlabMultiLevel:
                 "ghost_l": (0, a), "owned": (a, b), "ghost_r": (b, len(xs)),
                 "edge_l": (a, a + cnt(wl[0], 2 * wl[0])) if wl[0] else (a, a),
                 "edge_r": (b - cnt(ncol - 2 * wl[1], ncol - wl[1]), b) if wl[1] else (b, b)})
-        if init is not None:
-            self.set_fields(init)
         self._lv = {}
 
     def set_fields(self, fn):

@@ -75,6 +75,16 @@ SANDSTORM_3D_SMALL = {  # config 3 (C3) at test size: three levels, inflow, z pe
     "particles": {"blocks": [[16.0, 2.0, 0.0, 44.0, 7.0, 16.0]], "per_cell": 2},
     "runtime": {"seed": 9}}
 
+# dispersed cloud forcing per-step block churn across slab cuts (config 5 at test size)
+CLOUD_3D_SMALL = {
+    "domain": {"cells": [96, 32, 32], "levels": 2},
+    "fluid": {"tau0": 1.8, "eps_min": 0.5, "gravity": [0.0, -3e-4, 0.0]},
+    "boundaries": {"y_min": "wall", "y_max": "wall"},
+    "materials": {"density_ratio": 10.0, "E": 0.08},
+    "particles": {"blocks": [[26.0, 12.0, 8.0, 38.0, 24.0, 24.0],
+                             [58.0, 14.0, 10.0, 70.0, 26.0, 22.0]], "per_cell": 1},
+    "runtime": {"seed": 13}}
+
 POWDER_3D_SMALL = {     # config 4 ingredients at test size (powder on, solids)
     "domain": {"cells": [32, 32, 16], "levels": 1},
     "fluid": {"tau0": 1.8, "eps_min": 0.5, "gravity": [0.0, -5e-5, 0.0]},

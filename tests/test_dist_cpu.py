@@ -239,3 +239,49 @@ def test_slab_column_exchange(world):
         base = np.arange(24, dtype=float).reshape(4, 6)
         assert np.array_equal(gl, (base + 100 * lft)[:, 3:]), r      # left neighbour's high edge
         assert np.array_equal(gr, (base + 100 * rgt)[:, :3]), r      # right neighbour's low edge
+
+
+def case_p2p_exchanger(rank):
+    """slab_coupled.P2PExchanger with gloo on CPU tensors: columns, ghost
+    sums, particle payloads of ragged sizes, all-reduces."""
+    from types import SimpleNamespace
+    from paper_2603_14982_b200.slab_coupled import P2PExchanger
+    world = dist.get_world_size()
+    sl = SimpleNamespace(rank=rank, left=(rank - 1) % world, right=(rank + 1) % world)
+    x = P2PExchanger()
+    base = torch.arange(12, dtype=torch.float64).reshape(3, 4) + 100 * rank
+    el, er = base[:, :2].clone(), base[:, 2:].clone()
+    gl, gr = torch.zeros(3, 2, dtype=torch.float64), torch.zeros(3, 2, dtype=torch.float64)
+    x.columns(sl, el, er, gl, gr)
+    out = {"gl": gl.numpy().copy(), "gr": gr.numpy().copy()}
+    ghost_l = torch.full((3, 2), 1.0 + rank, dtype=torch.float64)
+    ghost_r = torch.full((3, 2), 10.0 + rank, dtype=torch.float64)
+    e_l, e_r = torch.zeros(3, 2, dtype=torch.float64), torch.zeros(3, 2, dtype=torch.float64)
+    x.ghost_reduce(sl, ghost_l, ghost_r, e_l, e_r)
+    out["el"], out["er"] = e_l.numpy().copy(), e_r.numpy().copy()
+    to_l = torch.full((5, rank + 1), -float(rank), dtype=torch.float64)
+    to_r = torch.full((5, 2 * rank + 1), float(rank), dtype=torch.float64)
+    got = x.particles(sl, to_l, to_r)
+    out["got"] = [g.numpy().copy() for g in got]
+    t = torch.tensor([float(rank), 5.0 - rank], dtype=torch.float64)
+    x.allreduce(sl, t, "sum")
+    m = torch.tensor([float(rank)], dtype=torch.float64)
+    x.allreduce(sl, m, "max")
+    out["sum"], out["max"] = t.numpy().copy(), m.numpy().copy()
+    return out
+
+
+def test_p2p_exchanger_gloo():
+    world = 3
+    out = run_world(case_p2p_exchanger, world)
+    for r in range(world):
+        lft, rgt = (r - 1) % world, (r + 1) % world
+        base = lambda k: np.arange(12, dtype=float).reshape(3, 4) + 100 * k   # noqa: E731
+        o = out[r]
+        assert np.array_equal(o["gl"], base(lft)[:, 2:])
+        assert np.array_equal(o["gr"], base(rgt)[:, :2])
+        assert np.all(o["el"] == 10.0 + lft) and np.all(o["er"] == 1.0 + rgt)
+        # got[0]: from the left (its to_right payload), got[1]: from the right (its to_left)
+        assert o["got"][0].shape == (5, 2 * lft + 1) and np.all(o["got"][0] == lft)
+        assert o["got"][1].shape == (5, rgt + 1) and np.all(o["got"][1] == -rgt)
+        assert np.array_equal(o["sum"], [0 + 1 + 2, 15 - 3]) and o["max"][0] == 2

@@ -20,22 +20,33 @@ def _need_gpu():
         pytest.skip("no CUDA device")
 
 
-def _ref(scene):
+def _ref(scene, adapt):
     from paper_2603_14982_b200.harness import build_scene, validate_scene
     sim = build_scene(validate_scene(scene))
-    sim.adaptor = None          # static hierarchy (the one built around the particles)
+    if not adapt:
+        sim.adaptor = None      # static hierarchy (the one built around the particles)
     sim.use_graphs = False
     sim.sort_particles = False
     return sim
 
 
-@pytest.mark.parametrize("scene,world,steps", [(S.COLUMN_3D_SMALL, 2, 6),
-                                               (S.SANDSTORM_3D_SMALL, 2, 6)])
-def test_coupled_slabs_equal_single_domain(scene, world, steps):
+@pytest.mark.parametrize("scene,world,steps,adapt", [
+    (S.COLUMN_3D_SMALL, 2, 6, False), (S.SANDSTORM_3D_SMALL, 2, 6, False),
+    (S.COLUMN_3D_SMALL, 2, 8, True), (S.SANDSTORM_3D_SMALL, 2, 8, True),
+    (S.CLOUD_3D_SMALL, 3, 14, True)])
+def test_coupled_slabs_equal_single_domain(scene, world, steps, adapt):
     _need_gpu()
     from paper_2603_14982_b200.slab_coupled import SlabCoupled, ThreadExchanger
-    ref = _ref(scene)
-    base = _ref(scene)                 # identical initial state for the slabs
+    ref = _ref(scene, adapt)
+    base = _ref(scene, adapt)          # identical initial state for the slabs
+    if scene is S.CLOUD_3D_SMALL:
+        # the two clouds drift towards each other at 0.3 cells/step: tiles are
+        # created / retired every few steps and particles cross the cuts
+        for sim in (ref, base):
+            x = sim.particles.x.cpu().numpy()
+            v = np.zeros_like(x)
+            v[:, 0] = np.where(x[:, 0] < 48.0, 0.3, -0.3)
+            sim.particles.v = v
     xch = ThreadExchanger(world)
     ranks = [SlabCoupled(base, r, world, xch) for r in range(world)]
     errs = []
@@ -78,6 +89,12 @@ def test_coupled_slabs_equal_single_domain(scene, world, steps):
             c2, got = r.sl.owned_cells(r.solver.last_roles(0)[1], 0, name)
             want = ga[name].cpu().numpy()[[gkey[tuple(c)] for c in c2.tolist()]]
             assert np.abs(got - want).max() <= 1e-10, (name, r.rank)
+    if adapt:
+        # block maintenance: every rank holds the same global hierarchy
+        for r in ranks:
+            assert r.gtopo.tile_set() == ref.topology.tile_set()
+        if scene is S.CLOUD_3D_SMALL:      # the churn scene must exercise rebuilds
+            assert ref.topology_changes > 0
     # diagnostics row (reduced over ranks)
     dr = ref.diagnostics[-1]
     for r in ranks:
