@@ -101,12 +101,30 @@ class ThreadExchanger:
 
 
 class P2PExchanger:
-    """torch.distributed point-to-point / all-reduce (NCCL between GPUs)."""
+    """torch.distributed point-to-point / all-reduce (NCCL between GPUs).
+    With a gloo process group (CPU transport) CUDA tensors are staged through
+    host memory, so the same multi-process code path runs on one GPU."""
 
     def __init__(self):
         self._bufs = {}
+        self.stage = dist.is_initialized() and dist.get_backend() == "gloo"
+
+    def _h(self, t):
+        return t.cpu() if (self.stage and t is not None and t.is_cuda) else t
 
     def columns(self, sl, edge_l, edge_r, ghost_l, ghost_r):
+        if self.stage:
+            gl = self._h(ghost_l).clone() if ghost_l is not None else None
+            gr = self._h(ghost_r).clone() if ghost_r is not None else None
+            send = [torch.empty_like(self._h(edge_l)), torch.empty_like(self._h(edge_r))]
+            recv = [torch.empty_like(gl if gl is not None else send[0]),
+                    torch.empty_like(gr if gr is not None else send[1])]
+            exchange_columns(self._h(edge_l), self._h(edge_r), gl, gr, sl.left, sl.right, send, recv)
+            if ghost_l is not None:
+                ghost_l.copy_(gl)
+            if ghost_r is not None:
+                ghost_r.copy_(gr)
+            return
         key = ("c", edge_l.shape, edge_r.shape)
         if key not in self._bufs:
             self._bufs[key] = ([torch.empty_like(edge_l), torch.empty_like(edge_r)],
@@ -117,13 +135,13 @@ class P2PExchanger:
 
     def ghost_reduce(self, sl, ghost_l, ghost_r, edge_l, edge_r):
         # send my ghost sums to their owners, receive theirs for my edges
-        recv_l = torch.empty_like(edge_l) if sl.left is not None else None
-        recv_r = torch.empty_like(edge_r) if sl.right is not None else None
+        recv_l = torch.empty_like(self._h(edge_l)) if sl.left is not None else None
+        recv_r = torch.empty_like(self._h(edge_r)) if sl.right is not None else None
         ops = []
         if sl.right is not None:
-            ops.append(dist.P2POp(dist.isend, ghost_r.contiguous(), sl.right))
+            ops.append(dist.P2POp(dist.isend, self._h(ghost_r).contiguous(), sl.right))
         if sl.left is not None:
-            ops.append(dist.P2POp(dist.isend, ghost_l.contiguous(), sl.left))
+            ops.append(dist.P2POp(dist.isend, self._h(ghost_l).contiguous(), sl.left))
         if sl.left is not None:
             ops.append(dist.P2POp(dist.irecv, recv_l, sl.left))
         if sl.right is not None:
@@ -131,11 +149,13 @@ class P2PExchanger:
         for q in dist.batch_isend_irecv(ops):
             q.wait()
         if recv_l is not None:
-            edge_l.add_(recv_l)
+            edge_l.add_(recv_l.to(edge_l.device))
         if recv_r is not None:
-            edge_r.add_(recv_r)
+            edge_r.add_(recv_r.to(edge_r.device))
 
     def particles(self, sl, to_left, to_right):
+        dev = to_left.device
+        to_left, to_right = self._h(to_left), self._h(to_right)
         got = []
         for send_to, payload, recv_from in ((sl.right, to_right, sl.left), (sl.left, to_left, sl.right)):
             n_out = torch.tensor([payload.shape[1] if payload is not None else 0], dtype=torch.int64,
@@ -158,12 +178,15 @@ class P2PExchanger:
             if ops:
                 for q in dist.batch_isend_irecv(ops):
                     q.wait()
-            got.append(buf)
+            got.append(buf.to(dev))
         return got
 
     def allreduce(self, sl, t, op):
-        dist.all_reduce(t, op={"min": dist.ReduceOp.MIN, "max": dist.ReduceOp.MAX}.get(
+        h = self._h(t)
+        dist.all_reduce(h, op={"min": dist.ReduceOp.MIN, "max": dist.ReduceOp.MAX}.get(
             op, dist.ReduceOp.SUM))
+        if h is not t:
+            t.copy_(h)
 
 
 class _SlabSolver(MultiLevelSolver):

@@ -102,3 +102,65 @@ def test_coupled_slabs_equal_single_domain(scene, world, steps, adapt):
         assert np.allclose(dd.fluid_mom, dr.fluid_mom, rtol=1e-9, atol=1e-12)
         assert np.allclose(dd.sediment_mom, dr.sediment_mom, rtol=1e-9, atol=1e-12)
         assert abs(dd.eps_min - dr.eps_min) <= 1e-12
+
+
+def _mp_worker(rank, world, port, scene_name, steps, q):
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import scenes as S2
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2603_14982_b200.slab_coupled import P2PExchanger, SlabCoupled
+        base = _ref(getattr(S2, scene_name), True)
+        sim = SlabCoupled(base, rank, world, P2PExchanger())
+        for _ in range(steps):
+            sim.step()
+        pid, x, v = sim.owned_particles()
+        d = sim.diagnostics[-1]
+        q.put((rank, pid, x, v, tuple(d.fluid_mom), tuple(d.sediment_mom),
+               sorted(sim.gtopo.tile_set())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_coupled_slabs_two_processes_p2p():
+    """The multi-process path (P2PExchanger over a torch.distributed group,
+    here gloo with host staging so both processes share cuda:0) reproduces
+    the single-domain run."""
+    _need_gpu()
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    world, steps = 2, 6
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, "SANDSTORM_3D_SMALL", steps, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    ref = _ref(S.SANDSTORM_3D_SMALL, True)
+    for _ in range(steps):
+        ref.step()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    rx = ref.particles.x.cpu().numpy()
+    rv = ref.particles.v.cpu().numpy()
+    seen = 0
+    for rank, pid, x, v, fm, sm, tiles in out:
+        seen += len(pid)
+        assert np.abs(x - rx[pid]).max() <= 1e-10, rank
+        assert np.abs(v - rv[pid]).max() <= 1e-10, rank
+        assert np.allclose(fm, ref.diagnostics[-1].fluid_mom, rtol=1e-9, atol=1e-12)
+        assert np.allclose(sm, ref.diagnostics[-1].sediment_mom, rtol=1e-9, atol=1e-12)
+        assert set(tiles) == ref.topology.tile_set()
+    assert seen == len(rx)
