@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--scene", default="c2", choices=["c2", "c3", "c1"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--slabs", action="store_true",
+                    help="coupled slab decomposition (slab_coupled.py) instead of replicas: "
+                         "weak-scaled C2 x N domain, NCCL P2P exchanges")
     return ap.parse_args()
 
 
@@ -465,6 +468,77 @@ def run_slab(args, rank, world, local_rank):
             "cpu_baseline": cpu, "clocks": clk}), flush=True)
 
 
+def run_slabs_coupled(args, rank, world, local_rank):
+    """--slabs: the C2 column replicated N times along x as ONE domain
+    (128 N x 128 x 128, walls), one 128-wide slab per GPU, coupled step with
+    the slab collectives (i)-(v) over NCCL (eager, host-driven exchanges)."""
+    import copy
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2603_14982_b200 import _lib as L
+    from paper_2603_14982_b200.harness import build_scene, validate_scene
+    from paper_2603_14982_b200.slab_coupled import P2PExchanger, SlabCoupled, ThreadExchanger
+    import scenes as S
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    sc = copy.deepcopy(S.COLUMN_3D_C2)
+    nx = sc["domain"]["cells"][0]
+    sc["domain"]["cells"][0] = nx * world
+    b = sc["particles"]["blocks"][0]
+    sc["particles"]["blocks"] = [[b[0] + k * nx, b[1], b[2], b[3] + k * nx, b[4], b[5]]
+                                 for k in range(world)]
+    ref = build_scene(validate_scene(sc))
+    ref.use_graphs = False
+    ref.sort_particles = False
+    xch = P2PExchanger() if world > 1 else ThreadExchanger(1)
+    sim = SlabCoupled(ref, rank, world, xch)
+    del ref
+    torch.cuda.empty_cache()
+    eff = int(np.prod(sc["domain"]["cells"]))
+    for _ in range(args.warmup):
+        sim.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local_rank)
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    l0 = L.TRACE.launches
+    e0.record()
+    for _ in range(args.steps):
+        sim.step()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    n_loc = torch.tensor([len(sim.particles)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(n_loc)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": round(eff * args.steps / (t_ms * 1e-3) / 1e6, 3),
+            "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(t_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C2 x N slabs: the C2 column replicated along x as one "
+                                   "(128 N) x 128 x 128 domain, one slab per GPU, coupled step "
+                                   "with ghost-column / ghost-node / particle / seed / diagnostic "
+                                   "exchanges (eager, host-driven)",
+                       "effective_cells": eff, "particles": int(n_loc.item()),
+                       "parallelism": f"slabs{world}"},
+            "particles_per_s": round(float(n_loc.item()) * args.steps / (t_ms * 1e-3), 1),
+            "e2e": None, "gpu_launches": L.TRACE.launches - l0, "clocks": clk,
+            "topology_changes": sim.topology_changes}), flush=True)
+
+
 def oracle_sample(scene):
     """Bounded CPU sample of the same workload: the fp64 NumPy oracle port."""
     from oracle import scene as OS
@@ -534,6 +608,8 @@ def main():
     try:
         if args.scene == "c1":
             run_slab(args, rank, world, local_rank)
+        elif args.slabs:
+            run_slabs_coupled(args, rank, world, local_rank)
         else:
             run_mine(args, rank, world, local_rank)
     finally:
