@@ -56,8 +56,8 @@ def scene_dict(name):
 def workload_name(name):
     return {"c2": "C2: two-level 128^3-effective 3D granular column collapse in air, 262,144 "
                   "MPM sand particles, two-way coupled, adapt every step",
-            "c3": "C3: three-level 512x256x128-effective sand bed under log-law wind inflow, "
-                  "3,932,160 MPM sand particles, two-way coupled, adapt every step",
+            "c3": "C3: three-level 512x256x128-effective dune under log-law wind inflow, "
+                  "4,194,304 MPM sand particles, two-way coupled, adapt every step",
             "c1": "C1: single-level 64^3 periodic Taylor-Green (D3Q27)"}[name]
 
 

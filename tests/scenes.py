@@ -107,18 +107,19 @@ COLUMN_3D_C2 = {
     "particles": {"blocks": [[48.0, 4.0, 48.0, 80.0, 68.0, 80.0]], "per_cell": 4},
     "runtime": {"seed": 5, "dtype": "f32"}}
 
-# BASELINE.json configs[2]: three-level 512x256x128-effective sand migration
-# under a log-law wind inflow, ~3.9M particles (a 384x20x128-cell bed, 4 per cell)
+# BASELINE.json configs[2]: three-level 512x256x128-effective
+# sand migration under a log-law wind inflow; dune block [96,352]x[2,18]x[0,128]
+# at 8 per cell = 4,194,304 particles, seed 42
 SANDSTORM_3D_C3 = {
     "domain": {"cells": [512, 256, 128], "levels": 3},
     "fluid": {"tau0": 1.8, "eps_min": 0.5, "gravity": [0.0, -1e-4, 0.0]},
-    "boundaries": {"x_min": {"kind": "log_inlet", "u0": 0.05, "beta": 0.35, "y0": 24.0},
+    "boundaries": {"x_min": {"kind": "log_inlet", "u0": 0.04, "beta": 0.35, "y0": 6.0},
                    "x_max": "outlet", "y_min": "wall", "y_max": "outlet",
                    "z_min": "periodic", "z_max": "periodic"},
     "materials": {"density_ratio": 40.0, "E": 0.08, "nu": 0.3, "friction_angle_deg": 30.0,
                   "floor_friction": 0.5},
-    "particles": {"blocks": [[64.0, 2.0, 0.0, 448.0, 22.0, 128.0]], "per_cell": 4},
-    "runtime": {"seed": 9, "dtype": "f32"}}
+    "particles": {"blocks": [[96.0, 2.0, 0.0, 352.0, 18.0, 128.0]], "per_cell": 8},
+    "runtime": {"seed": 42, "dtype": "f32"}}
 
 # configs[0]: single-level 64^3 periodic Taylor-Green
 TAYLOR_GREEN_3D_C1 = {"domain": {"cells": [64, 64, 64], "levels": 1},
