@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
-    ap.add_argument("--scene", default="c2", choices=["c2", "c3", "c1"])
+    ap.add_argument("--scene", default="c2", choices=["c2", "c3", "c5", "c1"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--slabs", action="store_true",
@@ -50,7 +50,8 @@ def parse():
 
 def scene_dict(name):
     import scenes as S
-    return {"c2": S.COLUMN_3D_C2, "c3": S.SANDSTORM_3D_C3, "c1": S.TAYLOR_GREEN_3D_C1}[name]
+    return {"c2": S.COLUMN_3D_C2, "c3": S.SANDSTORM_3D_C3, "c5": S.CLOUD_3D_C5,
+            "c1": S.TAYLOR_GREEN_3D_C1}[name]
 
 
 def workload_name(name):
@@ -58,6 +59,9 @@ def workload_name(name):
                   "MPM sand particles, two-way coupled, adapt every step",
             "c3": "C3: three-level 512x256x128-effective dune under log-law wind inflow, "
                   "4,194,304 MPM sand particles, two-way coupled, adapt every step",
+            "c5": "C5: dynamic-refinement stress, periodic 256^3, L = 3, 2,097,152 particles in a "
+                  "dispersed cloud with Gaussian velocities (sigma 0.1), blocks activated / "
+                  "retired every step",
             "c1": "C1: single-level 64^3 periodic Taylor-Green (D3Q27)"}[name]
 
 
@@ -170,6 +174,9 @@ def run_mine(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     cfg = validate_scene(scene_dict(args.scene))
     sim = build_scene(cfg)
+    if args.scene == "c5":
+        import scenes as S
+        S.cloud_velocities(sim)
     d = cfg.dim
     eff_cells = int(np.prod(cfg.cells))
     n_part = len(sim.particles)

@@ -121,6 +121,26 @@ SANDSTORM_3D_C3 = {
     "particles": {"blocks": [[96.0, 2.0, 0.0, 352.0, 18.0, 128.0]], "per_cell": 8},
     "runtime": {"seed": 42, "dtype": "f32"}}
 
+# BASELINE.json configs[4]: dynamic-refinement stress — a
+# dispersed cloud in a periodic 256^3 box, L = 3, 2,097,152 particles (a 128^3
+# block at 1 per cell) with Gaussian velocities sigma 0.1 clipped at 0.45
+# (set by cloud_velocities), density ratio 10
+CLOUD_3D_C5 = {
+    "domain": {"cells": [256, 256, 256], "levels": 3},
+    "fluid": {"tau0": 1.8, "eps_min": 0.5, "gravity": [0.0, 0.0, 0.0]},
+    "materials": {"density_ratio": 10.0, "E": 0.08},
+    "particles": {"blocks": [[64.0, 64.0, 64.0, 192.0, 192.0, 192.0]], "per_cell": 1},
+    "runtime": {"seed": 17, "dtype": "f32"}}
+
+
+def cloud_velocities(sim, sigma=0.1, clip=0.45, seed=17):
+    """C5 initial particle velocities: N(0, sigma^2) per component, clipped."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    v = np.clip(rng.normal(0.0, sigma, (len(sim.particles), sim.d)), -clip, clip)
+    sim.particles.v = v
+
+
 # configs[0]: single-level 64^3 periodic Taylor-Green
 TAYLOR_GREEN_3D_C1 = {"domain": {"cells": [64, 64, 64], "levels": 1},
                       "fluid": {"tau0": 0.8, "init": "taylor_green", "init_u0": 0.05},
