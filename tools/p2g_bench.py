@@ -6,7 +6,11 @@ import torch
 import scenes as S
 from paper_2603_14982_b200 import _lib as L
 from paper_2603_14982_b200.harness import build_scene, validate_scene
-sim = build_scene(validate_scene(S.COLUMN_3D_C2))
+import os
+sc = os.environ.get("SCENE", "COLUMN_3D_C2")
+sim = build_scene(validate_scene(getattr(S, sc)))
+if sc == "CLOUD_3D_C5":
+    S.cloud_velocities(sim)
 for _ in range(12):
     sim.step()
 torch.cuda.synchronize()

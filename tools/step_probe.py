@@ -6,6 +6,8 @@ import scenes as S
 from paper_2603_14982_b200.harness import build_scene, validate_scene
 import os
 sim = build_scene(validate_scene(getattr(S, os.environ.get("SCENE", "COLUMN_3D_C2"))))
+if os.environ.get("SCENE") == "CLOUD_3D_C5":
+    S.cloud_velocities(sim)
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 60
 rows = []
 for i in range(n):
