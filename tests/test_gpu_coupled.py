@@ -237,3 +237,21 @@ def test_host_mirror_round_trip_matches_resident_run():
     m.upload()
     torch.cuda.synchronize()
     assert torch.equal(b.particles.pd.cpu(), m.host[1])
+
+
+def test_c2_fp32_long_run_stable():
+    """The bench workload (C2, fp32, graph path) for 400 steps: no device
+    error, dozens of topology changes through the rebuild graph with few
+    captures, particle mass conserved, invariants clean."""
+    _need_gpu()
+    from paper_2603_14982_b200.harness import build_scene, validate_scene
+    sim = build_scene(validate_scene(S.COLUMN_3D_C2))
+    m0 = float(sim.particles.m.double().sum().item())
+    for _ in range(400):
+        sim.step()
+    assert sim.topology_changes >= 20
+    assert sim.graph_captures <= 16
+    assert abs(float(sim.particles.m.double().sum().item()) - m0) <= 1e-6 * m0
+    assert sim.last_report is not None and sim.last_report.violations == []
+    row = sim.diagnostics[-1]
+    assert np.all(np.isfinite(row.fluid_mom)) and np.all(np.isfinite(row.sediment_mom))
