@@ -1748,11 +1748,15 @@ __global__ void __launch_bounds__(32 * NW) k_p2g_cell2(PartArgs P, TopoL0 t0, Ma
     for (int a = 0; a < D; ++a) { lo[a] = s_lo[a]; ext[a] = s_hi[a] - s_lo[a] + 1; nbox *= ext[a]; }
     const bool use_smem = nbox > 0 && nbox <= MAXN;
     if (use_smem) {
+        // zero the [NW * NV rows][nbox] box copies as float4, iterating over a
+        // power-of-two padded row (no integer division)
+        constexpr int RP = MAXN / 4 <= 32 ? 32 : (MAXN / 4 <= 64 ? 64 : 128);
+        static_assert(MAXN / 4 <= RP, "row padding");
         const int n4 = (nbox + 3) >> 2;
         float4* s4 = reinterpret_cast<float4*>(sacc);
-        for (int i = threadIdx.x; i < NW * NV * n4; i += BT) {
-            const int row = i / n4, c4 = i - row * n4;
-            s4[row * (MAXN / 4) + c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = threadIdx.x; i < NW * NV * RP; i += BT) {
+            const int row = i / RP, c4 = i % RP;
+            if (c4 < n4) s4[row * (MAXN / 4) + c4] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
     }
     __syncthreads();
