@@ -255,3 +255,35 @@ def test_c2_fp32_long_run_stable():
     assert sim.last_report is not None and sim.last_report.violations == []
     row = sim.diagnostics[-1]
     assert np.all(np.isfinite(row.fluid_mom)) and np.all(np.isfinite(row.sediment_mom))
+
+
+def test_frame_outputs_match_reference_frame():
+    """write_frame from device buffers after 3 steps of the 2D dune scene
+    reads back to the reference's own frame files (the outputs fixture)
+    within fp64 summation noise; the particle dump and 'stored' map match
+    exactly in structure."""
+    _need_gpu()
+    import os
+    import tempfile
+    from paper_2603_14982_b200.harness import build_scene, validate_scene
+    from paper_2603_14982_b200.harness import outputs as O
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                             "outputs_dune_2d.npz"))
+    sc = S.scene(S.DUNE_2D, runtime__mpm_cadence=1)
+    sc.setdefault("outputs", {}).update({"fields": True, "particles": True, "quicklook": True})
+    cfg = validate_scene(sc)
+    sim = build_scene(cfg)
+    for _ in range(3):
+        sim.step()
+    with tempfile.TemporaryDirectory() as d:
+        O.write_frame(d, 7, sim, cfg)
+        for l in range(int(g["levels"])):
+            back = O.read_vtk_level(os.path.join(d, f"frame_00007_l{l}.vtk"))
+            assert np.array_equal(back["stored"], g[f"L{l}_stored"]), l
+            for nm in ("rho", "ux", "uy", "eps", "phi"):
+                assert np.abs(back[nm] - g[f"L{l}_{nm}"]).max() <= 1e-10, (l, nm)
+        x, v, m = O.read_particles(os.path.join(d, "frame_00007_particles.bin"))
+        assert np.abs(x - g["px"]).max() <= 1e-10 and np.abs(v - g["pv"]).max() <= 1e-10
+        assert np.array_equal(m, g["pm"])
+        assert os.path.getsize(os.path.join(d, "frame_00007_speed.ppm")) == \
+            len(g["file_frame_00007_speed.ppm"])
