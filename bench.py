@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
-    ap.add_argument("--scene", default="c2", choices=["c2", "c3", "c5", "c1"])
+    ap.add_argument("--scene", default="c2", choices=["c2", "c3", "c4", "c5", "c1"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--slabs", action="store_true",
@@ -48,8 +48,16 @@ def parse():
     return ap.parse_args()
 
 
-def scene_dict(name):
+_C4_DIR = None
+
+
+def scene_dict(name, scale=1):
     import scenes as S
+    if name == "c4":
+        import tempfile
+        global _C4_DIR
+        _C4_DIR = _C4_DIR or tempfile.mkdtemp(prefix="mlbm_c4_")
+        return S.avalanche_c4(os.path.join(_C4_DIR, f"terrain_s{scale}.npy"), scale=scale)
     return {"c2": S.COLUMN_3D_C2, "c3": S.SANDSTORM_3D_C3, "c5": S.CLOUD_3D_C5,
             "c1": S.TAYLOR_GREEN_3D_C1}[name]
 
@@ -59,6 +67,9 @@ def workload_name(name):
                   "MPM sand particles, two-way coupled, adapt every step",
             "c3": "C3: three-level 512x256x128-effective dune under log-law wind inflow, "
                   "4,194,304 MPM sand particles, two-way coupled, adapt every step",
+            "c4": "C4: four-level 1536x768x384-effective snow avalanche with powder cloud over a "
+                  "terrain heightmap, 55,836,672 MPM particles (Drucker-Prager), two-way coupled, "
+                  "powder entrainment, adapt every step, on ONE B200",
             "c5": "C5: dynamic-refinement stress, periodic 256^3, L = 3, 2,097,152 particles in a "
                   "dispersed cloud with Gaussian velocities (sigma 0.1), blocks activated / "
                   "retired every step",
@@ -546,12 +557,23 @@ def run_slabs_coupled(args, rank, world, local_rank):
             "topology_changes": sim.topology_changes}), flush=True)
 
 
+# C4's full scene is ~55.8M particles: the CPU sample is the same scene with
+# every extent divided by 4 (872,448 particles, ~50 s per oracle step)
+CPU_SAMPLE_SCALE = {"c4": 4}
+
+
 def oracle_sample(scene):
     """Bounded CPU sample of the same workload: the fp64 NumPy oracle port."""
     from oracle import scene as OS
     from paper_2603_14982_b200.harness.config import validate_scene
-    cfg = validate_scene(scene_dict(scene))
+    cfg = validate_scene(scene_dict(scene, CPU_SAMPLE_SCALE.get(scene, 1)))
     return cfg, OS.build_scene(cfg.raw, heightmap=cfg.heightmap())
+
+
+def sample_name(scene):
+    k = CPU_SAMPLE_SCALE.get(scene)
+    return (f"{scene.upper()} scene with every extent divided by {k}" if k else
+            f"full {scene.upper()} scene")
 
 
 def cpu_baseline(scene):
@@ -562,7 +584,7 @@ def cpu_baseline(scene):
     dt = time.perf_counter() - t0
     eff = int(np.prod(cfg.cells))
     return {"value": round(eff / dt / 1e6, 4), "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"1 coupled step of the full {scene.upper()} scene in the fp64 NumPy oracle "
+            "sample": f"1 coupled step of the {sample_name(scene)} in the fp64 NumPy oracle "
                       f"port (oracle/, single thread) after scene build: {dt:.2f} s",
             "particles_per_s": round(len(sim.p) / dt, 1)}
 
@@ -584,7 +606,7 @@ def run_reference(args, rank):
     dt = time.perf_counter() - t0
     value = eff * k / dt / 1e6
     sample = (f"{k} coupled steps (of {args.steps} requested, capped to bound CPU time) of the "
-              f"full {args.scene.upper()} scene in the fp64 NumPy oracle port, 1 thread")
+              f"{sample_name(args.scene)} in the fp64 NumPy oracle port, 1 thread")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
         "n_gpus": args.gpus, "steps": k, "warmup": min(args.warmup, 1),

@@ -57,11 +57,14 @@ struct AdaptArgs {
 __device__ __forceinline__ int64_t gi3(const int* d, int x, int y, int z) {
     return ((int64_t)x * d[1] + y) * d[2] + z;
 }
+// tile grids hold < 2^31 tiles (the host checks): 32-bit division only
 __device__ __forceinline__ void dec3(const int* d, int64_t g, int& x, int& y, int& z) {
-    z = (int)(g % d[2]);
-    g /= d[2];
-    y = (int)(g % d[1]);
-    x = (int)(g / d[1]);
+    const unsigned gg = (unsigned)g, d1 = (unsigned)d[1], d2 = (unsigned)d[2];
+    const unsigned q = gg / d2;
+    z = (int)(gg - q * d2);
+    const unsigned r = q / d1;
+    y = (int)(q - r * d1);
+    x = (int)r;
 }
 
 __device__ void grid_barrier(unsigned int* bar) {
@@ -173,7 +176,7 @@ __device__ void effective_stage(const AdaptArgs& A, int l, bool with_guard, int6
         bool cand = false, avail = false;
         int c[3] = {0, 0, 0};
         if (valid) {
-            const int64_t j = t / K;
+            const int64_t j = t >> (K == 8 ? 3 : K == 4 ? 2 : 0);
             const int k = (int)(t - j * K);
             int x[3];
             dec3(gd, j, x[0], x[1], x[2]);
@@ -664,15 +667,23 @@ extern "C" int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_
         A.ts = ts_env;
         g_ts_last = ts_env;
     }
-    static int grid = 0;
-    if (grid == 0) {
+    static int grid_sms = 0, grid_per = 1;
+    int grid = 0;
+    if (grid_sms == 0) {
         int dev = 0, sms = 0, per = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_adapt_pass, 512, 0);
-        grid = sms * std::min(per, 1);
-        if (grid < 1) grid = 1;
+        grid_sms = sms;
+        grid_per = std::max(per, 1);
     }
+    // small tile grids (C2: 32K level-0 tiles) are barrier-latency bound: one
+    // CTA per SM; large ones (C4: 7.1M) need every resident warp for memory
+    // parallelism: up to the occupancy limit, ~8 tiles per thread per stage
+    int64_t n0 = 1;
+    for (int a = 0; a < h->dim; ++a) n0 *= (h->finest[a] / 4);
+    const int64_t want = (n0 + (int64_t)grid_sms * 512 * 8 - 1) / ((int64_t)grid_sms * 512 * 8);
+    grid = grid_sms * (int)std::max<int64_t>(1, std::min<int64_t>(want, grid_per));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(512);

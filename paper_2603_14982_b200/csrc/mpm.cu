@@ -16,6 +16,7 @@
 // Particle positions are always float64 (sub-cell offsets at x ~ 1e3 need
 // ~1e-8 absolute resolution); everything else follows the run dtype.
 #include <algorithm>
+#include <cstdlib>
 #include <cub/cub.cuh>
 #include "common.cuh"
 
@@ -801,17 +802,24 @@ __global__ void k_stress_raster(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int
     if (bad) report_error(err, MLBM_ERR_STENCIL, 0, st.base[0], st.base[1], st.base[2]);
 }
 
-// renormalised multilinear sample of a level-0 field (coupling.py:200-227)
-template <int D, typename R>
-__device__ R sample_lin(const R* f, const double (&pos)[D], const mlbm_level_t& lv) {
+// renormalised multilinear sample of NC level-0 fields at one position
+// (coupling.py:200-227); the corner lookups are shared by the NC fields and
+// each field's sum runs in the reference's corner order
+template <int D, typename R, int NC>
+__device__ void sample_lin_n(const R* const (&f)[NC], const double (&pos)[D], const mlbm_level_t& lv,
+                             double (&out)[NC]) {
     constexpr int T = Geo<D>::T;
     int b[D];
     double fr[D];
     for (int a = 0; a < D; ++a) { const double fl = floor(pos[a]); b[a] = (int)fl; fr[a] = pos[a] - fl; }
-    double acc = 0.0, ws = 0.0;
+    double acc[NC], ws = 0.0;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) acc[q] = 0.0;
+#pragma unroll
     for (int k = 0; k < (1 << D); ++k) {
         int c[3] = {0, 0, 0};
         double w = 1.0;
+#pragma unroll
         for (int a = 0; a < D; ++a) {
             const int o = (k >> a) & 1;
             int v = b[a] + o;
@@ -823,10 +831,12 @@ __device__ R sample_lin(const R* f, const double (&pos)[D], const mlbm_level_t& 
         const int s = lv.tile_map[g3(lv.tiles, c[0] >> 2, c[1] >> 2, D == 3 ? c[2] >> 2 : 0)];
         if (s < 0) continue;
         const int64_t ni = (int64_t)s * T + local_of<D>(c[0] & 3, c[1] & 3, c[2] & 3);
-        acc += w * (double)f[ni];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) acc[q] += w * (double)f[q][ni];
         ws += w;
     }
-    return ws > 0.0 ? R(acc / ws) : R(acc);
+#pragma unroll
+    for (int q = 0; q < NC; ++q) out[q] = ws > 0.0 ? (double)R(acc[q] / ws) : (double)R(acc[q]);
 }
 
 struct PowderArgs {
@@ -852,13 +862,16 @@ __global__ void k_powder_advect(PowderArgs A) {
     const R* u[D];
     for (int a = 0; a < D; ++a) u[a] = &dst.at(1 + a, 0);
     double k1[D], k2[D], k3[D], q[D];
-    for (int a = 0; a < D; ++a) k1[a] = (double)sample_lin<D, R>(u[a], pos, A.lv);
+    sample_lin_n<D, R, D>(u, pos, A.lv, k1);
     for (int a = 0; a < D; ++a) q[a] = pos[a] - 0.5 * A.dt * k1[a];
-    for (int a = 0; a < D; ++a) k2[a] = (double)sample_lin<D, R>(u[a], q, A.lv);
+    sample_lin_n<D, R, D>(u, q, A.lv, k2);
     for (int a = 0; a < D; ++a) q[a] = pos[a] - 0.75 * A.dt * k2[a];
-    for (int a = 0; a < D; ++a) k3[a] = (double)sample_lin<D, R>(u[a], q, A.lv);
+    sample_lin_n<D, R, D>(u, q, A.lv, k3);
     for (int a = 0; a < D; ++a) q[a] = pos[a] - A.dt * (2.0 * k1[a] + 3.0 * k2[a] + 4.0 * k3[a]) / 9.0;
-    ((R*)A.tmp)[c] = sample_lin<D, R>(&src.at(fi_phi<D>(), 0), q, A.lv);
+    const R* ph[1] = {&src.at(fi_phi<D>(), 0)};
+    double phv[1];
+    sample_lin_n<D, R, 1>(ph, q, A.lv, phv);
+    ((R*)A.tmp)[c] = R(phv[0]);
 }
 
 template <int D, typename R>
@@ -1707,6 +1720,37 @@ __device__ __forceinline__ void p2g_record(const PartArgs& P, const MatParams& m
         for (int kk = 0; kk < D * D; ++kk) rec[o2++] = PC[kk];
     }
 
+// Sum the NW per-warp node-box copies and add the node totals into the
+// raster rows (one atomic per touched node and non-zero row).  STRESS = 0:
+// the P2G rows (a node is touched iff its mass or area is non-zero); STRESS =
+// 1: rows 0..NV-2 are written and row NV-1 counts the particles that touched
+// the node (an untouched node is neither written nor checked).
+template <int D, int NV, int STRESS>
+__device__ __forceinline__ void p2g_box_merge(const float* sacc, int NW, int MAXN, int nbox,
+                                              const int (&lo)[3], const int (&ext)[3], const TopoL0& t0,
+                                              float* ras, int64_t rs, mlbm_error_t* err) {
+    for (int i = threadIdx.x; i < nbox; i += blockDim.x) {
+        float tot[NV];
+#pragma unroll
+        for (int qv = 0; qv < NV; ++qv) {
+            float v = sacc[qv * MAXN + i];
+            for (int w2 = 1; w2 < NW; ++w2) v += sacc[(w2 * NV + qv) * MAXN + i];
+            tot[qv] = v;
+        }
+        if (STRESS ? tot[NV - 1] == 0.f : (tot[0] == 0.f && tot[2 + 2 * D] == 0.f)) continue;
+        int c[3] = {0, 0, 0};
+        int rr = i;
+#pragma unroll
+        for (int a = 0; a < D; ++a) { c[a] = lo[a] + rr % ext[a]; rr /= ext[a]; }
+        bool b2 = false;
+        const int64_t ni = node_index<D>(t0, c, b2);
+        if (ni < 0) { report_error(err, MLBM_ERR_STENCIL, 0, c[0], c[1], c[2]); continue; }
+#pragma unroll
+        for (int qv = 0; qv < NV - STRESS; ++qv)
+            if (tot[qv] != 0.f) atomicAdd(&ras[qv * rs + ni], tot[qv]);
+    }
+}
+
 template <int D, int NW, int ROUNDS>
 __global__ void __launch_bounds__(32 * NW) k_p2g_cell2(PartArgs P, TopoL0 t0, MatParams mp, float* ras,
                                                        int64_t rs, mlbm_error_t* err) {
@@ -1877,28 +1921,165 @@ __global__ void __launch_bounds__(32 * NW) k_p2g_cell2(PartArgs P, TopoL0 t0, Ma
     if (bad) report_error(err, MLBM_ERR_STENCIL, 0, cur[0], cur[1], cur[2]);
     if (!use_smem) return;
     __syncthreads();
-    for (int i = threadIdx.x; i < nbox; i += blockDim.x) {
-        float tot[NV];
-#pragma unroll
-        for (int qv = 0; qv < NV; ++qv) {
-            float v = sacc[qv * MAXN + i];
-#pragma unroll
-            for (int w2 = 1; w2 < NW; ++w2) v += sacc[(w2 * NV + qv) * MAXN + i];
-            tot[qv] = v;
-        }
-        if (tot[0] == 0.f && tot[2 + 2 * D] == 0.f) continue;
-        int c[3] = {0, 0, 0};
-        int rr = i;
-#pragma unroll
-        for (int a = 0; a < D; ++a) { c[a] = lo[a] + rr % ext[a]; rr /= ext[a]; }
-        bool b2 = false;
-        const int64_t ni = node_index<D>(t0, c, b2);
-        if (ni < 0) { report_error(err, MLBM_ERR_STENCIL, 0, c[0], c[1], c[2]); continue; }
-#pragma unroll
-        for (int qv = 0; qv < NV; ++qv)
-            if (tot[qv] != 0.f) atomicAdd(&ras[qv * rs + ni], tot[qv]);
-    }
+    p2g_box_merge<D, NV, 0>(sacc, NW, MAXN, nbox, lo, ext, t0, ras, rs, err);
 }
+
+// Entrainment stress raster (coupling.py:283-294) in the P2G layout: sum over
+// particles of V0 w_i tau (NS rows of RW::SIG) with post-G2P positions.  Lane
+// k = stencil node k of the current run of particles with equal stencil base;
+// records (base, f, V0 tau) are broadcast from a per-warp slab; per-warp node
+// box copies in shared memory, merged once into HBM (no per-particle atomics).
+template <int D, int NW>
+__global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0, MatParams mp, float* ras,
+                                                          int64_t rs, mlbm_error_t* err) {
+    constexpr int K = Geo<D>::K, NS = D * (D + 1) / 2, NV = NS + 1;
+    constexpr int MAXN = P2G2_MAXN, REC = 16, BT = 32 * NW;
+    using PR = PRows<D>;
+    using RW = Rows<D>;
+    extern __shared__ __align__(16) float p2g_smem[];
+    float* sacc = p2g_smem;                                  // [NW][NV][MAXN]
+    float* slab = p2g_smem + NW * NV * MAXN;                 // [NW][32][REC]
+    __shared__ int s_lo[3], s_hi[3];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int p = blockIdx.x * BT + threadIdx.x;
+    const bool valid = p < P.n;
+    if (threadIdx.x < 3) { s_lo[threadIdx.x] = 0x7fffffff; s_hi[threadIdx.x] = -0x7fffffff; }
+    // per-particle record: base[3] f[D] V0 tau[NS]
+    int base[3] = {0, 0, 0};
+    float f[D], S[NS];
+#pragma unroll
+    for (int a = 0; a < D; ++a) f[a] = 0.f;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) S[k] = 0.f;
+    if (valid) {
+        const float* pp = (const float*)P.p;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const double x = P.x[a * P.ps + p];
+            const double b = floor(x - 0.5);
+            base[a] = (int)b;
+            f[a] = (float)(x - b);
+        }
+        float F[D * D], tau[D * D];
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) F[k] = pp[(PR::F + k) * P.ps + p];
+        kirchhoff<D, float>(F, mp, tau);
+        const float V0 = pp[PR::V0 * P.ps + p];
+        int k = 0;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = a; b < D; ++b) S[k++] = V0 * tau[a * D + b];
+    }
+    __syncthreads();
+    {
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const int l2 = __reduce_min_sync(0xffffffffu, valid ? base[a] : 0x7fffffff);
+            const int h2 = __reduce_max_sync(0xffffffffu, valid ? base[a] + 2 : -0x7fffffff);
+            if (lane == 0 && l2 <= h2) { atomicMin(&s_lo[a], l2); atomicMax(&s_hi[a], h2); }
+        }
+    }
+    float* wslab = &slab[wid * 32 * REC];
+    {
+        float* r = &wslab[lane * REC];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) r[a] = __int_as_float(a < D ? base[a] : 0);
+#pragma unroll
+        for (int a = 0; a < D; ++a) r[3 + a] = f[a];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) r[3 + D + k] = S[k];
+    }
+    __syncthreads();
+    int lo[3] = {0, 0, 0}, ext[3] = {1, 1, 1}, nbox = 1;
+#pragma unroll
+    for (int a = 0; a < D; ++a) { lo[a] = s_lo[a]; ext[a] = s_hi[a] - s_lo[a] + 1; nbox *= ext[a]; }
+    const bool use_smem = nbox > 0 && nbox <= MAXN;
+    if (use_smem) {
+        constexpr int RP = MAXN / 4 <= 32 ? 32 : (MAXN / 4 <= 64 ? 64 : 128);
+        const int n4 = (nbox + 3) >> 2;
+        float4* s4 = reinterpret_cast<float4*>(sacc);
+        for (int i = threadIdx.x; i < NW * NV * RP; i += BT) {
+            const int row = i / RP, c4 = i % RP;
+            if (c4 < n4) s4[row * (MAXN / 4) + c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+    __syncthreads();
+
+    const int o[3] = {lane % 3, (lane / 3) % 3, D == 3 ? (lane / 9) % 3 : 0};
+    const bool node_lane = lane < K;
+    float c0[D], c1[D], c2[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const int oa = o[a];
+        c2[a] = oa == 1 ? -1.f : 0.5f;
+        c1[a] = oa == 0 ? -1.5f : (oa == 1 ? 2.f : -0.5f);
+        c0[a] = oa == 0 ? 1.125f : (oa == 1 ? -0.25f : 0.125f);
+    }
+    float* wacc = sacc + wid * NV * MAXN;
+    const int pw = blockIdx.x * BT + wid * 32;
+    const int nj = max(0, min(32, P.n - pw));
+    bool bad = false;
+    int cur[3] = {0, 0, 0};
+    bool start = lane < nj;
+    {
+        bool same = lane > 0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) same &= __shfl_up_sync(0xffffffffu, base[a], 1) == base[a];
+        start &= !same;
+    }
+    unsigned runs = __ballot_sync(0xffffffffu, start);
+    while (runs) {
+        const int j0 = __ffs(runs) - 1;
+        runs &= runs - 1;
+        const int j1 = runs ? __ffs(runs) - 1 : nj;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) cur[a] = __shfl_sync(0xffffffffu, a < D ? base[a] : 0, j0);
+        float acc[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) acc[q] = 0.f;
+        for (int j = j0; j < j1; ++j) {
+            const float4* rp = reinterpret_cast<const float4*>(&wslab[j * REC]);
+            float r[12];
+#pragma unroll
+            for (int v4 = 0; v4 < 3; ++v4) {
+                const float4 t = rp[v4];
+                r[4 * v4] = t.x; r[4 * v4 + 1] = t.y; r[4 * v4 + 2] = t.z; r[4 * v4 + 3] = t.w;
+            }
+            float w = 1.f;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                const float fa = r[3 + a];
+                w *= fmaf(fmaf(c2[a], fa, c1[a]), fa, c0[a]);
+            }
+#pragma unroll
+            for (int q = 0; q < NS; ++q) acc[q] = fmaf(w, r[3 + D + q], acc[q]);
+            acc[NS] += 1.f;
+        }
+        if (node_lane) {
+            int c[3] = {cur[0] + o[0], cur[1] + o[1], D == 3 ? cur[2] + o[2] : 0};
+            if (use_smem) {
+                int li = 0;
+#pragma unroll
+                for (int a = D - 1; a >= 0; --a) li = li * ext[a] + (c[a] - lo[a]);
+#pragma unroll
+                for (int q = 0; q < NV; ++q) wacc[q * MAXN + li] += acc[q];
+            } else {
+                const int64_t ni = node_index<D>(t0, c, bad);
+                if (ni >= 0) {
+#pragma unroll
+                    for (int q = 0; q < NS; ++q) atomicAdd(&ras[(RW::SIG + q) * rs + ni], acc[q]);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (bad) report_error(err, MLBM_ERR_STENCIL, 0, cur[0], cur[1], cur[2]);
+    if (!use_smem) return;
+    __syncthreads();
+    p2g_box_merge<D, NV, 1>(sacc, NW, MAXN, nbox, lo, ext, t0, ras + (int64_t)RW::SIG * rs, rs, err);
+}
+
 }  // namespace mlbm
 
 using namespace mlbm;
@@ -2034,6 +2215,20 @@ extern "C" int mlbm_stress_raster(const mlbm_level_t* lv0, int32_t n, const doub
     PartArgs P{lv0->dim, n, x, nullptr, (void*)p, ps, nullptr, nullptr, nullptr};
     MatParams mp{lam, mu, alpha, 0.0};
     const TopoL0 t = topo0(lv0);
+    if (dtype == 0 && !getenv("MLBM_STRESS_ATOMIC")) {
+        // fp32: the P2G layout (sorted particles, per-warp node boxes)
+        constexpr int NW = P2G2_NW;
+        const int sh = (NW * 7 * P2G2_MAXN + NW * 32 * 16) * (int)sizeof(float);   // NV <= 7
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_stress_cell2<3, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
+            cudaFuncSetAttribute(k_stress_cell2<2, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
+            attr = true;
+        }
+        if (lv0->dim == 2) k_stress_cell2<2, NW><<<nblk(n, 32 * NW), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
+        else k_stress_cell2<3, NW><<<nblk(n, 32 * NW), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
+        return launch_status(1);
+    }
 #define SR(D, R) k_stress_raster<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err)
     if (lv0->dim == 2) { if (dtype) SR(2, double); else SR(2, float); }
     else { if (dtype) SR(3, double); else SR(3, float); }

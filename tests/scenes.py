@@ -141,6 +141,45 @@ def cloud_velocities(sim, sigma=0.1, clip=0.45, seed=17):
     sim.particles.v = v
 
 
+def terrain_heightfield(cells, path, base=1.0, amp=2.5):
+    """Synthetic terrain under the C4 slab: heights in finest cells over
+    (x, z), a ramp falling along +x with a cross-slope undulation; every height
+    stays below the slab floor (y = 4), so no particle starts inside a solid.
+    Deterministic, written as an .npy for ``boundaries.heightfield``."""
+    import numpy as np
+    nx, nz = cells[0], cells[2]
+    x = (np.arange(nx) + 0.5) / nx
+    z = (np.arange(nz) + 0.5) / nz
+    h = base + amp * (0.6 * (1.0 - x)[:, None] + 0.4 * (0.5 + 0.5 * np.cos(2 * np.pi * z))[None, :])
+    np.save(path, np.minimum(h, 3.5).astype(np.float64))
+    return path
+
+
+def avalanche_c4(heightfield_path, scale=1):
+    """BASELINE.json configs[3]: four-level
+    1536x768x384-effective snow avalanche with powder cloud — floor wall over a
+    terrain heightmap (solids), outlets elsewhere, g along -y, a snow slab
+    (Drucker-Prager granular material; no NACC model exists in the reference)
+    [256,4,50]x[1280,28,334] = 6,979,584 cells at 8 per cell = 55,836,672
+    particles, powder entrainment on.  ``scale`` > 1 divides every extent (the
+    bounded CPU sample)."""
+    s = float(scale)
+    cells = [1536 // scale, 768 // scale, 384 // scale]
+    terrain_heightfield(cells, heightfield_path)
+    return {
+        "domain": {"cells": cells, "levels": 4},
+        "fluid": {"tau0": 1.8, "eps_min": 0.5, "gravity": [0.0, -1e-4, 0.0]},
+        "boundaries": {"x_min": "outlet", "x_max": "outlet", "y_min": "wall", "y_max": "outlet",
+                       "z_min": "outlet", "z_max": "outlet",
+                       "heightfield": heightfield_path},
+        "materials": {"density_ratio": 40.0, "E": 0.08, "nu": 0.3, "friction_angle_deg": 30.0,
+                      "floor_friction": 0.5},
+        "particles": {"blocks": [[256.0 / s, 4.0, 50.0 / s, 1280.0 / s, 4.0 + 24.0 / s, 334.0 / s]],
+                      "per_cell": 8},
+        "powder": {"enabled": True, "entrain": 0.02, "diffusion": 0.05},
+        "runtime": {"seed": 7, "dtype": "f32"}}
+
+
 # configs[0]: single-level 64^3 periodic Taylor-Green
 TAYLOR_GREEN_3D_C1 = {"domain": {"cells": [64, 64, 64], "levels": 1},
                       "fluid": {"tau0": 0.8, "init": "taylor_green", "init_u0": 0.05},
