@@ -168,6 +168,8 @@ def kernel_class(rec, d, s, live):
                                 + (NM + 2)) * s, n
     if name.startswith("mlbm_diag"):
         return "diagnostics", 0, 0
+    if name.startswith("mlbm_stress_raster") or name == "mlbm_powder":
+        return "powder", 0, 0
     if name == "mlbm_particle_sort":
         n = int(args[1])
         return "particle_sort", n * 2 * (8 * d + (d + 2 * d * d + 3) * s + 4), n

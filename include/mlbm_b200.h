@@ -315,6 +315,15 @@ int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, const double* x_in, double* x_o
 int mlbm_stress_raster(const mlbm_level_t* lv0, int32_t n, const double* x, const void* p,
                        int64_t ps, double lam, double mu, double alpha, void* ras, int64_t rs,
                        int32_t dtype, mlbm_error_t* err, void* stream);
+/* fp32: the stress raster restricted to the entrainment surface (the only
+ * cells k_powder reads it at): surf [n0] floats receives the surface flags
+ * (0 < eta < eta_surface with an absent / empty face neighbour), runs of
+ * particles none of whose stencil nodes is a surface cell are skipped; the
+ * sums at surface cells equal mlbm_stress_raster's.  fp64: the full raster. */
+int mlbm_stress_raster_surface(const mlbm_level_t* lv0, int32_t n, const double* x,
+                               const void* p, int64_t ps, double lam, double mu, double alpha,
+                               void* ras, int64_t rs, double eta_surface, void* surf,
+                               int32_t dtype, mlbm_error_t* err, void* stream);
 int mlbm_powder(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm_fields_t dst, void* ras,
                 int64_t rs, void* tmp, double diffusion, double sign, double dt,
                 double entrain, double eta_surface, int32_t with_source, int32_t dtype,

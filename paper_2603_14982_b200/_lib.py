@@ -152,6 +152,8 @@ _SIGS = {
                  I32, P, P, P],
     "mlbm_stress_raster": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64,
                            I32, P, P],
+    "mlbm_stress_raster_surface": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64, D, P,
+                                   I32, P, P],
     "mlbm_powder": [C.POINTER(Level), Fields, Fields, P, I64, P, D, D, D, D, D,
                     I32, I32, P],
     "mlbm_diag_level": [C.POINTER(Level), Fields, D, I32, P, P],

@@ -597,11 +597,14 @@ class CoupledSim:
             grid.ras[R["sig"]:R["n"]].zero_()
             p = self.particles
             lv0 = grid.level0()
-            L.check(lib.mlbm_stress_raster(L.C.byref(lv0), len(p), L.ptr(p.xd), L.ptr(p.pd),
-                                           p.pd.stride(0), self.material.lam, self.material.mu,
-                                           self.material.alpha, L.ptr(grid.ras),
-                                           grid.ras.stride(0), dcode, L.ptr(grid._err), s),
-                    "stress_raster")
+            # the raster is only read at entrainment surface cells: fp32 runs
+            # restrict it to them (surface flags in the powder scratch, which
+            # the advection overwrites afterwards); fp64 runs rasterise fully
+            L.check(lib.mlbm_stress_raster_surface(
+                L.C.byref(lv0), len(p), L.ptr(p.xd), L.ptr(p.pd), p.pd.stride(0),
+                self.material.lam, self.material.mu, self.material.alpha, L.ptr(grid.ras),
+                grid.ras.stride(0), float(self.powder.eta_surface), L.ptr(self._tmp), dcode,
+                L.ptr(grid._err), s), "stress_raster")
         lv0 = solver._structs[0]
         pw = self.powder
         L.check(lib.mlbm_powder(L.C.byref(lv0), L.fields(solver.arrays(r, 0).data),

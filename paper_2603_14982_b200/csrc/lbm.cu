@@ -359,11 +359,14 @@ namespace tp {
 MLBM_HD constexpr double hp(int n, int c) { return n == 0 ? 1.0 : n == 1 ? (double)c : (double)(c * c) - CS2; }
 MLBM_HD constexpr double w1(int c) { return c == 0 ? 2.0 / 3.0 : 1.0 / 6.0; }
 MLBM_HD constexpr bool has3(int nx, int ny, int nz) { return nx + ny + nz <= 3; }
+// D3Q27 direction index of velocity c (common.cuh ordering): 5-bit entries
+// k = (cx+1) + 3 (cy+1) + 9 (cz+1) packed in three words, so a call with
+// unrolled (compile-time) arguments folds to a constant and a runtime call
+// costs a few integer ops (no search over the 27 directions)
 MLBM_HD constexpr int dir3(int cx, int cy, int cz) {
-    int r = -1;
-    for (int i = 0; i < 27; ++i)
-        if (cvec<3>(i, 0) == cx && cvec<3>(i, 1) == cy && cvec<3>(i, 2) == cz) r = i;
-    return r;
+    const int k = (cx + 1) + 3 * (cy + 1) + 9 * (cz + 1);
+    const unsigned long long w = k < 12 ? 0x691158e16656614ull : (k < 24 ? 0x49597958e370402ull : 0x4dfaull);
+    return (int)((w >> (5 * (k % 12))) & 31ull);
 }
 // multiply by a compile-time Hermite value without rounding-neutral folds lost
 template <typename R> __device__ __forceinline__ R hmul(double h, R x) {
@@ -611,14 +614,15 @@ template <int A> MLBM_HD int dir_sel(bool neg, int cu, int cv) {
     return neg ? dir3(cm[0], cm[1], cm[2]) : dir3(cp[0], cp[1], cp[2]);
 }
 
-// runtime-velocity direction index (unrolled compare over the 26 moving directions)
-MLBM_HD int dir_rt(int cx, int cy, int cz) {
-    int dir = 0;
-#pragma unroll
-    for (int i = 1; i < 27; ++i)
-        if (cvec<3>(i, 0) == cx && cvec<3>(i, 1) == cy && cvec<3>(i, 2) == cz) dir = i;
-    return dir;
+constexpr bool dir3_table_ok() {
+    for (int i = 0; i < 27; ++i)
+        if (dir3(cvec<3>(i, 0), cvec<3>(i, 1), cvec<3>(i, 2)) != i) return false;
+    return true;
 }
+static_assert(dir3_table_ok(), "packed D3Q27 direction table");
+
+// runtime-velocity direction index (unrolled compare over the 26 moving directions)
+MLBM_HD int dir_rt(int cx, int cy, int cz) { return dir3(cx, cy, cz); }
 
 template <int A, typename R>
 __device__ __forceinline__ void face_body(const FieldsT<R>& src, R* fb, const int* snb, int f, R h3xyz) {

@@ -1929,9 +1929,15 @@ __global__ void __launch_bounds__(32 * NW) k_p2g_cell2(PartArgs P, TopoL0 t0, Ma
 // k = stencil node k of the current run of particles with equal stencil base;
 // records (base, f, V0 tau) are broadcast from a per-warp slab; per-warp node
 // box copies in shared memory, merged once into HBM (no per-particle atomics).
+// surf (optional, [n0] 0/1): the raster is only READ at entrainment surface
+// cells (k_powder_diffuse), so a run none of whose 27 nodes is a surface cell
+// is skipped before its particles' Kirchhoff stress is evaluated; the sums at
+// surface nodes are unchanged (same runs, same order).  Every run's nodes are
+// still checked for storage (stencil errors as in the reference).
 template <int D, int NW>
 __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0, MatParams mp, float* ras,
-                                                          int64_t rs, mlbm_error_t* err) {
+                                                          int64_t rs, const float* __restrict__ surf,
+                                                          mlbm_error_t* err) {
     constexpr int K = Geo<D>::K, NS = D * (D + 1) / 2, NV = NS + 1;
     constexpr int MAXN = P2G2_MAXN, REC = 16, BT = 32 * NW;
     using PR = PRows<D>;
@@ -1942,17 +1948,15 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
     __shared__ int s_lo[3], s_hi[3];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int p = blockIdx.x * BT + threadIdx.x;
-    const bool valid = p < P.n;
+    const int pw = blockIdx.x * BT + wid * 32;
+    const int nj = max(0, min(32, P.n - pw));
+    const bool valid = lane < nj;
     if (threadIdx.x < 3) { s_lo[threadIdx.x] = 0x7fffffff; s_hi[threadIdx.x] = -0x7fffffff; }
-    // per-particle record: base[3] f[D] V0 tau[NS]
     int base[3] = {0, 0, 0};
-    float f[D], S[NS];
+    float f[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) f[a] = 0.f;
-#pragma unroll
-    for (int k = 0; k < NS; ++k) S[k] = 0.f;
     if (valid) {
-        const float* pp = (const float*)P.p;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
             const double x = P.x[a * P.ps + p];
@@ -1960,37 +1964,77 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
             base[a] = (int)b;
             f[a] = (float)(x - b);
         }
+    }
+    // runs of equal stencil base; node lanes check storage and surface flags
+    const int o[3] = {lane % 3, (lane / 3) % 3, D == 3 ? (lane / 9) % 3 : 0};
+    const bool node_lane = lane < K;
+    bool start = valid;
+    {
+        bool same = lane > 0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) same &= __shfl_up_sync(0xffffffffu, base[a], 1) == base[a];
+        start &= !same;
+    }
+    const unsigned runs_all = __ballot_sync(0xffffffffu, start);
+    unsigned need_runs = 0u, need_parts = 0u;
+    bool bad = false;
+    int bad_at[3] = {0, 0, 0};
+    {
+        unsigned runs = runs_all;
+        while (runs) {
+            const int j0 = __ffs(runs) - 1;
+            runs &= runs - 1;
+            const int j1 = runs ? __ffs(runs) - 1 : nj;
+            int c[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) c[a] = __shfl_sync(0xffffffffu, a < D ? base[a] : 0, j0) + (a < D ? o[a] : 0);
+            bool hit = false;
+            if (node_lane) {
+                bool b2 = false;
+                const int cb[3] = {c[0] - o[0], c[1] - o[1], c[2] - (D == 3 ? o[2] : 0)};
+                const int64_t ni = node_index<D>(t0, c, b2);
+                if (b2 && !bad) { bad = true; bad_at[0] = cb[0]; bad_at[1] = cb[1]; bad_at[2] = cb[2]; }
+                hit = ni >= 0 && (surf == nullptr || surf[ni] != 0.f);
+            }
+            if (__any_sync(0xffffffffu, hit)) {
+                need_runs |= 1u << j0;
+                need_parts |= (j1 >= 32 ? 0xffffffffu : ((1u << j1) - 1u)) & ~((1u << j0) - 1u);
+            }
+        }
+    }
+    const bool need = (need_parts >> lane) & 1u;
+    // block node box over the particles of needed runs
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const int l2 = __reduce_min_sync(0xffffffffu, need ? base[a] : 0x7fffffff);
+        const int h2 = __reduce_max_sync(0xffffffffu, need ? base[a] + 2 : -0x7fffffff);
+        if (lane == 0 && l2 <= h2) { atomicMin(&s_lo[a], l2); atomicMax(&s_hi[a], h2); }
+    }
+    // per-particle record of needed particles: base[3] f[D] V0 tau[NS]
+    float* wslab = &slab[wid * 32 * REC];
+    if (need) {
+        const float* pp = (const float*)P.p;
         float F[D * D], tau[D * D];
 #pragma unroll
         for (int k = 0; k < D * D; ++k) F[k] = pp[(PR::F + k) * P.ps + p];
         kirchhoff<D, float>(F, mp, tau);
         const float V0 = pp[PR::V0 * P.ps + p];
-        int k = 0;
-#pragma unroll
-        for (int a = 0; a < D; ++a)
-#pragma unroll
-            for (int b = a; b < D; ++b) S[k++] = V0 * tau[a * D + b];
-    }
-    __syncthreads();
-    {
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-            const int l2 = __reduce_min_sync(0xffffffffu, valid ? base[a] : 0x7fffffff);
-            const int h2 = __reduce_max_sync(0xffffffffu, valid ? base[a] + 2 : -0x7fffffff);
-            if (lane == 0 && l2 <= h2) { atomicMin(&s_lo[a], l2); atomicMax(&s_hi[a], h2); }
-        }
-    }
-    float* wslab = &slab[wid * 32 * REC];
-    {
         float* r = &wslab[lane * REC];
 #pragma unroll
         for (int a = 0; a < 3; ++a) r[a] = __int_as_float(a < D ? base[a] : 0);
 #pragma unroll
         for (int a = 0; a < D; ++a) r[3 + a] = f[a];
+        int k = 0;
 #pragma unroll
-        for (int k = 0; k < NS; ++k) r[3 + D + k] = S[k];
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = a; b < D; ++b) r[3 + D + (k++)] = V0 * tau[a * D + b];
     }
     __syncthreads();
+    const int any_need = __syncthreads_or(need_runs != 0u);
+    if (bad) report_error(err, MLBM_ERR_STENCIL, 0, bad_at[0], bad_at[1], bad_at[2]);
+    if (!any_need) return;                                   // block-uniform
     int lo[3] = {0, 0, 0}, ext[3] = {1, 1, 1}, nbox = 1;
 #pragma unroll
     for (int a = 0; a < D; ++a) { lo[a] = s_lo[a]; ext[a] = s_hi[a] - s_lo[a] + 1; nbox *= ext[a]; }
@@ -2006,8 +2050,6 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
     }
     __syncthreads();
 
-    const int o[3] = {lane % 3, (lane / 3) % 3, D == 3 ? (lane / 9) % 3 : 0};
-    const bool node_lane = lane < K;
     float c0[D], c1[D], c2[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
@@ -2017,22 +2059,13 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
         c0[a] = oa == 0 ? 1.125f : (oa == 1 ? -0.25f : 0.125f);
     }
     float* wacc = sacc + wid * NV * MAXN;
-    const int pw = blockIdx.x * BT + wid * 32;
-    const int nj = max(0, min(32, P.n - pw));
-    bool bad = false;
-    int cur[3] = {0, 0, 0};
-    bool start = lane < nj;
-    {
-        bool same = lane > 0;
-#pragma unroll
-        for (int a = 0; a < D; ++a) same &= __shfl_up_sync(0xffffffffu, base[a], 1) == base[a];
-        start &= !same;
-    }
-    unsigned runs = __ballot_sync(0xffffffffu, start);
+    unsigned runs = need_runs;
     while (runs) {
         const int j0 = __ffs(runs) - 1;
         runs &= runs - 1;
-        const int j1 = runs ? __ffs(runs) - 1 : nj;
+        const unsigned later = runs_all & ~((2u << j0) - 1u);   // next run start after j0
+        const int j1 = later ? __ffs(later) - 1 : nj;
+        int cur[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) cur[a] = __shfl_sync(0xffffffffu, a < D ? base[a] : 0, j0);
         float acc[NV];
@@ -2065,7 +2098,8 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
 #pragma unroll
                 for (int q = 0; q < NV; ++q) wacc[q * MAXN + li] += acc[q];
             } else {
-                const int64_t ni = node_index<D>(t0, c, bad);
+                bool b2 = false;
+                const int64_t ni = node_index<D>(t0, c, b2);
                 if (ni >= 0) {
 #pragma unroll
                     for (int q = 0; q < NS; ++q) atomicAdd(&ras[(RW::SIG + q) * rs + ni], acc[q]);
@@ -2074,10 +2108,43 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
         }
         __syncwarp();
     }
-    if (bad) report_error(err, MLBM_ERR_STENCIL, 0, cur[0], cur[1], cur[2]);
     if (!use_smem) return;
     __syncthreads();
     p2g_box_merge<D, NV, 1>(sacc, NW, MAXN, nbox, lo, ext, t0, ras + (int64_t)RW::SIG * rs, rs, err);
+}
+
+// entrainment surface cells of level 0 (the source condition of
+// k_powder_diffuse, coupling.py:300-316, without the speed test): 0 < eta <
+// eta_surface and an absent / empty (eta < 1e-3) face neighbour
+template <int D, typename R>
+__global__ void k_surface_cells(mlbm_level_t lv, const R* __restrict__ ras, int64_t rs, double eta_surface,
+                                float* __restrict__ surf) {
+    constexpr int T = Geo<D>::T;
+    using RW = Rows<D>;
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= (int64_t)live_tiles(lv) * T) return;
+    const int slot = (int)(c / T), lc = (int)(c % T);
+    const R eta_c = ras[RW::ETA * rs + c];
+    bool s = eta_c > R(0) && eta_c < R(eta_surface);
+    if (s) {
+        const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
+        int g[3] = {0, 0, 0};
+        for (int a = 0; a < D; ++a) g[a] = lv.tile_xyz[slot * 3 + a] * 4 + l3[a];
+        bool has_empty = false;
+        for (int a = 0; a < D; ++a)
+            for (int sgn = 0; sgn < 2; ++sgn) {
+                int nb[3] = {g[0], g[1], g[2]};
+                nb[a] += sgn == 0 ? 1 : -1;
+                if (lv.periodic[a]) nb[a] = (nb[a] + lv.cells[a]) % lv.cells[a];
+                else nb[a] = nb[a] < 0 ? 0 : (nb[a] >= lv.cells[a] ? lv.cells[a] - 1 : nb[a]);
+                const int sl = lv.tile_map[g3(lv.tiles, nb[0] >> 2, nb[1] >> 2, D == 3 ? nb[2] >> 2 : 0)];
+                if (sl < 0) has_empty = true;
+                else if (ras[RW::ETA * rs + (int64_t)sl * T + local_of<D>(nb[0] & 3, nb[1] & 3, nb[2] & 3)] < R(1e-3))
+                    has_empty = true;
+            }
+        s = has_empty;
+    }
+    surf[c] = s ? 1.f : 0.f;
 }
 
 }  // namespace mlbm
@@ -2207,11 +2274,9 @@ extern "C" int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, const double* x_in, 
     return launch_status(1);
 }
 
-extern "C" int mlbm_stress_raster(const mlbm_level_t* lv0, int32_t n, const double* x, const void* p,
-                                  int64_t ps, double lam, double mu, double alpha, void* ras, int64_t rs,
-                                  int32_t dtype, mlbm_error_t* err, void* stream) {
-    if (n <= 0) return 0;
-    cudaStream_t s = as_stream(stream);
+static int stress_raster_impl(const mlbm_level_t* lv0, int32_t n, const double* x, const void* p,
+                              int64_t ps, double lam, double mu, double alpha, void* ras, int64_t rs,
+                              int32_t dtype, const float* surf, mlbm_error_t* err, cudaStream_t s) {
     PartArgs P{lv0->dim, n, x, nullptr, (void*)p, ps, nullptr, nullptr, nullptr};
     MatParams mp{lam, mu, alpha, 0.0};
     const TopoL0 t = topo0(lv0);
@@ -2225,15 +2290,44 @@ extern "C" int mlbm_stress_raster(const mlbm_level_t* lv0, int32_t n, const doub
             cudaFuncSetAttribute(k_stress_cell2<2, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
             attr = true;
         }
-        if (lv0->dim == 2) k_stress_cell2<2, NW><<<nblk(n, 32 * NW), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
-        else k_stress_cell2<3, NW><<<nblk(n, 32 * NW), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
-        return launch_status(1);
+        if (lv0->dim == 2) k_stress_cell2<2, NW><<<nblk(n, 32 * NW), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, surf, err);
+        else k_stress_cell2<3, NW><<<nblk(n, 32 * NW), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, surf, err);
+        return 1;
     }
 #define SR(D, R) k_stress_raster<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err)
     if (lv0->dim == 2) { if (dtype) SR(2, double); else SR(2, float); }
     else { if (dtype) SR(3, double); else SR(3, float); }
 #undef SR
-    return launch_status(1);
+    return 1;
+}
+
+extern "C" int mlbm_stress_raster(const mlbm_level_t* lv0, int32_t n, const double* x, const void* p,
+                                  int64_t ps, double lam, double mu, double alpha, void* ras, int64_t rs,
+                                  int32_t dtype, mlbm_error_t* err, void* stream) {
+    if (n <= 0) return 0;
+    const int k = stress_raster_impl(lv0, n, x, p, ps, lam, mu, alpha, ras, rs, dtype, nullptr, err,
+                                     as_stream(stream));
+    return launch_status(k);
+}
+
+extern "C" int mlbm_stress_raster_surface(const mlbm_level_t* lv0, int32_t n, const double* x,
+                                          const void* p, int64_t ps, double lam, double mu, double alpha,
+                                          void* ras, int64_t rs, double eta_surface, void* surf,
+                                          int32_t dtype, mlbm_error_t* err, void* stream) {
+    if (n <= 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    if (dtype != 0)   // fp64 (parity runs): the full raster
+        return launch_status(stress_raster_impl(lv0, n, x, p, ps, lam, mu, alpha, ras, rs, dtype, nullptr,
+                                                err, s));
+    const int T = lv0->dim == 2 ? 16 : 64;
+    const int64_t ncell = (int64_t)lv0->n_tiles * T;
+    if (ncell > 0) {
+        if (lv0->dim == 2) k_surface_cells<2, float><<<nblk(ncell, 256), 256, 0, s>>>(*lv0, (const float*)ras, rs, eta_surface, (float*)surf);
+        else k_surface_cells<3, float><<<nblk(ncell, 256), 256, 0, s>>>(*lv0, (const float*)ras, rs, eta_surface, (float*)surf);
+    }
+    const int k = stress_raster_impl(lv0, n, x, p, ps, lam, mu, alpha, ras, rs, dtype, (const float*)surf,
+                                     err, s);
+    return launch_status(k + (ncell > 0 ? 1 : 0));
 }
 
 extern "C" int mlbm_powder(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm_fields_t dst, void* ras,
