@@ -42,10 +42,35 @@ struct TopoL0 {
 
 MLBM_HD int64_t g3(const int* d, int x, int y, int z) { return ((int64_t)x * d[1] + y) * d[2] + z; }
 
+// periodic wrap of a coordinate that is almost always within one period of
+// the domain (stencil / box nodes): compare-and-add, modulo only otherwise
+__device__ __forceinline__ int wrap_near(int c, int n) {
+    if (c < 0) c += n;
+    else if (c >= n) c -= n;
+    if ((unsigned)c >= (unsigned)n) c = ((c % n) + n) % n;
+    return c;
+}
+
+// coordinates of entry i of a node box with extents ext (x fastest): the
+// divisions run in fp32 (i < 2^20, ext <= 2^10: (i + 0.5) / e is at least
+// 0.5 / e away from an integer, far above the reciprocal's rounding error)
+template <int D>
+__device__ __forceinline__ void box_coord(int i, const int (&lo)[3], const int (&ext)[3], int (&c)[3]) {
+    c[0] = c[1] = c[2] = 0;
+    int r = i;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        if (a == D - 1) { c[a] = lo[a] + r; break; }
+        const int q = (int)(((float)r + 0.5f) * __frcp_rn((float)ext[a]));
+        c[a] = lo[a] + (r - q * ext[a]);
+        r = q;
+    }
+}
+
 template <int D>
 __device__ __forceinline__ int64_t node_index(const TopoL0& t, int (&c)[3], bool& bad) {
     for (int a = 0; a < D; ++a) {
-        if (t.periodic[a]) c[a] = ((c[a] % t.cells[a]) + t.cells[a]) % t.cells[a];
+        if (t.periodic[a]) c[a] = wrap_near(c[a], t.cells[a]);
         else if (c[a] < 0 || c[a] >= t.cells[a]) { bad = true; return -1; }
     }
     const int s = t.tile_map[g3(t.tiles, c[0] >> 2, c[1] >> 2, D == 3 ? c[2] >> 2 : 0)];
@@ -549,9 +574,8 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
     const bool use_box = nbox > 0 && nbox <= MAXB;      // block-uniform
     if (use_box) {
         for (int i = threadIdx.x; i < nbox; i += blockDim.x) {
-            int c[3] = {0, 0, 0}, r = i;
-#pragma unroll
-            for (int a = 0; a < D; ++a) { c[a] = blo[a] + r % bext[a]; r /= bext[a]; }
+            int c[3];
+            box_coord<D>(i, blo, bext, c);
             bool nb = false;
             const int64_t ni = node_index<D>(t0, c, nb);
 #pragma unroll
@@ -590,6 +614,41 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
 #pragma unroll
             for (int o = 0; o < 3; ++o) { oy[o] = o * bext[0]; oz[o] = D == 3 ? o * bext[0] * bext[1] : 0; }
         }
+        if constexpr (D == 3) {
+            // sum factorisation over the tensor-product stencil: z, then y,
+            // then x contractions of the 27 node velocities (v and the APIC
+            // moments B = sum w v dx^T: 93 instead of 135 FMAs per component)
+            R wz[3], wdz[3], wy[3], wdy[3], wx[3], wdx[3];
+#pragma unroll
+            for (int o = 0; o < 3; ++o) {
+                wx[o] = st.w[0][o]; wdx[o] = st.w[0][o] * dp[0][o];
+                wy[o] = st.w[1][o]; wdy[o] = st.w[1][o] * dp[1][o];
+                wz[o] = st.w[2][o]; wdz[o] = st.w[2][o] * dp[2][o];
+            }
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                R T0[3], Ty[3], Tz[3];
+#pragma unroll
+                for (int ox = 0; ox < 3; ++ox) {
+                    R t0 = R(0), ty = R(0), tz = R(0);
+#pragma unroll
+                    for (int oyy = 0; oyy < 3; ++oyy) {
+                        const int b0 = pb + ox + oy[oyy];
+                        const R g0 = svel[a][b0 + oz[0]], g1 = svel[a][b0 + oz[1]], g2 = svel[a][b0 + oz[2]];
+                        const R s0 = wz[0] * g0 + wz[1] * g1 + wz[2] * g2;
+                        const R s1 = wdz[0] * g0 + wdz[1] * g1 + wdz[2] * g2;
+                        t0 += wy[oyy] * s0;
+                        ty += wdy[oyy] * s0;
+                        tz += wy[oyy] * s1;
+                    }
+                    T0[ox] = t0; Ty[ox] = ty; Tz[ox] = tz;
+                }
+                v[a] = wx[0] * T0[0] + wx[1] * T0[1] + wx[2] * T0[2];
+                B[a * 3 + 0] = wdx[0] * T0[0] + wdx[1] * T0[1] + wdx[2] * T0[2];
+                B[a * 3 + 1] = wx[0] * Ty[0] + wx[1] * Ty[1] + wx[2] * Ty[2];
+                B[a * 3 + 2] = wx[0] * Tz[0] + wx[1] * Tz[1] + wx[2] * Tz[2];
+            }
+        } else {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int o[3] = {k % 3, (k / 3) % 3, D == 3 ? k / 9 : 0};
@@ -604,6 +663,7 @@ __global__ void __launch_bounds__(128) k_g2p(PartArgs P, TopoL0 t0, MatParams mp
 #pragma unroll
                 for (int b = 0; b < D; ++b) B[a * D + b] += wg * dp[b][o[b]];
             }
+        }
         }
 #pragma unroll
         for (int a = 0; a < D; ++a) bad |= isnan((double)v[a]);
@@ -1056,7 +1116,7 @@ __global__ void k_sort_keys(int n, const double* x, int64_t ps, TopoL0 t0, uint3
     int c[3] = {0, 0, 0};
     for (int a = 0; a < D; ++a) {
         int b = (int)floor(x[a * ps + p] - 0.5);
-        if (t0.periodic[a]) b = ((b % t0.cells[a]) + t0.cells[a]) % t0.cells[a];
+        if (t0.periodic[a]) b = wrap_near(b, t0.cells[a]);
         else b = b < 0 ? 0 : (b >= t0.cells[a] ? t0.cells[a] - 1 : b);
         c[a] = b;
     }
@@ -1738,10 +1798,8 @@ __device__ __forceinline__ void p2g_box_merge(const float* sacc, int NW, int MAX
             tot[qv] = v;
         }
         if (STRESS ? tot[NV - 1] == 0.f : (tot[0] == 0.f && tot[2 + 2 * D] == 0.f)) continue;
-        int c[3] = {0, 0, 0};
-        int rr = i;
-#pragma unroll
-        for (int a = 0; a < D; ++a) { c[a] = lo[a] + rr % ext[a]; rr /= ext[a]; }
+        int c[3];
+        box_coord<D>(i, lo, ext, c);
         bool b2 = false;
         const int64_t ni = node_index<D>(t0, c, b2);
         if (ni < 0) { report_error(err, MLBM_ERR_STENCIL, 0, c[0], c[1], c[2]); continue; }

@@ -8,7 +8,13 @@ import torch
 import scenes as S
 from paper_2603_14982_b200 import _lib as L
 from paper_2603_14982_b200.harness import build_scene, validate_scene
-sim = build_scene(validate_scene(getattr(S, os.environ.get("SCENE", "SANDSTORM_3D_C3"))))
+_sc = os.environ.get("SCENE", "SANDSTORM_3D_C3")
+if _sc == "AVALANCHE_C4":
+    import tempfile
+    _scd = S.avalanche_c4(os.path.join(tempfile.mkdtemp(), "terrain.npy"))
+else:
+    _scd = getattr(S, _sc)
+sim = build_scene(validate_scene(_scd))
 for _ in range(4):
     sim.step()
 torch.cuda.synchronize()

@@ -8,7 +8,13 @@ from paper_2603_14982_b200 import _lib as L
 from paper_2603_14982_b200.harness import build_scene, validate_scene
 import os
 sc = os.environ.get("SCENE", "COLUMN_3D_C2")
-sim = build_scene(validate_scene(getattr(S, sc)))
+_sc = sc
+if _sc == "AVALANCHE_C4":
+    import tempfile
+    _scd = S.avalanche_c4(os.path.join(tempfile.mkdtemp(), "terrain.npy"))
+else:
+    _scd = getattr(S, _sc)
+sim = build_scene(validate_scene(_scd))
 if sc == "CLOUD_3D_C5":
     S.cloud_velocities(sim)
 for _ in range(12):
