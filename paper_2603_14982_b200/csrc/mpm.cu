@@ -922,7 +922,9 @@ __global__ void k_powder_advect(PowderArgs A) {
     const R* u[D];
     for (int a = 0; a < D; ++a) u[a] = &dst.at(1 + a, 0);
     double k1[D], k2[D], k3[D], q[D];
-    sample_lin_n<D, R, D>(u, pos, A.lv, k1);
+    // k1 samples at the cell's own (integer) position: weight 1 on the cell,
+    // exact zeros elsewhere, so the renormalised sample is the cell value
+    for (int a = 0; a < D; ++a) k1[a] = (double)u[a][c];
     for (int a = 0; a < D; ++a) q[a] = pos[a] - 0.5 * A.dt * k1[a];
     sample_lin_n<D, R, D>(u, q, A.lv, k2);
     for (int a = 0; a < D; ++a) q[a] = pos[a] - 0.75 * A.dt * k2[a];

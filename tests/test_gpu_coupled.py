@@ -173,6 +173,23 @@ def test_fp32_column_3d_short():
     assert rv <= 1e-4, rv
 
 
+def test_avalanche_terrain_3d_small(tmp_path):
+    """Config 4 ingredients at test size: two levels, a terrain heightmap under
+    a granular slab (solids near the refined region), outlets, powder on —
+    gate A against the oracle (tile sets, streaks, fields, particles)."""
+    hf = S.terrain_heightfield((32, 32, 32), str(tmp_path / "terrain.npy"))
+    sc = {"domain": {"cells": [32, 32, 32], "levels": 2},
+          "fluid": {"tau0": 1.8, "eps_min": 0.5, "gravity": [0.0, -1e-4, 0.0]},
+          "boundaries": {"x_min": "outlet", "x_max": "outlet", "y_min": "wall",
+                         "y_max": "outlet", "z_min": "outlet", "z_max": "outlet",
+                         "heightfield": hf},
+          "materials": {"density_ratio": 40.0, "E": 0.08},
+          "particles": {"blocks": [[8.0, 4.0, 8.0, 24.0, 8.0, 24.0]], "per_cell": 2},
+          "powder": {"enabled": True, "entrain": 0.02, "diffusion": 0.05},
+          "runtime": {"seed": 7}}
+    run_and_compare(sc, 6)
+
+
 def test_fp32_powder_3d_short():
     """Gate B with powder + entrainment (the fp32 stress raster in the P2G
     layout and the shared-corner RK3 backtrace): fp32 device vs fp64 oracle."""
