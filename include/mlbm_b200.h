@@ -316,10 +316,11 @@ int mlbm_stress_raster(const mlbm_level_t* lv0, int32_t n, const double* x, cons
                        int64_t ps, double lam, double mu, double alpha, void* ras, int64_t rs,
                        int32_t dtype, mlbm_error_t* err, void* stream);
 /* fp32: the stress raster restricted to the entrainment surface (the only
- * cells k_powder reads it at): surf [n0] floats receives the surface flags
- * (0 < eta < eta_surface with an absent / empty face neighbour), runs of
- * particles none of whose stencil nodes is a surface cell are skipped; the
- * sums at surface cells equal mlbm_stress_raster's.  fp64: the full raster. */
+ * cells k_powder reads it at).  surf [n0] floats receives 2 on surface cells
+ * (0 < eta < eta_surface with an absent / empty face neighbour) and 1 on the
+ * other cells of their 3^D neighbourhoods; particles whose nearest node has
+ * surf == 0 (no surface cell in their stencil) are skipped, so the sums at
+ * surface cells equal mlbm_stress_raster's.  fp64: the full raster. */
 int mlbm_stress_raster_surface(const mlbm_level_t* lv0, int32_t n, const double* x,
                                const void* p, int64_t ps, double lam, double mu, double alpha,
                                void* ras, int64_t rs, double eta_surface, void* surf,

@@ -2025,44 +2025,31 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
             f[a] = (float)(x - b);
         }
     }
-    // runs of equal stencil base; node lanes check storage and surface flags
+    // a particle's stencil is the 3^D node box centred on its nearest node
+    // m = floor(x + 1/2) = base + 1; need[m] marks boxes that contain an
+    // entrainment surface cell (k_surface_need), so one lookup per particle
+    // decides whether its stress is rasterised at all
+    bool need = false;
+    bool bad = false;
+    if (valid) {
+        int m[3] = {base[0] + 1, base[1] + 1, D == 3 ? base[2] + 1 : 0};
+        const int64_t ni = node_index<D>(t0, m, bad);
+        need = ni >= 0 && (surf == nullptr || surf[ni] != 0.f);
+    }
     const int o[3] = {lane % 3, (lane / 3) % 3, D == 3 ? (lane / 9) % 3 : 0};
     const bool node_lane = lane < K;
-    bool start = valid;
+    // runs of equal stencil base among the needed particles
+    bool start = need;
     {
         bool same = lane > 0;
 #pragma unroll
         for (int a = 0; a < D; ++a) same &= __shfl_up_sync(0xffffffffu, base[a], 1) == base[a];
+        same &= __shfl_up_sync(0xffffffffu, (int)need, 1) != 0;
         start &= !same;
     }
-    const unsigned runs_all = __ballot_sync(0xffffffffu, start);
-    unsigned need_runs = 0u, need_parts = 0u;
-    bool bad = false;
-    int bad_at[3] = {0, 0, 0};
-    {
-        unsigned runs = runs_all;
-        while (runs) {
-            const int j0 = __ffs(runs) - 1;
-            runs &= runs - 1;
-            const int j1 = runs ? __ffs(runs) - 1 : nj;
-            int c[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) c[a] = __shfl_sync(0xffffffffu, a < D ? base[a] : 0, j0) + (a < D ? o[a] : 0);
-            bool hit = false;
-            if (node_lane) {
-                bool b2 = false;
-                const int cb[3] = {c[0] - o[0], c[1] - o[1], c[2] - (D == 3 ? o[2] : 0)};
-                const int64_t ni = node_index<D>(t0, c, b2);
-                if (b2 && !bad) { bad = true; bad_at[0] = cb[0]; bad_at[1] = cb[1]; bad_at[2] = cb[2]; }
-                hit = ni >= 0 && (surf == nullptr || surf[ni] != 0.f);
-            }
-            if (__any_sync(0xffffffffu, hit)) {
-                need_runs |= 1u << j0;
-                need_parts |= (j1 >= 32 ? 0xffffffffu : ((1u << j1) - 1u)) & ~((1u << j0) - 1u);
-            }
-        }
-    }
-    const bool need = (need_parts >> lane) & 1u;
+    const unsigned need_runs = __ballot_sync(0xffffffffu, start);
+    const unsigned need_parts = __ballot_sync(0xffffffffu, need);
+    const int bad_at[3] = {base[0] + 1, base[1] + 1, base[2] + (D == 3 ? 1 : 0)};
     // block node box over the particles of needed runs
     __syncthreads();
 #pragma unroll
@@ -2123,8 +2110,10 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
     while (runs) {
         const int j0 = __ffs(runs) - 1;
         runs &= runs - 1;
-        const unsigned later = runs_all & ~((2u << j0) - 1u);   // next run start after j0
-        const int j1 = later ? __ffs(later) - 1 : nj;
+        // the run ends at the next run start or at the first non-needed lane
+        const unsigned after = ~((2u << j0) - 1u);
+        const unsigned stop = (need_runs | ~need_parts) & after;
+        const int j1 = stop ? __ffs(stop) - 1 : 32;
         int cur[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) cur[a] = __shfl_sync(0xffffffffu, a < D ? base[a] : 0, j0);
@@ -2175,36 +2164,51 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
 
 // entrainment surface cells of level 0 (the source condition of
 // k_powder_diffuse, coupling.py:300-316, without the speed test): 0 < eta <
-// eta_surface and an absent / empty (eta < 1e-3) face neighbour
+// eta_surface and an absent / empty (eta < 1e-3) face neighbour.  Every
+// surface cell marks need = 1 on the stored cells of its 3^D neighbourhood,
+// i.e. on every nearest node whose stencil box contains it, and 2 on itself
+// (need zeroed by the caller)
 template <int D, typename R>
-__global__ void k_surface_cells(mlbm_level_t lv, const R* __restrict__ ras, int64_t rs, double eta_surface,
-                                float* __restrict__ surf) {
+__global__ void k_surface_need(mlbm_level_t lv, const R* __restrict__ ras, int64_t rs, double eta_surface,
+                               float* __restrict__ need) {
     constexpr int T = Geo<D>::T;
     using RW = Rows<D>;
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= (int64_t)live_tiles(lv) * T) return;
-    const int slot = (int)(c / T), lc = (int)(c % T);
     const R eta_c = ras[RW::ETA * rs + c];
-    bool s = eta_c > R(0) && eta_c < R(eta_surface);
-    if (s) {
-        const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
-        int g[3] = {0, 0, 0};
-        for (int a = 0; a < D; ++a) g[a] = lv.tile_xyz[slot * 3 + a] * 4 + l3[a];
-        bool has_empty = false;
-        for (int a = 0; a < D; ++a)
-            for (int sgn = 0; sgn < 2; ++sgn) {
-                int nb[3] = {g[0], g[1], g[2]};
-                nb[a] += sgn == 0 ? 1 : -1;
-                if (lv.periodic[a]) nb[a] = (nb[a] + lv.cells[a]) % lv.cells[a];
-                else nb[a] = nb[a] < 0 ? 0 : (nb[a] >= lv.cells[a] ? lv.cells[a] - 1 : nb[a]);
-                const int sl = lv.tile_map[g3(lv.tiles, nb[0] >> 2, nb[1] >> 2, D == 3 ? nb[2] >> 2 : 0)];
-                if (sl < 0) has_empty = true;
-                else if (ras[RW::ETA * rs + (int64_t)sl * T + local_of<D>(nb[0] & 3, nb[1] & 3, nb[2] & 3)] < R(1e-3))
-                    has_empty = true;
-            }
-        s = has_empty;
+    if (!(eta_c > R(0) && eta_c < R(eta_surface))) return;
+    const int slot = (int)(c / T), lc = (int)(c % T);
+    const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
+    int g[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) g[a] = lv.tile_xyz[slot * 3 + a] * 4 + l3[a];
+    bool has_empty = false;
+    for (int a = 0; a < D; ++a)
+        for (int sgn = 0; sgn < 2; ++sgn) {
+            int nb[3] = {g[0], g[1], g[2]};
+            nb[a] += sgn == 0 ? 1 : -1;
+            if (lv.periodic[a]) nb[a] = (nb[a] + lv.cells[a]) % lv.cells[a];
+            else nb[a] = nb[a] < 0 ? 0 : (nb[a] >= lv.cells[a] ? lv.cells[a] - 1 : nb[a]);
+            const int sl = lv.tile_map[g3(lv.tiles, nb[0] >> 2, nb[1] >> 2, D == 3 ? nb[2] >> 2 : 0)];
+            if (sl < 0) has_empty = true;
+            else if (ras[RW::ETA * rs + (int64_t)sl * T + local_of<D>(nb[0] & 3, nb[1] & 3, nb[2] & 3)] < R(1e-3))
+                has_empty = true;
+        }
+    if (!has_empty) return;
+    for (int k = 0; k < Geo<D>::K; ++k) {
+        int q[3] = {g[0] + k % 3 - 1, g[1] + (k / 3) % 3 - 1, D == 3 ? g[2] + k / 9 - 1 : 0};
+        bool out = false;
+        for (int a = 0; a < D; ++a) {
+            if (lv.periodic[a]) q[a] = (q[a] + lv.cells[a]) % lv.cells[a];
+            else if (q[a] < 0 || q[a] >= lv.cells[a]) out = true;
+        }
+        if (out) continue;
+        const int sl = lv.tile_map[g3(lv.tiles, q[0] >> 2, q[1] >> 2, D == 3 ? q[2] >> 2 : 0)];
+        if (sl < 0) continue;
+        // 2 on the surface cell itself, 1 on its neighbours (max wins)
+        const float v = k == Geo<D>::K / 2 ? 2.f : 1.f;
+        atomicMax(reinterpret_cast<int*>(&need[(int64_t)sl * T + local_of<D>(q[0] & 3, q[1] & 3, q[2] & 3)]),
+                  __float_as_int(v));
     }
-    surf[c] = s ? 1.f : 0.f;
 }
 
 }  // namespace mlbm
@@ -2382,8 +2386,9 @@ extern "C" int mlbm_stress_raster_surface(const mlbm_level_t* lv0, int32_t n, co
     const int T = lv0->dim == 2 ? 16 : 64;
     const int64_t ncell = (int64_t)lv0->n_tiles * T;
     if (ncell > 0) {
-        if (lv0->dim == 2) k_surface_cells<2, float><<<nblk(ncell, 256), 256, 0, s>>>(*lv0, (const float*)ras, rs, eta_surface, (float*)surf);
-        else k_surface_cells<3, float><<<nblk(ncell, 256), 256, 0, s>>>(*lv0, (const float*)ras, rs, eta_surface, (float*)surf);
+        cudaMemsetAsync(surf, 0, (size_t)ncell * sizeof(float), s);
+        if (lv0->dim == 2) k_surface_need<2, float><<<nblk(ncell, 256), 256, 0, s>>>(*lv0, (const float*)ras, rs, eta_surface, (float*)surf);
+        else k_surface_need<3, float><<<nblk(ncell, 256), 256, 0, s>>>(*lv0, (const float*)ras, rs, eta_surface, (float*)surf);
     }
     const int k = stress_raster_impl(lv0, n, x, p, ps, lam, mu, alpha, ras, rs, dtype, (const float*)surf,
                                      err, s);

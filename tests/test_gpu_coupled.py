@@ -265,8 +265,9 @@ def test_stress_raster_fp32_kernels_agree():
     scale = out[0].abs().amax(dim=1, keepdim=True).clamp_min(1e-30)
     assert out[0].abs().max().item() > 0.0
     assert ((out[1] - out[0]).abs() / scale).max().item() <= 1e-5
-    m = surf[:grid._live()] != 0
+    m = surf[:grid._live()] == 2.0          # the entrainment surface cells
     assert int(m.sum().item()) > 0
+    assert int((surf[:grid._live()] == 1.0).sum().item()) > 0
     assert ((restricted[:, m] - out[0][:, m]).abs() / scale).max().item() <= 1e-5
 
 

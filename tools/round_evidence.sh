@@ -1,11 +1,13 @@
 #!/bin/bash
 # Round evidence for profiles/ (run under gpurun, 1 GPU): bench lines for C2
-# (default), C3 and C1, then — each only after its plain command exited 0 —
-# an ncu launch list of a short C2 bench and one ncu --set full capture of the
-# top kernels.
+# (default), C3, C4, C5 and C1, then — each only after its plain command
+# exited 0 — an ncu launch list of a short C2 bench and ncu --set full
+# captures of the top kernels on C2 and C4.
 mkdir -p gpurun_out
 python bench.py --steps 60 --warmup 20 > gpurun_out/ev_bench_c2.json 2> gpurun_out/ev_bench_c2.err; echo "bench c2 rc=$?"
 python bench.py --scene c3 --steps 30 --warmup 10 --no-cpu-baseline > gpurun_out/ev_bench_c3.json 2> gpurun_out/ev_bench_c3.err; echo "bench c3 rc=$?"
+python bench.py --scene c4 --steps 20 --warmup 5 > gpurun_out/ev_bench_c4.json 2> gpurun_out/ev_bench_c4.err; echo "bench c4 rc=$?"
+python bench.py --scene c5 --steps 30 --warmup 10 --no-cpu-baseline > gpurun_out/ev_bench_c5.json 2> gpurun_out/ev_bench_c5.err; echo "bench c5 rc=$?"
 python bench.py --scene c1 --steps 60 --warmup 10 > gpurun_out/ev_bench_c1.json 2> gpurun_out/ev_bench_c1.err; echo "bench c1 rc=$?"
 CMD="python bench.py --steps 8 --warmup 4 --no-cpu-baseline --no-e2e"
 $CMD > gpurun_out/ev_plain.log 2>&1 && \
@@ -17,4 +19,10 @@ SCENE=COLUMN_3D_C2 $CMD2 > gpurun_out/ev_plain2.log 2>&1 && \
 SCENE=COLUMN_3D_C2 ncu --set full --clock-control none --import-source on \
     -k regex:"level_kernel|k_p2g_cell2|k_g2p|k_adapt_pass|k_exchange|downward_kernel" -c 12 \
     -o gpurun_out/ev_full $CMD2 > gpurun_out/ev_ncu_full.log 2>&1
-echo "full set rc=$?"
+echo "full set c2 rc=$?"
+CMD3="python tools/kernel_probe.py 1"
+SCENE=AVALANCHE_C4 WARM=3 $CMD3 > gpurun_out/ev_plain3.log 2>&1 && \
+SCENE=AVALANCHE_C4 WARM=3 ncu --set full --clock-control none --import-source on \
+    -k regex:"level_kernel|k_p2g_cell2|k_g2p|k_stress_cell2|k_powder_advect|k_exchange|k_adapt_pass" -c 8 \
+    -o gpurun_out/ev_full_c4 $CMD3 > gpurun_out/ev_ncu_full_c4.log 2>&1
+echo "full set c4 rc=$?"
