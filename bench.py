@@ -119,11 +119,18 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def dram_traffic():
+TRAFFIC_FILES = {"c2": "r1_dram_traffic.json", "c4": "r1_dram_traffic_c4.json"}
+
+
+def dram_traffic(scene):
     """Per-launch DRAM bytes of the top kernels from the committed ncu full-set
-    capture (profiles/r1_dram_traffic.json, tools/full_summary.py)."""
+    capture of the same workload (profiles/r1_dram_traffic*.json,
+    tools/full_summary.py); {} when no capture of this scene is committed."""
+    fn = TRAFFIC_FILES.get(scene)
+    if fn is None:
+        return {}
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_dram_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", fn)) as f:
             return json.load(f)
     except (OSError, ValueError):
         return {}
@@ -315,7 +322,7 @@ def run_mine(args, rank, world, local_rank):
         c["achieved_gbs"] = c["bytes"] / (c["ms"] * 1e-3) / 1e9 if c["ms"] and c["bytes"] else None
     dom = max((k for k in classes if classes[k]["bytes"]), key=lambda k: classes[k]["ms"])
 
-    traffic = dram_traffic()
+    traffic = dram_traffic(args.scene)
 
     def roof(k):
         c = classes[k]
@@ -328,9 +335,10 @@ def run_mine(args, rank, world, local_rank):
                 "bytes_per_launch": c["bytes"] / c["launches"],
                 "avg_launch_us": 1e3 * c["ms"] / c["launches"],
                 "traffic": tr["bytes_per_launch"] if tr else None,
-                "traffic_source": ("profiles/r1_dram_traffic.json: dram__bytes_read.sum + "
-                                   "dram__bytes_write.sum per launch of " + kern + " from one "
-                                   "ncu --set full capture (C2)") if tr else None}
+                "traffic_source": ("profiles/" + TRAFFIC_FILES.get(args.scene, "") +
+                                   ": dram__bytes_read.sum + dram__bytes_write.sum per launch of "
+                                   + kern + " from one ncu --set full capture ("
+                                   + args.scene.upper() + ")") if tr else None}
 
     lbm_keys = [k for k in classes if k.startswith("level_step")]
     lbm_bytes = sum(classes[k]["bytes"] for k in lbm_keys)

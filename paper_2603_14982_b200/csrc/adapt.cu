@@ -216,6 +216,24 @@ __device__ __forceinline__ bool axis_or2(const uint8_t* src, const int* d, const
     return any;
 }
 
+// OR of src over the sibling-group window [g0 - 2, g0 + 3] (g0 = c & ~1)
+// along one axis (wrap / clip): one factor of group_window_any(r = 2)
+__device__ __forceinline__ bool axis_group_or2(const uint8_t* src, const int* d, const int* per,
+                                               const int (&c)[3], int axis) {
+    const int n = d[axis], g0 = c[axis] & ~1;
+    bool any = false;
+#pragma unroll
+    for (int k = -2; k <= 3; ++k) {
+        int v = g0 + k;
+        if (per[axis]) { v %= n; if (v < 0) v += n; }
+        else if (v < 0 || v >= n) continue;
+        int q[3] = {c[0], c[1], c[2]};
+        q[axis] = v;
+        any |= src[gi3(d, q[0], q[1], q[2])] != 0;
+    }
+    return any;
+}
+
 // Branchless, fully unrolled radius-2 windows: out-of-domain taps are
 // redirected to the centre tile and masked, so all 25 / 125 accesses issue
 // back to back (memory-level parallelism instead of a serial loop).
@@ -489,10 +507,30 @@ __global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
             }
         }
         STAMP_BARRIER(4);
+        // des[l] = align_up(dilate2(par)): the group window [g0 - 2, g0 + 3]
+        // (g0 = c & ~1) per axis, as separable ORs x -> own, y -> stor,
+        // z -> des (own and stor are free here: stor's ring data was consumed
+        // in C, own is written in I)
         for (int64_t g = tid; g < n; g += nth) {
             int c[3];
             dec3(d, g, c[0], c[1], c[2]);
-            A.des[l][g] = group_window_any(A.par[l], d, dim, A.periodic, c, 2);
+            A.own[l][g] = axis_group_or2(A.par[l], d, A.periodic, c, 0);
+        }
+        grid_barrier(A.bar);
+        for (int64_t g = tid; g < n; g += nth) {
+            int c[3];
+            dec3(d, g, c[0], c[1], c[2]);
+            const bool any = axis_group_or2(A.own[l], d, A.periodic, c, 1);
+            if (dim == 3) A.stor[l][g] = any;
+            else A.des[l][g] = any;
+        }
+        if (dim == 3) {
+            grid_barrier(A.bar);
+            for (int64_t g = tid; g < n; g += nth) {
+                int c[3];
+                dec3(d, g, c[0], c[1], c[2]);
+                A.des[l][g] = axis_group_or2(A.stor[l], d, A.periodic, c, 2);
+            }
         }
         STAMP_BARRIER(5);
     }

@@ -20,9 +20,16 @@ SCENE=COLUMN_3D_C2 ncu --set full --clock-control none --import-source on \
     -k regex:"level_kernel|k_p2g_cell2|k_g2p|k_adapt_pass|k_exchange|downward_kernel" -c 12 \
     -o gpurun_out/ev_full $CMD2 > gpurun_out/ev_ncu_full.log 2>&1
 echo "full set c2 rc=$?"
+python tools/full_summary.py gpurun_out/ev_full.ncu-rep gpurun_out/ev_full_summary.txt gpurun_out/ev_dram_traffic.json > /dev/null 2>&1
+for k in k_p2g_cell2 "level_kernel<(int)3, float, (int)1>" k_g2p; do python tools/src_hot.py gpurun_out/ev_full.ncu-rep "$k" 40; done > gpurun_out/ev_src_hot_c2.txt 2>&1
 CMD3="python tools/kernel_probe.py 1"
 SCENE=AVALANCHE_C4 WARM=3 $CMD3 > gpurun_out/ev_plain3.log 2>&1 && \
 SCENE=AVALANCHE_C4 WARM=3 ncu --set full --clock-control none --import-source on \
     -k regex:"level_kernel|k_p2g_cell2|k_g2p|k_stress_cell2|k_powder_advect|k_exchange|k_adapt_pass" -c 8 \
     -o gpurun_out/ev_full_c4 $CMD3 > gpurun_out/ev_ncu_full_c4.log 2>&1
 echo "full set c4 rc=$?"
+python tools/full_summary.py gpurun_out/ev_full_c4.ncu-rep gpurun_out/ev_full_summary_c4.txt gpurun_out/ev_dram_traffic_c4.json > /dev/null 2>&1
+for k in k_p2g_cell2 "level_kernel<(int)3, float, (int)1>" k_g2p k_stress_cell2; do python tools/src_hot.py gpurun_out/ev_full_c4.ncu-rep "$k" 40; done > gpurun_out/ev_src_hot_c4.txt 2>&1
+# the reports stay on the box (gpurun copies back at most 64 MiB)
+rm -f gpurun_out/ev_full_c4.ncu-rep
+du -sh gpurun_out
