@@ -165,7 +165,48 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
 
     int gf[3] = {0, 0, 0};
     for (int a = 0; a < D; ++a) gf[a] = g[a] << level;
-    const bool solid_c = solid_at(solid, D, gf);
+    // solids can only bounce a pull if one lies within one cell of the tile:
+    // boxes are tested against the dilated tile box, the heightmap by its
+    // maximum over the dilated footprint (a tile on a periodic seam is always
+    // scanned)
+    bool near = false;
+    if (solid.n_boxes > 0 || solid.heightmap != nullptr) {
+        bool seam = false;
+        for (int a = 0; a < D; ++a)
+            seam |= lv.periodic[a] && (tx[a] == 0 || tx[a] == lv.tiles[a] - 1);
+        const int sc = 1 << level;
+        int lo[3] = {0, 0, 0}, hi[3] = {1, 1, 1};      // finest, [lo, hi)
+        for (int a = 0; a < D; ++a) { lo[a] = (tx[a] * 4 - 1) * sc; hi[a] = (tx[a] * 4 + 5) * sc; }
+        bool mine = seam;
+        if (lc == 0 && !seam) {
+            for (int b = 0; b < solid.n_boxes && !mine; ++b) {
+                bool in = true;
+                for (int a = 0; a < D; ++a)
+                    in &= solid.boxes[b][a] < (double)hi[a] && solid.boxes[b][3 + a] > (double)lo[a];
+                mine |= in;
+            }
+        }
+        if (solid.heightmap && !seam && !mine) {
+            // footprint columns (x, z) strided over the block; heights clamp
+            // at the map edges exactly as solid_at does
+            const int nx = hi[0] - lo[0], nz = D == 3 ? hi[2] - lo[2] : 1;
+            float hmax = 0.f;
+            for (int i = lc; i < nx * nz; i += T) {
+                const int cx = lo[0] + i % nx, cz = D == 3 ? lo[2] + i / nx : 0;
+                const int hx = cx < 0 ? 0 : (cx >= solid.hm_dims[0] ? solid.hm_dims[0] - 1 : cx);
+                float h;
+                if (D == 2) h = solid.heightmap[hx];
+                else {
+                    const int hz = cz < 0 ? 0 : (cz >= solid.hm_dims[1] ? solid.hm_dims[1] - 1 : cz);
+                    h = solid.heightmap[(int64_t)hx * solid.hm_dims[1] + hz];
+                }
+                hmax = h > hmax ? h : hmax;
+            }
+            mine |= hmax > 0.f && (float)lo[1] < hmax;
+        }
+        near = __syncthreads_or(mine);
+    }
+    const bool solid_c = near && solid_at(solid, D, gf);
     bool bcl = false;
     for (int f = 0; f < 2 * D; ++f) {
         const int k = bc.face[f];
@@ -221,53 +262,12 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
     bool edge = false;
     for (int a = 0; a < D; ++a)
         edge |= !lv.periodic[a] && (tx[a] == 0 || tx[a] == lv.tiles[a] - 1);
-    // solids can only bounce a pull if one lies within one cell of the tile:
-    // boxes are tested against the dilated tile box, the heightmap by its
-    // maximum over the dilated footprint (a tile on a periodic seam is always
-    // scanned)
-    bool near = false;
-    if (solid.n_boxes > 0 || solid.heightmap != nullptr) {
-        bool seam = false;
-        for (int a = 0; a < D; ++a)
-            seam |= lv.periodic[a] && (tx[a] == 0 || tx[a] == lv.tiles[a] - 1);
-        const int sc = 1 << level;
-        int lo[3] = {0, 0, 0}, hi[3] = {1, 1, 1};      // finest, [lo, hi)
-        for (int a = 0; a < D; ++a) { lo[a] = (tx[a] * 4 - 1) * sc; hi[a] = (tx[a] * 4 + 5) * sc; }
-        bool mine = seam;
-        if (lc == 0 && !seam) {
-            for (int b = 0; b < solid.n_boxes && !mine; ++b) {
-                bool in = true;
-                for (int a = 0; a < D; ++a)
-                    in &= solid.boxes[b][a] < (double)hi[a] && solid.boxes[b][3 + a] > (double)lo[a];
-                mine |= in;
-            }
-        }
-        if (solid.heightmap && !seam && !mine) {
-            // footprint columns (x, z) strided over the block; heights clamp
-            // at the map edges exactly as solid_at does
-            const int nx = hi[0] - lo[0], nz = D == 3 ? hi[2] - lo[2] : 1;
-            float hmax = 0.f;
-            for (int i = lc; i < nx * nz; i += T) {
-                const int cx = lo[0] + i % nx, cz = D == 3 ? lo[2] + i / nx : 0;
-                const int hx = cx < 0 ? 0 : (cx >= solid.hm_dims[0] ? solid.hm_dims[0] - 1 : cx);
-                float h;
-                if (D == 2) h = solid.heightmap[hx];
-                else {
-                    const int hz = cz < 0 ? 0 : (cz >= solid.hm_dims[1] ? solid.hm_dims[1] - 1 : cz);
-                    h = solid.heightmap[(int64_t)hx * solid.hm_dims[1] + hz];
-                }
-                hmax = h > hmax ? h : hmax;
-            }
-            mine |= hmax > 0.f && (float)lo[1] < hmax;
-        }
-        near = __syncthreads_or(mine);
-    }
     const bool need = rim || edge || near;
     if (need) {
         // neighbour tile of the pull source from the smem neighbour slots (no
         // tile-map reads); out-of-domain = neighbour tile outside a
         // non-periodic axis
-        bool has_solids = solid.n_boxes > 0 || solid.heightmap != nullptr;
+        const bool has_solids = near;      // no solid within one cell: none to test
 #pragma unroll
         for (int i = 1; i < Q; ++i) {
             int o[3] = {0, 0, 0};
