@@ -249,6 +249,14 @@ int mlbm_migrate_level(int32_t dim, int32_t n_new_tiles, const int32_t* n_dev,
                        mlbm_fields_t old0, mlbm_fields_t old1, mlbm_fields_t new0,
                        mlbm_fields_t new1, int32_t dtype, void* stream);
 
+/* Copy the live cells (device count n_dev, capacity cap_tiles) of two field
+ * blocks into two others of the same stride: the migrated scratch blocks back
+ * into the trees after a rebuild (adapt.py:266-279 replaces the arrays; the
+ * device trees keep their pointers so captured graphs stay valid). */
+int mlbm_copy_live_fields(int32_t dim, int32_t cap_tiles, const int32_t* n_dev,
+                          mlbm_fields_t src0, mlbm_fields_t src1, mlbm_fields_t dst0,
+                          mlbm_fields_t dst1, int32_t dtype, void* stream);
+
 /* New-cell initialisation (adapt.py:301-372): for every cell of a fresh
  * tile of level `level` (new topology `nh`), interpolate from the nearest old
  * coarser level whose stencil is complete (S chain down), else copy the

@@ -137,6 +137,7 @@ _SIGS = {
     "mlbm_check_coverage": [C.POINTER(Hier), P, P],
     "mlbm_count_ring_violations": [I64, P, P, P, P],
     "mlbm_check_particles": [I32, I32, P, I64, I32, P, P, P, P],
+    "mlbm_copy_live_fields": [I32, I32, P, Fields, Fields, Fields, Fields, I32, P],
     "mlbm_migrate_level": [I32, I32, P, P, Fields, Fields, Fields, Fields, I32, P],
     "mlbm_init_new_cells": [C.POINTER(Hier), C.POINTER(Hier), I32, P, P, I32, P,
                             Fields, Fields, P, I32, I32, P, P],

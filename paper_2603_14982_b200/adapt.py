@@ -351,8 +351,11 @@ class GridAdaptor:
                                                     s), "init_new_cells")
             for l in changed:
                 sb = pair.scratch_blocks(l)
-                for t in range(2):
-                    pair.trees[t].levels[l].data.copy_(sb[t])
+                td = [pair.trees[t].levels[l].data for t in range(2)]
+                L.check(lib.mlbm_copy_live_fields(d, topo.lv[l].cap, L.ptr(topo.dcounts[l]),
+                                                  L.fields(sb[0]), L.fields(sb[1]),
+                                                  L.fields(td[0]), L.fields(td[1]), dcode, s),
+                        "copy_live_fields")
             topo.commit_device({l: self._new[l] for l in changed})
         return device
 

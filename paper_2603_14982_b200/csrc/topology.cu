@@ -533,6 +533,22 @@ __global__ void k_migrate(int64_t ncells, const int32_t* n_dev, const int32_t* o
     }
 }
 
+// copy the live cells (device count) of both trees' field blocks in 16-byte
+// vectors (V = 4 floats or 2 doubles); rows are capacity-strided and hold
+// whole tiles (16 / 64 cells), so the live range is a whole number of vectors
+template <int D, typename R, typename V>
+__global__ void k_copy_live(int64_t nvec_row, const int32_t* n_dev, int nf, const V* __restrict__ s0,
+                            const V* __restrict__ s1, V* __restrict__ d0, V* __restrict__ d1,
+                            int64_t stride_vec) {
+    constexpr int T = Geo<D>::T, PER = (int)(sizeof(V) / sizeof(R));
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t row = i / nvec_row, v = i - row * nvec_row;
+    if (row >= nf) return;
+    if (n_dev && v >= (int64_t)__ldg(n_dev) * (T / PER)) return;
+    d0[row * stride_vec + v] = s0[row * stride_vec + v];
+    d1[row * stride_vec + v] = s1[row * stride_vec + v];
+}
+
 MLBM_HD double kap_down(double tf, double tc, int conv) { return conv == 0 ? tf / (2.0 * tc) : 2.0 * tc / tf; }
 MLBM_HD double kap_up(double tf, double tc, int conv) { return conv == 0 ? 2.0 * tc / tf : tc / (2.0 * tf); }
 
@@ -812,6 +828,26 @@ extern "C" int mlbm_migrate_level(int32_t dim, int32_t n_new_tiles, const int32_
     if (dim == 2) { if (dtype) MIG(2, double); else MIG(2, float); }
     else { if (dtype) MIG(3, double); else MIG(3, float); }
 #undef MIG
+    return launch_status(1);
+}
+
+extern "C" int mlbm_copy_live_fields(int32_t dim, int32_t cap_tiles, const int32_t* n_dev,
+                                     mlbm_fields_t src0, mlbm_fields_t src1, mlbm_fields_t dst0,
+                                     mlbm_fields_t dst1, int32_t dtype, void* stream) {
+    if (cap_tiles <= 0) return 0;
+    if (src1.stride != src0.stride || dst0.stride != src0.stride || dst1.stride != src0.stride) return -1;
+    const int es = dtype ? 8 : 4;
+    if ((src0.stride * es) % 16 != 0) return -1;
+    const int T = dim == 2 ? 16 : 64;
+    const int nf = dim == 2 ? Geo<2>::NF : Geo<3>::NF;
+    const int64_t nvec = (int64_t)cap_tiles * T * es / 16, stride_vec = src0.stride * es / 16;
+    const int64_t total = nvec * nf;
+    cudaStream_t s = as_stream(stream);
+#define CPY(D, R, V) k_copy_live<D, R, V><<<blocks_for(total, 256), 256, 0, s>>>(nvec, n_dev, nf, \
+        (const V*)src0.ptr, (const V*)src1.ptr, (V*)dst0.ptr, (V*)dst1.ptr, stride_vec)
+    if (dim == 2) { if (dtype) CPY(2, double, double2); else CPY(2, float, float4); }
+    else { if (dtype) CPY(3, double, double2); else CPY(3, float, float4); }
+#undef CPY
     return launch_status(1);
 }
 
