@@ -202,7 +202,10 @@ __device__ __forceinline__ void sym_eig3(R a00, R a01, R a02, R a11, R a12, R a2
     R A[3][3] = {{a00, a01, a02}, {a01, a11, a12}, {a02, a12, a22}};
 #pragma unroll
     for (int i = 0; i < 9; ++i) Q[i] = (i % 4 == 0) ? R(1) : R(0);
-    const R tol = R(sizeof(R) == 8 ? 1e-32 : 1e-15);
+#ifndef MLBM_JACOBI_TOL32
+#define MLBM_JACOBI_TOL32 1e-15
+#endif
+    const R tol = R(sizeof(R) == 8 ? 1e-32 : MLBM_JACOBI_TOL32);
 #pragma unroll 1
     for (int sweep = 0; sweep < 8; ++sweep) {
         const R off = A[0][1] * A[0][1] + A[0][2] * A[0][2] + A[1][2] * A[1][2];
