@@ -772,8 +772,13 @@ template <int D, typename R> struct LevelCfg {
     static constexpr int THREADS = TPC * Geo<D>::T;
 };
 
+#ifndef LEVEL_MINB
+#define LEVEL_MINB 7
+#endif
 template <int D, typename R, int MODE>
-__global__ void __launch_bounds__(LevelCfg<D, R>::THREADS) level_kernel(const StepArgs A) {
+__global__ void __launch_bounds__(LevelCfg<D, R>::THREADS,
+                                  (D == 3 && sizeof(R) == 4 && MODE != 2) ? LEVEL_MINB : 1)
+level_kernel(const StepArgs A) {
     constexpr int T = Geo<D>::T, Q = Geo<D>::Q, NS = Geo<D>::NS, NM = Geo<D>::NM;
     constexpr int TPC = LevelCfg<D, R>::TPC;
     constexpr int HB = HaloTable<D>::HB, NCO = CoefSlots<D>::N;

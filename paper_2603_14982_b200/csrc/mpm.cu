@@ -422,8 +422,11 @@ __device__ __forceinline__ R eps_of(const R* ras, int64_t rs, const FieldsT<R>& 
     return e;
 }
 
+#ifndef EXCH_MINB
+#define EXCH_MINB 16
+#endif
 template <int D, typename R>
-__global__ void k_exchange(ExchArgs A) {
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? EXCH_MINB : 1) k_exchange(ExchArgs A) {
     constexpr int T = Geo<D>::T;
     using RW = Rows<D>;
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1078,7 +1081,7 @@ __global__ void k_diag_level(mlbm_level_t lv, mlbm_fields_t f, double vol, doubl
 
 // out[0..D-1] += sum m v ; out[D..2D-1] += sum fs (level-0 cells)
 template <int D, typename R>
-__global__ void k_diag_particles(PartArgs P, const R* ras, int64_t rs, int64_t n0,
+__global__ void __launch_bounds__(256, 4) k_diag_particles(PartArgs P, const R* ras, int64_t rs, int64_t n0,
                                  const int32_t* live, double* out) {
     using PR = PRows<D>;
     if (live) n0 = min(n0, (int64_t)live[0] * Geo<D>::T);
