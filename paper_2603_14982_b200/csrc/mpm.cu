@@ -2245,20 +2245,30 @@ extern "C" int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, voi
     PartArgs P{lv0->dim, n, x, nullptr, p, ps, nullptr, nullptr, nullptr};
     MatParams mp{lam, mu, alpha, 0.0};
     const TopoL0 t = topo0(lv0);
-    if (smem == 4 && dtype == 0) {
+    if ((smem == 4 || smem == 5) && dtype == 0) {
+        // 4: one round of 32 * NW particles per block; 5: two rounds sharing
+        // the block's node box (dense sampling, >= 8 per cell: 256 sorted
+        // particles span <= 32 cells, whose box fits P2G2_MAXN)
         constexpr int NW = P2G2_NW;
         const int sh = (NW * (3 + 3 * 3) * P2G2_MAXN + NW * 32 * 32) * (int)sizeof(float);
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute(k_p2g_cell2<3, NW, P2G2_ROUNDS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
-            cudaFuncSetAttribute(k_p2g_cell2<2, NW, P2G2_ROUNDS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
+            cudaFuncSetAttribute(k_p2g_cell2<3, NW, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
+            cudaFuncSetAttribute(k_p2g_cell2<2, NW, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
+            cudaFuncSetAttribute(k_p2g_cell2<3, NW, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
+            cudaFuncSetAttribute(k_p2g_cell2<2, NW, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
             attr = true;
         }
-        constexpr int RD = P2G2_ROUNDS;
-        if (lv0->dim == 2) k_p2g_cell2<2, NW, RD><<<nblk(n, 32 * NW * RD), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
-        else k_p2g_cell2<3, NW, RD><<<nblk(n, 32 * NW * RD), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
+        if (smem == 5) {
+            if (lv0->dim == 2) k_p2g_cell2<2, NW, 2><<<nblk(n, 32 * NW * 2), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
+            else k_p2g_cell2<3, NW, 2><<<nblk(n, 32 * NW * 2), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
+        } else {
+            if (lv0->dim == 2) k_p2g_cell2<2, NW, 1><<<nblk(n, 32 * NW), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
+            else k_p2g_cell2<3, NW, 1><<<nblk(n, 32 * NW), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
+        }
         return launch_status(1);
     }
+    if (smem == 5) smem = 3;
     if (smem == 4) smem = 3;
 #define P2G(D, R) do { if (smem == 3) k_p2g_cell<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err); \
                        else if (smem == 2) k_p2g_warp<D, R, 3><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (R*)ras, rs, err); \

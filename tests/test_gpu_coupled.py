@@ -293,7 +293,7 @@ def test_p2g_modes_agree(dtype):
                                    s), "sort")
     nacc = grid.R["nacc"]
     out = []
-    for mode in range(5):
+    for mode in range(6):
         grid.clear()
         L.check(lib.mlbm_p2g(L.C.byref(lv0), n, L.ptr(xa), L.ptr(pa), ps, mat.lam, mat.mu,
                              mat.alpha, L.ptr(grid.ras), grid.ras.stride(0), dcode, mode,
@@ -302,7 +302,7 @@ def test_p2g_modes_agree(dtype):
     grid.raise_pending()
     scale = out[0].abs().amax(dim=1, keepdim=True).clamp_min(1e-300)
     tol = 1e-12 if dtype == "f64" else 1e-5
-    for mode in range(1, 5):
+    for mode in range(1, 6):
         assert ((out[mode] - out[0]).abs() / scale).max().item() <= tol, mode
 
 
