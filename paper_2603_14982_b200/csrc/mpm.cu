@@ -1482,10 +1482,13 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
 #define P2G2_MAXN 144
 #endif
 #ifndef P2G2_NW
-#define P2G2_NW 4
+#define P2G2_NW 2
 #endif
 #ifndef P2G2_ROUNDS
 #define P2G2_ROUNDS 1
+#endif
+#ifndef P2G2_ROUNDS_DENSE
+#define P2G2_ROUNDS_DENSE 4
 #endif
 template <int D, typename R>
 __global__ void __launch_bounds__(128) k_p2g_cell(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int64_t rs,
@@ -2255,13 +2258,14 @@ extern "C" int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, voi
         if (!attr) {
             cudaFuncSetAttribute(k_p2g_cell2<3, NW, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
             cudaFuncSetAttribute(k_p2g_cell2<2, NW, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
-            cudaFuncSetAttribute(k_p2g_cell2<3, NW, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
-            cudaFuncSetAttribute(k_p2g_cell2<2, NW, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
+            cudaFuncSetAttribute(k_p2g_cell2<3, NW, P2G2_ROUNDS_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
+            cudaFuncSetAttribute(k_p2g_cell2<2, NW, P2G2_ROUNDS_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
             attr = true;
         }
         if (smem == 5) {
-            if (lv0->dim == 2) k_p2g_cell2<2, NW, 2><<<nblk(n, 32 * NW * 2), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
-            else k_p2g_cell2<3, NW, 2><<<nblk(n, 32 * NW * 2), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
+            constexpr int R2 = P2G2_ROUNDS_DENSE;
+            if (lv0->dim == 2) k_p2g_cell2<2, NW, R2><<<nblk(n, 32 * NW * R2), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
+            else k_p2g_cell2<3, NW, R2><<<nblk(n, 32 * NW * R2), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
         } else {
             if (lv0->dim == 2) k_p2g_cell2<2, NW, 1><<<nblk(n, 32 * NW), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
             else k_p2g_cell2<3, NW, 1><<<nblk(n, 32 * NW), 32 * NW, sh, s>>>(P, t, mp, (float*)ras, rs, err);
