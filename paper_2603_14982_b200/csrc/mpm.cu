@@ -880,28 +880,43 @@ template <int D, typename R, int NC>
 __device__ void sample_lin_n(const R* const (&f)[NC], const double (&pos)[D], const mlbm_level_t& lv,
                              double (&out)[NC]) {
     constexpr int T = Geo<D>::T;
-    int b[D];
-    double fr[D];
-    for (int a = 0; a < D; ++a) { const double fl = floor(pos[a]); b[a] = (int)fl; fr[a] = pos[a] - fl; }
+    // per axis: the two corner coordinates (wrapped / clamped), their tile
+    // and in-tile parts and weights; the 2^D corners only combine them, and
+    // a corner in the same tile as corner 0 reuses its slot (no lookup)
+    int tp[3][2] = {{0, 0}, {0, 0}, {0, 0}}, lp[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+    double wt[3][2];
+    unsigned same = 0u;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const double fl = floor(pos[a]);
+        const int b = (int)fl;
+        const double fr = pos[a] - fl;
+        wt[a][0] = 1.0 - fr;
+        wt[a][1] = fr;
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+            int v = b + o;
+            if (lv.periodic[a]) v = wrap_near(v, lv.cells[a]);
+            else v = v < 0 ? 0 : (v >= lv.cells[a] ? lv.cells[a] - 1 : v);
+            tp[a][o] = v >> 2;
+            lp[a][o] = v & 3;
+        }
+        if (tp[a][0] == tp[a][1]) same |= 1u << a;
+    }
+    const int s0 = lv.tile_map[g3(lv.tiles, tp[0][0], tp[1][0], tp[2][0])];
     double acc[NC], ws = 0.0;
 #pragma unroll
     for (int q = 0; q < NC; ++q) acc[q] = 0.0;
 #pragma unroll
     for (int k = 0; k < (1 << D); ++k) {
-        int c[3] = {0, 0, 0};
+        const int ox = k & 1, oy = (k >> 1) & 1, oz = D == 3 ? (k >> 2) & 1 : 0;
         double w = 1.0;
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-            const int o = (k >> a) & 1;
-            int v = b[a] + o;
-            if (lv.periodic[a]) v = ((v % lv.cells[a]) + lv.cells[a]) % lv.cells[a];
-            else v = v < 0 ? 0 : (v >= lv.cells[a] ? lv.cells[a] - 1 : v);
-            c[a] = v;
-            w *= o ? fr[a] : 1.0 - fr[a];
-        }
-        const int s = lv.tile_map[g3(lv.tiles, c[0] >> 2, c[1] >> 2, D == 3 ? c[2] >> 2 : 0)];
+        w *= wt[0][ox];
+        w *= wt[1][oy];
+        if (D == 3) w *= wt[2][oz];
+        const int s = (k & ~(int)same) == 0 ? s0 : lv.tile_map[g3(lv.tiles, tp[0][ox], tp[1][oy], tp[2][oz])];
         if (s < 0) continue;
-        const int64_t ni = (int64_t)s * T + local_of<D>(c[0] & 3, c[1] & 3, c[2] & 3);
+        const int64_t ni = (int64_t)s * T + local_of<D>(lp[0][ox], lp[1][oy], lp[2][oz]);
 #pragma unroll
         for (int q = 0; q < NC; ++q) acc[q] += w * (double)f[q][ni];
         ws += w;
