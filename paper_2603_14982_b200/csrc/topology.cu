@@ -151,6 +151,21 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
     int g[3] = {0, 0, 0};
     for (int a = 0; a < D; ++a) g[a] = tx[a] * 4 + l[a];
     // rim: some in-domain neighbour tile is absent
+    // per neighbour-tile offset: 1 = outside a non-periodic axis, 2 = outside
+    // through a wall face (bounce-back), 4 = stored (read by the pull scan)
+    __shared__ uint8_t sstate[NB];
+    if (lc < NB) {
+        const int o[3] = {lc % 3 - 1, (lc / 3) % 3 - 1, D == 3 ? lc / 9 - 1 : 0};
+        uint8_t st = 0;
+        for (int a = 0; a < D; ++a) {
+            if (lv.periodic[a] || o[a] == 0) continue;
+            const int t = tx[a] + o[a];
+            if (t < 0) { st |= 1; if (bc.face[2 * a] == MLBM_FACE_WALL) st |= 2; }
+            else if (t >= lv.tiles[a]) { st |= 1; if (bc.face[2 * a + 1] == MLBM_FACE_WALL) st |= 2; }
+        }
+        if (!(st & 1) && lv.nbr[(int64_t)tile * NB + lc] >= 0) st |= 4;
+        sstate[lc] = st;
+    }
     bool gapnb = false;
     if (lc < NB) {
         const int o[3] = {lc % 3 - 1, (lc / 3) % 3 - 1, D == 3 ? lc / 9 - 1 : 0};
@@ -271,20 +286,16 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
 #pragma unroll
         for (int i = 1; i < Q; ++i) {
             int o[3] = {0, 0, 0};
-            bool oob = false, bb = false;
 #pragma unroll
             for (int a = 0; a < D; ++a) {
                 const int sa = l[a] - cvec<D>(i, a);
                 o[a] = sa < 0 ? -1 : (sa > 3 ? 1 : 0);
-                if (!lv.periodic[a] && o[a] != 0) {
-                    const int t = tx[a] + o[a];
-                    if (t < 0) { oob = true; if (bc.face[2 * a] == MLBM_FACE_WALL) bb = true; }
-                    else if (t >= lv.tiles[a]) { oob = true; if (bc.face[2 * a + 1] == MLBM_FACE_WALL) bb = true; }
-                }
             }
-            bool stored = false;
+            const uint8_t st = sstate[nb_index<D>(o[0], o[1], o[2])];
+            const bool oob = st & 1;
+            bool bb = st & 2;
+            const bool stored = st & 4;
             if (!oob) {
-                stored = snb[nb_index<D>(o[0], o[1], o[2])] >= 0;
                 if (has_solids) {
                     int sf[3] = {0, 0, 0};
 #pragma unroll
