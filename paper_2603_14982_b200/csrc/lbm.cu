@@ -767,13 +767,16 @@ __device__ __forceinline__ void stream_pull(const FieldsT<R>& src, const R* fb, 
 }  // namespace tp
 
 // mode 0 fused, 1 stream only, 2 collide+bc only
+#ifndef LEVEL_TPC3
+#define LEVEL_TPC3 2
+#endif
 template <int D, typename R> struct LevelCfg {
-    static constexpr int TPC = D == 2 ? 8 : (sizeof(R) == 4 ? 2 : 1);   // tiles per CTA
+    static constexpr int TPC = D == 2 ? 8 : (sizeof(R) == 4 ? LEVEL_TPC3 : 1);   // tiles per CTA
     static constexpr int THREADS = TPC * Geo<D>::T;
 };
 
 #ifndef LEVEL_MINB
-#define LEVEL_MINB 7
+#define LEVEL_MINB (14 / LEVEL_TPC3)      // ~900 resident threads per SM (<= 72 registers)
 #endif
 template <int D, typename R, int MODE>
 __global__ void __launch_bounds__(LevelCfg<D, R>::THREADS,
