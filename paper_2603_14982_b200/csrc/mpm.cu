@@ -1777,7 +1777,8 @@ __device__ __forceinline__ void p2g_record(const PartArgs& P, const MatParams& m
             float tau[D * D];
             kirchhoff<D, float>(F, mp, tau);
             ap = D == 2 ? 2.f * sqrtf(V0 / 3.14159265358979323846f)
-                        : 3.14159265358979323846f * powf(3.f * V0 / (4.f * 3.14159265358979323846f), 2.f / 3.f);
+                        : [](float c) { return 3.14159265358979323846f * c * c; }(
+                              cbrtf(3.f * V0 / (4.f * 3.14159265358979323846f)));   // pi (3V/4pi)^(2/3)
 #pragma unroll
             for (int a = 0; a < D; ++a) {
                 mv[a] = m * v[a];
