@@ -624,6 +624,11 @@ static_assert(dir3_table_ok(), "packed D3Q27 direction table");
 // runtime-velocity direction index (unrolled compare over the 26 moving directions)
 MLBM_HD int dir_rt(int cx, int cy, int cz) { return dir3(cx, cy, cz); }
 
+// slot of velocity c in the push/pull buffer: the buffer is private to the
+// kernel, so it is indexed by the velocity's digits rather than by the D3Q27
+// direction number (no table lookup for runtime velocities)
+MLBM_HD constexpr int kidx(int cx, int cy, int cz) { return (cx + 1) + 3 * (cy + 1) + 9 * (cz + 1); }
+
 template <int A, typename R>
 __device__ __forceinline__ void face_body(const FieldsT<R>& src, R* fb, const int* snb, int f, R h3xyz) {
     constexpr int T = 64, U = A == 0 ? 1 : 0, V = A == 2 ? 1 : 2;
@@ -645,7 +650,9 @@ __device__ __forceinline__ void face_body(const FieldsT<R>& src, R* fb, const in
         for (int cv = -1; cv <= 1; ++cv) {
             const int lu = u + cu, lv = v + cv;
             if ((unsigned)lu > 3u || (unsigned)lv > 3u) continue;
-            fb[dir_sel<A>(side, cu, cv) * T + base + lu * SU + lv * SV] = gf[cu + 1][cv + 1];
+            constexpr int KA = A == 0 ? 1 : A == 1 ? 3 : 9, KU = U == 0 ? 1 : 3, KV = V == 1 ? 3 : 9;
+            const int k = (side ? 0 : 2) * KA + (cu + 1) * KU + (cv + 1) * KV;   // c_A = -1 / +1
+            fb[k * T + base + lu * SU + lv * SV] = gf[cu + 1][cv + 1];
         }
 }
 
@@ -671,7 +678,7 @@ __device__ __forceinline__ void edge_body(const FieldsT<R>& src, R* fb, const in
         if ((unsigned)le > 3u) continue;
         int c[3];
         c[E] = ce; c[P] = cP; c[Q] = cQ;
-        fb[dir_rt(c[0], c[1], c[2]) * T + base + le * SE] = ge[ce + 1];
+        fb[kidx(c[0], c[1], c[2]) * T + base + le * SE] = ge[ce + 1];
     }
 }
 
@@ -697,7 +704,7 @@ __device__ __forceinline__ void stream_push(const FieldsT<R>& src, R* fb, const 
                     const bool in = (cx < 0 ? okm[0] : cx > 0 ? okp[0] : true) &&
                                     (cy < 0 ? okm[1] : cy > 0 ? okp[1] : true) &&
                                     (cz < 0 ? okm[2] : cz > 0 ? okp[2] : true);
-                    if (in) fb[dir3(cx, cy, cz) * T + lc + cx + 4 * cy + 16 * cz] = g[cx + 1][cy + 1][cz + 1];
+                    if (in) fb[kidx(cx, cy, cz) * T + lc + cx + 4 * cy + 16 * cz] = g[cx + 1][cy + 1][cz + 1];
                 }
         // ---- halo faces: 96 cells; warp-uniform normal axis per round
 #pragma unroll
@@ -724,7 +731,7 @@ __device__ __forceinline__ void stream_push(const FieldsT<R>& src, R* fb, const 
                               h3xyz, a);
                 const int cx = sx ? -1 : 1, cy = sy ? -1 : 1, cz = sz ? -1 : 1;
                 const R gc = corner_eval<R>(a, R(cx), R(cy), R(cz));
-                const int dir = dir_rt(cx, cy, cz);
+                const int dir = kidx(cx, cy, cz);
                 fb[dir * T + (sx ? 3 : 0) + 4 * (sy ? 3 : 0) + 16 * (sz ? 3 : 0)] = gc;
             }
         }
@@ -744,7 +751,7 @@ __device__ __forceinline__ void stream_pull(const FieldsT<R>& src, const R* fb, 
 #pragma unroll
         for (int cy = -1; cy <= 1; ++cy)
 #pragma unroll
-            for (int cz = -1; cz <= 1; ++cz) g[cx + 1][cy + 1][cz + 1] = fb[dir3(cx, cy, cz) * T + lc];
+            for (int cz = -1; cz <= 1; ++cz) g[cx + 1][cy + 1][cz + 1] = fb[kidx(cx, cy, cz) * T + lc];
     if (special) {
         R a[3][3][3], own[3][3][3];
         load_tcoef<R>(src, cell, h3xyz, a);
