@@ -263,7 +263,12 @@ __device__ __forceinline__ void left_stretch3(const R (&F)[9], R (&U)[9], R (&s)
 
 struct MatParams {
     double lam, mu, alpha, floor_friction;
+    double kdg2, kdg3;      // (d lam + 2 mu) / (2 mu) for d = 2, 3 (host-computed)
 };
+static inline MatParams mat_params(double lam, double mu, double alpha) {
+    return MatParams{lam, mu, alpha, 0.0, (2.0 * lam + 2.0 * mu) / (2.0 * mu),
+                     (3.0 * lam + 2.0 * mu) / (2.0 * mu)};
+}
 
 // tau = U diag(2 mu eps + lam tr) U^T  (granular.py:260-279)
 template <int D, typename R>
@@ -779,7 +784,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(Part
 #pragma unroll
         for (int a = 0; a < D; ++a) { eh[a] = e[a] - tr / R(D); nrm2 += eh[a] * eh[a]; }
         const R nrm = sqrt(nrm2);
-        const R dg = nrm + R((D * mp.lam + 2.0 * mp.mu) / (2.0 * mp.mu)) * tr * R(mp.alpha);
+        const R dg = nrm + R(D == 3 ? mp.kdg3 : mp.kdg2) * tr * R(mp.alpha);
         R en[D];
         if (tr > R(0)) {
 #pragma unroll
@@ -2262,7 +2267,7 @@ extern "C" int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, voi
     if (n <= 0) return 0;
     cudaStream_t s = as_stream(stream);
     PartArgs P{lv0->dim, n, x, nullptr, p, ps, nullptr, nullptr, nullptr};
-    MatParams mp{lam, mu, alpha, 0.0};
+    MatParams mp = mat_params(lam, mu, alpha);
     const TopoL0 t = topo0(lv0);
     if ((smem == 4 || smem == 5) && dtype == 0) {
         // 4: one round of 32 * NW particles per block; 5: two rounds sharing
@@ -2370,7 +2375,7 @@ extern "C" int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, const double* x_in, 
     if (n <= 0) return 0;
     cudaStream_t s = as_stream(stream);
     PartArgs P{lv0->dim, n, x_in, x_out, (void*)p_in, ps, p_out, pid_in, pid_in ? pid_out : nullptr};
-    MatParams mp{lam, mu, alpha, 0.0};
+    MatParams mp = mat_params(lam, mu, alpha);
     const TopoL0 t = topo0(lv0);
 #define G2P(D, R) k_g2p<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (const R*)ras, rs, dt, plastic, clamped, err)
     if (lv0->dim == 2) { if (dtype) G2P(2, double); else G2P(2, float); }
@@ -2383,7 +2388,7 @@ static int stress_raster_impl(const mlbm_level_t* lv0, int32_t n, const double* 
                               int64_t ps, double lam, double mu, double alpha, void* ras, int64_t rs,
                               int32_t dtype, const float* surf, mlbm_error_t* err, cudaStream_t s) {
     PartArgs P{lv0->dim, n, x, nullptr, (void*)p, ps, nullptr, nullptr, nullptr};
-    MatParams mp{lam, mu, alpha, 0.0};
+    MatParams mp = mat_params(lam, mu, alpha);
     const TopoL0 t = topo0(lv0);
     if (dtype == 0 && !getenv("MLBM_STRESS_ATOMIC")) {
         // fp32: the P2G layout (sorted particles, per-warp node boxes)
