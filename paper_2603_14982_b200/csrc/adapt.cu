@@ -359,7 +359,10 @@ __device__ __forceinline__ void stamp(const AdaptArgs& A, int k) {
 }
 #define STAMP_BARRIER(k) do { grid_barrier(A.bar); stamp(A, k); } while (0)
 
-__global__ void __launch_bounds__(512) k_adapt_pass(AdaptArgs A) {
+#ifndef ADAPT_MINB
+#define ADAPT_MINB 2      // 64 registers, 2 x 512 threads per SM (explicit 1 lets ptxas take 69)
+#endif
+__global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int dim = A.dim, L = A.levels;
