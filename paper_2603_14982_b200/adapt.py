@@ -264,12 +264,16 @@ class GridAdaptor:
                 "adapt_pass")
         self.launches += 1
 
-    def finish(self, driver, pair, status, err, check_after=True, device_runner=None):
+    def finish(self, driver, pair, status, err, check_after=True, device_runner=None,
+               latest_only=None):
         """Host half: raise on seed errors; when a level changed, rebuild and
         migrate on the device without host synchronisation (the new counts
         come from the adapt pass); build the report.  ``check_after`` re-runs
         the invariants on the new topology (one readback); the graph path
-        skips it and the next pass reports them.  ``device_runner(fn, key)``
+        skips it and the next pass reports them.  ``latest_only`` {level: tree}
+        migrates / initialises only that tree of a level whose other tree is
+        fully rewritten before it is read again (the coupled step's level 0).
+        ``device_runner(fn, key)``
         (graph path) runs the device half ``fn`` — eagerly or as a replay of a
         graph cached under ``key`` — after the host bookkeeping is done."""
         topo = self.topology
@@ -288,13 +292,15 @@ class GridAdaptor:
                 rep.created[l] = fresh[l]
                 rep.deleted[l] = topo.n_tiles(l) - (new_counts[l] - fresh[l])
             if device_runner is None:
-                self._prepare(changed, pair, new_counts, fresh)()
+                lo = {l: t for l, t in (latest_only or {}).items() if l in changed}
+                self._prepare(changed, pair, new_counts, fresh, lo)()
             else:
                 # graph path: the init kernel always runs (it finds no fresh tile
                 # when there is none), so the rebuild graph's key is only the set
                 # of changed levels
-                dev = self._prepare(changed, pair, new_counts, [1] * Lv)
-                device_runner(dev, tuple(changed))
+                lo = {l: t for l, t in (latest_only or {}).items() if l in changed}
+                dev = self._prepare(changed, pair, new_counts, [1] * Lv, lo)
+                device_runner(dev, (tuple(changed), tuple(sorted(lo.items()))))
             if check_after:
                 self._invariants_device(driver)
                 viol = self._status[Lv:Lv + 3].cpu().numpy()
@@ -303,7 +309,7 @@ class GridAdaptor:
         self._report_invariants(viol, rep)
         return rep
 
-    def _prepare(self, changed, pair, new_counts, fresh):
+    def _prepare(self, changed, pair, new_counts, fresh, latest_only=None):
         """Rebuild + bitwise migration + new-cell init (adapt.py:232-372).
         Host part here (capacity growth, host counts, version bump); returns
         the device part — compaction into the spare tile map, neighbours,
@@ -325,6 +331,7 @@ class GridAdaptor:
         dcode = dtype_code(pair.dtype)
         conv = 0 if self.rescale_convention == "derived" else 1
         init = {l: bool(fresh[l]) for l in changed}
+        latest_only = latest_only or {}
 
         def device():
             lib = L.lib()
@@ -337,24 +344,24 @@ class GridAdaptor:
                 lt = topo.lv[l]
                 sb = pair.scratch_blocks(l)
                 cnt = L.ptr(topo.dcounts[l])
-                L.check(lib.mlbm_migrate_level(d, lt.cap, cnt, L.ptr(lt.old_slot),
-                                               L.fields(pair.trees[0].levels[l].data),
-                                               L.fields(pair.trees[1].levels[l].data),
-                                               L.fields(sb[0]), L.fields(sb[1]), dcode, s),
-                        "migrate_level")
+                # trees to carry over: both, or only the one read next (the
+                # other is rewritten before it is read; its stale cells stay)
+                ts = (latest_only[l],) if l in latest_only else (0, 1)
+                old = [L.fields(pair.trees[t].levels[l].data) for t in ts] + [L.fields(None)]
+                new = [L.fields(sb[t]) for t in ts] + [L.fields(None)]
+                L.check(lib.mlbm_migrate_level(d, lt.cap, cnt, L.ptr(lt.old_slot), old[0], old[1],
+                                               new[0], new[1], dcode, s), "migrate_level")
                 if init[l]:
                     L.check(lib.mlbm_init_new_cells(L.C.byref(old_h), L.C.byref(new_h), l,
                                                     L.ptr(lt.tile_xyz), L.ptr(lt.old_slot),
-                                                    lt.cap, cnt, L.fields(sb[0]),
-                                                    L.fields(sb[1]), L.ptr(self._taus), conv,
+                                                    lt.cap, cnt, new[0], new[1],
+                                                    L.ptr(self._taus), conv,
                                                     dcode, L.ptr(self._status[Lv_slot(topo)]),
                                                     s), "init_new_cells")
-            for l in changed:
-                sb = pair.scratch_blocks(l)
-                td = [pair.trees[t].levels[l].data for t in range(2)]
-                L.check(lib.mlbm_copy_live_fields(d, topo.lv[l].cap, L.ptr(topo.dcounts[l]),
-                                                  L.fields(sb[0]), L.fields(sb[1]),
-                                                  L.fields(td[0]), L.fields(td[1]), dcode, s),
+                L.check(lib.mlbm_copy_live_fields(d, lt.cap, cnt, new[0], new[1],
+                                                  *[L.fields(pair.trees[t].levels[l].data)
+                                                    for t in ts], *([L.fields(None)] if len(ts) == 1
+                                                                    else []), dcode, s),
                         "copy_live_fields")
             topo.commit_device({l: self._new[l] for l in changed})
         return device

@@ -185,6 +185,7 @@ class CoupledSim:
         # graphs of this many upcoming steps are captured whenever capacities
         # change (first step included), so steady stepping only replays
         self.precapture_steps = int(os.environ.get("MLBM_PRECAPTURE", "16")) or None
+        self.latest_only_rebuild = os.environ.get("MLBM_LATEST_ONLY_REBUILD", "1") != "0"
         self.p2g_mode = 4          # sorted input: 1 block smem, 2 warp registers, 3 cell lanes,
                                    # 4 cell lanes + per-warp box copies (fp32; fp64 runs mode 3),
                                    # 5 = 4 with two rounds of particles per block
@@ -511,9 +512,13 @@ class CoupledSim:
             nst = 3 * self.topology.levels + 4
             status = h[2 * ne + 2:2 * ne + 2 + nst]
             err = h[2 * ne + 2 + nst:]
+            # level 0 steps once per finest cycle: of its two trees only the one
+            # read next carries state (the other is rewritten by the next
+            # stream / exchange before any read), so a rebuild migrates that one
             self.last_report = self.adaptor.finish(self._driver(), self.pair, status, err,
                                                    check_after=False,
-                                                   device_runner=self._run_rebuild)
+                                                   device_runner=self._run_rebuild,
+                                                   latest_only=self._latest_only())
             if not self.last_report.noop:
                 # the rebuild graph re-takes this step's diagnostics on the new
                 # topology (coupling.py:481) into a second pinned buffer; the row
@@ -522,6 +527,11 @@ class CoupledSim:
                 self._push_diag_row(None)
                 return
         self._push_diag_row(diag)
+
+    def _latest_only(self):
+        if not self.latest_only_rebuild:
+            return None
+        return {0: self.solver.roles(0)[0]}
 
     def _run_rebuild(self, device_fn, key):
         """Device half of a topology change + the table rebuild as one CUDA
@@ -539,7 +549,8 @@ class CoupledSim:
             self._rb_graphs, self._rb_seen, self._rb_ver = {}, set(), topo.cap_version
 
         # tables of the changed levels and of their neighbours (interfaces)
-        affected = sorted({m for l in key for m in (l - 1, l, l + 1) if 0 <= m < topo.levels})
+        changed = key[0] if key and isinstance(key[0], tuple) else key
+        affected = sorted({m for l in changed for m in (l - 1, l, l + 1) if 0 <= m < topo.levels})
 
         def body():
             device_fn()

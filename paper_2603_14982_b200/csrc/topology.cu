@@ -536,11 +536,12 @@ __global__ void k_migrate(int64_t ncells, const int32_t* n_dev, const int32_t* o
     if (c >= ncells || (n_dev && c >= (int64_t)__ldg(n_dev) * T)) return;
     const int os = old_slot[c / T];
     const int64_t oc = (int64_t)os * T + c % T;
+    const bool two = n1.p != nullptr;          // second tree optional (latest-only rebuild)
 #pragma unroll
     for (int k = 0; k < NF; ++k) {
         const R def = k == fi_eps<D>() ? R(1) : R(0);
         n0.at(k, c) = os >= 0 ? o0.at(k, oc) : def;
-        n1.at(k, c) = os >= 0 ? o1.at(k, oc) : def;
+        if (two) n1.at(k, c) = os >= 0 ? o1.at(k, oc) : def;
     }
 }
 
@@ -557,7 +558,7 @@ __global__ void k_copy_live(int64_t nvec_row, const int32_t* n_dev, int nf, cons
     if (row >= nf) return;
     if (n_dev && v >= (int64_t)__ldg(n_dev) * (T / PER)) return;
     d0[row * stride_vec + v] = s0[row * stride_vec + v];
-    d1[row * stride_vec + v] = s1[row * stride_vec + v];
+    if (d1) d1[row * stride_vec + v] = s1[row * stride_vec + v];
 }
 
 MLBM_HD double kap_down(double tf, double tc, int conv) { return conv == 0 ? tf / (2.0 * tc) : 2.0 * tc / tf; }
@@ -603,6 +604,7 @@ __global__ void k_init_new(mlbm_hier_t oh, mlbm_hier_t nh, int level, const int3
         }
         if (!ok) continue;
         for (int t = 0; t < 2; ++t) {
+            if (dstt[t].p == nullptr) continue;   // latest-only rebuild
             const FieldsT<R> src{(R*)oh.fields[t][sl], oh.stride[sl]};
             R v[NM + 2];
             for (int q = 0; q < NM + 2; ++q) {
@@ -636,6 +638,7 @@ __global__ void k_init_new(mlbm_hier_t oh, mlbm_hier_t nh, int level, const int3
         if (s < 0) continue;
         const int64_t si = (int64_t)s * T + local_of<D>(cc[0] & 3, cc[1] & 3, cc[2] & 3);
         for (int t = 0; t < 2; ++t) {
+            if (dstt[t].p == nullptr) continue;   // latest-only rebuild
             const FieldsT<R> src{(R*)oh.fields[t][sl], oh.stride[sl]};
             R v[NM + 2];
             for (int q = 0; q < NM + 2; ++q) {
@@ -846,7 +849,8 @@ extern "C" int mlbm_copy_live_fields(int32_t dim, int32_t cap_tiles, const int32
                                      mlbm_fields_t src0, mlbm_fields_t src1, mlbm_fields_t dst0,
                                      mlbm_fields_t dst1, int32_t dtype, void* stream) {
     if (cap_tiles <= 0) return 0;
-    if (src1.stride != src0.stride || dst0.stride != src0.stride || dst1.stride != src0.stride) return -1;
+    if (dst0.stride != src0.stride || (dst1.ptr && (src1.stride != src0.stride || dst1.stride != src0.stride)))
+        return -1;
     const int es = dtype ? 8 : 4;
     if ((src0.stride * es) % 16 != 0) return -1;
     const int T = dim == 2 ? 16 : 64;
