@@ -725,6 +725,10 @@ extern "C" int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_
     for (int a = 0; a < h->dim; ++a) n0 *= (h->finest[a] / 4);
     const int64_t want = (n0 + (int64_t)grid_sms * 512 * 8 - 1) / ((int64_t)grid_sms * 512 * 8);
     grid = grid_sms * (int)std::max<int64_t>(1, std::min<int64_t>(want, grid_per));
+    if (const char* g = getenv("MLBM_ADAPT_GRID")) {          // tuning experiments
+        const int v = atoi(g);
+        if (v > 0 && v <= grid_sms * grid_per) grid = v;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(512);
