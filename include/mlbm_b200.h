@@ -243,7 +243,10 @@ int mlbm_check_particles(int32_t dim, int32_t n, const void* x, int64_t xstride,
                          int32_t* viol, void* stream);
 
 /* Data migration after a rebuild (adapt.py:259-283): both trees, surviving
- * tiles bitwise, fresh tiles get drho = 0, eps = 1, others 0. */
+ * tiles bitwise, fresh tiles get drho = 0, eps = 1, others 0.  A null second
+ * tree (new1.ptr == NULL) migrates only the first (the coupled step's level 0,
+ * whose other tree is rewritten before it is read); mlbm_init_new_cells and
+ * mlbm_copy_live_fields accept the same. */
 int mlbm_migrate_level(int32_t dim, int32_t n_new_tiles, const int32_t* n_dev,
                        const int32_t* old_slot,
                        mlbm_fields_t old0, mlbm_fields_t old1, mlbm_fields_t new0,
