@@ -203,7 +203,7 @@ __device__ __forceinline__ void sym_eig3(R a00, R a01, R a02, R a11, R a12, R a2
 #pragma unroll
     for (int i = 0; i < 9; ++i) Q[i] = (i % 4 == 0) ? R(1) : R(0);
 #ifndef MLBM_JACOBI_TOL32
-#define MLBM_JACOBI_TOL32 1e-15
+#define MLBM_JACOBI_TOL32 1e-13   // off-diagonal ~3e-7 relative: fp32 round-off level
 #endif
     const R tol = R(sizeof(R) == 8 ? 1e-32 : MLBM_JACOBI_TOL32);
 #pragma unroll 1
