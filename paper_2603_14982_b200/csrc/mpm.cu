@@ -1860,6 +1860,7 @@ __global__ void __launch_bounds__(32 * NW) k_p2g_cell2(PartArgs P, TopoL0 t0, Ma
     // block node box over all rounds
     if (threadIdx.x < 3) { s_lo[threadIdx.x] = 0x7fffffff; s_hi[threadIdx.x] = -0x7fffffff; }
     __syncthreads();
+    int wl[3] = {0, 0, 0}, wh[3] = {0, 0, 0};        // this warp's node box
     {
         int bl[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, bh[3] = {-0x7fffffff, -0x7fffffff, -0x7fffffff};
 #pragma unroll
@@ -1878,6 +1879,8 @@ __global__ void __launch_bounds__(32 * NW) k_p2g_cell2(PartArgs P, TopoL0 t0, Ma
         for (int a = 0; a < D; ++a) {
             const int l2 = __reduce_min_sync(0xffffffffu, bl[a]);
             const int h2 = __reduce_max_sync(0xffffffffu, bh[a]);
+            wl[a] = l2;
+            wh[a] = h2;
             if (lane == 0 && l2 <= h2) { atomicMin(&s_lo[a], l2); atomicMax(&s_hi[a], h2); }
         }
     }
@@ -1885,7 +1888,30 @@ __global__ void __launch_bounds__(32 * NW) k_p2g_cell2(PartArgs P, TopoL0 t0, Ma
     int lo[3] = {0, 0, 0}, ext[3] = {1, 1, 1}, nbox = 1;
 #pragma unroll
     for (int a = 0; a < D; ++a) { lo[a] = s_lo[a]; ext[a] = s_hi[a] - s_lo[a] + 1; nbox *= ext[a]; }
-    const bool use_smem = nbox > 0 && nbox <= MAXN;
+    const bool use_smem = nbox > 0 && nbox <= MAXN;        // block-uniform
+    // a block whose box is too large (particles drifted since the last sort)
+    // falls back to per-warp boxes in the same per-warp copies (warp-uniform)
+    // before resorting to per-run global atomics
+    bool warp_box = false;
+    if (!use_smem) {
+        int nw = 1;
+        bool okw = true;
+#pragma unroll
+        for (int a = 0; a < D; ++a) { okw &= wl[a] <= wh[a]; nw *= wh[a] - wl[a] + 1; }
+        warp_box = okw && nw <= MAXN;
+        if (warp_box) {
+#pragma unroll
+            for (int a = 0; a < D; ++a) { lo[a] = wl[a]; ext[a] = wh[a] - wl[a] + 1; }
+            nbox = nw;
+            constexpr int RP = MAXN / 4 <= 32 ? 32 : (MAXN / 4 <= 64 ? 64 : 128);
+            const int n4 = (nbox + 3) >> 2;
+            float4* s4 = reinterpret_cast<float4*>(sacc + wid * NV * MAXN);
+            for (int i = lane; i < NV * RP; i += 32) {
+                const int row = i / RP, c4 = i % RP;
+                if (c4 < n4) s4[row * (MAXN / 4) + c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+    }
     if (use_smem) {
         // zero the [NW * NV rows][nbox] box copies as float4, iterating over a
         // power-of-two padded row (no integer division)
@@ -1995,7 +2021,7 @@ __global__ void __launch_bounds__(32 * NW) k_p2g_cell2(PartArgs P, TopoL0 t0, Ma
             }
             if (node_lane && (acc[0] != 0.f || acc[2 + 2 * D] != 0.f)) {
                 int c[3] = {cur[0] + o[0], cur[1] + o[1], D == 3 ? cur[2] + o[2] : 0};
-                if (use_smem) {
+                if (use_smem || warp_box) {
                     int li = 0;
     #pragma unroll
                     for (int a = D - 1; a >= 0; --a) li = li * ext[a] + (c[a] - lo[a]);
@@ -2014,6 +2040,26 @@ __global__ void __launch_bounds__(32 * NW) k_p2g_cell2(PartArgs P, TopoL0 t0, Ma
         __syncwarp();                                     // slab reused next round
     }
     if (bad) report_error(err, MLBM_ERR_STENCIL, 0, cur[0], cur[1], cur[2]);
+    if (warp_box) {
+        // this warp's copy only (lanes stride over its box)
+        __syncwarp();
+        const float* wa = sacc + wid * NV * MAXN;
+        for (int i = lane; i < nbox; i += 32) {
+            float tot[NV];
+#pragma unroll
+            for (int qv = 0; qv < NV; ++qv) tot[qv] = wa[qv * MAXN + i];
+            if (tot[0] == 0.f && tot[2 + 2 * D] == 0.f) continue;
+            int c[3];
+            box_coord<D>(i, lo, ext, c);
+            bool b2 = false;
+            const int64_t ni = node_index<D>(t0, c, b2);
+            if (ni < 0) { report_error(err, MLBM_ERR_STENCIL, 0, c[0], c[1], c[2]); continue; }
+#pragma unroll
+            for (int qv = 0; qv < NV; ++qv)
+                if (tot[qv] != 0.f) atomicAdd(&ras[qv * rs + ni], tot[qv]);
+        }
+        return;
+    }
     if (!use_smem) return;
     __syncthreads();
     p2g_box_merge<D, NV, 0>(sacc, NW, MAXN, nbox, lo, ext, t0, ras, rs, err);
