@@ -271,15 +271,19 @@ def test_stress_raster_fp32_kernels_agree():
     assert ((restricted[:, m] - out[0][:, m]).abs() / scale).max().item() <= 1e-5
 
 
-@pytest.mark.parametrize("dtype", ["f32", "f64"])
-def test_p2g_modes_agree(dtype):
+@pytest.mark.parametrize("dtype,scene", [("f32", "column"), ("f64", "column"),
+                                         ("f32", "cloud"), ("f32", "cloud_unsorted")])
+def test_p2g_modes_agree(dtype, scene):
     """Every P2G variant (atomic, block smem, warp registers, cell lanes,
-    per-warp box copies) rasterises the same sorted particle set: fp64
-    within summation-order noise, fp32 within 1e-5 of the row maximum."""
+    per-warp box copies) rasterises the same particle set: fp64 within
+    summation-order noise, fp32 within 1e-5 of the row maximum.  The dense
+    column fits the block node boxes; the 1-per-cell cloud overflows them
+    (per-warp boxes), and unsorted it overflows those too (global atomics)."""
     _need_gpu()
     from paper_2603_14982_b200 import _lib as L
     from paper_2603_14982_b200.harness import build_scene, validate_scene
-    sim = build_scene(validate_scene(S.scene(S.COLUMN_3D_SMALL, runtime__dtype=dtype)))
+    base = S.COLUMN_3D_SMALL if scene == "column" else S.CLOUD_3D_SMALL
+    sim = build_scene(validate_scene(S.scene(base, runtime__dtype=dtype)))
     for _ in range(3):
         sim.step()
     lib, s = L.lib(), L.stream_handle()
@@ -291,6 +295,10 @@ def test_p2g_modes_agree(dtype):
     L.check(lib.mlbm_particle_sort(L.C.byref(lv0), n, L.ptr(p.xd), L.ptr(p.pd), L.ptr(p.pid), ps,
                                    L.ptr(xa), L.ptr(pa), L.ptr(ida), dcode, L.ptr(ws), ws.numel(),
                                    s), "sort")
+    if scene == "cloud_unsorted":
+        perm = torch.randperm(n, generator=torch.Generator().manual_seed(3)).cuda()
+        xa[:, :n] = xa[:, :n][:, perm].clone()
+        pa[:, :n] = pa[:, :n][:, perm].clone()
     nacc = grid.R["nacc"]
     out = []
     for mode in range(6):
