@@ -57,7 +57,7 @@ struct AdaptArgs {
 __device__ __forceinline__ int64_t gi3(const int* d, int x, int y, int z) {
     return ((int64_t)x * d[1] + y) * d[2] + z;
 }
-// tile grids hold < 2^31 tiles (the host checks): 32-bit division only
+// tile grids hold < 2^31 tiles (mlbm_adapt_pass refuses larger): 32-bit division only
 __device__ __forceinline__ void dec3(const int* d, int64_t g, int& x, int& y, int& z) {
     const unsigned gg = (unsigned)g, d1 = (unsigned)d[1], d2 = (unsigned)d[2];
     const unsigned q = gg / d2;
@@ -723,6 +723,7 @@ extern "C" int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_
     // parallelism: up to the occupancy limit, ~8 tiles per thread per stage
     int64_t n0 = 1;
     for (int a = 0; a < h->dim; ++a) n0 *= (h->finest[a] / 4);
+    if (n0 >= ((int64_t)1 << 31)) return -(int)cudaErrorInvalidValue;   // 32-bit tile indices (dec3)
     const int64_t want = (n0 + (int64_t)grid_sms * 512 * 8 - 1) / ((int64_t)grid_sms * 512 * 8);
     grid = grid_sms * (int)std::max<int64_t>(1, std::min<int64_t>(want, grid_per));
     if (const char* g = getenv("MLBM_ADAPT_GRID")) {          // tuning experiments

@@ -18,4 +18,4 @@ for _ in range(n):
 torch.cuda.synchronize()
 pr.disable()
 print("steps", n, "changes", sim.topology_changes - c0, "captures", sim.graph_captures)
-pstats.Stats(pr).sort_stats("cumulative").print_stats(35)
+pstats.Stats(pr).sort_stats(os.environ.get("SORT", "cumulative")).print_stats(int(os.environ.get("TOP", "35")))
