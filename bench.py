@@ -177,6 +177,17 @@ def kernel_class(rec, d, s, live):
         return "diagnostics", 0, 0
     if name.startswith("mlbm_stress_raster") or name == "mlbm_powder":
         return "powder", 0, 0
+    if name == "mlbm_adapt_pass":
+        return "adapt_pass", 0, 0
+    if name.startswith("mlbm_check_") or name in ("mlbm_count_ring_violations", "mlbm_bitmap_op",
+                                                   "mlbm_dilate"):
+        # re-checked after a rebuild only on the eager path (the graph path
+        # leaves them to the next adapt pass): not part of the timed steps
+        return "invariants (eager profile only)", 0, 0
+    if name in ("mlbm_compact_tiles", "mlbm_build_neighbors", "mlbm_migrate_level",
+                "mlbm_copy_live_fields", "mlbm_init_new_cells", "mlbm_classify_level",
+                "mlbm_build_interface"):
+        return "rebuild (topology changes)", 0, 0
     if name == "mlbm_particle_sort":
         n = int(args[1])
         return "particle_sort", n * 2 * (8 * d + (d + 2 * d * d + 3) * s + 4), n
