@@ -529,7 +529,9 @@ class CoupledSim:
         self._push_diag_row(diag)
 
     def _latest_only(self):
-        if not self.latest_only_rebuild:
+        # it halves the level-0 migration but doubles the rebuild-graph keys
+        # (the tree is part of the key): worth it only for large level 0s
+        if not self.latest_only_rebuild or self.topology.capacity_cells(0) < (1 << 22):
             return None
         return {0: self.solver.roles(0)[0]}
 
