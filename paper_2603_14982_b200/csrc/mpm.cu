@@ -554,8 +554,11 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? EXCH_MINB : 1) k_exchang
 #ifndef G2P_MINB
 #define G2P_MINB 8
 #endif
+#ifndef G2P_BT
+#define G2P_BT 128      // particles (threads) per block: one node box per block
+#endif
 template <int D, typename R>
-__global__ void __launch_bounds__(128, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(PartArgs P, TopoL0 t0, MatParams mp, const R* ras, int64_t rs,
+__global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(PartArgs P, TopoL0 t0, MatParams mp, const R* ras, int64_t rs,
                                              double dt, int plastic, int32_t* clamped, mlbm_error_t* err) {
     constexpr int K = Geo<D>::K;
     using RW = Rows<D>;
@@ -2423,7 +2426,7 @@ extern "C" int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, const double* x_in, 
     PartArgs P{lv0->dim, n, x_in, x_out, (void*)p_in, ps, p_out, pid_in, pid_in ? pid_out : nullptr};
     MatParams mp = mat_params(lam, mu, alpha);
     const TopoL0 t = topo0(lv0);
-#define G2P(D, R) k_g2p<D, R><<<nblk(n, 128), 128, 0, s>>>(P, t, mp, (const R*)ras, rs, dt, plastic, clamped, err)
+#define G2P(D, R) k_g2p<D, R><<<nblk(n, G2P_BT), G2P_BT, 0, s>>>(P, t, mp, (const R*)ras, rs, dt, plastic, clamped, err)
     if (lv0->dim == 2) { if (dtype) G2P(2, double); else G2P(2, float); }
     else { if (dtype) G2P(3, double); else G2P(3, float); }
 #undef G2P
