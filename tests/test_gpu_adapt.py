@@ -47,10 +47,15 @@ def test_adapt_walk_matches_reference_golden(fused, path, monkeypatch):
         assert rep.violations == []
 
 
-@pytest.mark.parametrize("path", ["bits", "coop"])
-def test_adapt_3d_random_walk_vs_oracle(path, monkeypatch):
+@pytest.mark.parametrize("path,grid", [("bits", None), ("coop", None), ("coop", "296"),
+                                       ("coop", "37")])
+def test_adapt_3d_random_walk_vs_oracle(path, grid, monkeypatch):
+    """grid: the cooperative pass with 2 CTAs per SM (the large-grid launch
+    shape C4 uses) and with fewer CTAs than SMs (several tiles per thread)."""
     _need_gpu()
     monkeypatch.setenv("MLBM_ADAPT_PATH", path)
+    if grid:
+        monkeypatch.setenv("MLBM_ADAPT_GRID", grid)
     rng = np.random.default_rng(11)
     cells, levels = (64, 32, 32), 3
     otopo = OG.Topology.uniform(cells, levels)
