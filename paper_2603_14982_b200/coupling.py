@@ -186,6 +186,7 @@ class CoupledSim:
         # change (first step included), so steady stepping only replays
         self.precapture_steps = int(os.environ.get("MLBM_PRECAPTURE", "16")) or None
         self.latest_only_rebuild = os.environ.get("MLBM_LATEST_ONLY_REBUILD", "1") != "0"
+        self.latest_only_min_cells = 1 << 22
         self.p2g_mode = 4          # sorted input: 1 block smem, 2 warp registers, 3 cell lanes,
                                    # 4 cell lanes + per-warp box copies (fp32; fp64 runs mode 3),
                                    # 5 = 4 with two rounds of particles per block
@@ -531,7 +532,7 @@ class CoupledSim:
     def _latest_only(self):
         # it halves the level-0 migration but doubles the rebuild-graph keys
         # (the tree is part of the key): worth it only for large level 0s
-        if not self.latest_only_rebuild or self.topology.capacity_cells(0) < (1 << 22):
+        if not self.latest_only_rebuild or self.topology.capacity_cells(0) < self.latest_only_min_cells:
             return None
         return {0: self.solver.roles(0)[0]}
 

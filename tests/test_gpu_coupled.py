@@ -100,9 +100,14 @@ def test_dune_2d_three_levels():
     run_and_compare(S.DUNE_2D, 12)
 
 
-def test_cloud_2d_block_churn():
+@pytest.mark.parametrize("latest_only", [False, True])
+def test_cloud_2d_block_churn(latest_only):
+    """Per-step block churn; latest_only forces the single-tree level-0
+    rebuild (on by default only for level 0s of >= 4M cells)."""
     sc = S.scene(S.CLOUD_2D)
     osim, dsim = build_both(sc)
+    if latest_only:
+        dsim.latest_only_min_cells = 0
     rng = np.random.default_rng(4)
     n = len(osim.p)
     v = rng.normal(0, 0.08, (n, 2)).clip(-0.45, 0.45)
@@ -124,6 +129,47 @@ def test_cloud_2d_block_churn():
 
 def test_column_3d_two_levels():
     run_and_compare(S.COLUMN_3D_SMALL, 8)
+
+
+def test_cloud_3d_churn_latest_only_rebuild():
+    """3D dispersed cloud with topology changes through the graph path and the
+    single-tree level-0 rebuild forced on: gate A against the oracle."""
+    _need_gpu()
+    osim, dsim = build_both(S.scene(S.CLOUD_3D_SMALL))
+    dsim.latest_only_min_cells = 0
+    rng = np.random.default_rng(21)
+    v = rng.normal(0, 0.08, (len(osim.p), 3)).clip(-0.45, 0.45)
+    osim.p.v[:] = v
+    dsim.particles.v = v
+    changes = 0
+    for s in range(12):
+        osim.step()
+        dsim.step()
+        assert dsim.topology.tile_set() == osim.topo.tile_set(), f"step {s}"
+        if not osim.last_report.noop:
+            changes += 1
+    assert changes > 0
+    assert field_diff(osim, dsim) <= 1e-9
+    assert particle_diff(osim, dsim) <= 1e-9
+
+
+def test_fp32_dense_column_mode5():
+    """Dense sampling (8 per cell) selects the 4-round P2G blocks (mode 5):
+    gate B against the fp64 oracle after 15 steps."""
+    _need_gpu()
+    sc = S.scene(S.COLUMN_3D_SMALL, runtime__dtype="f32", particles__per_cell=8)
+    osim, dsim = build_both(sc)
+    assert dsim.p2g_mode == 5
+    for _ in range(15):
+        osim.step()
+        dsim.step()
+    assert dsim.topology.tile_set() == osim.topo.tile_set()
+    x = dsim.particles.x.cpu().numpy()
+    v = dsim.particles.v.double().cpu().numpy()
+    rx = np.linalg.norm(x - osim.p.x) / np.linalg.norm(osim.p.x)
+    rv = np.linalg.norm(v - osim.p.v) / max(np.linalg.norm(osim.p.v), 1e-30)
+    assert rx <= 1e-5, rx
+    assert rv <= 1e-4, rv
 
 
 def test_dune_3d_inlet_outlet():
