@@ -262,6 +262,31 @@ def test_fp32_powder_3d_short():
     assert np.abs(da[perm] - oa).max() <= 1e-9
 
 
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_powder_entrainment_stressed_column(dtype):
+    """Entrainment from a collapsing (stressed) column: fp64 gate A on phi
+    (<= 1e-9 relative L2); fp32 (surface-restricted stress raster in the P2G
+    layout) within 5e-3 relative L2 of the fp64 oracle: phi ~ 1e-8 here and
+    the source's surface / eta thresholds amplify fp32 round-off."""
+    _need_gpu()
+    sc = S.scene(S.COLUMN_3D_SMALL, runtime__dtype=dtype, powder__enabled=True,
+                 powder__entrain=0.02)
+    osim, dsim = build_both(sc)
+    for _ in range(20):
+        osim.step()
+        dsim.step()
+    assert dsim.topology.tile_set() == osim.topo.tile_set()
+    ow = osim.solver.last_roles(0)[1] if osim.solver.k[0] else 0
+    dw = dsim.solver.last_roles(0)[1] if dsim.solver.k[0] else 0
+    oa = osim.solver.arrays(ow, 0)["phi"]
+    da = dsim.solver.arrays(dw, 0)["phi"].double().cpu().numpy()
+    dmap = {tuple(c): i for i, c in enumerate(dsim.topology.cell_coords(0))}
+    perm = np.array([dmap[tuple(c)] for c in osim.topo.cell_coords(0)])
+    assert np.abs(oa).max() > 0.0
+    rel = np.linalg.norm(da[perm] - oa) / np.linalg.norm(oa)
+    assert rel <= (1e-9 if dtype == "f64" else 5e-3), rel
+
+
 def test_stress_raster_fp32_kernels_agree():
     """The fp32 stress raster in the P2G layout (per-warp node boxes) equals
     the per-particle atomic kernel within fp32 summation order."""
