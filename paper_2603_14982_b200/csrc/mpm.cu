@@ -1501,6 +1501,11 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
 // cell's particles are broadcast; at each cell change the lanes flush into a
 // block-wide shared-memory box (one conflict-free RED per lane and row), and
 // the block box is flushed to HBM once.  No coverage tests, no idle-node work.
+// min resident 64-thread blocks per SM for the fp32 P2G (10 = the dynamic
+// shared-memory limit; caps the 3D kernel at 96 registers)
+#ifndef P2G2_MIN_BLOCKS
+#define P2G2_MIN_BLOCKS 10
+#endif
 #ifndef P2G2_MAXN
 #define P2G2_MAXN 144
 #endif
@@ -1850,13 +1855,13 @@ __device__ __forceinline__ void p2g_box_merge(const float* sacc, int NW, int MAX
 }
 
 template <int D, int NW, int ROUNDS>
-__global__ void __launch_bounds__(32 * NW) k_p2g_cell2(PartArgs P, TopoL0 t0, MatParams mp, float* ras,
+__global__ void __launch_bounds__(32 * NW, P2G2_MIN_BLOCKS) k_p2g_cell2(PartArgs P, TopoL0 t0, MatParams mp, float* ras,
                                                        int64_t rs, mlbm_error_t* err) {
     constexpr int K = Geo<D>::K, NV = 3 + 3 * D, NS = D * (D + 1) / 2;
     constexpr int MAXN = P2G2_MAXN, REC = 32, BT = 32 * NW;
     extern __shared__ __align__(16) float p2g_smem[];
     float* sacc = p2g_smem;                                  // [NW][NV][MAXN]
-    float* slab = p2g_smem + NW * NV * MAXN;                 // [NW][32][REC]
+    float* slab = p2g_smem + NW * NV * MAXN;                 // [NW][REC / 4][32] float4
     __shared__ int s_lo[3], s_hi[3];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int p0 = blockIdx.x * (BT * ROUNDS);
@@ -1955,12 +1960,25 @@ __global__ void __launch_bounds__(32 * NW) k_p2g_cell2(PartArgs P, TopoL0 t0, Ma
         const int nj = min(32, P.n - pw);
         if (nj <= 0) break;                               // warp-uniform
         const int p = pw + lane;
-        p2g_record<D>(P, mp, p, lane < nj, &wslab[lane * REC]);
+        int base[3];
+        {
+            // the record is built in registers and stored chunk-major
+            // ([chunk][lane] float4): the 128-bit stores are conflict-free (a
+            // lane-major 128 B record stride is an 8-way conflict) and the
+            // broadcast reads of particle j sit at constant offsets from j
+            float rec[REC];
+#pragma unroll
+            for (int k = 0; k < REC; ++k) rec[k] = 0.f;
+            p2g_record<D>(P, mp, p, lane < nj, rec);
+            float4* w4 = reinterpret_cast<float4*>(wslab) + lane;
+#pragma unroll
+            for (int v4 = 0; v4 < NREC4; ++v4)
+                w4[v4 * 32] = make_float4(rec[4 * v4], rec[4 * v4 + 1], rec[4 * v4 + 2], rec[4 * v4 + 3]);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) base[a] = __float_as_int(rec[a]);
+        }
         __syncwarp();
         // runs of equal stencil base (particles sorted by cell)
-        int base[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) base[a] = __float_as_int(wslab[lane * REC + a]);
         bool start = lane < nj;
         {
             bool same = lane > 0;
@@ -1978,11 +1996,11 @@ __global__ void __launch_bounds__(32 * NW) k_p2g_cell2(PartArgs P, TopoL0 t0, Ma
     #pragma unroll
             for (int qv = 0; qv < NV; ++qv) acc[qv] = 0.f;
             for (int j = j0; j < j1; ++j) {
-                const float4* rp = reinterpret_cast<const float4*>(&wslab[j * REC]);
+                const float4* rp = reinterpret_cast<const float4*>(wslab) + j;
                 float r[4 * NREC4];
     #pragma unroll
                 for (int v4 = 0; v4 < NREC4; ++v4) {
-                    const float4 t = rp[v4];
+                    const float4 t = rp[v4 * 32];
                     r[4 * v4] = t.x; r[4 * v4 + 1] = t.y; r[4 * v4 + 2] = t.z; r[4 * v4 + 3] = t.w;
                 }
                 float wa[D], dwa[D];
@@ -2088,7 +2106,7 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
     using RW = Rows<D>;
     extern __shared__ __align__(16) float p2g_smem[];
     float* sacc = p2g_smem;                                  // [NW][NV][MAXN]
-    float* slab = p2g_smem + NW * NV * MAXN;                 // [NW][32][REC]
+    float* slab = p2g_smem + NW * NV * MAXN;                 // [NW][REC / 4][32] float4
     __shared__ int s_lo[3], s_hi[3];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int p = blockIdx.x * BT + threadIdx.x;
@@ -2151,7 +2169,9 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
         for (int k = 0; k < D * D; ++k) F[k] = pp[(PR::F + k) * P.ps + p];
         kirchhoff<D, float>(F, mp, tau);
         const float V0 = pp[PR::V0 * P.ps + p];
-        float* r = &wslab[lane * REC];
+        float r[REC];
+#pragma unroll
+        for (int k = 0; k < REC; ++k) r[k] = 0.f;
 #pragma unroll
         for (int a = 0; a < 3; ++a) r[a] = __int_as_float(a < D ? base[a] : 0);
 #pragma unroll
@@ -2161,6 +2181,12 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
         for (int a = 0; a < D; ++a)
 #pragma unroll
             for (int b = a; b < D; ++b) r[3 + D + (k++)] = V0 * tau[a * D + b];
+        // chunk-major records ([chunk][lane] float4): conflict-free 128-bit
+        // stores, broadcast reads at constant offsets from the particle
+        float4* w4 = reinterpret_cast<float4*>(wslab) + lane;
+#pragma unroll
+        for (int v4 = 0; v4 < 3; ++v4)
+            w4[v4 * 32] = make_float4(r[4 * v4], r[4 * v4 + 1], r[4 * v4 + 2], r[4 * v4 + 3]);
     }
     __syncthreads();
     const int any_need = __syncthreads_or(need_runs != 0u);
@@ -2205,11 +2231,11 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
 #pragma unroll
         for (int q = 0; q < NV; ++q) acc[q] = 0.f;
         for (int j = j0; j < j1; ++j) {
-            const float4* rp = reinterpret_cast<const float4*>(&wslab[j * REC]);
+            const float4* rp = reinterpret_cast<const float4*>(wslab) + j;
             float r[12];
 #pragma unroll
             for (int v4 = 0; v4 < 3; ++v4) {
-                const float4 t = rp[v4];
+                const float4 t = rp[v4 * 32];
                 r[4 * v4] = t.x; r[4 * v4 + 1] = t.y; r[4 * v4 + 2] = t.z; r[4 * v4 + 3] = t.w;
             }
             float w = 1.f;
