@@ -1501,10 +1501,10 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
 // cell's particles are broadcast; at each cell change the lanes flush into a
 // block-wide shared-memory box (one conflict-free RED per lane and row), and
 // the block box is flushed to HBM once.  No coverage tests, no idle-node work.
-// min resident 64-thread blocks per SM for the fp32 P2G (10 = the dynamic
-// shared-memory limit; caps the 3D kernel at 96 registers)
+// min resident 64-thread blocks per SM for the fp32 P2G (9: up to 112
+// registers; 1-3 % faster than 10 at 96 registers, profiles/r1_p2g_box_sweep.txt)
 #ifndef P2G2_MIN_BLOCKS
-#define P2G2_MIN_BLOCKS 10
+#define P2G2_MIN_BLOCKS 9
 #endif
 #ifndef P2G2_MAXN
 #define P2G2_MAXN 144
