@@ -113,7 +113,7 @@ class CouplingFields:
         r = grid.ras[:, :n]
         R = grid.R
         self.eps = r[R["eps"]]
-        self.eta = r[R["eta"]]
+        self.eta = r[R["etae"]]          # eta_eff (coupling.py:127)
         self.v = r[R["vmom"]:R["vmom"] + d].t()
         self.area = r[R["area"]]
         self.mass = r[R["mass"]]
@@ -533,6 +533,11 @@ class CoupledSim:
         # it halves the level-0 migration but doubles the rebuild-graph keys
         # (the tree is part of the key): worth it only for large level 0s
         if not self.latest_only_rebuild or self.topology.capacity_cells(0) < self.latest_only_min_cells:
+            return None
+        # with mpm_cadence > 1 the held hook (coupling.py:460-465) reads the
+        # force / eps rows of the write tree on the non-MPM steps: that tree
+        # must migrate too
+        if self.cadence > 1:
             return None
         return {0: self.solver.roles(0)[0]}
 

@@ -773,7 +773,8 @@ __device__ __forceinline__ void stream_pull(const FieldsT<R>& src, const R* fb, 
 
 }  // namespace tp
 
-// mode 0 fused, 1 stream only, 2 collide+bc only
+// mode 0 fused stream+collide+bc, 1 stream only, 2 collide+bc of dst's bare
+// moments, 3 collide only (collide_kernel), 4 boundaries only (boundary_kernel)
 #ifndef LEVEL_TPC3
 #define LEVEL_TPC3 2
 #endif
@@ -787,14 +788,14 @@ template <int D, typename R> struct LevelCfg {
 #endif
 template <int D, typename R, int MODE>
 __global__ void __launch_bounds__(LevelCfg<D, R>::THREADS,
-                                  (D == 3 && sizeof(R) == 4 && MODE != 2) ? LEVEL_MINB : 1)
+                                  (D == 3 && sizeof(R) == 4 && MODE <= 1) ? LEVEL_MINB : 1)
 level_kernel(const StepArgs A) {
     constexpr int T = Geo<D>::T, Q = Geo<D>::Q, NS = Geo<D>::NS, NM = Geo<D>::NM;
     constexpr int TPC = LevelCfg<D, R>::TPC;
     constexpr int HB = HaloTable<D>::HB, NCO = CoefSlots<D>::N;
     __shared__ R fbuf_all[TPC][Q * T];
     // halo coefficient staging: 2D only (3D evaluates its halo in registers)
-    constexpr bool HC = !(MODE == 2 || MODE == 3 || MODE == 4) && D == 2;
+    constexpr bool HC = MODE <= 1 && D == 2;
     __shared__ R hcoef_all[HC ? TPC : 1][HC ? NCO * HB : 1];
     __shared__ int snb_all[TPC][Geo<D>::NB];
 
@@ -807,7 +808,7 @@ level_kernel(const StepArgs A) {
     const FieldsT<R> src = fields_of<R>(A.src), dst = fields_of<R>(A.dst);
     const R h3xyz = R(A.cp.h3_xyz);
 
-    if (MODE != 2 && valid && lc < Geo<D>::NB) snb[lc] = A.lv.nbr[(int64_t)tile * Geo<D>::NB + lc];
+    if (MODE <= 1 && valid && lc < Geo<D>::NB) snb[lc] = A.lv.nbr[(int64_t)tile * Geo<D>::NB + lc];
 
     const int64_t cell = (int64_t)tile * T + lc;
     int l[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
@@ -821,9 +822,13 @@ level_kernel(const StepArgs A) {
     }
     const int any_bc = __syncthreads_or(valid && (tf & MLBM_TF_BC));
     const bool active = cf & MLBM_CF_ACTIVE;
+    // boundary_kernel touches the outlet / inlet layers only (block-uniform)
+    if constexpr (MODE == 4) {
+        if (!any_bc) return;
+    }
 
     R dr, mm[D], pi[NS];
-    if constexpr (MODE != 2 && D == 3) {
+    if constexpr (MODE <= 1 && D == 3) {
         // eps / phi ride along to the write tree: fetch them now so the
         // loads overlap the stream instead of stalling the epilogue
         R eps_c = R(0), phi_c = R(0);
@@ -857,7 +862,7 @@ level_kernel(const StepArgs A) {
             }
             return;
         }
-    } else if constexpr (MODE != 2) {
+    } else if constexpr (MODE <= 1) {
         Coef<D, R> own;
         if (valid) {
             R m[NM];
@@ -1006,7 +1011,7 @@ level_kernel(const StepArgs A) {
         }
     }
 
-    if (valid) {
+    if (valid && (MODE != 4 || (tf & MLBM_TF_BC))) {
 #pragma unroll
         for (int k = 0; k < NM; ++k) dst.at(k, cell) = out[k];
         if ((MODE == 0 || !active) && MODE != 4) {

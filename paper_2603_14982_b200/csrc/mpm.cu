@@ -27,7 +27,10 @@ template <int D> struct Rows {
     static constexpr int MASS = 0, MOM = 1, FINT = 1 + D, ETA = 1 + 2 * D, AREA = 2 + 2 * D,
                          VMOM = 3 + 2 * D, VEL = 3 + 3 * D, FS = 3 + 4 * D, EPS = 3 + 5 * D,
                          GRAD = 4 + 5 * D, REL = 4 + 6 * D, SIG = 4 + 7 * D,
-                         N = 4 + 7 * D + Geo<D>::NS, NACC = 3 + 3 * D;
+                         // eta_eff = max(eta - phi, 0) (coupling.py:127) in its own
+                         // row: k_exchange's neighbour eps reads the raw ETA row
+                         ETAE = 4 + 7 * D + Geo<D>::NS,
+                         N = 5 + 7 * D + Geo<D>::NS, NACC = 3 + 3 * D;
 };
 // particle row layout (after the float64 positions): v[D] C[D*D] F[D*D] m V0 vc
 template <int D> struct PRows {
@@ -514,7 +517,7 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? EXCH_MINB : 1) k_exchang
         t0.at(fi_eps<D>(), c) = eps;
         t1.at(fi_eps<D>(), c) = eps;
         ras[RW::EPS * rs + c] = eps;
-        ras[RW::ETA * rs + c] = eta;                   // becomes eta_eff
+        ras[RW::ETAE * rs + c] = eta;                  // eta_eff (ETA stays raw: neighbours read it)
     }
     // MPM grid update (granular.py:313-341)
     R vel[D];
@@ -986,7 +989,7 @@ __global__ void k_powder_diffuse(PowderArgs A) {
     for (int a = 0; a < D; ++a) g[a] = A.lv.tile_xyz[slot * 3 + a] * 4 + l3[a];
     R lap = R(-2 * D) * adv[c];
     bool has_empty = false;
-    const R eta_c = A.with_source ? ras[RW::ETA * rs + c] : R(0);
+    const R eta_c = A.with_source ? ras[RW::ETAE * rs + c] : R(0);
     for (int a = 0; a < D; ++a)
         for (int sgn = 0; sgn < 2; ++sgn) {
             int nb[3] = {g[0], g[1], g[2]};
@@ -998,7 +1001,7 @@ __global__ void k_powder_diffuse(PowderArgs A) {
             lap += adv[ni];
             if (A.with_source) {
                 if (s < 0) has_empty = true;
-                else if (ras[RW::ETA * rs + ni] < R(1e-3)) has_empty = true;
+                else if (ras[RW::ETAE * rs + ni] < R(1e-3)) has_empty = true;
             }
         }
     R out = adv[c] + R(A.sign * A.diffusion * A.dt) * lap;
@@ -2285,7 +2288,7 @@ __global__ void k_surface_need(mlbm_level_t lv, const R* __restrict__ ras, int64
     using RW = Rows<D>;
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= (int64_t)live_tiles(lv) * T) return;
-    const R eta_c = ras[RW::ETA * rs + c];
+    const R eta_c = ras[RW::ETAE * rs + c];
     if (!(eta_c > R(0) && eta_c < R(eta_surface))) return;
     const int slot = (int)(c / T), lc = (int)(c % T);
     const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
@@ -2300,7 +2303,7 @@ __global__ void k_surface_need(mlbm_level_t lv, const R* __restrict__ ras, int64
             else nb[a] = nb[a] < 0 ? 0 : (nb[a] >= lv.cells[a] ? lv.cells[a] - 1 : nb[a]);
             const int sl = lv.tile_map[g3(lv.tiles, nb[0] >> 2, nb[1] >> 2, D == 3 ? nb[2] >> 2 : 0)];
             if (sl < 0) has_empty = true;
-            else if (ras[RW::ETA * rs + (int64_t)sl * T + local_of<D>(nb[0] & 3, nb[1] & 3, nb[2] & 3)] < R(1e-3))
+            else if (ras[RW::ETAE * rs + (int64_t)sl * T + local_of<D>(nb[0] & 3, nb[1] & 3, nb[2] & 3)] < R(1e-3))
                 has_empty = true;
         }
     if (!has_empty) return;

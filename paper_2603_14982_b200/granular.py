@@ -217,7 +217,8 @@ def raster_rows(d):
     NS = d * (d + 1) // 2
     return {"mass": 0, "mom": 1, "fint": 1 + d, "eta": 1 + 2 * d, "area": 2 + 2 * d,
             "vmom": 3 + 2 * d, "vel": 3 + 3 * d, "fs": 3 + 4 * d, "eps": 3 + 5 * d,
-            "grad": 4 + 5 * d, "rel": 4 + 6 * d, "sig": 4 + 7 * d, "n": 4 + 7 * d + NS,
+            "grad": 4 + 5 * d, "rel": 4 + 6 * d, "sig": 4 + 7 * d, "etae": 4 + 7 * d + NS,
+            "n": 5 + 7 * d + NS,
             "nacc": 3 + 3 * d}
 
 

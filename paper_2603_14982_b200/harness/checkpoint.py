@@ -23,7 +23,9 @@ def save_checkpoint(path, sim):
     state = {
         "format": FORMAT, "d": topo.d, "levels": L, "finest": tuple(topo.finest_cells),
         "dtype": str(pair.dtype),
-        "tiles": sorted(topo.tile_set()),
+        # (level, tile coords, kind) rows as one int64 tensor: the file holds only
+        # tensors and plain containers, so it loads with weights_only=True
+        "tiles": torch.tensor(sorted(topo.tile_set()), dtype=torch.int64).reshape(-1, 2 + topo.d),
         "trees": [[pair.trees[t].levels[l].data[:, :topo.cell_count(l)].cpu().clone()
                    for l in range(L)] for t in range(2)],
         "k": list(solver.k), "bounce": pair.bounce, "step_count": sim.step_count,
@@ -38,7 +40,7 @@ def save_checkpoint(path, sim):
 
 def load_checkpoint(path, sim):
     """Restore ``sim`` (built from the same scene) to the saved state."""
-    st = torch.load(path, weights_only=False)
+    st = torch.load(path, weights_only=True)
     topo, pair, solver = sim.topology, sim.pair, sim.solver
     if st.get("format") != FORMAT:
         raise ValueError(f"unsupported checkpoint format {st.get('format')}")
@@ -47,7 +49,7 @@ def load_checkpoint(path, sim):
     if st["dtype"] != str(pair.dtype):
         raise ValueError(f"checkpoint dtype {st['dtype']} != {pair.dtype}")
     torch.cuda.synchronize()
-    topo.set_tile_set(st["tiles"])
+    topo.set_tile_set({tuple(int(v) for v in row) for row in st["tiles"].tolist()})
     pair.ensure_capacity()
     for t in range(2):
         for l in range(topo.levels):

@@ -59,9 +59,21 @@ def particle_diff(osim, dsim):
     return float(max(dx, dv, dF))
 
 
-def run_and_compare(scene_dict, steps, tol=1e-9, check_streaks=True):
+def set_level0_field(osim, dsim, name, fn):
+    """Write fn(coords) into field `name` of level 0 in both trees of both
+    sims (coordinate-keyed: the device stores cells in its own slot order)."""
+    oc = osim.topo.cell_coords(0).astype(float)
+    dc = dsim.topology.cell_coords(0).astype(float)
+    for t in range(2):
+        osim.solver.arrays(t, 0)[name][:] = fn(oc)
+        dsim.solver.arrays(t, 0)[name] = fn(dc)
+
+
+def run_and_compare(scene_dict, steps, tol=1e-9, check_streaks=True, prepare=None):
     _need_gpu()
     osim, dsim = build_both(scene_dict)
+    if prepare is not None:
+        prepare(osim, dsim)
     assert dsim.topology.tile_set() == osim.topo.tile_set()
     for s in range(steps):
         osim.step()
@@ -200,6 +212,19 @@ def test_fp32_sandstorm_3d_three_levels():
 
 def test_powder_3d_solids():
     run_and_compare(S.POWDER_3D_SMALL, 6)
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_powder_over_sand_exchange_fp64(d):
+    """A powder fraction of O(1e-2) over the sand (eta > phi > 0): the
+    exchange's neighbour eps for grad eps must use the raw eta, not eta_eff
+    written by another thread (coupling.py:127,159-182); gate A."""
+    sc = S.scene(S.POWDER_BOX_2D if d == 2 else S.POWDER_3D_SMALL)
+
+    def phi0(c):
+        return 0.03 * (1.0 + np.sin(0.37 * c[:, 0] + 0.21 * c[:, 1])) * (c[:, 1] < 24)
+
+    run_and_compare(sc, 6, prepare=lambda o, dd: set_level0_field(o, dd, "phi", phi0))
 
 
 def test_fp32_column_3d_short():

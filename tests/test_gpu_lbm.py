@@ -179,3 +179,158 @@ def test_fp32_shifted_rel_l2(d):
     for nm in names:
         r = rel_l2(otopo, lambda l: last(osv, l), dsv.topology, lambda l: last(dsv, l), [nm])
         assert r <= 1e-5, (nm, r)
+
+
+class DeviceNaive:
+    """The reference's NaiveReference (harness/reference.py:31-106) over the
+    device kernels: one dedicated (current, next) buffer pair per level (2L
+    buffers outside the solver's ping-pong pair), each level step driven as
+    stream_kernel -> collide_kernel -> boundary_kernel (reference.py:67-72)."""
+
+    def __init__(self, dsv):
+        from paper_2603_14982_b200.sparse_grid import LevelFields, fresh_block
+        self.sv = dsv
+        topo = dsv.topology
+        self.buffers = []
+        for l in range(topo.levels):
+            pair = []
+            for _ in range(2):
+                blk = fresh_block(topo.d, topo.capacity_cells(l), dsv.dtype, topo.device)
+                pair.append(LevelFields(topo.d, blk, live=(lambda l=l: topo.cell_count(l))))
+            self.buffers.append(pair)
+        self.k = [0] * topo.levels
+
+    def load_from(self, trees_levels):
+        for l, lf in enumerate(trees_levels):
+            for b in self.buffers[l]:
+                b.data.copy_(lf.data)
+
+    def cur(self, l):
+        return self.buffers[l][self.k[l] % 2]
+
+    def nxt(self, l):
+        return self.buffers[l][1 - self.k[l] % 2]
+
+    def _sc(self, l):
+        self.sv.stream_kernel(l, self.cur(l), self.nxt(l))
+        self.sv.collide_kernel(l, self.cur(l), self.nxt(l))
+        self.sv.boundary_kernel(l, self.nxt(l))
+        self.k[l] += 1
+
+    def _down(self, l, sub):
+        c = l + 1
+        kc = self.k[c]
+        self.sv.downward_kernel(l, sub, self.buffers[c][(kc - 1) % 2], self.buffers[c][kc % 2],
+                                self.cur(l))
+
+    def _up(self, l):
+        c = l + 1
+        self.sv.upward_kernel(l, self.cur(l), self.buffers[c][self.k[c] % 2])
+
+    def advance_bounce(self):
+        levels = self.sv.topology.levels
+        for cycle in self.sv._schedule:
+            for kind, level, sub in cycle["pre"]:
+                {"down": lambda: self._down(level, sub), "sc": lambda: self._sc(level),
+                 "up": lambda: self._up(level)}[kind]()
+            if levels > 1:
+                self._down(0, cycle["s0"])
+            self._sc(0)
+            if levels > 1 and cycle["s0"] == 2:
+                self._up(0)
+        self.sv.raise_pending()
+
+
+def _bc_spec(d, y0):
+    if d == 2:
+        faces = {"x_min": OL.LogInlet(0.04, 0.35, y0), "x_max": "outlet",
+                 "y_min": "wall", "y_max": "outlet"}
+    else:
+        faces = {"x_min": OL.LogInlet(0.04, 0.35, y0), "x_max": "outlet",
+                 "y_min": "wall", "y_max": "outlet", "z_min": "periodic", "z_max": "periodic"}
+    return OL.BoundarySpec(d=d, faces=faces)
+
+
+@pytest.mark.parametrize("d,levels", [(2, 3), (3, 2)])
+def test_naive_reference_order_fp64(d, levels):
+    """stream_kernel -> collide_kernel -> boundary_kernel on external 2L
+    buffers (test_harness.py:119-146) reproduces the oracle's two-tree run,
+    with outlets, a log inlet and a wall, across refinement interfaces."""
+    _need_gpu()
+    cells = (64, 64) if d == 2 else (32, 32, 32)
+    spec = _bc_spec(d, 6.0 if d == 2 else 3.0)
+    otopo = oracle_static_refined(cells, levels, central_mask(cells, pad=8 if d == 2 else 4),
+                                  periodic=spec.periodic_axes())
+    g = (0.0, -1e-5) + ((0.0,) if d == 3 else ())
+    osv, dsv = build_pair(otopo, torch.float64, smooth_fields(d, 17), spec=spec, gravity=g)
+    naive = DeviceNaive(dsv)
+    naive.load_from(dsv.pair.trees[0].levels)
+    for _ in range(4):
+        osv.advance_bounce()
+        naive.advance_bounce()
+    names = moments(d) + ["eps", "phi"]
+    w = compare_levels(otopo, lambda l: last(osv, l), dsv.topology,
+                       lambda l: naive.cur(l), names)
+    assert max(w.values()) <= 1e-12, w
+    # and the device's own fused two-tree run agrees with its per-kernel run
+    for _ in range(4):
+        dsv.advance_bounce()
+    w2 = compare_levels(otopo, lambda l: last(osv, l), dsv.topology, lambda l: last(dsv, l), names)
+    assert max(w2.values()) <= 1e-12, w2
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_collide_kernel_force_and_tau_arrays_fp64(d):
+    """collide_kernel with a per-cell force pair and a per-cell tau array
+    (solver.py:410-418) and boundary_kernel alone, vs the oracle."""
+    _need_gpu()
+    cells = (32, 32) if d == 2 else (16, 16, 16)
+    spec = _bc_spec(d, 3.0)
+    otopo = OG.Topology.uniform(cells, 1, spec.periodic_axes())
+    osv, dsv = build_pair(otopo, torch.float64, smooth_fields(d, 19), spec=spec)
+    # the device stores cells in its own slot order: build the per-cell
+    # arrays from coordinates so both sides see the same values
+    rng = np.random.default_rng(4)
+    kf = rng.uniform(0.1, 0.7, size=(d + 1, d))
+
+    def per_cell(pos):
+        F = [1e-4 * np.sin(pos @ kf[a]) for a in range(d)]
+        tau = 0.8 + 0.3 * (1 + np.sin(pos @ kf[d]))
+        return F, tau
+    opos = otopo.cell_coords(0).astype(float)
+    dpos = dsv.topology.cell_coords(0).astype(float)
+    oF, otau = per_cell(opos)
+    dF, dtau = per_cell(dpos)
+    orr, ow = osv.roles(0)
+    osv.stream_kernel(0, osv.arrays(orr, 0), osv.arrays(ow, 0))
+    osv.collide_kernel(0, osv.arrays(orr, 0), osv.arrays(ow, 0), force=oF, tau_eff=otau)
+    osv.boundary_kernel(0, osv.arrays(ow, 0))
+    dr_, dw_ = dsv.roles(0)
+    dsv.stream_kernel(0, dsv.arrays(dr_, 0), dsv.arrays(dw_, 0))
+    dsv.collide_kernel(0, dsv.arrays(dr_, 0), dsv.arrays(dw_, 0), force=dF, tau_eff=dtau)
+    dsv.boundary_kernel(0, dsv.arrays(dw_, 0))
+    dsv.raise_pending()
+    w = compare_levels(otopo, lambda l: osv.arrays(ow, l), dsv.topology,
+                       lambda l: dsv.arrays(dw_, l), moments(d) + ["eps", "phi"])
+    assert max(w.values()) <= 1e-13, w
+
+
+def test_collide_kernel_reports_divergence():
+    """Non-physical density after streaming raises DivergenceError with the
+    cell coordinates (solver.py:398-406)."""
+    _need_gpu()
+    from paper_2603_14982_b200.lattice import DivergenceError
+    otopo = OG.Topology.uniform((16, 16), 1)
+    _, dsv = build_pair(otopo, torch.float64, smooth_fields(2, 1))
+    r, w = dsv.roles(0)
+    dsv.stream_kernel(0, dsv.arrays(r, 0), dsv.arrays(w, 0))
+    dst = dsv.arrays(w, 0)
+    rho = dst["rho"].clone()
+    pos = dsv.topology.cell_coords(0)
+    bad = int(np.nonzero((pos[:, 0] == 5) & (pos[:, 1] == 7))[0][0])
+    rho[bad] = -1.0
+    dst["rho"] = rho
+    dsv.collide_kernel(0, dsv.arrays(r, 0), dst)
+    with pytest.raises(DivergenceError) as ei:
+        dsv.raise_pending()
+    assert ei.value.level == 0 and (5, 7) in [tuple(c) for c in ei.value.cells]
