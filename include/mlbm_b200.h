@@ -225,13 +225,20 @@ int mlbm_plan_level(int32_t n, const uint8_t* own, const uint8_t* storage,
  * invariant counts status[L..L+2] of the current topology (ring violations
  * are counted as (leaf, absent neighbour) pairs), and per level the tile count
  * status[L+4+l] and fresh-tile count status[2L+4+l] of the new plan.  Per-level buffer
- * arrays have h->levels entries; bar: 2 zero-initialised words. */
+ * arrays have h->levels entries; bar: 2 zero-initialised words.  Seeds come either
+ * from the n positions x (stride xs) or, with n = 0 and ext_count non-NULL, from
+ * mlbm_g2p of the same step (seeds filled, *ext_count = its leaf-invariant count,
+ * consumed and reset to 0 here).  seeds are all zero again on return. */
 int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_t* const* cur,
                     uint8_t* const* eff, uint8_t* const* par, uint8_t* const* own,
                     uint8_t* const* nkind, uint8_t* const* stor, int16_t* const* streak,
                     uint8_t* seeds, const uint8_t* static_tiles, const double* x, int64_t xs,
-                    int32_t n, int32_t* status, mlbm_error_t* err, unsigned int* bar,
-                    void* stream);
+                    int32_t n, int32_t* ext_count, int32_t* status, mlbm_error_t* err,
+                    unsigned int* bar, void* stream);
+/* optional stage timestamps of the adapt passes into a caller-owned buffer of 64
+ * uint64 (NULL: off); the library never allocates */
+int mlbm_adapt_set_timestamps(unsigned long long* buf);
+int mlbm_adapt_bits_set_timestamps(unsigned long long* buf);
 
 /* Invariants (adapt.py:374-389): leaf coverage of every finest tile exactly
  * once, two-tile rings, particles inside level-0 leaves -> viol[0..2]. */
@@ -277,6 +284,14 @@ int mlbm_init_new_cells(const mlbm_hier_t* old_h, const mlbm_hier_t* nh, int32_t
 int mlbm_raster_rows(int32_t dim);
 int mlbm_particle_rows(int32_t dim);
 
+/* Kirchhoff stress rows tau(F) = U diag(2 mu ln s + lam tr ln s) U^T
+ * (granular.py:260-279) of every particle from its F rows.  mlbm_g2p keeps them
+ * current (from its own decomposition of the updated F); call this once after
+ * F is set from outside (initial state, user edits).  mlbm_p2g and the stress
+ * rasters read these rows. */
+int mlbm_particle_stress(int32_t dim, int32_t n, void* p, int64_t ps, double lam, double mu,
+                         double alpha, int32_t dtype, void* stream);
+
 /* stencil + Kirchhoff stress + P2G scatter fused with rasterize_fractions
  * (granular.py:137-178, 260-310; coupling.py:96-131).  x: float64 [dim][ps];
  * p: run-dtype particle rows [rows][ps]; ras: zeroed accumulator rows. */
@@ -313,12 +328,28 @@ int mlbm_exchange(const mlbm_level_t* lv0, mlbm_fields_t w_tree, mlbm_fields_t r
 
 /* gather, advect (wrap / clamp to [2, dim-2]), F update, SVD + Drucker-Prager
  * (granular.py:344-412), reading the (sorted) _in rows and writing the _out rows
- * (in place when they alias). clamped[0] += clamped coordinates; clamped[1] |= CFL
- * violation (max |v| dt >= 0.5, granular.py:428-432). */
+ * (in place when they alias); the tau rows get the Kirchhoff stress of the new F.
+ * clamped[0] += clamped coordinates; clamped[1] |= CFL violation (max |v| dt >= 0.5,
+ * granular.py:428-432).  seeds (optional, level-0 tile grid bytes, all zero on
+ * entry): seeds[tile of floor(x_new) // 4] = 1 for the adapt pass that follows
+ * (adapt.py:54-65), with nonleaf[0] += particles whose tile is not a level-0 leaf
+ * of kind0 (adapt.py:374-389) and MLBM_ERR_DOMAIN for a non-finite position;
+ * mlbm_adapt_pass then runs with n = 0 and ext_count = nonleaf. */
+/* NACC snow (absent from the reference, oracle/mpm.py:
+ * nacc_return_map is the specification): critical-state slope M, cohesion beta,
+ * hardening factor xi, softening coefficient alpha_soft.  With snow non-NULL,
+ * mlbm_g2p's return map is NACC on the Hencky elasticity (lam, mu) and the
+ * vol_corr row holds the hardening state (q >= 0; -(q + 1) once cracked). */
+typedef struct {
+    double M, beta, xi, alpha_soft;
+} mlbm_snow_t;
+
 int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, const double* x_in, double* x_out,
              const void* p_in, void* p_out, const int32_t* pid_in, int32_t* pid_out,
-             int64_t ps, double lam, double mu, double alpha, const void* ras, int64_t rs,
-             double dt, int32_t plastic, int32_t dtype, int32_t* clamped, mlbm_error_t* err,
+             int64_t ps, double lam, double mu, double alpha, const mlbm_snow_t* snow,
+             const void* ras, int64_t rs,
+             double dt, int32_t plastic, int32_t dtype, int32_t* clamped,
+             uint8_t* seeds, const uint8_t* kind0, int32_t* nonleaf, mlbm_error_t* err,
              void* stream);
 
 /* entrainment stress raster (coupling.py:283-294) and powder transport
@@ -341,6 +372,41 @@ int mlbm_powder(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm_fields_t dst, v
                 double entrain, double eta_surface, int32_t with_source, int32_t dtype,
                 void* stream);
 
+/* The reference's standalone coupling functions as per-cell passes over the
+ * level-0 raster (the fused mlbm_exchange runs the same device code):
+ *   MLBM_COUPLE_FRACTIONS     rasterize_fractions' finish (coupling.py:96-131): a0 = phi;
+ *                             ETAE = max(eta - phi, 0), EPS = clip(1 - eta_eff - phi,
+ *                             eps_min, 1), VMOM <- v_cell = sum w m v / mass
+ *   MLBM_COUPLE_DRAG          difelice_drag (coupling.py:134-156): a0 = rho, u = velocity
+ *                             rows [dim][us]; FS, REL rows (no limiter)
+ *   MLBM_COUPLE_LIMIT         CoupledSim._limit_drag (coupling.py:379-401) on the FS rows
+ *   MLBM_COUPLE_GRAD_EPS      grad_eps (coupling.py:159-182) of a0 (NULL: the EPS row) into
+ *                             out [dim][os]
+ *   MLBM_COUPLE_MIXTURE_FORCE mixture_force (coupling.py:185-197): a0 = rho; GRAD rows,
+ *                             out [dim][os] = force on the fluid (g = lattice gravity) */
+enum { MLBM_COUPLE_FRACTIONS = 0, MLBM_COUPLE_DRAG = 1, MLBM_COUPLE_LIMIT = 2,
+       MLBM_COUPLE_GRAD_EPS = 3, MLBM_COUPLE_MIXTURE_FORCE = 4 };
+int mlbm_coupling_op(const mlbm_level_t* lv0, int32_t op, void* ras, int64_t rs, const void* a0,
+                     const void* u, int64_t us, void* out, int64_t os, double eps_min,
+                     double nu, double d_p, double re_min, double dt, double rho0,
+                     const double* g, int32_t dtype, void* stream);
+
+/* granular.stencil (granular.py:137-178): for particle p and node k of its 3^dim
+ * stencil (offsets k % 3, (k / 3) % 3, k / 9): idx[k][os] flat level-0 cell, w[k][os]
+ * weight, grad[b][k][os] dw/dx_b, dpos[b][k][os] node - particle.  Nodes outside a
+ * non-periodic domain or not stored at level 0 -> idx -1 and MLBM_ERR_STENCIL. */
+int mlbm_stencil(const mlbm_level_t* lv0, int32_t n, const double* x, int64_t ps, int32_t* idx,
+                 void* w, void* grad, void* dpos, int64_t os, int32_t dtype, mlbm_error_t* err,
+                 void* stream);
+
+/* powder_step (coupling.py:230-272): RK3 semi-Lagrangian backtrace of src's phi
+ * row along dst's velocity rows, 2*dim-point diffusion (sign = +1 stable, -1 the
+ * printed form), + dt * source[c] when source is non-NULL; writes dst's phi row.
+ * tmp: [n0] run-dtype scratch. */
+int mlbm_powder_step(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm_fields_t dst, void* tmp,
+                     double diffusion, double sign, double dt, const void* source,
+                     int32_t dtype, void* stream);
+
 /* diagnostics (coupling.py:500-531): out[0..dim-1] += vol sum rho u, out[dim] +=
  * vol sum phi, out[dim+1] = min(out[dim+1], eps) over leaf cells;
  * particles: out[0..dim-1] += sum m v, out[dim..2dim-1] += sum fs over the first
@@ -350,6 +416,12 @@ int mlbm_diag_level(const mlbm_level_t* lv, mlbm_fields_t f, double vol, int32_t
 int mlbm_diag_particles(int32_t dim, int32_t n, const void* p, int64_t ps, const void* ras,
                         int64_t rs, int64_t n0, const int32_t* live, int32_t dtype,
                         double* out, void* stream);
+
+/* buffer initialisation on the stream (used inside the captured step graphs
+ * instead of framework fill kernels): mlbm_memset = cudaMemsetAsync of bytes;
+ * mlbm_fill writes n elements of kind 0 u8, 1 i32, 2 f32, 3 f64 = value. */
+int mlbm_memset(void* p, int32_t value, int64_t bytes, void* stream);
+int mlbm_fill(void* p, int64_t n, int32_t kind, double value, void* stream);
 
 #ifdef __cplusplus
 }

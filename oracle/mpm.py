@@ -11,6 +11,8 @@ Restates ``pkg/src/mlbm/granular.py``:
     e = eps + vc/d, (d lam + 2 mu)/(2 mu))  granular.py:216-241
   * Kirchhoff stress                       granular.py:260-279
   * p2g / grid_update / g2p / mpm_step     granular.py:282-425
+  * SnowMaterial + nacc_return_map: the paper's snow, absent
+    from the reference — PARITY UNPINNED, see nacc_return_map
 """
 from __future__ import annotations
 
@@ -34,6 +36,134 @@ class SandMaterial:
         self.mu = self.E / (2 * (1 + self.nu))
         sf = np.sin(np.radians(self.friction_deg))
         self.alpha = np.sqrt(2.0 / 3.0) * 2.0 * sf / (3.0 - sf)
+
+
+@dataclass
+class SnowMaterial:
+    """Snow for the avalanche scene: Non-Associated Cam
+    Clay (Wolper et al. 2019) on the same Hencky elasticity as the sand, with
+    the paper's modified hardening law.  Not in the reference:
+    this restatement is the specification the device follows (parity
+    unpinned).
+
+    M: critical-state slope; beta: cohesion (tensile / compressive strength
+    ratio); xi: hardening factor of p0 = kappa (1e-5 + sinh(xi max(q, 0)));
+    alpha_soft: the paper's softening coefficient alpha; q_init: the initial
+    (softened) hardening parameter q."""
+    E: float = 3.5e5
+    nu: float = 0.3
+    M: float = 1.85
+    beta: float = 0.3
+    xi: float = 1.0
+    alpha_soft: float = 0.5
+    q_init: float = 0.05
+    floor_friction: float = 0.5
+    friction_deg: float = 30.0       # unused by NACC (kept for the scene schema)
+
+    def __post_init__(self):
+        self.lam = self.E * self.nu / ((1 + self.nu) * (1 - 2 * self.nu))
+        self.mu = self.E / (2 * (1 + self.nu))
+        self.alpha = 0.0
+
+    def kappa(self, d):
+        """Hencky bulk modulus: p = -kappa tr(e) with tau = 2 mu e + lam tr(e) I."""
+        return self.lam + 2.0 * self.mu / d
+
+
+def nacc_state_decode(qs):
+    """The per-particle hardening state lives in the vol_corr row: qs >= 0 is
+    the hardening parameter q of a particle that never reached q = 0; a
+    particle that did (cracked, cohesion 0 from then on) stores -(q + 1)."""
+    cracked = qs < 0.0
+    return np.where(cracked, -qs - 1.0, qs), cracked
+
+
+def nacc_return_map(e, qs, mat: SnowMaterial):
+    """NACC return map in principal log-strain space (Hencky elasticity) with
+    the softening law of PAPER.md:630-637.
+
+    e: (n, d) trial log stretches; qs: (n,) hardening state (nacc_state_decode).
+    p = -kappa tr(e), s = 2 mu dev(e), q_s = sqrt((6 - d)/2) |s|; yield
+    y = (1 + 2 beta) q_s^2 + M^2 (p + beta p0)(p - p0) <= 0 (Wolper et al. 2019):
+      p > p0          -> compressive tip  (p = p0, s = 0)
+      p < -beta p0    -> tensile tip      (p = -beta p0, s = 0)
+      y <= 0          -> elastic
+      else            -> s scaled onto the surface at fixed p (non-associated)
+    NACC's hardening increment of h = -log Jp is dh0 = log J_x - log J_trial,
+    J_x the elastic volume on the surface: the tip in the tip cases, else the
+    surface point on the line from (p_c = (1 - beta) p0 / 2, 0) to the trial
+    state.  The paper's law: dq = -alpha_soft dh0 until q first reaches 0
+    (the particle cracks, its cohesion beta becomes 0), dq = +dh0 after.
+    Returns (e_new, qs_new)."""
+    n, d = e.shape
+    kappa = mat.kappa(d)
+    mu = mat.mu
+    q, cracked = nacc_state_decode(np.asarray(qs, dtype=float))
+    beta = np.where(cracked, 0.0, mat.beta)
+    p0 = kappa * (1e-5 + np.sinh(mat.xi * np.maximum(q, 0.0)))
+    ev = e.sum(axis=1)
+    eh = e - ev[:, None] / d
+    sn = 2.0 * mu * np.sqrt((eh ** 2).sum(axis=1))
+    cs = np.sqrt((6.0 - d) / 2.0)
+    p_tr = -kappa * ev
+    q_tr = cs * sn
+    M2 = mat.M * mat.M
+    yp = M2 * (p_tr + beta * p0) * (p_tr - p0)
+    y = (1.0 + 2.0 * beta) * q_tr ** 2 + yp
+    out = e.copy()
+    dlogjp = np.zeros(n)
+    c1 = p_tr > p0
+    c2 = (~c1) & (p_tr < -beta * p0)
+    c4 = (~c1) & (~c2) & (y > 1e-12 * np.maximum(p0 * p0 * M2, 1e-300))
+    ev1 = -p0 / kappa
+    out[c1] = (ev1[c1] / d)[:, None]
+    dlogjp[c1] = ev[c1] - ev1[c1]
+    ev2 = beta * p0 / kappa
+    out[c2] = (ev2[c2] / d)[:, None]
+    dlogjp[c2] = ev[c2] - ev2[c2]
+    if c4.any():
+        s_new = np.sqrt(np.maximum(-yp[c4], 0.0) / (1.0 + 2.0 * beta[c4])) / cs
+        scale = np.where(sn[c4] > 0.0, s_new / np.where(sn[c4] > 0.0, sn[c4], 1.0), 0.0)
+        out[c4] = eh[c4] * scale[:, None] + (ev[c4] / d)[:, None]
+        # hardening: the surface point towards the ellipse centre
+        pb, qb, b4, p04 = p_tr[c4], q_tr[c4], beta[c4], p0[c4]
+        pc = (1.0 - b4) * p04 / 2.0
+        d0, d1 = pc - pb, -qb
+        nrm = np.sqrt(d0 * d0 + d1 * d1)
+        nrm = np.where(nrm > 0.0, nrm, 1.0)
+        d0, d1 = d0 / nrm, d1 / nrm
+        A = M2 * d0 * d0 + (1.0 + 2.0 * b4) * d1 * d1
+        B = M2 * d0 * (2.0 * pc - p04 + b4 * p04)
+        C = M2 * (pc + b4 * p04) * (pc - p04)
+        disc = np.sqrt(np.maximum(B * B - 4.0 * A * C, 0.0))
+        A = np.where(A > 0.0, A, 1.0)
+        l1 = (-B + disc) / (2.0 * A)
+        l2 = (-B - disc) / (2.0 * A)
+        p1 = pc + l1 * d0
+        p2 = pc + l2 * d0
+        px = np.where((pb - pc) * (p1 - pc) > 0.0, p1, p2)
+        dlogjp[c4] = ev[c4] + px / kappa
+    dh0 = -dlogjp
+    qn = q + np.where(cracked, 1.0, -mat.alpha_soft) * dh0
+    newly = (~cracked) & (qn <= 0.0)
+    cr = cracked | newly
+    qn = np.where(cr, np.maximum(qn, 0.0), qn)
+    qn = np.where(newly, 0.0, qn)
+    return out, np.where(cr, -qn - 1.0, qn)
+
+
+def nacc_yield(e, qs, mat: SnowMaterial):
+    """y(p, q_s) of nacc_return_map for states e (test helper)."""
+    n, d = e.shape
+    kappa = mat.kappa(d)
+    q, cracked = nacc_state_decode(np.asarray(qs, dtype=float))
+    beta = np.where(cracked, 0.0, mat.beta)
+    p0 = kappa * (1e-5 + np.sinh(mat.xi * np.maximum(q, 0.0)))
+    ev = e.sum(axis=1)
+    eh = e - ev[:, None] / d
+    q_s = np.sqrt((6.0 - d) / 2.0) * 2.0 * mat.mu * np.sqrt((eh ** 2).sum(axis=1))
+    p = -kappa * ev
+    return (1.0 + 2.0 * beta) * q_s ** 2 + mat.M ** 2 * (p + beta * p0) * (p - p0), p0
 
 
 class Particles:
@@ -292,7 +422,10 @@ def g2p(p: Particles, grid: MpmGrid, dt, mat, plastic=True, st=None):
     if plastic:
         U, sig, V = svd(p.F)
         sig = np.clip(sig, 0.05, 4.0)
-        eps_new, vc = dp_return_map(np.log(sig), p.vol_corr, mat)
+        if isinstance(mat, SnowMaterial):
+            eps_new, vc = nacc_return_map(np.log(sig), p.vol_corr, mat)
+        else:
+            eps_new, vc = dp_return_map(np.log(sig), p.vol_corr, mat)
         p.vol_corr = vc
         p.F = np.einsum("nik,nk,njk->nij", U, np.exp(eps_new), V)
     return clamped

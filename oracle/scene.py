@@ -37,6 +37,12 @@ def material(raw):
     m = raw["materials"]
     u = raw["units"]
     stress = u["rho"] * (u["dx"] / u["dt"]) ** 2
+    if m.get("model", "sand") == "snow":
+        return mpm.SnowMaterial(E=m["E"] / stress, nu=m["nu"], M=m["nacc_M"],
+                                beta=m["nacc_beta"], xi=m["nacc_xi"],
+                                alpha_soft=m["nacc_alpha"], q_init=m["nacc_q0"],
+                                floor_friction=m["floor_friction"],
+                                friction_deg=m["friction_angle_deg"])
     return mpm.SandMaterial(E=m["E"] / stress, nu=m["nu"],
                             friction_deg=m["friction_angle_deg"],
                             floor_friction=m["floor_friction"])
@@ -86,6 +92,8 @@ def build_scene(raw, heightmap=None):
         parts = mpm.sample_blocks(
             [tuple(float(v) for v in b) for b in raw["particles"]["blocks"]],
             raw["particles"]["per_cell"], dens, rng, d=d)
+        if raw["materials"].get("model", "sand") == "snow":
+            parts.vol_corr[:] = raw["materials"]["nacc_q0"]
     static = None
     if raw["adapt"]["static_boxes"]:
         static = np.zeros(topo.tiles_dims(0), dtype=bool)

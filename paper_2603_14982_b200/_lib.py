@@ -69,6 +69,12 @@ def build(force=False, verbose=False, extra=(), out=None):
 
 # -- C structs (mirror include/mlbm_b200.h) ------------------------------------
 
+class Snow(C.Structure):
+    """mlbm_snow_t: NACC snow parameters (include/mlbm_b200.h)."""
+    _fields_ = [("M", C.c_double), ("beta", C.c_double), ("xi", C.c_double),
+                ("alpha_soft", C.c_double)]
+
+
 class Level(C.Structure):
     _fields_ = [("dim", C.c_int32), ("level", C.c_int32),
                 ("cells", C.c_int32 * 3), ("tiles", C.c_int32 * 3),
@@ -112,6 +118,8 @@ class Hier(C.Structure):
 
 
 ERR_INTS = 19   # mlbm_error_t as int32 words
+# mlbm_coupling_op operations (include/mlbm_b200.h)
+COUPLE_FRACTIONS, COUPLE_DRAG, COUPLE_LIMIT, COUPLE_GRAD_EPS, COUPLE_MIXTURE_FORCE = range(5)
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -141,7 +149,10 @@ _SIGS = {
     "mlbm_migrate_level": [I32, I32, P, P, Fields, Fields, Fields, Fields, I32, P],
     "mlbm_init_new_cells": [C.POINTER(Hier), C.POINTER(Hier), I32, P, P, I32, P,
                             Fields, Fields, P, I32, I32, P, P],
-    "mlbm_adapt_pass": [C.POINTER(Hier), P, P, P, P, P, P, P, P, P, P, P, I64, I32, P, P, P, P],
+    "mlbm_adapt_pass": [C.POINTER(Hier), P, P, P, P, P, P, P, P, P, P, P, I64, I32, P, P, P, P,
+                        P],
+    "mlbm_adapt_set_timestamps": [P],
+    "mlbm_adapt_bits_set_timestamps": [P],
     "mlbm_raster_rows": [I32],
     "mlbm_particle_rows": [I32],
     "mlbm_p2g": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64, I32, I32, P, P],
@@ -149,14 +160,21 @@ _SIGS = {
     "mlbm_particle_sort": [C.POINTER(Level), I32, P, P, P, I64, P, P, P, I32, P, I64, P],
     "mlbm_exchange": [C.POINTER(Level), Fields, Fields, Fields, Fields, P, I64,
                       D, D, D, D, D, D, P, P, P, D, I32, I32, P],
-    "mlbm_g2p": [C.POINTER(Level), I32, P, P, P, P, P, P, I64, D, D, D, P, I64, D, I32,
-                 I32, P, P, P],
+    "mlbm_g2p": [C.POINTER(Level), I32, P, P, P, P, P, P, I64, D, D, D, C.POINTER(Snow), P,
+                 I64, D, I32, I32, P, P, P, P, P, P],
     "mlbm_stress_raster": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64,
                            I32, P, P],
     "mlbm_stress_raster_surface": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64, D, P,
                                    I32, P, P],
     "mlbm_powder": [C.POINTER(Level), Fields, Fields, P, I64, P, D, D, D, D, D,
                     I32, I32, P],
+    "mlbm_coupling_op": [C.POINTER(Level), I32, P, I64, P, P, I64, P, I64, D, D, D, D, D, D,
+                         P, I32, P],
+    "mlbm_memset": [P, I32, I64, P],
+    "mlbm_fill": [P, I64, I32, D, P],
+    "mlbm_particle_stress": [I32, I32, P, I64, D, D, D, I32, P],
+    "mlbm_stencil": [C.POINTER(Level), I32, P, I64, P, P, P, P, I64, I32, P, P],
+    "mlbm_powder_step": [C.POINTER(Level), Fields, Fields, P, D, D, D, P, I32, P],
     "mlbm_diag_level": [C.POINTER(Level), Fields, D, I32, P, P],
     "mlbm_diag_particles": [I32, I32, P, I64, P, I64, I64, P, I32, P, P],
 }
@@ -257,6 +275,25 @@ def check(status, what):
 
 def ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def zero(t):
+    """Zero a contiguous device tensor on the current stream (cudaMemsetAsync:
+    no framework kernel inside captured graphs)."""
+    if t is None or t.numel() == 0:
+        return
+    assert t.is_contiguous()
+    check(lib().mlbm_memset(ptr(t), 0, t.numel() * t.element_size(), stream_handle()), "memset")
+
+
+def fill(t, value):
+    """Fill a contiguous device tensor with ``value`` (library kernel)."""
+    import torch
+    if t is None or t.numel() == 0:
+        return
+    assert t.is_contiguous()
+    kind = {torch.uint8: 0, torch.int32: 1, torch.float32: 2, torch.float64: 3}[t.dtype]
+    check(lib().mlbm_fill(ptr(t), t.numel(), kind, float(value), stream_handle()), "fill")
 
 
 def stream_handle():

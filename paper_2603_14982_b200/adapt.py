@@ -46,6 +46,9 @@ class RefineDriver:
     static_tiles: np.ndarray | None = None
     levels: int = 1
     positions_soa: object = None
+    # the seed tiles of this update were written by mlbm_g2p of the same step
+    # (CoupledSim with a fused adaptor): the fused pass reads no positions
+    g2p_seeds: bool = False
 
     def device_positions(self, d, device):
         if self.positions_soa is not None:
@@ -122,6 +125,9 @@ class GridAdaptor:
         self._static_dev = None
         self._bar = torch.zeros(2, dtype=torch.int32, device=dev)
         self.fused = True          # one cooperative launch per pass (csrc/adapt.cu)
+        # seeds written by G2P (CoupledSim): the next fused pass reads no positions
+        # and takes G2P's count of particles outside level-0 leaves from here
+        self.ext_count = torch.zeros(1, dtype=torch.int32, device=dev)
         self.launches = 0
 
     @property
@@ -181,6 +187,8 @@ class GridAdaptor:
         (status[L:L+3]).  No host synchronisation (CUDA-graph capturable)."""
         if self.fused:
             return self._plan_fused(driver)
+        if driver.g2p_seeds:
+            L.zero(self.ext_count)     # the per-op pass seeds from the positions itself
         self._seeds_dirty = True
         topo = self.topology
         lib = L.lib()
@@ -246,20 +254,23 @@ class GridAdaptor:
     def _plan_fused(self, driver):
         topo = self.topology
         if getattr(self, "_seeds_dirty", False):     # left set by the unfused path
-            self._seeds.zero_()
+            L.zero(self._seeds)
             self._seeds_dirty = False
         Lv = topo.levels
         arr = lambda ts: (L.C.c_void_p * Lv)(*[t.data_ptr() for t in ts])   # noqa: E731
-        x = driver.device_positions(topo.d, topo.device)
+        ext = self.ext_count if driver.g2p_seeds else None
+        x = None if driver.g2p_seeds else driver.device_positions(topo.d, topo.device)
         st = self._static(driver.static_tiles)
         h = topo.hier_struct()
-        self._status.zero_()
+        L.zero(self._status)
         L.check(L.lib().mlbm_adapt_pass(L.C.byref(h), arr(self._des), arr(self._cur),
                                         arr(self._eff), arr(self._par), arr(self._own),
                                         arr(self._new), arr(self._stor), arr(self._streak),
                                         L.ptr(self._seeds),
                                         L.ptr(st), L.ptr(x), x.stride(0) if x is not None else 0,
-                                        x.shape[1] if x is not None else 0, L.ptr(self._status),
+                                        x.shape[1] if x is not None else 0,
+                                        L.ptr(ext),
+                                        L.ptr(self._status),
                                         L.ptr(self._err), L.ptr(self._bar), L.stream_handle()),
                 "adapt_pass")
         self.launches += 1

@@ -31,7 +31,7 @@ import torch
 
 from . import _lib as L
 from .adapt import GridAdaptor, RefineDriver
-from .granular import MpmGrid, Particles, SandMaterial, _d3, _faces
+from .granular import MpmGrid, Particles, SandMaterial, SnowMaterial, _d3, _faces, snow_arg
 from .solver import FIELD_FORCE, FIELD_TAU, MultiLevelSolver
 from .sparse_grid import dtype_code
 
@@ -106,8 +106,9 @@ def particle_diameter(V0, d):
 class CouplingFields:
     """Device views of the last exchange (coupling.py:80-93)."""
 
-    def __init__(self, grid: MpmGrid, tree_level0):
+    def __init__(self, grid: MpmGrid, tree_level0=None):
         d = grid.d
+        self.grid = grid
         self.d = d
         n = grid._live()
         r = grid.ras[:, :n]
@@ -120,8 +121,151 @@ class CouplingFields:
         self.fs = r[R["fs"]:R["fs"] + d].t()
         self.grad_term = r[R["grad"]:R["grad"] + d].t()
         self.rel = r[R["rel"]:R["rel"] + d].t()
-        base = tree_level0.index["f" + "x"]
-        self.force = tree_level0.data[base:base + d, :n].t()
+        self.force = None
+        if tree_level0 is not None:
+            base = tree_level0.index["f" + "x"]
+            self.force = tree_level0.data[base:base + d, :n].t()
+
+
+# -- the reference's standalone coupling functions (coupling.py:96-322) -------------
+# Each is one mlbm_coupling_op pass over the level-0 raster of a MpmGrid (the
+# fused CoupledSim step runs the same device functions inside mlbm_exchange).
+# Arrays are level-0 cell vectors in this topology's cell order (device tensors
+# or host arrays); results are device tensors.
+
+def _seam_grid(topology, dtype=None):
+    """A level-0 raster for the standalone seams: faces follow the topology's
+    periodicity (non-periodic faces as outlets: no solids, no wall bands)."""
+    from .solver import BoundarySpec
+    faces = {}
+    for a, ax in enumerate("xyz"[:topology.d]):
+        kind = "periodic" if topology.periodic[a] else "outlet"
+        faces[ax + "_min"] = faces[ax + "_max"] = kind
+    return MpmGrid(topology, BoundarySpec(faces=faces, dim=topology.d), dtype=dtype)
+
+
+def _cell_vec(v, grid, n):
+    t = torch.as_tensor(v if torch.is_tensor(v) else np.asarray(v, dtype=np.float64),
+                        dtype=grid.dtype, device=grid.ras.device).reshape(-1)
+    if t.numel() != n:
+        raise ValueError(f"expected {n} level-0 cell values, got {t.numel()}")
+    return t.contiguous()
+
+
+def _cell_rows(vs, grid, n):
+    return torch.stack([_cell_vec(v, grid, n) for v in vs]).contiguous()
+
+
+def _couple(grid, op, a0=None, u=None, out=None, eps_min=0.3, nu=1.0, d_p=1.0, re_min=0.01,
+            dt=1.0, rho0=1.0, g=(0.0, 0.0, 0.0)):
+    lv0 = grid.level0()
+    L.check(L.lib().mlbm_coupling_op(
+        L.C.byref(lv0), op, L.ptr(grid.ras), grid.ras.stride(0), L.ptr(a0),
+        L.ptr(u), u.stride(0) if u is not None else 0, L.ptr(out),
+        out.stride(0) if out is not None else 0, float(eps_min), float(nu), float(d_p),
+        float(re_min), float(dt), float(rho0), _d3(g, grid.d), dtype_code(grid.dtype),
+        L.stream_handle()), "coupling_op")
+
+
+def rasterize_fractions(particles: Particles, topology, phi, eps_min: float,
+                        drag: "DragParams" = None, st=None, grid: MpmGrid | None = None):
+    """coupling.py:96-131: B-spline rasterisation of the sediment fraction,
+    mass, cell velocity and cross-section area (the P2G scatter), then
+    eps = clip(1 - eta_eff - phi, eps_min, 1).  Returns CouplingFields views of
+    the grid raster (``grid`` defaults to a fresh MpmGrid of the topology)."""
+    grid = grid or _seam_grid(topology, particles.dtype)
+    grid.sync_topology()
+    grid.clear()
+    n = topology.cell_count(0)
+    if len(particles):
+        lv0 = grid.level0()
+        # zero elastic moduli: the stress rows stay zero, the rest is the P2G scatter
+        L.check(L.lib().mlbm_p2g(L.C.byref(lv0), len(particles), L.ptr(particles.xd),
+                                 L.ptr(particles.pd), particles.pd.stride(0), 0.0, 0.0, 0.0,
+                                 L.ptr(grid.ras), grid.ras.stride(0), dtype_code(grid.dtype), 0,
+                                 L.ptr(grid._err), L.stream_handle()), "p2g")
+        grid.raise_pending()
+    _couple(grid, L.COUPLE_FRACTIONS, a0=_cell_vec(phi, grid, n), eps_min=eps_min)
+    return CouplingFields(grid)
+
+
+def difelice_drag(fields: CouplingFields, rho, ux, uy, nu: float, params: "DragParams",
+                  d_p: float, uz=None):
+    """coupling.py:134-156: Di Felice drag on the sediment per cell (fields.fs,
+    fields.rel); the fluid receives -fs.  3D passes ``uz``."""
+    grid = fields.grid
+    n = grid._live()
+    u = _cell_rows([ux, uy] + ([uz] if grid.d == 3 else []), grid, n)
+    _couple(grid, L.COUPLE_DRAG, a0=_cell_vec(rho, grid, n), u=u, nu=nu, d_p=d_p,
+            re_min=params.re_min)
+    return fields.fs
+
+
+def limit_drag(fields: CouplingFields, rho, ux, uy, dt: float, uz=None):
+    """CoupledSim._limit_drag (coupling.py:379-401) on fields.fs, in place."""
+    grid = fields.grid
+    n = grid._live()
+    u = _cell_rows([ux, uy] + ([uz] if grid.d == 3 else []), grid, n)
+    _couple(grid, L.COUPLE_LIMIT, a0=_cell_vec(rho, grid, n), u=u, dt=dt)
+
+
+def grad_eps(eps, topology, grid: MpmGrid | None = None):
+    """coupling.py:159-182: central differences on level 0 (a missing
+    neighbour counts as the cell itself); returns (n, d)."""
+    grid = grid or _seam_grid(topology)
+    n = topology.cell_count(0)
+    e = _cell_vec(eps, grid, n)
+    out = torch.empty((grid.d, n), dtype=grid.dtype, device=grid.ras.device)
+    _couple(grid, L.COUPLE_GRAD_EPS, a0=e, out=out)
+    return out.t()
+
+
+def mixture_force(fields: CouplingFields, rho, topology, gravity, rho0: float = 1.0):
+    """coupling.py:185-197: ((rho - rho0)/eps) grad eps + rho g - fs; sets
+    fields.grad_term and fields.force, returns the force (n, d)."""
+    grid = fields.grid
+    n = grid._live()
+    out = torch.empty((grid.d, n), dtype=grid.dtype, device=grid.ras.device)
+    _couple(grid, L.COUPLE_MIXTURE_FORCE, a0=_cell_vec(rho, grid, n), out=out, rho0=rho0,
+            g=tuple(gravity))
+    fields.force = out.t()
+    return fields.force
+
+
+def powder_step(phi, ux, uy, topology, params: "PowderParams", dt: float, source=None, uz=None):
+    """coupling.py:230-272: RK3 semi-Lagrangian advection with multilinear
+    sampling, forward-Euler diffusion (params.sign), then + dt * source.
+    Returns the new phi (n,) as a device tensor."""
+    from .sparse_grid import field_names, fresh_block
+    params.check_stability(dt)
+    d = topology.d
+    n = topology.cell_count(0)
+    cap = topology.capacity_cells(0)
+    dt_ = torch.float64 if (torch.is_tensor(phi) and phi.dtype == torch.float64) or \
+        not torch.is_tensor(phi) else phi.dtype
+    names = field_names(d)
+    src = fresh_block(d, cap, dt_, topology.device)
+    dst = fresh_block(d, cap, dt_, topology.device)
+
+    def put(block, row, v):
+        t = torch.as_tensor(v if torch.is_tensor(v) else np.asarray(v, dtype=np.float64),
+                            dtype=dt_, device=topology.device).reshape(-1)
+        block[row, :n].copy_(t)
+    put(src, names.index("phi"), phi)
+    for a, v in enumerate([ux, uy] + ([uz] if d == 3 else [])):
+        put(dst, 1 + a, v)
+    srcv = None
+    if source is not None:
+        srcv = torch.zeros(cap, dtype=dt_, device=topology.device)
+        srcv[:n].copy_(torch.as_tensor(source if torch.is_tensor(source) else
+                                       np.asarray(source, dtype=np.float64), dtype=dt_).reshape(-1))
+    tmp = torch.empty(cap, dtype=dt_, device=topology.device)
+    lv0 = topology.level_struct(0)
+    L.check(L.lib().mlbm_powder_step(L.C.byref(lv0), L.fields(src), L.fields(dst), L.ptr(tmp),
+                                     float(params.diffusion), float(params.sign), float(dt),
+                                     L.ptr(srcv), dtype_code(dt_), L.stream_handle()),
+            "powder_step")
+    return dst[names.index("phi"), :n].clone()
 
 
 class CoupledSim:
@@ -256,11 +400,17 @@ class CoupledSim:
                                   float(self.cadence), float(sp.rho0), _d3(sp.gravity, self.d),
                                   _d3(self.sediment_gravity, self.d), _faces(solver.boundaries),
                                   float(mat.floor_friction), 1, dcode, s), "exchange")
+        seeds = self._g2p_seeds()
+        ad = self.adaptor
         L.check(lib.mlbm_g2p(L.C.byref(lv0), n, L.ptr(src_x), L.ptr(p.xd), L.ptr(src_p),
                              L.ptr(p.pd), L.ptr(src_id), L.ptr(p.pid) if src_id is not None else
-                             L.ptr(None), ps, mat.lam, mat.mu, mat.alpha, L.ptr(grid.ras),
-                             grid.ras.stride(0), float(self.cadence), 1, dcode,
-                             L.ptr(self._counters), L.ptr(grid._err), s), "g2p")
+                             L.ptr(None), ps, mat.lam, mat.mu, mat.alpha, snow_arg(mat),
+                             L.ptr(grid.ras), grid.ras.stride(0), float(self.cadence), 1, dcode,
+                             L.ptr(self._counters),
+                             L.ptr(ad._seeds if seeds else None),
+                             L.ptr(self.topology.lv[0].kind if seeds else None),
+                             L.ptr(ad.ext_count if seeds else None),
+                             L.ptr(grid._err), s), "g2p")
         solver.launches += 3
         self.last_fields = CouplingFields(grid, self.pair.trees[0].levels[0])
         return FIELD_FORCE, FIELD_TAU
@@ -289,6 +439,9 @@ class CoupledSim:
         is_mpm = self.coupling_active and (self.step_count % self.cadence == 0)
         adapt_now = self.adaptor is not None and self.coupling_active and \
             self.step_count % self.cadence == 0
+        if self.particles is not None and (is_mpm or self.powder is not None):
+            # P2G / the entrainment raster read the particles' stress rows
+            self.particles.ensure_stress(self.material)
         if self.use_graphs and torch.cuda.is_available():
             self._step_graph(ci, is_mpm, adapt_now)
         else:
@@ -321,9 +474,15 @@ class CoupledSim:
         self._record_diagnostics()
         self._push_diag_row(self._diag_buf.cpu().numpy())
 
+    def _g2p_seeds(self):
+        """G2P writes the next adapt pass's seed tiles (fused cooperative pass
+        only; the bit-packed and per-op paths seed from the positions)."""
+        return (self.adaptor is not None and self.adaptor.fused and len(self.particles) > 0
+                and not os.environ.get("MLBM_ADAPT_PATH", "").startswith("b"))
+
     def _driver(self):
         return RefineDriver(positions_soa=self.particles.xd, static_tiles=self.static_tiles,
-                            levels=self.topology.levels)
+                            levels=self.topology.levels, g2p_seeds=self._g2p_seeds())
 
     # -- graph path: all kernels of the step replayed as one CUDA graph, one
     #    device->host status copy, host work only when the topology changes --
@@ -620,7 +779,7 @@ class CoupledSim:
             and len(self.particles) > 0
         if src:
             R = grid.R
-            grid.ras[R["sig"]:R["n"]].zero_()
+            L.zero(grid.ras[R["sig"]:R["etae"]])
             p = self.particles
             lv0 = grid.level0()
             # the raster is only read at entrainment surface cells: fp32 runs
@@ -648,8 +807,8 @@ class CoupledSim:
         s = L.stream_handle()
         dcode = dtype_code(self.dtype)
         out = self._diag_buf
-        out.zero_()
-        out[d + 1:d + 2].fill_(1.0)
+        L.zero(out)
+        L.fill(out[d + 1:d + 2], 1.0)
         for l in range(self.topology.levels):
             if not self.topology.n_tiles(l):
                 continue

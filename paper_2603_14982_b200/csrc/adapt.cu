@@ -52,6 +52,7 @@ struct AdaptArgs {
     mlbm_error_t* err;
     unsigned int* bar;      // 2 words, zero-initialised once
     unsigned long long* ts; // optional stage timestamps (block 0), may be null
+    int32_t* ext_count;     // particles outside level-0 leaves counted by G2P with the seeds (or null)
 };
 
 __device__ __forceinline__ int64_t gi3(const int* d, int x, int y, int z) {
@@ -441,6 +442,11 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
             if (A.kind[0][g] != 1) atomicAdd(&A.status[L + 2], 1);
         }
     }
+    if (A.ext_count && tid == 0) {
+        // the seeds came from G2P: its leaf-invariant count joins status[L+2]
+        atomicAdd(&A.status[L + 2], *A.ext_count);
+        *A.ext_count = 0;
+    }
     STAMP_BARRIER(2);
 
     // ---- C: des[0], cur[1]
@@ -656,22 +662,28 @@ int mlbm_adapt_bits_launch(const mlbm_hier_t* h, uint8_t* const* nkind, int16_t*
                            int32_t n, int32_t* status, mlbm_error_t* err, int64_t seeds_bytes,
                            void* stream);
 
+// optional stage timestamps (tools/adapt_bench.py): a caller-owned buffer of
+// 64 uint64 set once; the library never allocates
 static unsigned long long* g_ts_last = nullptr;
 extern "C" unsigned long long* mlbm_adapt_timestamps_ptr() { return g_ts_last; }
+extern "C" int mlbm_adapt_set_timestamps(unsigned long long* buf) {
+    g_ts_last = buf;
+    return 0;
+}
 
 extern "C" int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_t* const* cur,
                                uint8_t* const* eff, uint8_t* const* par, uint8_t* const* own,
                                uint8_t* const* nkind, uint8_t* const* stor, int16_t* const* streak,
                                uint8_t* seeds,
                                const uint8_t* static_tiles, const double* x, int64_t xs, int32_t n,
+                               int32_t* ext_count,
                                int32_t* status, mlbm_error_t* err, unsigned int* bar, void* stream) {
-    static unsigned long long* ts_env = nullptr;
     // MLBM_ADAPT_PATH=bits selects the bit-packed single-CTA pass
     // (adapt_bits.cu) when the hierarchy's bitmaps fit in shared memory.  It
     // is bit-exact but slower on B200 (one SM against 148: 74 us vs 52 us on
     // C2), so the cooperative byte pass is the default.
     const char* path = getenv("MLBM_ADAPT_PATH");
-    if (path && path[0] == 'b') {
+    if (path && path[0] == 'b' && !ext_count) {
         int64_t n0 = 1;
         for (int a = 0; a < h->dim; ++a) n0 *= h->finest[a] / 4;
         const int r = mlbm_adapt_bits_launch(h, nkind, streak, seeds, static_tiles, x, xs, n, status, err,
@@ -699,15 +711,11 @@ extern "C" int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_
     A.x = x;
     A.xs = xs;
     A.n = n;
+    A.ext_count = ext_count;
     A.status = status;
     A.err = err;
     A.bar = bar;
-    A.ts = nullptr;
-    if (getenv("MLBM_ADAPT_TIMESTAMPS")) {
-        if (!ts_env) cudaMalloc(&ts_env, 64 * sizeof(unsigned long long));
-        A.ts = ts_env;
-        g_ts_last = ts_env;
-    }
+    A.ts = g_ts_last;
     static int grid_sms = 0, grid_per = 1;
     int grid = 0;
     if (grid_sms == 0) {

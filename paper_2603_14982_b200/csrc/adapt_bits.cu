@@ -485,6 +485,10 @@ using namespace mlbm;
 
 static unsigned long long* g_bits_ts = nullptr;
 extern "C" unsigned long long* mlbm_adapt_bits_ts_ptr() { return g_bits_ts; }
+extern "C" int mlbm_adapt_bits_set_timestamps(unsigned long long* buf) {
+    g_bits_ts = buf;
+    return 0;
+}
 
 // host side: geometry, eligibility, launch (called from mlbm_adapt_pass)
 int mlbm_adapt_bits_launch(const mlbm_hier_t* h, uint8_t* const* nkind, int16_t* const* streak,
@@ -526,14 +530,8 @@ int mlbm_adapt_bits_launch(const mlbm_hier_t* h, uint8_t* const* nkind, int16_t*
     A.seeds = (uint32_t*)seeds;
     A.static_tiles = static_tiles;
     A.status = status;
-    A.ts = nullptr;
-    if (getenv("MLBM_ADAPT_TIMESTAMPS")) {
-        static unsigned long long* tsb = nullptr;
-        if (!tsb) cudaMalloc(&tsb, 64 * sizeof(unsigned long long));
-        cudaMemsetAsync(tsb, 0, 64 * sizeof(unsigned long long), as_stream(stream));
-        A.ts = tsb;
-        g_bits_ts = tsb;
-    }
+    A.ts = g_bits_ts;       // caller-owned (mlbm_adapt_bits_set_timestamps), may be null
+    if (A.ts) cudaMemsetAsync(A.ts, 0, 64 * sizeof(unsigned long long), as_stream(stream));
     cudaStream_t s = as_stream(stream);
     static size_t attr = 0;
     if (smem > attr) {

@@ -33,9 +33,13 @@ template <int D> struct Rows {
                          N = 5 + 7 * D + Geo<D>::NS, NACC = 3 + 3 * D;
 };
 // particle row layout (after the float64 positions): v[D] C[D*D] F[D*D] m V0 vc
+// TAU: the Kirchhoff stress tau(F) (granular.py:260-279, symmetric, NS rows)
+// of the particle's current F, written by G2P from its own decomposition of the
+// updated F (and by mlbm_particle_stress when F is set from outside), so P2G and
+// the entrainment raster read it instead of re-decomposing F
 template <int D> struct PRows {
     static constexpr int V = 0, C = D, F = D + D * D, M = D + 2 * D * D, V0 = M + 1, VC = M + 2,
-                         N = M + 3;
+                         TAU = M + 3, N = M + 3 + D * (D + 1) / 2;
 };
 
 struct TopoL0 {
@@ -267,10 +271,78 @@ __device__ __forceinline__ void left_stretch3(const R (&F)[9], R (&U)[9], R (&s)
 struct MatParams {
     double lam, mu, alpha, floor_friction;
     double kdg2, kdg3;      // (d lam + 2 mu) / (2 mu) for d = 2, 3 (host-computed)
+    int snow;               // 0 Drucker-Prager sand, 1 NACC snow
+    double M, beta, xi, alpha_soft;
 };
-static inline MatParams mat_params(double lam, double mu, double alpha) {
-    return MatParams{lam, mu, alpha, 0.0, (2.0 * lam + 2.0 * mu) / (2.0 * mu),
-                     (3.0 * lam + 2.0 * mu) / (2.0 * mu)};
+static inline MatParams mat_params(double lam, double mu, double alpha, const mlbm_snow_t* sn = nullptr) {
+    MatParams m{lam, mu, alpha, 0.0, mu != 0.0 ? (2.0 * lam + 2.0 * mu) / (2.0 * mu) : 0.0,
+                mu != 0.0 ? (3.0 * lam + 2.0 * mu) / (2.0 * mu) : 0.0, 0, 0.0, 0.0, 0.0, 0.0};
+    if (sn) { m.snow = 1; m.M = sn->M; m.beta = sn->beta; m.xi = sn->xi; m.alpha_soft = sn->alpha_soft; }
+    return m;
+}
+
+// NACC return map + the paper's softening law in principal log-strain space
+// (Hencky elasticity, p = -kappa tr e, s = 2 mu dev e): the device statement of
+// oracle/mpm.py:nacc_return_map (parity unpinned).  qs: the
+// hardening state (q >= 0, or -(q + 1) once the particle has cracked)
+template <int D, typename R>
+__device__ __forceinline__ void nacc_return(R (&e)[D], R& qs, const MatParams& mp) {
+    const R kappa = R(mp.lam) + R(2.0 * mp.mu / D);
+    const bool cracked = qs < R(0);
+    const R q = cracked ? -qs - R(1) : qs;
+    const R beta = cracked ? R(0) : R(mp.beta);
+    const R p0 = kappa * (R(1e-5) + sinh(R(mp.xi) * (q > R(0) ? q : R(0))));
+    R ev = R(0);
+#pragma unroll
+    for (int a = 0; a < D; ++a) ev += e[a];
+    R eh[D], n2 = R(0);
+#pragma unroll
+    for (int a = 0; a < D; ++a) { eh[a] = e[a] - ev / R(D); n2 += eh[a] * eh[a]; }
+    const R sn = R(2.0 * mp.mu) * sqrt(n2);
+    const R cs = sqrt(R(6 - D) / R(2));
+    const R p_tr = -kappa * ev, q_tr = cs * sn;
+    const R M2 = R(mp.M * mp.M);
+    const R yp = M2 * (p_tr + beta * p0) * (p_tr - p0);
+    const R y = (R(1) + R(2) * beta) * q_tr * q_tr + yp;
+    R dlogjp = R(0);
+    const R ytol = R(1e-12) * fmax(p0 * p0 * M2, R(1e-30));
+    if (p_tr > p0) {                          // compressive tip
+        const R ev1 = -p0 / kappa;
+#pragma unroll
+        for (int a = 0; a < D; ++a) e[a] = ev1 / R(D);
+        dlogjp = ev - ev1;
+    } else if (p_tr < -beta * p0) {           // tensile tip
+        const R ev2 = beta * p0 / kappa;
+#pragma unroll
+        for (int a = 0; a < D; ++a) e[a] = ev2 / R(D);
+        dlogjp = ev - ev2;
+    } else if (y > ytol) {                    // deviatoric return at fixed p
+        const R snew = sqrt(fmax(-yp, R(0)) / (R(1) + R(2) * beta)) / cs;
+        const R scale = sn > R(0) ? snew / sn : R(0);
+#pragma unroll
+        for (int a = 0; a < D; ++a) e[a] = eh[a] * scale + ev / R(D);
+        // hardening: the surface point on the line from the centre (p_c, 0)
+        const R pc = (R(1) - beta) * p0 / R(2);
+        R d0 = pc - p_tr, d1 = -q_tr;
+        R nr = sqrt(d0 * d0 + d1 * d1);
+        nr = nr > R(0) ? nr : R(1);
+        d0 /= nr;
+        d1 /= nr;
+        R A = M2 * d0 * d0 + (R(1) + R(2) * beta) * d1 * d1;
+        const R B = M2 * d0 * (R(2) * pc - p0 + beta * p0);
+        const R C = M2 * (pc + beta * p0) * (pc - p0);
+        const R disc = sqrt(fmax(B * B - R(4) * A * C, R(0)));
+        A = A > R(0) ? A : R(1);
+        const R p1 = pc + (-B + disc) / (R(2) * A) * d0;
+        const R p2 = pc + (-B - disc) / (R(2) * A) * d0;
+        const R px = (p_tr - pc) * (p1 - pc) > R(0) ? p1 : p2;
+        dlogjp = ev + px / kappa;
+    }
+    R qn = q + (cracked ? R(1) : -R(mp.alpha_soft)) * (-dlogjp);
+    const bool newly = !cracked && qn <= R(0);
+    if (cracked || newly) qn = qn > R(0) ? qn : R(0);
+    if (newly) qn = R(0);
+    qs = (cracked || newly) ? -qn - R(1) : qn;
 }
 
 // tau = U diag(2 mu eps + lam tr) U^T  (granular.py:260-279)
@@ -298,6 +370,37 @@ __device__ void kirchhoff(const R (&F)[D * D], const MatParams& mp, R (&tau)[D *
             for (int k = 0; k < D; ++k) acc += U[i * D + k] * tp[k] * U[j * D + k];
             tau[i * D + j] = acc;
         }
+}
+
+// the stored Kirchhoff stress of particle p as a full D x D matrix
+template <int D, typename R>
+__device__ __forceinline__ void load_tau(const R* pp, int64_t ps, int p, R (&tau)[D * D]) {
+#pragma unroll
+    for (int k = 0; k < Geo<D>::NS; ++k) {
+        const R t = pp[(PRows<D>::TAU + k) * ps + p];
+        tau[s_a<D>(k) * D + s_b<D>(k)] = t;
+        tau[s_b<D>(k) * D + s_a<D>(k)] = t;
+    }
+}
+
+// tau = U diag(2 mu e + lam tr e) U^T from left vectors U and log stretches e
+template <int D, typename R>
+__device__ __forceinline__ void store_tau(R* pw, int64_t ps, int p, const R (&U)[D * D], const R (&e)[D],
+                                          const MatParams& mp) {
+    R tr = R(0);
+#pragma unroll
+    for (int a = 0; a < D; ++a) tr += e[a];
+    R tp[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) tp[a] = R(2.0 * mp.mu) * e[a] + R(mp.lam) * tr;
+#pragma unroll
+    for (int k = 0; k < Geo<D>::NS; ++k) {
+        const int i = s_a<D>(k), j = s_b<D>(k);
+        R acc = R(0);
+#pragma unroll
+        for (int q = 0; q < D; ++q) acc += U[i * D + q] * tp[q] * U[j * D + q];
+        pw[(PRows<D>::TAU + k) * ps + p] = acc;
+    }
 }
 
 // B-spline stencil of one particle (granular.py:137-178)
@@ -340,6 +443,12 @@ struct PartArgs {
     void* pw;            // g2p output rows (may alias p)
     const int32_t* pid;  // g2p: particle ids in / out (may be null)
     int32_t* pidw;
+    // g2p: the level-0 seed tiles of the next adapt pass (adapt.py:54-65) from
+    // the new positions, and the count of particles outside level-0 leaves of
+    // the current topology (adapt.py:374-389); null: not written
+    uint8_t* seeds;
+    const uint8_t* kind0;
+    int32_t* nonleaf;
 };
 
 template <typename R> __device__ __forceinline__ void aadd(R* a, R v) { atomicAdd(a, v); }
@@ -359,14 +468,14 @@ __global__ void __launch_bounds__(128) k_p2g(PartArgs P, TopoL0 t0, MatParams mp
     for (int a = 0; a < D; ++a) x[a] = P.x[a * P.ps + p];
     Stencil<D, R> st;
     make_stencil<D, R>(x, st);
-    R v[D], C[D * D], F[D * D];
+    R v[D], C[D * D];
 #pragma unroll
     for (int a = 0; a < D; ++a) v[a] = pp[(PR::V + a) * P.ps + p];
 #pragma unroll
-    for (int k = 0; k < D * D; ++k) { C[k] = pp[(PR::C + k) * P.ps + p]; F[k] = pp[(PR::F + k) * P.ps + p]; }
+    for (int k = 0; k < D * D; ++k) C[k] = pp[(PR::C + k) * P.ps + p];
     const R m = pp[PR::M * P.ps + p], V0 = pp[PR::V0 * P.ps + p];
     R tau[D * D];
-    kirchhoff<D, R>(F, mp, tau);
+    load_tau<D, R>(pp, P.ps, p, tau);
     const R ap = D == 2 ? R(2) * sqrt(V0 / R(3.14159265358979323846))
                         : R(3.14159265358979323846) * pow(R(3) * V0 / (R(4) * R(3.14159265358979323846)), R(2.0 / 3.0));
     bool bad = false;
@@ -430,6 +539,60 @@ __device__ __forceinline__ R eps_of(const R* ras, int64_t rs, const FieldsT<R>& 
     return e;
 }
 
+// Di Felice drag on the sediment of one cell (coupling.py:134-156): rel =
+// u - v_cell, Re = max(eps |rel| d_p / nu, re_min), C_d, chi, f_s
+template <int D, typename R>
+__device__ __forceinline__ void difelice_cell(R eps, R rho, const R (&rel)[D], R speed, R area, R d_p,
+                                              R nu, R re_min, R (&fs)[D]) {
+    for (int a = 0; a < D; ++a) fs[a] = R(0);
+    if (!(area > R(0) && speed > R(0))) return;
+    R re = eps * speed * d_p / nu;
+    re = re > re_min ? re : re_min;
+    const R cd = (R(0.63) + R(4.8) / sqrt(re)) * (R(0.63) + R(4.8) / sqrt(re));
+    const R lg = R(1.5) - log10(re);
+    const R chi = R(3.7) - R(0.65) * exp(R(-0.5) * lg * lg);
+    const R coef = R(0.5) * cd * pow(eps, -chi) * rho * area * speed;
+    for (int a = 0; a < D; ++a) fs[a] = coef * rel[a];
+}
+
+// smooth drag limiter (CoupledSim._limit_drag, coupling.py:379-401)
+template <int D, typename R>
+__device__ __forceinline__ void limit_drag_cell(R (&fs)[D], R rho, R mass, R speed, R dt) {
+    R mag2 = R(0);
+    for (int a = 0; a < D; ++a) mag2 += fs[a] * fs[a];
+    const R mag = sqrt(mag2);
+    if (!(mag > R(0))) return;
+    const R inv_m = R(1) / rho + R(1) / (mass > R(1e-12) ? mass : R(1e-12));
+    const R beta = mag * dt * inv_m / (speed > R(1e-14) ? speed : R(1e-14));
+    R over = beta - R(0.5);
+    over = over > R(0) ? over : R(0);
+    const R real = (beta < R(0.5) ? beta : R(0.5)) + over / (R(1) + over);
+    const R scale = real / (beta > R(1e-14) ? beta : R(1e-14));
+    for (int a = 0; a < D; ++a) fs[a] *= scale;
+}
+
+// central differences of a level-0 cell field (coupling.py:159-182): the
+// neighbour wraps (periodic) or clamps to the domain; a neighbour that is
+// not stored counts as the cell itself.  val(ni) returns the field at cell ni.
+template <int D, typename R, typename F>
+__device__ __forceinline__ void grad_cell(const mlbm_level_t& lv, const int (&g)[3], int64_t c, F val,
+                                          R (&grad)[D]) {
+    constexpr int T = Geo<D>::T;
+    for (int a = 0; a < D; ++a) {
+        R pm[2];
+        for (int sgn = 0; sgn < 2; ++sgn) {
+            int nb[3] = {g[0], g[1], g[2]};
+            nb[a] += sgn == 0 ? 1 : -1;
+            if (lv.periodic[a]) nb[a] = (nb[a] + lv.cells[a]) % lv.cells[a];
+            else nb[a] = nb[a] < 0 ? 0 : (nb[a] >= lv.cells[a] ? lv.cells[a] - 1 : nb[a]);
+            const int s = lv.tile_map[g3(lv.tiles, nb[0] >> 2, nb[1] >> 2, D == 3 ? nb[2] >> 2 : 0)];
+            const int64_t ni = s >= 0 ? (int64_t)s * T + local_of<D>(nb[0] & 3, nb[1] & 3, nb[2] & 3) : c;
+            pm[sgn] = val(ni);
+        }
+        grad[a] = R(0.5) * (pm[0] - pm[1]);
+    }
+}
+
 #ifndef EXCH_MINB
 #define EXCH_MINB 16
 #endif
@@ -465,43 +628,12 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? EXCH_MINB : 1) k_exchang
         }
         const R speed = sqrt(sp2);
         const R area = ras[RW::AREA * rs + c];
-        if (area > R(0) && speed > R(0)) {
-            R re = eps * speed * R(A.d_p) / R(A.nu);
-            re = re > R(A.re_min) ? re : R(A.re_min);
-            const R cd = (R(0.63) + R(4.8) / sqrt(re)) * (R(0.63) + R(4.8) / sqrt(re));
-            const R lg = R(1.5) - log10(re);
-            const R chi = R(3.7) - R(0.65) * exp(R(-0.5) * lg * lg);
-            const R coef = R(0.5) * cd * pow(eps, -chi) * rho * area * speed;
-            for (int a = 0; a < D; ++a) fs[a] = coef * rel[a];
-            // limiter (coupling.py:379-401)
-            R mag2 = R(0);
-            for (int a = 0; a < D; ++a) mag2 += fs[a] * fs[a];
-            const R mag = sqrt(mag2);
-            if (mag > R(0)) {
-                const R inv_m = R(1) / rho + R(1) / (mass > R(1e-12) ? mass : R(1e-12));
-                const R beta = mag * R(A.dt) * inv_m / (speed > R(1e-14) ? speed : R(1e-14));
-                R over = beta - R(0.5);
-                over = over > R(0) ? over : R(0);
-                const R real = (beta < R(0.5) ? beta : R(0.5)) + over / (R(1) + over);
-                const R scale = real / (beta > R(1e-14) ? beta : R(1e-14));
-                for (int a = 0; a < D; ++a) fs[a] *= scale;
-            }
-        }
-        // grad eps (coupling.py:159-182): neighbours clip / wrap, missing -> own
+        difelice_cell<D, R>(eps, rho, rel, speed, area, R(A.d_p), R(A.nu), R(A.re_min), fs);
+        if (area > R(0) && speed > R(0)) limit_drag_cell<D, R>(fs, rho, mass, speed, R(A.dt));
+        // grad eps: the neighbours' eps from the raw eta (never overwritten here)
         R grad[D];
-        for (int a = 0; a < D; ++a) {
-            R pm[2];
-            for (int sgn = 0; sgn < 2; ++sgn) {
-                int nb[3] = {g[0], g[1], g[2]};
-                nb[a] += sgn == 0 ? 1 : -1;
-                if (A.lv.periodic[a]) nb[a] = (nb[a] + A.lv.cells[a]) % A.lv.cells[a];
-                else nb[a] = nb[a] < 0 ? 0 : (nb[a] >= A.lv.cells[a] ? A.lv.cells[a] - 1 : nb[a]);
-                const int s = A.lv.tile_map[g3(A.lv.tiles, nb[0] >> 2, nb[1] >> 2, D == 3 ? nb[2] >> 2 : 0)];
-                const int64_t ni = s >= 0 ? (int64_t)s * T + local_of<D>(nb[0] & 3, nb[1] & 3, nb[2] & 3) : c;
-                pm[sgn] = eps_of<D, R>(ras, rs, rt, ni, eps_min);
-            }
-            grad[a] = R(0.5) * (pm[0] - pm[1]);
-        }
+        grad_cell<D, R>(A.lv, g, c, [&](int64_t ni) { return eps_of<D, R>(ras, rs, rt, ni, eps_min); },
+                        grad);
         const R coefg = (rho - R(A.rho0)) / eps;
         const FieldsT<R> t0 = fields_of<R>(A.tree0), t1 = fields_of<R>(A.tree1);
         for (int a = 0; a < D; ++a) {
@@ -549,6 +681,150 @@ __global__ void __launch_bounds__(128, sizeof(R) == 4 ? EXCH_MINB : 1) k_exchang
     if (A.lv.cell_flags[c] & MLBM_CF_SOLID)
         for (int a = 0; a < D; ++a) vel[a] = R(0);
     for (int a = 0; a < D; ++a) ras[(RW::VEL + a) * rs + c] = vel[a];
+}
+
+// ---------------------------------------------------------------------------
+// The reference's standalone coupling functions (coupling.py:96-197,379-401)
+// as per-cell passes over the level-0 raster, sharing the device functions of
+// the fused k_exchange (difelice_cell, limit_drag_cell, grad_cell):
+//   FRACTIONS      eta_eff, eps, v_cell from the accumulated P2G rows and phi (a0)
+//   DRAG           f_s and rel = u - v_cell from eps, area, rho (a0), u rows
+//   LIMIT          the smooth limiter on the FS rows (rho a0, u rows, dt)
+//   GRAD_EPS       out rows = central differences of a0 (or of the EPS row)
+//   MIXTURE_FORCE  GRAD rows = (rho - rho0)/eps grad eps, out = GRAD + rho g - f_s
+struct CoupleArgs {
+    mlbm_level_t lv;
+    void* ras;
+    int64_t rs;
+    const void* a0;
+    const void* u;
+    int64_t us;
+    void* out;
+    int64_t os;
+    double eps_min, nu, d_p, re_min, dt, rho0, g[3];
+    int32_t op;
+};
+
+template <int D, typename R>
+__global__ void k_coupling_op(CoupleArgs A) {
+    constexpr int T = Geo<D>::T;
+    using RW = Rows<D>;
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= (int64_t)live_tiles(A.lv) * T) return;
+    R* ras = (R*)A.ras;
+    const int64_t rs = A.rs;
+    const R* a0 = (const R*)A.a0;
+    const R* u = (const R*)A.u;
+    R* out = (R*)A.out;
+    if (A.op == MLBM_COUPLE_FRACTIONS) {
+        const R mass = ras[RW::MASS * rs + c];
+        const R phi = a0 ? a0[c] : R(0);
+        R eta = ras[RW::ETA * rs + c] - phi;
+        eta = eta > R(0) ? eta : R(0);
+        R e = R(1) - eta - phi;
+        e = e < R(A.eps_min) ? R(A.eps_min) : (e > R(1) ? R(1) : e);
+        ras[RW::ETAE * rs + c] = eta;
+        ras[RW::EPS * rs + c] = e;
+        for (int a = 0; a < D; ++a)
+            ras[(RW::VMOM + a) * rs + c] = mass > R(0) ? ras[(RW::VMOM + a) * rs + c] / mass : R(0);
+        return;
+    }
+    if (A.op == MLBM_COUPLE_DRAG || A.op == MLBM_COUPLE_LIMIT) {
+        const R rho = a0[c];
+        R rel[D], sp2 = R(0);
+        for (int a = 0; a < D; ++a) {
+            rel[a] = u[a * A.us + c] - ras[(RW::VMOM + a) * rs + c];
+            sp2 += rel[a] * rel[a];
+        }
+        const R speed = sqrt(sp2);
+        R fs[D];
+        if (A.op == MLBM_COUPLE_DRAG) {
+            difelice_cell<D, R>(ras[RW::EPS * rs + c], rho, rel, speed, ras[RW::AREA * rs + c], R(A.d_p),
+                                R(A.nu), R(A.re_min), fs);
+            for (int a = 0; a < D; ++a) ras[(RW::REL + a) * rs + c] = rel[a];
+        } else {
+            for (int a = 0; a < D; ++a) fs[a] = ras[(RW::FS + a) * rs + c];
+            limit_drag_cell<D, R>(fs, rho, ras[RW::MASS * rs + c], speed, R(A.dt));
+        }
+        for (int a = 0; a < D; ++a) ras[(RW::FS + a) * rs + c] = fs[a];
+        return;
+    }
+    const int slot = (int)(c / T), lc = (int)(c % T);
+    const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
+    int g[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) g[a] = A.lv.tile_xyz[slot * 3 + a] * 4 + l3[a];
+    const R* fld = (A.op == MLBM_COUPLE_GRAD_EPS && a0) ? a0 : ras + RW::EPS * rs;
+    R grad[D];
+    grad_cell<D, R>(A.lv, g, c, [&](int64_t ni) { return fld[ni]; }, grad);
+    if (A.op == MLBM_COUPLE_GRAD_EPS) {
+        for (int a = 0; a < D; ++a) out[a * A.os + c] = grad[a];
+        return;
+    }
+    const R rho = a0[c];
+    const R coefg = (rho - R(A.rho0)) / ras[RW::EPS * rs + c];
+    for (int a = 0; a < D; ++a) {
+        const R gt = coefg * grad[a];
+        ras[(RW::GRAD + a) * rs + c] = gt;
+        out[a * A.os + c] = gt + rho * R(A.g[a]) - ras[(RW::FS + a) * rs + c];
+    }
+}
+
+// granular.stencil (granular.py:137-178) per particle: flat node index, weight,
+// weight gradient and node offset for each of the 3^D nodes (node k: offsets
+// k % 3, (k / 3) % 3, k / 9, the reference's _OFF_X/_OFF_Y order); a node
+// outside a non-periodic domain or not stored at level 0 is a stencil fault
+template <int D, typename R>
+__global__ void k_stencil(int n, const double* __restrict__ x, int64_t ps, TopoL0 t0, int32_t* idx,
+                          R* w, R* grad, R* dpos, int64_t os, mlbm_error_t* err) {
+    constexpr int K = Geo<D>::K;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    double xp[3] = {0, 0, 0}, f[3] = {0, 0, 0}, wa[3][3], da[3][3];
+    int base[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) {
+        xp[a] = x[a * ps + p];
+        const double b = floor(xp[a] - 0.5);
+        base[a] = (int)b;
+        f[a] = xp[a] - b;
+        wa[a][0] = 0.5 * (1.5 - f[a]) * (1.5 - f[a]);
+        wa[a][1] = 0.75 - (f[a] - 1.0) * (f[a] - 1.0);
+        wa[a][2] = 0.5 * (f[a] - 0.5) * (f[a] - 0.5);
+        da[a][0] = f[a] - 1.5;
+        da[a][1] = -2.0 * (f[a] - 1.0);
+        da[a][2] = f[a] - 0.5;
+    }
+    bool bad = false;
+    for (int k = 0; k < K; ++k) {
+        const int o[3] = {k % 3, (k / 3) % 3, D == 3 ? k / 9 : 0};
+        int c[3] = {0, 0, 0};
+        for (int a = 0; a < D; ++a) c[a] = base[a] + o[a];
+        const int64_t ni = node_index<D>(t0, c, bad);
+        idx[(int64_t)k * os + p] = (int32_t)ni;
+        double ww = 1.0;
+        for (int a = 0; a < D; ++a) ww *= wa[a][o[a]];
+        w[(int64_t)k * os + p] = R(ww);
+        for (int b = 0; b < D; ++b) {
+            double gb = da[b][o[b]];
+            for (int e = 0; e < D; ++e) if (e != b) gb *= wa[e][o[e]];
+            grad[((int64_t)b * K + k) * os + p] = R(gb);
+            dpos[((int64_t)b * K + k) * os + p] = R((double)(base[b] + o[b]) - xp[b]);
+        }
+    }
+    if (bad) report_error(err, MLBM_ERR_STENCIL, 0, base[0], base[1], base[2]);
+}
+
+// Kirchhoff stress rows from F for every particle (granular.py:260-279): the
+// initial state and any F set from outside G2P
+template <int D, typename R>
+__global__ void k_particle_stress(int n, R* pp, int64_t ps, MatParams mp) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    R F[D * D], tau[D * D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) F[k] = pp[(PRows<D>::F + k) * ps + p];
+    kirchhoff<D, R>(F, mp, tau);
+#pragma unroll
+    for (int k = 0; k < Geo<D>::NS; ++k) pp[(PRows<D>::TAU + k) * ps + p] = tau[s_a<D>(k) * D + s_b<D>(k)];
 }
 
 // ---------------------------------------------------------------------------
@@ -736,6 +1012,7 @@ __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(P
 #pragma unroll
     for (int k = 0; k < D * D; ++k) C[k] = R(4) * B[k];
     int ncl = 0;
+    double xnew[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
         double xn = x[a] + dt * (double)v[a];
@@ -749,9 +1026,31 @@ __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(P
             xn = xn < 2.0 ? 2.0 : (xn > dim - 2.0 ? dim - 2.0 : xn);
         }
         P.xw[a * P.ps + p] = xn;
+        xnew[a] = xn;
         pw[(PR::V + a) * P.ps + p] = v[a];
     }
     if (ncl) atomicAdd(clamped, ncl);
+    if (P.seeds) {
+        // seeds of the adapt pass that follows (its particle stage reads no
+        // positions then): tile of floor(x) // 4 of the new position
+        int tc[3] = {0, 0, 0};
+        bool bad_x = false;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            const double xv = xnew[a];
+            const int c = (int)floor(xv);
+            if (!(xv == xv) || c < 0 || c >= t0.cells[a]) bad_x = true;
+            tc[a] = c >> 2;
+        }
+        if (bad_x) {
+            report_error(err, MLBM_ERR_DOMAIN, 0, tc[0], tc[1], tc[2]);
+            atomicAdd(P.nonleaf, 1);
+        } else {
+            const int64_t g = g3(t0.tiles, tc[0], tc[1], tc[2]);
+            P.seeds[g] = 1;
+            if (P.kind0[g] != 1) atomicAdd(P.nonleaf, 1);
+        }
+    }
     {
         R vmax = R(0);
 #pragma unroll
@@ -778,35 +1077,53 @@ __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(P
             fast = fabs(s[0]) > R(1e-6) && fabs(s[1]) > R(1e-6) && fabs(s[2]) > R(1e-6);
         }
         if (!fast) svd<D, R>(Fn, U, s, V);
-        R e[D], tr = R(0);
         const R vc = vc_pre;
+        R en[D], se[D];
+        if (mp.snow) {
+            // NACC snow with the paper's softening law; vc is the hardening state
 #pragma unroll
-        for (int a = 0; a < D; ++a) {
-            R sa = s[a] < R(0.05) ? R(0.05) : (s[a] > R(4) ? R(4) : s[a]);
-            e[a] = log(sa) + vc / R(D);
-            tr += e[a];
-        }
-        R eh[D], nrm2 = R(0);
+            for (int a = 0; a < D; ++a) {
+                const R sa = s[a] < R(0.05) ? R(0.05) : (s[a] > R(4) ? R(4) : s[a]);
+                en[a] = log(sa);
+            }
+            R qs = vc;
+            nacc_return<D, R>(en, qs, mp);
+            pw[PR::VC * P.ps + p] = qs;
 #pragma unroll
-        for (int a = 0; a < D; ++a) { eh[a] = e[a] - tr / R(D); nrm2 += eh[a] * eh[a]; }
-        const R nrm = sqrt(nrm2);
-        const R dg = nrm + R(D == 3 ? mp.kdg3 : mp.kdg2) * tr * R(mp.alpha);
-        R en[D];
-        if (tr > R(0)) {
-#pragma unroll
-            for (int a = 0; a < D; ++a) en[a] = R(0);
-        } else if (nrm > R(0) && dg > R(0)) {
-            const R sc = dg / nrm;
-#pragma unroll
-            for (int a = 0; a < D; ++a) en[a] = e[a] - sc * eh[a];
+            for (int a = 0; a < D; ++a) se[a] = exp(en[a]);
         } else {
+            R e[D], tr = R(0);
 #pragma unroll
-            for (int a = 0; a < D; ++a) en[a] = e[a];
+            for (int a = 0; a < D; ++a) {
+                R sa = s[a] < R(0.05) ? R(0.05) : (s[a] > R(4) ? R(4) : s[a]);
+                e[a] = log(sa) + vc / R(D);
+                tr += e[a];
+            }
+            R eh[D], nrm2 = R(0);
+#pragma unroll
+            for (int a = 0; a < D; ++a) { eh[a] = e[a] - tr / R(D); nrm2 += eh[a] * eh[a]; }
+            const R nrm = sqrt(nrm2);
+            const R dg = nrm + R(D == 3 ? mp.kdg3 : mp.kdg2) * tr * R(mp.alpha);
+            if (tr > R(0)) {
+#pragma unroll
+                for (int a = 0; a < D; ++a) en[a] = R(0);
+            } else if (nrm > R(0) && dg > R(0)) {
+                const R sc = dg / nrm;
+#pragma unroll
+                for (int a = 0; a < D; ++a) en[a] = e[a] - sc * eh[a];
+            } else {
+#pragma unroll
+                for (int a = 0; a < D; ++a) en[a] = e[a];
+            }
+            R sum = R(0);
+#pragma unroll
+            for (int a = 0; a < D; ++a) { sum += en[a]; se[a] = exp(en[a]); }
+            pw[PR::VC * P.ps + p] = tr - sum;
         }
-        R sum = R(0), se[D];
-#pragma unroll
-        for (int a = 0; a < D; ++a) { sum += en[a]; se[a] = exp(en[a]); }
-        pw[PR::VC * P.ps + p] = tr - sum;
+        // F_new has left vectors U and stretches exp(en): its Kirchhoff stress
+        // (what the next P2G would get from an SVD of F_new) is U diag(2 mu en
+        // + lam tr en) U^T
+        store_tau<D, R>(pw, P.ps, p, U, en, mp);
         if (fast) {
             // F_new = U diag(s_new / s) U^T F  ( = U diag(s_new) V^T )
             R M[D * D], G[D * D];
@@ -842,6 +1159,19 @@ __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(P
                 }
         }
     }
+    if (!plastic) {
+        // elastic: decompose the updated F for its stress
+        R U[D * D], s[D], e[D];
+        if constexpr (D == 3) {
+            left_stretch3<R>(Fn, U, s);
+        } else {
+            R V[D * D];
+            svd<D, R>(Fn, U, s, V);
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a) e[a] = log(s[a] > R(1e-12) ? s[a] : R(1e-12));
+        store_tau<D, R>(pw, P.ps, p, U, e, mp);
+    }
 #pragma unroll
     for (int k = 0; k < D * D; ++k) pw[(PR::F + k) * P.ps + p] = Fn[k];
     if (copy_rows) {
@@ -866,10 +1196,8 @@ __global__ void k_stress_raster(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int
     for (int a = 0; a < D; ++a) x[a] = P.x[a * P.ps + p];
     Stencil<D, R> st;
     make_stencil<D, R>(x, st);
-    R F[D * D];
-    for (int k = 0; k < D * D; ++k) F[k] = pp[(PR::F + k) * P.ps + p];
     R tau[D * D];
-    kirchhoff<D, R>(F, mp, tau);
+    load_tau<D, R>(pp, P.ps, p, tau);
     const R V0 = pp[PR::V0 * P.ps + p];
     bool bad = false;
     for (int k = 0; k < K; ++k) {
@@ -944,6 +1272,7 @@ struct PowderArgs {
     void* tmp;                // [n0] scratch (advected phi)
     double diffusion, sign, dt, entrain, eta_surface;
     int32_t with_source;
+    const void* source;       // optional explicit per-cell source (powder_step's `source`)
 };
 
 template <int D, typename R>
@@ -1020,6 +1349,7 @@ __global__ void k_powder_diffuse(PowderArgs A) {
         }
         out += R(A.dt) * q;
     }
+    if (A.source) out += R(A.dt) * ((const R*)A.source)[c];
     dst.at(fi_phi<D>(), c) = out;
 }
 
@@ -1220,14 +1550,14 @@ __global__ void __launch_bounds__(256) k_p2g_smem(PartArgs P, TopoL0 t0, MatPara
     }
     __syncthreads();
     if (valid) {
-        R v[D], C[D * D], F[D * D];
+        R v[D], C[D * D];
 #pragma unroll
         for (int a = 0; a < D; ++a) v[a] = pp[(PR::V + a) * P.ps + p];
 #pragma unroll
-        for (int k = 0; k < D * D; ++k) { C[k] = pp[(PR::C + k) * P.ps + p]; F[k] = pp[(PR::F + k) * P.ps + p]; }
+        for (int k = 0; k < D * D; ++k) C[k] = pp[(PR::C + k) * P.ps + p];
         const R m = pp[PR::M * P.ps + p], V0 = pp[PR::V0 * P.ps + p];
         R tau[D * D];
-        kirchhoff<D, R>(F, mp, tau);
+        load_tau<D, R>(pp, P.ps, p, tau);
         const R ap = D == 2 ? R(2) * sqrt(V0 / R(3.14159265358979323846))
                             : R(3.14159265358979323846) * pow(R(3) * V0 / (R(4) * R(3.14159265358979323846)), R(2.0 / 3.0));
         bool bad = false;
@@ -1341,13 +1671,13 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
         }
         m = pp[PR::M * P.ps + p];
         V0 = pp[PR::V0 * P.ps + p];
-        R v[D], C[D * D], F[D * D];
+        R v[D], C[D * D];
 #pragma unroll
         for (int a = 0; a < D; ++a) v[a] = pp[(PR::V + a) * P.ps + p];
 #pragma unroll
-        for (int k = 0; k < D * D; ++k) { C[k] = pp[(PR::C + k) * P.ps + p]; F[k] = pp[(PR::F + k) * P.ps + p]; }
+        for (int k = 0; k < D * D; ++k) C[k] = pp[(PR::C + k) * P.ps + p];
         R tau[D * D];
-        kirchhoff<D, R>(F, mp, tau);
+        load_tau<D, R>(pp, P.ps, p, tau);
         ap = D == 2 ? R(2) * sqrt(V0 / R(3.14159265358979323846))
                     : R(3.14159265358979323846) * pow(R(3) * V0 / (R(4) * R(3.14159265358979323846)), R(2.0 / 3.0));
 #pragma unroll
@@ -1556,13 +1886,13 @@ __global__ void __launch_bounds__(128) k_p2g_cell(PartArgs P, TopoL0 t0, MatPara
         }
         m = pp[PR::M * P.ps + p];
         V0 = pp[PR::V0 * P.ps + p];
-        R v[D], C[D * D], F[D * D];
+        R v[D], C[D * D];
 #pragma unroll
         for (int a = 0; a < D; ++a) v[a] = pp[(PR::V + a) * P.ps + p];
 #pragma unroll
-        for (int k = 0; k < D * D; ++k) { C[k] = pp[(PR::C + k) * P.ps + p]; F[k] = pp[(PR::F + k) * P.ps + p]; }
+        for (int k = 0; k < D * D; ++k) C[k] = pp[(PR::C + k) * P.ps + p];
         R tau[D * D];
-        kirchhoff<D, R>(F, mp, tau);
+        load_tau<D, R>(pp, P.ps, p, tau);
         ap = D == 2 ? R(2) * sqrt(V0 / R(3.14159265358979323846))
                     : R(3.14159265358979323846) * pow(R(3) * V0 / (R(4) * R(3.14159265358979323846)), R(2.0 / 3.0));
 #pragma unroll
@@ -1785,13 +2115,13 @@ __device__ __forceinline__ void p2g_record(const PartArgs& P, const MatParams& m
             }
             m = pp[PR::M * P.ps + p];
             V0 = pp[PR::V0 * P.ps + p];
-            float v[D], C[D * D], F[D * D];
+            float v[D], C[D * D];
 #pragma unroll
             for (int a = 0; a < D; ++a) v[a] = pp[(PR::V + a) * P.ps + p];
 #pragma unroll
-            for (int k = 0; k < D * D; ++k) { C[k] = pp[(PR::C + k) * P.ps + p]; F[k] = pp[(PR::F + k) * P.ps + p]; }
+            for (int k = 0; k < D * D; ++k) C[k] = pp[(PR::C + k) * P.ps + p];
             float tau[D * D];
-            kirchhoff<D, float>(F, mp, tau);
+            load_tau<D, float>(pp, P.ps, p, tau);
             ap = D == 2 ? 2.f * sqrtf(V0 / 3.14159265358979323846f)
                         : [](float c) { return 3.14159265358979323846f * c * c; }(
                               cbrtf(3.f * V0 / (4.f * 3.14159265358979323846f)));   // pi (3V/4pi)^(2/3)
@@ -2167,10 +2497,8 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
     float* wslab = &slab[wid * 32 * REC];
     if (need) {
         const float* pp = (const float*)P.p;
-        float F[D * D], tau[D * D];
-#pragma unroll
-        for (int k = 0; k < D * D; ++k) F[k] = pp[(PR::F + k) * P.ps + p];
-        kirchhoff<D, float>(F, mp, tau);
+        float tau[D * D];
+        load_tau<D, float>(pp, P.ps, p, tau);
         const float V0 = pp[PR::V0 * P.ps + p];
         float r[REC];
 #pragma unroll
@@ -2447,13 +2775,17 @@ extern "C" int mlbm_exchange(const mlbm_level_t* lv0, mlbm_fields_t w_tree, mlbm
 
 extern "C" int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, const double* x_in, double* x_out,
                         const void* p_in, void* p_out, const int32_t* pid_in, int32_t* pid_out,
-                        int64_t ps, double lam, double mu, double alpha, const void* ras, int64_t rs,
+                        int64_t ps, double lam, double mu, double alpha, const mlbm_snow_t* snow,
+                        const void* ras, int64_t rs,
                         double dt, int32_t plastic, int32_t dtype, int32_t* clamped,
+                        uint8_t* seeds, const uint8_t* kind0, int32_t* nonleaf,
                         mlbm_error_t* err, void* stream) {
     if (n <= 0) return 0;
+    if (seeds && (!kind0 || !nonleaf)) return -1;
     cudaStream_t s = as_stream(stream);
-    PartArgs P{lv0->dim, n, x_in, x_out, (void*)p_in, ps, p_out, pid_in, pid_in ? pid_out : nullptr};
-    MatParams mp = mat_params(lam, mu, alpha);
+    PartArgs P{lv0->dim, n, x_in, x_out, (void*)p_in, ps, p_out, pid_in, pid_in ? pid_out : nullptr,
+               seeds, kind0, nonleaf};
+    MatParams mp = mat_params(lam, mu, alpha, snow);
     const TopoL0 t = topo0(lv0);
 #define G2P(D, R) k_g2p<D, R><<<nblk(n, G2P_BT), G2P_BT, 0, s>>>(P, t, mp, (const R*)ras, rs, dt, plastic, clamped, err)
     if (lv0->dim == 2) { if (dtype) G2P(2, double); else G2P(2, float); }
@@ -2526,7 +2858,7 @@ extern "C" int mlbm_powder(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm_fiel
     const int T = lv0->dim == 2 ? 16 : 64;
     const int64_t n = (int64_t)lv0->n_tiles * T;
     if (n == 0) return 0;
-    PowderArgs A{*lv0, src, dst, ras, rs, tmp, diffusion, sign, dt, entrain, eta_surface, with_source};
+    PowderArgs A{*lv0, src, dst, ras, rs, tmp, diffusion, sign, dt, entrain, eta_surface, with_source, nullptr};
     cudaStream_t s = as_stream(stream);
 #define PW(D, R) do { k_powder_advect<D, R><<<nblk(n, 128), 128, 0, s>>>(A); \
                       k_powder_diffuse<D, R><<<nblk(n, 128), 128, 0, s>>>(A); } while (0)
@@ -2566,5 +2898,65 @@ extern "C" int mlbm_diag_particles(int32_t dim, int32_t n, const void* p, int64_
     if (dim == 2) { if (dtype) DP(2, double); else DP(2, float); }
     else { if (dtype) DP(3, double); else DP(3, float); }
 #undef DP
+    return launch_status(1);
+}
+
+extern "C" int mlbm_coupling_op(const mlbm_level_t* lv0, int32_t op, void* ras, int64_t rs, const void* a0,
+                                const void* u, int64_t us, void* out, int64_t os, double eps_min,
+                                double nu, double d_p, double re_min, double dt, double rho0,
+                                const double* g, int32_t dtype, void* stream) {
+    if (op < MLBM_COUPLE_FRACTIONS || op > MLBM_COUPLE_MIXTURE_FORCE) return -1;
+    const int T = lv0->dim == 2 ? 16 : 64;
+    const int64_t n = (int64_t)lv0->n_tiles * T;
+    if (n == 0) return 0;
+    CoupleArgs A{*lv0, ras, rs, a0, u, us, out, os, eps_min, nu, d_p, re_min, dt, rho0,
+                 {g ? g[0] : 0.0, g ? g[1] : 0.0, g ? g[2] : 0.0}, op};
+    cudaStream_t s = as_stream(stream);
+#define CO(D, R) k_coupling_op<D, R><<<nblk(n, 128), 128, 0, s>>>(A)
+    if (lv0->dim == 2) { if (dtype) CO(2, double); else CO(2, float); }
+    else { if (dtype) CO(3, double); else CO(3, float); }
+#undef CO
+    return launch_status(1);
+}
+
+extern "C" int mlbm_stencil(const mlbm_level_t* lv0, int32_t n, const double* x, int64_t ps, int32_t* idx,
+                            void* w, void* grad, void* dpos, int64_t os, int32_t dtype, mlbm_error_t* err,
+                            void* stream) {
+    if (n <= 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    const TopoL0 t = topo0(lv0);
+#define ST(D, R) k_stencil<D, R><<<nblk(n, 128), 128, 0, s>>>(n, x, ps, t, idx, (R*)w, (R*)grad, (R*)dpos, os, err)
+    if (lv0->dim == 2) { if (dtype) ST(2, double); else ST(2, float); }
+    else { if (dtype) ST(3, double); else ST(3, float); }
+#undef ST
+    return launch_status(1);
+}
+
+extern "C" int mlbm_powder_step(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm_fields_t dst, void* tmp,
+                                double diffusion, double sign, double dt, const void* source,
+                                int32_t dtype, void* stream) {
+    const int T = lv0->dim == 2 ? 16 : 64;
+    const int64_t n = (int64_t)lv0->n_tiles * T;
+    if (n == 0) return 0;
+    PowderArgs A{*lv0, src, dst, nullptr, 0, tmp, diffusion, sign, dt, 0.0, 0.0, 0, source};
+    cudaStream_t s = as_stream(stream);
+#define PW(D, R) do { k_powder_advect<D, R><<<nblk(n, 128), 128, 0, s>>>(A); \
+                      k_powder_diffuse<D, R><<<nblk(n, 128), 128, 0, s>>>(A); } while (0)
+    if (lv0->dim == 2) { if (dtype) PW(2, double); else PW(2, float); }
+    else { if (dtype) PW(3, double); else PW(3, float); }
+#undef PW
+    return launch_status(2);
+}
+
+extern "C" int mlbm_particle_stress(int32_t dim, int32_t n, void* p, int64_t ps, double lam, double mu,
+                                    double alpha, int32_t dtype, void* stream) {
+    if (n <= 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    const MatParams mp = mat_params(lam, mu, alpha);
+#define PSK(D, R) k_particle_stress<D, R><<<nblk(n, 128), 128, 0, s>>>(n, (R*)p, ps, mp)
+    if (dim == 2) { if (dtype) PSK(2, double); else PSK(2, float); }
+    else if (dim == 3) { if (dtype) PSK(3, double); else PSK(3, float); }
+    else return -1;
+#undef PSK
     return launch_status(1);
 }

@@ -882,3 +882,35 @@ extern "C" int mlbm_init_new_cells(const mlbm_hier_t* old_h, const mlbm_hier_t* 
 #undef INI
     return launch_status(1);
 }
+
+// ---------------------------------------------------------------------------
+// buffer initialisation inside the step (no framework fill kernels in the
+// captured graphs): byte memset on the stream, typed fill for non-zero values
+namespace mlbm {
+template <typename T>
+__global__ void k_fill(T* p, int64_t n, T v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+}  // namespace mlbm
+
+extern "C" int mlbm_memset(void* p, int32_t value, int64_t bytes, void* stream) {
+    if (bytes <= 0) return 0;
+    const cudaError_t e = cudaMemsetAsync(p, value, (size_t)bytes, as_stream(stream));
+    return e == cudaSuccess ? 0 : -(int)e;
+}
+
+extern "C" int mlbm_fill(void* p, int64_t n, int32_t kind, double value, void* stream) {
+    if (n <= 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    const int B = 256;
+    const int G = (int)std::min<int64_t>((n + B - 1) / B, 148 * 8);
+    switch (kind) {
+    case 0: k_fill<uint8_t><<<G, B, 0, s>>>((uint8_t*)p, n, (uint8_t)value); break;
+    case 1: k_fill<int32_t><<<G, B, 0, s>>>((int32_t*)p, n, (int32_t)value); break;
+    case 2: k_fill<float><<<G, B, 0, s>>>((float*)p, n, (float)value); break;
+    case 3: k_fill<double><<<G, B, 0, s>>>((double*)p, n, value); break;
+    default: return -1;
+    }
+    return launch_status(1);
+}

@@ -40,10 +40,58 @@ class SandMaterial:
     def wave_speed(self, density: float) -> float:
         return float(np.sqrt((self.lam + 2 * self.mu) / density))
 
+    def snow_struct(self):
+        return None
+
+
+@dataclass
+class SnowMaterial:
+    """The paper's snow: Non-Associated Cam Clay (Wolper et
+    al. 2019) on the sand's Hencky elasticity with the modified hardening law
+    dq/dt = -alpha_soft q0' until q first reaches 0 (the particle cracks, its
+    cohesion becomes 0), +q0' after.  Absent from the reference:
+    oracle/mpm.py:nacc_return_map is the specification (parity unpinned).
+    The hardening state rides in the vol_corr row (q >= 0, or -(q + 1) once
+    cracked); particles start at q_init."""
+    E: float = 3.5e5
+    nu: float = 0.3
+    M: float = 1.85
+    beta: float = 0.3
+    xi: float = 1.0
+    alpha_soft: float = 0.5
+    q_init: float = 0.05
+    floor_friction: float = 0.5
+    friction_deg: float = 30.0
+
+    def __post_init__(self):
+        self.lam = self.E * self.nu / ((1 + self.nu) * (1 - 2 * self.nu))
+        self.mu = self.E / (2 * (1 + self.nu))
+        self.alpha = 0.0
+
+    def wave_speed(self, density: float) -> float:
+        return float(np.sqrt((self.lam + 2 * self.mu) / density))
+
+    def snow_struct(self):
+        s = L.Snow()
+        s.M, s.beta, s.xi, s.alpha_soft = self.M, self.beta, self.xi, self.alpha_soft
+        return s
+
+
+def snow_arg(mat):
+    """mlbm_g2p's snow parameter block (NULL: Drucker-Prager sand)."""
+    s = mat.snow_struct() if hasattr(mat, "snow_struct") else None
+    if s is None:
+        return None
+    mat._snow_c = s                 # keep the struct alive for the call
+    return L.C.byref(s)
+
 
 def prow(d):
+    """Run-dtype particle rows: v, C, F, m, V0, vol_corr and the Kirchhoff
+    stress tau(F) (symmetric, kept current by G2P; mlbm_particle_stress)."""
     return {"v": 0, "C": d, "F": d + d * d, "m": d + 2 * d * d, "V0": d + 2 * d * d + 1,
-            "vc": d + 2 * d * d + 2, "n": d + 2 * d * d + 3}
+            "vc": d + 2 * d * d + 2, "tau": d + 2 * d * d + 3,
+            "n": d + 2 * d * d + 3 + d * (d + 1) // 2}
 
 
 class Particles:
@@ -65,6 +113,20 @@ class Particles:
         self.pid = torch.arange(n, dtype=torch.int32, device=self.device)
         self.permuted = False
         self._scratch = None
+        # the tau rows hold the Kirchhoff stress of F for the material they
+        # were computed with (None: stale, recomputed before the next P2G)
+        self.stress_mat = None
+
+    def ensure_stress(self, mat):
+        """(Re)compute the tau rows from F when F changed outside G2P or the
+        material differs (mlbm_particle_stress); G2P keeps them current."""
+        key = (float(mat.lam), float(mat.mu))
+        if self.stress_mat == key or not len(self):
+            return
+        L.check(L.lib().mlbm_particle_stress(self.d, len(self), L.ptr(self.pd), self.pd.stride(0),
+                                             mat.lam, mat.mu, mat.alpha, dtype_code(self.dtype),
+                                             L.stream_handle()), "particle_stress")
+        self.stress_mat = key
 
     def scratch(self):
         """Sort targets + radix-sort workspace (allocated once)."""
@@ -129,6 +191,7 @@ class Particles:
 
     @F.setter
     def F(self, val):
+        self.stress_mat = None
         self._store(self._rows("F", self.d * self.d), self._as(val).reshape(-1, self.d * self.d).t())
 
     def _row(self, name):
@@ -291,7 +354,7 @@ class MpmGrid:
         return self.rows("fs", self.d)[:, :self._live()].t()
 
     def clear(self):
-        self.ras[:self.R["nacc"]].zero_()
+        L.zero(self.ras[:self.R["nacc"]])
 
     def raise_pending(self):
         e = self._err.cpu().numpy()
@@ -315,11 +378,47 @@ def _d3(v, d):
     return t
 
 
+def stencil(positions, topology: Topology):
+    """granular.py:137-178 on the device: quadratic B-spline stencil over the
+    level-0 node map.  ``positions`` is a Particles object or an (n, d) array.
+    Returns (idx, w, g_x, g_y[, g_z], dpos_x, dpos_y[, dpos_z]), each (n, 3^d)
+    in the reference's node order (x offset fastest); idx are level-0 cell
+    indices of this topology.  A node outside a non-periodic domain or not
+    stored at level 0 raises TopologyError (granular.py:160-173)."""
+    d = topology.d
+    if isinstance(positions, Particles):
+        xd = positions.xd
+    else:
+        xd = torch.as_tensor(np.asarray(positions, dtype=np.float64) if not torch.is_tensor(positions)
+                             else positions, dtype=torch.float64,
+                             device=topology.device).reshape(-1, d).t().contiguous()
+    n = xd.shape[1]
+    K = 3 ** d
+    dev = topology.device
+    idx = torch.empty((K, n), dtype=torch.int32, device=dev)
+    w = torch.empty((K, n), dtype=torch.float64, device=dev)
+    g = torch.empty((d, K, n), dtype=torch.float64, device=dev)
+    dp = torch.empty((d, K, n), dtype=torch.float64, device=dev)
+    err = torch.zeros(L.ERR_INTS, dtype=torch.int32, device=dev)
+    if n:
+        lv0 = topology.level_struct(0)
+        L.check(L.lib().mlbm_stencil(L.C.byref(lv0), n, L.ptr(xd), xd.stride(0), L.ptr(idx),
+                                     L.ptr(w), L.ptr(g), L.ptr(dp), n, 1, L.ptr(err),
+                                     L.stream_handle()), "stencil")
+        e = err.cpu().numpy()
+        if e[0]:
+            raise TopologyError(f"particle stencil node near ({e[3]},{e[4]},{e[5]}) not stored at "
+                                f"the finest level / outside the domain")
+    return (idx.t().long(), w.t()) + tuple(g[a].t() for a in range(d)) + \
+        tuple(dp[a].t() for a in range(d))
+
+
 def p2g(particles: Particles, grid: MpmGrid, mat: SandMaterial, st=None):
     grid.sync_topology()
     grid.clear()
     if not len(particles):
         return
+    particles.ensure_stress(mat)
     lv0 = grid.level0()
     L.check(L.lib().mlbm_p2g(L.C.byref(lv0), len(particles), L.ptr(particles.xd),
                              L.ptr(particles.pd), particles.pd.stride(0), mat.lam, mat.mu,
@@ -354,8 +453,9 @@ def g2p(particles: Particles, grid: MpmGrid, dt: float, mat: SandMaterial,
     L.check(L.lib().mlbm_g2p(L.C.byref(lv0), len(particles), L.ptr(particles.xd),
                              L.ptr(particles.xd), L.ptr(particles.pd), L.ptr(particles.pd),
                              L.ptr(None), L.ptr(None), particles.pd.stride(0), mat.lam, mat.mu,
-                             mat.alpha, L.ptr(grid.ras), grid.ras.stride(0), float(dt),
+                             mat.alpha, snow_arg(mat), L.ptr(grid.ras), grid.ras.stride(0), float(dt),
                              1 if plastic else 0, dtype_code(grid.dtype), L.ptr(grid.counters),
+                             L.ptr(None), L.ptr(None), L.ptr(None),
                              L.ptr(grid._err), L.stream_handle()), "g2p")
     grid.raise_pending()
     return int(grid.counters[0].item())

@@ -32,7 +32,8 @@ def save_checkpoint(path, sim):
         "streaks": ([s.cpu().clone() for s in sim.adaptor._streak]
                     if sim.adaptor is not None else None),
         "particles": {"xd": p.xd.cpu().clone(), "pd": p.pd.cpu().clone(),
-                      "pid": p.pid.cpu().clone(), "permuted": p.permuted},
+                      "pid": p.pid.cpu().clone(), "permuted": p.permuted,
+                      "stress_valid": p.stress_mat is not None},
         "topology_changes": sim.topology_changes,
     }
     torch.save(state, path)
@@ -70,6 +71,9 @@ def load_checkpoint(path, sim):
     p.pd.copy_(ps["pd"].to(p.device))
     p.pid.copy_(ps["pid"].to(p.device))
     p.permuted = ps["permuted"]
+    # the tau rows were saved with the state they describe
+    p.stress_mat = ((float(sim.material.lam), float(sim.material.mu))
+                    if ps.get("stress_valid") else None)
     # derived state: tables, rasters, captured graphs
     solver._tables_version = -1
     solver._refresh_tables()

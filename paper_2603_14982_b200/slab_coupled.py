@@ -35,7 +35,7 @@ import torch.distributed as dist
 from . import _lib as L
 from .adapt import GridAdaptor, RefineDriver
 from .coupling import CoupledSim
-from .granular import Particles, _d3, _faces
+from .granular import Particles, _d3, _faces, snow_arg
 from .slab_lbm import SlabMultiLevel, exchange_columns
 from .solver import FIELD_FORCE, FIELD_TAU, MultiLevelSolver
 from .sparse_grid import TILE, Topology, dtype_code, moment_names
@@ -357,8 +357,9 @@ class SlabCoupled(CoupledSim):
         if n:
             L.check(lib.mlbm_g2p(L.C.byref(lv0), n, L.ptr(p.xd), L.ptr(p.xd), L.ptr(p.pd),
                                  L.ptr(p.pd), L.ptr(None), L.ptr(None), ps, mat.lam, mat.mu,
-                                 mat.alpha, L.ptr(grid.ras), grid.ras.stride(0),
+                                 mat.alpha, snow_arg(mat), L.ptr(grid.ras), grid.ras.stride(0),
                                  float(self.cadence), 1, dcode, L.ptr(self._counters),
+                                 L.ptr(None), L.ptr(None), L.ptr(None),
                                  L.ptr(grid._err), s), "g2p")
         from .coupling import CouplingFields
         self.last_fields = CouplingFields(grid, self.pair.trees[0].levels[0])
@@ -443,6 +444,8 @@ class SlabCoupled(CoupledSim):
         """coupling.py:448-481 on the slab: cycle (with (i)/(ii) inside),
         migration (iii), global block maintenance (iv), reduced diagnostics (v)."""
         solver = self.solver
+        if self.particles is not None:
+            self.particles.ensure_stress(self.material)
         cycle = solver._schedule[ci]
         if is_mpm:
             solver.run_cycle(cycle, hook=self._exchange)

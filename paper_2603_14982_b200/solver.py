@@ -385,7 +385,8 @@ class MultiLevelSolver:
             dd = _data(dst)
             base = field_names(self.d).index("fx")
             for a in range(self.d):
-                dd[base + a].copy_(torch.as_tensor(force[a], dtype=self.dtype, device=dd.device))
+                fa = torch.as_tensor(force[a], dtype=self.dtype, device=dd.device).reshape(-1)
+                dd[base + a, :fa.numel()].copy_(fa)
             force_mode = 1
         if tau_eff is FIELD_TAU:
             tau_mode = 1

@@ -137,6 +137,10 @@ def adapt_walk():
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "variants":
+        scene_fixture("dune_2d_cadence2_literal", S.DUNE_2D_CADENCE2_LITERAL, 20)
+        scene_fixture("powder_box_2d_literal", S.POWDER_BOX_2D_LITERAL, 20)
+        sys.exit(0)
     one_step_golden()
     multilevel_tg(2)
     multilevel_tg(3)
@@ -146,3 +150,5 @@ if __name__ == "__main__":
     scene_fixture("powder_box_2d", S.POWDER_BOX_2D, 20)
     scene_fixture("dune_2d", S.DUNE_2D, 20)
     scene_fixture("cloud_2d", S.CLOUD_2D, 25, velocity_seed=4)
+    scene_fixture("dune_2d_cadence2_literal", S.DUNE_2D_CADENCE2_LITERAL, 20)
+    scene_fixture("powder_box_2d_literal", S.POWDER_BOX_2D_LITERAL, 20)

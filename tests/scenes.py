@@ -44,6 +44,19 @@ CLOUD_2D = {
     "particles": {"blocks": [[40.0, 40.0, 56.0, 56.0], [80.0, 70.0, 92.0, 86.0]], "per_cell": 1},
     "runtime": {"seed": 9}}
 
+# reference behaviours the default scenes never reach: the held hook at
+# mpm_cadence = 2 (coupling.py:454-465), the paper-literal S rescale
+# (solver.py:41-52) and average upward transfer on three levels, and the
+# paper-literal powder diffusion sign (coupling.py:262-267)
+DUNE_2D_CADENCE2_LITERAL = copy.deepcopy(DUNE_2D)
+DUNE_2D_CADENCE2_LITERAL["runtime"]["mpm_cadence"] = 2
+DUNE_2D_CADENCE2_LITERAL["fluid"]["rescale_convention"] = "paper_literal"
+DUNE_2D_CADENCE2_LITERAL["fluid"]["upward_mode"] = "average"
+
+POWDER_BOX_2D_LITERAL = copy.deepcopy(POWDER_BOX_2D)
+POWDER_BOX_2D_LITERAL["powder"]["sign"] = "paper_literal"
+POWDER_BOX_2D_LITERAL["runtime"]["mpm_cadence"] = 2
+
 # ---- 3D -------------------------------------------------------------------------
 COLUMN_3D_SMALL = {     # config 2 at test size
     "domain": {"cells": [32, 32, 32], "levels": 2},
@@ -94,6 +107,16 @@ POWDER_3D_SMALL = {     # config 4 ingredients at test size (powder on, solids)
     "particles": {"blocks": [[12.0, 6.0, 4.0, 20.0, 14.0, 12.0]], "per_cell": 2},
     "powder": {"enabled": True, "entrain": 0.02, "diffusion": 0.05},
     "runtime": {"seed": 3}}
+
+# the paper's snow (NACC + softening law; parity unpinned):
+# a softened column under strong gravity cracks within a few steps, so both
+# hardening branches run
+SNOW_3D_SMALL = copy.deepcopy(COLUMN_3D_SMALL)
+SNOW_3D_SMALL["fluid"]["gravity"] = [0.0, -1e-3, 0.0]
+SNOW_3D_SMALL["materials"].update({"model": "snow", "nacc_q0": 0.002, "nacc_alpha": 2.0})
+
+SNOW_2D = copy.deepcopy(SAND_COLLAPSE_2D)
+SNOW_2D["materials"].update({"model": "snow", "nacc_q0": 0.002, "nacc_alpha": 2.0})
 
 # BASELINE.json configs[1]: two-level 128^3-effective column collapse in air,
 # 262,144 particles
@@ -159,7 +182,8 @@ def avalanche_c4(heightfield_path, scale=1):
     """BASELINE.json configs[3]: four-level
     1536x768x384-effective snow avalanche with powder cloud — floor wall over a
     terrain heightmap (solids), outlets elsewhere, g along -y, a snow slab
-    (Drucker-Prager granular material; no NACC model exists in the reference)
+    (NACC snow with the paper's softening law; the reference
+    has no snow model, so this part is parity-unpinned)
     [256,4,50]x[1280,28,334] = 6,979,584 cells at 8 per cell = 55,836,672
     particles, powder entrainment on.  ``scale`` > 1 divides every extent (the
     bounded CPU sample)."""
@@ -173,7 +197,8 @@ def avalanche_c4(heightfield_path, scale=1):
                        "z_min": "outlet", "z_max": "outlet",
                        "heightfield": heightfield_path},
         "materials": {"density_ratio": 40.0, "E": 0.08, "nu": 0.3, "friction_angle_deg": 30.0,
-                      "floor_friction": 0.5},
+                      "floor_friction": 0.5, "model": "snow", "nacc_q0": 0.02,
+                      "nacc_alpha": 0.5},
         "particles": {"blocks": [[256.0 / s, 4.0, 50.0 / s, 1280.0 / s, 4.0 + 24.0 / s, 334.0 / s]],
                       "per_cell": 8},
         "powder": {"enabled": True, "entrain": 0.02, "diffusion": 0.05},

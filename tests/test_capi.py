@@ -64,6 +64,9 @@ def test_pure_host_size_queries():
     if not os.path.exists(_lib.LIBPATH):
         pytest.skip("library not built")
     lib = _lib.load()
-    assert lib.mlbm_particle_rows(3) == 24      # + 3 float64 positions = 27 reals
-    assert lib.mlbm_particle_rows(2) == 13
+    # the reference's 27 reals per particle in 3D (3 float64 positions + 24 rows)
+    # plus the cached Kirchhoff stress (6 rows in 3D, 3 in 2D)
+    assert lib.mlbm_particle_rows(3) == 24 + 6
+    assert lib.mlbm_particle_rows(2) == 13 + 3
+    assert lib.mlbm_raster_rows(3) == 4 + 7 * 3 + 6 + 1
     assert lib.mlbm_ws_bytes(1000) > 8000

@@ -112,6 +112,49 @@ def test_dune_2d_three_levels():
     run_and_compare(S.DUNE_2D, 12)
 
 
+def test_dune_2d_cadence2_paper_literal():
+    """mpm_cadence = 2 (the held hook on odd steps, coupling.py:454-465), the
+    paper-literal S rescale and average upward transfer (solver.py:41-52,
+    543-548) on three levels with adaptation: gate A (the oracle is pinned to
+    the reference on this scene by tests/golden/dune_2d_cadence2_literal.npz)."""
+    run_and_compare(S.DUNE_2D_CADENCE2_LITERAL, 12)
+
+
+@pytest.mark.parametrize("latest_only", [False, True])
+def test_cadence2_churn_3d(latest_only):
+    """Held hook with topology changes between MPM steps in 3D, with the
+    single-tree level-0 rebuild requested (it must fall back to both trees
+    when mpm_cadence > 1)."""
+    sc = S.scene(S.CLOUD_3D_SMALL, runtime__mpm_cadence=2)
+    _need_gpu()
+    osim, dsim = build_both(sc)
+    if latest_only:
+        dsim.latest_only_min_cells = 0
+    rng = np.random.default_rng(23)
+    v = rng.normal(0, 0.08, (len(osim.p), 3)).clip(-0.45, 0.45)
+    osim.p.v[:] = v
+    dsim.particles.v = v
+    changes = 0
+    for s in range(12):
+        osim.step()
+        dsim.step()
+        assert dsim.topology.tile_set() == osim.topo.tile_set(), f"step {s}"
+        if not osim.last_report.noop:
+            changes += 1
+    assert changes > 0
+    assert field_diff(osim, dsim) <= 1e-9
+    assert particle_diff(osim, dsim) <= 1e-9
+
+
+def test_powder_box_2d_paper_literal_sign():
+    run_and_compare(S.POWDER_BOX_2D_LITERAL, 12)
+
+
+def test_h3_xyz_paper_literal_3d():
+    """fluid.h3_xyz = paper_literal (PAPER.md's uniform 1/(2 cs^6) on Gamma_xyz)."""
+    run_and_compare(S.scene(S.DUNE_3D_SMALL, fluid__h3_xyz="paper_literal"), 4)
+
+
 @pytest.mark.parametrize("latest_only", [False, True])
 def test_cloud_2d_block_churn(latest_only):
     """Per-step block churn; latest_only forces the single-tree level-0
@@ -337,7 +380,7 @@ def test_stress_raster_fp32_kernels_agree():
         if atomic:
             os.environ["MLBM_STRESS_ATOMIC"] = "1"
         try:
-            grid.ras[R["sig"]:R["n"]].zero_()
+            grid.ras[R["sig"]:R["etae"]].zero_()
             L.check(lib.mlbm_stress_raster(L.C.byref(lv0), len(p), L.ptr(p.xd), L.ptr(p.pd),
                                            p.pd.stride(0), mat.lam, mat.mu, mat.alpha,
                                            L.ptr(grid.ras), grid.ras.stride(0), 0,
@@ -345,18 +388,18 @@ def test_stress_raster_fp32_kernels_agree():
             torch.cuda.synchronize()
         finally:
             os.environ.pop("MLBM_STRESS_ATOMIC", None)
-        out.append(grid.ras[R["sig"]:R["n"], :grid._live()].double().clone())
+        out.append(grid.ras[R["sig"]:R["etae"], :grid._live()].double().clone())
     # the surface-restricted raster (the production call) equals the full one
     # at every entrainment surface cell
     surf = torch.zeros(grid.ras.shape[1], dtype=torch.float32, device="cuda")
-    grid.ras[R["sig"]:R["n"]].zero_()
+    grid.ras[R["sig"]:R["etae"]].zero_()
     L.check(lib.mlbm_stress_raster_surface(L.C.byref(lv0), len(p), L.ptr(p.xd), L.ptr(p.pd),
                                            p.pd.stride(0), mat.lam, mat.mu, mat.alpha,
                                            L.ptr(grid.ras), grid.ras.stride(0),
                                            float(sim.powder.eta_surface), L.ptr(surf), 0,
                                            L.ptr(grid._err), s), "stress_raster_surface")
     torch.cuda.synchronize()
-    restricted = grid.ras[R["sig"]:R["n"], :grid._live()].double().clone()
+    restricted = grid.ras[R["sig"]:R["etae"], :grid._live()].double().clone()
     grid.raise_pending()
     scale = out[0].abs().amax(dim=1, keepdim=True).clamp_min(1e-30)
     assert out[0].abs().max().item() > 0.0

@@ -78,3 +78,30 @@ def test_gate_b_multilevel_lbm_fp32(levels):
         else:
             r = rel_l2(otopo, lambda l: last(osv, l), dsv.topology, lambda l: last(dsv, l), [nm])
         assert r <= GATE_B, (nm, r)
+
+
+def test_c2_full_size_gate_a_and_b():
+    """BASELINE.json configs[1] at its bench size (128^3-effective, two
+    levels, 262,144 particles): fp64 device at gate A (tile sets and streaks
+    exact, fields / particles <= 1e-9) and the fp32 bench path at gate B
+    (<= 1e-5 relative L2), both after 2 coupled steps against the oracle."""
+    _need_gpu()
+    from test_gpu_coupled import field_diff, particle_diff
+    steps = 2
+    o64, d64 = build_both(S.scene(S.COLUMN_3D_C2, runtime__dtype="f64"))
+    _, d32 = build_both(S.scene(S.COLUMN_3D_C2, runtime__dtype="f32"))
+    ox0 = o64.p.x.copy()
+    dx0 = d32.particles.x.cpu().numpy().copy()
+    for s in range(steps):
+        o64.step()
+        d64.step()
+        d32.step()
+        assert d64.topology.tile_set() == o64.topo.tile_set(), s
+        assert d32.topology.tile_set() == o64.topo.tile_set(), s
+        for a, b in zip(d64.adaptor.streak, o64.adaptor.streak):
+            assert np.array_equal(a, b)
+    assert field_diff(o64, d64) <= 1e-9
+    assert particle_diff(o64, d64) <= 1e-9
+    m = gate_b_metrics(o64, d32, ox0, dx0)
+    print("c2", m)
+    assert all(v <= GATE_B for v in m.values()), m

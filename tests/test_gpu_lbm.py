@@ -334,3 +334,73 @@ def test_collide_kernel_reports_divergence():
     with pytest.raises(DivergenceError) as ei:
         dsv.raise_pending()
     assert ei.value.level == 0 and (5, 7) in [tuple(c) for c in ei.value.cells]
+
+
+def test_reference_subclass_binding_naive_order():
+    """a reference-API solver class (the oracle's Solver,
+    which has the reference's signatures — the reference itself does not
+    travel to the GPU box) whose five kernel seams are forwarded to
+    refbind.B200Kernels, driven in the NaiveReference order on NumPy dicts,
+    reproduces the unmodified class on a three-level 2D run with an inlet,
+    outlets and a wall; the divergence error type is the caller's."""
+    _need_gpu()
+    from paper_2603_14982_b200.refbind import B200Kernels
+
+    class Boom(Exception):
+        def __init__(self, msg, level=None, cells=None):
+            super().__init__(msg)
+            self.level, self.cells = level, cells
+
+    class SolverB200(OL.Solver):
+        def __init__(self, *a, **k):
+            super().__init__(*a, **k)
+            # the reference's attribute names (the oracle abbreviates them)
+            self.topology, self.level_params, self.boundaries = self.topo, self.lp, self.spec
+            self.b200 = B200Kernels(self, divergence_error=Boom)
+
+        def stream_kernel(self, level, src_a, dst):
+            self.b200.stream_kernel(level, src_a, dst)
+
+        def collide_kernel(self, level, src_a, dst, force=None, tau_eff=None):
+            self.b200.collide_kernel(level, src_a, dst, force, tau_eff)
+
+        def boundary_kernel(self, level, dst):
+            self.b200.boundary_kernel(level, dst)
+
+        def downward_kernel(self, level, step, olda, newa, dst):
+            self.b200.downward_kernel(level, step, olda, newa, dst)
+
+        def upward_kernel(self, level, fine, dst):
+            self.b200.upward_kernel(level, fine, dst)
+
+    cells, levels = (64, 64), 3
+    spec = _bc_spec(2, 6.0)
+    fn = smooth_fields(2, 29)
+    runs = []
+    for cls in (OL.Solver, SolverB200):
+        otopo = oracle_static_refined(cells, levels, central_mask(cells, pad=8),
+                                      periodic=spec.periodic_axes())
+        pair = OG.PingPongPair(otopo)
+        sv = cls(otopo, pair, OL.SolverParams(levels=levels, gravity=(0.0, -1e-5)),
+                 OL.LevelParams(levels, 0.8), spec)
+        OL.set_fields(otopo, pair, fn)
+        for _ in range(3):
+            sv.advance_bounce()
+        runs.append((otopo, sv))
+    (ot, a), (_, b) = runs
+    names = moments(2) + ["eps", "phi"]
+    worst = 0.0
+    for l in range(levels):
+        if not ot.cell_count(l):
+            continue
+        x, y = last(a, l), last(b, l)
+        for nm in names:
+            worst = max(worst, float(np.abs(np.asarray(x[nm]) - np.asarray(y[nm])).max()))
+    assert worst <= 1e-12, worst
+    # a non-physical density surfaces as the caller's exception type
+    r, w = b.roles(0)
+    dst = b.arrays(w, 0)
+    b.stream_kernel(0, b.arrays(r, 0), dst)
+    dst["rho"][5] = -1.0
+    with pytest.raises(Boom):
+        b.collide_kernel(0, b.arrays(r, 0), dst)

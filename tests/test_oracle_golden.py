@@ -103,6 +103,8 @@ def test_adapt_walk_golden():
     ("powder_box_2d", S.POWDER_BOX_2D, 20, None),
     ("dune_2d", S.DUNE_2D, 20, None),
     ("cloud_2d", S.CLOUD_2D, 25, 4),
+    ("dune_2d_cadence2_literal", S.DUNE_2D_CADENCE2_LITERAL, 20, None),
+    ("powder_box_2d_literal", S.POWDER_BOX_2D_LITERAL, 20, None),
 ])
 def test_scene_golden(name, scene, steps, vseed):
     g = load(name)

@@ -33,13 +33,11 @@ if os.environ.get("MLBM_ADAPT_TIMESTAMPS"):
     ad.fused = True
     ad.plan_device(drv); torch.cuda.synchronize()
     lib = L.load()
-    lib.mlbm_adapt_timestamps_ptr.restype = ctypes.c_void_p
-    ptr = lib.mlbm_adapt_timestamps_ptr()
-    buf = (ctypes.c_uint64 * 64)()
-    import ctypes.util
-    cudart = ctypes.CDLL("libcudart.so")
-    cudart.cudaMemcpy(buf, ctypes.c_void_p(ptr), ctypes.c_size_t(64 * 8), 2)
-    ts = list(buf)[:16]
+    tsbuf = torch.zeros(64, dtype=torch.int64, device="cuda")     # caller-owned stamps
+    lib.mlbm_adapt_set_timestamps(ctypes.c_void_p(tsbuf.data_ptr()))
+    ad.plan_device(drv); torch.cuda.synchronize()
+    lib.mlbm_adapt_set_timestamps(ctypes.c_void_p(0))
+    ts = tsbuf.cpu().tolist()[:16]
     names = {0: "start", 2: "A+B seeds/invariants", 3: "C des0/cur1", 4: "D par/cur", 5: "E des[l]",
              6: "F eff0", 7: "G par(eff)", 8: "H eff[l]", 9: "top eff", 10: "I own", 11: "J storage/kinds"}
     prev = ts[0]

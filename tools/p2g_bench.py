@@ -60,8 +60,9 @@ for plastic in (1, 0):
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         L.check(lib.mlbm_g2p(L.C.byref(lv0), n, L.ptr(xa), L.ptr(xo), L.ptr(pa), L.ptr(po), L.ptr(ida),
-                             L.ptr(ido), ps, mat.lam, mat.mu, mat.alpha, L.ptr(grid.ras),
+                             L.ptr(ido), ps, mat.lam, mat.mu, mat.alpha, None, L.ptr(grid.ras),
                              grid.ras.stride(0), float(sim.cadence), plastic, 0, L.ptr(cnt),
+                             L.ptr(None), L.ptr(None), L.ptr(None),
                              L.ptr(grid._err), s), "g2p")
         e1.record()
         torch.cuda.synchronize()
