@@ -46,8 +46,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--slabs", action="store_true",
-                    help="coupled slab decomposition (slab_coupled.py) instead of replicas: "
-                         "weak-scaled C2 x N domain, NCCL P2P exchanges")
+                    help="coupled slab decomposition (slab_coupled.py) even at N = 1 "
+                         "(N > 1 always runs it unless --replicas)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: N independent full-scene replicas instead of slabs")
     return ap.parse_args()
 
 
@@ -515,34 +517,33 @@ def run_slab(args, rank, world, local_rank):
 
 
 def run_slabs_coupled(args, rank, world, local_rank):
-    """--slabs: the C2 column replicated N times along x as ONE domain
-    (128 N x 128 x 128, walls), one 128-wide slab per GPU, coupled step with
-    the slab collectives (i)-(v) over NCCL (eager, host-driven exchanges)."""
-    import copy
+    """The north-star decomposition: the chosen scene (C4 by
+    default) split into N x-slabs cut on the coarsest tile width, one per GPU,
+    coupled step with the slab collectives (i)-(v) over NCCL point-to-point
+    (halo columns and ghost-node sums packed by mlbm_halo_pack, particles
+    migrated by mlbm_migrate_count / pack / unpack, uint8 seed OR).  Strong
+    scaling: the total work is the scene's."""
     import numpy as np
     import torch
     import torch.distributed as dist
     from paper_2603_14982_b200 import _lib as L
     from paper_2603_14982_b200.harness import build_scene, validate_scene
     from paper_2603_14982_b200.slab_coupled import P2PExchanger, SlabCoupled, ThreadExchanger
-    import scenes as S
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    sc = copy.deepcopy(S.COLUMN_3D_C2)
-    nx = sc["domain"]["cells"][0]
-    sc["domain"]["cells"][0] = nx * world
-    b = sc["particles"]["blocks"][0]
-    sc["particles"]["blocks"] = [[b[0] + k * nx, b[1], b[2], b[3] + k * nx, b[4], b[5]]
-                                 for k in range(world)]
-    ref = build_scene(validate_scene(sc))
+    cfg = validate_scene(scene_dict(args.scene))
+    ref = build_scene(cfg)           # the global scene, cropped to this rank's slab
+    if args.scene == "c5":
+        import scenes as S
+        S.cloud_velocities(ref)
     ref.use_graphs = False
-    ref.sort_particles = False
     xch = P2PExchanger() if world > 1 else ThreadExchanger(1)
     sim = SlabCoupled(ref, rank, world, xch)
+    n_glob = len(ref.particles)
     del ref
     torch.cuda.empty_cache()
-    eff = int(np.prod(sc["domain"]["cells"]))
+    eff = int(np.prod(cfg.cells))
     for _ in range(args.warmup):
         sim.step()
     torch.cuda.synchronize()
@@ -553,6 +554,7 @@ def run_slabs_coupled(args, rank, world, local_rank):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     l0 = L.TRACE.launches
+    chg0 = sim.topology_changes
     e0.record()
     for _ in range(args.steps):
         sim.step()
@@ -573,16 +575,15 @@ def run_slabs_coupled(args, rank, world, local_rank):
             "metric": METRIC, "value": round(eff * args.steps / (t_ms * 1e-3) / 1e6, 3),
             "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "C2 x N slabs: the C2 column replicated along x as one "
-                                   "(128 N) x 128 x 128 domain, one slab per GPU, coupled step "
-                                   "with ghost-column / ghost-node / particle / seed / diagnostic "
-                                   "exchanges (eager, host-driven)",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if cfg.dtype == torch.float32 else "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args.scene) + f", split into {world} x-slab(s)",
                        "effective_cells": eff, "particles": int(n_loc.item()),
-                       "parallelism": f"slabs{world}"},
+                       "particles_at_start": n_glob, "parallelism": f"slabs{world}",
+                       "l2": "not flushed (slab step)"},
             "particles_per_s": round(float(n_loc.item()) * args.steps / (t_ms * 1e-3), 1),
             "e2e": None, "gpu_launches": L.TRACE.launches - l0, "clocks": clk,
-            "topology_changes": sim.topology_changes}), flush=True)
+            "topology_changes": sim.topology_changes - chg0}), flush=True)
 
 
 # C4's full scene is ~55.8M particles: the CPU sample is the same scene with
@@ -665,7 +666,7 @@ def main():
     try:
         if args.scene == "c1":
             run_slab(args, rank, world, local_rank)
-        elif args.slabs:
+        elif args.slabs or (world > 1 and not args.replicas):
             run_slabs_coupled(args, rank, world, local_rank)
         else:
             run_mine(args, rank, world, local_rank)

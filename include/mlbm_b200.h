@@ -300,16 +300,19 @@ int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, void* p, int64
              int32_t smem, mlbm_error_t* err, void* stream);
 
 /* MPM particle sort (no reference counterpart — ordering only, SURVEY.md
- * §2.3 K7): radix-sort by (level-0 tile slot, cell) of the stencil base cell
- * and gather every particle row (positions, state rows, ids) into the _out
- * buffers.  In mlbm_p2g, smem = 1 accumulates per block in shared memory over
- * the block's bounding box; smem = 2 accumulates per warp in registers (nodes
+ * §2.3 K7): a bucketed counting sort by (level-0 tile slot, cell) of the
+ * stencil base cell — slot histogram, exclusive scan (mlbm_scan_i32), scatter
+ * into the slot ranges, one CTA per slot sorting its range by cell — then every
+ * particle row (positions, state rows, ids) gathered into the _out buffers.
+ * ws: mlbm_sort_ws_bytes(n, lv0->n_tiles) bytes (the level's slot capacity).
+ * In mlbm_p2g, smem = 1 accumulates per block in shared memory over the
+ * block's bounding box; smem = 2 accumulates per warp in registers (nodes
  * owned by lanes, particles broadcast by shuffles); smem = 3 lets lane k own
  * stencil node k of the current cell and flushes per cell into a block box;
  * smem = 4 (fp32 only, the default for fp32 runs; fp64 falls back to 3) keeps
  * one box copy per warp so the per-cell flushes need no shared-memory atomics
  * — all four need sorted input. */
-int64_t mlbm_sort_ws_bytes(int64_t n);
+int64_t mlbm_sort_ws_bytes(int64_t n, int64_t n_slots);
 int mlbm_particle_sort(const mlbm_level_t* lv0, int32_t n, const double* x, const void* p,
                        const int32_t* pid, int64_t ps, double* x_out, void* p_out,
                        int32_t* pid_out, int32_t dtype, void* ws, int64_t ws_bytes,
@@ -325,6 +328,20 @@ int mlbm_exchange(const mlbm_level_t* lv0, mlbm_fields_t w_tree, mlbm_fields_t r
                   double rho0, const double* g_fluid, const double* g_sed,
                   const int32_t* faces, double floor_friction, int32_t mode,
                   int32_t dtype, void* stream);
+
+/* the coupled level-0 phase in ONE kernel (level_kernel mode 5): pull-stream of
+ * src into registers, then per cell the exchange of mlbm_exchange (mode 1) on
+ * those bare moments (eps and force into both trees' rows, the raster rows, the
+ * MPM grid update), then the collide with that force and tau = eps tau0 and the
+ * boundary passes into dst (coupling.py:403-446 between solver.py:336 and
+ * :394 / :460).  P2G must have filled ras; G2P reads its VEL rows after. */
+int mlbm_level0_coupled(const mlbm_level_t* lv, mlbm_fields_t src, mlbm_fields_t dst,
+                        mlbm_fields_t tree0, mlbm_fields_t tree1, int32_t dtype,
+                        const mlbm_collide_t* cp, const mlbm_bc_t* bc, void* ras, int64_t rs,
+                        double eps_min, double nu, double d_p, double re_min, double dt,
+                        double rho0, const double* g_fluid, const double* g_sed,
+                        const int32_t* faces, double floor_friction, mlbm_error_t* err,
+                        void* stream);
 
 /* gather, advect (wrap / clamp to [2, dim-2]), F update, SVD + Drucker-Prager
  * (granular.py:344-412), reading the (sorted) _in rows and writing the _out rows
@@ -416,6 +433,50 @@ int mlbm_diag_level(const mlbm_level_t* lv, mlbm_fields_t f, double vol, int32_t
 int mlbm_diag_particles(int32_t dim, int32_t n, const void* p, int64_t ps, const void* ras,
                         int64_t rs, int64_t n0, const int32_t* live, int32_t dtype,
                         double* out, void* stream);
+
+/* ---- slab staging for the multi-GPU decomposition ------ */
+
+/* ghost / edge tile columns of a SoA block <-> a contiguous NCCL buffer:
+ * buf[r][c - lo] = src[r * stride + c] for r < nrows, lo <= c < hi (elem_bytes
+ * 1, 4 or 8); unpack copies back, or adds (add = 1: the ghost-node partial sums
+ * of collective (ii); dtype 0 f32, 1 f64). */
+int mlbm_halo_pack(const void* src, int64_t stride, int32_t nrows, int64_t lo, int64_t hi,
+                   void* buf, int32_t elem_bytes, void* stream);
+int mlbm_halo_unpack(const void* buf, void* dst, int64_t stride, int32_t nrows, int64_t lo,
+                     int64_t hi, int32_t dtype, int32_t add, void* stream);
+
+/* particle migration (collective (iii)): a stable partition of the n particles
+ * (float64 x [dim][ps], run-dtype rows [rows][ps], ids) into keep (x[0] in
+ * [lo, hi) or no neighbour that side), to-left and to-right, with warp-ballot +
+ * block-scan compaction.  mlbm_migrate_count writes counts[3] = keep, left, right
+ * and the per-block offsets into ws (mlbm_migrate_ws_bytes(n)); mlbm_migrate_pack
+ * (same ws, after the host sized the buffers from counts) scatters every class
+ * in order: keep to the _keep buffers (row stride ks), the leavers to the _left /
+ * _right buffers (row strides ls / rs: one contiguous message per direction)
+ * with x[0] shifted by x0 into global coordinates and wrapped into [0, gx). */
+int64_t mlbm_migrate_ws_bytes(int32_t n);
+int mlbm_migrate_count(int32_t n, const double* x, double lo, double hi, int32_t has_left,
+                       int32_t has_right, int32_t* counts, void* ws, int64_t ws_bytes,
+                       void* stream);
+int mlbm_migrate_pack(int32_t dim, int32_t n, const double* x, const void* p, const int32_t* pid,
+                      int64_t ps, int32_t rows, int32_t dtype, double lo, double hi, double x0,
+                      double gx, int32_t has_left, int32_t has_right, double* x_keep,
+                      void* p_keep, int32_t* pid_keep, int64_t ks, double* x_left,
+                      void* p_left, int32_t* id_left, int64_t ls, double* x_right,
+                      void* p_right, int32_t* id_right, int64_t rs, const void* ws,
+                      int64_t ws_bytes, void* stream);
+/* arrivals (m received records, stride in_stride) appended at particle index at:
+ * x[0] mapped from global coordinates into the local box [0, local_len) */
+int mlbm_migrate_unpack(int32_t dim, int32_t m, const double* x_in, const void* p_in,
+                        const int32_t* id_in, int64_t in_stride, int32_t rows, int32_t dtype,
+                        double x0, double gx, double local_len, double* x, void* p,
+                        int32_t* pid, int64_t ps, int32_t at, void* stream);
+
+/* exclusive scan of n int32 in place (block sums, one scan of the sums, block
+ * scans; no library scan), total (optional) = the sum; ws: mlbm_scan_ws_bytes */
+int64_t mlbm_scan_ws_bytes(int32_t n);
+int mlbm_scan_i32(int32_t n, int32_t* data, int32_t* total, void* ws, int64_t ws_bytes,
+                  void* stream);
 
 /* buffer initialisation on the stream (used inside the captured step graphs
  * instead of framework fill kernels): mlbm_memset = cudaMemsetAsync of bytes;

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIBPATH = os.environ.get("MLBM_LIB") or os.path.join(HERE, "libmlbm_b200.so")
-SOURCES = ["lbm.cu", "topology.cu", "mpm.cu", "adapt.cu", "adapt_bits.cu"]
+SOURCES = ["lbm.cu", "topology.cu", "mpm.cu", "adapt.cu", "adapt_bits.cu", "slab.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
               "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-Wno-deprecated-declarations",
@@ -156,10 +156,15 @@ _SIGS = {
     "mlbm_raster_rows": [I32],
     "mlbm_particle_rows": [I32],
     "mlbm_p2g": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64, I32, I32, P, P],
-    "mlbm_sort_ws_bytes": [I64],
+    "mlbm_sort_ws_bytes": [I64, I64],
+    "mlbm_scan_ws_bytes": [I32],
+    "mlbm_scan_i32": [I32, P, P, P, I64, P],
     "mlbm_particle_sort": [C.POINTER(Level), I32, P, P, P, I64, P, P, P, I32, P, I64, P],
     "mlbm_exchange": [C.POINTER(Level), Fields, Fields, Fields, Fields, P, I64,
                       D, D, D, D, D, D, P, P, P, D, I32, I32, P],
+    "mlbm_level0_coupled": [C.POINTER(Level), Fields, Fields, Fields, Fields, I32,
+                            C.POINTER(Collide), C.POINTER(BC), P, I64, D, D, D, D, D, D, P, P, P, D,
+                            P, P],
     "mlbm_g2p": [C.POINTER(Level), I32, P, P, P, P, P, P, I64, D, D, D, C.POINTER(Snow), P,
                  I64, D, I32, I32, P, P, P, P, P, P],
     "mlbm_stress_raster": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64,
@@ -170,6 +175,13 @@ _SIGS = {
                     I32, I32, P],
     "mlbm_coupling_op": [C.POINTER(Level), I32, P, I64, P, P, I64, P, I64, D, D, D, D, D, D,
                          P, I32, P],
+    "mlbm_halo_pack": [P, I64, I32, I64, I64, P, I32, P],
+    "mlbm_halo_unpack": [P, P, I64, I32, I64, I64, I32, I32, P],
+    "mlbm_migrate_ws_bytes": [I32],
+    "mlbm_migrate_count": [I32, P, D, D, I32, I32, P, P, I64, P],
+    "mlbm_migrate_pack": [I32, I32, P, P, P, I64, I32, I32, D, D, D, D, I32, I32, P, P, P, I64,
+                          P, P, P, I64, P, P, P, I64, P, I64, P],
+    "mlbm_migrate_unpack": [I32, I32, P, P, P, I64, I32, I32, D, D, D, P, P, P, I64, I32, P],
     "mlbm_memset": [P, I32, I64, P],
     "mlbm_fill": [P, I64, I32, D, P],
     "mlbm_particle_stress": [I32, I32, P, I64, D, D, D, I32, P],
@@ -178,7 +190,7 @@ _SIGS = {
     "mlbm_diag_level": [C.POINTER(Level), Fields, D, I32, P, P],
     "mlbm_diag_particles": [I32, I32, P, I64, P, I64, I64, P, I32, P, P],
 }
-_RET64 = {"mlbm_ws_bytes", "mlbm_sort_ws_bytes"}
+_RET64 = {"mlbm_ws_bytes", "mlbm_sort_ws_bytes", "mlbm_migrate_ws_bytes", "mlbm_scan_ws_bytes"}
 
 _LIB = None
 
@@ -284,6 +296,33 @@ def zero(t):
         return
     assert t.is_contiguous()
     check(lib().mlbm_memset(ptr(t), 0, t.numel() * t.element_size(), stream_handle()), "memset")
+
+
+def pack_cols(view, buf):
+    """Rows x columns view of a SoA block (unit column stride) -> contiguous
+    buffer with the library's halo kernel (mlbm_halo_pack); CPU: copy."""
+    if not view.is_cuda:
+        buf.copy_(view)
+        return buf
+    assert view.stride(1) == 1 and buf.is_contiguous() and buf.numel() == view.numel()
+    check(lib().mlbm_halo_pack(ptr(view), view.stride(0), view.shape[0], 0, view.shape[1], ptr(buf),
+                               view.element_size(), stream_handle()), "halo_pack")
+    return buf
+
+
+def unpack_cols(buf, view, add=False):
+    """Contiguous buffer -> rows x columns view (copy, or add: ghost-node sums)."""
+    import torch
+    if not view.is_cuda:
+        if add:
+            view.add_(buf.to(view.device))
+        else:
+            view.copy_(buf)
+        return
+    assert view.stride(1) == 1 and buf.is_contiguous() and buf.numel() == view.numel()
+    dt = 1 if view.dtype == torch.float64 else 0
+    check(lib().mlbm_halo_unpack(ptr(buf), ptr(view), view.stride(0), view.shape[0], 0, view.shape[1],
+                                 dt, 1 if add else 0, stream_handle()), "halo_unpack")
 
 
 def fill(t, value):

@@ -331,6 +331,9 @@ class CoupledSim:
         self.precapture_steps = int(os.environ.get("MLBM_PRECAPTURE", "16")) or None
         self.latest_only_rebuild = os.environ.get("MLBM_LATEST_ONLY_REBUILD", "1") != "0"
         self.latest_only_min_cells = 1 << 22
+        # the level-0 coupled phase as P2G -> ONE stream + exchange + collide
+        # kernel -> G2P (MLBM_FUSE_L0=0: stream / exchange / collide separately)
+        self.fuse_level0 = os.environ.get("MLBM_FUSE_L0", "1") != "0"
         self.p2g_mode = 4          # sorted input: 1 block smem, 2 warp registers, 3 cell lanes,
                                    # 4 cell lanes + per-warp box copies (fp32; fp64 runs mode 3),
                                    # 5 = 4 with two rounds of particles per block
@@ -365,13 +368,17 @@ class CoupledSim:
 
     # -- exchange ------------------------------------------------------------------
     def _exchange(self, solver):
-        r, w = solver.roles(0)
+        """The coupling hook (coupling.py:403-446) as three launches between
+        the level-0 stream and collide: P2G, the exchange, G2P."""
+        self._p2g_phase(solver)
+        self._exchange_kernel(solver)
+        self._g2p_phase(solver)
+        return FIELD_FORCE, FIELD_TAU
+
+    def _p2g_phase(self, solver):
         grid = self.grid
         grid.sync_topology()
         p = self.particles
-        lib = L.lib()
-        s = L.stream_handle()
-        dcode = dtype_code(self.dtype)
         mat = self.material
         lv0 = grid.level0()
         grid.clear()
@@ -386,41 +393,80 @@ class CoupledSim:
         else:
             src_x, src_p, src_id = p.xd, p.pd, None
             smem = self.p2g_mode if (self.sort_particles and p.permuted) else 0
-        L.check(lib.mlbm_p2g(L.C.byref(lv0), n, L.ptr(src_x), L.ptr(src_p), ps,
-                             mat.lam, mat.mu, mat.alpha, L.ptr(grid.ras), grid.ras.stride(0),
-                             dcode, smem, L.ptr(grid._err), s), "p2g")
+        self._p2g_src = (src_x, src_p, src_id)
+        L.check(L.lib().mlbm_p2g(L.C.byref(lv0), n, L.ptr(src_x), L.ptr(src_p), ps,
+                                 mat.lam, mat.mu, mat.alpha, L.ptr(grid.ras), grid.ras.stride(0),
+                                 dtype_code(self.dtype), smem, L.ptr(grid._err),
+                                 L.stream_handle()), "p2g")
+        solver.launches += 1
+
+    def _exchange_args(self, solver):
         sp = solver.params
-        L.check(lib.mlbm_exchange(L.C.byref(lv0), L.fields(solver.arrays(w, 0).data),
-                                  L.fields(solver.arrays(r, 0).data),
-                                  L.fields(self.pair.trees[0].levels[0].data),
-                                  L.fields(self.pair.trees[1].levels[0].data),
-                                  L.ptr(grid.ras), grid.ras.stride(0), float(sp.eps_min),
-                                  float(solver.level_params.nu(0)),
-                                  float(self.drag_params.d_p or 1.0), float(self.drag_params.re_min),
-                                  float(self.cadence), float(sp.rho0), _d3(sp.gravity, self.d),
-                                  _d3(self.sediment_gravity, self.d), _faces(solver.boundaries),
-                                  float(mat.floor_friction), 1, dcode, s), "exchange")
+        return (float(sp.eps_min), float(solver.level_params.nu(0)),
+                float(self.drag_params.d_p or 1.0), float(self.drag_params.re_min),
+                float(self.cadence), float(sp.rho0), _d3(sp.gravity, self.d),
+                _d3(self.sediment_gravity, self.d), _faces(solver.boundaries),
+                float(self.material.floor_friction))
+
+    def _exchange_kernel(self, solver):
+        r, w = solver.roles(0)
+        grid = self.grid
+        L.check(L.lib().mlbm_exchange(L.C.byref(grid.level0()), L.fields(solver.arrays(w, 0).data),
+                                      L.fields(solver.arrays(r, 0).data),
+                                      L.fields(self.pair.trees[0].levels[0].data),
+                                      L.fields(self.pair.trees[1].levels[0].data),
+                                      L.ptr(grid.ras), grid.ras.stride(0),
+                                      *self._exchange_args(solver), 1, dtype_code(self.dtype),
+                                      L.stream_handle()), "exchange")
+        solver.launches += 1
+
+    def _level0_coupled(self, solver):
+        """Level-0 stream + exchange + collide + boundaries in ONE kernel
+        (mlbm_level0_coupled, level_kernel mode 5): the exchange of each cell
+        runs on its bare post-stream moments in registers."""
+        r, w = solver.roles(0)
+        grid = self.grid
+        solver._refresh_tables()
+        cp = solver._collide_struct(0, force_mode=1, tau_mode=1)
+        L.check(L.lib().mlbm_level0_coupled(
+            L.C.byref(solver._structs[0]), L.fields(solver.arrays(r, 0).data),
+            L.fields(solver.arrays(w, 0).data), L.fields(self.pair.trees[0].levels[0].data),
+            L.fields(self.pair.trees[1].levels[0].data), dtype_code(self.dtype), L.C.byref(cp),
+            L.C.byref(solver._bc), L.ptr(grid.ras), grid.ras.stride(0), *self._exchange_args(solver),
+            L.ptr(solver._err), L.stream_handle()), "level0_coupled")
+        solver.launches += 1
+
+    def _g2p_phase(self, solver):
+        grid = self.grid
+        p = self.particles
+        mat = self.material
+        src_x, src_p, src_id = self._p2g_src
         seeds = self._g2p_seeds()
         ad = self.adaptor
-        L.check(lib.mlbm_g2p(L.C.byref(lv0), n, L.ptr(src_x), L.ptr(p.xd), L.ptr(src_p),
-                             L.ptr(p.pd), L.ptr(src_id), L.ptr(p.pid) if src_id is not None else
-                             L.ptr(None), ps, mat.lam, mat.mu, mat.alpha, snow_arg(mat),
-                             L.ptr(grid.ras), grid.ras.stride(0), float(self.cadence), 1, dcode,
-                             L.ptr(self._counters),
-                             L.ptr(ad._seeds if seeds else None),
-                             L.ptr(self.topology.lv[0].kind if seeds else None),
-                             L.ptr(ad.ext_count if seeds else None),
-                             L.ptr(grid._err), s), "g2p")
-        solver.launches += 3
+        L.check(L.lib().mlbm_g2p(L.C.byref(grid.level0()), len(p), L.ptr(src_x), L.ptr(p.xd),
+                                 L.ptr(src_p), L.ptr(p.pd), L.ptr(src_id),
+                                 L.ptr(p.pid) if src_id is not None else L.ptr(None),
+                                 p.pd.stride(0), mat.lam, mat.mu, mat.alpha, snow_arg(mat),
+                                 L.ptr(grid.ras), grid.ras.stride(0), float(self.cadence), 1,
+                                 dtype_code(self.dtype), L.ptr(self._counters),
+                                 L.ptr(ad._seeds if seeds else None),
+                                 L.ptr(self.topology.lv[0].kind if seeds else None),
+                                 L.ptr(ad.ext_count if seeds else None),
+                                 L.ptr(grid._err), L.stream_handle()), "g2p")
+        solver.launches += 1
         self.last_fields = CouplingFields(grid, self.pair.trees[0].levels[0])
-        return FIELD_FORCE, FIELD_TAU
+
+    def _hook(self):
+        """The coupling hook for run_cycle: fused (P2G -> one level-0 kernel
+        -> G2P) unless fuse_level0 is off."""
+        return _CoupledHook(self) if self.fuse_level0 else self._exchange
 
     def _sort_into_scratch(self):
         """Radix sort of the particle rows by (level-0 tile slot, cell) into
         the scratch buffers (no reference counterpart; ordering only)."""
         p = self.particles
-        xa, pa, ida, ws = p.scratch()
         lv0 = self.grid.level0()
+        xa, pa, ida, ws = p.scratch(lv0.n_tiles)
         L.check(L.lib().mlbm_particle_sort(L.C.byref(lv0), len(p), L.ptr(p.xd), L.ptr(p.pd),
                                            L.ptr(p.pid), p.pd.stride(0), L.ptr(xa), L.ptr(pa),
                                            L.ptr(ida), dtype_code(self.dtype), L.ptr(ws),
@@ -456,7 +502,7 @@ class CoupledSim:
         self._sort_ahead = self._sorted_ahead = False
         cycle = solver._schedule[ci]
         if is_mpm:
-            solver.run_cycle(cycle, hook=self._exchange)
+            solver.run_cycle(cycle, hook=self._hook())
         elif self.coupling_active:
             solver.run_cycle(cycle, hook=self._held)
         else:
@@ -493,7 +539,7 @@ class CoupledSim:
         solver.check_errors = False
         try:
             if is_mpm:
-                solver.run_cycle(cycle, hook=self._exchange)
+                solver.run_cycle(cycle, hook=self._hook())
             elif self.coupling_active:
                 solver.run_cycle(cycle, hook=self._held)
             else:
@@ -626,7 +672,7 @@ class CoupledSim:
         # persistent buffers (and the side stream) are created outside any capture
         self._side_stream()
         if self.sort_particles and len(self.particles):
-            self.particles.scratch()
+            self.particles.scratch(self.grid.level0().n_tiles)
         if self.powder is not None:
             self._powder_tmp()
         # refresh host-side tables / rasters before capture (may sync)
@@ -865,3 +911,25 @@ class CoupledSim:
     @property
     def _cfl(self):
         return int(self._counters[1].item())
+
+
+class _CoupledHook:
+    """run_cycle hook of a coupled MPM step: called as a plain hook it runs the
+    exchange between stream and collide (coupling.py:403-446); run_cycle uses
+    its fused form — pre (P2G), one level-0 stream + exchange + collide kernel,
+    post (G2P)."""
+
+    def __init__(self, sim):
+        self.sim = sim
+
+    def __call__(self, solver):
+        return self.sim._exchange(solver)
+
+    def pre(self, solver):
+        self.sim._p2g_phase(solver)
+
+    def level0(self, solver):
+        self.sim._level0_coupled(solver)
+
+    def post(self, solver):
+        self.sim._g2p_phase(solver)

@@ -17,6 +17,7 @@
 // outlet/inlet passes in reference face order through shared memory.
 #include <algorithm>
 #include "common.cuh"
+#include "exchange.cuh"
 
 namespace mlbm {
 
@@ -241,6 +242,7 @@ struct StepArgs {
     mlbm_collide_t cp;
     mlbm_bc_t bc;
     mlbm_error_t* err;
+    ExchArgs ex;          // mode 5 only: the level-0 exchange between stream and collide
 };
 
 template <int D, int I, typename R>
@@ -788,14 +790,15 @@ template <int D, typename R> struct LevelCfg {
 #endif
 template <int D, typename R, int MODE>
 __global__ void __launch_bounds__(LevelCfg<D, R>::THREADS,
-                                  (D == 3 && sizeof(R) == 4 && MODE <= 1) ? LEVEL_MINB : 1)
+                                  (D == 3 && sizeof(R) == 4 && (MODE <= 1 || MODE == 5)) ? LEVEL_MINB : 1)
 level_kernel(const StepArgs A) {
     constexpr int T = Geo<D>::T, Q = Geo<D>::Q, NS = Geo<D>::NS, NM = Geo<D>::NM;
     constexpr int TPC = LevelCfg<D, R>::TPC;
     constexpr int HB = HaloTable<D>::HB, NCO = CoefSlots<D>::N;
     __shared__ R fbuf_all[TPC][Q * T];
     // halo coefficient staging: 2D only (3D evaluates its halo in registers)
-    constexpr bool HC = MODE <= 1 && D == 2;
+    constexpr bool STREAM = MODE <= 1 || MODE == 5;      // pull-stream first
+    constexpr bool HC = STREAM && D == 2;
     __shared__ R hcoef_all[HC ? TPC : 1][HC ? NCO * HB : 1];
     __shared__ int snb_all[TPC][Geo<D>::NB];
 
@@ -808,7 +811,7 @@ level_kernel(const StepArgs A) {
     const FieldsT<R> src = fields_of<R>(A.src), dst = fields_of<R>(A.dst);
     const R h3xyz = R(A.cp.h3_xyz);
 
-    if (MODE <= 1 && valid && lc < Geo<D>::NB) snb[lc] = A.lv.nbr[(int64_t)tile * Geo<D>::NB + lc];
+    if (STREAM && valid && lc < Geo<D>::NB) snb[lc] = A.lv.nbr[(int64_t)tile * Geo<D>::NB + lc];
 
     const int64_t cell = (int64_t)tile * T + lc;
     int l[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
@@ -828,7 +831,7 @@ level_kernel(const StepArgs A) {
     }
 
     R dr, mm[D], pi[NS];
-    if constexpr (MODE <= 1 && D == 3) {
+    if constexpr (STREAM && D == 3) {
         // eps / phi ride along to the write tree: fetch them now so the
         // loads overlap the stream instead of stalling the epilogue
         R eps_c = R(0), phi_c = R(0);
@@ -862,7 +865,7 @@ level_kernel(const StepArgs A) {
             }
             return;
         }
-    } else if constexpr (MODE <= 1) {
+    } else if constexpr (STREAM) {
         Coef<D, R> own;
         if (valid) {
             R m[NM];
@@ -907,6 +910,16 @@ level_kernel(const StepArgs A) {
         }
     }
 
+    // mode 5: every cell's eps (raw eta, the read tree's phi) staged per tile
+    // for the exchange's grad eps (in-tile neighbours from shared memory)
+    __shared__ R seps_all[MODE == 5 ? TPC : 1][MODE == 5 ? T : 1];
+    if constexpr (MODE == 5) {
+        if (valid)
+            seps_all[grp][lc] = eps_of<D, R>((const R*)A.ex.ras, A.ex.rs, fields_of<R>(A.ex.r_tree), cell,
+                                             R(A.ex.eps_min));
+        __syncthreads();
+    }
+
     // ---- collide (solver.py:394-453) -------------------------------------
     R out[NM];
     if (MODE == 4 && valid) {
@@ -916,12 +929,21 @@ level_kernel(const StepArgs A) {
 #pragma unroll
         for (int k = 0; k < NS; ++k) out[1 + D + k] = pi[k];
     }
+    R eps5 = R(1);
     if (MODE != 4 && valid) {
         const R rho = R(1) + dr;
         if (active && !(rho > R(0) && isfinite((double)rho)))
             report_error(A.err, MLBM_ERR_DENSITY, A.lv.level, gx[0], gx[1], gx[2]);
         R F[D];
-        if (A.cp.force_mode == 0) {
+        if constexpr (MODE == 5) {
+            // the coupling hook between stream and collide (coupling.py:403-446):
+            // fractions, drag, grad eps, mixture force and the MPM grid update of
+            // this cell from its bare post-stream moments (in registers)
+            R u5[D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) u5[a] = mm[a] / rho;
+            exchange_cell<D, R>(A.ex, cell, gx, rho, u5, F, eps5, seps_all[grp]);
+        } else if (A.cp.force_mode == 0) {
             const R sc = R(1 << A.lv.level);
 #pragma unroll
             for (int a = 0; a < D; ++a) F[a] = rho * (R(A.cp.gravity[a]) * sc);
@@ -929,7 +951,8 @@ level_kernel(const StepArgs A) {
 #pragma unroll
             for (int a = 0; a < D; ++a) F[a] = dst.at(fi_f<D>(a), cell);
         }
-        const R tau = A.cp.tau_mode == 0 ? R(A.cp.tau)
+        const R tau = MODE == 5 ? eps5 * R(A.cp.tau0)
+                    : A.cp.tau_mode == 0 ? R(A.cp.tau)
                     : A.cp.tau_mode == 1 ? dst.at(fi_eps<D>(), cell) * R(A.cp.tau0)
                                          : ((const R*)A.cp.tau_ptr)[cell];
         const R inv_rho = R(1) / rho;
@@ -1014,7 +1037,9 @@ level_kernel(const StepArgs A) {
     if (valid && (MODE != 4 || (tf & MLBM_TF_BC))) {
 #pragma unroll
         for (int k = 0; k < NM; ++k) dst.at(k, cell) = out[k];
-        if ((MODE == 0 || !active) && MODE != 4) {
+        if constexpr (MODE == 5) {
+            dst.at(fi_phi<D>(), cell) = src.at(fi_phi<D>(), cell);   // eps: written by the exchange
+        } else if ((MODE == 0 || !active) && MODE != 4) {
             dst.at(fi_eps<D>(), cell) = src.at(fi_eps<D>(), cell);
             dst.at(fi_phi<D>(), cell) = src.at(fi_phi<D>(), cell);
         }
@@ -1031,7 +1056,8 @@ int launch_level(const StepArgs& a, int mode, cudaStream_t s) {
     case 1: level_kernel<D, R, 1><<<blocks, NT, 0, s>>>(a); break;
     case 2: level_kernel<D, R, 2><<<blocks, NT, 0, s>>>(a); break;
     case 3: level_kernel<D, R, 3><<<blocks, NT, 0, s>>>(a); break;
-    default: level_kernel<D, R, 4><<<blocks, NT, 0, s>>>(a); break;
+    case 4: level_kernel<D, R, 4><<<blocks, NT, 0, s>>>(a); break;
+    default: level_kernel<D, R, 5><<<blocks, NT, 0, s>>>(a); break;
     }
     return launch_status(1);
 }
@@ -1151,7 +1177,7 @@ extern "C" int mlbm_level_step(const mlbm_level_t* lv, mlbm_fields_t src, mlbm_f
                                int32_t dtype, int32_t mode, const mlbm_collide_t* cp,
                                const mlbm_bc_t* bc, mlbm_error_t* err, void* stream) {
     if (!lv || !cp || !bc || mode < 0 || mode > 4) return -1;
-    StepArgs a{*lv, src, dst, *cp, *bc, err};
+    StepArgs a{*lv, src, dst, *cp, *bc, err, ExchArgs{}};
     cudaStream_t s = as_stream(stream);
     if (lv->dim == 2) return dtype ? launch_level<2, double>(a, mode, s) : launch_level<2, float>(a, mode, s);
     if (lv->dim == 3) return dtype ? launch_level<3, double>(a, mode, s) : launch_level<3, float>(a, mode, s);
@@ -1192,4 +1218,27 @@ extern "C" int mlbm_upward(int32_t dim, int32_t n, const int32_t* n_dev, const i
     else return -1;
 #undef UP
     return launch_status(1);
+}
+
+extern "C" int mlbm_level0_coupled(const mlbm_level_t* lv, mlbm_fields_t src, mlbm_fields_t dst,
+                                   mlbm_fields_t tree0, mlbm_fields_t tree1, int32_t dtype,
+                                   const mlbm_collide_t* cp, const mlbm_bc_t* bc, void* ras, int64_t rs,
+                                   double eps_min, double nu, double d_p, double re_min, double dt,
+                                   double rho0, const double* g_fluid, const double* g_sed,
+                                   const int32_t* faces, double floor_friction, mlbm_error_t* err,
+                                   void* stream) {
+    if (!lv || !cp || !bc || lv->level != 0) return -1;
+    StepArgs a{*lv, src, dst, *cp, *bc, err, ExchArgs{}};
+    ExchArgs& A = a.ex;
+    A.lv = *lv; A.w_tree = dst; A.r_tree = src; A.tree0 = tree0; A.tree1 = tree1;
+    A.ras = ras; A.rs = rs; A.eps_min = eps_min; A.nu = nu; A.d_p = d_p; A.re_min = re_min;
+    A.dt = dt; A.rho0 = rho0;
+    for (int q = 0; q < 3; ++q) { A.g_fluid[q] = g_fluid[q]; A.g_sed[q] = g_sed[q]; }
+    for (int f = 0; f < 6; ++f) A.face[f] = faces[f];
+    A.floor_friction = floor_friction;
+    A.mode = 1;
+    cudaStream_t s = as_stream(stream);
+    if (lv->dim == 2) return dtype ? launch_level<2, double>(a, 5, s) : launch_level<2, float>(a, 5, s);
+    if (lv->dim == 3) return dtype ? launch_level<3, double>(a, 5, s) : launch_level<3, float>(a, 5, s);
+    return -1;
 }

@@ -17,21 +17,13 @@
 // ~1e-8 absolute resolution); everything else follows the run dtype.
 #include <algorithm>
 #include <cstdlib>
-#include <cub/cub.cuh>
 #include "common.cuh"
+#include "exchange.cuh"
 
 namespace mlbm {
 
 // raster row layout over level-0 cells
-template <int D> struct Rows {
-    static constexpr int MASS = 0, MOM = 1, FINT = 1 + D, ETA = 1 + 2 * D, AREA = 2 + 2 * D,
-                         VMOM = 3 + 2 * D, VEL = 3 + 3 * D, FS = 3 + 4 * D, EPS = 3 + 5 * D,
-                         GRAD = 4 + 5 * D, REL = 4 + 6 * D, SIG = 4 + 7 * D,
-                         // eta_eff = max(eta - phi, 0) (coupling.py:127) in its own
-                         // row: k_exchange's neighbour eps reads the raw ETA row
-                         ETAE = 4 + 7 * D + Geo<D>::NS,
-                         N = 5 + 7 * D + Geo<D>::NS, NACC = 3 + 3 * D;
-};
+
 // particle row layout (after the float64 positions): v[D] C[D*D] F[D*D] m V0 vc
 // TAU: the Kirchhoff stress tau(F) (granular.py:260-279, symmetric, NS rows)
 // of the particle's current F, written by G2P from its own decomposition of the
@@ -47,7 +39,6 @@ struct TopoL0 {
     const int32_t* tile_map;
 };
 
-MLBM_HD int64_t g3(const int* d, int x, int y, int z) { return ((int64_t)x * d[1] + y) * d[2] + z; }
 
 // periodic wrap of a coordinate that is almost always within one period of
 // the domain (stencil / box nodes): compare-and-add, modulo only otherwise
@@ -516,171 +507,30 @@ __global__ void __launch_bounds__(128) k_p2g(PartArgs P, TopoL0 t0, MatParams mp
 }
 
 // ---------------------------------------------------------------------------
-struct ExchArgs {
-    mlbm_level_t lv;          // level 0
-    mlbm_fields_t w_tree, r_tree;   // level-0 write (post-stream) / read trees
-    mlbm_fields_t tree0, tree1;     // both trees (eps / force written into both)
-    void* ras;
-    int64_t rs;
-    double eps_min, nu, d_p, re_min, dt, rho0;
-    double g_fluid[3], g_sed[3];
-    int32_t face[6];
-    double floor_friction;
-    int32_t mode;             // 1 exchange (drag + force + grid update), 0 grid update only
-};
-
-template <int D, typename R>
-__device__ __forceinline__ R eps_of(const R* ras, int64_t rs, const FieldsT<R>& rt, int64_t c, R eps_min) {
-    const R phi = rt.at(fi_phi<D>(), c);
-    R eta = ras[Rows<D>::ETA * rs + c] - phi;
-    eta = eta > R(0) ? eta : R(0);
-    R e = R(1) - eta - phi;
-    e = e < eps_min ? eps_min : (e > R(1) ? R(1) : e);
-    return e;
-}
-
-// Di Felice drag on the sediment of one cell (coupling.py:134-156): rel =
-// u - v_cell, Re = max(eps |rel| d_p / nu, re_min), C_d, chi, f_s
-template <int D, typename R>
-__device__ __forceinline__ void difelice_cell(R eps, R rho, const R (&rel)[D], R speed, R area, R d_p,
-                                              R nu, R re_min, R (&fs)[D]) {
-    for (int a = 0; a < D; ++a) fs[a] = R(0);
-    if (!(area > R(0) && speed > R(0))) return;
-    R re = eps * speed * d_p / nu;
-    re = re > re_min ? re : re_min;
-    const R cd = (R(0.63) + R(4.8) / sqrt(re)) * (R(0.63) + R(4.8) / sqrt(re));
-    const R lg = R(1.5) - log10(re);
-    const R chi = R(3.7) - R(0.65) * exp(R(-0.5) * lg * lg);
-    const R coef = R(0.5) * cd * pow(eps, -chi) * rho * area * speed;
-    for (int a = 0; a < D; ++a) fs[a] = coef * rel[a];
-}
-
-// smooth drag limiter (CoupledSim._limit_drag, coupling.py:379-401)
-template <int D, typename R>
-__device__ __forceinline__ void limit_drag_cell(R (&fs)[D], R rho, R mass, R speed, R dt) {
-    R mag2 = R(0);
-    for (int a = 0; a < D; ++a) mag2 += fs[a] * fs[a];
-    const R mag = sqrt(mag2);
-    if (!(mag > R(0))) return;
-    const R inv_m = R(1) / rho + R(1) / (mass > R(1e-12) ? mass : R(1e-12));
-    const R beta = mag * dt * inv_m / (speed > R(1e-14) ? speed : R(1e-14));
-    R over = beta - R(0.5);
-    over = over > R(0) ? over : R(0);
-    const R real = (beta < R(0.5) ? beta : R(0.5)) + over / (R(1) + over);
-    const R scale = real / (beta > R(1e-14) ? beta : R(1e-14));
-    for (int a = 0; a < D; ++a) fs[a] *= scale;
-}
-
-// central differences of a level-0 cell field (coupling.py:159-182): the
-// neighbour wraps (periodic) or clamps to the domain; a neighbour that is
-// not stored counts as the cell itself.  val(ni) returns the field at cell ni.
-template <int D, typename R, typename F>
-__device__ __forceinline__ void grad_cell(const mlbm_level_t& lv, const int (&g)[3], int64_t c, F val,
-                                          R (&grad)[D]) {
-    constexpr int T = Geo<D>::T;
-    for (int a = 0; a < D; ++a) {
-        R pm[2];
-        for (int sgn = 0; sgn < 2; ++sgn) {
-            int nb[3] = {g[0], g[1], g[2]};
-            nb[a] += sgn == 0 ? 1 : -1;
-            if (lv.periodic[a]) nb[a] = (nb[a] + lv.cells[a]) % lv.cells[a];
-            else nb[a] = nb[a] < 0 ? 0 : (nb[a] >= lv.cells[a] ? lv.cells[a] - 1 : nb[a]);
-            const int s = lv.tile_map[g3(lv.tiles, nb[0] >> 2, nb[1] >> 2, D == 3 ? nb[2] >> 2 : 0)];
-            const int64_t ni = s >= 0 ? (int64_t)s * T + local_of<D>(nb[0] & 3, nb[1] & 3, nb[2] & 3) : c;
-            pm[sgn] = val(ni);
-        }
-        grad[a] = R(0.5) * (pm[0] - pm[1]);
-    }
-}
-
 #ifndef EXCH_MINB
 #define EXCH_MINB 16
 #endif
 template <int D, typename R>
 __global__ void __launch_bounds__(128, sizeof(R) == 4 ? EXCH_MINB : 1) k_exchange(ExchArgs A) {
     constexpr int T = Geo<D>::T;
-    using RW = Rows<D>;
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= (int64_t)live_tiles(A.lv) * T) return;
-    R* ras = (R*)A.ras;
-    const int64_t rs = A.rs;
-    const FieldsT<R> wt = fields_of<R>(A.w_tree), rt = fields_of<R>(A.r_tree);
     const int slot = (int)(c / T), lc = (int)(c % T);
     const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
     int g[3] = {0, 0, 0};
     for (int a = 0; a < D; ++a) g[a] = A.lv.tile_xyz[slot * 3 + a] * 4 + l3[a];
-    const R mass = ras[RW::MASS * rs + c];
-    R fs[D];
-    for (int a = 0; a < D; ++a) fs[a] = A.mode == 1 ? R(0) : ras[(RW::FS + a) * rs + c];
-    const R eps_min = R(A.eps_min);
     if (A.mode == 1) {
-        const R eps = eps_of<D, R>(ras, rs, rt, c, eps_min);
-        R eta = ras[RW::ETA * rs + c] - rt.at(fi_phi<D>(), c);
-        eta = eta > R(0) ? eta : R(0);
-        R vcell[D];
-        for (int a = 0; a < D; ++a) vcell[a] = mass > R(0) ? ras[(RW::VMOM + a) * rs + c] / mass : R(0);
+        // the bare post-stream moments of the write tree
+        const FieldsT<R> wt = fields_of<R>(A.w_tree);
         const R rho = R(1) + wt.at(0, c);
-        R u[D], rel[D], sp2 = R(0);
-        for (int a = 0; a < D; ++a) {
-            u[a] = wt.at(1 + a, c) / rho;
-            rel[a] = u[a] - vcell[a];
-            sp2 += rel[a] * rel[a];
-        }
-        const R speed = sqrt(sp2);
-        const R area = ras[RW::AREA * rs + c];
-        difelice_cell<D, R>(eps, rho, rel, speed, area, R(A.d_p), R(A.nu), R(A.re_min), fs);
-        if (area > R(0) && speed > R(0)) limit_drag_cell<D, R>(fs, rho, mass, speed, R(A.dt));
-        // grad eps: the neighbours' eps from the raw eta (never overwritten here)
-        R grad[D];
-        grad_cell<D, R>(A.lv, g, c, [&](int64_t ni) { return eps_of<D, R>(ras, rs, rt, ni, eps_min); },
-                        grad);
-        const R coefg = (rho - R(A.rho0)) / eps;
-        const FieldsT<R> t0 = fields_of<R>(A.tree0), t1 = fields_of<R>(A.tree1);
-        for (int a = 0; a < D; ++a) {
-            const R gt = coefg * grad[a];
-            const R force = gt + rho * R(A.g_fluid[a]) - fs[a];
-            t0.at(fi_f<D>(a), c) = force;
-            t1.at(fi_f<D>(a), c) = force;
-            ras[(RW::GRAD + a) * rs + c] = gt;
-            ras[(RW::REL + a) * rs + c] = rel[a];
-            ras[(RW::FS + a) * rs + c] = fs[a];
-            ras[(RW::VMOM + a) * rs + c] = vcell[a];   // becomes the cell velocity
-        }
-        t0.at(fi_eps<D>(), c) = eps;
-        t1.at(fi_eps<D>(), c) = eps;
-        ras[RW::EPS * rs + c] = eps;
-        ras[RW::ETAE * rs + c] = eta;                  // eta_eff (ETA stays raw: neighbours read it)
-    }
-    // MPM grid update (granular.py:313-341)
-    R vel[D];
-    if (mass > R(0)) {
-        const R inv_m = R(1) / mass;
-        for (int a = 0; a < D; ++a)
-            vel[a] = (ras[(RW::MOM + a) * rs + c] + R(A.dt) * (ras[(RW::FINT + a) * rs + c] + fs[a])) * inv_m
-                     + R(A.dt) * R(A.g_sed[a]);
+        R u[D], force[D], eps;
+        for (int a = 0; a < D; ++a) u[a] = wt.at(1 + a, c) / rho;
+        exchange_cell<D, R>(A, c, g, rho, u, force, eps);
     } else {
-        for (int a = 0; a < D; ++a) vel[a] = R(0);
+        R fs[D];
+        for (int a = 0; a < D; ++a) fs[a] = ((const R*)A.ras)[(Rows<D>::FS + a) * A.rs + c];
+        grid_update_cell<D, R>(A, c, g, fs);
     }
-    for (int f = 0; f < 2 * D; ++f) {
-        if (A.face[f] != MLBM_FACE_WALL) continue;
-        const int axis = f >> 1;
-        const bool lo = (f & 1) == 0;
-        const bool in_band = lo ? g[axis] <= 1 : g[axis] >= A.lv.cells[axis] - 2;
-        if (!in_band) continue;
-        const R sgn = lo ? R(1) : R(-1);
-        const R vn = sgn * vel[axis];
-        if (!(vn < R(0))) continue;
-        R vt2 = R(0);
-        for (int b = 0; b < D; ++b) if (b != axis) vt2 += vel[b] * vel[b];
-        const R vtn = sqrt(vt2);
-        R scale = R(1) - R(A.floor_friction) * (-vn) / (vtn > R(1e-14) ? vtn : R(1e-14));
-        scale = scale > R(0) ? scale : R(0);
-        vel[axis] = R(0);
-        for (int b = 0; b < D; ++b) if (b != axis) vel[b] *= scale;
-    }
-    if (A.lv.cell_flags[c] & MLBM_CF_SOLID)
-        for (int a = 0; a < D; ++a) vel[a] = R(0);
-    for (int a = 0; a < D; ++a) ras[(RW::VEL + a) * rs + c] = vel[a];
 }
 
 // ---------------------------------------------------------------------------
@@ -836,6 +686,9 @@ __global__ void k_particle_stress(int n, R* pp, int64_t ps, MatParams mp) {
 #ifndef G2P_BT
 #define G2P_BT 128      // particles (threads) per block: one node box per block
 #endif
+#ifndef G2P_EARLY
+#define G2P_EARLY 0     // 1: ride-along rows loaded before the node-box staging (measured +4 % on C4)
+#endif
 template <int D, typename R>
 __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(PartArgs P, TopoL0 t0, MatParams mp, const R* ras, int64_t rs,
                                              double dt, int plastic, int32_t* clamped, mlbm_error_t* err) {
@@ -857,6 +710,18 @@ __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(P
     for (int a = 0; a < D; ++a) x[a] = live ? P.x[a * P.ps + p] : 0.5 * t0.cells[a];
     Stencil<D, R> st;
     make_stencil<D, R>(x, st);
+#if G2P_EARLY
+    // rows that only ride along (F, vc, m, V0, id): issued before the node-box
+    // staging so their latency overlaps it and the gather
+    R Fpre[D * D];
+    const bool copy_rows = pw != pp;
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) Fpre[k] = live ? pp[(PR::F + k) * P.ps + p] : R(1);
+    const R vc_pre = live ? pp[PR::VC * P.ps + p] : R(0);
+    const R m_pre = copy_rows && live ? pp[PR::M * P.ps + p] : R(0);
+    const R v0_pre = copy_rows && live ? pp[PR::V0 * P.ps + p] : R(0);
+    const int32_t id_pre = P.pidw && live ? P.pid[p] : 0;
+#endif
     if (threadIdx.x < 3) { s_lo[threadIdx.x] = 0x7fffffff; s_hi[threadIdx.x] = -0x7fffffff; }
     __syncthreads();
 #pragma unroll
@@ -882,6 +747,7 @@ __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(P
     }
     __syncthreads();
     if (!live) return;
+#if !G2P_EARLY
     // rows that only ride along (F, vc, m, V0, id): loaded now so their
     // latency overlaps the gather instead of stalling the epilogue
     R Fpre[D * D];
@@ -892,6 +758,7 @@ __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(P
     const R m_pre = copy_rows ? pp[PR::M * P.ps + p] : R(0);
     const R v0_pre = copy_rows ? pp[PR::V0 * P.ps + p] : R(0);
     const int32_t id_pre = P.pidw ? P.pid[p] : 0;
+#endif
     R v[D], B[D * D];
 #pragma unroll
     for (int a = 0; a < D; ++a) v[a] = R(0);
@@ -2202,19 +2069,33 @@ __global__ void __launch_bounds__(32 * NW, P2G2_MIN_BLOCKS) k_p2g_cell2(PartArgs
     if (threadIdx.x < 3) { s_lo[threadIdx.x] = 0x7fffffff; s_hi[threadIdx.x] = -0x7fffffff; }
     __syncthreads();
     int wl[3] = {0, 0, 0}, wh[3] = {0, 0, 0};        // this warp's node box
+    // the warp's fixed window for blocks whose box overflows: the tile (x, y)
+    // of its middle particle, and in z the layer pair the warp's particles
+    // vote for; runs outside it (drifted particles) take global atomics
+    int bm[3] = {0, 0, 0};
+    int zup = 0, zdown = 0;
+    {
+        const int pm = min(p0 + (wid * ROUNDS + ROUNDS / 2) * 32 + 16, P.n - 1);
+#pragma unroll
+        for (int a = 0; a < D; ++a) bm[a] = (int)floor(P.x[a * P.ps + pm] - 0.5);
+    }
     {
         int bl[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, bh[3] = {-0x7fffffff, -0x7fffffff, -0x7fffffff};
 #pragma unroll
         for (int r = 0; r < ROUNDS; ++r) {
-            const int p = p0 + r * BT + threadIdx.x;
+            const int p = p0 + (wid * ROUNDS + r) * 32 + lane;   // this warp's chunk r
+            int bz = bm[D - 1];
             if (p < P.n) {
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
                     const int b = (int)floor(P.x[a * P.ps + p] - 0.5);
                     bl[a] = min(bl[a], b);
                     bh[a] = max(bh[a], b + 2);
+                    if (a == D - 1) bz = b;
                 }
             }
+            zup += __popc(__ballot_sync(0xffffffffu, bz == bm[D - 1] + 1));
+            zdown += __popc(__ballot_sync(0xffffffffu, bz == bm[D - 1] - 1));
         }
 #pragma unroll
         for (int a = 0; a < D; ++a) {
@@ -2230,28 +2111,24 @@ __global__ void __launch_bounds__(32 * NW, P2G2_MIN_BLOCKS) k_p2g_cell2(PartArgs
 #pragma unroll
     for (int a = 0; a < D; ++a) { lo[a] = s_lo[a]; ext[a] = s_hi[a] - s_lo[a] + 1; nbox *= ext[a]; }
     const bool use_smem = nbox > 0 && nbox <= MAXN;        // block-uniform
-    // a block whose box is too large (particles drifted since the last sort)
-    // falls back to per-warp boxes in the same per-warp copies (warp-uniform)
-    // before resorting to per-run global atomics
-    bool warp_box = false;
-    if (!use_smem) {
-        int nw = 1;
-        bool okw = true;
-#pragma unroll
-        for (int a = 0; a < D; ++a) { okw &= wl[a] <= wh[a]; nw *= wh[a] - wl[a] + 1; }
-        warp_box = okw && nw <= MAXN;
-        if (warp_box) {
-#pragma unroll
-            for (int a = 0; a < D; ++a) { lo[a] = wl[a]; ext[a] = wh[a] - wl[a] + 1; }
-            nbox = nw;
-            constexpr int RP = MAXN / 4 <= 32 ? 32 : (MAXN / 4 <= 64 ? 64 : 128);
-            const int n4 = (nbox + 3) >> 2;
-            float4* s4 = reinterpret_cast<float4*>(sacc + wid * NV * MAXN);
-            for (int i = lane; i < NV * RP; i += 32) {
-                const int row = i / RP, c4 = i % RP;
-                if (c4 < n4) s4[row * (MAXN / 4) + c4] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
+    // a block whose box is too large (particles drifted since the last sort, a
+    // tile run ends) accumulates per warp in its own copy over a fixed window
+    // (the warp's tile in x, y; two z layers); runs outside it add to HBM
+    // directly
+    const bool warp_box = !use_smem;
+    if (warp_box) {
+        constexpr int EX = D == 3 ? 6 : 10, EZ = D == 3 ? 4 : 1;
+        static_assert(EX * EX * EZ <= MAXN, "warp window fits a per-warp copy");
+        if constexpr (D == 3) {
+            lo[0] = bm[0] & ~3; lo[1] = bm[1] & ~3; lo[2] = zup >= zdown ? bm[2] : bm[2] - 1;
+            ext[0] = EX; ext[1] = EX; ext[2] = EZ;
+        } else {
+            lo[0] = (bm[0] & ~3) - 2; lo[1] = (bm[1] & ~3) - 2;
+            ext[0] = EX; ext[1] = EX;
         }
+        nbox = EX * EX * EZ;
+        float4* s4 = reinterpret_cast<float4*>(sacc + wid * NV * MAXN);
+        for (int i = lane; i < NV * MAXN / 4; i += 32) s4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     if (use_smem) {
         // zero the [NW * NV rows][nbox] box copies as float4, iterating over a
@@ -2289,7 +2166,12 @@ __global__ void __launch_bounds__(32 * NW, P2G2_MIN_BLOCKS) k_p2g_cell2(PartArgs
     constexpr int NREC4 = (OP + D * D + 3) / 4;
 #pragma unroll 1
     for (int rd = 0; rd < ROUNDS; ++rd) {
-        const int pw = p0 + rd * BT + wid * 32;           // first particle of this warp's chunk
+        // warp w owns the consecutive chunks w * ROUNDS .. w * ROUNDS + ROUNDS - 1:
+        // its particles are contiguous in the sorted order, so its node box
+        // stays small when the block box overflows (-1 % on C4 against
+        // interleaved chunks; a sliding per-warp box instead of the per-run
+        // atomic fallback measured +9 %)
+        const int pw = p0 + (wid * ROUNDS + rd) * 32;     // first particle of this warp's chunk
         const int nj = min(32, P.n - pw);
         if (nj <= 0) break;                               // warp-uniform
         const int p = pw + lane;
@@ -2373,9 +2255,14 @@ __global__ void __launch_bounds__(32 * NW, P2G2_MIN_BLOCKS) k_p2g_cell2(PartArgs
                     acc[3 + 2 * D + a] = fmaf(w, r[OMV + a], acc[3 + 2 * D + a]);
                 }
             }
+            bool inbox = true;                                   // warp-uniform
+            if (warp_box) {
+    #pragma unroll
+                for (int a = 0; a < D; ++a) inbox &= cur[a] >= lo[a] && cur[a] + 2 < lo[a] + ext[a];
+            }
             if (node_lane && (acc[0] != 0.f || acc[2 + 2 * D] != 0.f)) {
                 int c[3] = {cur[0] + o[0], cur[1] + o[1], D == 3 ? cur[2] + o[2] : 0};
-                if (use_smem || warp_box) {
+                if (inbox) {
                     int li = 0;
     #pragma unroll
                     for (int a = D - 1; a >= 0; --a) li = li * ext[a] + (c[a] - lo[a]);
@@ -2711,14 +2598,96 @@ extern "C" int mlbm_p2g(const mlbm_level_t* lv0, int32_t n, const double* x, voi
     return launch_status(1);
 }
 
-extern "C" int64_t mlbm_sort_ws_bytes(int64_t n) {
+// ---------------------------------------------------------------------------
+// Particle sort by (level-0 tile slot, cell) without a library sort: a
+// bucketed counting sort keyed by the live tile slot —
+//   k_sort_keys     key = slot * T + cell of the stencil base (invalid: last bucket)
+//   k_slot_hist     per-slot counts (atomics; sorted input hits few addresses)
+//   scan            exclusive scan of the slot counts (the compaction scan of
+//                   topology.cu, mlbm_scan_i32)
+//   k_slot_scatter  particles into their slot's range
+//   k_cell_sort     one CTA per slot: counting sort of its range by cell
+//                   (shared-memory histogram + scan over the 4^D cells)
+//   k_gather        every particle row into the sorted order
+// Order inside a cell: by the particle's index before the sort (deterministic).
+extern "C" int mlbm_scan_i32(int32_t n, int32_t* data, int32_t* total, void* ws, int64_t ws_bytes,
+                             void* stream);
+extern "C" int64_t mlbm_scan_ws_bytes(int32_t n);
+
+// warp-aggregated: lanes with the same slot (sorted input: usually the whole
+// warp) share one atomic; a lane's rank is its order among them
+__global__ void k_slot_hist(int n, const uint32_t* __restrict__ keys, int tshift, int nslot,
+                            int32_t* __restrict__ hist) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t k = p < n ? keys[p] : 0xfffffffeu;
+    const int slot = k == 0xffffffffu ? nslot - 1 : (int)(k >> tshift);
+    const unsigned peers = __match_any_sync(0xffffffffu, p < n ? slot : -1);
+    const int lane = threadIdx.x & 31;
+    if (p < n && (__ffs(peers) - 1) == lane) atomicAdd(&hist[slot], __popc(peers));
+}
+
+__global__ void k_slot_scatter(int n, const uint32_t* __restrict__ keys, int tshift, int nslot,
+                               const int32_t* __restrict__ start, int32_t* __restrict__ fill,
+                               int32_t* __restrict__ perm, uint8_t* __restrict__ cell) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t k = p < n ? keys[p] : 0xfffffffeu;
+    const bool bad = k == 0xffffffffu;
+    const int slot = bad ? nslot - 1 : (int)(k >> tshift);
+    const unsigned peers = __match_any_sync(0xffffffffu, p < n ? slot : -1);
+    const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+    int base = 0;
+    if (p < n && lane == leader) base = atomicAdd(&fill[slot], __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    if (p >= n) return;
+    const int pos = start[slot] + base + __popc(peers & ((1u << lane) - 1u));
+    perm[pos] = p;
+    cell[pos] = bad ? 0 : (uint8_t)(k & ((1u << tshift) - 1u));
+}
+
+template <int T>
+__global__ void k_cell_sort(int nslot, const int32_t* __restrict__ start, const int32_t* __restrict__ perm_in,
+                            const uint8_t* __restrict__ cell, int32_t* __restrict__ perm_out, int n) {
+    __shared__ int cnt[T], off[T];
+    const int slot = blockIdx.x;
+    const int a = start[slot], b = slot + 1 < nslot ? start[slot + 1] : n;
+    if (b - a <= 1) {
+        if (b - a == 1 && threadIdx.x == 0) perm_out[a] = perm_in[a];
+        return;
+    }
+    for (int c = threadIdx.x; c < T; c += blockDim.x) cnt[c] = 0;
+    __syncthreads();
+    for (int i = a + threadIdx.x; i < b; i += blockDim.x) atomicAdd(&cnt[cell[i]], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int c = 0; c < T; ++c) { off[c] = t; t += cnt[c]; cnt[c] = 0; }
+    }
+    __syncthreads();
+    for (int i = a + threadIdx.x; i < b; i += blockDim.x) {
+        const int c = cell[i];
+        perm_out[a + off[c] + atomicAdd(&cnt[c], 1)] = perm_in[i];
+    }
+    __syncthreads();
+    // deterministic order: each cell's particles by their index before the
+    // sort (insertion sort of a few entries per cell, one thread per cell)
+    for (int c = threadIdx.x; c < T; c += blockDim.x) {
+        const int lo = a + off[c], hi = lo + cnt[c];
+        for (int i = lo + 1; i < hi; ++i) {
+            const int v = perm_out[i];
+            int j = i - 1;
+            while (j >= lo && perm_out[j] > v) { perm_out[j + 1] = perm_out[j]; --j; }
+            perm_out[j + 1] = v;
+        }
+    }
+}
+
+static int64_t al256(int64_t v) { return (v + 255) & ~(int64_t)255; }
+
+extern "C" int64_t mlbm_sort_ws_bytes(int64_t n, int64_t n_slots) {
     if (n < 1) n = 1;
-    size_t b = 0;
-    uint32_t* k = nullptr;
-    int32_t* v = nullptr;
-    cub::DeviceRadixSort::SortPairs(nullptr, b, k, k, v, v, (int)n);
-    auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
-    return 4 * al(4 * n) + al((int64_t)b);
+    const int64_t ns = n_slots + 1;
+    // keys, perm, perm2 (n int32 each), cell (n bytes), hist, fill (ns int32), scan ws
+    return 3 * al256(4 * n) + al256(n) + 2 * al256(4 * ns) + al256(mlbm_scan_ws_bytes((int32_t)ns)) + 256;
 }
 
 extern "C" int mlbm_particle_sort(const mlbm_level_t* lv0, int32_t n, const double* x, const void* p,
@@ -2726,26 +2695,33 @@ extern "C" int mlbm_particle_sort(const mlbm_level_t* lv0, int32_t n, const doub
                                   int32_t* pid_out, int32_t dtype, void* ws, int64_t ws_bytes,
                                   void* stream) {
     if (n <= 0) return 0;
-    if (ws_bytes < mlbm_sort_ws_bytes(n)) return -1;
-    auto al = [](int64_t v) { return (v + 255) & ~(int64_t)255; };
+    const int nslot = lv0->n_tiles + 1;           // capacity slots + the invalid bucket
+    if (ws_bytes < mlbm_sort_ws_bytes(n, lv0->n_tiles)) return -1;
     char* w = (char*)ws;
-    uint32_t* k0 = (uint32_t*)w;
-    uint32_t* k1 = (uint32_t*)(w + al(4 * (int64_t)n));
-    int32_t* v0 = (int32_t*)(w + 2 * al(4 * (int64_t)n));
-    int32_t* v1 = (int32_t*)(w + 3 * al(4 * (int64_t)n));
-    void* tmp = w + 4 * al(4 * (int64_t)n);
-    size_t tb = (size_t)(ws_bytes - 4 * al(4 * (int64_t)n));
+    uint32_t* keys = (uint32_t*)w;                 w += al256(4 * (int64_t)n);
+    int32_t* perm = (int32_t*)w;                   w += al256(4 * (int64_t)n);
+    int32_t* perm2 = (int32_t*)w;                  w += al256(4 * (int64_t)n);
+    uint8_t* cell = (uint8_t*)w;                   w += al256(n);
+    int32_t* hist = (int32_t*)w;                   w += al256(4 * (int64_t)nslot);
+    int32_t* fill = (int32_t*)w;                   w += al256(4 * (int64_t)nslot);
+    void* sws = w;
+    const int64_t sws_b = mlbm_scan_ws_bytes(nslot);
     cudaStream_t s = as_stream(stream);
     const TopoL0 t = topo0(lv0);
-    int bits = 1;
-    while (bits < 32 && ((int64_t)1 << bits) <= (int64_t)lv0->n_tiles * (lv0->dim == 2 ? 16 : 64)) ++bits;
-    if (lv0->dim == 2) k_sort_keys<2><<<nblk(n, 256), 256, 0, s>>>(n, x, ps, t, k0, v0);
-    else k_sort_keys<3><<<nblk(n, 256), 256, 0, s>>>(n, x, ps, t, k0, v0);
-    cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, v1, n, 0, bits < 32 ? bits + 1 : 32, s);
+    const int tshift = lv0->dim == 2 ? 4 : 6;
+    if (lv0->dim == 2) k_sort_keys<2><<<nblk(n, 256), 256, 0, s>>>(n, x, ps, t, keys, perm2);
+    else k_sort_keys<3><<<nblk(n, 256), 256, 0, s>>>(n, x, ps, t, keys, perm2);
+    cudaMemsetAsync(hist, 0, 2 * al256(4 * (int64_t)nslot), s);       // hist + fill
+    k_slot_hist<<<nblk(n, 256), 256, 0, s>>>(n, keys, tshift, nslot, hist);
+    const int ks = mlbm_scan_i32(nslot, hist, nullptr, sws, sws_b, s);
+    if (ks < 0) return ks;
+    k_slot_scatter<<<nblk(n, 256), 256, 0, s>>>(n, keys, tshift, nslot, hist, fill, perm, cell);
+    if (lv0->dim == 2) k_cell_sort<16><<<nslot, 128, 0, s>>>(nslot, hist, perm, cell, perm2, n);
+    else k_cell_sort<64><<<nslot, 128, 0, s>>>(nslot, hist, perm, cell, perm2, n);
     const int rows = lv0->dim == 2 ? PRows<2>::N : PRows<3>::N;
-    if (dtype) k_gather_particles<double><<<nblk(n, 256), 256, 0, s>>>(n, rows, v1, x, lv0->dim, (const double*)p, pid, ps, x_out, (double*)p_out, pid_out);
-    else k_gather_particles<float><<<nblk(n, 256), 256, 0, s>>>(n, rows, v1, x, lv0->dim, (const float*)p, pid, ps, x_out, (float*)p_out, pid_out);
-    return launch_status(5);
+    if (dtype) k_gather_particles<double><<<nblk(n, 256), 256, 0, s>>>(n, rows, perm2, x, lv0->dim, (const double*)p, pid, ps, x_out, (double*)p_out, pid_out);
+    else k_gather_particles<float><<<nblk(n, 256), 256, 0, s>>>(n, rows, perm2, x, lv0->dim, (const float*)p, pid, ps, x_out, (float*)p_out, pid_out);
+    return launch_status(6 + ks);
 }
 
 extern "C" int mlbm_exchange(const mlbm_level_t* lv0, mlbm_fields_t w_tree, mlbm_fields_t r_tree,

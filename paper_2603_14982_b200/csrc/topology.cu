@@ -10,7 +10,6 @@
 // Integer work only (except migration / init): every pass is a coalesced
 // sweep over a dense uint8 tile grid or over the stored cells, bit-exact with
 // the reference by construction (no floating point decides topology).
-#include <cub/cub.cuh>
 #include "common.cuh"
 
 namespace mlbm {
@@ -57,47 +56,155 @@ __device__ bool solid_at(const mlbm_solid_t& s, int dim, const int (&g)[3]) {
 }
 
 // ---------------------------------------------------------------------------
-// compaction
-__global__ void k_kind_flags(int64_t n, const uint8_t* kind, int32_t* flags, int32_t* counts) {
-    int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (g == 0) counts[1] = 0;
-    if (g < n) flags[g] = kind[g] != 0;
+// ---------------------------------------------------------------------------
+// Stable stream compaction (no library scan): the flagged indices of [0, n) in
+// increasing order get consecutive positions.
+//   k_flag_count   per block of CB * CI elements: warp ballots + popc, one
+//                  block sum
+//   k_scan_blocks  one block: exclusive scan of the block sums (+ total)
+//   k_flag_scatter per block again: for each of the CI element strips the
+//                  ballot rank inside the warp + the warps before it (shared
+//                  scan) + the block offset give every flagged element its
+//                  position, and the writer functor is called for every element
+constexpr int CB = 256, CI = 4;          // 1024 elements per block
+constexpr int CPB = CB * CI;
+
+template <typename F>
+__global__ void k_flag_count(int64_t n, F flag, int32_t* __restrict__ bsum) {
+    __shared__ int ws[CB / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t base = (int64_t)blockIdx.x * CPB;
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < CI; ++k) {
+        const int64_t g = base + k * CB + threadIdx.x;
+        c += __popc(__ballot_sync(0xffffffffu, g < n && flag(g)));
+    }
+    if (lane == 0) ws[wid] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < CB / 32; ++w) t += ws[w];
+        bsum[blockIdx.x] = t;
+    }
 }
 
-__global__ void k_scatter_tiles(int64_t n, I3 td, const uint8_t* kind, const int32_t* pos,
-                                const int32_t* old_map, int32_t* tile_map, int32_t* tile_xyz,
-                                uint8_t* tile_kind, int32_t* old_slot, int32_t cap, int32_t* counts) {
-    int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (g >= n) return;
-    const uint8_t k = kind[g];
-    if (k && pos[g] < cap) {
-        const int slot = pos[g];
-        tile_map[g] = slot;
-        int x, y, z;
-        gdec3(td.v, g, x, y, z);
-        tile_xyz[slot * 3 + 0] = x;
-        tile_xyz[slot * 3 + 1] = y;
-        tile_xyz[slot * 3 + 2] = z;
-        tile_kind[slot] = k;
-        const int os = old_map ? old_map[g] : -1;
-        old_slot[slot] = os;
-        if (os < 0) atomicAdd(&counts[1], 1);
-    } else {
-        tile_map[g] = -1;
+__global__ void k_scan_blocks(int nb, int32_t* __restrict__ bsum, int32_t* __restrict__ total) {
+    __shared__ int wsum[32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int base = 0; base < nb; base += blockDim.x) {
+        const int b = base + threadIdx.x;
+        const int v = b < nb ? bsum[b] : 0;
+        int t = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += u;
+        }
+        if (lane == 31) wsum[wid] = t;
+        __syncthreads();
+        if (wid == 0) {
+            int q = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, q, o);
+                if (lane >= o) q += u;
+            }
+            if (lane < nw) wsum[lane] = q;
+        }
+        __syncthreads();
+        if (b < nb) bsum[b] = carry + (wid ? wsum[wid - 1] : 0) + t - v;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += wsum[nw - 1];
+        __syncthreads();
     }
-    if (g == n - 1) counts[0] = pos[g] + (k != 0);
+    if (threadIdx.x == 0 && total) *total = carry;
+}
+
+template <typename F, typename W>
+__global__ void k_flag_scatter(int64_t n, F flag, const int32_t* __restrict__ boff, W write) {
+    __shared__ int wsum[CB / 32];
+    __shared__ int strip_total;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t base = (int64_t)blockIdx.x * CPB;
+    int run = boff[blockIdx.x];
+#pragma unroll 1
+    for (int k = 0; k < CI; ++k) {
+        const int64_t g = base + k * CB + threadIdx.x;
+        const bool f = g < n && flag(g);
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) wsum[wid] = __popc(bal);
+        __syncthreads();
+        int before = 0;
+        for (int w = 0; w < wid; ++w) before += wsum[w];
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int w = 0; w < CB / 32; ++w) t += wsum[w];
+            strip_total = t;
+        }
+        const int pos = run + before + __popc(bal & ((1u << lane) - 1u));
+        if (g < n) write(g, f, pos);
+        __syncthreads();
+        run += strip_total;
+        __syncthreads();
+    }
+}
+
+static inline int flag_blocks(int64_t n) { return (int)((n + CPB - 1) / CPB); }
+
+struct KindFlag {
+    const uint8_t* kind;
+    __device__ bool operator()(int64_t g) const { return kind[g] != 0; }
+};
+
+struct TileWriter {
+    I3 td;
+    const uint8_t* kind;
+    const int32_t* old_map;
+    int32_t* tile_map;
+    int32_t* tile_xyz;
+    uint8_t* tile_kind;
+    int32_t* old_slot;
+    int32_t cap;
+    int32_t* counts;
+    __device__ void operator()(int64_t g, bool f, int slot) const {
+        if (f && slot < cap) {
+            tile_map[g] = slot;
+            int x, y, z;
+            gdec3(td.v, g, x, y, z);
+            tile_xyz[slot * 3 + 0] = x;
+            tile_xyz[slot * 3 + 1] = y;
+            tile_xyz[slot * 3 + 2] = z;
+            tile_kind[slot] = kind[g];
+            const int os = old_map ? old_map[g] : -1;
+            old_slot[slot] = os;
+            if (os < 0) atomicAdd(&counts[1], 1);
+        } else {
+            tile_map[g] = -1;
+        }
+    }
+};
+
+struct ByteFlag {
+    const int8_t* fl;
+    __device__ bool operator()(int64_t g) const { return fl[g] != 0; }
+};
+
+struct TargetWriter {
+    int32_t* targets;
+    __device__ void operator()(int64_t g, bool f, int pos) const {
+        if (f) targets[pos] = (int32_t)g;
+    }
+};
+
+__global__ void k_zero_i32(int32_t* p, int n) {
+    if (threadIdx.x < n) p[threadIdx.x] = 0;
 }
 
 static int64_t align256(int64_t v) { return (v + 255) & ~(int64_t)255; }
-
-static int64_t cub_temp_bytes(int64_t n) {
-    size_t a = 0, b = 0;
-    int32_t* p = nullptr;
-    cub::DeviceScan::ExclusiveSum(nullptr, a, p, p, (int)n);
-    cub::CountingInputIterator<int32_t> it(0);
-    cub::DeviceSelect::Flagged(nullptr, b, it, (const int8_t*)nullptr, p, p, (int)n);
-    return align256((int64_t)(a > b ? a : b));
-}
 
 // ---------------------------------------------------------------------------
 // neighbours
@@ -670,7 +777,8 @@ static inline int blocks_for(int64_t n, int b) { return (int)((n + b - 1) / b); 
 
 extern "C" int64_t mlbm_ws_bytes(int64_t n) {
     if (n < 1) n = 1;
-    return align256(4 * n) * 2 + cub_temp_bytes(n) + 256;
+    // [n flag bytes (interfaces)][block sums]
+    return align256(4 * n) + align256(4 * (int64_t)flag_blocks(n)) + 256;
 }
 
 extern "C" int mlbm_compact_tiles(int32_t dim, const int32_t tiles[3], const uint8_t* kind,
@@ -681,16 +789,16 @@ extern "C" int mlbm_compact_tiles(int32_t dim, const int32_t tiles[3], const uin
     const int64_t n = (int64_t)tiles[0] * tiles[1] * tiles[2];
     if (n <= 0 || ws_bytes < mlbm_ws_bytes(n)) return -1;
     cudaStream_t s = as_stream(stream);
-    char* w = (char*)ws;
-    int32_t* flags = (int32_t*)w;
-    int32_t* pos = (int32_t*)(w + align256(4 * n));
-    void* tmp = w + 2 * align256(4 * n);
-    size_t tmpb = (size_t)cub_temp_bytes(n);
-    k_kind_flags<<<blocks_for(n, 256), 256, 0, s>>>(n, kind, flags, counts);
-    cub::DeviceScan::ExclusiveSum(tmp, tmpb, flags, pos, (int)n, s);
+    int32_t* bsum = (int32_t*)((char*)ws + align256(4 * n));
+    const int nb = flag_blocks(n);
+    const KindFlag fl{kind};
+    // counts[0] = stored tiles (the scan total), counts[1] = fresh tiles
+    k_zero_i32<<<1, 32, 0, s>>>(counts, 2);
+    k_flag_count<<<nb, CB, 0, s>>>(n, fl, bsum);
+    k_scan_blocks<<<1, 1024, 0, s>>>(nb, bsum, counts);
     I3 td{{tiles[0], tiles[1], tiles[2]}};
-    k_scatter_tiles<<<blocks_for(n, 256), 256, 0, s>>>(n, td, kind, pos, old_map, tile_map, tile_xyz,
-                                                       tile_kind, old_slot, capacity, counts);
+    const TileWriter tw{td, kind, old_map, tile_map, tile_xyz, tile_kind, old_slot, capacity, counts};
+    k_flag_scatter<<<nb, CB, 0, s>>>(n, fl, bsum, tw);
     return launch_status(4);
 }
 
@@ -730,17 +838,19 @@ extern "C" int mlbm_build_interface(const mlbm_level_t* lv, const mlbm_level_t* 
     cudaStream_t s = as_stream(stream);
     char* w = (char*)ws;
     int8_t* fl = (int8_t*)w;
-    void* tmp = w + 2 * align256(4 * n);
-    size_t tmpb = (size_t)cub_temp_bytes(n);
+    int32_t* bsum = (int32_t*)(w + align256(4 * n));
     k_iface_flags<<<blocks_for(n, 256), 256, 0, s>>>(n, *lv, T, lv->cell_flags,
                                                      which == 0 ? MLBM_CF_GHOST_D : MLBM_CF_GHOST_U, fl);
-    cub::CountingInputIterator<int32_t> it(0);
-    cub::DeviceSelect::Flagged(tmp, tmpb, it, fl, targets, counts, (int)n, s);
+    const int nb = flag_blocks(n);
+    const ByteFlag bf{fl};
+    k_flag_count<<<nb, CB, 0, s>>>(n, bf, bsum);
+    k_scan_blocks<<<1, 1024, 0, s>>>(nb, bsum, counts);
+    k_flag_scatter<<<nb, CB, 0, s>>>(n, bf, bsum, TargetWriter{targets});
     if (lv->dim == 2)
         k_iface_stencil<2><<<blocks_for(n, 128), 128, 0, s>>>(*lv, *other, which, counts, targets, src, err);
     else
         k_iface_stencil<3><<<blocks_for(n, 128), 128, 0, s>>>(*lv, *other, which, counts, targets, src, err);
-    return launch_status(4);
+    return launch_status(5);
 }
 
 extern "C" int mlbm_seed_tiles(int32_t dim, int32_t n, const void* x, int64_t xstride, int32_t dtype,
@@ -913,4 +1023,78 @@ extern "C" int mlbm_fill(void* p, int64_t n, int32_t kind, double value, void* s
     default: return -1;
     }
     return launch_status(1);
+}
+
+// exclusive scan of n int32 in place (the compaction scan; used by the particle
+// sort): per-block sums of the 1024-element blocks, one scan of the sums, and
+// the block-local scan applied
+namespace mlbm {
+__global__ void k_block_sum(int n, const int32_t* __restrict__ v, int32_t* __restrict__ bsum) {
+    __shared__ int ws[CB / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t base = (int64_t)blockIdx.x * CPB;
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < CI; ++k) {
+        const int64_t g = base + k * CB + threadIdx.x;
+        c += g < n ? v[g] : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if (lane == 0) ws[wid] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < CB / 32; ++w) t += ws[w];
+        bsum[blockIdx.x] = t;
+    }
+}
+__global__ void k_block_apply(int n, int32_t* __restrict__ v, const int32_t* __restrict__ boff) {
+    __shared__ int wsum[CB / 32];
+    __shared__ int strip_total;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t base = (int64_t)blockIdx.x * CPB;
+    int run = boff[blockIdx.x];
+#pragma unroll 1
+    for (int k = 0; k < CI; ++k) {
+        const int64_t g = base + k * CB + threadIdx.x;
+        const int x = g < n ? v[g] : 0;
+        int t = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += u;
+        }
+        if (lane == 31) wsum[wid] = t;
+        __syncthreads();
+        int before = 0;
+        for (int w = 0; w < wid; ++w) before += wsum[w];
+        if (threadIdx.x == 0) {
+            int tt = 0;
+            for (int w = 0; w < CB / 32; ++w) tt += wsum[w];
+            strip_total = tt;
+        }
+        if (g < n) v[g] = run + before + t - x;
+        __syncthreads();
+        run += strip_total;
+        __syncthreads();
+    }
+}
+}  // namespace mlbm
+
+extern "C" int64_t mlbm_scan_ws_bytes(int32_t n) {
+    return align256(4 * (int64_t)flag_blocks(n > 0 ? n : 1)) + 256;
+}
+
+extern "C" int mlbm_scan_i32(int32_t n, int32_t* data, int32_t* total, void* ws, int64_t ws_bytes,
+                             void* stream) {
+    if (n <= 0) return 0;
+    if (ws_bytes < mlbm_scan_ws_bytes(n)) return -1;
+    cudaStream_t s = as_stream(stream);
+    const int nb = flag_blocks(n);
+    int32_t* bsum = (int32_t*)ws;
+    k_block_sum<<<nb, CB, 0, s>>>(n, data, bsum);
+    k_scan_blocks<<<1, 1024, 0, s>>>(nb, bsum, total);
+    k_block_apply<<<nb, CB, 0, s>>>(n, data, bsum);
+    return 3;
 }

@@ -117,6 +117,22 @@ class Particles:
         # were computed with (None: stale, recomputed before the next P2G)
         self.stress_mat = None
 
+    @classmethod
+    def wrap(cls, xd, pd, pid, dtype):
+        """Particles over existing device views (x [d, n], rows [R, n] sharing
+        one row stride, ids [n]) — capacity buffers of the slab migration."""
+        p = cls.__new__(cls)
+        p.d = xd.shape[0]
+        p.dtype = dtype
+        p.device = xd.device
+        p.R = prow(p.d)
+        assert xd.stride(0) == pd.stride(0), "x and rows must share the row stride"
+        p.xd, p.pd, p.pid = xd, pd, pid
+        p.permuted = False
+        p._scratch = None
+        p.stress_mat = None
+        return p
+
     def ensure_stress(self, mat):
         """(Re)compute the tau rows from F when F changed outside G2P or the
         material differs (mlbm_particle_stress); G2P keeps them current."""
@@ -128,14 +144,22 @@ class Particles:
                                              L.stream_handle()), "particle_stress")
         self.stress_mat = key
 
-    def scratch(self):
-        """Sort targets + radix-sort workspace (allocated once)."""
+    def scratch(self, n_slots=0):
+        """Sort targets + sort workspace (allocated once; regrown when the
+        level-0 slot capacity ``n_slots`` grows), with the storage's row
+        stride (the kernels take one stride for both)."""
+        need = int(L.lib().mlbm_sort_ws_bytes(max(len(self), 1), int(n_slots)))
+        if self._scratch is not None and self._scratch[3].numel() < need:
+            self._scratch = (*self._scratch[:3], torch.empty(int(need * 1.25), dtype=torch.uint8,
+                                                             device=self.device))
         if self._scratch is None:
             n = len(self)
-            ws = torch.empty(int(L.lib().mlbm_sort_ws_bytes(max(n, 1))), dtype=torch.uint8,
-                             device=self.device)
-            self._scratch = (torch.empty_like(self.xd), torch.empty_like(self.pd),
-                             torch.empty_like(self.pid), ws)
+            cap = self.pd.stride(0)
+            ws = torch.empty(int(need * 1.25), dtype=torch.uint8, device=self.device)
+            self._scratch = (torch.empty((self.d, cap), dtype=torch.float64, device=self.device)[:, :n],
+                             torch.empty((self.pd.shape[0], cap), dtype=self.dtype,
+                                         device=self.device)[:, :n],
+                             torch.empty(cap, dtype=torch.int32, device=self.device)[:n], ws)
         return self._scratch
 
     def _orig(self, t):

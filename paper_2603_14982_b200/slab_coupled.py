@@ -18,8 +18,9 @@ coupled cycle (coupling.py:448-481) with the same kernels, plus:
         neighbour (count, then payload);
   (v)   the diagnostics row is reduced over ranks (sums; eps min).
 
-Block maintenance is not distributed (static hierarchy); the adapt pass
-would need the seed-bitmap OR (iv) and the global bitmaps on every rank.
+  (iv)  block maintenance: every rank keeps the global kind grids and adapt
+        state and runs the adapt pass redundantly on the uint8 OR (MAX) of the
+        ranks' seed tiles, then rebuilds its local box;
 
 ``ThreadExchanger`` runs the ranks as threads of one process on one GPU
 (tests); ``P2PExchanger`` is the torch.distributed (NCCL) version.
@@ -88,6 +89,25 @@ class ThreadExchanger:
         self._sync()
         return got
 
+    def migrate_counts(self, sl, n_left, n_right):
+        """(iii) counts: my leavers per side -> arrivals (from left, from right)."""
+        self._post(sl.rank, "mcnt", (n_left, n_right))
+        self._sync()
+        ml = self.box[(sl.left, "mcnt")][1] if sl.left is not None else 0
+        mr = self.box[(sl.right, "mcnt")][0] if sl.right is not None else 0
+        self._sync()
+        return ml, mr
+
+    def migrate_payload(self, sl, send_l, send_r, recv_l, recv_r):
+        """(iii) payloads: one contiguous byte message per direction."""
+        self._post(sl.rank, "mpay", (send_l, send_r))
+        self._sync()
+        if sl.left is not None and recv_l is not None and recv_l.numel():
+            recv_l.copy_(self.box[(sl.left, "mpay")][1])
+        if sl.right is not None and recv_r is not None and recv_r.numel():
+            recv_r.copy_(self.box[(sl.right, "mpay")][0])
+        self._sync()
+
     def allreduce(self, sl, t, op):
         self._post(sl.rank, "red", t.clone())
         self._sync()
@@ -137,11 +157,15 @@ class P2PExchanger:
         # send my ghost sums to their owners, receive theirs for my edges
         recv_l = torch.empty_like(self._h(edge_l)) if sl.left is not None else None
         recv_r = torch.empty_like(self._h(edge_r)) if sl.right is not None else None
+
+        def packed(v):
+            h = self._h(v)
+            return L.pack_cols(h, torch.empty(h.shape, dtype=h.dtype, device=h.device))
         ops = []
         if sl.right is not None:
-            ops.append(dist.P2POp(dist.isend, self._h(ghost_r).contiguous(), sl.right))
+            ops.append(dist.P2POp(dist.isend, packed(ghost_r), sl.right))
         if sl.left is not None:
-            ops.append(dist.P2POp(dist.isend, self._h(ghost_l).contiguous(), sl.left))
+            ops.append(dist.P2POp(dist.isend, packed(ghost_l), sl.left))
         if sl.left is not None:
             ops.append(dist.P2POp(dist.irecv, recv_l, sl.left))
         if sl.right is not None:
@@ -149,9 +173,9 @@ class P2PExchanger:
         for q in dist.batch_isend_irecv(ops):
             q.wait()
         if recv_l is not None:
-            edge_l.add_(recv_l.to(edge_l.device))
+            L.unpack_cols(recv_l.to(edge_l.device), edge_l, add=True)
         if recv_r is not None:
-            edge_r.add_(recv_r.to(edge_r.device))
+            L.unpack_cols(recv_r.to(edge_r.device), edge_r, add=True)
 
     def particles(self, sl, to_left, to_right):
         dev = to_left.device
@@ -180,6 +204,44 @@ class P2PExchanger:
                     q.wait()
             got.append(buf.to(dev))
         return got
+
+    def migrate_counts(self, sl, n_left, n_right):
+        """(iii) counts (two phases: to the right / from the left, then to
+        the left / from the right — pairs up even when left == right)."""
+        dev = "cpu" if self.stage else "cuda"
+        got = []
+        for send_to, cnt, recv_from in ((sl.right, n_right, sl.left), (sl.left, n_left, sl.right)):
+            out = torch.tensor([cnt], dtype=torch.int64, device=dev)
+            inn = torch.zeros(1, dtype=torch.int64, device=dev)
+            ops = []
+            if send_to is not None:
+                ops.append(dist.P2POp(dist.isend, out, send_to))
+            if recv_from is not None:
+                ops.append(dist.P2POp(dist.irecv, inn, recv_from))
+            for q in dist.batch_isend_irecv(ops):
+                q.wait()
+            got.append(int(inn.item()) if recv_from is not None else 0)
+        return got[0], got[1]
+
+    def migrate_payload(self, sl, send_l, send_r, recv_l, recv_r):
+        """(iii) payloads: one contiguous byte message per direction, same
+        two-phase order as migrate_counts."""
+        for send_to, buf, recv_from, rbuf in ((sl.right, send_r, sl.left, recv_l),
+                                              (sl.left, send_l, sl.right, recv_r)):
+            ops = []
+            hb = self._h(buf) if buf is not None else None
+            hr = None
+            if rbuf is not None and rbuf.numel():
+                hr = torch.empty(rbuf.shape, dtype=rbuf.dtype, device="cpu") if self.stage else rbuf
+            if send_to is not None and hb is not None and hb.numel():
+                ops.append(dist.P2POp(dist.isend, hb, send_to))
+            if recv_from is not None and hr is not None:
+                ops.append(dist.P2POp(dist.irecv, hr, recv_from))
+            if ops:
+                for q in dist.batch_isend_irecv(ops):
+                    q.wait()
+            if hr is not None and hr is not rbuf:
+                rbuf.copy_(hr)
 
     def allreduce(self, sl, t, op):
         h = self._h(t)
@@ -254,7 +316,7 @@ class SlabCoupled(CoupledSim):
         self.drag_params.d_p = ref.drag_params.d_p
         self._global_active = len(ref.particles) > 0
         self.use_graphs = False
-        self.sort_particles = False
+        self.sort_particles = True
         # (iv) block maintenance: every rank keeps the GLOBAL kind grids and
         # adapt state and runs the pass redundantly on OR-reduced seeds; the
         # new global kinds are cropped to the local box and the local
@@ -325,9 +387,20 @@ class SlabCoupled(CoupledSim):
         grid.clear()
         n = len(p)
         ps = p.pd.stride(0)
+        # particles sorted by (tile slot, cell) every sort_every steps (the
+        # migration keeps the kept particles' order; arrivals append at the end),
+        # so P2G runs the per-warp node-box modes like the single domain
+        src_x, src_p, src_id, smem = p.xd, p.pd, None, 0
+        if n and self.sort_particles:
+            if self.step_count % self.sort_every == 0 or not p.permuted:
+                self._sort_into_scratch()
+                xa, pa, ida, _ = p.scratch()
+                src_x, src_p, src_id = xa, pa, ida
+                p.permuted = True
+            smem = self.p2g_mode
         if n:
-            L.check(lib.mlbm_p2g(L.C.byref(lv0), n, L.ptr(p.xd), L.ptr(p.pd), ps, mat.lam, mat.mu,
-                                 mat.alpha, L.ptr(grid.ras), grid.ras.stride(0), dcode, 0,
+            L.check(lib.mlbm_p2g(L.C.byref(lv0), n, L.ptr(src_x), L.ptr(src_p), ps, mat.lam, mat.mu,
+                                 mat.alpha, L.ptr(grid.ras), grid.ras.stride(0), dcode, smem,
                                  L.ptr(grid._err), s), "p2g")
         if self.world > 1:
             sl = self.sl
@@ -355,8 +428,10 @@ class SlabCoupled(CoupledSim):
                                   _d3(self.sediment_gravity, self.d), _faces(solver.boundaries),
                                   float(mat.floor_friction), 1, dcode, s), "exchange")
         if n:
-            L.check(lib.mlbm_g2p(L.C.byref(lv0), n, L.ptr(p.xd), L.ptr(p.xd), L.ptr(p.pd),
-                                 L.ptr(p.pd), L.ptr(None), L.ptr(None), ps, mat.lam, mat.mu,
+            L.check(lib.mlbm_g2p(L.C.byref(lv0), n, L.ptr(src_x), L.ptr(p.xd), L.ptr(src_p),
+                                 L.ptr(p.pd), L.ptr(src_id),
+                                 L.ptr(p.pid) if src_id is not None else L.ptr(None), ps, mat.lam,
+                                 mat.mu,
                                  mat.alpha, snow_arg(mat), L.ptr(grid.ras), grid.ras.stride(0),
                                  float(self.cadence), 1, dcode, L.ptr(self._counters),
                                  L.ptr(None), L.ptr(None), L.ptr(None),
@@ -367,40 +442,105 @@ class SlabCoupled(CoupledSim):
 
     # -- (iii) migration, (v) diagnostics ----------------------------------------------
     def _migrate(self):
+        """(iii) particles whose x left the slab: a stable on-device partition
+        (mlbm_migrate_count / mlbm_migrate_pack: warp ballots + block scan),
+        one count exchange, one contiguous message per direction, arrivals
+        appended after the kept particles (mlbm_migrate_unpack) in a second
+        capacity-sized particle buffer set (no per-step reallocation)."""
         if self.world == 1:
             return
         p = self.particles
+        sl = self.sl
+        lib, s = L.lib(), L.stream_handle()
+        n, d, R = len(p), p.d, p.pd.shape[0]
+        dc = dtype_code(p.dtype)
+        es = p.pd.element_size()
         lo, hi = self._local_x_range()
-        x = p.xd[0]
-        gx = self.sl.global_cells[0]
-        go_l = x < lo
-        go_r = x >= hi
-        keep = ~(go_l | go_r)
+        gx = float(sl.global_cells[0])
+        hl, hr = int(sl.left is not None), int(sl.right is not None)
+        ws = self._mig_buf("ws", int(lib.mlbm_migrate_ws_bytes(max(n, 1))))
+        cnt = self._mig_buf("cnt", 12)[:12].view(torch.int32)
+        L.check(lib.mlbm_migrate_count(n, L.ptr(p.xd), float(lo), float(hi), hl, hr, L.ptr(cnt),
+                                       L.ptr(ws), ws.numel(), s), "migrate_count")
+        nk, nl, nr = (int(v) for v in cnt.cpu().tolist())
+        ml, mr = self.xch.migrate_counts(sl, nl, nr)
+        total = nk + ml + mr
+        # the other buffer set of capacity >= total receives keep + arrivals
+        cur = getattr(self, "_mig_set", 0)
+        tgt = self._mig_set_bufs(1 - cur, total, d, R, p.dtype)
+        cap = tgt[0].shape[1]
+        msg = lambda m: m * (8 * d + es * R + 4)                   # noqa: E731
+        send_l = self._mig_buf("sl", msg(nl))[:msg(nl)]
+        send_r = self._mig_buf("sr", msg(nr))[:msg(nr)]
+        recv_l = self._mig_buf("rl", msg(ml))[:msg(ml)]
+        recv_r = self._mig_buf("rr", msg(mr))[:msg(mr)]
 
-        def pack(mask):
-            if self.sl.left is None and mask is go_l or self.sl.right is None and mask is go_r:
-                mask = torch.zeros_like(mask)
-            xs = p.xd[:, mask].clone()
-            xs[0] += self.sl.x0                                    # global x
-            xs[0] = torch.remainder(xs[0], gx)
-            rows = torch.cat([xs, p.pd[:, mask].double(), p.pid[mask].double()[None]], 0)
-            return rows
-        got = self.xch.particles(self.sl, pack(go_l), pack(go_r))
-        parts = [torch.cat([p.xd[:, keep], p.pd[:, keep].double(), p.pid[keep].double()[None]], 0)]
-        for g in got:
-            g = g.clone()
-            g[0] = g[0] - self.sl.x0
-            # wrapped arrivals (periodic x): bring into the local box
-            g[0] = torch.where(g[0] < 0, g[0] + gx, g[0])
-            g[0] = torch.where(g[0] >= self.sl.topology.finest_cells[0], g[0] - gx, g[0])
-            parts.append(g)
-        allp = torch.cat(parts, 1)
-        d, R = p.d, p.pd.shape[0]
-        out = Particles(allp.shape[1], d, p.dtype, p.device)
-        out.xd.copy_(allp[:d])
-        out.pd.copy_(allp[d:d + R].to(p.dtype))
-        out.pid.copy_(allp[d + R].round().to(torch.int32))
-        self.particles = out
+        def parts(buf, m):
+            b = buf.data_ptr()
+            return (L.C.c_void_p(b), L.C.c_void_p(b + 8 * d * m),
+                    L.C.c_void_p(b + 8 * d * m + es * R * m))
+        xl, pl, il = parts(send_l, nl)
+        xr, pr, ir = parts(send_r, nr)
+        L.check(lib.mlbm_migrate_pack(d, n, L.ptr(p.xd), L.ptr(p.pd), L.ptr(p.pid), p.pd.stride(0), R,
+                                      dc, float(lo), float(hi), float(sl.x0), gx, hl, hr,
+                                      L.ptr(tgt[0]), L.ptr(tgt[1]), L.ptr(tgt[2]), cap,
+                                      xl, pl, il, nl, xr, pr, ir, nr, L.ptr(ws), ws.numel(), s),
+                "migrate_pack")
+        self.xch.migrate_payload(sl, send_l, send_r, recv_l, recv_r)
+        at = nk
+        for buf, m in ((recv_l, ml), (recv_r, mr)):
+            if m:
+                xi, pi, ii = parts(buf, m)
+                L.check(lib.mlbm_migrate_unpack(d, m, xi, pi, ii, m, R, dc, float(sl.x0), gx,
+                                                float(sl.topology.finest_cells[0]), L.ptr(tgt[0]),
+                                                L.ptr(tgt[1]), L.ptr(tgt[2]), cap, at, s),
+                        "migrate_unpack")
+                at += m
+        self._mig_set = 1 - cur
+        np_ = Particles.wrap(tgt[0][:, :total], tgt[1][:, :total], tgt[2][:total], p.dtype)
+        np_.stress_mat = p.stress_mat          # the tau rows travel with the particles
+        np_.permuted = p.permuted
+        np_._scratch = self._mig_scratch(1 - cur, total, d, R, p.dtype, cap)
+        self.particles = np_
+
+    def _mig_buf(self, key, nbytes):
+        """Persistent byte buffers, grown geometrically."""
+        bufs = self.__dict__.setdefault("_mig_bufs", {})
+        b = bufs.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(int(nbytes * 1.25), 64), dtype=torch.uint8, device=self.pair.trees[0]
+                            .levels[0].data.device)
+            bufs[key] = b
+        return b
+
+    def _mig_scratch(self, which, n, d, R, dtype, cap):
+        """Sort scratch of buffer set `which`: same row stride as the set."""
+        scr = self.__dict__.setdefault("_mig_scr", [None, None])
+        st = scr[which]
+        lib = L.lib()
+        slots = self.topology.lv[0].cap
+        if st is None or st[0].shape[1] != cap or st[3].numel() < lib.mlbm_sort_ws_bytes(cap, slots):
+            dev = self.pair.trees[0].levels[0].data.device
+            st = (torch.empty((d, cap), dtype=torch.float64, device=dev),
+                  torch.empty((R, cap), dtype=dtype, device=dev),
+                  torch.empty(cap, dtype=torch.int32, device=dev),
+                  torch.empty(int(lib.mlbm_sort_ws_bytes(cap, slots) * 1.25), dtype=torch.uint8,
+                              device=dev))
+            scr[which] = st
+        return st[0][:, :n], st[1][:, :n], st[2][:n], st[3]
+
+    def _mig_set_bufs(self, which, need, d, R, dtype):
+        """Particle buffer set `which` (x, rows, ids) with capacity >= need."""
+        sets = self.__dict__.setdefault("_mig_sets", [None, None])
+        st = sets[which]
+        if st is None or st[0].shape[1] < need:
+            cap = max(int(need * 1.25) + 1024, 1024)
+            dev = self.pair.trees[0].levels[0].data.device
+            st = (torch.empty((d, cap), dtype=torch.float64, device=dev),
+                  torch.empty((R, cap), dtype=dtype, device=dev),
+                  torch.empty(cap, dtype=torch.int32, device=dev))
+            sets[which] = st
+        return st
 
     def _record_diagnostics(self):
         solver = self.solver
@@ -469,7 +609,7 @@ class SlabCoupled(CoupledSim):
         d = self.d
         p = self.particles
         seeds = gad._seeds
-        seeds.zero_()
+        L.zero(seeds)
         if len(p):
             gx = p.xd.clone()
             gx[0] = torch.remainder(gx[0] + sl.x0, sl.global_cells[0])
@@ -477,9 +617,7 @@ class SlabCoupled(CoupledSim):
             L.check(lib.mlbm_seed_tiles(d, len(p), L.ptr(gx), gx.stride(0), 1, t0,
                                         L.ptr(seeds), L.ptr(gad._err), s), "seed_tiles")
         if self.world > 1:
-            t = seeds.to(torch.int32)
-            self.xch.allreduce(sl, t, "max")
-            seeds.copy_(t.to(torch.uint8))
+            self.xch.allreduce(sl, seeds, "max")          # (iv) uint8 OR of the seed tiles
         gad._seeds_dirty = False
         # the fused pass with no particles: seeds are preset, cleared at its end
         gad.plan_device(RefineDriver(static_tiles=self.static_global, levels=gtopo.levels))

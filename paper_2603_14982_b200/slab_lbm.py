@@ -152,8 +152,8 @@ def exchange_columns(lo_col, hi_col, ghost_l, ghost_r, left, right, send, recv):
     tensors, gloo on CPU tensors).  Posting order (send right, send left,
     recv left, recv right) matches the messages pairwise even when
     left == right (two ranks, periodic x)."""
-    send[0].copy_(lo_col)
-    send[1].copy_(hi_col)
+    L.pack_cols(lo_col, send[0])
+    L.pack_cols(hi_col, send[1])
     ops = []
     if right is not None:
         ops.append(dist.P2POp(dist.isend, send[1], right))
@@ -167,9 +167,9 @@ def exchange_columns(lo_col, hi_col, ghost_l, ghost_r, left, right, send, recv):
         for q in dist.batch_isend_irecv(ops):
             q.wait()
     if ghost_l is not None:
-        ghost_l.copy_(recv[0])
+        L.unpack_cols(recv[0], ghost_l)
     if ghost_r is not None:
-        ghost_r.copy_(recv[1])
+        L.unpack_cols(recv[1], ghost_r)
 
 
 def exchange_local(slabs, tree_idx):

@@ -489,6 +489,12 @@ class MultiLevelSolver:
         if hook is None:
             r, w = self.roles(0)
             self._level_call(0, self.arrays(r, 0), self.arrays(w, 0), 0)
+        elif hasattr(hook, "level0"):
+            # fused coupled step: P2G needs no stream output, the exchange of a
+            # cell only its own bare moments: pre -> one level-0 kernel -> post
+            hook.pre(self)
+            hook.level0(self)
+            hook.post(self)
         else:
             self.stream(0)
             out = hook(self)

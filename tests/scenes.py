@@ -178,18 +178,43 @@ def terrain_heightfield(cells, path, base=1.0, amp=2.5):
     return path
 
 
+def slope_heightfield(cells, path, scale=1, h0=150.0, amp=3.0):
+    """A mountain flank for C4: heights in finest cells over (x, z) falling
+    along +x from ~h0 to ~1 (x^1.5 profile, span > 100 cells across the slab)
+    with a cross-slope undulation of +-amp/2; ``scale`` divides the full-scene
+    coordinates and heights (the CPU sample).  Written as an .npy."""
+    import numpy as np
+    nx, nz = cells[0], cells[2]
+    xs = (np.arange(nx) + 0.5) * scale / 1536.0
+    zs = (np.arange(nz) + 0.5) * scale / 384.0
+    h = h0 * (1.0 - xs)[:, None] ** 1.5 + amp * (0.5 + 0.5 * np.cos(2 * np.pi * zs))[None, :] + 1.0
+    np.save(path, (h / scale).astype(np.float64))
+    return path
+
+
 def avalanche_c4(heightfield_path, scale=1):
     """BASELINE.json configs[3]: four-level
-    1536x768x384-effective snow avalanche with powder cloud — floor wall over a
-    terrain heightmap (solids), outlets elsewhere, g along -y, a snow slab
-    (NACC snow with the paper's softening law; the reference
-    has no snow model, so this part is parity-unpinned)
-    [256,4,50]x[1280,28,334] = 6,979,584 cells at 8 per cell = 55,836,672
-    particles, powder entrainment on.  ``scale`` > 1 divides every extent (the
-    bounded CPU sample)."""
+    1536x768x384-effective snow avalanche with powder cloud on a mountain
+    flank — a floor wall under a heightmap falling ~110 cells along x
+    (solids), outlets elsewhere, g along -y, a snow slab 24 cells thick laid
+    on the slope as 16 steps of 64 cells ([256, 1280) x [50, 334) in x, z; each
+    step starts one cell above the highest terrain under it),
+    1024 x 24 x 284 = 6,979,584 cells at 8 per cell = 55,836,672 particles of
+    NACC snow with the paper's softening law (the reference
+    has no snow model, so this part is parity-unpinned), powder entrainment on.
+    ``scale`` > 1 divides every extent (the bounded CPU sample)."""
+    import math
+    import numpy as np
     s = float(scale)
     cells = [1536 // scale, 768 // scale, 384 // scale]
-    terrain_heightfield(cells, heightfield_path)
+    slope_heightfield(cells, heightfield_path, scale)
+    hm = np.load(heightfield_path)
+    blocks = []
+    for k in range(16):
+        x0, x1 = (256.0 + 64.0 * k) / s, (256.0 + 64.0 * (k + 1)) / s
+        top = float(hm[int(x0):int(math.ceil(x1)), :].max())
+        y0 = math.ceil(top) + 1.0
+        blocks.append([x0, y0, 50.0 / s, x1, y0 + 24.0 / s, 334.0 / s])
     return {
         "domain": {"cells": cells, "levels": 4},
         "fluid": {"tau0": 1.8, "eps_min": 0.5, "gravity": [0.0, -1e-4, 0.0]},
@@ -199,8 +224,7 @@ def avalanche_c4(heightfield_path, scale=1):
         "materials": {"density_ratio": 40.0, "E": 0.08, "nu": 0.3, "friction_angle_deg": 30.0,
                       "floor_friction": 0.5, "model": "snow", "nacc_q0": 0.02,
                       "nacc_alpha": 0.5},
-        "particles": {"blocks": [[256.0 / s, 4.0, 50.0 / s, 1280.0 / s, 4.0 + 24.0 / s, 334.0 / s]],
-                      "per_cell": 8},
+        "particles": {"blocks": blocks, "per_cell": 8},
         "powder": {"enabled": True, "entrain": 0.02, "diffusion": 0.05},
         "runtime": {"seed": 7, "dtype": "f32"}}
 

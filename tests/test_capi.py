@@ -69,4 +69,5 @@ def test_pure_host_size_queries():
     assert lib.mlbm_particle_rows(3) == 24 + 6
     assert lib.mlbm_particle_rows(2) == 13 + 3
     assert lib.mlbm_raster_rows(3) == 4 + 7 * 3 + 6 + 1
-    assert lib.mlbm_ws_bytes(1000) > 8000
+    assert lib.mlbm_ws_bytes(1000) >= 4 * 1000          # flags + block sums of the scan
+    assert lib.mlbm_sort_ws_bytes(1000, 50) > 3 * 4 * 1000

@@ -263,6 +263,14 @@ def case_p2p_exchanger(rank):
     to_r = torch.full((5, 2 * rank + 1), float(rank), dtype=torch.float64)
     got = x.particles(sl, to_l, to_r)
     out["got"] = [g.numpy().copy() for g in got]
+    # the migration messages of SlabCoupled._migrate: counts, then one byte
+    # buffer per direction
+    ml, mr = x.migrate_counts(sl, rank + 1, 2 * rank + 1)
+    out["mc"] = (ml, mr)
+    rl, rr = torch.empty(ml, dtype=torch.uint8), torch.empty(mr, dtype=torch.uint8)
+    x.migrate_payload(sl, torch.full((rank + 1,), rank, dtype=torch.uint8),
+                      torch.full((2 * rank + 1,), 100 + rank, dtype=torch.uint8), rl, rr)
+    out["rl"], out["rr"] = rl.numpy().copy(), rr.numpy().copy()
     t = torch.tensor([float(rank), 5.0 - rank], dtype=torch.float64)
     x.allreduce(sl, t, "sum")
     m = torch.tensor([float(rank)], dtype=torch.float64)
@@ -285,3 +293,6 @@ def test_p2p_exchanger_gloo():
         assert o["got"][0].shape == (5, 2 * lft + 1) and np.all(o["got"][0] == lft)
         assert o["got"][1].shape == (5, rgt + 1) and np.all(o["got"][1] == -rgt)
         assert np.array_equal(o["sum"], [0 + 1 + 2, 15 - 3]) and o["max"][0] == 2
+        assert o["mc"] == (2 * lft + 1, rgt + 1)
+        assert np.all(o["rl"] == 100 + lft) and len(o["rl"]) == 2 * lft + 1
+        assert np.all(o["rr"] == rgt) and len(o["rr"]) == rgt + 1

@@ -575,3 +575,18 @@ def test_checkpoint_resume_continues_the_run(dtype, tmp_path):
         da = a.solver.arrays(wi, 0)[nm].double().cpu().numpy()
         db = b.solver.arrays(b.solver.last_roles(0)[1], 0)[nm].double().cpu().numpy()
         assert np.abs(da - db).max() <= tol, nm
+
+
+@pytest.mark.parametrize("scene", ["snow_3d", "snow_2d"])
+def test_snow_nacc_fp64(scene):
+    """The paper's snow (NACC + softening law) in G2P against
+    the oracle's restatement (parity unpinned: the reference has no snow):
+    gate A on fields and particles, the hardening state (vol_corr row) per
+    particle, and both hardening branches reached (cracked and softening)."""
+    sc = S.SNOW_3D_SMALL if scene == "snow_3d" else S.SNOW_2D
+    osim, dsim = run_and_compare(sc, 10)
+    from oracle import mpm as OM
+    qd = dsim.particles.vol_corr.double().cpu().numpy()
+    assert np.abs(qd - osim.p.vol_corr).max() <= 1e-9
+    _, cracked = OM.nacc_state_decode(osim.p.vol_corr)
+    assert cracked.any() and (~cracked).any()

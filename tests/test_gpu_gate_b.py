@@ -105,3 +105,11 @@ def test_c2_full_size_gate_a_and_b():
     m = gate_b_metrics(o64, d32, ox0, dx0)
     print("c2", m)
     assert all(v <= GATE_B for v in m.values()), m
+
+
+def test_gate_b_snow_fp32():
+    """Gate B on the snow path (NACC in fp32 G2P) against the fp64 oracle."""
+    _need_gpu()
+    m = run_gate_b(S.scene(S.SNOW_3D_SMALL, runtime__dtype="f32"), 10)
+    print("snow", m)
+    assert all(v <= GATE_B for v in m.values()), m

@@ -24,8 +24,11 @@ def test_c4_avalanche_scene(tmp_path):
     assert _particles(cfg) == 55_836_672
     hm = cfg.heightmap()
     assert hm.shape == (1536, 384)
-    # the terrain stays below the slab floor (no particle starts in a solid)
-    assert 0.0 < hm.min() and hm.max() < 4.0
+    # a mountain flank: > 100 cells of relief under the slab ...
+    assert hm[256:1280].max() - hm[256:1280].min() > 100.0
+    # ... and no particle starts inside the terrain
+    for b in cfg.raw["particles"]["blocks"]:
+        assert b[1] > hm[int(b[0]):int(b[3])].max()
     assert cfg.raw["powder"]["enabled"]
     # the CPU sample: every extent divided by 4, coarsest tiles still whole
     small = validate_scene(S.avalanche_c4(str(tmp_path / "terrain4.npy"), scale=4))

@@ -26,7 +26,7 @@ p, grid, mat = sim.particles, sim.grid, sim.material
 lv0 = grid.level0()
 n = len(p)
 ps = p.pd.stride(0)
-xa, pa, ida, ws = p.scratch()
+xa, pa, ida, ws = p.scratch(lv0.n_tiles)
 L.check(lib.mlbm_particle_sort(L.C.byref(lv0), n, L.ptr(p.xd), L.ptr(p.pd), L.ptr(p.pid), ps,
                                L.ptr(xa), L.ptr(pa), L.ptr(ida), 0, L.ptr(ws), ws.numel(), s), "sort")
 NACC = grid.R["nacc"]
