@@ -98,6 +98,9 @@ typedef struct {
     double boxes[MLBM_MAX_BOXES][6];   /* lo[3], hi[3] in finest units (2D: lo x,y,_ hi x,y,_) */
     const float* heightmap;            /* finest (x[, z]) heights or NULL */
     int32_t hm_dims[2];
+    /* per level (or NULL): 1 where a solid lies within one cell of the tile
+     * (mlbm_solid_near, computed once: the geometry is static) */
+    const uint8_t* near[MLBM_MAX_LEVELS];
 } mlbm_solid_t;
 
 typedef struct {
@@ -174,6 +177,12 @@ int mlbm_build_neighbors(const mlbm_level_t* lv, int32_t* nbr, void* stream);
  * classify_interfaces, solver.py:177-273 _LevelTables): I^d / I^u ghosts,
  * BC layer, solid, active, per-direction bounce-back / self-source masks,
  * tile flags.  counts[0] += |I^d|, counts[1] += |I^u|; violations -> err. */
+/* the static near-solid map of one level over its whole tile grid (1 where a
+ * solid box or the heightmap reaches within one cell of the tile; periodic
+ * seams always 1), read by mlbm_classify_level instead of rescanning the
+ * geometry at every rebuild */
+int mlbm_solid_near(const mlbm_level_t* lv, const mlbm_solid_t* solid, uint8_t* near, void* stream);
+
 int mlbm_classify_level(const mlbm_level_t* lv, const mlbm_hier_t* h,
                         const mlbm_bc_t* bc, const mlbm_solid_t* solid,
                         uint8_t* cell_flags, uint64_t* dir_masks, uint8_t* tile_flags,

@@ -97,7 +97,8 @@ class BC(C.Structure):
 
 class Solid(C.Structure):
     _fields_ = [("n_boxes", C.c_int32), ("boxes", (C.c_double * 6) * 16),
-                ("heightmap", C.c_void_p), ("hm_dims", C.c_int32 * 2)]
+                ("heightmap", C.c_void_p), ("hm_dims", C.c_int32 * 2),
+                ("near", C.c_void_p * 6)]
 
 
 class Collide(C.Structure):
@@ -184,6 +185,7 @@ _SIGS = {
     "mlbm_migrate_unpack": [I32, I32, P, P, P, I64, I32, I32, D, D, D, P, P, P, I64, I32, P],
     "mlbm_memset": [P, I32, I64, P],
     "mlbm_fill": [P, I64, I32, D, P],
+    "mlbm_solid_near": [C.POINTER(Level), C.POINTER(Solid), P, P],
     "mlbm_particle_stress": [I32, I32, P, I64, D, D, D, I32, P],
     "mlbm_stencil": [C.POINTER(Level), I32, P, I64, P, P, P, P, I64, I32, P, P],
     "mlbm_powder_step": [C.POINTER(Level), Fields, Fields, P, D, D, D, P, I32, P],

@@ -331,9 +331,12 @@ class CoupledSim:
         self.precapture_steps = int(os.environ.get("MLBM_PRECAPTURE", "16")) or None
         self.latest_only_rebuild = os.environ.get("MLBM_LATEST_ONLY_REBUILD", "1") != "0"
         self.latest_only_min_cells = 1 << 22
-        # the level-0 coupled phase as P2G -> ONE stream + exchange + collide
-        # kernel -> G2P (MLBM_FUSE_L0=0: stream / exchange / collide separately)
-        self.fuse_level0 = os.environ.get("MLBM_FUSE_L0", "1") != "0"
+        # MLBM_FUSE_L0=1: the level-0 coupled phase as P2G -> ONE stream +
+        # exchange + collide kernel -> G2P.  Measured on C4 it is no faster
+        # than the three kernels (the exchange's neighbour gathers lose the
+        # separate kernel's occupancy: 1.97 vs 1.88 ms per step; graph step
+        # 23.0 vs 22.1 ms), so the separate kernels stay the default.
+        self.fuse_level0 = os.environ.get("MLBM_FUSE_L0", "0") == "1"
         self.p2g_mode = 4          # sorted input: 1 block smem, 2 warp registers, 3 cell lanes,
                                    # 4 cell lanes + per-warp box copies (fp32; fp64 runs mode 3),
                                    # 5 = 4 with two rounds of particles per block
@@ -836,6 +839,7 @@ class CoupledSim:
                 self.material.lam, self.material.mu, self.material.alpha, L.ptr(grid.ras),
                 grid.ras.stride(0), float(self.powder.eta_surface), L.ptr(self._tmp), dcode,
                 L.ptr(grid._err), s), "stress_raster")
+            self._powder_stress_done()
         lv0 = solver._structs[0]
         pw = self.powder
         L.check(lib.mlbm_powder(L.C.byref(lv0), L.fields(solver.arrays(r, 0).data),
@@ -843,6 +847,15 @@ class CoupledSim:
                                 grid.ras.stride(0), L.ptr(self._tmp), float(pw.diffusion),
                                 float(pw.sign), 1.0, float(pw.entrain), float(pw.eta_surface),
                                 1 if src else 0, dcode, s), "powder")
+        self._powder_done()
+
+    def _powder_stress_done(self):
+        """Hook after the entrainment stress raster (the slab step sums the
+        ghost-node stress of its neighbours here)."""
+
+    def _powder_done(self):
+        """Hook after the powder transport (the slab step refreshes the ghost
+        columns of phi here)."""
 
     # -- diagnostics -------------------------------------------------------------------
     def _record_diagnostics(self):

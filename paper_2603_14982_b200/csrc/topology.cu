@@ -188,9 +188,13 @@ struct TileWriter {
     }
 };
 
-struct ByteFlag {
-    const int8_t* fl;
-    __device__ bool operator()(int64_t g) const { return fl[g] != 0; }
+struct IfaceFlag {      // interface target: a live cell with the ghost bit
+    mlbm_level_t lv;       // live tile count on the device (lv.counts)
+    int T;
+    uint8_t bit;
+    __device__ bool operator()(int64_t g) const {
+        return g < (int64_t)live_tiles(lv) * T && (lv.cell_flags[g] & bit);
+    }
 };
 
 struct TargetWriter {
@@ -292,7 +296,9 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
     // maximum over the dilated footprint (a tile on a periodic seam is always
     // scanned)
     bool near = false;
-    if (solid.n_boxes > 0 || solid.heightmap != nullptr) {
+    if (solid.near[level]) {
+        near = solid.near[level][gidx3(lv.tiles, tx[0], tx[1], tx[2])] != 0;   // static map
+    } else if (solid.n_boxes > 0 || solid.heightmap != nullptr) {
         bool seam = false;
         for (int a = 0; a < D; ++a)
             seam |= lv.periodic[a] && (tx[a] == 0 || tx[a] == lv.tiles[a] - 1);
@@ -444,10 +450,6 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
 
 // ---------------------------------------------------------------------------
 // interfaces
-__global__ void k_iface_flags(int64_t n, mlbm_level_t lv, int T, const uint8_t* cf, uint8_t bit, int8_t* out) {
-    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c < n) out[c] = (c < (int64_t)live_tiles(lv) * T && (cf[c] & bit)) ? 1 : 0;
-}
 
 template <int D>
 __global__ void k_iface_stencil(mlbm_level_t lv, mlbm_level_t other, int which, const int32_t* counts,
@@ -769,6 +771,45 @@ __global__ void k_init_new(mlbm_hier_t oh, mlbm_hier_t nh, int level, const int3
     atomicAdd(viol, 1);
 }
 
+// the static near-solid map of one level (the same test as k_classify's
+// inline scan, one thread per tile of the whole tile grid)
+template <int D>
+__global__ void k_solid_near(mlbm_level_t lv, mlbm_solid_t solid, uint8_t* near) {
+    const int64_t n = (int64_t)lv.tiles[0] * lv.tiles[1] * lv.tiles[2];
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    int tx[3];
+    gdec3(lv.tiles, t, tx[0], tx[1], tx[2]);
+    bool seam = false;
+    for (int a = 0; a < D; ++a) seam |= lv.periodic[a] && (tx[a] == 0 || tx[a] == lv.tiles[a] - 1);
+    const int sc = 1 << lv.level;
+    int lo[3] = {0, 0, 0}, hi[3] = {1, 1, 1};
+    for (int a = 0; a < D; ++a) { lo[a] = (tx[a] * 4 - 1) * sc; hi[a] = (tx[a] * 4 + 5) * sc; }
+    bool mine = seam;
+    for (int b = 0; b < solid.n_boxes && !mine; ++b) {
+        bool in = true;
+        for (int a = 0; a < D; ++a) in &= solid.boxes[b][a] < (double)hi[a] && solid.boxes[b][3 + a] > (double)lo[a];
+        mine |= in;
+    }
+    if (solid.heightmap && !mine) {
+        const int nx = hi[0] - lo[0], nz = D == 3 ? hi[2] - lo[2] : 1;
+        float hmax = 0.f;
+        for (int i = 0; i < nx * nz; ++i) {
+            const int cx = lo[0] + i % nx, cz = D == 3 ? lo[2] + i / nx : 0;
+            const int hx = cx < 0 ? 0 : (cx >= solid.hm_dims[0] ? solid.hm_dims[0] - 1 : cx);
+            float h;
+            if (D == 2) h = solid.heightmap[hx];
+            else {
+                const int hz = cz < 0 ? 0 : (cz >= solid.hm_dims[1] ? solid.hm_dims[1] - 1 : cz);
+                h = solid.heightmap[(int64_t)hx * solid.hm_dims[1] + hz];
+            }
+            hmax = h > hmax ? h : hmax;
+        }
+        mine |= hmax > 0.f && (float)lo[1] < hmax;
+    }
+    near[t] = mine ? 1 : 0;
+}
+
 }  // namespace mlbm
 
 using namespace mlbm;
@@ -837,15 +878,16 @@ extern "C" int mlbm_build_interface(const mlbm_level_t* lv, const mlbm_level_t* 
     if (ws_bytes < mlbm_ws_bytes(n)) return -1;
     cudaStream_t s = as_stream(stream);
     char* w = (char*)ws;
-    int8_t* fl = (int8_t*)w;
     int32_t* bsum = (int32_t*)(w + align256(4 * n));
-    k_iface_flags<<<blocks_for(n, 256), 256, 0, s>>>(n, *lv, T, lv->cell_flags,
-                                                     which == 0 ? MLBM_CF_GHOST_D : MLBM_CF_GHOST_U, fl);
     const int nb = flag_blocks(n);
-    const ByteFlag bf{fl};
-    k_flag_count<<<nb, CB, 0, s>>>(n, bf, bsum);
+    // the flags are read straight from the cell flags (no flag array pass);
+    // the live count is a device value: kernels launched over the capacity
+    // read it themselves
+    const uint8_t bit = which == 0 ? MLBM_CF_GHOST_D : MLBM_CF_GHOST_U;
+    const IfaceFlag fl{*lv, T, bit};
+    k_flag_count<<<nb, CB, 0, s>>>(n, fl, bsum);
     k_scan_blocks<<<1, 1024, 0, s>>>(nb, bsum, counts);
-    k_flag_scatter<<<nb, CB, 0, s>>>(n, bf, bsum, TargetWriter{targets});
+    k_flag_scatter<<<nb, CB, 0, s>>>(n, fl, bsum, TargetWriter{targets});
     if (lv->dim == 2)
         k_iface_stencil<2><<<blocks_for(n, 128), 128, 0, s>>>(*lv, *other, which, counts, targets, src, err);
     else
@@ -1097,4 +1139,15 @@ extern "C" int mlbm_scan_i32(int32_t n, int32_t* data, int32_t* total, void* ws,
     k_scan_blocks<<<1, 1024, 0, s>>>(nb, bsum, total);
     k_block_apply<<<nb, CB, 0, s>>>(n, data, bsum);
     return 3;
+}
+
+extern "C" int mlbm_solid_near(const mlbm_level_t* lv, const mlbm_solid_t* solid, uint8_t* near, void* stream) {
+    const int64_t n = (int64_t)lv->tiles[0] * lv->tiles[1] * lv->tiles[2];
+    if (n <= 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    mlbm_solid_t sl = *solid;
+    for (int l = 0; l < MLBM_MAX_LEVELS; ++l) sl.near[l] = nullptr;
+    if (lv->dim == 2) k_solid_near<2><<<blocks_for(n, 128), 128, 0, s>>>(*lv, sl, near);
+    else k_solid_near<3><<<blocks_for(n, 128), 128, 0, s>>>(*lv, sl, near);
+    return launch_status(1);
 }

@@ -311,7 +311,7 @@ class SlabCoupled(CoupledSim):
         own = (sl.part.owner(gx[:, 0]) == rank)
         part = self._make_particles(ref, torch.as_tensor(np.nonzero(own)[0], device=topo.device))
         super().__init__(sl.solver, part, ref.material, sediment_gravity=ref.sediment_gravity,
-                         drag=ref.drag_params, powder=None, adaptor=None,
+                         drag=ref.drag_params, powder=ref.powder, adaptor=None,
                          unit_scale=ref.unit_scale)
         self.drag_params.d_p = ref.drag_params.d_p
         self._global_active = len(ref.particles) > 0
@@ -358,20 +358,52 @@ class SlabCoupled(CoupledSim):
         return self.x_lo - self.sl.x0, self.x_hi - self.sl.x0
 
     # -- (i) per-level ghost columns ----------------------------------------------------
-    def exchange_level(self, level, dst):
+    def exchange_level(self, level, dst, rows=None):
+        """(i) owned edge columns -> the neighbours' ghost columns (rows: a row
+        slice of the SoA block, default the moments)."""
         sl = self.sl
         if self.world == 1:
             return
-        nm = len(moment_names(sl.d))
+        rows = rows or slice(0, len(moment_names(sl.d)))
         a = dst_data(dst)
         r = sl.ranges[level]
         lo_l, hi_l = sl.cells(level, r["edge_l"])
         lo_r, hi_r = sl.cells(level, r["edge_r"])
         glo_l, ghi_l = sl.cells(level, r["ghost_l"])
         glo_r, ghi_r = sl.cells(level, r["ghost_r"])
-        self.xch.columns(sl, a[:nm, lo_l:hi_l], a[:nm, lo_r:hi_r],
-                         a[:nm, glo_l:ghi_l] if sl.left is not None else None,
-                         a[:nm, glo_r:ghi_r] if sl.right is not None else None)
+        self.xch.columns(sl, a[rows, lo_l:hi_l], a[rows, lo_r:hi_r],
+                         a[rows, glo_l:ghi_l] if sl.left is not None else None,
+                         a[rows, glo_r:ghi_r] if sl.right is not None else None)
+
+    # -- powder across the cut -------------------------------------------------------------
+    def _ghost_rows_reduce(self, r0, r1):
+        """(ii) for raster rows [r0, r1): ghost-node partial sums to the owners,
+        completed edge rows back into the ghost region."""
+        if self.world == 1:
+            return
+        sl, ras = self.sl, self.grid.ras
+        rr = sl.ranges[0]
+        lo_l, hi_l = sl.cells(0, rr["edge_l"])
+        lo_r, hi_r = sl.cells(0, rr["edge_r"])
+        glo_l, ghi_l = sl.cells(0, rr["ghost_l"])
+        glo_r, ghi_r = sl.cells(0, rr["ghost_r"])
+        gl = ras[r0:r1, glo_l:ghi_l] if sl.left is not None else None
+        gr = ras[r0:r1, glo_r:ghi_r] if sl.right is not None else None
+        el, er = ras[r0:r1, lo_l:hi_l], ras[r0:r1, lo_r:hi_r]
+        self.xch.ghost_reduce(sl, gl, gr, el, er)
+        self.xch.columns(sl, el, er, gl, gr)
+
+    def _powder_stress_done(self):
+        # the entrainment stress raster of surface cells near the cut needs the
+        # neighbour's particles: sum the SIG rows like the P2G rows
+        R = self.grid.R
+        self._ghost_rows_reduce(R["sig"], R["etae"])
+
+    def _powder_done(self):
+        # the next backtrace and exchange read phi in the ghost columns
+        _, w = self.solver.last_roles(0)
+        phi = self.pair.trees[w].levels[0].index["phi"]
+        self.exchange_level(0, self.pair.trees[w].levels[0], rows=slice(phi, phi + 1))
 
     # -- the coupling hook with (ii) ------------------------------------------------------
     def _exchange(self, solver):
@@ -595,6 +627,8 @@ class SlabCoupled(CoupledSim):
             solver.run_cycle(cycle)
         if self.coupling_active and is_mpm:
             self.grid.raise_pending()
+        if self.powder is not None:
+            self._powder_cycle(is_mpm)
         self._migrate()
         if self.gad is not None and self.coupling_active and self.step_count % self.cadence == 0:
             self._adapt()

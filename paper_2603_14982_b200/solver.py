@@ -303,6 +303,17 @@ class MultiLevelSolver:
         self._err = torch.zeros(L.ERR_INTS, dtype=torch.int32, device=topology.device)
         self._bc = self.boundaries.bc_struct(params.rho0)
         self._solid = self.boundaries.solid_struct(self.d, topology.device)
+        self._near_maps = []
+        if self._solid.n_boxes or self._solid.heightmap:
+            # the geometry is static: its near-solid tile maps once per level
+            for l in range(topology.levels):
+                nm = torch.zeros(int(np.prod(topology.tile_grid(l))), dtype=torch.uint8,
+                                 device=topology.device)
+                L.check(L.lib().mlbm_solid_near(L.C.byref(topology.level_struct(l)),
+                                                L.C.byref(self._solid), L.ptr(nm),
+                                                L.stream_handle()), "solid_near")
+                self._near_maps.append(nm)
+                self._solid.near[l] = nm.data_ptr()
         self._schedule = build_schedule(topology.levels)
         self.launches = 0
         self._refresh_tables()

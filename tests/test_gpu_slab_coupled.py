@@ -33,7 +33,10 @@ def _ref(scene, adapt):
 @pytest.mark.parametrize("scene,world,steps,adapt", [
     (S.COLUMN_3D_SMALL, 2, 6, False), (S.SANDSTORM_3D_SMALL, 2, 6, False),
     (S.COLUMN_3D_SMALL, 2, 8, True), (S.SANDSTORM_3D_SMALL, 2, 8, True),
-    (S.CLOUD_3D_SMALL, 3, 14, True)])
+    (S.CLOUD_3D_SMALL, 3, 14, True),
+    # powder transport + entrainment across the cut (stress raster ghost sums,
+    # phi ghost columns), the column straddling it
+    (S.scene(S.COLUMN_3D_SMALL, powder__enabled=True, powder__entrain=0.02), 2, 10, True)])
 def test_coupled_slabs_equal_single_domain(scene, world, steps, adapt):
     _need_gpu()
     from paper_2603_14982_b200.slab_coupled import SlabCoupled, ThreadExchanger
@@ -84,8 +87,11 @@ def test_coupled_slabs_equal_single_domain(scene, world, steps, adapt):
     wi = ref.solver.last_roles(0)[1]
     ga = ref.solver.arrays(wi, 0)
     gkey = {tuple(c): i for i, c in enumerate(ref.topology.cell_coords(0).tolist())}
+    names = moment_names(ref.d) + (["phi"] if ref.powder is not None else [])
+    if ref.powder is not None:
+        assert np.abs(ga["phi"].cpu().numpy()).max() > 0.0     # entrainment happened
     for r in ranks:
-        for name in moment_names(ref.d):
+        for name in names:
             c2, got = r.sl.owned_cells(r.solver.last_roles(0)[1], 0, name)
             want = ga[name].cpu().numpy()[[gkey[tuple(c)] for c in c2.tolist()]]
             assert np.abs(got - want).max() <= 1e-10, (name, r.rank)
