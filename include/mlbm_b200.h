@@ -393,10 +393,13 @@ int mlbm_stress_raster_surface(const mlbm_level_t* lv0, int32_t n, const double*
                                const void* p, int64_t ps, double lam, double mu, double alpha,
                                void* ras, int64_t rs, double eta_surface, void* surf,
                                int32_t dtype, mlbm_error_t* err, void* stream);
+/* tile_ws (optional, 2 x lv0->n_tiles bytes): per tile whether phi is non-zero
+ * within its 3^dim tile neighbourhood; cells of inactive tiles skip the RK3
+ * velocity sampling (their advected value is exactly 0). */
 int mlbm_powder(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm_fields_t dst, void* ras,
-                int64_t rs, void* tmp, double diffusion, double sign, double dt,
-                double entrain, double eta_surface, int32_t with_source, int32_t dtype,
-                void* stream);
+                int64_t rs, void* tmp, uint8_t* tile_ws, double diffusion, double sign,
+                double dt, double entrain, double eta_surface, int32_t with_source,
+                int32_t dtype, void* stream);
 
 /* The reference's standalone coupling functions as per-cell passes over the
  * level-0 raster (the fused mlbm_exchange runs the same device code):

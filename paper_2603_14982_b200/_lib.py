@@ -172,7 +172,7 @@ _SIGS = {
                            I32, P, P],
     "mlbm_stress_raster_surface": [C.POINTER(Level), I32, P, P, I64, D, D, D, P, I64, D, P,
                                    I32, P, P],
-    "mlbm_powder": [C.POINTER(Level), Fields, Fields, P, I64, P, D, D, D, D, D,
+    "mlbm_powder": [C.POINTER(Level), Fields, Fields, P, I64, P, P, D, D, D, D, D,
                     I32, I32, P],
     "mlbm_coupling_op": [C.POINTER(Level), I32, P, I64, P, P, I64, P, I64, D, D, D, D, D, D,
                          P, I32, P],

@@ -514,13 +514,16 @@ class CoupledSim:
             self.grid.raise_pending()
         if self.powder is not None:
             self._powder_cycle(is_mpm)
+        # the particle part on the raster of this step's exchange (before the
+        # rebuild renumbers the level-0 slots), the fluid part after the adapt
+        self._record_diagnostics(fluid=False)
         if adapt_now:
             driver = self._driver()
             self.last_report = self.adaptor.update(driver, self.pair)
             if not self.last_report.noop:
                 self.topology_changes += 1
             self.grid.sync_topology()
-        self._record_diagnostics()
+        self._record_diagnostics(particles=False)
         self._push_diag_row(self._diag_buf.cpu().numpy())
 
     def _g2p_seeds(self):
@@ -798,7 +801,8 @@ class CoupledSim:
             L.TRACE.launches += g.nk
             solver._tables_version = topo.version
             self.rebuild_replays += 1
-        self._record_diagnostics()
+        # the step graph left this step's particle diagnostics in the buffer
+        self._record_diagnostics(particles=False)
         self._host_rb.copy_(self._diag_buf, non_blocking=True)
 
     def _resolve_pending_diag(self):
@@ -814,6 +818,10 @@ class CoupledSim:
         n0 = self.topology.capacity_cells(0)
         if self._tmp is None or self._tmp.numel() != n0:
             self._tmp = torch.empty(n0, dtype=self.dtype, device=self.topology.device)
+            # per-tile powder activity (the advection skips tiles with no phi
+            # within reach)
+            self._tile_ws = torch.empty(2 * self.topology.lv[0].cap, dtype=torch.uint8,
+                                        device=self.topology.device)
         return self._tmp
 
     def _powder_cycle(self, is_mpm):
@@ -844,7 +852,8 @@ class CoupledSim:
         pw = self.powder
         L.check(lib.mlbm_powder(L.C.byref(lv0), L.fields(solver.arrays(r, 0).data),
                                 L.fields(solver.arrays(w, 0).data), L.ptr(grid.ras),
-                                grid.ras.stride(0), L.ptr(self._tmp), float(pw.diffusion),
+                                grid.ras.stride(0), L.ptr(self._tmp), L.ptr(self._tile_ws),
+                                float(pw.diffusion),
                                 float(pw.sign), 1.0, float(pw.entrain), float(pw.eta_surface),
                                 1 if src else 0, dcode, s), "powder")
         self._powder_done()
@@ -858,17 +867,23 @@ class CoupledSim:
         columns of phi here)."""
 
     # -- diagnostics -------------------------------------------------------------------
-    def _record_diagnostics(self):
-        """Device reductions of coupling.py:500-531 into a persistent buffer."""
+    def _record_diagnostics(self, fluid=True, particles=True):
+        """Device reductions of coupling.py:500-531 into a persistent buffer.
+        The fluid part (leaf-weighted momentum, sum phi, eps min) depends on
+        the topology; the particle part (momentum, drag impulse of the last
+        exchange) does not — after a rebuild only the fluid part is retaken."""
         solver = self.solver
         d = self.d
         lib = L.lib()
         s = L.stream_handle()
         dcode = dtype_code(self.dtype)
         out = self._diag_buf
-        L.zero(out)
-        L.fill(out[d + 1:d + 2], 1.0)
-        for l in range(self.topology.levels):
+        if fluid:
+            L.zero(out[:d + 2])
+            L.fill(out[d + 1:d + 2], 1.0)
+        if particles:
+            L.zero(out[d + 2:])
+        for l in range(self.topology.levels if fluid else 0):
             if not self.topology.n_tiles(l):
                 continue
             lw = solver.last_roles(l)[1] if solver.k[l] else 0
@@ -876,6 +891,8 @@ class CoupledSim:
             L.check(lib.mlbm_diag_level(L.C.byref(solver._structs[l]), L.fields(a.data),
                                         float((1 << d) ** l), dcode, L.ptr(out[:d + 2]), s),
                     "diag_level")
+        if not particles:
+            return
         p = self.particles
         g = self.grid
         n0 = self.topology.capacity_cells(0) if self.last_fields is not None else 0

@@ -1140,7 +1140,36 @@ struct PowderArgs {
     double diffusion, sign, dt, entrain, eta_surface;
     int32_t with_source;
     const void* source;       // optional explicit per-cell source (powder_step's `source`)
+    const uint8_t* active;    // optional per tile: phi non-zero within its 3^D tile neighbourhood
 };
+
+// The backtrace of one RK3 step moves less than a tile (|u| dt < 1 cell), so a
+// cell whose tile has phi = 0 in all its 3^D neighbour tiles advects exactly 0:
+// those cells skip the velocity sampling (the result is bit-identical).
+template <int D, typename R>
+__global__ void k_phi_tiles(mlbm_level_t lv, mlbm_fields_t src, uint8_t* __restrict__ tflag) {
+    constexpr int T = Geo<D>::T;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= live_tiles(lv)) return;
+    const FieldsT<R> f = fields_of<R>(src);
+    const R* phi = &f.at(fi_phi<D>(), (int64_t)t * T);
+    uint8_t nz = 0;
+    for (int i = 0; i < T && !nz; ++i) nz = phi[i] != R(0);
+    tflag[t] = nz;
+}
+
+template <int D>
+__global__ void k_phi_region(mlbm_level_t lv, const uint8_t* __restrict__ tflag, uint8_t* __restrict__ active) {
+    constexpr int NB = Geo<D>::NB;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= live_tiles(lv)) return;
+    uint8_t a = 0;
+    for (int k = 0; k < NB && !a; ++k) {
+        const int s = lv.nbr[(int64_t)t * NB + k];
+        a = s >= 0 ? tflag[s] : 0;
+    }
+    active[t] = a;
+}
 
 template <int D, typename R>
 __global__ void k_powder_advect(PowderArgs A) {
@@ -1149,6 +1178,10 @@ __global__ void k_powder_advect(PowderArgs A) {
     if (c >= (int64_t)live_tiles(A.lv) * T) return;
     const FieldsT<R> src = fields_of<R>(A.src), dst = fields_of<R>(A.dst);
     const int slot = (int)(c / T), lc = (int)(c % T);
+    if (A.active && !A.active[slot]) {       // no powder within reach: exactly 0
+        ((R*)A.tmp)[c] = R(0);
+        return;
+    }
     const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
     double pos[D];
     for (int a = 0; a < D; ++a) pos[a] = (double)(A.lv.tile_xyz[slot * 3 + a] * 4 + l3[a]);
@@ -2828,20 +2861,35 @@ extern "C" int mlbm_stress_raster_surface(const mlbm_level_t* lv0, int32_t n, co
 }
 
 extern "C" int mlbm_powder(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm_fields_t dst, void* ras,
-                           int64_t rs, void* tmp, double diffusion, double sign, double dt,
-                           double entrain, double eta_surface, int32_t with_source, int32_t dtype,
-                           void* stream) {
+                           int64_t rs, void* tmp, uint8_t* tile_ws, double diffusion, double sign,
+                           double dt, double entrain, double eta_surface, int32_t with_source,
+                           int32_t dtype, void* stream) {
     const int T = lv0->dim == 2 ? 16 : 64;
     const int64_t n = (int64_t)lv0->n_tiles * T;
     if (n == 0) return 0;
-    PowderArgs A{*lv0, src, dst, ras, rs, tmp, diffusion, sign, dt, entrain, eta_surface, with_source, nullptr};
+    PowderArgs A{*lv0, src, dst, ras, rs, tmp, diffusion, sign, dt, entrain, eta_surface, with_source,
+                 nullptr, tile_ws ? tile_ws + lv0->n_tiles : nullptr};
     cudaStream_t s = as_stream(stream);
+    const int nt = lv0->n_tiles;
+    int k = 2;
+    if (tile_ws) {
+        k += 2;
+        if (lv0->dim == 2) {
+            if (dtype) k_phi_tiles<2, double><<<nblk(nt, 128), 128, 0, s>>>(*lv0, src, tile_ws);
+            else k_phi_tiles<2, float><<<nblk(nt, 128), 128, 0, s>>>(*lv0, src, tile_ws);
+            k_phi_region<2><<<nblk(nt, 128), 128, 0, s>>>(*lv0, tile_ws, tile_ws + nt);
+        } else {
+            if (dtype) k_phi_tiles<3, double><<<nblk(nt, 128), 128, 0, s>>>(*lv0, src, tile_ws);
+            else k_phi_tiles<3, float><<<nblk(nt, 128), 128, 0, s>>>(*lv0, src, tile_ws);
+            k_phi_region<3><<<nblk(nt, 128), 128, 0, s>>>(*lv0, tile_ws, tile_ws + nt);
+        }
+    }
 #define PW(D, R) do { k_powder_advect<D, R><<<nblk(n, 128), 128, 0, s>>>(A); \
                       k_powder_diffuse<D, R><<<nblk(n, 128), 128, 0, s>>>(A); } while (0)
     if (lv0->dim == 2) { if (dtype) PW(2, double); else PW(2, float); }
     else { if (dtype) PW(3, double); else PW(3, float); }
 #undef PW
-    return launch_status(2);
+    return launch_status(k);
 }
 
 extern "C" int mlbm_diag_level(const mlbm_level_t* lv, mlbm_fields_t f, double vol, int32_t dtype,
@@ -2914,7 +2962,7 @@ extern "C" int mlbm_powder_step(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm
     const int T = lv0->dim == 2 ? 16 : 64;
     const int64_t n = (int64_t)lv0->n_tiles * T;
     if (n == 0) return 0;
-    PowderArgs A{*lv0, src, dst, nullptr, 0, tmp, diffusion, sign, dt, 0.0, 0.0, 0, source};
+    PowderArgs A{*lv0, src, dst, nullptr, 0, tmp, diffusion, sign, dt, 0.0, 0.0, 0, source, nullptr};
     cudaStream_t s = as_stream(stream);
 #define PW(D, R) do { k_powder_advect<D, R><<<nblk(n, 128), 128, 0, s>>>(A); \
                       k_powder_diffuse<D, R><<<nblk(n, 128), 128, 0, s>>>(A); } while (0)

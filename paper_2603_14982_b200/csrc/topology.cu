@@ -366,19 +366,50 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
             sown[i] = v;
         }
         __syncthreads();
-        const int b[3] = {l[0], l[1], D == 3 ? l[2] : 0};   // window origin = cell - 2 + 2
-#pragma unroll 1
-        for (int dz = (D == 3 ? 0 : 2); dz <= (D == 3 ? 4 : 2); ++dz)
+        // id: a coarser owner within Chebyshev 2; iu: a finer owner within 1 —
+        // box dilations of two indicator bits, done separably over the window
+        // (x over the tile's 4 columns, then y, then z) instead of a 5^D scan
+        // per cell
+        __shared__ uint8_t sx[D == 3 ? 4 * 8 * 8 : 4 * 8], sy[D == 3 ? 4 * 4 * 8 : 16];
+        auto bits = [&](int i) -> uint8_t {
+            const int own = sown[i];
+            return (uint8_t)((own > level ? 1 : 0) | (own >= 0 && own < level ? 2 : 0));
+        };
+        for (int i = lc; i < (D == 3 ? 256 : 32); i += T) {            // x pass
+            const int x = i & 3, y = (i >> 2) & 7, z = D == 3 ? i >> 5 : 0;
+            const int row = 8 * y + 64 * z;
+            uint8_t v = 0;
 #pragma unroll
-            for (int dy = 0; dy <= 4; ++dy)
+            for (int dx = -2; dx <= 2; ++dx) {
+                const uint8_t q = bits(row + x + 2 + dx);
+                v |= (q & 1) | ((dx >= -1 && dx <= 1) ? (q & 2) : 0);
+            }
+            sx[i] = v;
+        }
+        __syncthreads();
+        for (int i = lc; i < (D == 3 ? 128 : 16); i += T) {            // y pass
+            const int x = i & 3, y = (i >> 2) & 3, z = D == 3 ? i >> 4 : 0;
+            uint8_t v = 0;
 #pragma unroll
-                for (int dx = 0; dx <= 4; ++dx) {
-                    const int idx = (b[0] + dx) + 8 * (b[1] + dy) + (D == 3 ? 64 * (b[2] + dz) : 0);
-                    const int own = sown[idx];
-                    const int dist = max(max(abs(dx - 2), abs(dy - 2)), abs(dz - 2));
-                    if (own > level) id = true;
-                    if (own >= 0 && own < level && dist <= 1) iu = true;
-                }
+            for (int dy = -2; dy <= 2; ++dy) {
+                const uint8_t q = sx[x + 4 * (y + 2 + dy) + 32 * z];
+                v |= (q & 1) | ((dy >= -1 && dy <= 1) ? (q & 2) : 0);
+            }
+            sy[i] = v;
+        }
+        __syncthreads();
+        uint8_t v = 0;
+        if constexpr (D == 3) {
+#pragma unroll
+            for (int dz = -2; dz <= 2; ++dz) {
+                const uint8_t q = sy[l[0] + 4 * l[1] + 16 * (l[2] + 2 + dz)];
+                v |= (q & 1) | ((dz >= -1 && dz <= 1) ? (q & 2) : 0);
+            }
+        } else {
+            v = sy[l[0] + 4 * l[1]];
+        }
+        id = v & 1;
+        iu = (v & 2) != 0;
         if (id && iu) report_error(err, MLBM_ERR_TOPOLOGY, level, g[0], g[1], g[2], 1);
         if (id && level == h.levels - 1) report_error(err, MLBM_ERR_TOPOLOGY, level, g[0], g[1], g[2], 2);
         if (iu && level == 0) report_error(err, MLBM_ERR_TOPOLOGY, level, g[0], g[1], g[2], 3);
