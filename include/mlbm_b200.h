@@ -176,7 +176,11 @@ int mlbm_build_neighbors(const mlbm_level_t* lv, int32_t* nbr, void* stream);
 /* Per-cell classification of one level (sparse_grid.py:468-544
  * classify_interfaces, solver.py:177-273 _LevelTables): I^d / I^u ghosts,
  * BC layer, solid, active, per-direction bounce-back / self-source masks,
- * tile flags.  counts[0] += |I^d|, counts[1] += |I^u|; violations -> err. */
+ * tile flags.  counts[0] += |I^d|, counts[1] += |I^u|; violations -> err.
+ * Incremental (dirty non-NULL, over the level's tile grid): a tile not marked
+ * dirty copies its flags / masks / tile flag from the old arrays at
+ * old_slot[tile] (NULL: the same slot) instead of being classified; dirty =
+ * the tiles within one tile of a kind change at any level (mlbm_bitmap_op). */
 /* the static near-solid map of one level over its whole tile grid (1 where a
  * solid box or the heightmap reaches within one cell of the tile; periodic
  * seams always 1), read by mlbm_classify_level instead of rescanning the
@@ -186,7 +190,20 @@ int mlbm_solid_near(const mlbm_level_t* lv, const mlbm_solid_t* solid, uint8_t* 
 int mlbm_classify_level(const mlbm_level_t* lv, const mlbm_hier_t* h,
                         const mlbm_bc_t* bc, const mlbm_solid_t* solid,
                         uint8_t* cell_flags, uint64_t* dir_masks, uint8_t* tile_flags,
-                        int32_t* counts, mlbm_error_t* err, void* stream);
+                        int32_t* counts, mlbm_error_t* err, const uint8_t* dirty,
+                        const int32_t* old_slot, const uint8_t* old_cf,
+                        const uint64_t* old_masks, const uint8_t* old_tf, void* stream);
+/* the tiles of a level whose kind differs between two kind grids (stable
+ * compaction; count[0] = how many; ws: mlbm_ws_bytes(n)), and the scatter of
+ * the dirty maps of mlbm_classify_level: for every changed tile of `level` and
+ * every level l with dirty[l] non-NULL, the level-l tiles within one tile of the
+ * region it covers are marked 1 (dirty maps zeroed by the caller) */
+int mlbm_changed_tiles(int64_t n, const uint8_t* old_kind, const uint8_t* new_kind, int32_t* list,
+                       int32_t* count, void* ws, int64_t ws_bytes, void* stream);
+int mlbm_mark_dirty(const mlbm_hier_t* h, int32_t level, const int32_t* list,
+                    const int32_t* count, uint8_t* const* dirty, void* stream);
+/* device-to-device copy on the stream */
+int mlbm_copy(void* dst, const void* src, int64_t bytes, void* stream);
 
 /* Compacts the I^d (which = 0) / I^u (which = 1) cells of `lv` in cell order
  * and builds their 2^dim stencils into the coarser / finer level `other`
@@ -204,7 +221,8 @@ int mlbm_seed_tiles(int32_t dim, int32_t n, const void* x, int64_t xstride, int3
 /* out = op(in) over a level's tile grid (dims = child grid for group ops):
  * op 0 align_up (adapt.py:77-81), 1 parents (adapt.py:84-87; out on the parent
  * grid), 2 or-into (out |= in), 3 and-not (out &= ~in), 4 copy, 5 fill ones,
- * 6 leaf-of-kind (out = kind == 1). */
+ * 6 leaf-of-kind (out = kind == 1), 7 non-zero, 8 differs (out = out != in),
+ * 9 raw copy, 10 or-parent (out |= in at the parent tile; dims = child grid). */
 int mlbm_bitmap_op(int32_t op, int32_t dim, const int32_t dims[3], const uint8_t* in,
                    uint8_t* out, void* stream);
 

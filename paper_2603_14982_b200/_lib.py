@@ -135,7 +135,10 @@ _SIGS = {
     "mlbm_compact_tiles": [I32, P, P, P, P, P, P, P, I32, P, P, I64, P],
     "mlbm_build_neighbors": [C.POINTER(Level), P, P],
     "mlbm_classify_level": [C.POINTER(Level), C.POINTER(Hier), C.POINTER(BC),
-                            C.POINTER(Solid), P, P, P, P, P, P],
+                            C.POINTER(Solid), P, P, P, P, P, P, P, P, P, P, P],
+    "mlbm_copy": [P, P, I64, P],
+    "mlbm_changed_tiles": [I64, P, P, P, P, P, I64, P],
+    "mlbm_mark_dirty": [C.POINTER(Hier), I32, P, P, P, P],
     "mlbm_build_interface": [C.POINTER(Level), C.POINTER(Level), I32, P, P, P, P,
                              P, I64, P],
     "mlbm_seed_tiles": [I32, I32, P, I64, I32, P, P, P, P],
@@ -325,6 +328,13 @@ def unpack_cols(buf, view, add=False):
     dt = 1 if view.dtype == torch.float64 else 0
     check(lib().mlbm_halo_unpack(ptr(buf), ptr(view), view.stride(0), view.shape[0], 0, view.shape[1],
                                  dt, 1 if add else 0, stream_handle()), "halo_unpack")
+
+
+def copy(dst, src):
+    """Device-to-device copy of a whole contiguous tensor on the stream."""
+    assert dst.is_contiguous() and src.is_contiguous() and dst.numel() == src.numel()
+    check(lib().mlbm_copy(ptr(dst), ptr(src), src.numel() * src.element_size(), stream_handle()),
+          "copy")
 
 
 def fill(t, value):

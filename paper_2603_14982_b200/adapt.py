@@ -116,6 +116,11 @@ class GridAdaptor:
         self._stor = [z(k) for k in n]
         self._tmp = [z(k) for k in n]
         self._new = [z(k) for k in n]
+        # incremental classification after a rebuild: changed-tile lists and
+        # the dirty maps the classification reads
+        self._chg_list = [torch.zeros(k, dtype=torch.int32, device=dev) for k in n]
+        self._chg_n = torch.zeros(len(n), dtype=torch.int32, device=dev)
+        self._dirty = [z(k) for k in n]
         self._seeds = z(n[0])
         # [changed L][violations 3][pad][new tile counts L][fresh tile counts L]
         self._status = torch.zeros(3 * topology.levels + 4, dtype=torch.int32, device=dev)
@@ -343,10 +348,34 @@ class GridAdaptor:
         conv = 0 if self.rescale_convention == "derived" else 1
         init = {l: bool(fresh[l]) for l in changed}
         latest_only = latest_only or {}
+        Lv = topo.levels
+        # the classification that follows is incremental: it reads these dirty
+        # maps (tiles within one tile of a kind change at any level)
+        topo._dirty = {l: self._dirty[l] for l in range(Lv)}
+        topo._dirty_changed = set(changed)
+
+        def dirty_maps():
+            # sparse: the changed tiles of each changed level (compacted), then
+            # their one-tile neighbourhoods marked at every level
+            for l in range(Lv):
+                L.zero(self._dirty[l])
+            h = topo.hier_struct()
+            arr = (L.C.c_void_p * Lv)(*[t.data_ptr() for t in self._dirty])
+            for l in changed:
+                n = self._new[l].numel()
+                ws = topo.workspace(n)
+                L.check(L.lib().mlbm_changed_tiles(n, L.ptr(topo.lv[l].kind), L.ptr(self._new[l]),
+                                                   L.ptr(self._chg_list[l]), L.ptr(self._chg_n[l:l + 1]),
+                                                   L.ptr(ws), ws.numel(), L.stream_handle()),
+                        "changed_tiles")
+                L.check(L.lib().mlbm_mark_dirty(L.C.byref(h), l, L.ptr(self._chg_list[l]),
+                                                L.ptr(self._chg_n[l:l + 1]), arr, L.stream_handle()),
+                        "mark_dirty")
 
         def device():
             lib = L.lib()
             s = L.stream_handle()
+            dirty_maps()
             for l in changed:
                 topo.compact(l, self._new[l])
             for l in changed:

@@ -197,6 +197,12 @@ struct IfaceFlag {      // interface target: a live cell with the ghost bit
     }
 };
 
+struct ChangedFlag {     // a tile whose kind differs between two kind grids
+    const uint8_t* a;
+    const uint8_t* b;
+    __device__ bool operator()(int64_t g) const { return a[g] != b[g]; }
+};
+
 struct TargetWriter {
     int32_t* targets;
     __device__ void operator()(int64_t g, bool f, int pos) const {
@@ -245,15 +251,45 @@ __device__ int owner_of(const mlbm_hier_t& h, int l, const int (&c)[3]) {
     return -1;
 }
 
+// incremental classification after a topology change: a tile whose tile
+// neighbourhood saw no kind change at any level (dirty == 0) keeps its
+// classification, copied from its old slot
+struct ClassifyPrev {
+    const uint8_t* dirty;      // the level's tile grid, or null: classify every tile
+    const int32_t* old_slot;   // new slot -> old slot (null: unchanged slots)
+    const uint8_t* cf;         // old cell flags / masks / tile flags
+    const uint64_t* masks;
+    const uint8_t* tf;
+};
+
 template <int D>
 __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hier_t h, mlbm_bc_t bc,
                                                      mlbm_solid_t solid, uint8_t* cell_flags,
                                                      uint64_t* dir_masks, uint8_t* tile_flags,
-                                                     int32_t* counts, mlbm_error_t* err) {
+                                                     int32_t* counts, mlbm_error_t* err,
+                                                     ClassifyPrev prev) {
     constexpr int T = Geo<D>::T, NB = Geo<D>::NB, Q = Geo<D>::Q;
     const int tile = blockIdx.x, lc = threadIdx.x;
     const int level = lv.level;
     if (tile >= live_tiles(lv)) return;      // block-uniform
+    if (prev.dirty) {
+        const int t3[3] = {lv.tile_xyz[tile * 3], lv.tile_xyz[tile * 3 + 1], lv.tile_xyz[tile * 3 + 2]};
+        const int os = prev.old_slot ? prev.old_slot[tile] : tile;
+        if (os >= 0 && !prev.dirty[gidx3(lv.tiles, t3[0], t3[1], t3[2])]) {   // block-uniform
+            const int64_t oc = (int64_t)os * T + lc, nc = (int64_t)tile * T + lc;
+            const uint8_t f = prev.cf[oc];
+            cell_flags[nc] = f;
+            dir_masks[nc] = prev.masks[oc];
+            const int nid = __syncthreads_count(f & MLBM_CF_GHOST_D);
+            const int niu = __syncthreads_count(f & MLBM_CF_GHOST_U);
+            if (lc == 0) {
+                if (nid) atomicAdd(&counts[0], nid);
+                if (niu) atomicAdd(&counts[1], niu);
+                tile_flags[tile] = prev.tf[os];
+            }
+            return;
+        }
+    }
     __shared__ int snb[NB];
     if (lc < NB) snb[lc] = lv.nbr[(int64_t)tile * NB + lc];
     const int tx[3] = {lv.tile_xyz[tile * 3], lv.tile_xyz[tile * 3 + 1], lv.tile_xyz[tile * 3 + 2]};
@@ -566,6 +602,16 @@ __global__ void k_bitmap_op(int op, int dim, I3 d, const uint8_t* in, uint8_t* o
     case 5: out[g] = 1; break;
     case 6: out[g] = in[g] == 1 ? 1 : 0; break;
     case 7: out[g] = in[g] != 0 ? 1 : 0; break;
+    case 8: out[g] = out[g] != in[g] ? 1 : 0; break;        // differs (out: a raw copy)
+    case 9: out[g] = in[g]; break;                          // raw copy
+    case 10: {                                              // out |= in at the parent tile
+        I3 pd = d;
+        for (int a = 0; a < dim; ++a) pd.v[a] = d.v[a] / 2;
+        int q[3] = {x[0], x[1], x[2]};
+        for (int a = 0; a < dim; ++a) q[a] >>= 1;
+        out[g] = out[g] | (in[gidx3(pd.v, q[0], q[1], q[2])] ? 1 : 0);
+        break;
+    }
     }
 }
 
@@ -887,17 +933,26 @@ extern "C" int mlbm_build_neighbors(const mlbm_level_t* lv, int32_t* nbr, void* 
 extern "C" int mlbm_classify_level(const mlbm_level_t* lv, const mlbm_hier_t* h, const mlbm_bc_t* bc,
                                    const mlbm_solid_t* solid, uint8_t* cell_flags, uint64_t* dir_masks,
                                    uint8_t* tile_flags, int32_t* counts, mlbm_error_t* err,
-                                   void* stream) {
+                                   const uint8_t* dirty, const int32_t* old_slot, const uint8_t* old_cf,
+                                   const uint64_t* old_masks, const uint8_t* old_tf, void* stream) {
     if (lv->n_tiles == 0) return 0;
+    if (dirty && (!old_cf || !old_masks || !old_tf)) return -1;
     cudaStream_t s = as_stream(stream);
     if (counts) cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), s);
+    const ClassifyPrev prev{dirty, old_slot, old_cf, old_masks, old_tf};
     if (lv->dim == 2)
         k_classify<2><<<lv->n_tiles, 16, 0, s>>>(*lv, *h, *bc, *solid, cell_flags, dir_masks,
-                                                 tile_flags, counts, err);
+                                                 tile_flags, counts, err, prev);
     else
         k_classify<3><<<lv->n_tiles, 64, 0, s>>>(*lv, *h, *bc, *solid, cell_flags, dir_masks,
-                                                 tile_flags, counts, err);
+                                                 tile_flags, counts, err, prev);
     return launch_status(1);
+}
+
+extern "C" int mlbm_copy(void* dst, const void* src, int64_t bytes, void* stream) {
+    if (bytes <= 0) return 0;
+    const cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, as_stream(stream));
+    return e == cudaSuccess ? 0 : -(int)e;
 }
 
 extern "C" int mlbm_build_interface(const mlbm_level_t* lv, const mlbm_level_t* other, int32_t which,
@@ -1180,5 +1235,72 @@ extern "C" int mlbm_solid_near(const mlbm_level_t* lv, const mlbm_solid_t* solid
     for (int l = 0; l < MLBM_MAX_LEVELS; ++l) sl.near[l] = nullptr;
     if (lv->dim == 2) k_solid_near<2><<<blocks_for(n, 128), 128, 0, s>>>(*lv, sl, near);
     else k_solid_near<3><<<blocks_for(n, 128), 128, 0, s>>>(*lv, sl, near);
+    return launch_status(1);
+}
+
+// ---------------------------------------------------------------------------
+// Dirty tiles of an incremental classification, sparse: the tiles whose kind
+// changed at one level (compacted list), and for every level the tiles within
+// one tile of the region each changed tile covers (marked by scatter).
+extern "C" int mlbm_changed_tiles(int64_t n, const uint8_t* old_kind, const uint8_t* new_kind,
+                                  int32_t* list, int32_t* count, void* ws, int64_t ws_bytes,
+                                  void* stream) {
+    if (n <= 0) return 0;
+    if (ws_bytes < mlbm_ws_bytes(n)) return -1;
+    cudaStream_t s = as_stream(stream);
+    int32_t* bsum = (int32_t*)((char*)ws + align256(4 * n));
+    const int nb = flag_blocks(n);
+    const ChangedFlag fl{old_kind, new_kind};
+    k_flag_count<<<nb, CB, 0, s>>>(n, fl, bsum);
+    k_scan_blocks<<<1, 1024, 0, s>>>(nb, bsum, count);
+    k_flag_scatter<<<nb, CB, 0, s>>>(n, fl, bsum, TargetWriter{list});
+    return launch_status(3);
+}
+
+namespace mlbm {
+__global__ void k_mark_dirty(mlbm_hier_t h, int m, const int32_t* __restrict__ list,
+                             const int32_t* __restrict__ count, uint8_t* d0, uint8_t* d1, uint8_t* d2,
+                             uint8_t* d3, uint8_t* d4, uint8_t* d5) {
+    uint8_t* dirty[6] = {d0, d1, d2, d3, d4, d5};
+    const int dim = h.dim;
+    const int nc = *count;
+    const I3 dm = tdims_of(h, m);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)nc * h.levels;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(i / h.levels), l = (int)(i % h.levels);
+        if (!dirty[l]) continue;
+        int t[3];
+        gdec3(dm.v, list[j], t[0], t[1], t[2]);
+        const I3 dl = tdims_of(h, l);
+        int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};       // level-l tiles, inclusive, before dilation
+        for (int a = 0; a < 3; ++a) {
+            if (a >= dim) continue;
+            if (m >= l) { lo[a] = t[a] << (m - l); hi[a] = ((t[a] + 1) << (m - l)) - 1; }
+            else { lo[a] = t[a] >> (l - m); hi[a] = lo[a]; }
+            lo[a] -= 1;
+            hi[a] += 1;
+        }
+        for (int z = lo[2]; z <= hi[2]; ++z)
+            for (int y = lo[1]; y <= hi[1]; ++y)
+                for (int x = lo[0]; x <= hi[0]; ++x) {
+                    int c[3] = {x, y, z};
+                    bool in = true;
+                    for (int a = 0; a < 3; ++a) {
+                        if (a >= dim) { c[a] = 0; continue; }
+                        if (h.periodic[a]) c[a] = (c[a] % dl.v[a] + dl.v[a]) % dl.v[a];
+                        else in &= c[a] >= 0 && c[a] < dl.v[a];
+                    }
+                    if (in) dirty[l][gidx3(dl.v, c[0], c[1], c[2])] = 1;
+                }
+    }
+}
+}  // namespace mlbm
+
+extern "C" int mlbm_mark_dirty(const mlbm_hier_t* h, int32_t level, const int32_t* list,
+                               const int32_t* count, uint8_t* const* dirty, void* stream) {
+    uint8_t* d[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    for (int l = 0; l < h->levels && l < 6; ++l) d[l] = dirty[l];
+    k_mark_dirty<<<148 * 4, 128, 0, as_stream(stream)>>>(*h, level, list, count, d[0], d[1], d[2], d[3],
+                                                         d[4], d[5]);
     return launch_status(1);
 }

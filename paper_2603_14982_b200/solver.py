@@ -235,6 +235,12 @@ def build_tables(topo: Topology, bc, solid, err, tables=None, only=None):
     s = L.stream_handle()
     T = TILE ** topo.d
     tables = dict(tables or {})
+    fresh = set()                       # levels whose tables are (re)allocated here
+
+    def fresh_ok(t, l):
+        return l not in fresh
+    if not hasattr(topo, "_dirty"):
+        topo._dirty, topo._dirty_changed = None, set()
     hier = topo.hier_struct()
     NC = 1 << topo.d
     scratch = torch.zeros((topo.levels, 2), dtype=torch.int32, device=topo.device) \
@@ -253,13 +259,28 @@ def build_tables(topo: Topology, bc, solid, err, tables=None, only=None):
                     torch.full((cap * T, NC), -1, dtype=torch.int32, device=topo.device),
                     cap * T)
             tables[l] = t
+            fresh.add(l)
         if not cap or (only is not None and l not in only):
             continue
         lvs = topo.level_struct(l)
+        # incremental after a topology change (adapt._prepare left the dirty
+        # maps): tiles with no kind change within one tile at any level copy
+        # their classification from the old arrays
+        dirty = (topo._dirty or {}).get(l) if only is not None and fresh_ok(t, l) else None
+        prev = (None,) * 4
+        if dirty is not None:
+            if getattr(t, "prev", None) is None or t.prev[0].numel() != t.cell_flags.numel():
+                t.prev = (torch.empty_like(t.cell_flags), torch.empty_like(t.dir_masks),
+                          torch.empty_like(t.tile_flags))
+            for a, b in zip(t.prev, (t.cell_flags, t.dir_masks, t.tile_flags)):
+                L.copy(a, b)
+            old_slot = topo.lv[l].old_slot if l in topo._dirty_changed else None
+            prev = (old_slot,) + t.prev
         L.check(lib.mlbm_classify_level(L.C.byref(lvs), L.C.byref(hier), L.C.byref(bc),
                                         L.C.byref(solid), L.ptr(t.cell_flags),
                                         L.ptr(t.dir_masks), L.ptr(t.tile_flags),
-                                        L.ptr(scratch[l]), L.ptr(err), s), "classify_level")
+                                        L.ptr(scratch[l]), L.ptr(err), L.ptr(dirty),
+                                        *[L.ptr(x) for x in prev], s), "classify_level")
     for l, t in tables.items():
         if not topo.lv[l].cap or (only is not None and l not in only):
             continue
@@ -275,6 +296,7 @@ def build_tables(topo: Topology, bc, solid, err, tables=None, only=None):
             L.check(lib.mlbm_build_interface(L.C.byref(lv_a), L.C.byref(lv_b), which,
                                              L.ptr(tg), L.ptr(src), L.ptr(cnt), L.ptr(err),
                                              L.ptr(ws), ws.numel(), s), "build_interface")
+    topo._dirty, topo._dirty_changed = None, set()       # consumed
     return tables
 
 

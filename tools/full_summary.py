@@ -18,7 +18,7 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio"]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6}
 ki = h.index("Kernel Name")
-lines = ["# ncu --set full --clock-control none (tools/round_evidence.sh), C2 eager pass "
+lines = ["# ncu --set full --clock-control none (tools/round_evidence.sh), eager pass "
          "(tools/kernel_probe.py), one block per launch", ""]
 traffic = collections.defaultdict(list)
 for r in rows[2:]:
