@@ -1068,69 +1068,61 @@ int launch_level(const StepArgs& a, int mode, cudaStream_t s) {
 // loop of 12 x 8 dependent-address loads was latency-bound at ~12 % warps
 // active); the S rescale takes u from lanes 1..D of the group by shuffles.
 template <int D, typename R>
-__global__ void downward_kernel(int n, const int32_t* __restrict__ n_dev, const int32_t* __restrict__ targets,
-                                const int32_t* __restrict__ srcs,
-                                const int32_t* __restrict__ tile_xyz,
-                                FieldsT<R> olda, FieldsT<R> newa, FieldsT<R> dst,
-                                int step, R kappa) {
-    constexpr int NC = Geo<D>::NC, T = Geo<D>::T, NM = Geo<D>::NM;
+__global__ void __launch_bounds__(128) downward_kernel(int n, const int32_t* __restrict__ n_dev,
+                                                       const int32_t* __restrict__ targets,
+                                                       const int32_t* __restrict__ srcs,
+                                                       FieldsT<R> olda, FieldsT<R> newa, FieldsT<R> dst,
+                                                       int step, R kappa) {
+    // one thread per target cell: consecutive targets of a warp read each
+    // row at neighbouring coarse cells and write it at neighbouring fine cells
+    // (coalesced), where a 16-lane group per target touched 16 rows of one
+    // cell per instruction (one sector per lane: l1tex-bound, 0.4 ms per C4
+    // launch)
+    constexpr int NC = Geo<D>::NC, T = Geo<D>::T, NM = Geo<D>::NM, NS = Geo<D>::NS;
     constexpr int NV = NM + 2;   // moments + eps + phi
-    static_assert(NV <= 16, "one 16-lane group per target");
-    (void)tile_xyz;
-    const int q = threadIdx.x & 15;
     const int live = n_dev ? __ldg(n_dev) : n;
-    const int groups = (gridDim.x * blockDim.x) >> 4;
-    const int base = threadIdx.x & ~15 & 31;
-    // grid-stride over the live targets (the launch is sized by the SM count,
-    // not by the interface capacity)
-    for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;; j += groups) {
-        if (__all_sync(0xffffffffu, j >= live)) break;      // warp-uniform exit
-        const bool on = j < live;
-        int tgt = 0;
-        R val = R(0);
-        if (on && q < NV) {
-            tgt = targets[j];
-            const int lc = tgt % T;
-            const int par[3] = {lc & 1, (lc >> 2) & 1, (lc >> 4) & 1};
-            const int fk = q < NM ? q : (q == NM ? fi_eps<D>() : fi_phi<D>());
-            int sk[NC];
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < live; j += gridDim.x * blockDim.x) {
+        const int tgt = targets[j];
+        const int lc = tgt % T;
+        const int par[3] = {lc & 1, (lc >> 2) & 1, (lc >> 4) & 1};
+        int sk[NC];
+        R wk[NC];
 #pragma unroll
-            for (int k = 0; k < NC; ++k) sk[k] = __ldg(&srcs[(int64_t)j * NC + k]);
-            R xs[NC];
+        for (int k = 0; k < NC; ++k) {
+            sk[k] = __ldg(&srcs[(int64_t)j * NC + k]);
+            R w = R(1);
 #pragma unroll
-            for (int k = 0; k < NC; ++k) {
-                xs[k] = R(0);
-                if (sk[k] >= 0) {
-                    R x = olda.at(fk, sk[k]);
-                    if (step == 2) x = R(0.5) * (x + newa.at(fk, sk[k]));
-                    xs[k] = x;
-                }
+            for (int a = 0; a < D; ++a) {
+                const int o = (k >> a) & 1;
+                const R fr = par[a] ? R(0.5) : R(0);
+                w *= o ? fr : R(1) - fr;
             }
+            wk[k] = w;
+        }
+        R v[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const int fk = q < NM ? q : (q == NM ? fi_eps<D>() : fi_phi<D>());
+            R val = R(0);
 #pragma unroll
             for (int k = 0; k < NC; ++k) {
                 if (sk[k] < 0) continue;
-                R wk = R(1);
-#pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    const int o = (k >> a) & 1;
-                    const R fr = par[a] ? R(0.5) : R(0);
-                    wk *= o ? fr : R(1) - fr;
-                }
-                val += xs[k] * wk;
+                R x = olda.at(fk, sk[k]);
+                if (step == 2) x = R(0.5) * (x + newa.at(fk, sk[k]));
+                val += x * wk[k];
             }
+            v[q] = val;
         }
-        // S rescale: v_S = kappa (v_S - u_a u_b) + u_a u_b (lanes 1..D hold u)
-        R u[D];
+        // S rescale: v_S = kappa (v_S - u_a u_b) + u_a u_b
 #pragma unroll
-        for (int a = 0; a < D; ++a) u[a] = __shfl_sync(0xffffffffu, val, base + 1 + a);
-        if (on && q >= 1 + D && q < NM) {
-            const int k = q - 1 - D;
-            const R eq = u[s_a<D>(k)] * u[s_b<D>(k)];
-            val = kappa * (val - eq) + eq;
+        for (int k = 0; k < NS; ++k) {
+            const R eq = v[1 + s_a<D>(k)] * v[1 + s_b<D>(k)];
+            v[1 + D + k] = kappa * (v[1 + D + k] - eq) + eq;
         }
-        if (on && q < NV) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
             const int fk = q < NM ? q : (q == NM ? fi_eps<D>() : fi_phi<D>());
-            dst.at(fk, tgt) = val;
+            dst.at(fk, tgt) = v[q];
         }
     }
 }
@@ -1193,9 +1185,10 @@ extern "C" int mlbm_downward(int32_t dim, int32_t n, const int32_t* n_dev, const
     cudaStream_t s = as_stream(stream);
     static int sms = 0;
     if (!sms) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev); }
-    const int B = 256;
-    const int G = (int)std::min<int64_t>(((int64_t)n * 16 + B - 1) / B, (int64_t)sms * 8);
-#define DOWN(D, R) downward_kernel<D, R><<<G, B, 0, s>>>(n, n_dev, targets, src, tile_xyz, \
+    const int B = 128;
+    const int G = (int)std::min<int64_t>(((int64_t)n + B - 1) / B, (int64_t)sms * 16);
+    (void)tile_xyz;
+#define DOWN(D, R) downward_kernel<D, R><<<G, B, 0, s>>>(n, n_dev, targets, src, \
         fields_of<R>(olda), fields_of<R>(newa), fields_of<R>(dst), step, R(kappa))
     if (dim == 2) { if (dtype) DOWN(2, double); else DOWN(2, float); }
     else if (dim == 3) { if (dtype) DOWN(3, double); else DOWN(3, float); }

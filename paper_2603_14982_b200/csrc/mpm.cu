@@ -2087,17 +2087,17 @@ __device__ __forceinline__ void p2g_box_merge(const float* sacc, int NW, int MAX
     }
 }
 
-template <int D, int NW, int ROUNDS>
-__global__ void __launch_bounds__(32 * NW, P2G2_MIN_BLOCKS) k_p2g_cell2(PartArgs P, TopoL0 t0, MatParams mp, float* ras,
-                                                       int64_t rs, mlbm_error_t* err) {
-    constexpr int K = Geo<D>::K, NV = 3 + 3 * D, NS = D * (D + 1) / 2;
-    constexpr int MAXN = P2G2_MAXN, REC = 32, BT = 32 * NW;
-    extern __shared__ __align__(16) float p2g_smem[];
-    float* sacc = p2g_smem;                                  // [NW][NV][MAXN]
-    float* slab = p2g_smem + NW * NV * MAXN;                 // [NW][REC / 4][32] float4
+// Node boxes of the fp32 P2G kernel (k_p2g_cell2): the block's
+// box over all its rounds (use_smem: every warp accumulates into its own copy
+// of it), or, when it overflows P2G2_MAXN nodes, each warp's fixed window (its
+// middle particle's tile in x, y; the z layer pair its particles vote for) —
+// runs outside it take global atomics.  Zeroes the copies in use.
+template <int D, int NW, int ROUNDS, int NV>
+__device__ __forceinline__ void p2g2_boxes(const PartArgs& P, float* sacc, int p0, int (&lo)[3],
+                                           int (&ext)[3], int& nbox, bool& use_smem, bool& warp_box) {
+    constexpr int MAXN = P2G2_MAXN, BT = 32 * NW;
     __shared__ int s_lo[3], s_hi[3];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int p0 = blockIdx.x * (BT * ROUNDS);
     // block node box over all rounds
     if (threadIdx.x < 3) { s_lo[threadIdx.x] = 0x7fffffff; s_hi[threadIdx.x] = -0x7fffffff; }
     __syncthreads();
@@ -2140,15 +2140,17 @@ __global__ void __launch_bounds__(32 * NW, P2G2_MIN_BLOCKS) k_p2g_cell2(PartArgs
         }
     }
     __syncthreads();
-    int lo[3] = {0, 0, 0}, ext[3] = {1, 1, 1}, nbox = 1;
+    lo[0] = lo[1] = lo[2] = 0;
+    ext[0] = ext[1] = ext[2] = 1;
+    nbox = 1;
 #pragma unroll
     for (int a = 0; a < D; ++a) { lo[a] = s_lo[a]; ext[a] = s_hi[a] - s_lo[a] + 1; nbox *= ext[a]; }
-    const bool use_smem = nbox > 0 && nbox <= MAXN;        // block-uniform
+    use_smem = nbox > 0 && nbox <= MAXN;                   // block-uniform
     // a block whose box is too large (particles drifted since the last sort, a
     // tile run ends) accumulates per warp in its own copy over a fixed window
     // (the warp's tile in x, y; two z layers); runs outside it add to HBM
     // directly
-    const bool warp_box = !use_smem;
+    warp_box = !use_smem;
     if (warp_box) {
         constexpr int EX = D == 3 ? 6 : 10, EZ = D == 3 ? 4 : 1;
         static_assert(EX * EX * EZ <= MAXN, "warp window fits a per-warp copy");
@@ -2176,6 +2178,54 @@ __global__ void __launch_bounds__(32 * NW, P2G2_MIN_BLOCKS) k_p2g_cell2(PartArgs
         }
     }
     __syncthreads();
+}
+
+// Flush of the fp32 P2G node boxes into the raster rows: a warp window (the
+// warp's own copy, lanes striding over it) or the block box (sum of the NW
+// copies, after a block barrier).
+template <int D, int NW, int NV>
+__device__ __forceinline__ void p2g2_merge(const float* sacc, const int (&lo)[3], const int (&ext)[3], int nbox,
+                                           bool use_smem, bool warp_box, const TopoL0& t0, float* ras,
+                                           int64_t rs, mlbm_error_t* err) {
+    constexpr int MAXN = P2G2_MAXN;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (warp_box) {
+        __syncwarp();
+        const float* wa = sacc + wid * NV * MAXN;
+        for (int i = lane; i < nbox; i += 32) {
+            float tot[NV];
+#pragma unroll
+            for (int qv = 0; qv < NV; ++qv) tot[qv] = wa[qv * MAXN + i];
+            if (tot[0] == 0.f && tot[2 + 2 * D] == 0.f) continue;
+            int c[3];
+            box_coord<D>(i, lo, ext, c);
+            bool b2 = false;
+            const int64_t ni = node_index<D>(t0, c, b2);
+            if (ni < 0) { report_error(err, MLBM_ERR_STENCIL, 0, c[0], c[1], c[2]); continue; }
+#pragma unroll
+            for (int qv = 0; qv < NV; ++qv)
+                if (tot[qv] != 0.f) atomicAdd(&ras[qv * rs + ni], tot[qv]);
+        }
+        return;
+    }
+    if (!use_smem) return;
+    __syncthreads();
+    p2g_box_merge<D, NV, 0>(sacc, NW, MAXN, nbox, lo, ext, t0, ras, rs, err);
+}
+
+template <int D, int NW, int ROUNDS>
+__global__ void __launch_bounds__(32 * NW, P2G2_MIN_BLOCKS) k_p2g_cell2(PartArgs P, TopoL0 t0, MatParams mp, float* ras,
+                                                       int64_t rs, mlbm_error_t* err) {
+    constexpr int K = Geo<D>::K, NV = 3 + 3 * D, NS = D * (D + 1) / 2;
+    constexpr int MAXN = P2G2_MAXN, REC = 32, BT = 32 * NW;
+    extern __shared__ __align__(16) float p2g_smem[];
+    float* sacc = p2g_smem;                                  // [NW][NV][MAXN]
+    float* slab = p2g_smem + NW * NV * MAXN;                 // [NW][REC / 4][32] float4
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int p0 = blockIdx.x * (BT * ROUNDS);
+    int lo[3], ext[3], nbox;
+    bool use_smem, warp_box;
+    p2g2_boxes<D, NW, ROUNDS, NV>(P, sacc, p0, lo, ext, nbox, use_smem, warp_box);
 
     const int o[3] = {lane % 3, (lane / 3) % 3, D == 3 ? (lane / 9) % 3 : 0};
     const bool node_lane = lane < K;
@@ -2314,29 +2364,7 @@ __global__ void __launch_bounds__(32 * NW, P2G2_MIN_BLOCKS) k_p2g_cell2(PartArgs
         __syncwarp();                                     // slab reused next round
     }
     if (bad) report_error(err, MLBM_ERR_STENCIL, 0, cur[0], cur[1], cur[2]);
-    if (warp_box) {
-        // this warp's copy only (lanes stride over its box)
-        __syncwarp();
-        const float* wa = sacc + wid * NV * MAXN;
-        for (int i = lane; i < nbox; i += 32) {
-            float tot[NV];
-#pragma unroll
-            for (int qv = 0; qv < NV; ++qv) tot[qv] = wa[qv * MAXN + i];
-            if (tot[0] == 0.f && tot[2 + 2 * D] == 0.f) continue;
-            int c[3];
-            box_coord<D>(i, lo, ext, c);
-            bool b2 = false;
-            const int64_t ni = node_index<D>(t0, c, b2);
-            if (ni < 0) { report_error(err, MLBM_ERR_STENCIL, 0, c[0], c[1], c[2]); continue; }
-#pragma unroll
-            for (int qv = 0; qv < NV; ++qv)
-                if (tot[qv] != 0.f) atomicAdd(&ras[qv * rs + ni], tot[qv]);
-        }
-        return;
-    }
-    if (!use_smem) return;
-    __syncthreads();
-    p2g_box_merge<D, NV, 0>(sacc, NW, MAXN, nbox, lo, ext, t0, ras, rs, err);
+    p2g2_merge<D, NW, NV>(sacc, lo, ext, nbox, use_smem, warp_box, t0, ras, rs, err);
 }
 
 // Entrainment stress raster (coupling.py:283-294) in the P2G layout: sum over
