@@ -255,12 +255,19 @@ int mlbm_plan_level(int32_t n, const uint8_t* own, const uint8_t* storage,
  * arrays have h->levels entries; bar: 2 zero-initialised words.  Seeds come either
  * from the n positions x (stride xs) or, with n = 0 and ext_count non-NULL, from
  * mlbm_g2p of the same step (seeds filled, *ext_count = its leaf-invariant count,
- * consumed and reset to 0 here).  seeds are all zero again on return. */
+ * consumed and reset to 0 here).  seeds are all zero again on return.
+ * win (optional, int32 [2][levels][6], caller-owned, used only with ext_count):
+ * per level the tile window of the last pass (lo xyz, hi xyz inclusive; empty
+ * when lo > hi) and the bounding box of its non-zero kinds; the pass works
+ * inside max(last window, kinds box + 8 tiles, parent footprint of the finer
+ * window + 8 tiles) and writes both back (the top level, periodic axes and
+ * win = NULL span the whole grid).  Every bitmap buffer must be zero outside
+ * the windows: start from zeroed buffers and never shrink a window. */
 int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_t* const* cur,
                     uint8_t* const* eff, uint8_t* const* par, uint8_t* const* own,
                     uint8_t* const* nkind, uint8_t* const* stor, int16_t* const* streak,
                     uint8_t* seeds, const uint8_t* static_tiles, const double* x, int64_t xs,
-                    int32_t n, int32_t* ext_count, int32_t* status, mlbm_error_t* err,
+                    int32_t n, int32_t* ext_count, int32_t* win, int32_t* status, mlbm_error_t* err,
                     unsigned int* bar, void* stream);
 /* optional stage timestamps of the adapt passes into a caller-owned buffer of 64
  * uint64 (NULL: off); the library never allocates */

@@ -153,7 +153,7 @@ _SIGS = {
     "mlbm_migrate_level": [I32, I32, P, P, Fields, Fields, Fields, Fields, I32, P],
     "mlbm_init_new_cells": [C.POINTER(Hier), C.POINTER(Hier), I32, P, P, I32, P,
                             Fields, Fields, P, I32, I32, P, P],
-    "mlbm_adapt_pass": [C.POINTER(Hier), P, P, P, P, P, P, P, P, P, P, P, I64, I32, P, P, P, P,
+    "mlbm_adapt_pass": [C.POINTER(Hier), P, P, P, P, P, P, P, P, P, P, P, I64, I32, P, P, P, P, P,
                         P],
     "mlbm_adapt_set_timestamps": [P],
     "mlbm_adapt_bits_set_timestamps": [P],

@@ -134,6 +134,12 @@ class GridAdaptor:
         # and takes G2P's count of particles outside level-0 leaves from here
         self.ext_count = torch.zeros(1, dtype=torch.int32, device=dev)
         self.launches = 0
+        # tile windows of the G2P-seeded fused pass ([2][levels][6] int32, see
+        # mlbm_adapt_pass): valid for the key (host rebuilds, static mask) they
+        # were derived under; any other pass invalidates them
+        self.windows = True
+        self._win = torch.zeros(2 * topology.levels * 6, dtype=torch.int32, device=dev)
+        self._win_key = None
 
     @property
     def streak(self):
@@ -192,6 +198,7 @@ class GridAdaptor:
         (status[L:L+3]).  No host synchronisation (CUDA-graph capturable)."""
         if self.fused:
             return self._plan_fused(driver)
+        self._win_key = None                        # the per-op pass writes whole grids
         if driver.g2p_seeds:
             L.zero(self.ext_count)     # the per-op pass seeds from the positions itself
         self._seeds_dirty = True
@@ -256,6 +263,38 @@ class GridAdaptor:
             self._status[2 * Lv + 4 + l] = (nz & (topo.lv[l].kind == 0)).sum().to(torch.int32)
         self._invariants_device(driver)
 
+    def prepare_windows(self, static_tiles):
+        """(Re)derive the pass windows from the current kinds when the topology
+        was set from the host or the static mask changed (syncs; call outside
+        graph capture).  Returns whether windows are in use."""
+        if not self.windows:
+            return False
+        topo = self.topology
+        self._static(static_tiles)
+        key = (getattr(topo, "host_rebuilds", 0), self._static_key if static_tiles is not None else None)
+        if self._win_key == key:
+            return True
+        Lv = topo.levels
+        w = np.zeros((2, Lv, 6), dtype=np.int32)
+        w[:, :, :3] = np.iinfo(np.int32).max
+        w[:, :, 3:] = -np.iinfo(np.int32).max
+        for l in range(Lv - 1):
+            g = self._grids[l]
+            nz = torch.nonzero(topo.lv[l].kind.view(*g))
+            boxes = []
+            if nz.shape[0]:
+                boxes.append((nz.min(0).values.cpu().numpy(), nz.max(0).values.cpu().numpy()))
+            if l == 0 and static_tiles is not None:
+                st = np.nonzero(np.asarray(static_tiles).reshape(g))
+                if st[0].size:
+                    boxes.append((np.array([a.min() for a in st]), np.array([a.max() for a in st])))
+            for lo, hi in boxes:
+                w[1, l, :3] = np.minimum(w[1, l, :3], lo)
+                w[1, l, 3:] = np.maximum(w[1, l, 3:], hi)
+        self._win.copy_(torch.as_tensor(w.reshape(-1)))
+        self._win_key = key
+        return True
+
     def _plan_fused(self, driver):
         topo = self.topology
         if getattr(self, "_seeds_dirty", False):     # left set by the unfused path
@@ -266,6 +305,15 @@ class GridAdaptor:
         ext = self.ext_count if driver.g2p_seeds else None
         x = None if driver.g2p_seeds else driver.device_positions(topo.d, topo.device)
         st = self._static(driver.static_tiles)
+        win = None
+        if ext is not None and self.windows:
+            if torch.cuda.is_current_stream_capturing():
+                if self._win_key is not None:
+                    win = self._win                 # prepared before the capture
+            elif self.prepare_windows(driver.static_tiles):
+                win = self._win
+        if win is None:
+            self._win_key = None                    # a full-grid pass: re-derive next time
         h = topo.hier_struct()
         L.zero(self._status)
         L.check(L.lib().mlbm_adapt_pass(L.C.byref(h), arr(self._des), arr(self._cur),
@@ -274,7 +322,7 @@ class GridAdaptor:
                                         L.ptr(self._seeds),
                                         L.ptr(st), L.ptr(x), x.stride(0) if x is not None else 0,
                                         x.shape[1] if x is not None else 0,
-                                        L.ptr(ext),
+                                        L.ptr(ext), L.ptr(win),
                                         L.ptr(self._status),
                                         L.ptr(self._err), L.ptr(self._bar), L.stream_handle()),
                 "adapt_pass")

@@ -686,6 +686,8 @@ class CoupledSim:
         self.grid.sync_topology()
         self.grid.level0()
         self._ensure_host_status(adapt_now)
+        if self.adaptor is not None and self.adaptor.fused:
+            self.adaptor.prepare_windows(self.static_tiles)   # syncs: never inside a capture
         if fresh and self.precapture_steps:
             self._precapture(self.precapture_steps)
         flags = self._sort_flags(self.step_count, self._sorted_ahead, is_mpm, adapt_now)

@@ -53,6 +53,7 @@ struct AdaptArgs {
     unsigned int* bar;      // 2 words, zero-initialised once
     unsigned long long* ts; // optional stage timestamps (block 0), may be null
     int32_t* ext_count;     // particles outside level-0 leaves counted by G2P with the seeds (or null)
+    int32_t* win;           // [2][levels][6] tile windows (lo xyz, hi xyz; see k_adapt_pass) or null
 };
 
 __device__ __forceinline__ int64_t gi3(const int* d, int x, int y, int z) {
@@ -66,6 +67,19 @@ __device__ __forceinline__ void dec3(const int* d, int64_t g, int& x, int& y, in
     const unsigned r = q / d1;
     y = (int)(q - r * d1);
     x = (int)r;
+}
+
+// Tile window of one level in a pass: every bitmap of the level is zero
+// outside it (the arrays start zeroed and no pass writes outside its window;
+// windows never shrink).  n = number of tiles in it.
+struct Win {
+    int lo[3], ext[3];
+    int64_t n;
+};
+__device__ __forceinline__ int64_t win_tile(const Win& w, const int* d, int64_t i, int (&c)[3]) {
+    dec3(w.ext, i, c[0], c[1], c[2]);
+    c[0] += w.lo[0]; c[1] += w.lo[1]; c[2] += w.lo[2];
+    return gi3(d, c[0], c[1], c[2]);
 }
 
 __device__ void grid_barrier(unsigned int* bar) {
@@ -159,13 +173,16 @@ __device__ bool children_any(const uint8_t* src, const int* dc, int dim, const i
 // Hysteresis of one level (adapt.py:140-181): one thread per tile; the 2^dim
 // tiles of a sibling group sit in consecutive lanes, so "all siblings may
 // coarsen" is a 2^dim-lane AND over shuffles.
-__device__ void effective_stage(const AdaptArgs& A, int l, bool with_guard, int64_t tid, int64_t nth) {
+__device__ void effective_stage(const AdaptArgs& A, int l, bool with_guard, int64_t tid, int64_t nth,
+                                const Win& W) {
     const int* d = A.tdims[l];
     const int dim = A.dim;
     bool grouped = true;
     for (int a = 0; a < dim; ++a) grouped &= (d[a] % 2) == 0;
-    int gd[3] = {d[0], d[1], d[2]};
-    if (grouped) for (int a = 0; a < dim; ++a) gd[a] = d[a] / 2;
+    // sibling groups of the window (its bounds are group-aligned when grouped)
+    int gd[3] = {W.ext[0], W.ext[1], W.ext[2]}, g0[3] = {W.lo[0], W.lo[1], W.lo[2]};
+    if (grouped)
+        for (int a = 0; a < dim; ++a) { gd[a] = W.ext[a] / 2; g0[a] = W.lo[a] / 2; }
     const int K = grouped ? (1 << dim) : 1;
     const int64_t total = (int64_t)gd[0] * gd[1] * gd[2] * K;
     const uint8_t* par = A.par[l];
@@ -181,7 +198,8 @@ __device__ void effective_stage(const AdaptArgs& A, int l, bool with_guard, int6
             const int k = (int)(t - j * K);
             int x[3];
             dec3(gd, j, x[0], x[1], x[2]);
-            for (int a = 0; a < 3; ++a) c[a] = (grouped && a < dim) ? 2 * x[a] + ((k >> a) & 1) : x[a];
+            for (int a = 0; a < 3; ++a)
+                c[a] = (grouped && a < dim) ? 2 * (g0[a] + x[a]) + ((k >> a) & 1) : g0[a] + x[a];
             g = gi3(d, c[0], c[1], c[2]);
             cand = A.cur[l][g] && !A.des[l][g];
             const int16_t sv = cand ? (int16_t)(A.streak[l][g] + 1) : (int16_t)0;
@@ -360,6 +378,9 @@ __device__ __forceinline__ void stamp(const AdaptArgs& A, int k) {
 }
 #define STAMP_BARRIER(k) do { grid_barrier(A.bar); stamp(A, k); } while (0)
 
+#ifndef WIN_MARGIN
+#define WIN_MARGIN 8      // tiles added around the inputs of a level's window
+#endif
 #ifndef ADAPT_MINB
 #define ADAPT_MINB 2      // 64 registers, 2 x 512 threads per SM (explicit 1 lets ptxas take 69)
 #endif
@@ -369,6 +390,45 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
     const int dim = A.dim, L = A.levels;
     const int* d0 = A.tdims[0];
     const int64_t n0 = (int64_t)d0[0] * d0[1] * d0[2];
+    // tile windows of this pass (every block derives the same ones): the last
+    // pass's window, the bounding box of the kinds it produced widened by
+    // WIN_MARGIN tiles, and the parent footprint of the finer level's window
+    // widened the same way — wider than any chain of stages reaches from a
+    // non-zero input (seeds within 1 tile of a leaf, group alignment 1,
+    // dilations 2 + 2 + 3).  The top level, periodic axes and win = null
+    // span the whole grid.
+    __shared__ Win W[MLBM_MAX_LEVELS];
+    if (threadIdx.x == 0) {
+        for (int l = 0; l < L; ++l) {
+            const int* d = A.tdims[l];
+            bool grouped = true;
+            for (int a = 0; a < dim; ++a) grouped &= (d[a] % 2) == 0;
+            int lo[3], hi[3];
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = 0; hi[a] = d[a] - 1;
+                if (a >= dim || !A.win || l == L - 1 || A.periodic[a]) continue;
+                const int* cw = A.win + l * 6;
+                const int* nx = A.win + (L + l) * 6;
+                int wl = cw[a], wh = cw[3 + a];                   // empty: wl > wh
+                if (nx[a] <= nx[3 + a]) { wl = min(wl, nx[a] - WIN_MARGIN); wh = max(wh, nx[3 + a] + WIN_MARGIN); }
+                if (l > 0 && W[l - 1].n > 0) {
+                    wl = min(wl, (W[l - 1].lo[a] >> 1) - WIN_MARGIN);
+                    wh = max(wh, ((W[l - 1].lo[a] + W[l - 1].ext[a] - 1) >> 1) + WIN_MARGIN);
+                }
+                if (grouped) { wl &= ~1; wh |= 1; }
+                lo[a] = max(wl, 0);
+                hi[a] = min(wh, d[a] - 1);
+            }
+            int64_t n = 1;
+            for (int a = 0; a < 3; ++a) {
+                W[l].lo[a] = lo[a];
+                W[l].ext[a] = hi[a] >= lo[a] ? hi[a] - lo[a] + 1 : 0;
+                n *= W[l].ext[a];
+            }
+            W[l].n = n;
+        }
+    }
+    __syncthreads();
     stamp(A, 0);
 
     // ---- A: seeds <- static, invariants of the current topology, cur[0]
@@ -390,12 +450,11 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
     // (y -> nkind) and F (z + count), in buffers that are free until I/J
     for (int l = 0; l < L; ++l) {
         const int* d = A.tdims[l];
-        const int64_t n = (int64_t)d[0] * d[1] * d[2];
         const uint8_t* kind = A.kind[l];
         const int nx = d[0], per0 = A.periodic[0];
-        for (int64_t g = tid; g < n; g += nth) {
+        for (int64_t i = tid; i < W[l].n; i += nth) {
             int c[3];
-            dec3(d, g, c[0], c[1], c[2]);
+            const int64_t g = win_tile(W[l], d, i, c);
             bool any = false;
 #pragma unroll
             for (int k = -2; k <= 2; ++k) {
@@ -448,14 +507,24 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
         *A.ext_count = 0;
     }
     STAMP_BARRIER(2);
+    if (A.win && blockIdx.x == 0 && threadIdx.x == 0) {
+        // this pass's windows; the kinds' bounding boxes are collected anew in J
+        for (int l = 0; l < L; ++l)
+            for (int a = 0; a < 3; ++a) {
+                A.win[l * 6 + a] = W[l].lo[a];
+                A.win[l * 6 + 3 + a] = W[l].lo[a] + W[l].ext[a] - 1;
+                A.win[(L + l) * 6 + a] = 0x7fffffff;
+                A.win[(L + l) * 6 + 3 + a] = -0x7fffffff;
+            }
+    }
 
     // ---- C: des[0], cur[1]
     if (L == 1) {
         for (int64_t g = tid; g < n0; g += nth) A.des[0][g] = 1;
     } else {
-        for (int64_t g = tid; g < n0; g += nth) {
+        for (int64_t i = tid; i < W[0].n; i += nth) {
             int c[3];
-            dec3(d0, g, c[0], c[1], c[2]);
+            const int64_t g = win_tile(W[0], d0, i, c);
             int g0[3] = {c[0] & ~1, c[1] & ~1, dim == 3 ? (c[2] & ~1) : c[2]};
             bool any = false;
             for (int k = 0; k < (1 << dim) && !any; ++k) {
@@ -467,10 +536,9 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
             A.des[0][g] = any;
         }
         const int* d1 = A.tdims[1];
-        const int64_t n1 = (int64_t)d1[0] * d1[1] * d1[2];
-        for (int64_t g = tid; g < n1; g += nth) {
+        for (int64_t i = tid; i < W[1].n; i += nth) {
             int c[3];
-            dec3(d1, g, c[0], c[1], c[2]);
+            const int64_t g = win_tile(W[1], d1, i, c);
             A.cur[1][g] = (A.kind[1][g] == 1) || children_any(A.cur[0], d0, dim, c);
         }
     }
@@ -478,10 +546,9 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
         int miss = 0;
         for (int l = 0; l < L; ++l) {
             const int* d = A.tdims[l];
-            const int64_t n = (int64_t)d[0] * d[1] * d[2];
-            for (int64_t g = tid; g < n; g += nth) {
+            for (int64_t i = tid; i < W[l].n; i += nth) {
                 int c[3];
-                dec3(d, g, c[0], c[1], c[2]);
+                const int64_t g = win_tile(W[l], d, i, c);
                 const bool any = axis_or2(A.stor[l], d, A.periodic, c, 1);
                 if (dim == 3) A.nkind[l][g] = any;
                 else miss += any && A.kind[l][g] == 0;
@@ -496,22 +563,21 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
     //      and needs neither its parents bitmap nor a barrier)
     for (int l = 1; l < L; ++l) {
         const int* d = A.tdims[l];
-        const int64_t n = (int64_t)d[0] * d[1] * d[2];
         if (l == L - 1) {
+            const int64_t n = (int64_t)d[0] * d[1] * d[2];
             for (int64_t g = tid; g < n; g += nth) A.des[l][g] = 1;
             break;
         }
-        for (int64_t g = tid; g < n; g += nth) {
+        for (int64_t i = tid; i < W[l].n; i += nth) {
             int c[3];
-            dec3(d, g, c[0], c[1], c[2]);
+            const int64_t g = win_tile(W[l], d, i, c);
             A.par[l][g] = children_any(A.des[l - 1], A.tdims[l - 1], dim, c);
         }
         if (l + 1 < L) {
             const int* dn = A.tdims[l + 1];
-            const int64_t nn = (int64_t)dn[0] * dn[1] * dn[2];
-            for (int64_t g = tid; g < nn; g += nth) {
+            for (int64_t i = tid; i < W[l + 1].n; i += nth) {
                 int c[3];
-                dec3(dn, g, c[0], c[1], c[2]);
+                const int64_t g = win_tile(W[l + 1], dn, i, c);
                 A.cur[l + 1][g] = (A.kind[l + 1][g] == 1) || children_any(A.cur[l], d, dim, c);
             }
         }
@@ -520,24 +586,24 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
         // (g0 = c & ~1) per axis, as separable ORs x -> own, y -> stor,
         // z -> des (own and stor are free here: stor's ring data was consumed
         // in C, own is written in I)
-        for (int64_t g = tid; g < n; g += nth) {
+        for (int64_t i = tid; i < W[l].n; i += nth) {
             int c[3];
-            dec3(d, g, c[0], c[1], c[2]);
+            const int64_t g = win_tile(W[l], d, i, c);
             A.own[l][g] = axis_group_or2(A.par[l], d, A.periodic, c, 0);
         }
         grid_barrier(A.bar);
-        for (int64_t g = tid; g < n; g += nth) {
+        for (int64_t i = tid; i < W[l].n; i += nth) {
             int c[3];
-            dec3(d, g, c[0], c[1], c[2]);
+            const int64_t g = win_tile(W[l], d, i, c);
             const bool any = axis_group_or2(A.own[l], d, A.periodic, c, 1);
             if (dim == 3) A.stor[l][g] = any;
             else A.des[l][g] = any;
         }
         if (dim == 3) {
             grid_barrier(A.bar);
-            for (int64_t g = tid; g < n; g += nth) {
+            for (int64_t i = tid; i < W[l].n; i += nth) {
                 int c[3];
-                dec3(d, g, c[0], c[1], c[2]);
+                const int64_t g = win_tile(W[l], d, i, c);
                 A.des[l][g] = axis_group_or2(A.stor[l], d, A.periodic, c, 2);
             }
         }
@@ -549,25 +615,23 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
         int miss = 0;
         for (int l = 0; l < L; ++l) {
             const int* d = A.tdims[l];
-            const int64_t n = (int64_t)d[0] * d[1] * d[2];
-            for (int64_t g = tid; g < n; g += nth) {
-                if (A.kind[l][g] != 0) continue;
+            for (int64_t i = tid; i < W[l].n; i += nth) {
                 int c[3];
-                dec3(d, g, c[0], c[1], c[2]);
+                const int64_t g = win_tile(W[l], d, i, c);
+                if (A.kind[l][g] != 0) continue;
                 miss += axis_or2(A.nkind[l], d, A.periodic, c, 2);
             }
         }
         for (int off = 16; off > 0; off >>= 1) miss += __shfl_down_sync(0xffffffffu, miss, off);
         if ((threadIdx.x & 31) == 0 && miss) atomicAdd(&A.status[L + 1], miss);
     }
-    effective_stage(A, 0, false, tid, nth);
+    effective_stage(A, 0, false, tid, nth, W[0]);
     STAMP_BARRIER(6);
     for (int l = 1; l < L; ++l) {
         const int* d = A.tdims[l];
-        const int64_t n = (int64_t)d[0] * d[1] * d[2];
-        for (int64_t g = tid; g < n; g += nth) {
+        for (int64_t i = tid; i < W[l].n; i += nth) {
             int c[3];
-            dec3(d, g, c[0], c[1], c[2]);
+            const int64_t g = win_tile(W[l], d, i, c);
             A.par[l][g] = children_any(A.eff[l - 1], A.tdims[l - 1], dim, c);
         }
         STAMP_BARRIER(7);
@@ -575,7 +639,7 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
         // streaks stay 0) and its effective coverage is all ones
         // (adapt.py:180-181): skipped, phase I reads eff[L-1] as 1
         if (l < L - 1) {
-            effective_stage(A, l, true, tid, nth);
+            effective_stage(A, l, true, tid, nth, W[l]);
             STAMP_BARRIER(8);
         }
     }
@@ -586,11 +650,10 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
     //      new kinds, no-op flags (adapt.py:184-225); seeds cleared
     for (int l = 0; l < L; ++l) {
         const int* d = A.tdims[l];
-        const int64_t n = (int64_t)d[0] * d[1] * d[2];
         const int per0 = A.periodic[0], nx = d[0];
-        for (int64_t g = tid; g < n; g += nth) {
+        for (int64_t i = tid; i < W[l].n; i += nth) {
             int c[3];
-            dec3(d, g, c[0], c[1], c[2]);
+            const int64_t g = win_tile(W[l], d, i, c);
             A.own[l][g] = (l == L - 1 || A.eff[l][g]) && !(l > 0 && A.par[l][g]);
             bool any = false;
 #pragma unroll
@@ -604,15 +667,21 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
             A.stor[l][g] = any;
         }
     }
-    for (int64_t g = tid; g < n0; g += nth) A.seeds[g] = 0;
+    {
+        // all seeds cleared (not only the window's: a seed of a particle far
+        // from every leaf must not survive into a later window), 16 B per store
+        uint4* s16 = reinterpret_cast<uint4*>(A.seeds);      // torch allocations: 512 B aligned
+        const int64_t n16 = n0 >> 4;
+        for (int64_t g = tid; g < n16; g += nth) s16[g] = make_uint4(0u, 0u, 0u, 0u);
+        for (int64_t g = (n16 << 4) + tid; g < n0; g += nth) A.seeds[g] = 0;
+    }
     STAMP_BARRIER(10);
     if (dim == 3) {
         for (int l = 0; l < L; ++l) {
             const int* d = A.tdims[l];
-            const int64_t n = (int64_t)d[0] * d[1] * d[2];
-            for (int64_t g = tid; g < n; g += nth) {
+            for (int64_t i = tid; i < W[l].n; i += nth) {
                 int c[3];
-                dec3(d, g, c[0], c[1], c[2]);
+                const int64_t g = win_tile(W[l], d, i, c);
                 A.des[l][g] = axis_or2(A.stor[l], d, A.periodic, c, 1);
             }
         }
@@ -620,15 +689,15 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
     }
     for (int l = 0; l < L; ++l) {
         const int* d = A.tdims[l];
-        const int64_t n = (int64_t)d[0] * d[1] * d[2];
         bool changed = false;
         int cnt = 0, fresh = 0;
-        for (int64_t g = tid; g < n; g += nth) {
+        int blo[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, bhi[3] = {-0x7fffffff, -0x7fffffff, -0x7fffffff};
+        for (int64_t i = tid; i < W[l].n; i += nth) {
+            int c[3];
+            const int64_t g = win_tile(W[l], d, i, c);
             uint8_t k;
             if (A.own[l][g]) k = 1;
             else {
-                int c[3];
-                dec3(d, g, c[0], c[1], c[2]);
                 const bool dil = dim == 3 ? axis_or2(A.des[l], d, A.periodic, c, 2)
                                           : axis_or2(A.stor[l], d, A.periodic, c, 1);
                 k = dil ? 2 : 0;
@@ -638,6 +707,20 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
             changed |= k != old;
             cnt += k != 0;
             fresh += (k != 0 && old == 0);
+            if (k) {
+                for (int a = 0; a < 3; ++a) { blo[a] = min(blo[a], c[a]); bhi[a] = max(bhi[a], c[a]); }
+            }
+        }
+        if (A.win && l < L - 1) {
+            // bounding box of the new kinds: the next pass's window input
+            for (int a = 0; a < 3; ++a) {
+                const int wl = __reduce_min_sync(0xffffffffu, blo[a]);
+                const int wh = __reduce_max_sync(0xffffffffu, bhi[a]);
+                if ((threadIdx.x & 31) == 0 && wl <= wh) {
+                    atomicMin(&A.win[(L + l) * 6 + a], wl);
+                    atomicMax(&A.win[(L + l) * 6 + 3 + a], wh);
+                }
+            }
         }
         if (__syncthreads_or(changed) && threadIdx.x == 0) atomicOr(&A.status[l], 1);
         for (int off = 16; off > 0; off >>= 1) {
@@ -676,7 +759,7 @@ extern "C" int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_
                                uint8_t* const* nkind, uint8_t* const* stor, int16_t* const* streak,
                                uint8_t* seeds,
                                const uint8_t* static_tiles, const double* x, int64_t xs, int32_t n,
-                               int32_t* ext_count,
+                               int32_t* ext_count, int32_t* win,
                                int32_t* status, mlbm_error_t* err, unsigned int* bar, void* stream) {
     // MLBM_ADAPT_PATH=bits selects the bit-packed single-CTA pass
     // (adapt_bits.cu) when the hierarchy's bitmaps fit in shared memory.  It
@@ -712,6 +795,7 @@ extern "C" int mlbm_adapt_pass(const mlbm_hier_t* h, uint8_t* const* des, uint8_
     A.xs = xs;
     A.n = n;
     A.ext_count = ext_count;
+    A.win = ext_count ? win : nullptr;       // windows need G2P's seeds (within a tile of a leaf)
     A.status = status;
     A.err = err;
     A.bar = bar;

@@ -245,6 +245,7 @@ class Topology:
         """Replace the kind grids of the given levels (host-driven path used
         at construction and by ``set_tile_set``; counts read back)."""
         counts = {l: int((k != 0).sum().item()) for l, k in kinds.items()}
+        self.host_rebuilds = getattr(self, "host_rebuilds", 0) + 1   # GridAdaptor windows reset
         for l, n in counts.items():
             self.ensure_capacity(l, n)
         for l, k in kinds.items():
