@@ -326,6 +326,7 @@ class CoupledSim:
         self._sort_now = True
         self._use_sorted = self._sort_ahead = self._sorted_ahead = False
         self.overlap_diag = os.environ.get("MLBM_OVERLAP_DIAG", "1") != "0"
+        self._fork_pdiag = self._pdiag_forked = False
         # graphs of this many upcoming steps are captured whenever capacities
         # change (first step included), so steady stepping only replays
         self.precapture_steps = int(os.environ.get("MLBM_PRECAPTURE", "16")) or None
@@ -458,6 +459,20 @@ class CoupledSim:
                                  L.ptr(grid._err), L.stream_handle()), "g2p")
         solver.launches += 1
         self.last_fields = CouplingFields(grid, self.pair.trees[0].levels[0])
+        if self._fork_pdiag:
+            # graph step: the particle part of the diagnostics row (sum m v of
+            # the new velocities, sum fs of this exchange) reads only what G2P
+            # and the exchange wrote: it runs on the side stream concurrently
+            # with the collide, the stress raster and the powder transport
+            # (joined before the step's status copy)
+            main = torch.cuda.current_stream()
+            side = self._side_stream()
+            fork = torch.cuda.Event()
+            fork.record(main)
+            side.wait_event(fork)
+            with torch.cuda.stream(side):
+                self._record_diagnostics(fluid=False)
+            self._pdiag_forked = True
 
     def _hook(self):
         """The coupling hook for run_cycle: fused (P2G -> one level-0 kernel
@@ -543,6 +558,8 @@ class CoupledSim:
         cycle = solver._schedule[ci]
         check = solver.check_errors
         solver.check_errors = False
+        self._fork_pdiag = self.overlap_diag
+        self._pdiag_forked = False
         try:
             if is_mpm:
                 solver.run_cycle(cycle, hook=self._hook())
@@ -552,8 +569,11 @@ class CoupledSim:
                 solver.run_cycle(cycle)
         finally:
             solver.check_errors = check
+            self._fork_pdiag = False
         if self.powder is not None:
             self._powder_cycle(is_mpm)
+        # particles: already recorded on the side stream after G2P
+        pdiag = not self._pdiag_forked
         if adapt_now and self.overlap_diag:
             # the diagnostics reductions read only fields and particles: they
             # run on a side stream concurrently with the latency-bound adapt
@@ -564,7 +584,7 @@ class CoupledSim:
             fork.record(main)
             side.wait_event(fork)
             with torch.cuda.stream(side):
-                self._record_diagnostics()
+                self._record_diagnostics(particles=pdiag)
                 if self._sort_ahead:
                     self._sort_into_scratch()
             self.adaptor.plan_device(self._driver())
@@ -574,7 +594,11 @@ class CoupledSim:
         else:
             if adapt_now:
                 self.adaptor.plan_device(self._driver())
-            self._record_diagnostics()
+            if not pdiag:
+                join = torch.cuda.Event()
+                join.record(self._side_stream())
+                torch.cuda.current_stream().wait_event(join)
+            self._record_diagnostics(particles=pdiag)
         self._host_i32.copy_(self._sblock, non_blocking=True)
         self._host_f64.copy_(self._diag_buf, non_blocking=True)
 
