@@ -177,10 +177,14 @@ def kernel_class(rec, d, s, live):
         cells = live(args[0]._obj) * T
         return "exchange", cells * (17 + 25) * s, cells
     if name in ("mlbm_downward", "mlbm_upward"):
+        # unique bytes: upward reads its 2^d fine sources (disjoint between
+        # targets); downward targets share their 2^d coarse sources with their
+        # neighbours (the gathers hit L2): about one coarse cell (old and new
+        # trees) per fine target
         n = live(args[2])
         nc = 1 << d
-        return "transfer", n * (nc * (NM + 2) * (2 if name == "mlbm_downward" else 1)
-                                + (NM + 2)) * s, n
+        reads = nc if name == "mlbm_upward" else 2
+        return "transfer", n * (reads + 1) * (NM + 2) * s, n
     if name.startswith("mlbm_diag"):
         return "diagnostics", 0, 0
     if name.startswith("mlbm_stress_raster") or name == "mlbm_powder":

@@ -1202,6 +1202,104 @@ __global__ void k_powder_advect(PowderArgs A) {
     ((R*)A.tmp)[c] = R(phv[0]);
 }
 
+// 3D advection with the tile's velocities and phi staged in shared memory:
+// one CTA per level-0 tile, the 6^3 cells of the tile and its one-cell halo
+// (coordinates wrapped / clamped and looked up exactly as sample_lin_n does)
+// loaded once, then every cell's three trilinear samples read shared memory —
+// the same corners, weights, order and renormalisation as k_powder_advect, so
+// the result is bit-identical.  A sample whose corners leave the halo (a
+// backtrace longer than one cell) falls back to sample_lin_n.
+template <typename R>
+__device__ __forceinline__ bool sample_halo(const R* const (&f)[3], int nc, const uint8_t* pres,
+                                            const double (&pos)[3], const int (&h0)[3], double (&out)[3]) {
+    int hb[3];
+    double wt[3][2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double fl = floor(pos[a]);
+        const double fr = pos[a] - fl;
+        wt[a][0] = 1.0 - fr;
+        wt[a][1] = fr;
+        hb[a] = (int)fl - h0[a];
+        if (hb[a] < 0 || hb[a] > 4) return false;
+    }
+    double acc[3] = {0.0, 0.0, 0.0}, ws = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int ox = k & 1, oy = (k >> 1) & 1, oz = (k >> 2) & 1;
+        double w = 1.0;
+        w *= wt[0][ox];
+        w *= wt[1][oy];
+        w *= wt[2][oz];
+        const int h = (hb[0] + ox) + 6 * (hb[1] + oy) + 36 * (hb[2] + oz);
+        if (!pres[h]) continue;
+        for (int q = 0; q < nc; ++q) acc[q] += w * (double)f[q][h];
+        ws += w;
+    }
+    for (int q = 0; q < nc; ++q) out[q] = ws > 0.0 ? (double)R(acc[q] / ws) : (double)R(acc[q]);
+    return true;
+}
+
+template <typename R>
+__global__ void __launch_bounds__(64) k_powder_advect_tile(PowderArgs A) {
+    constexpr int T = 64, NH = 216;
+    const int slot = blockIdx.x;
+    if (slot >= live_tiles(A.lv)) return;
+    const int lc = threadIdx.x;
+    const int64_t c = (int64_t)slot * T + lc;
+    if (A.active && !A.active[slot]) {       // no powder within reach: exactly 0 (block-uniform)
+        ((R*)A.tmp)[c] = R(0);
+        return;
+    }
+    __shared__ R su[3][NH], sph[NH];
+    __shared__ uint8_t spres[NH];
+    const FieldsT<R> src = fields_of<R>(A.src), dst = fields_of<R>(A.dst);
+    const mlbm_level_t& lv = A.lv;
+    int h0[3];                               // global cell of halo index 0
+#pragma unroll
+    for (int a = 0; a < 3; ++a) h0[a] = lv.tile_xyz[slot * 3 + a] * 4 - 1;
+    for (int h = threadIdx.x; h < NH; h += T) {
+        int v[3] = {h0[0] + h % 6, h0[1] + (h / 6) % 6, h0[2] + h / 36};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (lv.periodic[a]) v[a] = wrap_near(v[a], lv.cells[a]);
+            else v[a] = v[a] < 0 ? 0 : (v[a] >= lv.cells[a] ? lv.cells[a] - 1 : v[a]);
+        }
+        const int s = lv.tile_map[g3(lv.tiles, v[0] >> 2, v[1] >> 2, v[2] >> 2)];
+        spres[h] = s >= 0;
+        if (s >= 0) {
+            const int64_t ni = (int64_t)s * T + local_of<3>(v[0] & 3, v[1] & 3, v[2] & 3);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) su[a][h] = dst.at(1 + a, ni);
+            sph[h] = src.at(fi_phi<3>(), ni);
+        }
+    }
+    __syncthreads();
+    const int l3[3] = {lc & 3, (lc >> 2) & 3, (lc >> 4) & 3};
+    double pos[3];
+    for (int a = 0; a < 3; ++a) pos[a] = (double)(h0[a] + 1 + l3[a]);
+    const R* u[3] = {su[0], su[1], su[2]};
+    const R* ug[3];
+    for (int a = 0; a < 3; ++a) ug[a] = &dst.at(1 + a, 0);
+    double k1[3], k2[3], k3[3], q[3];
+    const int own = (l3[0] + 1) + 6 * (l3[1] + 1) + 36 * (l3[2] + 1);
+    for (int a = 0; a < 3; ++a) k1[a] = (double)su[a][own];
+    for (int a = 0; a < 3; ++a) q[a] = pos[a] - 0.5 * A.dt * k1[a];
+    if (!sample_halo<R>(u, 3, spres, q, h0, k2)) sample_lin_n<3, R, 3>(ug, q, lv, k2);
+    for (int a = 0; a < 3; ++a) q[a] = pos[a] - 0.75 * A.dt * k2[a];
+    if (!sample_halo<R>(u, 3, spres, q, h0, k3)) sample_lin_n<3, R, 3>(ug, q, lv, k3);
+    for (int a = 0; a < 3; ++a) q[a] = pos[a] - A.dt * (2.0 * k1[a] + 3.0 * k2[a] + 4.0 * k3[a]) / 9.0;
+    const R* ph[3] = {sph, sph, sph};
+    double phv[3];
+    if (!sample_halo<R>(ph, 1, spres, q, h0, phv)) {
+        const R* pg[1] = {&src.at(fi_phi<3>(), 0)};
+        double pv[1];
+        sample_lin_n<3, R, 1>(pg, q, lv, pv);
+        phv[0] = pv[0];
+    }
+    ((R*)A.tmp)[c] = R(phv[0]);
+}
+
 template <int D, typename R>
 __global__ void k_powder_diffuse(PowderArgs A) {
     constexpr int T = Geo<D>::T, NS = Geo<D>::NS;
@@ -2912,7 +3010,8 @@ extern "C" int mlbm_powder(const mlbm_level_t* lv0, mlbm_fields_t src, mlbm_fiel
             k_phi_region<3><<<nblk(nt, 128), 128, 0, s>>>(*lv0, tile_ws, tile_ws + nt);
         }
     }
-#define PW(D, R) do { k_powder_advect<D, R><<<nblk(n, 128), 128, 0, s>>>(A); \
+#define PW(D, R) do { if (D == 3) k_powder_advect_tile<R><<<nt, 64, 0, s>>>(A); \
+                      else k_powder_advect<D, R><<<nblk(n, 128), 128, 0, s>>>(A); \
                       k_powder_diffuse<D, R><<<nblk(n, 128), 128, 0, s>>>(A); } while (0)
     if (lv0->dim == 2) { if (dtype) PW(2, double); else PW(2, float); }
     else { if (dtype) PW(3, double); else PW(3, float); }
