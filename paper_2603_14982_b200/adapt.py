@@ -21,6 +21,7 @@ reference's by construction (integer work only).
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -137,7 +138,7 @@ class GridAdaptor:
         # tile windows of the G2P-seeded fused pass ([2][levels][6] int32, see
         # mlbm_adapt_pass): valid for the key (host rebuilds, static mask) they
         # were derived under; any other pass invalidates them
-        self.windows = True
+        self.windows = os.environ.get("MLBM_ADAPT_WINDOWS", "1") != "0"
         self._win = torch.zeros(2 * topology.levels * 6, dtype=torch.int32, device=dev)
         self._win_key = None
 

@@ -21,10 +21,14 @@ for _ in range(int(os.environ.get("WARM", "12"))):
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 sim.use_graphs = False
 torch.cuda.synchronize()
+# ncu --profile-from-start off captures only the probed steps (not the scene
+# build's initial adapt pass or the warm-up)
+torch.cuda.cudart().cudaProfilerStart()
 L.TRACE.start()
 for _ in range(n):
     sim.step()
 torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStop()
 recs = L.TRACE.stop()
 acc = collections.defaultdict(float)
 cnt = collections.Counter()

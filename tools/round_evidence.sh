@@ -17,7 +17,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 echo "launch list rc=$?"
 CMD3="python tools/kernel_probe.py 1"
 SCENE=AVALANCHE_C4 WARM=4 $CMD3 > gpurun_out/${R}_plain3.log 2>&1 && \
-SCENE=AVALANCHE_C4 WARM=4 ncu --set full --clock-control none --import-source on \
+SCENE=AVALANCHE_C4 WARM=4 ncu --set full --clock-control none --import-source on --profile-from-start off \
     -k regex:"level_kernel|k_p2g_cell2|k_g2p|k_stress_cell2|k_powder_advect|k_exchange|k_adapt_pass|k_classify|downward_kernel" -c 10 \
     -o gpurun_out/${R}_full_c4 -f $CMD3 > gpurun_out/${R}_ncu_full_c4.log 2>&1
 echo "full set c4 rc=$?"
@@ -25,7 +25,7 @@ python tools/full_summary.py gpurun_out/${R}_full_c4.ncu-rep gpurun_out/${R}_ful
 for k in k_p2g_cell2 "level_kernel<(int)3, float, (int)1>" k_g2p k_stress_cell2 k_exchange; do python tools/src_hot.py gpurun_out/${R}_full_c4.ncu-rep "$k" 40; done > gpurun_out/${R}_src_hot_c4.txt 2>&1
 CMD2="python tools/kernel_probe.py 2"
 SCENE=COLUMN_3D_C2 $CMD2 > gpurun_out/${R}_plain2.log 2>&1 && \
-SCENE=COLUMN_3D_C2 ncu --set full --clock-control none --import-source on \
+SCENE=COLUMN_3D_C2 ncu --set full --clock-control none --import-source on --profile-from-start off \
     -k regex:"level_kernel|k_p2g_cell2|k_g2p|k_adapt_pass|k_exchange|downward_kernel" -c 12 \
     -o gpurun_out/${R}_full_c2 -f $CMD2 > gpurun_out/${R}_ncu_full_c2.log 2>&1
 echo "full set c2 rc=$?"
@@ -33,3 +33,4 @@ python tools/full_summary.py gpurun_out/${R}_full_c2.ncu-rep gpurun_out/${R}_ful
 # the reports stay on the box (gpurun copies back at most 64 MiB)
 rm -f gpurun_out/${R}_full_c4.ncu-rep gpurun_out/${R}_full_c2.ncu-rep
 du -sh gpurun_out
+python tools/launch_summary.py gpurun_out/${R}_launches.csv > gpurun_out/${R}_launch_summary.txt 2>&1
