@@ -432,17 +432,46 @@ __global__ void __launch_bounds__(512, ADAPT_MINB) k_adapt_pass(AdaptArgs A) {
     stamp(A, 0);
 
     // ---- A: seeds <- static, invariants of the current topology, cur[0]
-    for (int64_t g = tid; g < n0; g += nth) {
-        A.cur[0][g] = A.kind[0][g] == 1;
-        int x[3];
-        dec3(d0, g, x[0], x[1], x[2]);
-        int cnt = 0;
-        for (int l = 0; l < L; ++l) {
-            int c[3];
-            for (int a = 0; a < 3; ++a) c[a] = a < dim ? x[a] >> l : 0;
-            cnt += A.kind[l][gi3(A.tdims[l], c[0], c[1], c[2])] == 1;
+    if (dim == 3 && (d0[2] & 15) == 0 && L <= 5) {
+        // 16 consecutive z tiles of one (x, y) row per trip: level-0 kinds and
+        // cur[0] as 16-byte vectors, level l's 16 >> l covering kinds as bytes
+        int viol = 0;
+        for (int64_t q = tid; q < (n0 >> 4); q += nth) {
+            const int64_t g = q << 4;
+            int x[3];
+            dec3(d0, g, x[0], x[1], x[2]);
+            const uint4 k0 = *reinterpret_cast<const uint4*>(A.kind[0] + g);
+            const unsigned kw[4] = {k0.x, k0.y, k0.z, k0.w};
+            unsigned cw[4], nw[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                cw[i] = __vcmpeq4(kw[i], 0x01010101u) & 0x01010101u;     // leaf bytes -> 1
+                nw[i] = cw[i];                                          // per-tile leaf count
+            }
+            *reinterpret_cast<uint4*>(A.cur[0] + g) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+            for (int l = 1; l < L; ++l) {
+                const uint8_t* kl = A.kind[l] + gi3(A.tdims[l], x[0] >> l, x[1] >> l, x[2] >> l);
+#pragma unroll
+                for (int z = 0; z < 16; ++z)
+                    if (kl[z >> l] == 1) nw[z >> 2] += 1u << (8 * (z & 3));
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) viol += __popc(__vcmpne4(nw[i], 0x01010101u)) >> 3;
         }
-        if (cnt != 1) atomicAdd(&A.status[L], 1);
+        if (viol) atomicAdd(&A.status[L], viol);
+    } else {
+        for (int64_t g = tid; g < n0; g += nth) {
+            A.cur[0][g] = A.kind[0][g] == 1;
+            int x[3];
+            dec3(d0, g, x[0], x[1], x[2]);
+            int cnt = 0;
+            for (int l = 0; l < L; ++l) {
+                int c[3];
+                for (int a = 0; a < 3; ++a) c[a] = a < dim ? x[a] >> l : 0;
+                cnt += A.kind[l][gi3(A.tdims[l], c[0], c[1], c[2])] == 1;
+            }
+            if (cnt != 1) atomicAdd(&A.status[L], 1);
+        }
     }
     // two-tile rings of the current leaves (sparse_grid.py:320-337): the
     // absent tiles inside dilate2(leaf) are counted; the dilation is done as
