@@ -287,7 +287,7 @@ def build_tables(topo: Topology, bc, solid, err, tables=None, only=None):
         for which, other in ((0, l + 1), (1, l - 1)):
             cnt = topo.dcounts[l, 2 + which:3 + which]
             if other < 0 or other >= topo.levels or not topo.lv[other].cap:
-                cnt.zero_()
+                L.zero(cnt)                  # cudaMemsetAsync: no framework kernel in the graph
                 continue
             tg, src, _ = t.down if which == 0 else t.up
             ws = topo.workspace(topo.capacity_cells(l))

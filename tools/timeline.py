@@ -28,6 +28,11 @@ path = os.path.join(tempfile.mkdtemp(), "trace.json")
 prof.export_chrome_trace(path)
 ev = json.load(open(path))["traceEvents"]
 ks = [e for e in ev if e.get("cat") in ("kernel", "gpu_memset", "gpu_memcpy") and "dur" in e]
+# framework (aten) kernels: which host op launched them
+ops = {e.get("args", {}).get("External id"): e["name"] for e in ev if e.get("cat") == "cpu_op"}
+for e in ks:
+    if "at::" in e["name"]:
+        print("framework kernel %s <- host op %s" % (e["name"][:60], ops.get(e.get("args", {}).get("External id"))))
 ks.sort(key=lambda e: e["ts"])
 # split into steps at host synchronisations: gaps > 200 us between kernels
 steps, cur = [], [ks[0]]
@@ -56,6 +61,14 @@ for si, st in enumerate(steps):
           % (si, len(st), (t1 - t0) / 1e3, busy / 1e3, (t1 - t0 - busy) / 1e3, tot / 1e3,
              {k: round(v / 1e3, 3) for k, v in per_stream.items()}))
     if si == len(steps) // 2:
+        agg = collections.defaultdict(lambda: [0, 0.0])
+        for e in st:
+            nm = e["name"].replace("void ", "").split("(")[0].split("<")[0]
+            agg[nm][0] += 1
+            agg[nm][1] += e["dur"]
+        print("  every kernel / copy / memset of this step (name, count, total us):")
+        for nm, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+            print("    %-44s %4d %10.1f" % (nm, c, t))
         # the exposed (not overlapped) time of each kernel name on the busy timeline
         print("  largest idle gaps (us):", sorted([round(g, 1) for g, _ in gaps], reverse=True)[:8])
         seq = []
