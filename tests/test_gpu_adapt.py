@@ -143,3 +143,54 @@ def test_invariant_violations_reported_fused_and_unfused(dim, path, monkeypatch)
     ad.fused = True
     ad.plan_device(drv)
     assert ad._status[Lv:Lv + 3].cpu().numpy().tolist() == [0, 0, 0]
+
+
+def test_adapt_windows_bit_identical_to_full_grid():
+    """The G2P-seeded adapt pass works inside per-level tile windows
+    (mlbm_adapt_pass `win`): a churning 3D cloud in a domain much larger than
+    the cloud runs identically with the windows and over the whole grids —
+    tile sets and int16 streaks bitwise after every step, fields and
+    particles to the fp64 atomic-order noise — and the level-0 window stays
+    smaller than the grid."""
+    import scenes as S
+    from paper_2603_14982_b200.harness import build_scene, validate_scene
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    sc = S.scene(S.CLOUD_3D_SMALL)
+    sc["domain"]["cells"] = [256, 96, 64]
+    sc["domain"]["levels"] = 3
+    # no periodic axis (a periodic axis keeps its whole extent)
+    sc["boundaries"] = {"x_min": "outlet", "x_max": "outlet", "y_min": "wall", "y_max": "wall",
+                        "z_min": "outlet", "z_max": "outlet"}
+    sims = []
+    for windows in (True, False):
+        sim = build_scene(validate_scene(sc))
+        sim.adaptor.windows = windows
+        rng = np.random.default_rng(5)
+        sim.particles.v = rng.normal(0, 0.1, (len(sim.particles), 3)).clip(-0.45, 0.45)
+        sims.append(sim)
+    changes = 0
+    for s in range(16):
+        for sim in sims:
+            sim.step()
+        a, b = sims
+        assert a.topology.tile_set() == b.topology.tile_set(), f"step {s}"
+        for x, y in zip(a.adaptor._streak, b.adaptor._streak):
+            assert torch.equal(x, y), f"streaks, step {s}"
+        changes = a.topology_changes
+    assert changes > 0
+    a, b = sims
+    # fields and particles: equal up to the fp64 atomic summation order of P2G
+    for l in range(a.topology.levels):
+        for t in range(2):
+            x = a.pair.trees[t].levels[l].data[:, :a.topology.cell_count(l)]
+            y = b.pair.trees[t].levels[l].data[:, :b.topology.cell_count(l)]
+            assert (x - y).abs().max().item() <= 1e-9
+    assert (a.particles.xd - b.particles.xd).abs().max().item() <= 1e-9
+    assert (a.particles.pd - b.particles.pd).abs().max().item() <= 1e-9
+    # the windows were in use and narrower than the level-0 tile grid
+    w = a.adaptor._win.view(2, a.topology.levels, 6).cpu().numpy()
+    g0 = a.topology.tile_grid(0)
+    ext = w[0, 0, 3:] - w[0, 0, :3] + 1
+    assert a.adaptor._win_key is not None
+    assert int(np.prod(ext)) < int(np.prod(g0))
