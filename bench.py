@@ -271,7 +271,11 @@ def run_mine(args, rank, world, local_rank):
     if not args.no_e2e:
         from paper_2603_14982_b200.host_io import HostMirror
         p = sim.particles
-        mirror = HostMirror([p.xd, p.pd])      # host-owned particle state, pinned
+        # host-owned particle state, pinned: positions and the reference's
+        # particle rows (v, C, F, m, V0, vol_corr); the Kirchhoff stress rows
+        # are a device cache of F (not reference state) and are recomputed from
+        # the uploaded F on the device every step (mlbm_particle_stress)
+        mirror = HostMirror([p.xd, p.pd[:p.R["tau"]]])
         torch.cuda.synchronize()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -280,6 +284,8 @@ def run_mine(args, rank, world, local_rank):
         diag_bytes = 0
         for _ in range(args.steps):
             mirror.upload()                  # host -> device, chunked on a copy stream
+            sim.particles.stress_mat = None  # tau(F) of the uploaded F
+            sim.particles.ensure_stress(sim.material)
             sim.step()
             mirror.download()                # device -> host, overlaps the next upload
             row = sim.diagnostics[-1]        # D2H of the step's diagnostics row
@@ -297,9 +303,11 @@ def run_mine(args, rank, world, local_rank):
                "particles_per_s": round(world * n_part * args.steps / (te * 1e-3), 1),
                "ms_per_step": te / args.steps,
                "path": "CoupledSim.step() with the particle state owned by pinned host memory "
-                       "(host_io.HostMirror): uploaded before and read back after every step "
-                       "in row chunks on two copy streams (download of step k overlaps upload "
-                       "of step k+1) + diagnostics row D2H"}
+                       "(host_io.HostMirror: positions + the reference's rows v, C, F, m, V0, "
+                       "vol_corr): uploaded before and read back after every step in row chunks "
+                       "on two copy streams (download of step k overlaps upload of step k+1), "
+                       "the stress cache tau(F) recomputed from the uploaded F on the device, "
+                       "+ diagnostics row D2H"}
         del row
 
     # ---- per-kernel device times: an eager pass of the same steps with every
