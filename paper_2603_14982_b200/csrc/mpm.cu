@@ -17,6 +17,7 @@
 // ~1e-8 absolute resolution); everything else follows the run dtype.
 #include <algorithm>
 #include <cstdlib>
+#include <cuda_pipeline.h>
 #include "common.cuh"
 #include "exchange.cuh"
 
@@ -689,6 +690,9 @@ __global__ void k_particle_stress(int n, R* pp, int64_t ps, MatParams mp) {
 #ifndef G2P_EARLY
 #define G2P_EARLY 0     // 1: ride-along rows loaded before the node-box staging (measured +4 % on C4)
 #endif
+#ifndef G2P_ASYNC
+#define G2P_ASYNC 1     // ride-along rows copied to shared memory asynchronously (cp.async) before the staging
+#endif
 template <int D, typename R>
 __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(PartArgs P, TopoL0 t0, MatParams mp, const R* ras, int64_t rs,
                                              double dt, int plastic, int32_t* clamped, mlbm_error_t* err) {
@@ -705,6 +709,28 @@ __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(P
     const bool live = p < P.n;
     const R* pp = (const R*)P.p;
     R* pw = (R*)P.pw;
+#if G2P_ASYNC && !G2P_EARLY
+    // the rows that only ride along (F, vc, m, V0, id) are copied into shared
+    // memory by cp.async (LDGSTS) now: their latency overlaps the node-box
+    // staging and its barriers without holding registers (the register form,
+    // G2P_EARLY, measured slower at the 64-register bound)
+    constexpr int NPRE = D * D + 3;
+    __shared__ R spre[NPRE][G2P_BT];
+    __shared__ int32_t spid[G2P_BT];
+    const bool copy_rows = pw != pp;
+    if (live) {
+#pragma unroll
+        for (int k = 0; k < D * D; ++k)
+            __pipeline_memcpy_async(&spre[k][threadIdx.x], &pp[(PR::F + k) * P.ps + p], sizeof(R));
+        __pipeline_memcpy_async(&spre[D * D][threadIdx.x], &pp[PR::VC * P.ps + p], sizeof(R));
+        if (copy_rows) {
+            __pipeline_memcpy_async(&spre[D * D + 1][threadIdx.x], &pp[PR::M * P.ps + p], sizeof(R));
+            __pipeline_memcpy_async(&spre[D * D + 2][threadIdx.x], &pp[PR::V0 * P.ps + p], sizeof(R));
+        }
+        if (P.pidw) __pipeline_memcpy_async(&spid[threadIdx.x], &P.pid[p], sizeof(int32_t));
+    }
+    __pipeline_commit();
+#endif
     double x[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) x[a] = live ? P.x[a * P.ps + p] : 0.5 * t0.cells[a];
@@ -747,7 +773,16 @@ __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(P
     }
     __syncthreads();
     if (!live) return;
-#if !G2P_EARLY
+#if G2P_ASYNC && !G2P_EARLY
+    __pipeline_wait_prior(0);                 // this thread's own copies (no other thread reads them)
+    R Fpre[D * D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) Fpre[k] = spre[k][threadIdx.x];
+    const R vc_pre = spre[D * D][threadIdx.x];
+    const R m_pre = copy_rows ? spre[D * D + 1][threadIdx.x] : R(0);
+    const R v0_pre = copy_rows ? spre[D * D + 2][threadIdx.x] : R(0);
+    const int32_t id_pre = P.pidw ? spid[threadIdx.x] : 0;
+#elif !G2P_EARLY
     // rows that only ride along (F, vc, m, V0, id): loaded now so their
     // latency overlaps the gather instead of stalling the epilogue
     R Fpre[D * D];
