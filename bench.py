@@ -241,6 +241,11 @@ def run_mine(args, rank, world, local_rank):
     barrier()
     torch.cuda.synchronize()
     clocks.start()
+    # MLBM_PROFILE_TIMED=1: the profiler range covers the timed steps only
+    # (ncu --profile-from-start off: a launch list without the scene build)
+    prof_timed = os.environ.get("MLBM_PROFILE_TIMED") == "1"
+    if prof_timed:
+        torch.cuda.cudart().cudaProfilerStart()
     ev = []
     for _ in range(args.steps):
         L.zero(flush)                      # L2 flush: a memset, not a kernel
@@ -251,6 +256,8 @@ def run_mine(args, rank, world, local_rank):
         e1.record()
         ev.append((e0, e1))
     torch.cuda.synchronize()
+    if prof_timed:
+        torch.cuda.cudart().cudaProfilerStop()
     barrier()
     clk = clocks.stop()
     launches = L.TRACE.launches - launches0

@@ -337,6 +337,28 @@ def copy(dst, src):
           "copy")
 
 
+def zeros(shape, dtype, device):
+    """A zeroed device tensor (cudaMemsetAsync; no framework kernel), torch
+    elsewhere."""
+    import torch
+    if torch.device(device).type != "cuda":
+        return torch.zeros(shape, dtype=dtype, device=device)
+    t = torch.empty(shape, dtype=dtype, device=device)
+    zero(t)
+    return t
+
+
+def full(shape, value, dtype, device):
+    """A device tensor filled with ``value`` (library fill kernel; uint8,
+    int32, float32, float64), torch elsewhere."""
+    import torch
+    if torch.device(device).type != "cuda":
+        return torch.full(shape, value, dtype=dtype, device=device)
+    t = torch.empty(shape, dtype=dtype, device=device)
+    fill(t, value)
+    return t
+
+
 def fill(t, value):
     """Fill a contiguous device tensor with ``value`` (library kernel)."""
     import torch

@@ -213,9 +213,9 @@ class _LevelTables:
     """Device classification of one level (solver.py:177-274)."""
 
     def __init__(self, n_cells, n_tiles, device):
-        self.cell_flags = torch.zeros(n_cells, dtype=torch.uint8, device=device)
-        self.dir_masks = torch.zeros(n_cells, dtype=torch.int64, device=device)
-        self.tile_flags = torch.zeros(n_tiles, dtype=torch.uint8, device=device)
+        self.cell_flags = L.zeros(n_cells, torch.uint8, device)
+        self.dir_masks = L.zeros(n_cells, torch.int64, device)
+        self.tile_flags = L.zeros(n_tiles, torch.uint8, device)
         self.down = None   # (targets, src, n)
         self.up = None
 
@@ -252,12 +252,10 @@ def build_tables(topo: Topology, bc, solid, err, tables=None, only=None):
         if t is None or t.cap != cap:
             t = _LevelTables(cap * T, cap, topo.device)
             t.cap = cap
-            t.down = (torch.zeros(cap * T, dtype=torch.int32, device=topo.device),
-                      torch.full((cap * T, NC), -1, dtype=torch.int32, device=topo.device),
-                      cap * T)
-            t.up = (torch.zeros(cap * T, dtype=torch.int32, device=topo.device),
-                    torch.full((cap * T, NC), -1, dtype=torch.int32, device=topo.device),
-                    cap * T)
+            t.down = (L.zeros(cap * T, torch.int32, topo.device),
+                      L.full((cap * T, NC), -1, torch.int32, topo.device), cap * T)
+            t.up = (L.zeros(cap * T, torch.int32, topo.device),
+                    L.full((cap * T, NC), -1, torch.int32, topo.device), cap * T)
             tables[l] = t
             fresh.add(l)
         if not cap or (only is not None and l not in only):

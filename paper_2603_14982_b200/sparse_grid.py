@@ -86,10 +86,12 @@ class LevelTopo:
         dev = self.device
         old = (getattr(self, "tile_xyz", None), getattr(self, "tile_kind", None),
                getattr(self, "nbr", None), getattr(self, "old_slot", None))
-        self.tile_xyz = torch.zeros((cap, 3), dtype=torch.int32, device=dev)
-        self.tile_kind = torch.zeros(cap, dtype=torch.uint8, device=dev)
-        self.nbr = torch.full((cap, n_nbr(self.d)), -1, dtype=torch.int32, device=dev)
-        self.old_slot = torch.full((cap,), -1, dtype=torch.int32, device=dev)
+        # library memsets / fills: a capacity growth inside the timed steps
+        # launches no framework kernel
+        self.tile_xyz = L.zeros((cap, 3), torch.int32, dev)
+        self.tile_kind = L.zeros(cap, torch.uint8, dev)
+        self.nbr = L.full((cap, n_nbr(self.d)), -1, torch.int32, dev)
+        self.old_slot = L.full((cap,), -1, torch.int32, dev)
         if old[0] is not None and self.cap:
             k = min(self.cap, cap)
             self.tile_xyz[:k].copy_(old[0][:k])
@@ -426,8 +428,11 @@ class LevelFields(MutableMapping):
 
 
 def fresh_block(d, n, dtype, device):
-    data = torch.zeros((len(field_names(d)), n), dtype=dtype, device=device)
-    data[field_names(d).index("eps")] = 1.0
+    data = L.zeros((len(field_names(d)), n), dtype, device)
+    if data.is_cuda:
+        L.fill(data[field_names(d).index("eps")], 1.0)
+    else:
+        data[field_names(d).index("eps")] = 1.0
     return data
 
 

@@ -10,10 +10,10 @@ python bench.py --scene c2 --steps 60 --warmup 20 > gpurun_out/${R}_bench_c2.jso
 python bench.py --scene c3 --steps 30 --warmup 10 --no-cpu-baseline > gpurun_out/${R}_bench_c3.json 2> gpurun_out/${R}_bench_c3.err; echo "bench c3 rc=$?"
 python bench.py --scene c5 --steps 30 --warmup 10 --no-cpu-baseline > gpurun_out/${R}_bench_c5.json 2> gpurun_out/${R}_bench_c5.err; echo "bench c5 rc=$?"
 python bench.py --scene c1 --steps 60 --warmup 10 > gpurun_out/${R}_bench_c1.json 2> gpurun_out/${R}_bench_c1.err; echo "bench c1 rc=$?"
-CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
+CMD="python bench.py --steps 10 --warmup 4 --no-cpu-baseline --no-e2e"
 $CMD > gpurun_out/${R}_plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-    --log-file gpurun_out/${R}_launches.csv $CMD > gpurun_out/${R}_ncu_launches.log 2>&1
+MLBM_PROFILE_TIMED=1 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --profile-from-start off --log-file gpurun_out/${R}_launches.csv $CMD > gpurun_out/${R}_ncu_launches.log 2>&1
 echo "launch list rc=$?"
 CMD3="python tools/kernel_probe.py 1"
 SCENE=AVALANCHE_C4 WARM=4 $CMD3 > gpurun_out/${R}_plain3.log 2>&1 && \
