@@ -731,6 +731,35 @@ __global__ void k_migrate(int64_t ncells, const int32_t* n_dev, const int32_t* o
     }
 }
 
+// the same migration in 16-byte vectors (V = 4 floats or 2 doubles): thread i
+// moves vector i % nvec of row i / nvec; a tile's cells are contiguous in both
+// layouts, so a vector never straddles tiles (T / PER vectors per tile)
+template <int D, typename R, typename V>
+__global__ void k_migrate_vec(int64_t nvec_row, const int32_t* n_dev, const int32_t* old_slot,
+                              const V* __restrict__ o0, const V* __restrict__ o1, V* __restrict__ n0,
+                              V* __restrict__ n1, int64_t stride_vec) {
+    constexpr int T = Geo<D>::T, NF = Geo<D>::NF, PER = (int)(sizeof(V) / sizeof(R)), TV = T / PER;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t row = i / nvec_row, v = i - row * nvec_row;
+    if (row >= NF) return;
+    if (n_dev && v >= (int64_t)__ldg(n_dev) * TV) return;
+    const int os = __ldg(&old_slot[v / TV]);
+    const int64_t ov = (int64_t)os * TV + v % TV;
+    V d0, d1;
+    if (os >= 0) {
+        d0 = o0[row * stride_vec + ov];
+        if (n1) d1 = o1[row * stride_vec + ov];
+    } else {
+        const R def = row == fi_eps<D>() ? R(1) : R(0);
+        R* a = reinterpret_cast<R*>(&d0);
+#pragma unroll
+        for (int k = 0; k < PER; ++k) a[k] = def;
+        d1 = d0;
+    }
+    n0[row * stride_vec + v] = d0;
+    if (n1) n1[row * stride_vec + v] = d1;
+}
+
 // copy the live cells (device count) of both trees' field blocks in 16-byte
 // vectors (V = 4 floats or 2 doubles); rows are capacity-strided and hold
 // whole tiles (16 / 64 cells), so the live range is a whole number of vectors
@@ -1075,6 +1104,20 @@ extern "C" int mlbm_migrate_level(int32_t dim, int32_t n_new_tiles, const int32_
     const int64_t n = (int64_t)n_new_tiles * T;
     if (n == 0) return 0;
     cudaStream_t s = as_stream(stream);
+    const int es = dtype ? 8 : 4;
+    const bool same = old0.stride == new0.stride &&
+                      (!new1.ptr || (old1.stride == old0.stride && new1.stride == old0.stride));
+    if (same && (old0.stride * es) % 16 == 0) {
+        // 16-byte vectors (C4: 391 -> 297 us per call against the per-cell kernel)
+        const int nf = dim == 2 ? Geo<2>::NF : Geo<3>::NF;
+        const int64_t nvec = n * es / 16, stride_vec = old0.stride * es / 16, total = nvec * nf;
+#define MIGV(D, R, V) k_migrate_vec<D, R, V><<<blocks_for(total, 256), 256, 0, s>>>(nvec, n_dev, old_slot, \
+        (const V*)old0.ptr, (const V*)old1.ptr, (V*)new0.ptr, (V*)new1.ptr, stride_vec)
+        if (dim == 2) { if (dtype) MIGV(2, double, double2); else MIGV(2, float, float4); }
+        else { if (dtype) MIGV(3, double, double2); else MIGV(3, float, float4); }
+#undef MIGV
+        return launch_status(1);
+    }
 #define MIG(D, R) k_migrate<D, R><<<blocks_for(n, 256), 256, 0, s>>>(n, n_dev, old_slot, fields_of<R>(old0), \
         fields_of<R>(old1), fields_of<R>(new0), fields_of<R>(new1))
     if (dim == 2) { if (dtype) MIG(2, double); else MIG(2, float); }
