@@ -1178,6 +1178,31 @@ struct PowderArgs {
     const uint8_t* active;    // optional per tile: phi non-zero within its 3^D tile neighbourhood
 };
 
+// Face neighbour (axis a, side sgn: +1 / -1) of cell lc of tile slot with the
+// coordinate conventions of the level-0 face stencils (coupling.py:300-316):
+// periodic axes wrap, other axes clamp (the neighbour of a boundary cell is
+// the cell itself); absent tiles -> returns -1.  In-tile neighbours need no
+// lookup; the others read one entry of the tile's neighbour table.
+template <int D>
+__device__ __forceinline__ int64_t face_nbr(const mlbm_level_t& lv, int slot, int lc, int a, int sgn) {
+    constexpr int T = Geo<D>::T;
+    int l[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
+    const int la = l[a] + sgn;
+    if (la >= 0 && la <= 3) {
+        l[a] = la;
+        return (int64_t)slot * T + local_of<D>(l[0], l[1], l[2]);
+    }
+    // leaves the tile: a domain face clamps (non-periodic), else the neighbour tile
+    const int ta = lv.tile_xyz[slot * 3 + a] + sgn;
+    if (!lv.periodic[a] && (ta < 0 || ta >= lv.tiles[a])) return (int64_t)slot * T + lc;
+    int o[3] = {0, 0, 0};
+    o[a] = sgn;
+    const int ns = lv.nbr[(int64_t)slot * Geo<D>::NB + nb_index<D>(o[0], o[1], o[2])];
+    if (ns < 0) return -1;
+    l[a] = la & 3;
+    return (int64_t)ns * T + local_of<D>(l[0], l[1], l[2]);
+}
+
 // The backtrace of one RK3 step moves less than a tile (|u| dt < 1 cell), so a
 // cell whose tile has phi = 0 in all its 3^D neighbour tiles advects exactly 0:
 // those cells skip the velocity sampling (the result is bit-identical).
@@ -1346,23 +1371,16 @@ __global__ void k_powder_diffuse(PowderArgs A) {
     const R* ras = (const R*)A.ras;
     const int64_t rs = A.rs;
     const int slot = (int)(c / T), lc = (int)(c % T);
-    const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
-    int g[3] = {0, 0, 0};
-    for (int a = 0; a < D; ++a) g[a] = A.lv.tile_xyz[slot * 3 + a] * 4 + l3[a];
     R lap = R(-2 * D) * adv[c];
     bool has_empty = false;
     const R eta_c = A.with_source ? ras[RW::ETAE * rs + c] : R(0);
     for (int a = 0; a < D; ++a)
         for (int sgn = 0; sgn < 2; ++sgn) {
-            int nb[3] = {g[0], g[1], g[2]};
-            nb[a] += sgn == 0 ? 1 : -1;
-            if (A.lv.periodic[a]) nb[a] = (nb[a] + A.lv.cells[a]) % A.lv.cells[a];
-            else nb[a] = nb[a] < 0 ? 0 : (nb[a] >= A.lv.cells[a] ? A.lv.cells[a] - 1 : nb[a]);
-            const int s = A.lv.tile_map[g3(A.lv.tiles, nb[0] >> 2, nb[1] >> 2, D == 3 ? nb[2] >> 2 : 0)];
-            const int64_t ni = s >= 0 ? (int64_t)s * T + local_of<D>(nb[0] & 3, nb[1] & 3, nb[2] & 3) : c;
+            const int64_t nb = face_nbr<D>(A.lv, slot, lc, a, sgn == 0 ? 1 : -1);
+            const int64_t ni = nb >= 0 ? nb : c;
             lap += adv[ni];
             if (A.with_source) {
-                if (s < 0) has_empty = true;
+                if (nb < 0) has_empty = true;
                 else if (ras[RW::ETAE * rs + ni] < R(1e-3)) has_empty = true;
             }
         }
@@ -2701,21 +2719,15 @@ __global__ void k_surface_need(mlbm_level_t lv, const R* __restrict__ ras, int64
     if (!(eta_c > R(0) && eta_c < R(eta_surface))) return;
     const int slot = (int)(c / T), lc = (int)(c % T);
     const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
-    int g[3] = {0, 0, 0};
-    for (int a = 0; a < D; ++a) g[a] = lv.tile_xyz[slot * 3 + a] * 4 + l3[a];
     bool has_empty = false;
     for (int a = 0; a < D; ++a)
         for (int sgn = 0; sgn < 2; ++sgn) {
-            int nb[3] = {g[0], g[1], g[2]};
-            nb[a] += sgn == 0 ? 1 : -1;
-            if (lv.periodic[a]) nb[a] = (nb[a] + lv.cells[a]) % lv.cells[a];
-            else nb[a] = nb[a] < 0 ? 0 : (nb[a] >= lv.cells[a] ? lv.cells[a] - 1 : nb[a]);
-            const int sl = lv.tile_map[g3(lv.tiles, nb[0] >> 2, nb[1] >> 2, D == 3 ? nb[2] >> 2 : 0)];
-            if (sl < 0) has_empty = true;
-            else if (ras[RW::ETAE * rs + (int64_t)sl * T + local_of<D>(nb[0] & 3, nb[1] & 3, nb[2] & 3)] < R(1e-3))
-                has_empty = true;
+            const int64_t nb = face_nbr<D>(lv, slot, lc, a, sgn == 0 ? 1 : -1);
+            if (nb < 0 || ras[RW::ETAE * rs + nb] < R(1e-3)) has_empty = true;
         }
     if (!has_empty) return;
+    int g[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) g[a] = lv.tile_xyz[slot * 3 + a] * 4 + l3[a];
     for (int k = 0; k < Geo<D>::K; ++k) {
         int q[3] = {g[0] + k % 3 - 1, g[1] + (k / 3) % 3 - 1, D == 3 ? g[2] + k / 9 - 1 : 0};
         bool out = false;
