@@ -1203,6 +1203,31 @@ __device__ __forceinline__ int64_t face_nbr(const mlbm_level_t& lv, int slot, in
     return (int64_t)ns * T + local_of<D>(l[0], l[1], l[2]);
 }
 
+// Cell at offset o (|o_a| <= 1) from cell lc of tile slot: periodic axes
+// wrap, a position outside a non-periodic domain or in an absent tile -> -1
+// (the 3^D neighbourhood of the entrainment-surface flags).
+template <int D>
+__device__ __forceinline__ int64_t cell_nbr(const mlbm_level_t& lv, int slot, int lc, const int (&o)[3]) {
+    constexpr int T = Geo<D>::T;
+    int l[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
+    int to[3] = {0, 0, 0};
+    bool inside = true;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const int la = l[a] + o[a];
+        to[a] = la < 0 ? -1 : (la > 3 ? 1 : 0);
+        l[a] = la & 3;
+        if (to[a] != 0) {
+            inside = false;
+            const int ta = lv.tile_xyz[slot * 3 + a] + to[a];
+            if (!lv.periodic[a] && (ta < 0 || ta >= lv.tiles[a])) return -1;
+        }
+    }
+    const int ns = inside ? slot : lv.nbr[(int64_t)slot * Geo<D>::NB + nb_index<D>(to[0], to[1], to[2])];
+    if (ns < 0) return -1;
+    return (int64_t)ns * T + local_of<D>(l[0], l[1], l[2]);
+}
+
 // The backtrace of one RK3 step moves less than a tile (|u| dt < 1 cell), so a
 // cell whose tile has phi = 0 in all its 3^D neighbour tiles advects exactly 0:
 // those cells skip the velocity sampling (the result is bit-identical).
@@ -2711,14 +2736,13 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
 template <int D, typename R>
 __global__ void k_surface_need(mlbm_level_t lv, const R* __restrict__ ras, int64_t rs, double eta_surface,
                                float* __restrict__ need) {
-    constexpr int T = Geo<D>::T;
+    constexpr int T = Geo<D>::T, K = Geo<D>::K;
     using RW = Rows<D>;
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= (int64_t)live_tiles(lv) * T) return;
     const R eta_c = ras[RW::ETAE * rs + c];
     if (!(eta_c > R(0) && eta_c < R(eta_surface))) return;
     const int slot = (int)(c / T), lc = (int)(c % T);
-    const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
     bool has_empty = false;
     for (int a = 0; a < D; ++a)
         for (int sgn = 0; sgn < 2; ++sgn) {
@@ -2726,22 +2750,16 @@ __global__ void k_surface_need(mlbm_level_t lv, const R* __restrict__ ras, int64
             if (nb < 0 || ras[RW::ETAE * rs + nb] < R(1e-3)) has_empty = true;
         }
     if (!has_empty) return;
-    int g[3] = {0, 0, 0};
-    for (int a = 0; a < D; ++a) g[a] = lv.tile_xyz[slot * 3 + a] * 4 + l3[a];
-    for (int k = 0; k < Geo<D>::K; ++k) {
-        int q[3] = {g[0] + k % 3 - 1, g[1] + (k / 3) % 3 - 1, D == 3 ? g[2] + k / 9 - 1 : 0};
-        bool out = false;
-        for (int a = 0; a < D; ++a) {
-            if (lv.periodic[a]) q[a] = (q[a] + lv.cells[a]) % lv.cells[a];
-            else if (q[a] < 0 || q[a] >= lv.cells[a]) out = true;
-        }
-        if (out) continue;
-        const int sl = lv.tile_map[g3(lv.tiles, q[0] >> 2, q[1] >> 2, D == 3 ? q[2] >> 2 : 0)];
-        if (sl < 0) continue;
-        // 2 on the surface cell itself, 1 on its neighbours (max wins)
-        const float v = k == Geo<D>::K / 2 ? 2.f : 1.f;
-        atomicMax(reinterpret_cast<int*>(&need[(int64_t)sl * T + local_of<D>(q[0] & 3, q[1] & 3, q[2] & 3)]),
-                  __float_as_int(v));
+    // 2 on the surface cell itself, 1 on the other cells of its 3^D
+    // neighbourhood (max wins; positions outside a non-periodic domain or in
+    // absent tiles skipped)
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int o[3] = {k % 3 - 1, (k / 3) % 3 - 1, D == 3 ? k / 9 - 1 : 0};
+        const int64_t nb = cell_nbr<D>(lv, slot, lc, o);
+        if (nb < 0) continue;
+        const float v = k == K / 2 ? 2.f : 1.f;
+        atomicMax(reinterpret_cast<int*>(&need[nb]), __float_as_int(v));
     }
 }
 
