@@ -264,6 +264,8 @@ def run_mine(args, rank, world, local_rank):
     graph_info = {"graph_replays_per_step": 1, "graph_captures": sim.graph_captures - caps0,
                   "topology_changes": sim.topology_changes - chg0}
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    graph_info["step_ms"] = {"min": round(min(step_ms), 3), "median": round(statistics.median(step_ms), 3),
+                             "max": round(max(step_ms), 3)}
     t_ms = sum(step_ms)
     t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     if world > 1:
