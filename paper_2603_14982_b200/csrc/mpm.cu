@@ -693,9 +693,14 @@ __global__ void k_particle_stress(int n, R* pp, int64_t ps, MatParams mp) {
 #ifndef G2P_ASYNC
 #define G2P_ASYNC 1     // ride-along rows copied to shared memory asynchronously (cp.async) before the staging
 #endif
-template <int D, typename R>
+// MAT: 0 elastic (plastic = 0), 1 Drucker-Prager sand, 2 NACC snow — one
+// instantiation per model, so the kernel holds only its own return map (G2P
+// stalled on instruction fetch: 2.7 no-instruction stalls per issue with
+// both return maps in one kernel)
+template <int D, typename R, int MAT>
 __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(PartArgs P, TopoL0 t0, MatParams mp, const R* ras, int64_t rs,
-                                             double dt, int plastic, int32_t* clamped, mlbm_error_t* err) {
+                                             double dt, int32_t* clamped, mlbm_error_t* err) {
+    constexpr bool plastic = MAT != 0;
     constexpr int K = Geo<D>::K;
     using RW = Rows<D>;
     using PR = PRows<D>;
@@ -971,7 +976,7 @@ __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(P
             for (int k = 0; k < D; ++k) acc += ((i == k ? R(1) : R(0)) + R(dt) * C[i * D + k]) * F[k * D + j];
             Fn[i * D + j] = acc;
         }
-    if (plastic) {
+    if constexpr (plastic) {
         R U[D * D], s[D], V[D * D];
         bool fast = false;
         if constexpr (D == 3) {
@@ -981,7 +986,7 @@ __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(P
         if (!fast) svd<D, R>(Fn, U, s, V);
         const R vc = vc_pre;
         R en[D], se[D];
-        if (mp.snow) {
+        if constexpr (MAT == 2) {
             // NACC snow with the paper's softening law; vc is the hardening state
 #pragma unroll
             for (int a = 0; a < D; ++a) {
@@ -1061,7 +1066,7 @@ __global__ void __launch_bounds__(G2P_BT, sizeof(R) == 4 ? G2P_MINB : 1) k_g2p(P
                 }
         }
     }
-    if (!plastic) {
+    if constexpr (!plastic) {
         // elastic: decompose the updated F for its stress
         R U[D * D], s[D], e[D];
         if constexpr (D == 3) {
@@ -2987,7 +2992,10 @@ extern "C" int mlbm_g2p(const mlbm_level_t* lv0, int32_t n, const double* x_in, 
                seeds, kind0, nonleaf};
     MatParams mp = mat_params(lam, mu, alpha, snow);
     const TopoL0 t = topo0(lv0);
-#define G2P(D, R) k_g2p<D, R><<<nblk(n, G2P_BT), G2P_BT, 0, s>>>(P, t, mp, (const R*)ras, rs, dt, plastic, clamped, err)
+    const int mat = !plastic ? 0 : (mp.snow ? 2 : 1);
+#define G2P(D, R) do { if (mat == 0) k_g2p<D, R, 0><<<nblk(n, G2P_BT), G2P_BT, 0, s>>>(P, t, mp, (const R*)ras, rs, dt, clamped, err); \
+                       else if (mat == 1) k_g2p<D, R, 1><<<nblk(n, G2P_BT), G2P_BT, 0, s>>>(P, t, mp, (const R*)ras, rs, dt, clamped, err); \
+                       else k_g2p<D, R, 2><<<nblk(n, G2P_BT), G2P_BT, 0, s>>>(P, t, mp, (const R*)ras, rs, dt, clamped, err); } while (0)
     if (lv0->dim == 2) { if (dtype) G2P(2, double); else G2P(2, float); }
     else { if (dtype) G2P(3, double); else G2P(3, float); }
 #undef G2P
