@@ -823,6 +823,21 @@ level_kernel(const StepArgs A) {
 #pragma unroll
         for (int a = 0; a < D; ++a) gx[a] = A.lv.tile_xyz[tile * 3 + a] * 4 + l[a];
     }
+    // modes 2-4 read dst's moments (and the force / eps rows): issued before
+    // the block vote so their latency overlaps it (the collide was
+    // latency-bound: 18 long-scoreboard stalls per issue)
+    R pre[STREAM ? 1 : NM + D + 1];
+    if constexpr (!STREAM) {
+        if (valid) {
+#pragma unroll
+            for (int k = 0; k < NM; ++k) pre[k] = dst.at(k, cell);
+            if (MODE != 4 && A.cp.force_mode != 0) {
+#pragma unroll
+                for (int a = 0; a < D; ++a) pre[NM + a] = dst.at(fi_f<D>(a), cell);
+            }
+            if (MODE != 4 && A.cp.tau_mode == 1) pre[NM + D] = dst.at(fi_eps<D>(), cell);
+        }
+    }
     const int any_bc = __syncthreads_or(valid && (tf & MLBM_TF_BC));
     const bool active = cf & MLBM_CF_ACTIVE;
     // boundary_kernel touches the outlet / inlet layers only (block-uniform)
@@ -902,11 +917,11 @@ level_kernel(const StepArgs A) {
         }
     } else {   // MODE 2, 3, 4 read the bare (2, 3) or collided (4) moments of dst
         if (valid) {
-            dr = dst.at(0, cell);
+            dr = pre[0];
 #pragma unroll
-            for (int a = 0; a < D; ++a) mm[a] = dst.at(1 + a, cell);
+            for (int a = 0; a < D; ++a) mm[a] = pre[1 + a];
 #pragma unroll
-            for (int k = 0; k < NS; ++k) pi[k] = dst.at(1 + D + k, cell);
+            for (int k = 0; k < NS; ++k) pi[k] = pre[1 + D + k];
         }
     }
 
@@ -949,11 +964,19 @@ level_kernel(const StepArgs A) {
             for (int a = 0; a < D; ++a) F[a] = rho * (R(A.cp.gravity[a]) * sc);
         } else {
 #pragma unroll
-            for (int a = 0; a < D; ++a) F[a] = dst.at(fi_f<D>(a), cell);
+            for (int a = 0; a < D; ++a) {
+                if constexpr (STREAM) F[a] = dst.at(fi_f<D>(a), cell);
+                else F[a] = pre[NM + a];
+            }
+        }
+        R eps_d = R(1);
+        if (MODE != 5 && A.cp.tau_mode == 1) {
+            if constexpr (STREAM) eps_d = dst.at(fi_eps<D>(), cell);
+            else eps_d = pre[NM + D];
         }
         const R tau = MODE == 5 ? eps5 * R(A.cp.tau0)
                     : A.cp.tau_mode == 0 ? R(A.cp.tau)
-                    : A.cp.tau_mode == 1 ? dst.at(fi_eps<D>(), cell) * R(A.cp.tau0)
+                    : A.cp.tau_mode == 1 ? eps_d * R(A.cp.tau0)
                                          : ((const R*)A.cp.tau_ptr)[cell];
         const R inv_rho = R(1) / rho;
         R us[D];
