@@ -1576,14 +1576,25 @@ __global__ void k_sort_keys(int n, const double* x, int64_t ps, TopoL0 t0, uint3
 }
 
 template <typename R>
-__global__ void k_gather_particles(int n, int nrows, const int32_t* perm, const double* x, int dim,
-                                   const R* pdat, const int32_t* pid, int64_t ps, double* xo, R* po,
-                                   int32_t* pido) {
+__global__ void k_gather_particles(int n, int nrows, const int32_t* __restrict__ perm,
+                                   const double* __restrict__ x, int dim, const R* __restrict__ pdat,
+                                   const int32_t* __restrict__ pid, int64_t ps, double* __restrict__ xo,
+                                   R* __restrict__ po, int32_t* __restrict__ pido) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int j = perm[i];
     for (int a = 0; a < dim; ++a) xo[a * ps + i] = x[a * ps + j];
-    for (int r = 0; r < nrows; ++r) po[r * ps + i] = pdat[r * ps + j];
+    // rows in batches of 8: the (non-aliasing) loads of a batch are in flight
+    // together instead of one row's latency at a time
+    int r = 0;
+    for (; r + 8 <= nrows; r += 8) {
+        R v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = pdat[(r + k) * ps + j];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) po[(r + k) * ps + i] = v[k];
+    }
+    for (; r < nrows; ++r) po[r * ps + i] = pdat[r * ps + j];
     pido[i] = pid[j];
 }
 
