@@ -328,8 +328,11 @@ class CoupledSim:
         self.overlap_diag = os.environ.get("MLBM_OVERLAP_DIAG", "1") != "0"
         self._fork_pdiag = self._pdiag_forked = False
         # graphs of this many upcoming steps are captured whenever capacities
-        # change (first step included), so steady stepping only replays
-        self.precapture_steps = int(os.environ.get("MLBM_PRECAPTURE", "16")) or None
+        # change (first step included), so steady stepping only replays: two
+        # sort periods + 1, so the keys of the first sorted steps (which
+        # differ from the unsorted start) are among them (a 35 ms capture
+        # otherwise lands on step 16)
+        self.precapture_steps = int(os.environ.get("MLBM_PRECAPTURE", str(2 * self.sort_every + 1))) or None
         self.latest_only_rebuild = os.environ.get("MLBM_LATEST_ONLY_REBUILD", "1") != "0"
         self.latest_only_min_cells = 1 << 22
         # MLBM_FUSE_L0=1: the level-0 coupled phase as P2G -> ONE stream +
