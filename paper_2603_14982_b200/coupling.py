@@ -333,6 +333,9 @@ class CoupledSim:
         # differ from the unsorted start) are among them (a 35 ms capture
         # otherwise lands on step 16)
         self.precapture_steps = int(os.environ.get("MLBM_PRECAPTURE", str(2 * self.sort_every + 1))) or None
+        # a rebuild key runs eagerly this many times before its graph is
+        # captured (a capture costs a few ms of host time)
+        self.rebuild_capture_after = int(os.environ.get("MLBM_REBUILD_CAPTURE_AFTER", "1"))
         self.latest_only_rebuild = os.environ.get("MLBM_LATEST_ONLY_REBUILD", "1") != "0"
         self.latest_only_min_cells = 1 << 22
         # MLBM_FUSE_L0=1: the level-0 coupled phase as P2G -> ONE stream +
@@ -795,6 +798,7 @@ class CoupledSim:
         full = (topo.cap_version, key, tuple(topo.n_tiles(l) > 0 for l in range(topo.levels)))
         if getattr(self, "_rb_ver", None) != topo.cap_version:
             self._rb_graphs, self._rb_seen, self._rb_ver = {}, set(), topo.cap_version
+            self._rb_seen_n = {}
 
         # tables of the changed levels and of their neighbours (interfaces)
         changed = key[0] if key and isinstance(key[0], tuple) else key
@@ -805,7 +809,11 @@ class CoupledSim:
             solver._refresh_tables(only=affected)
 
         g = self._rb_graphs.get(full)
-        if g is None and full not in self._rb_seen:
+        seen = self._rb_seen_n.get(full, 0) if isinstance(getattr(self, "_rb_seen_n", None), dict) else 0
+        if g is None and seen < self.rebuild_capture_after:
+            # eager (the first time: every buffer allocated outside capture)
+            self._rb_seen_n = getattr(self, "_rb_seen_n", None) or {}
+            self._rb_seen_n[full] = seen + 1
             self._rb_seen.add(full)
             body()
             self.rebuild_eager += 1
