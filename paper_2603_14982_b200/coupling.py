@@ -301,7 +301,8 @@ class CoupledSim:
         self._diag_rows = []
         self._tmp = None
         self.last_report = None
-        self._diag_buf = torch.zeros(2 * self.d + 4, dtype=torch.float64,
+        # [fluid momentum d][sum phi][eps min][sediment momentum d][drag impulse d]
+        self._diag_buf = torch.zeros(3 * self.d + 2, dtype=torch.float64,
                                      device=self.topology.device)
         # CUDA-graph step: one graph per (cycle, buffer parities,
         # exchange kind), recaptured after every topology change
@@ -536,8 +537,11 @@ class CoupledSim:
         if self.powder is not None:
             self._powder_cycle(is_mpm)
         # the particle part on the raster of this step's exchange (before the
-        # rebuild renumbers the level-0 slots), the fluid part after the adapt
-        self._record_diagnostics(fluid=False)
+        # rebuild renumbers the level-0 slots), the fluid part after the adapt;
+        # a step without MPM keeps the last MPM step's particle part (the
+        # particles and the last exchange's fields are unchanged)
+        if is_mpm:
+            self._record_diagnostics(fluid=False)
         if adapt_now:
             driver = self._driver()
             self.last_report = self.adaptor.update(driver, self.pair)
@@ -578,8 +582,11 @@ class CoupledSim:
             self._fork_pdiag = False
         if self.powder is not None:
             self._powder_cycle(is_mpm)
-        # particles: already recorded on the side stream after G2P
-        pdiag = not self._pdiag_forked
+        # particles: already recorded on the side stream after G2P; a step
+        # without MPM keeps the last MPM step's particle part (particles and
+        # the last exchange's drag unchanged — recomputing it would read a
+        # raster the rebuild may have renumbered)
+        pdiag = is_mpm and not self._pdiag_forked
         if adapt_now and self.overlap_diag:
             # the diagnostics reductions read only fields and particles: they
             # run on a side stream concurrently with the latency-bound adapt
@@ -600,7 +607,7 @@ class CoupledSim:
         else:
             if adapt_now:
                 self.adaptor.plan_device(self._driver())
-            if not pdiag:
+            if self._pdiag_forked:
                 join = torch.cuda.Event()
                 join.record(self._side_stream())
                 torch.cuda.current_stream().wait_event(join)

@@ -90,6 +90,8 @@ def run_and_compare(scene_dict, steps, tol=1e-9, check_streaks=True, prepare=Non
     dd = dsim.diagnostics[-1]
     assert np.allclose(dd.fluid_mom, od["fluid_mom"], rtol=1e-9, atol=1e-12)
     assert np.allclose(dd.sediment_mom, od["sediment_mom"], rtol=1e-9, atol=1e-12)
+    assert len(dd.drag_impulse) == len(od["drag_impulse"]) == dsim.d
+    assert np.allclose(dd.drag_impulse, od["drag_impulse"], rtol=1e-9, atol=1e-12), (dd.drag_impulse, od["drag_impulse"])
     assert dd.tiles == od["tiles"]
     assert abs(dd.sum_phi - od["sum_phi"]) <= 1e-9 * max(1.0, abs(od["sum_phi"]))
     assert abs(dd.eps_min - od["eps_min"]) <= 1e-12

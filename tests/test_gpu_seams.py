@@ -139,3 +139,62 @@ def test_powder_step(sims, sign):
                         DC.PowderParams(diffusion=0.05, sign=sign), 1.0, source=dev(src, inv),
                         uz=dev(u[2], inv) if d == 3 else None)
     assert np.abs(back(dd, perm) - o).max() <= 1e-13
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_fp32_diagnostics_match_torch_reductions(d):
+    """The fp32 diagnostics kernels (4 cells / particles per thread, 16-byte
+    row loads) against torch reductions of the same device state: fluid
+    momentum, sum phi and eps min over the leaf cells of every level; sediment
+    momentum and the drag-force sum over level 0."""
+    _need_gpu()
+    from paper_2603_14982_b200 import _lib as L
+    from paper_2603_14982_b200.harness import build_scene, validate_scene
+    sc = S.scene(S.SAND_COLLAPSE_2D if d == 2 else S.COLUMN_3D_SMALL)
+    sc.setdefault("runtime", {})["dtype"] = "f32"
+    sim = build_scene(validate_scene(sc))
+    for _ in range(3):
+        sim.step()
+    torch.cuda.synchronize()
+    solver, lib = sim.solver, L.lib()
+    out = torch.zeros(3 * d + 2, dtype=torch.float64, device="cuda")
+    names = B.field_names(d)
+    ref_mom = np.zeros(d)
+    ref_phi, ref_emin = 0.0, 1.0
+    for l in range(sim.topology.levels):
+        n = sim.topology.cell_count(l)
+        if not n:
+            continue
+        lw = solver.last_roles(l)[1] if solver.k[l] else 0
+        a = solver.arrays(lw, l)
+        vol = float((1 << d) ** l)
+        out[:d + 2].zero_()
+        out[d + 1] = 1.0
+        L.check(lib.mlbm_diag_level(L.C.byref(solver._structs[l]), L.fields(a.data), vol, 0,
+                                    L.ptr(out[:d + 2]), L.stream_handle()), "diag_level")
+        torch.cuda.synchronize()
+        leaf = (solver._tables[l].cell_flags[:n] & 64) != 0
+        data = a.data[:, :n].double()
+        rho = 1.0 + data[names.index("rho")]          # row 0 holds rho - 1
+        for k in range(d):
+            m = float((vol * rho * data[1 + k])[leaf].sum().item())
+            assert abs(out[k].item() - m) <= 1e-9 * max(1.0, abs(m)) + 1e-12
+            ref_mom[k] += m
+        phi = float((vol * data[names.index("phi")])[leaf].sum().item())
+        assert abs(out[d].item() - phi) <= 1e-9 * max(1.0, abs(phi)) + 1e-12
+        emin = float(data[names.index("eps")][leaf].min().item()) if bool(leaf.any()) else 1.0
+        assert out[d + 1].item() == pytest.approx(min(emin, 1.0), abs=0)
+    # particles: sum m v over particles, sum fs over the level-0 cells
+    p, g = sim.particles, sim.grid
+    out.zero_()
+    n0 = sim.topology.capacity_cells(0)
+    L.check(lib.mlbm_diag_particles(d, len(p), L.ptr(p.pd), p.pd.stride(0), L.ptr(g.ras),
+                                    g.ras.stride(0), n0, L.ptr(sim.topology.dcounts[0]), 0,
+                                    L.ptr(out[d + 2:]), L.stream_handle()), "diag_particles")
+    torch.cuda.synchronize()
+    R = p.R
+    mv = (p.pd[R["m"]].double() * p.pd[R["v"]:R["v"] + d].double()).sum(dim=1)
+    fs = g.ras[g.R["fs"]:g.R["fs"] + d, :sim.topology.cell_count(0)].double().sum(dim=1)
+    for k in range(d):
+        assert abs(out[d + 2 + k].item() - mv[k].item()) <= 1e-9 * max(1.0, abs(mv[k].item())) + 1e-12
+        assert abs(out[2 * d + 2 + k].item() - fs[k].item()) <= 1e-9 * max(1.0, abs(fs[k].item())) + 1e-12
