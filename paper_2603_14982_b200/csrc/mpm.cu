@@ -1940,6 +1940,11 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
 #ifndef P2G2_ROUNDS
 #define P2G2_ROUNDS 1
 #endif
+// 3D fp32 P2G node arithmetic on register pairs (FFMA2 / FMUL2: one issue slot
+// for two lanes of fp32 math; tools/micro/ffma2_mix.cu)
+#ifndef P2G2_PAIRED
+#define P2G2_PAIRED 1
+#endif
 #ifndef P2G2_ROUNDS_DENSE
 #define P2G2_ROUNDS_DENSE 4
 #endif
@@ -2250,6 +2255,25 @@ __device__ __forceinline__ void p2g_record(const PartArgs& P, const MatParams& m
         for (int kk = 0; kk < D * D; ++kk) rec[o2++] = PC[kk];
     }
 
+// The 3D record of p2g_record (base[3] f[3] m V0 ap q[3] mv[3] S[6] PC[9])
+// permuted for the paired node arithmetic of k_p2g_cell2: every operand pair
+// of an FFMA2 sits in an aligned register pair of one 128-bit load (28 floats,
+// seven broadcast loads):
+//   (fx fy) fz q2 | (m V0)(ap mv0) | (mv1 mv2)(q0 q1) | (PC00 PC10)(PC01 PC11) |
+//   (PC02 PC12) PC20 PC21 | PC22 -S22 (-S00 -S01) | (-S01 -S11)(-S02 -S12)
+__device__ __forceinline__ void p2g_pair_record(const float (&r)[32], float (&p)[28]) {
+    constexpr int F = 3, M = 6, Q = 9, MV = 12, S = 15, PC = 21;
+    const float q[28] = {r[F], r[F + 1], r[F + 2], r[Q + 2],
+                         r[M], r[M + 1], r[M + 2], r[MV],
+                         r[MV + 1], r[MV + 2], r[Q], r[Q + 1],
+                         r[PC + 0], r[PC + 3], r[PC + 1], r[PC + 4],
+                         r[PC + 2], r[PC + 5], r[PC + 6], r[PC + 7],
+                         r[PC + 8], -r[S + 5], -r[S + 0], -r[S + 1],
+                         -r[S + 1], -r[S + 3], -r[S + 2], -r[S + 4]};
+#pragma unroll
+    for (int k = 0; k < 28; ++k) p[k] = q[k];
+}
+
 // Sum the NW per-warp node-box copies and add the node totals into the
 // raster rows (one atomic per touched node and non-zero row).  STRESS = 0:
 // the P2G rows (a node is touched iff its mass or area is non-zero); STRESS =
@@ -2432,6 +2456,14 @@ __global__ void __launch_bounds__(32 * NW, P2G2_MIN_BLOCKS) k_p2g_cell2(PartArgs
         d0[a] = oa == 0 ? -1.5f : (oa == 1 ? 2.f : -0.5f);
         of[a] = (float)oa;
     }
+    constexpr bool PAIRED = D == 3 && P2G2_PAIRED;
+    // lane constants of the paired arithmetic (x / y weights and derivatives
+    // in one pair each; z scalar)
+    const float2 pC2xy = make_float2(c2[0], c2[D > 1 ? 1 : 0]), pC1xy = make_float2(c1[0], c1[D > 1 ? 1 : 0]),
+                 pC0xy = make_float2(c0[0], c0[D > 1 ? 1 : 0]);
+    const float2 pD1xy = make_float2(d1[0], d1[D > 1 ? 1 : 0]), pD0xy = make_float2(d0[0], d0[D > 1 ? 1 : 0]);
+    const float2 pO0 = make_float2(of[0], of[0]), pO1 = make_float2(of[D > 1 ? 1 : 0], of[D > 1 ? 1 : 0]),
+                 pO2 = make_float2(of[D - 1], of[D - 1]);
     float* wacc = sacc + wid * NV * MAXN;
     float* wslab = &slab[wid * 32 * REC];
     float acc[NV];
@@ -2461,9 +2493,17 @@ __global__ void __launch_bounds__(32 * NW, P2G2_MIN_BLOCKS) k_p2g_cell2(PartArgs
             for (int k = 0; k < REC; ++k) rec[k] = 0.f;
             p2g_record<D>(P, mp, p, lane < nj, rec);
             float4* w4 = reinterpret_cast<float4*>(wslab) + lane;
+            if constexpr (PAIRED) {
+                float pr[28];
+                p2g_pair_record(rec, pr);
 #pragma unroll
-            for (int v4 = 0; v4 < NREC4; ++v4)
-                w4[v4 * 32] = make_float4(rec[4 * v4], rec[4 * v4 + 1], rec[4 * v4 + 2], rec[4 * v4 + 3]);
+                for (int v4 = 0; v4 < 7; ++v4)
+                    w4[v4 * 32] = make_float4(pr[4 * v4], pr[4 * v4 + 1], pr[4 * v4 + 2], pr[4 * v4 + 3]);
+            } else {
+#pragma unroll
+                for (int v4 = 0; v4 < NREC4; ++v4)
+                    w4[v4 * 32] = make_float4(rec[4 * v4], rec[4 * v4 + 1], rec[4 * v4 + 2], rec[4 * v4 + 3]);
+            }
 #pragma unroll
             for (int a = 0; a < 3; ++a) base[a] = __float_as_int(rec[a]);
         }
@@ -2485,6 +2525,49 @@ __global__ void __launch_bounds__(32 * NW, P2G2_MIN_BLOCKS) k_p2g_cell2(PartArgs
             for (int a = 0; a < 3; ++a) cur[a] = __shfl_sync(0xffffffffu, a < D ? base[a] : 0, j0);
     #pragma unroll
             for (int qv = 0; qv < NV; ++qv) acc[qv] = 0.f;
+            if constexpr (PAIRED) {
+                // rows: (m V0) (ap mv0) (mv1 mv2) (mom0 mom1) mom2; the force
+                // rows as (b = 1, b = 0) pair partial sums + the b = 2 term
+                const float2 z2 = make_float2(0.f, 0.f);
+                float2 aMV = z2, aA = z2, aV = z2, aM = z2, aF0 = z2, aF1 = z2, aF2 = z2;
+                float aM2 = 0.f, aG0 = 0.f, aG1 = 0.f, aG2 = 0.f;
+                for (int j = j0; j < j1; ++j) {
+                    const float4* rp = reinterpret_cast<const float4*>(wslab) + j;
+                    float4 t[7];
+    #pragma unroll
+                    for (int v4 = 0; v4 < 7; ++v4) t[v4] = rp[v4 * 32];
+                    const float2 Fxy = make_float2(t[0].x, t[0].y);
+                    const float fz = t[0].z;
+                    const float2 Wxy = __ffma2_rn(__ffma2_rn(pC2xy, Fxy, pC1xy), Fxy, pC0xy);
+                    const float wz = fmaf(fmaf(c2[2], fz, c1[2]), fz, c0[2]);
+                    const float2 T = make_float2(Wxy.y * wz, Wxy.x * wz);         // (wy wz, wx wz)
+                    const float2 G01 = __fmul2_rn(__ffma2_rn(pD1xy, Fxy, pD0xy), T);  // (g0, g1)
+                    const float2 W2 = make_float2(T.x * Wxy.x, T.y * Wxy.y);       // (w, w)
+                    const float g2 = (Wxy.x * Wxy.y) * fmaf(d1[2], fz, d0[2]);
+                    aMV = __ffma2_rn(W2, make_float2(t[1].x, t[1].y), aMV);
+                    aA = __ffma2_rn(W2, make_float2(t[1].z, t[1].w), aA);
+                    aV = __ffma2_rn(W2, make_float2(t[2].x, t[2].y), aV);
+                    float2 mo = __ffma2_rn(make_float2(t[3].x, t[3].y), pO0, make_float2(t[2].z, t[2].w));
+                    mo = __ffma2_rn(make_float2(t[3].z, t[3].w), pO1, mo);
+                    mo = __ffma2_rn(make_float2(t[4].x, t[4].y), pO2, mo);
+                    aM = __ffma2_rn(W2, mo, aM);
+                    float mo2 = fmaf(t[4].z, of[0], t[0].w);
+                    mo2 = fmaf(t[4].w, of[1], mo2);
+                    mo2 = fmaf(t[5].x, of[2], mo2);
+                    aM2 = fmaf(W2.x, mo2, aM2);
+                    aF0 = __ffma2_rn(make_float2(t[5].z, t[5].w), G01, aF0);
+                    aF1 = __ffma2_rn(make_float2(t[6].x, t[6].y), G01, aF1);
+                    aF2 = __ffma2_rn(make_float2(t[6].z, t[6].w), G01, aF2);
+                    aG0 = fmaf(t[6].z, g2, aG0);
+                    aG1 = fmaf(t[6].w, g2, aG1);
+                    aG2 = fmaf(t[5].y, g2, aG2);
+                }
+                acc[0] = aMV.x;
+                acc[1] = aM.x; acc[2] = aM.y; acc[3] = aM2;
+                acc[4] = aF0.x + aF0.y + aG0; acc[5] = aF1.x + aF1.y + aG1; acc[6] = aF2.x + aF2.y + aG2;
+                acc[7] = aMV.y; acc[8] = aA.x;
+                acc[9] = aA.y; acc[10] = aV.x; acc[11] = aV.y;
+            } else
             for (int j = j0; j < j1; ++j) {
                 const float4* rp = reinterpret_cast<const float4*>(wslab) + j;
                 float r[4 * NREC4];

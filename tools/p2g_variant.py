@@ -37,3 +37,17 @@ ts.sort()
 print("%s: p2g mode 5 on %d particles: median %.1f us  min %.1f us" % (tag, n, ts[len(ts) // 2], ts[0]))
 os.makedirs("/tmp/p2gvar", exist_ok=True)
 torch.save(grid.ras[:NACC].cpu(), "/tmp/p2gvar/%s.pt" % tag)
+if os.environ.get("F64REF"):
+    # fp64 raster of the same (fp32) particle state: the yardstick for the
+    # rounding of the fp32 variants (tools/p2g_variant_cmp.py f64 v_old v_new)
+    p64 = p.pd.double()
+    ras64 = torch.zeros(grid.ras.shape, dtype=torch.float64, device=grid.ras.device)
+    L.check(lib.mlbm_p2g(L.C.byref(lv0), n, L.ptr(p.xd), L.ptr(p64), p64.stride(0), mat.lam, mat.mu,
+                         mat.alpha, L.ptr(ras64), ras64.stride(0), 1, 0, L.ptr(grid._err), s), "p2g f64")
+    torch.cuda.synchronize()
+    # the warm-up steps ran this variant's P2G: its state is its own, so the
+    # yardstick is saved per variant
+    ref = ras64[:NACC].cpu()
+    mine = grid.ras[:NACC].double().cpu()
+    rel = [float((mine[q] - ref[q]).norm() / ref[q].norm().clamp_min(1e-300)) for q in range(NACC)]
+    print("%s vs fp64 P2G of the same state, rel L2 per row: %s" % (tag, " ".join("%.1e" % r for r in rel)))
