@@ -238,6 +238,7 @@ def run_mine(args, rank, world, local_rank):
     clocks = Clocks(local_rank)
     launches0 = L.TRACE.launches
     caps0, chg0 = sim.graph_captures, sim.topology_changes
+    cnt0 = {k: getattr(sim, k, 0) for k in ("step_graph_captures", "rebuild_graph_captures", "rebuild_eager")}
     barrier()
     torch.cuda.synchronize()
     clocks.start()
@@ -263,7 +264,10 @@ def run_mine(args, rank, world, local_rank):
     launches = L.TRACE.launches - launches0
     graph_info = {"graph_replays_per_step": 1, "graph_captures": sim.graph_captures - caps0,
                   "topology_changes": sim.topology_changes - chg0}
+    graph_info.update({k: getattr(sim, k, 0) - v for k, v in cnt0.items()})
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    if os.environ.get("MLBM_STEP_TIMES") == "1":
+        graph_info["step_ms_all"] = [round(x, 2) for x in step_ms]
     graph_info["step_ms"] = {"min": round(min(step_ms), 3), "median": round(statistics.median(step_ms), 3),
                              "max": round(max(step_ms), 3)}
     t_ms = sum(step_ms)

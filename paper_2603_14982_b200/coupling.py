@@ -359,6 +359,7 @@ class CoupledSim:
         self._pool = None
         self.graph_replays = 0
         self.graph_captures = 0
+        self.step_graph_captures = self.rebuild_graph_captures = 0
         self.topology_changes = 0
         self.rebuild_eager = 0
         self.rebuild_replays = 0
@@ -673,6 +674,7 @@ class CoupledSim:
         solver.k[:] = k0
         self._graphs[key] = entry
         self.graph_captures += 1
+        self.step_graph_captures += 1
         return entry
 
     def _key(self, ci, k, is_mpm, adapt_now, flags, lf_set):
@@ -841,6 +843,7 @@ class CoupledSim:
                 L.TRACE.launches = n0
                 self._rb_graphs[full] = g
                 self.graph_captures += 1
+                self.rebuild_graph_captures += 1
             g.replay()
             L.TRACE.launches += g.nk
             solver._tables_version = topo.version
