@@ -139,6 +139,9 @@ class GridAdaptor:
         # mlbm_adapt_pass): valid for the key (host rebuilds, static mask) they
         # were derived under; any other pass invalidates them
         self.windows = os.environ.get("MLBM_ADAPT_WINDOWS", "1") != "0"
+        # latest-only levels: migrate into the other tree and swap the roles
+        # (one pass over the level) instead of scratch + copy back (two)
+        self.latest_swap = os.environ.get("MLBM_LATEST_SWAP", "1") != "0"
         self._win = torch.zeros(2 * topology.levels * 6, dtype=torch.int32, device=dev)
         self._win_key = None
 
@@ -388,8 +391,17 @@ class GridAdaptor:
         if grown:
             pair.ensure_capacity()
         for l in changed:
-            pair.scratch_blocks(l)
+            if not (self.latest_swap and l in (latest_only or {})):
+                pair.scratch_blocks(l)
         old_h = topo.hier_struct(pair)           # old maps, old fields, old counts
+        # latest-only levels migrate their latest tree t straight into the
+        # other tree's storage (no scratch, no copy back; the caller swaps the
+        # level's tree roles): the old hierarchy shows tree t in both places,
+        # so a finer-level fallback of another level's init reads the latest
+        # old-layout values, never the tree being rewritten
+        swap = {l: t for l, t in (latest_only or {}).items() if self.latest_swap}
+        for l, t in swap.items():
+            old_h.fields[1 - t][l] = old_h.fields[t][l]
         topo.commit_host({l: new_counts[l] for l in changed})
         new_h = topo.hier_struct()
         d = topo.d
@@ -431,13 +443,16 @@ class GridAdaptor:
                 topo.build_neighbors(l, new_map=True)
             for l in changed:
                 lt = topo.lv[l]
-                sb = pair.scratch_blocks(l)
                 cnt = L.ptr(topo.dcounts[l])
                 # trees to carry over: both, or only the one read next (the
                 # other is rewritten before it is read; its stale cells stay)
                 ts = (latest_only[l],) if l in latest_only else (0, 1)
                 old = [L.fields(pair.trees[t].levels[l].data) for t in ts] + [L.fields(None)]
-                new = [L.fields(sb[t]) for t in ts] + [L.fields(None)]
+                if l in swap:
+                    new = [L.fields(pair.trees[1 - swap[l]].levels[l].data), L.fields(None)]
+                else:
+                    sb = pair.scratch_blocks(l)
+                    new = [L.fields(sb[t]) for t in ts] + [L.fields(None)]
                 L.check(lib.mlbm_migrate_level(d, lt.cap, cnt, L.ptr(lt.old_slot), old[0], old[1],
                                                new[0], new[1], dcode, s), "migrate_level")
                 if init[l]:
@@ -447,6 +462,8 @@ class GridAdaptor:
                                                     L.ptr(self._taus), conv,
                                                     dcode, L.ptr(self._status[Lv_slot(topo)]),
                                                     s), "init_new_cells")
+                if l in swap:
+                    continue
                 L.check(lib.mlbm_copy_live_fields(d, lt.cap, cnt, new[0], new[1],
                                                   *[L.fields(pair.trees[t].levels[l].data)
                                                     for t in ts], *([L.fields(None)] if len(ts) == 1

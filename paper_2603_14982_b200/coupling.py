@@ -679,13 +679,27 @@ class CoupledSim:
 
     def _key(self, ci, k, is_mpm, adapt_now, flags, lf_set):
         use_sorted, sort_now, sort_ahead = flags
-        return (ci, tuple(v & 1 for v in k), is_mpm, adapt_now, sort_now, use_sorted, sort_ahead,
+        return (ci, tuple((v + f) & 1 for v, f in zip(k, self.solver.flip)), is_mpm, adapt_now,
+                sort_now, use_sorted, sort_ahead,
                 self.powder is not None and is_mpm and lf_set)
 
     def _precapture(self, n):
         """Capture the graphs of the next ``n`` steps now (host state
         predicted from each graph's level-counter increments), so steady
         stepping replays only — re-run whenever capacities change."""
+        solver = self.solver
+        f0 = solver.flip[0]
+        # a latest-only rebuild swaps level 0's trees: the graphs of both
+        # placements are captured up front
+        swaps = self.adaptor is not None and self.adaptor.latest_swap and self._latest_only()
+        try:
+            for f in ((f0, 1 - f0) if swaps else (f0,)):
+                solver.flip[0] = f
+                self._precapture_run(n)
+        finally:
+            solver.flip[0] = f0
+
+    def _precapture_run(self, n):
         schedule = self.solver._schedule
         k = list(self.solver.k)
         b = self.pair.bounce
@@ -848,6 +862,10 @@ class CoupledSim:
             L.TRACE.launches += g.nk
             solver._tables_version = topo.version
             self.rebuild_replays += 1
+        if self.adaptor.latest_swap:
+            # latest-only levels now hold their latest values in the other tree
+            for l, _ in (key[1] if key and isinstance(key[0], tuple) else ()):
+                solver.flip[l] ^= 1
         # the step graph left this step's particle diagnostics in the buffer
         self._record_diagnostics(particles=False)
         self._host_rb.copy_(self._diag_buf, non_blocking=True)

@@ -26,7 +26,9 @@ def save_checkpoint(path, sim):
         # (level, tile coords, kind) rows as one int64 tensor: the file holds only
         # tensors and plain containers, so it loads with weights_only=True
         "tiles": torch.tensor(sorted(topo.tile_set()), dtype=torch.int64).reshape(-1, 2 + topo.d),
-        "trees": [[pair.trees[t].levels[l].data[:, :topo.cell_count(l)].cpu().clone()
+        # logical tree order (a level whose trees swapped places is saved
+        # unswapped), so a restored run starts with no swap
+        "trees": [[pair.trees[t ^ solver.flip[l]].levels[l].data[:, :topo.cell_count(l)].cpu().clone()
                    for l in range(L)] for t in range(2)],
         "k": list(solver.k), "bounce": pair.bounce, "step_count": sim.step_count,
         "streaks": ([s.cpu().clone() for s in sim.adaptor._streak]
@@ -57,6 +59,7 @@ def load_checkpoint(path, sim):
             src = st["trees"][t][l]
             pair.trees[t].levels[l].data[:, :src.shape[1]].copy_(src.to(topo.device))
     solver.k[:] = list(st["k"])
+    solver.flip[:] = [0] * topo.levels
     pair.bounce = st["bounce"]
     sim.step_count = st["step_count"]
     sim.topology_changes = st.get("topology_changes", 0)

@@ -317,6 +317,9 @@ class MultiLevelSolver:
         self.dtype = pair.dtype
         self.dcode = dtype_code(self.dtype)
         self.k = [0] * topology.levels
+        # per level: 1 when the level's two trees swapped places (a latest-only
+        # rebuild migrated the latest tree into the other one's storage)
+        self.flip = [0] * topology.levels
         self._tables_version = -1
         self._tables = {}
         self.check_errors = True
@@ -368,10 +371,10 @@ class MultiLevelSolver:
         return self.pair.trees[tree_idx].levels[level]
 
     def roles(self, level):
-        return buffer_roles(level, self.k[level] & 1)
+        return buffer_roles(level, (self.k[level] + self.flip[level]) & 1)
 
     def last_roles(self, level):
-        return buffer_roles(level, (self.k[level] - 1) & 1)
+        return buffer_roles(level, (self.k[level] - 1 + self.flip[level]) & 1)
 
     # -- kernels ----------------------------------------------------------------
     def _collide_struct(self, level, force_mode=0, tau_mode=0, tau=None, tau_ptr=None):

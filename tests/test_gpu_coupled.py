@@ -40,7 +40,7 @@ def field_diff(osim, dsim):
             continue
         ow = osim.solver.last_roles(l)[1] if osim.solver.k[l] else 0
         dw = dsim.solver.last_roles(l)[1] if dsim.solver.k[l] else 0
-        assert ow == dw
+        assert ow == dw ^ dsim.solver.flip[l]   # the device may have swapped the trees
         oa = osim.solver.arrays(ow, l)
         da = dsim.solver.arrays(dw, l)
         dmap = {tuple(c): i for i, c in enumerate(dt.cell_coords(l))}
@@ -537,7 +537,8 @@ def test_frame_outputs_match_reference_frame():
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_checkpoint_resume_continues_the_run(dtype, tmp_path):
+@pytest.mark.parametrize("swap", [False, True])
+def test_checkpoint_resume_continues_the_run(dtype, swap, tmp_path):
     """Run, checkpoint, run on; a fresh simulation loaded from the checkpoint
     continues identically (topology and streaks exact, fields / particles to
     atomic-order noise) through topology changes."""
@@ -552,15 +553,22 @@ def test_checkpoint_resume_continues_the_run(dtype, tmp_path):
         v = np.zeros_like(x)
         v[:, 0] = np.where(x[:, 0] < 48.0, 0.3, -0.3)
         sim.particles.v = v
+        if swap:
+            # latest-only level-0 rebuild with swapped trees (the C4 path)
+            sim.latest_only_min_cells = 0
         return sim
 
     a = fresh()
+    flipped = False
     for _ in range(6):
         a.step()
+        flipped |= a.solver.flip[0] == 1
     path = str(tmp_path / "ck.pt")
     save_checkpoint(path, a)
     for _ in range(8):
         a.step()
+        flipped |= a.solver.flip[0] == 1
+    assert flipped == swap
     b = fresh()
     load_checkpoint(path, b)
     for _ in range(8):
