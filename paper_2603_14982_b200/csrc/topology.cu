@@ -780,14 +780,11 @@ MLBM_HD double kap_down(double tf, double tc, int conv) { return conv == 0 ? tf 
 MLBM_HD double kap_up(double tf, double tc, int conv) { return conv == 0 ? 2.0 * tc / tf : tc / (2.0 * tf); }
 
 template <int D, typename R>
-__global__ void k_init_new(mlbm_hier_t oh, mlbm_hier_t nh, int level, const int32_t* tile_xyz,
-                           const int32_t* old_slot, int n_tiles, const int32_t* n_dev, FieldsT<R> n0,
-                           FieldsT<R> n1, const double* taus, int conv, int32_t* viol) {
+__device__ void init_new_cell(const mlbm_hier_t& oh, int level, const int32_t* tile_xyz, int64_t c,
+                              const FieldsT<R>& n0, const FieldsT<R>& n1, const double* taus, int conv,
+                              int32_t* viol) {
     constexpr int T = Geo<D>::T, NC = Geo<D>::NC, NS = Geo<D>::NS, NM = Geo<D>::NM;
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= (int64_t)n_tiles * T || (n_dev && c >= (int64_t)__ldg(n_dev) * T)) return;
     const int slot = (int)(c / T), lc = (int)(c % T);
-    if (old_slot[slot] >= 0) return;
     const int l3[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
     int g[3] = {0, 0, 0};
     for (int a = 0; a < D; ++a) g[a] = tile_xyz[slot * 3 + a] * 4 + l3[a];
@@ -875,6 +872,31 @@ __global__ void k_init_new(mlbm_hier_t oh, mlbm_hier_t nh, int level, const int3
         return;
     }
     atomicAdd(viol, 1);
+}
+
+// fresh tiles only: each warp reads the old slots of 32 consecutive tiles
+// (one coalesced load), then initialises the cells of its fresh ones — the
+// kept tiles (nearly all) cost one load instead of 64 idle threads
+template <int D, typename R>
+__global__ void __launch_bounds__(256) k_init_new(mlbm_hier_t oh, int level, const int32_t* tile_xyz,
+                                                  const int32_t* old_slot, int n_tiles, const int32_t* n_dev,
+                                                  FieldsT<R> n0, FieldsT<R> n1, const double* taus, int conv,
+                                                  int32_t* viol) {
+    constexpr int T = Geo<D>::T;
+    const int n = n_dev ? min(n_tiles, __ldg(n_dev)) : n_tiles;
+    const int lane = threadIdx.x & 31;
+    const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+    for (int s0 = warp * 32; s0 < n; s0 += nwarps * 32) {
+        const int sl = s0 + lane;
+        unsigned fresh = __ballot_sync(0xffffffffu, sl < n && old_slot[sl] < 0);
+        while (fresh) {
+            const int j = __ffs(fresh) - 1;
+            fresh &= fresh - 1;
+            for (int lc = lane; lc < T; lc += 32)
+                init_new_cell<D, R>(oh, level, tile_xyz, (int64_t)(s0 + j) * T + lc, n0, n1, taus, conv, viol);
+        }
+    }
 }
 
 // the static near-solid map of one level (the same test as k_classify's
@@ -1156,7 +1178,9 @@ extern "C" int mlbm_init_new_cells(const mlbm_hier_t* old_h, const mlbm_hier_t* 
     const int64_t n = (int64_t)n_tiles * T;
     if (n == 0) return 0;
     cudaStream_t s = as_stream(stream);
-#define INI(D, R) k_init_new<D, R><<<blocks_for(n, 128), 128, 0, s>>>(*old_h, *nh, level, tile_xyz, old_slot, \
+    (void)nh;
+    const int64_t blocks = std::min<int64_t>(((int64_t)n_tiles + 255) / 256, 148 * 16);
+#define INI(D, R) k_init_new<D, R><<<(unsigned)blocks, 256, 0, s>>>(*old_h, level, tile_xyz, old_slot, \
         n_tiles, n_dev, fields_of<R>(new0), fields_of<R>(new1), taus, conv, viol)
     if (old_h->dim == 2) { if (dtype) INI(2, double); else INI(2, float); }
     else { if (dtype) INI(3, double); else INI(3, float); }
