@@ -215,9 +215,25 @@ __device__ __forceinline__ void sym_eig3(R a00, R a01, R a02, R a11, R a12, R a2
             const int p = pq == 2 ? 1 : 0, q = pq == 0 ? 1 : 2, r = 3 - p - q;
             const R apq = A[p][q];
             if (apq == R(0)) continue;
-            const R theta = (A[q][q] - A[p][p]) / (R(2) * apq);
-            const R t = (theta >= R(0) ? R(1) : R(-1)) / (fabs(theta) + sqrt(theta * theta + R(1)));
-            const R c = R(1) / sqrt(t * t + R(1)), sn = t * c;
+            R t, c;
+            if constexpr (sizeof(R) == 4) {
+                // fp32: the angle only steers the sweep (apq is zeroed
+                // explicitly), so it takes the approximate divide / square
+                // root; the rotation itself stays orthogonal to round-off:
+                // c = 1 / sqrt(1 + t^2) by rsqrt + one Newton step, s = t c
+                const float theta = __fdividef(A[q][q] - A[p][p], 2.f * apq);
+                const float at = fabsf(theta);
+                t = at < 1e18f ? __fdividef(1.f, at + __fsqrt_rz(fmaf(theta, theta, 1.f))) : 0.5f / at;
+                t = theta >= 0.f ? t : -t;
+                const float x = fmaf(t, t, 1.f);
+                const float r0 = rsqrtf(x);
+                c = r0 * fmaf(-0.5f * x * r0, r0, 1.5f);
+            } else {
+                const R theta = (A[q][q] - A[p][p]) / (R(2) * apq);
+                t = (theta >= R(0) ? R(1) : R(-1)) / (fabs(theta) + sqrt(theta * theta + R(1)));
+                c = R(1) / sqrt(t * t + R(1));
+            }
+            const R sn = t * c;
             A[p][p] -= t * apq;
             A[q][q] += t * apq;
             A[p][q] = A[q][p] = R(0);
