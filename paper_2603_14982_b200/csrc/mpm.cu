@@ -695,10 +695,11 @@ __global__ void k_particle_stress(int n, R* pp, int64_t ps, MatParams mp) {
 }
 
 // ---------------------------------------------------------------------------
-// fp32: 8 resident CTAs per SM (80 registers, a few bytes of spill) beat
-// 5 CTAs at 96 registers by 17 % on C3 (latency-bound gathers / stores)
+// fp32: 7 resident CTAs per SM (72 registers, 80 B of stack) — C4 G2P 4.07 ms
+// against 4.13 at 8 CTAs (64 registers) and 4.20 at 6 (80 registers)
+// (tools/lib_ab.sh); 5 CTAs at 96 registers were 17 % slower on C3
 #ifndef G2P_MINB
-#define G2P_MINB 8
+#define G2P_MINB 7
 #endif
 #ifndef G2P_BT
 #define G2P_BT 128      // particles (threads) per block: one node box per block
