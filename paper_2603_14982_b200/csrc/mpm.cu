@@ -1951,6 +1951,11 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
 #ifndef P2G2_MAXN
 #define P2G2_MAXN 144
 #endif
+// node-box capacity of the stress raster (its box spans only the particles
+// near an entrainment surface)
+#ifndef STRESS_MAXN
+#define STRESS_MAXN 64      // 144 (the P2G box): +0.08 ms on C4 (occupancy); 48-72 alike
+#endif
 #ifndef P2G2_NW
 #define P2G2_NW 2
 #endif
@@ -2674,7 +2679,7 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
                                                           int64_t rs, const float* __restrict__ surf,
                                                           mlbm_error_t* err) {
     constexpr int K = Geo<D>::K, NS = D * (D + 1) / 2, NV = NS + 1;
-    constexpr int MAXN = P2G2_MAXN, REC = 16, BT = 32 * NW;
+    constexpr int MAXN = STRESS_MAXN, REC = 16, BT = 32 * NW;
     using PR = PRows<D>;
     using RW = Rows<D>;
     extern __shared__ __align__(16) float p2g_smem[];
@@ -3122,7 +3127,7 @@ static int stress_raster_impl(const mlbm_level_t* lv0, int32_t n, const double* 
     if (dtype == 0 && !getenv("MLBM_STRESS_ATOMIC")) {
         // fp32: the P2G layout (sorted particles, per-warp node boxes)
         constexpr int NW = P2G2_NW;
-        const int sh = (NW * 7 * P2G2_MAXN + NW * 32 * 16) * (int)sizeof(float);   // NV <= 7
+        const int sh = (NW * 7 * STRESS_MAXN + NW * 32 * 16) * (int)sizeof(float);   // NV <= 7
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(k_stress_cell2<3, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh);
