@@ -1967,8 +1967,10 @@ __global__ void __launch_bounds__(128, 4) k_p2g_warp(PartArgs P, TopoL0 t0, MatP
 #ifndef P2G2_PAIRED
 #define P2G2_PAIRED 1
 #endif
+// rounds of a dense-sampling block (mode 5): C4 P2G 5.60 / 5.41 / 5.43 / 5.51 ms
+// at 4 / 8 / 12 / 16 rounds, 5.89 at 2 (tools/p2g_sweep.sh)
 #ifndef P2G2_ROUNDS_DENSE
-#define P2G2_ROUNDS_DENSE 4
+#define P2G2_ROUNDS_DENSE 8
 #endif
 template <int D, typename R>
 __global__ void __launch_bounds__(128) k_p2g_cell(PartArgs P, TopoL0 t0, MatParams mp, R* ras, int64_t rs,
