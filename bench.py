@@ -124,7 +124,7 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
-TRAFFIC_FILES = {"c2": "r2c_dram_traffic_c2.json", "c4": "r2c_dram_traffic_c4.json"}
+TRAFFIC_FILES = {"c2": "r2e_dram_traffic_c2.json", "c4": "r2e_dram_traffic_c4.json"}
 
 
 def dram_traffic(scene):
