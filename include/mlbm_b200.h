@@ -180,7 +180,10 @@ int mlbm_build_neighbors(const mlbm_level_t* lv, int32_t* nbr, void* stream);
  * Incremental (dirty non-NULL, over the level's tile grid): a tile not marked
  * dirty copies its flags / masks / tile flag from the old arrays at
  * old_slot[tile] (NULL: the same slot) instead of being classified; dirty =
- * the tiles within one tile of a kind change at any level (mlbm_bitmap_op). */
+ * the tiles within one tile of a kind change at any level (mlbm_bitmap_op).
+ * work (optional, incremental only): int32 [1 + n_tiles]; with it the clean
+ * tiles are copied one warp per tile and only the listed dirty tiles are
+ * classified (persistent grid); NULL: one block per tile. */
 /* the static near-solid map of one level over its whole tile grid (1 where a
  * solid box or the heightmap reaches within one cell of the tile; periodic
  * seams always 1), read by mlbm_classify_level instead of rescanning the
@@ -192,7 +195,8 @@ int mlbm_classify_level(const mlbm_level_t* lv, const mlbm_hier_t* h,
                         uint8_t* cell_flags, uint64_t* dir_masks, uint8_t* tile_flags,
                         int32_t* counts, mlbm_error_t* err, const uint8_t* dirty,
                         const int32_t* old_slot, const uint8_t* old_cf,
-                        const uint64_t* old_masks, const uint8_t* old_tf, void* stream);
+                        const uint64_t* old_masks, const uint8_t* old_tf, int32_t* work,
+                        void* stream);
 /* the tiles of a level whose kind differs between two kind grids (stable
  * compaction; count[0] = how many; ws: mlbm_ws_bytes(n)), and the scatter of
  * the dirty maps of mlbm_classify_level: for every changed tile of `level` and

@@ -135,7 +135,7 @@ _SIGS = {
     "mlbm_compact_tiles": [I32, P, P, P, P, P, P, P, I32, P, P, I64, P],
     "mlbm_build_neighbors": [C.POINTER(Level), P, P],
     "mlbm_classify_level": [C.POINTER(Level), C.POINTER(Hier), C.POINTER(BC),
-                            C.POINTER(Solid), P, P, P, P, P, P, P, P, P, P, P],
+                            C.POINTER(Solid), P, P, P, P, P, P, P, P, P, P, P, P],
     "mlbm_copy": [P, P, I64, P],
     "mlbm_changed_tiles": [I64, P, P, P, P, P, I64, P],
     "mlbm_mark_dirty": [C.POINTER(Hier), I32, P, P, P, P],

@@ -267,12 +267,23 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
                                                      mlbm_solid_t solid, uint8_t* cell_flags,
                                                      uint64_t* dir_masks, uint8_t* tile_flags,
                                                      int32_t* counts, mlbm_error_t* err,
-                                                     ClassifyPrev prev) {
+                                                     ClassifyPrev prev, const int32_t* list,
+                                                     const int32_t* n_list) {
     constexpr int T = Geo<D>::T, NB = Geo<D>::NB, Q = Geo<D>::Q;
-    const int tile = blockIdx.x, lc = threadIdx.x;
+    const int lc = threadIdx.x;
     const int level = lv.level;
-    if (tile >= live_tiles(lv)) return;      // block-uniform
-    if (prev.dirty) {
+    // one tile per block, or (list) a persistent loop over the dirty tiles the
+    // copy kernel listed
+    for (int it = blockIdx.x;; it += gridDim.x) {
+    int tile;
+    if (list) {
+        if (it >= __ldg(n_list)) break;         // block-uniform
+        tile = list[it];
+    } else {
+        if (it >= live_tiles(lv)) break;        // block-uniform
+        tile = it;
+    }
+    if (prev.dirty && !list) {
         const int t3[3] = {lv.tile_xyz[tile * 3], lv.tile_xyz[tile * 3 + 1], lv.tile_xyz[tile * 3 + 2]};
         const int os = prev.old_slot ? prev.old_slot[tile] : tile;
         if (os >= 0 && !prev.dirty[gidx3(lv.tiles, t3[0], t3[1], t3[2])]) {   // block-uniform
@@ -287,7 +298,7 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
                 if (niu) atomicAdd(&counts[1], niu);
                 tile_flags[tile] = prev.tf[os];
             }
-            return;
+            continue;
         }
     }
     __shared__ int snb[NB];
@@ -513,6 +524,49 @@ __global__ void __launch_bounds__(Geo<D>::T) k_classify(mlbm_level_t lv, mlbm_hi
     if (lc == 0)
         tile_flags[tile] = (plain ? MLBM_TF_PLAIN : 0) | (anybc ? MLBM_TF_BC : 0) |
                            (tkind == 1 ? MLBM_TF_LEAF : 0);
+    __syncthreads();                            // shared staging reused by the next tile
+    }
+}
+
+// incremental classification, clean tiles: one warp per tile copies the
+// flags / masks / tile flag from the old slot (coalesced rows instead of one
+// 64-thread block per tile) and lists the dirty / fresh tiles for k_classify
+template <int D>
+__global__ void __launch_bounds__(256) k_classify_copy(mlbm_level_t lv, uint8_t* cell_flags,
+                                                       uint64_t* dir_masks, uint8_t* tile_flags,
+                                                       int32_t* counts, ClassifyPrev prev,
+                                                       int32_t* list, int32_t* n_list) {
+    constexpr int T = Geo<D>::T;
+    const int lane = threadIdx.x & 31;
+    const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+    const int ntl = live_tiles(lv);
+    int nid = 0, niu = 0;
+    for (int tile = warp; tile < ntl; tile += nw) {
+        const int os = prev.old_slot ? prev.old_slot[tile] : tile;
+        bool dirty = os < 0;
+        if (!dirty) {
+            const int* t3 = lv.tile_xyz + tile * 3;
+            dirty = prev.dirty[gidx3(lv.tiles, t3[0], t3[1], t3[2])] != 0;
+        }
+        if (dirty) {                              // warp-uniform
+            if (lane == 0) list[atomicAdd(n_list, 1)] = tile;
+            continue;
+        }
+        for (int c = lane; c < T; c += 32) {
+            const int64_t oc = (int64_t)os * T + c, nc = (int64_t)tile * T + c;
+            const uint8_t f = prev.cf[oc];
+            cell_flags[nc] = f;
+            dir_masks[nc] = prev.masks[oc];
+            nid += (f & MLBM_CF_GHOST_D) ? 1 : 0;
+            niu += (f & MLBM_CF_GHOST_U) ? 1 : 0;
+        }
+        if (lane == 0) tile_flags[tile] = prev.tf[os];
+    }
+    nid = __reduce_add_sync(0xffffffffu, nid);
+    niu = __reduce_add_sync(0xffffffffu, niu);
+    if (lane == 0 && nid) atomicAdd(&counts[0], nid);
+    if (lane == 0 && niu) atomicAdd(&counts[1], niu);
 }
 
 // ---------------------------------------------------------------------------
@@ -985,18 +1039,36 @@ extern "C" int mlbm_classify_level(const mlbm_level_t* lv, const mlbm_hier_t* h,
                                    const mlbm_solid_t* solid, uint8_t* cell_flags, uint64_t* dir_masks,
                                    uint8_t* tile_flags, int32_t* counts, mlbm_error_t* err,
                                    const uint8_t* dirty, const int32_t* old_slot, const uint8_t* old_cf,
-                                   const uint64_t* old_masks, const uint8_t* old_tf, void* stream) {
+                                   const uint64_t* old_masks, const uint8_t* old_tf, int32_t* work,
+                                   void* stream) {
     if (lv->n_tiles == 0) return 0;
     if (dirty && (!old_cf || !old_masks || !old_tf)) return -1;
     cudaStream_t s = as_stream(stream);
     if (counts) cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), s);
     const ClassifyPrev prev{dirty, old_slot, old_cf, old_masks, old_tf};
+    const int T = lv->dim == 2 ? 16 : 64;
+    int32_t* list = nullptr;
+    int32_t* n_list = nullptr;
+    int grid = lv->n_tiles;
+    if (dirty && work) {
+        // clean tiles copied by warps, the dirty ones listed and classified by
+        // a persistent grid
+        n_list = work;
+        list = work + 1;
+        cudaMemsetAsync(n_list, 0, sizeof(int32_t), s);
+        const int cb = (int)std::min<int64_t>(((int64_t)lv->n_tiles + 7) / 8, 148 * 8);
+        if (lv->dim == 2)
+            k_classify_copy<2><<<cb, 256, 0, s>>>(*lv, cell_flags, dir_masks, tile_flags, counts, prev, list, n_list);
+        else
+            k_classify_copy<3><<<cb, 256, 0, s>>>(*lv, cell_flags, dir_masks, tile_flags, counts, prev, list, n_list);
+        grid = std::min(lv->n_tiles, 148 * (2048 / T));
+    }
     if (lv->dim == 2)
-        k_classify<2><<<lv->n_tiles, 16, 0, s>>>(*lv, *h, *bc, *solid, cell_flags, dir_masks,
-                                                 tile_flags, counts, err, prev);
+        k_classify<2><<<grid, 16, 0, s>>>(*lv, *h, *bc, *solid, cell_flags, dir_masks,
+                                          tile_flags, counts, err, prev, list, n_list);
     else
-        k_classify<3><<<lv->n_tiles, 64, 0, s>>>(*lv, *h, *bc, *solid, cell_flags, dir_masks,
-                                                 tile_flags, counts, err, prev);
+        k_classify<3><<<grid, 64, 0, s>>>(*lv, *h, *bc, *solid, cell_flags, dir_masks,
+                                          tile_flags, counts, err, prev, list, n_list);
     return launch_status(1);
 }
 

@@ -274,11 +274,14 @@ def build_tables(topo: Topology, bc, solid, err, tables=None, only=None):
                 L.copy(a, b)
             old_slot = topo.lv[l].old_slot if l in topo._dirty_changed else None
             prev = (old_slot,) + t.prev
+            if getattr(t, "cls_work", None) is None or t.cls_work.numel() < cap + 1:
+                t.cls_work = L.zeros(cap + 1, torch.int32, topo.device)
+        work = t.cls_work if dirty is not None else None
         L.check(lib.mlbm_classify_level(L.C.byref(lvs), L.C.byref(hier), L.C.byref(bc),
                                         L.C.byref(solid), L.ptr(t.cell_flags),
                                         L.ptr(t.dir_masks), L.ptr(t.tile_flags),
                                         L.ptr(scratch[l]), L.ptr(err), L.ptr(dirty),
-                                        *[L.ptr(x) for x in prev], s), "classify_level")
+                                        *[L.ptr(x) for x in prev], L.ptr(work), s), "classify_level")
     for l, t in tables.items():
         if not topo.lv[l].cap or (only is not None and l not in only):
             continue

@@ -600,3 +600,38 @@ def test_snow_nacc_fp64(scene):
     assert np.abs(qd - osim.p.vol_corr).max() <= 1e-9
     _, cracked = OM.nacc_state_decode(osim.p.vol_corr)
     assert cracked.any() and (~cracked).any()
+
+
+def test_incremental_classification_matches_full():
+    """The rebuild's incremental classification (clean tiles copied by warps,
+    the dirty ones classified by a persistent grid over their list) leaves
+    the same flags, masks and tile flags as classifying every tile anew."""
+    _need_gpu()
+    from paper_2603_14982_b200.harness import build_scene, validate_scene
+    from paper_2603_14982_b200.solver import build_tables
+    sim = build_scene(validate_scene(S.scene(S.CLOUD_3D_SMALL)))
+    x = sim.particles.x.cpu().numpy()
+    v = np.zeros_like(x)
+    v[:, 0] = np.where(x[:, 0] < 48.0, 0.3, -0.3)
+    sim.particles.v = v
+    topo, solver = sim.topology, sim.solver
+    T = 4 ** topo.d
+    checked = 0
+    for _ in range(10):
+        c0 = sim.topology_changes
+        sim.step()
+        if sim.topology_changes == c0:
+            continue
+        torch.cuda.synchronize()
+        err = torch.zeros_like(solver._err)
+        full = build_tables(topo, solver._bc, solver._solid, err)
+        for l in range(topo.levels):
+            n = topo.n_tiles(l)
+            if not n:
+                continue
+            inc = solver._tables[l]
+            for nm in ("cell_flags", "dir_masks"):
+                assert torch.equal(getattr(inc, nm)[:n * T], getattr(full[l], nm)[:n * T]), (l, nm)
+            assert torch.equal(inc.tile_flags[:n], full[l].tile_flags[:n]), l
+        checked += 1
+    assert checked > 0
