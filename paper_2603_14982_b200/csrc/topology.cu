@@ -576,8 +576,10 @@ template <int D>
 __global__ void k_iface_stencil(mlbm_level_t lv, mlbm_level_t other, int which, const int32_t* counts,
                                 const int32_t* targets, int32_t* src, mlbm_error_t* err) {
     constexpr int T = Geo<D>::T, NC = Geo<D>::NC;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= counts[0]) return;
+    // grid-stride over the device count (the grid is sized for the SMs, not
+    // for the capacity bound: most of a capacity-sized grid would exit at once)
+    const int nt = __ldg(counts);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nt; j += gridDim.x * blockDim.x) {
     const int c = targets[j];
     const int slot = c / T, lc = c % T;
     const int l[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
@@ -606,6 +608,7 @@ __global__ void k_iface_stencil(mlbm_level_t lv, mlbm_level_t other, int which, 
         else if ((which == 0 && wpos) || which == 1)
             report_error(err, MLBM_ERR_TOPOLOGY, lv.level, g[0], g[1], g[2], which == 0 ? 5 : 6);
         src[(int64_t)j * NC + k] = idx;
+    }
     }
 }
 
@@ -1097,10 +1100,11 @@ extern "C" int mlbm_build_interface(const mlbm_level_t* lv, const mlbm_level_t* 
     k_flag_count<<<nb, CB, 0, s>>>(n, fl, bsum);
     k_scan_blocks<<<1, 1024, 0, s>>>(nb, bsum, counts);
     k_flag_scatter<<<nb, CB, 0, s>>>(n, fl, bsum, TargetWriter{targets});
+    const int gs = (int)std::min<int64_t>(blocks_for(n, 128), 148 * 16);
     if (lv->dim == 2)
-        k_iface_stencil<2><<<blocks_for(n, 128), 128, 0, s>>>(*lv, *other, which, counts, targets, src, err);
+        k_iface_stencil<2><<<gs, 128, 0, s>>>(*lv, *other, which, counts, targets, src, err);
     else
-        k_iface_stencil<3><<<blocks_for(n, 128), 128, 0, s>>>(*lv, *other, which, counts, targets, src, err);
+        k_iface_stencil<3><<<gs, 128, 0, s>>>(*lv, *other, which, counts, targets, src, err);
     return launch_status(5);
 }
 
