@@ -2857,32 +2857,70 @@ __global__ void __launch_bounds__(32 * NW) k_stress_cell2(PartArgs P, TopoL0 t0,
 // i.e. on every nearest node whose stencil box contains it, and 2 on itself
 // (need zeroed by the caller)
 template <int D, typename R>
-__global__ void k_surface_need(mlbm_level_t lv, const R* __restrict__ ras, int64_t rs, double eta_surface,
-                               float* __restrict__ need) {
-    constexpr int T = Geo<D>::T, K = Geo<D>::K;
+__global__ void __launch_bounds__(256) k_surface_need(mlbm_level_t lv, const R* __restrict__ ras, int64_t rs,
+                                                      double eta_surface, float* __restrict__ need) {
+    // one tile per T threads: the surface cells mark the tile's 6^D window
+    // (tile + one-cell halo) in shared memory — no per-offset neighbour
+    // lookups, no atomics — and the marked window cells are then written
+    // once: the tile's own cells by plain stores, the halo cells (owned by
+    // neighbour tiles, which may store 2 there) by an integer atomicMax of 1
+    constexpr int T = Geo<D>::T, TPB = 256 / T, W6 = D == 3 ? 216 : 36;
     using RW = Rows<D>;
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= (int64_t)live_tiles(lv) * T) return;
-    const R eta_c = ras[RW::ETAE * rs + c];
-    if (!(eta_c > R(0) && eta_c < R(eta_surface))) return;
-    const int slot = (int)(c / T), lc = (int)(c % T);
-    bool has_empty = false;
-    for (int a = 0; a < D; ++a)
-        for (int sgn = 0; sgn < 2; ++sgn) {
-            const int64_t nb = face_nbr<D>(lv, slot, lc, a, sgn == 0 ? 1 : -1);
-            if (nb < 0 || ras[RW::ETAE * rs + nb] < R(1e-3)) has_empty = true;
+    __shared__ uint8_t win_all[TPB][W6];
+    const int grp = threadIdx.x / T, lc = threadIdx.x % T;
+    const int slot = blockIdx.x * TPB + grp;
+    const bool valid = slot < live_tiles(lv);
+    uint8_t* win = win_all[grp];
+    for (int i = lc; i < W6; i += T) win[i] = 0;
+    const int l[3] = {lc & 3, (lc >> 2) & 3, D == 3 ? (lc >> 4) & 3 : 0};
+    bool surf = false;
+    if (valid) {
+        const int64_t c = (int64_t)slot * T + lc;
+        const R eta_c = ras[RW::ETAE * rs + c];
+        if (eta_c > R(0) && eta_c < R(eta_surface)) {
+            for (int a = 0; a < D; ++a)
+                for (int sgn = 0; sgn < 2; ++sgn) {
+                    const int64_t nb = face_nbr<D>(lv, slot, lc, a, sgn == 0 ? 1 : -1);
+                    if (nb < 0 || ras[RW::ETAE * rs + nb] < R(1e-3)) surf = true;
+                }
         }
-    if (!has_empty) return;
-    // 2 on the surface cell itself, 1 on the other cells of its 3^D
-    // neighbourhood (max wins; positions outside a non-periodic domain or in
-    // absent tiles skipped)
+    }
+    const int wc = (l[0] + 1) + 6 * (l[1] + 1) + (D == 3 ? 36 * (l[2] + 1) : 0);
+    __syncthreads();
+    if (surf) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const int o[3] = {k % 3 - 1, (k / 3) % 3 - 1, D == 3 ? k / 9 - 1 : 0};
-        const int64_t nb = cell_nbr<D>(lv, slot, lc, o);
-        if (nb < 0) continue;
-        const float v = k == K / 2 ? 2.f : 1.f;
-        atomicMax(reinterpret_cast<int*>(&need[nb]), __float_as_int(v));
+        for (int k = 0; k < Geo<D>::K; ++k) {
+            const int o[3] = {k % 3 - 1, (k / 3) % 3 - 1, D == 3 ? k / 9 - 1 : 0};
+            win[wc + o[0] + 6 * o[1] + (D == 3 ? 36 * o[2] : 0)] = 1;
+        }
+    }
+    const int any = __syncthreads_or(surf);
+    if (!any) return;                                    // block-uniform
+    if (surf) win[wc] = 2;                               // 2 on the surface cell itself
+    __syncthreads();
+    if (!valid) return;
+    for (int i = lc; i < W6; i += T) {
+        const uint8_t v = win[i];
+        if (!v) continue;
+        const int w[3] = {i % 6 - 1, (i / 6) % 6 - 1, D == 3 ? i / 36 - 1 : 0};
+        int to[3] = {0, 0, 0}, ll[3] = {0, 0, 0};
+        bool inside = true;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            to[a] = w[a] < 0 ? -1 : (w[a] > 3 ? 1 : 0);
+            ll[a] = w[a] & 3;
+            inside &= to[a] == 0;
+        }
+        if (inside) {
+            need[(int64_t)slot * T + local_of<D>(ll[0], ll[1], ll[2])] = (float)v;
+        } else {
+            // a position outside a non-periodic domain or in an absent tile has
+            // no neighbour slot (-1)
+            const int ns = lv.nbr[(int64_t)slot * Geo<D>::NB + nb_index<D>(to[0], to[1], to[2])];
+            if (ns >= 0)
+                atomicMax(reinterpret_cast<int*>(&need[(int64_t)ns * T + local_of<D>(ll[0], ll[1], ll[2])]),
+                          __float_as_int(1.f));
+        }
     }
 }
 
@@ -3169,8 +3207,8 @@ extern "C" int mlbm_stress_raster_surface(const mlbm_level_t* lv0, int32_t n, co
     const int64_t ncell = (int64_t)lv0->n_tiles * T;
     if (ncell > 0) {
         cudaMemsetAsync(surf, 0, (size_t)ncell * sizeof(float), s);
-        if (lv0->dim == 2) k_surface_need<2, float><<<nblk(ncell, 256), 256, 0, s>>>(*lv0, (const float*)ras, rs, eta_surface, (float*)surf);
-        else k_surface_need<3, float><<<nblk(ncell, 256), 256, 0, s>>>(*lv0, (const float*)ras, rs, eta_surface, (float*)surf);
+        if (lv0->dim == 2) k_surface_need<2, float><<<nblk(lv0->n_tiles, 16), 256, 0, s>>>(*lv0, (const float*)ras, rs, eta_surface, (float*)surf);
+        else k_surface_need<3, float><<<nblk(lv0->n_tiles, 4), 256, 0, s>>>(*lv0, (const float*)ras, rs, eta_surface, (float*)surf);
     }
     const int k = stress_raster_impl(lv0, n, x, p, ps, lam, mu, alpha, ras, rs, dtype, (const float*)surf,
                                      err, s);
