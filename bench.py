@@ -16,6 +16,7 @@ DESIGN.md §1).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -235,6 +236,11 @@ def run_mine(args, rank, world, local_rank):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
     # ---- timed region: device time per step (CUDA events), L2 flushed between steps
+    # the scene / graph objects built so far are long-lived: frozen out of the
+    # cyclic collector's scans (a full collection over them stalls the host
+    # between graph launches for tens of ms; collection itself stays on)
+    gc.collect()
+    gc.freeze()
     clocks = Clocks(local_rank)
     launches0 = L.TRACE.launches
     caps0, chg0 = sim.graph_captures, sim.topology_changes
