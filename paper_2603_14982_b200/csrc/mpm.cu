@@ -1421,29 +1421,34 @@ __global__ void k_powder_diffuse(PowderArgs A) {
     R lap = R(-2 * D) * adv[c];
     bool has_empty = false;
     const R eta_c = A.with_source ? ras[RW::ETAE * rs + c] : R(0);
+    // only a cell with 0 < eta < eta_surface can be a source: the others skip
+    // the neighbours' eta and their own velocity / stress rows (q = 0 either way)
+    const bool cand = A.with_source && eta_c > R(0) && eta_c < R(A.eta_surface);
     for (int a = 0; a < D; ++a)
         for (int sgn = 0; sgn < 2; ++sgn) {
             const int64_t nb = face_nbr<D>(A.lv, slot, lc, a, sgn == 0 ? 1 : -1);
             const int64_t ni = nb >= 0 ? nb : c;
             lap += adv[ni];
-            if (A.with_source) {
+            if (cand) {
                 if (nb < 0) has_empty = true;
                 else if (ras[RW::ETAE * rs + ni] < R(1e-3)) has_empty = true;
             }
         }
     R out = adv[c] + R(A.sign * A.diffusion * A.dt) * lap;
     if (A.with_source) {
-        R sp2 = R(0), v[D];
-        for (int a = 0; a < D; ++a) { v[a] = ras[(RW::VMOM + a) * rs + c]; sp2 += v[a] * v[a]; }
-        const R speed = sqrt(sp2);
         R q = R(0);
-        if (eta_c > R(0) && eta_c < R(A.eta_surface) && has_empty && speed > R(0)) {
-            R vsv = R(0);
-            for (int k = 0; k < NS; ++k) {
-                const int a = s_a<D>(k), b = s_b<D>(k);
-                vsv += (a == b ? R(1) : R(2)) * v[a] * v[b] * ras[(RW::SIG + k) * rs + c];
+        if (cand && has_empty) {
+            R sp2 = R(0), v[D];
+            for (int a = 0; a < D; ++a) { v[a] = ras[(RW::VMOM + a) * rs + c]; sp2 += v[a] * v[a]; }
+            const R speed = sqrt(sp2);
+            if (speed > R(0)) {
+                R vsv = R(0);
+                for (int k = 0; k < NS; ++k) {
+                    const int a = s_a<D>(k), b = s_b<D>(k);
+                    vsv += (a == b ? R(1) : R(2)) * v[a] * v[b] * ras[(RW::SIG + k) * rs + c];
+                }
+                q = R(A.entrain) * fabs(vsv) / speed;
             }
-            q = R(A.entrain) * fabs(vsv) / speed;
         }
         out += R(A.dt) * q;
     }
