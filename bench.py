@@ -74,7 +74,7 @@ def workload_name(name):
             "c3": "C3: three-level 512x256x128-effective dune under log-law wind inflow, "
                   "4,194,304 MPM sand particles, two-way coupled, adapt every step",
             "c4": "C4: four-level 1536x768x384-effective snow avalanche with powder cloud over a "
-                  "terrain heightmap, 55,836,672 MPM particles (Drucker-Prager), two-way coupled, "
+                  "terrain heightmap, 55,836,672 MPM particles (NACC snow), two-way coupled, "
                   "powder entrainment, adapt every step, on ONE B200",
             "c5": "C5: dynamic-refinement stress, periodic 256^3, L = 3, 2,097,152 particles in a "
                   "dispersed cloud with Gaussian velocities (sigma 0.1), blocks activated / "
