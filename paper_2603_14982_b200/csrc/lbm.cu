@@ -786,7 +786,9 @@ template <int D, typename R> struct LevelCfg {
 };
 
 #ifndef LEVEL_MINB
-#define LEVEL_MINB (14 / LEVEL_TPC3)      // ~900 resident threads per SM (<= 72 registers)
+#define LEVEL_MINB (16 / LEVEL_TPC3)      // 1024 resident threads per SM (64 registers, 8 B of stack):
+                                          // C4 level-0 stream 0.794 -> 0.773 ms against 7 CTAs at 72
+                                          // registers; 6 CTAs: 0.84 (tools/lib_ab.sh)
 #endif
 template <int D, typename R, int MODE>
 __global__ void __launch_bounds__(LevelCfg<D, R>::THREADS,
