@@ -635,3 +635,65 @@ def test_incremental_classification_matches_full():
             assert torch.equal(inc.tile_flags[:n], full[l].tile_flags[:n]), l
         checked += 1
     assert checked > 0
+
+
+def test_entrainment_surface_flags_match_numpy():
+    """The entrainment-surface flags of the fp32 stress raster (per-tile
+    shared-memory window): 2 on every surface cell (0 < eta < eta_surface with
+    an absent or empty face neighbour), 1 on the other stored cells of its 3^3
+    neighbourhood, 0 elsewhere — against a dense NumPy restatement."""
+    _need_gpu()
+    from paper_2603_14982_b200 import _lib as L
+    sc = S.scene(S.POWDER_3D_SMALL, runtime__dtype="f32")
+    from paper_2603_14982_b200.harness import build_scene, validate_scene
+    sim = build_scene(validate_scene(sc))
+    for _ in range(3):
+        sim.step()
+    torch.cuda.synchronize()
+    topo, grid, p = sim.topology, sim.grid, sim.particles
+    lv0 = grid.level0()
+    cells = np.asarray(topo.cell_coords(0))
+    n0 = len(cells)
+    surf = torch.zeros(n0 + 64, dtype=torch.float32, device="cuda")
+    eta_s = float(sim.powder.eta_surface)
+    L.check(L.lib().mlbm_stress_raster_surface(
+        L.C.byref(lv0), len(p), L.ptr(p.xd), L.ptr(p.pd), p.pd.stride(0), sim.material.lam,
+        sim.material.mu, sim.material.alpha, L.ptr(grid.ras), grid.ras.stride(0), eta_s,
+        L.ptr(surf), 0, L.ptr(grid._err), L.stream_handle()), "stress_raster_surface")
+    got = surf[:n0].cpu().numpy()
+    eta = grid.ras[grid.R["etae"]][:n0].double().cpu().numpy()
+    dims = topo.finest_cells
+    per = topo.periodic3()
+    idx = -np.ones(dims, dtype=np.int64)
+    idx[cells[:, 0], cells[:, 1], cells[:, 2]] = np.arange(n0)
+    want = np.zeros(n0)
+    for i in np.nonzero((eta > 0) & (eta < eta_s))[0]:
+        c = cells[i]
+        empty = False
+        for a in range(3):
+            for sgn in (1, -1):
+                q = c.copy()
+                q[a] += sgn
+                if per[a]:
+                    q[a] %= dims[a]
+                elif q[a] < 0 or q[a] >= dims[a]:
+                    q = c                       # a domain face clamps to the cell itself
+                j = idx[tuple(q)]
+                if j < 0 or eta[j] < 1e-3:
+                    empty = True
+        if not empty:
+            continue
+        for o in np.ndindex(3, 3, 3):
+            q = c + np.array(o) - 1
+            ok = True
+            for a in range(3):
+                if per[a]:
+                    q[a] %= dims[a]
+                elif q[a] < 0 or q[a] >= dims[a]:
+                    ok = False
+            if not ok or idx[tuple(q)] < 0:
+                continue
+            j = idx[tuple(q)]
+            want[j] = max(want[j], 2.0 if o == (1, 1, 1) else 1.0)
+    assert (want == 2).any()
+    assert np.array_equal(got, want)
